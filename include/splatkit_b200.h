@@ -107,6 +107,14 @@ int sk_ctx_set_stream(sk_ctx* ctx, void* cuda_stream);
 int sk_ctx_synchronize(sk_ctx* ctx);
 /* Number of library kernels launched on this context so far. */
 int sk_ctx_launch_count(const sk_ctx* ctx, int64_t* out);
+/* Per-phase device timing of training steps (CUDA events on the context
+ * stream). Phases: 0 preprocess (K1), 1 binning + sort (K2-K5), 2 forward
+ * blend (K6), 3 loss (K7), 4 backward blend (K8), 5 project-backward + Adam
+ * (K9+K10). ms[6] accumulates milliseconds, steps counts timed steps. */
+#define SK_NUM_PHASES 6
+int sk_ctx_enable_timing(sk_ctx* ctx, int on);
+int sk_ctx_get_timing(const sk_ctx* ctx, double* ms, int64_t* steps);
+int sk_ctx_reset_timing(sk_ctx* ctx);
 const char* sk_version(void);
 
 /* ---- scene (Scene<T>, scene.hpp:30-52) ---------------------------------- */
@@ -146,6 +154,7 @@ int sk_render_forward(sk_ctx* ctx, sk_frame* frame, const uint8_t* mask_host,
 
 /* frame readback */
 int sk_frame_num_projected(const sk_frame* frame, int64_t* n);
+int sk_frame_dims(const sk_frame* frame, int* width, int* height);
 int sk_frame_get_projected(sk_ctx* ctx, const sk_frame* frame, sk_projected* out);
 int sk_frame_get_image(sk_ctx* ctx, const sk_frame* frame, float* hwc);
 int sk_frame_get_transmittance(sk_ctx* ctx, const sk_frame* frame, float* hw);
@@ -171,6 +180,134 @@ int sk_frame_set_dimage(sk_ctx* ctx, sk_frame* frame, const float* hwc);
 /* ---- backward (blend_backward raster.hpp:281-355) ---------------------- */
 int sk_render_backward(sk_ctx* ctx, sk_frame* frame);
 int sk_frame_get_blend_grads(sk_ctx* ctx, const sk_frame* frame, sk_blend_grads* out);
+
+/* ---- optimizer (adam.hpp) and score table (adc.hpp:23-45) ---------------- */
+/* LearningRates<T> (adam.hpp:78-86). */
+typedef struct sk_learning_rates {
+  float position, position_final, sh_dc, sh_rest, opacity, scale, rotation;
+} sk_learning_rates;
+void sk_default_learning_rates(sk_learning_rates* out);
+/* expon_lr (adam.hpp:23-26), evaluated in float exactly as the reference. */
+float sk_expon_lr(float lr_init, float lr_final, int step, int max_steps);
+
+/* ScoreTable<T> as host SoA arrays [n] (grad3d_acc [n][3]); NULL = skip. */
+typedef struct sk_score_table {
+  float* s_d;
+  float* s_p_raw;
+  float* s_p;
+  float* grad_norm_acc;
+  float* abs_grad_acc;
+  float* grad3d_acc;
+  int32_t* views_seen;
+  float* max_radius2d;
+} sk_score_table;
+int sk_scene_get_score_table(sk_ctx* ctx, sk_scene* scene, sk_score_table* out);
+int sk_scene_set_score_table(sk_ctx* ctx, sk_scene* scene, const sk_score_table* in);
+int sk_scene_reset_score_table(sk_ctx* ctx, sk_scene* scene);
+
+/* K9: cov_grad_from_inv_grad + project_backward (camera.hpp:148-213) for every
+ * Gaussian the frame projected, into the scene's planar gradient buffer
+ * (culled Gaussians get zeros, SceneGrads::init adam.hpp:90-97); with
+ * accumulate_stats the ScoreTable statistics of trainer.hpp:139-156 are
+ * updated. grads_host ([C][n]) may be NULL. */
+int sk_project_backward(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, int accumulate_stats, float* grads_host);
+/* Overwrites the scene's gradient buffer (planar [C][n]). */
+int sk_scene_set_grads(sk_ctx* ctx, sk_scene* scene, const float* grads_host);
+/* K10: SceneOptimizer::step (adam.hpp:124-143) from the gradient buffer. */
+int sk_adam_step(sk_ctx* ctx, sk_scene* scene, const sk_learning_rates* lrs, float position_lr, int update_sh_rest);
+/* K9 + K10 fused: gradients stay in registers. */
+int sk_project_backward_adam(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_learning_rates* lrs,
+                             float position_lr, int update_sh_rest, int accumulate_stats);
+/* Adam moments (planar [C][n], may be NULL) and the six group step counters. */
+int sk_scene_get_adam(sk_ctx* ctx, const sk_scene* scene, float* m, float* v, int64_t* t6);
+
+/* ---- multi-view density control (adc.hpp, the paper's contribution) ------- */
+/* accumulate_scores (adc.hpp:91-115): renders each of the k views, builds its
+ * error maps (error_maps.hpp:22-43), counts per Gaussian the high-error pixels
+ * it contributes to (second blend pass), and fills s_d / s_p_raw / s_p of
+ * the scene's ScoreTable (scores_from_counts :69-84). images: k float32 HWC
+ * images concatenated. counts_out ([k][n]) and photometric_out ([k]) may be
+ * NULL. */
+int sk_accumulate_scores(sk_ctx* ctx, sk_scene* scene, int k, const sk_camera* cams, const float* images, float tau,
+                         float lambda, const sk_binning* binning, int32_t* counts_out, float* photometric_out);
+/* select_densify (adc.hpp:135-153) over the scene's ScoreTable; flags [n]. */
+int sk_select_densify(sk_ctx* ctx, sk_scene* scene, float tau_d, float grad_threshold, float percent_dense,
+                      int use_vcd, float extent, uint8_t* clone, uint8_t* split);
+/* PruneParams<T> (adc.hpp:208-217). */
+typedef struct sk_prune_params {
+  float tau_p, min_opacity, opacity_late, world_size_frac, screen_size;
+  int32_t size_prune_from, densify_until, use_vcp;
+} sk_prune_params;
+void sk_default_prune_params(sk_prune_params* out);
+/* select_prune (adc.hpp:224-270); flags [n]. */
+int sk_select_prune(sk_ctx* ctx, sk_scene* scene, int iteration, const sk_prune_params* params, float extent,
+                    uint8_t* prune);
+/* apply_prune (adc.hpp:273-289), then apply_densify (:167-205), with the Adam
+ * moment remaps (adam.hpp:45-58), sequenced as Trainer::density_event
+ * (trainer.hpp:203-233). Flags are host arrays over the pre-event indices
+ * (any may be NULL); clone/split entries whose prune flag is set are dropped.
+ * eps: 6 standard normals per split Gaussian in ascending index order (child
+ * 0 then child 1), drawn by the caller's Rng. old_to_new ([n], the final
+ * index of every original Gaussian or -1) and new_size may be NULL. The score
+ * table is reset afterwards (trainer.hpp:241). */
+int sk_apply_prune_densify(sk_ctx* ctx, sk_scene* scene, const uint8_t* prune, const uint8_t* clone,
+                           const uint8_t* split, float clone_step_lr, const float* eps, int32_t* old_to_new,
+                           int64_t* new_size);
+
+/* ---- training (trainer.hpp, config.hpp) ------------------------------------ */
+/* TrainConfig (config.hpp:20-61); bin_mode "compact" <=> compact != 0. */
+typedef struct sk_train_config {
+  int32_t iterations, k;
+  double lambda, tau, tau_d, tau_p, beta, tau_alpha;
+  int32_t densify_from, densify_until, densify_every, prune_every_early, prune_every_late;
+  double grad_threshold, percent_dense;
+  double lr_position, lr_position_final, lr_sh_dc, lr_sh_rest, lr_opacity, lr_scale, lr_rotation;
+  int32_t opacity_reset_every, lazy_opt_enabled, lazy_opt_interval_15k, lazy_opt_interval_20k;
+  uint64_t seed;
+  int32_t tile_size, workers, sh_degree, compact, vcd, vcp;
+  double prune_min_opacity, prune_opacity_late, prune_world_size_frac, prune_screen_size;
+  int32_t size_prune_from, schedule_dry_run;
+} sk_train_config;
+void sk_default_config(sk_train_config* out);
+/* TrainConfig::validate (config.hpp:63-80), same messages. */
+int sk_validate_config(sk_ctx* ctx, const sk_train_config* cfg);
+
+/* LogRow (trainer.hpp:21-28) plus the view drawn and an event flag. */
+typedef struct sk_log_row {
+  int32_t iteration, gaussians;
+  int64_t tile_pairs;
+  double loss, psnr, elapsed_ms;
+  int32_t view, event; /* event: bit0 densify, bit1 prune */
+} sk_log_row;
+
+/* Dataset<T> (dataset.hpp:24-32): cameras + 8-bit GT images resident in HBM.
+ * images: n_views images, each [H_v][W_v][3] u8, concatenated in view order. */
+typedef struct sk_dataset sk_dataset;
+int sk_dataset_create(sk_ctx* ctx, int n_views, const sk_camera* cams, const uint8_t* images,
+                      const int32_t* train_indices, int n_train, float extent, sk_dataset** out);
+int sk_dataset_destroy(sk_dataset* d);
+
+typedef struct sk_trainer sk_trainer;
+/* Trainer(scene, data, cfg) (trainer.hpp:70-87). The trainer borrows scene and
+ * dataset; both must outlive it. */
+int sk_trainer_create(sk_ctx* ctx, sk_scene* scene, const sk_dataset* data, const sk_train_config* cfg,
+                      sk_trainer** out);
+int sk_trainer_destroy(sk_trainer* t);
+/* Trainer::run (trainer.hpp:89-119) for `iterations` more iterations (clamped
+ * to cfg.iterations); rows may be NULL. */
+int sk_trainer_run(sk_trainer* t, int iterations, sk_log_row* rows);
+int sk_trainer_iteration(const sk_trainer* t, int* it);
+/* Density-event records (for parity checks): header [7] = iteration,
+ * n_before, n_after, n_clone, n_split, n_prune, k; flags are [n_before] u8. */
+int sk_trainer_record_events(sk_trainer* t, int on);
+int sk_trainer_num_events(const sk_trainer* t, int* n);
+int sk_trainer_event(const sk_trainer* t, int e, int32_t* header, uint8_t* clone, uint8_t* split, uint8_t* prune,
+                     int32_t* sampled, float* photometric);
+
+/* One train_iteration (trainer.hpp:124-175) on an explicit camera with the
+ * GT image in HOST memory (copied in) — the end-to-end entry point. */
+int sk_train_step_host(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_camera* cam, const uint8_t* gt_host,
+                       const sk_train_config* cfg, float extent, int iteration, sk_log_row* row);
 
 #ifdef __cplusplus
 }

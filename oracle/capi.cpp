@@ -710,6 +710,120 @@ int or_select_prune_f(const float* params, int64_t n, int deg, const or_table_f*
   });
 }
 
+// accumulate_scores (adc.hpp:91-115) over k explicit views with float HWC
+// images (concatenated); fills counts [k][n], photometric [k], s_d/s_p_raw/s_p.
+int or_accumulate_scores_f(const float* params, int64_t n, int deg, int k, const sk_camera* cams,
+                           const float* images, float tau, float lambda, const sk_binning* bin, int workers,
+                           int32_t* counts_out, float* photo_out, float* s_d, float* s_p_raw, float* s_p) {
+  return guard([&] {
+    const Scene<float> s = scene_from_planar(params, n, deg);
+    std::vector<Camera<float>> cv;
+    std::vector<Image<float>> iv;
+    size_t off = 0;
+    for (int j = 0; j < k; ++j) {
+      cv.push_back(to_camera<float>(&cams[j]));
+      iv.push_back(image_from(images + off, cams[j].width, cams[j].height));
+      off += size_t(cams[j].width) * cams[j].height * 3;
+    }
+    std::vector<ViewRef<float>> views;
+    for (int j = 0; j < k; ++j) views.push_back({&cv[j], &iv[j]});
+    ScoreTable<float> t;
+    t.reset(int(n));
+    std::vector<std::vector<int>> counts;
+    std::vector<float> photo;
+    accumulate_scores(s, views, tau, lambda, to_binning<float>(bin), tile_size_of(bin), t, workers, &counts, &photo);
+    for (int j = 0; j < k; ++j) {
+      if (photo_out) photo_out[j] = photo[j];
+      if (counts_out)
+        for (int64_t i = 0; i < n; ++i) counts_out[j * n + i] = counts[j][i];
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      if (s_d) s_d[i] = t.s_d[i];
+      if (s_p_raw) s_p_raw[i] = t.s_p_raw[i];
+      if (s_p) s_p[i] = t.s_p[i];
+    }
+  });
+}
+
+// Trainer::density_event compaction (trainer.hpp:203-233) with explicit split
+// normals: prune -> Adam remap -> densify -> Adam remap. m/v planar [C][n] in,
+// [C][new_n] out (caller sizes them for n + clones + 2 splits).
+int or_apply_prune_densify_f(const float* params, int64_t n, int deg, const uint8_t* prune, const uint8_t* clone,
+                             const uint8_t* split, const float* grad3d, const int32_t* views_seen, float clone_lr,
+                             const float* eps, const float* m_in, const float* v_in, float* params_out,
+                             float* m_out, float* v_out, int64_t* new_n, int32_t* old_to_new) {
+  return guard([&] {
+    Scene<float> s = scene_from_planar(params, n, deg);
+    const int comps = 11 + 3 * sh_coeff_count(deg);
+    SceneOptimizer<float> opt;
+    opt.init(s);
+    AdamGroup<float>* groups[6] = {&opt.pos_, &opt.rot_, &opt.scale_, &opt.opacity_, &opt.sh_dc_, &opt.sh_rest_};
+    auto locate = [&](int c, int& g, int& d) {
+      if (c < 3) { g = 0; d = c; }
+      else if (c < 7) { g = 1; d = c - 3; }
+      else if (c < 10) { g = 2; d = c - 7; }
+      else if (c < 11) { g = 3; d = 0; }
+      else if (c < 14) { g = 4; d = c - 11; }
+      else { g = 5; d = c - 14; }
+    };
+    if (m_in && v_in)
+      for (int c = 0; c < comps; ++c) {
+        int g, d;
+        locate(c, g, d);
+        for (int64_t i = 0; i < n; ++i) {
+          groups[g]->m[i * groups[g]->dim + d] = m_in[c * n + i];
+          groups[g]->v[i * groups[g]->dim + d] = v_in[c * n + i];
+        }
+      }
+    std::vector<int> prune_set, cl, sp;
+    for (int64_t i = 0; i < n; ++i) {
+      if (prune && prune[i]) prune_set.push_back(int(i));
+      else {
+        if (clone && clone[i]) cl.push_back(int(i));
+        if (split && split[i]) sp.push_back(int(i));
+      }
+    }
+    ScoreTable<float> table;
+    table.reset(int(n));
+    for (int64_t i = 0; i < n; ++i) {
+      table.views_seen[i] = views_seen ? views_seen[i] : 0;
+      for (int d = 0; d < 3; ++d) table.grad3d_acc[i][d] = grad3d ? grad3d[3 * i + d] : 0.0f;
+    }
+    const IndexRemap pr = apply_prune(s, prune_set);
+    opt.remap(pr);
+    for (int& i : cl) i = pr.old_to_new[i];
+    for (int& i : sp) i = pr.old_to_new[i];
+    ScoreTable<float> mapped;
+    mapped.reset(pr.new_size);
+    for (size_t i = 0; i < pr.old_to_new.size(); ++i) {
+      const int j = pr.old_to_new[i];
+      if (j < 0) continue;
+      mapped.grad3d_acc[j] = table.grad3d_acc[i];
+      mapped.views_seen[j] = table.views_seen[i];
+    }
+    size_t e = 0;
+    const IndexRemap dr = apply_densify_with(s, cl, sp, mapped, clone_lr, [&] { return double(eps[e++]); });
+    opt.remap(dr);
+    const int64_t nn = s.size();
+    *new_n = nn;
+    scene_to_planar(s, params_out);
+    if (m_out && v_out)
+      for (int c = 0; c < comps; ++c) {
+        int g, d;
+        locate(c, g, d);
+        for (int64_t i = 0; i < nn; ++i) {
+          m_out[c * nn + i] = groups[g]->m[i * groups[g]->dim + d];
+          v_out[c * nn + i] = groups[g]->v[i * groups[g]->dim + d];
+        }
+      }
+    if (old_to_new)
+      for (int64_t i = 0; i < n; ++i) {
+        const int a = pr.old_to_new[i];
+        old_to_new[i] = a < 0 ? -1 : dr.old_to_new[a];
+      }
+  });
+}
+
 // ---- datasets / training ------------------------------------------------------
 struct or_dataset {
   Dataset<float> data;
@@ -907,8 +1021,34 @@ int or_prune_due(int it, const or_train_config* c) { return prune_due(it, to_cfg
 double or_expon_lr_f(float a, float b, int step, int max_steps) { return expon_lr(a, b, step, max_steps); }
 
 struct or_trainer {
+  std::unique_ptr<Dataset<float>> owned;  // single-view trainers own their dataset
   std::unique_ptr<Trainer<float>> t;
 };
+
+// A Trainer over a one-view dataset (camera + 8-bit GT): the CPU baseline of
+// the config-2 training step (the Rng's view draw always picks view 0).
+or_trainer* or_view_trainer_create(const float* params, int64_t n, int deg, const sk_camera* cam,
+                                   const uint8_t* gt_hwc, const or_train_config* cfg, float extent) {
+  try {
+    auto* h = new or_trainer;
+    h->owned = std::make_unique<Dataset<float>>();
+    Dataset<float>& d = *h->owned;
+    d.cameras.push_back(to_camera<float>(cam));
+    const size_t px = size_t(cam->width) * cam->height;
+    d.images_u8.emplace_back(gt_hwc, gt_hwc + 3 * px);
+    Image<float> img(cam->width, cam->height);
+    for (size_t p = 0; p < px; ++p)
+      for (int c = 0; c < 3; ++c) img.pixels[p][c] = gt_hwc[3 * p + c] / 255.0f;
+    d.images.push_back(std::move(img));
+    d.train_indices = {0};
+    d.extent = extent;
+    h->t = std::make_unique<Trainer<float>>(scene_from_planar(params, n, deg), d, to_cfg(cfg));
+    return h;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
 
 or_trainer* or_trainer_create(const float* params, int64_t n, int deg, const or_dataset* d,
                               const or_train_config* cfg) {

@@ -598,3 +598,65 @@ def train_step_view(params, deg, cam, gt_hwc, cfg: OrTrainConfig, extent, iterat
                                    C.byref(pairs), ptr(gn), ptr(ag), ptr(g3), ptr(vs), ptr(mr)))
     return dict(params=out, loss=lp[0], psnr=lp[1], pairs=pairs.value, grad_norm_acc=gn, abs_grad_acc=ag,
                 grad3d_acc=g3, views_seen=vs, max_radius2d=mr)
+
+
+def accumulate_scores(params, deg, cams, images, tau=0.5, lam=0.2, bin_=None, workers=1):
+    """accumulate_scores (adc.hpp:91-115) over explicit views; images float HWC."""
+    p = np.ascontiguousarray(params, np.float32)
+    n = p.shape[1]
+    k = len(cams)
+    arr = (SkCamera * k)(*[SkCamera.from_buffer_copy(bytes(c)) for c in cams])
+    imgs = np.ascontiguousarray(np.concatenate([np.asarray(i, np.float32).reshape(-1) for i in images]))
+    counts = np.zeros((k, n), np.int32)
+    photo = np.zeros(k, np.float32)
+    s_d = np.zeros(n, np.float32)
+    s_p_raw = np.zeros(n, np.float32)
+    s_p = np.zeros(n, np.float32)
+    check(lib().or_accumulate_scores_f(ptr(p), C.c_int64(n), C.c_int(deg), C.c_int(k), arr, ptr(imgs),
+                                       C.c_float(tau), C.c_float(lam), C.byref(bin_ or binning()), C.c_int(workers),
+                                       ptr(counts), ptr(photo), ptr(s_d), ptr(s_p_raw), ptr(s_p)))
+    return counts, photo, s_d, s_p_raw, s_p
+
+
+def apply_prune_densify(params, deg, prune, clone, split, grad3d, views_seen, clone_lr, eps, m=None, v=None):
+    """Trainer::density_event compaction (trainer.hpp:203-233) with explicit split normals."""
+    p = np.ascontiguousarray(params, np.float32)
+    n = p.shape[1]
+    cap = n + int(np.sum(clone)) + 2 * int(np.sum(split))
+    out = np.zeros((p.shape[0], cap), np.float32)
+    mo = np.zeros_like(out)
+    vo = np.zeros_like(out)
+    nn = C.c_int64()
+    o2n = np.zeros(n, np.int32)
+    args = [np.ascontiguousarray(a, np.uint8) for a in (prune, clone, split)]
+    g3 = np.ascontiguousarray(grad3d, np.float32)
+    vs = np.ascontiguousarray(views_seen, np.int32)
+    e = np.ascontiguousarray(eps, np.float32) if len(eps) else np.zeros(1, np.float32)
+    mi = None if m is None else np.ascontiguousarray(m, np.float32)
+    vi = None if v is None else np.ascontiguousarray(v, np.float32)
+    check(lib().or_apply_prune_densify_f(ptr(p), C.c_int64(n), C.c_int(deg), *[ptr(a) for a in args], ptr(g3),
+                                         ptr(vs), C.c_float(clone_lr), ptr(e), ptr(mi), ptr(vi), ptr(out), ptr(mo),
+                                         ptr(vo), C.byref(nn), ptr(o2n)))
+    k = nn.value
+    # scene_to_planar wrote [C][k] contiguously at the start of each buffer
+    flat = out.reshape(-1)[: p.shape[0] * k].reshape(p.shape[0], k)
+    mflat = mo.reshape(-1)[: p.shape[0] * k].reshape(p.shape[0], k)
+    vflat = vo.reshape(-1)[: p.shape[0] * k].reshape(p.shape[0], k)
+    return flat.copy(), mflat.copy(), vflat.copy(), o2n
+
+
+class ViewTrainer(Trainer):
+    """Trainer over a one-view dataset (camera + 8-bit GT) — the CPU baseline of
+    the config-2 training step."""
+
+    def __init__(self, params, deg, cam, gt_u8, cfg, extent):
+        p = np.ascontiguousarray(params, np.float32)
+        g = np.ascontiguousarray(gt_u8, np.uint8)
+        self.deg = deg
+        self.dataset = None
+        f = lib().or_view_trainer_create
+        f.restype = C.c_void_p
+        self.h = f(ptr(p), C.c_int64(p.shape[1]), C.c_int(deg), C.byref(SkCamera.from_buffer_copy(bytes(cam))),
+                   ptr(g), C.byref(cfg), C.c_float(extent))
+        if not self.h:
+            raise ValueError(lib().or_last_error().decode())

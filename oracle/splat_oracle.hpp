@@ -1437,9 +1437,22 @@ struct IndexRemap {
 
 inline constexpr double kSplitScaleShrink = 1.6;
 
+// Split noise: Vec3(normal(), normal(), normal()) (adc.hpp:196). The order in
+// which C++ evaluates those three constructor arguments is unspecified; this
+// restatement (and the GPU trainer) draws them left to right.
+template <typename T, typename NormalSource>
+inline IndexRemap apply_densify_with(Scene<T>& scene, const std::vector<int>& clone, const std::vector<int>& split,
+                                     const ScoreTable<T>& table, T clone_step_lr, NormalSource&& normal);
+
 template <typename T>
 inline IndexRemap apply_densify(Scene<T>& scene, const std::vector<int>& clone, const std::vector<int>& split,
                                 const ScoreTable<T>& table, T clone_step_lr, Rng& rng) {
+  return apply_densify_with(scene, clone, split, table, clone_step_lr, [&] { return rng.normal(); });
+}
+
+template <typename T, typename NormalSource>
+inline IndexRemap apply_densify_with(Scene<T>& scene, const std::vector<int>& clone, const std::vector<int>& split,
+                                     const ScoreTable<T>& table, T clone_step_lr, NormalSource&& normal) {
   const int n = scene.size();
   IndexRemap remap;
   remap.old_to_new.assign(n, -1);
@@ -1467,9 +1480,9 @@ inline IndexRemap apply_densify(Scene<T>& scene, const std::vector<int>& clone, 
     for (int c = 0; c < 2; ++c) {
       Gaussian3D<T> child = parent;
       Vec3<T> eps;
-      eps[0] = T(rng.normal());
-      eps[1] = T(rng.normal());
-      eps[2] = T(rng.normal());
+      eps[0] = T(normal());
+      eps[1] = T(normal());
+      eps[2] = T(normal());
       Vec3<T> es;
       for (int d = 0; d < 3; ++d) es[d] = eps[d] * scale[d];
       child.mu = parent.mu + rot * es;

@@ -1,0 +1,670 @@
+"""splatkit_b200: B200-native (sm_100a) 3DGS training hot path.
+
+Python host mirror of the reference's splat:: API over the C ABI in
+include/splatkit_b200.h (libsplatkit_b200.so, built in-tree by build.py).
+There is no CPU fallback: every compute call goes through the CUDA library,
+and importing the package fails loudly if the library is missing.
+
+Reference interface mirrored (proj/include/splatkit/):
+  project_scene      camera.hpp:137     -> Context.project_scene
+  build_tile_grid    raster.hpp:157     -> Context.build_tile_grid
+  blend_forward      raster.hpp:194     -> Context.blend_forward
+  blend_backward     raster.hpp:281     -> Context.blend_backward
+  training_loss      loss.hpp:21        -> Context.training_loss
+  ssim / psnr        metrics.hpp:83,126 -> Context.ssim
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsplatkit_b200.so")
+
+SK_OK = 0
+SK_ERR_INVALID_ARGUMENT = 1
+SK_ERR_RUNTIME = 2
+SK_ERR_CUDA = 3
+SK_ERR_OUT_OF_MEMORY = 4
+
+
+class SkCamera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("world_to_cam", C.c_float * 16),
+                ("near_plane", C.c_float)]
+
+
+class SkBinning(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("beta", C.c_float), ("tau_alpha", C.c_float), ("tile_size", C.c_int32)]
+
+
+class SkProjected(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("visible", "mu2d", "cov2d", "conic", "depth", "color", "opacity",
+                                          "tiles_touched")]
+
+
+class SkBlendGrads(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("d_mu2d", "d_conic", "d_color", "d_opacity", "abs_grad")]
+
+
+class SkLossValues(C.Structure):
+    _fields_ = [("loss", C.c_double), ("l1", C.c_double), ("ssim", C.c_double), ("psnr", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Loads libsplatkit_b200.so. Raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run paper_2511_04283_b200/build.py (no CPU fallback)")
+        _lib = C.CDLL(LIB_PATH)
+        _lib.sk_last_error.restype = C.c_char_p
+        _lib.sk_last_error.argtypes = [C.c_void_p]
+        _lib.sk_version.restype = C.c_char_p
+    return _lib
+
+
+def build(verbose=False, force=False):
+    from . import builder as _b
+    return _b.build(verbose=verbose, force=force)
+
+
+def _p(a):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"]
+    return C.c_void_p(a.ctypes.data)
+
+
+class SplatError(RuntimeError):
+    pass
+
+
+def camera(width, height, fx, fy, cx, cy, world_to_cam=None, near=0.2) -> SkCamera:
+    c = SkCamera()
+    c.width, c.height = int(width), int(height)
+    c.fx, c.fy, c.cx, c.cy = float(fx), float(fy), float(cx), float(cy)
+    w = np.eye(4) if world_to_cam is None else np.asarray(world_to_cam, np.float64)
+    for i, v in enumerate(w.reshape(-1)):
+        c.world_to_cam[i] = float(v)
+    c.near_plane = float(near)
+    return c
+
+
+def binning(mode="aabb", beta=1.0, tau_alpha=1.0 / 255, tile_size=16) -> SkBinning:
+    b = SkBinning()
+    b.mode = 1 if mode in ("compact", 1) else 0
+    b.beta = float(beta)
+    b.tau_alpha = float(tau_alpha)
+    b.tile_size = int(tile_size)
+    return b
+
+
+def as_camera(cam) -> SkCamera:
+    """Accepts any ctypes struct with the sk_camera layout (e.g. the oracle's)."""
+    if isinstance(cam, SkCamera):
+        return cam
+    return SkCamera.from_buffer_copy(bytes(cam))
+
+
+def as_binning(b) -> SkBinning:
+    if b is None:
+        return binning()
+    if isinstance(b, SkBinning):
+        return b
+    return SkBinning.from_buffer_copy(bytes(b))
+
+
+def n_components(deg: int) -> int:
+    return 11 + 3 * (deg + 1) ** 2
+
+
+@dataclass
+class Projected:
+    visible: np.ndarray
+    mu2d: np.ndarray
+    cov2d: np.ndarray
+    conic: np.ndarray
+    depth: np.ndarray
+    color: np.ndarray
+    opacity: np.ndarray
+    tiles_touched: np.ndarray
+
+
+@dataclass
+class TileLists:
+    ranges: np.ndarray  # [tiles][2]
+    values: np.ndarray  # [pairs] projected (== source) indices
+    pairs: int
+
+
+@dataclass
+class Render:
+    image: np.ndarray          # [H][W][3]
+    transmittance: np.ndarray  # [H][W]
+    contrib: np.ndarray        # [H][W]
+    counts: np.ndarray | None = None
+
+
+@dataclass
+class BlendGrads:
+    d_mu2d: np.ndarray
+    d_conic: np.ndarray
+    d_color: np.ndarray
+    d_opacity: np.ndarray
+    abs_grad: np.ndarray
+
+
+class Context:
+    """One CUDA device + stream (sk_ctx). Not thread-safe."""
+
+    def __init__(self, device: int = 0):
+        self._lib = lib()
+        h = C.c_void_p()
+        rc = self._lib.sk_ctx_create(C.c_int(device), C.byref(h))
+        if rc != SK_OK:
+            raise SplatError(f"sk_ctx_create failed ({rc})")
+        self.h = h
+        self._frame = self._new_frame()
+
+    def close(self):
+        if getattr(self, "h", None):
+            if getattr(self, "_frame", None):
+                self._lib.sk_frame_destroy(self._frame)
+                self._frame = None
+            self._lib.sk_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc):
+        if rc != SK_OK:
+            msg = self._lib.sk_last_error(self.h).decode()
+            if rc == SK_ERR_INVALID_ARGUMENT:
+                raise ValueError(msg)
+            raise SplatError(msg)
+
+    def _new_frame(self):
+        f = C.c_void_p()
+        self.check(self._lib.sk_frame_create(self.h, C.byref(f)))
+        return f
+
+    def synchronize(self):
+        self.check(self._lib.sk_ctx_synchronize(self.h))
+
+    def launch_count(self) -> int:
+        v = C.c_int64()
+        self._lib.sk_ctx_launch_count(self.h, C.byref(v))
+        return v.value
+
+    # ---- scene ----------------------------------------------------------
+    def scene(self, params: np.ndarray, sh_degree: int, capacity: int | None = None) -> "Scene":
+        return Scene(self, params, sh_degree, capacity)
+
+    # ---- frame-level pipeline (reference free functions) -------------------
+    def project_scene(self, scene: "Scene", cam, bin_=None, frame=None) -> Projected:
+        frame = frame or self._frame
+        self.check(self._lib.sk_preprocess(self.h, scene.h, C.byref(as_camera(cam)), C.byref(as_binning(bin_)),
+                                           frame))
+        return self.get_projected(frame)
+
+    def preprocess(self, scene: "Scene", cam, bin_=None, frame=None):
+        frame = frame or self._frame
+        self.check(self._lib.sk_preprocess(self.h, scene.h, C.byref(as_camera(cam)), C.byref(as_binning(bin_)),
+                                           frame))
+
+    def set_projected(self, pg, width, height, bin_=None, frame=None):
+        """pg: object with mu2d [n,2], cov2d [n,4], conic [n,4], depth, color [n,3], opacity (float32)."""
+        frame = frame or self._frame
+        arrs = [np.ascontiguousarray(getattr(pg, f), np.float32) for f in
+                ("mu2d", "cov2d", "conic", "depth", "color", "opacity")]
+        s = SkProjected()
+        s.mu2d, s.cov2d, s.conic, s.depth, s.color, s.opacity = [a.ctypes.data for a in arrs]
+        self.check(self._lib.sk_frame_set_projected(self.h, frame, C.byref(s), C.c_int64(arrs[0].shape[0]),
+                                                    C.c_int(width), C.c_int(height), C.byref(as_binning(bin_))))
+
+    def get_projected(self, frame=None) -> Projected:
+        frame = frame or self._frame
+        n = C.c_int64()
+        self._lib.sk_frame_num_projected(frame, C.byref(n))
+        n = n.value
+        out = Projected(np.zeros(n, np.int32), np.zeros((n, 2), np.float32), np.zeros((n, 4), np.float32),
+                        np.zeros((n, 4), np.float32), np.zeros(n, np.float32), np.zeros((n, 3), np.float32),
+                        np.zeros(n, np.float32), np.zeros(n, np.int32))
+        s = SkProjected()
+        for f in ("visible", "mu2d", "cov2d", "conic", "depth", "color", "opacity", "tiles_touched"):
+            setattr(s, f, getattr(out, f).ctypes.data)
+        self.check(self._lib.sk_frame_get_projected(self.h, frame, C.byref(s)))
+        return out
+
+    def build_tile_grid(self, frame=None) -> int:
+        frame = frame or self._frame
+        pairs = C.c_int64()
+        self.check(self._lib.sk_bin_sort(self.h, frame, C.byref(pairs)))
+        return pairs.value
+
+    def tile_lists(self, frame=None) -> TileLists:
+        frame = frame or self._frame
+        tx, ty = C.c_int(), C.c_int()
+        self._lib.sk_frame_num_tiles(frame, C.byref(tx), C.byref(ty))
+        ranges = np.zeros((tx.value * ty.value, 2), np.int32)
+        self.check(self._lib.sk_frame_get_tile_lists(self.h, frame, _p(ranges), None))
+        total = int(ranges[:, 1].max()) if ranges.size else 0
+        values = np.zeros(max(total, 1), np.int32)
+        self.check(self._lib.sk_frame_get_tile_lists(self.h, frame, _p(ranges), _p(values)))
+        return TileLists(ranges, values[:total], total)
+
+    def blend_forward(self, mask=None, frame=None, counts_len=None) -> Render:
+        frame = frame or self._frame
+        counts = None
+        m = None
+        if mask is not None:
+            m = np.ascontiguousarray(mask, np.uint8)
+            n = C.c_int64()
+            self._lib.sk_frame_num_projected(frame, C.byref(n))
+            counts = np.zeros(counts_len or n.value, np.int32)
+        self.check(self._lib.sk_render_forward(self.h, frame, _p(m), _p(counts)))
+        return self.get_render(frame, counts)
+
+    def get_render(self, frame=None, counts=None) -> Render:
+        frame = frame or self._frame
+        w, h = self._frame_dims(frame)
+        img = np.zeros((h, w, 3), np.float32)
+        tr = np.zeros((h, w), np.float32)
+        cc = np.zeros((h, w), np.int32)
+        self.check(self._lib.sk_frame_get_image(self.h, frame, _p(img)))
+        self.check(self._lib.sk_frame_get_transmittance(self.h, frame, _p(tr)))
+        self.check(self._lib.sk_frame_get_contrib_count(self.h, frame, _p(cc)))
+        return Render(img, tr, cc, counts)
+
+    def _frame_dims(self, frame):
+        w, h = C.c_int(), C.c_int()
+        self._lib.sk_frame_dims(frame, C.byref(w), C.byref(h))
+        return w.value, h.value
+
+    def training_loss(self, gt, lam=0.2, frame=None):
+        frame = frame or self._frame
+        v = SkLossValues()
+        if gt.dtype == np.uint8:
+            g = np.ascontiguousarray(gt, np.uint8)
+            self.check(self._lib.sk_loss_u8(self.h, frame, _p(g), C.c_float(lam), C.byref(v)))
+        else:
+            g = np.ascontiguousarray(gt, np.float32)
+            self.check(self._lib.sk_loss(self.h, frame, _p(g), C.c_float(lam), C.byref(v)))
+        return v
+
+    def get_dimage(self, frame=None):
+        frame = frame or self._frame
+        w, h = self._frame_dims(frame)
+        d = np.zeros((h, w, 3), np.float32)
+        self.check(self._lib.sk_frame_get_dimage(self.h, frame, _p(d)))
+        return d
+
+    def set_dimage(self, d, frame=None):
+        frame = frame or self._frame
+        d = np.ascontiguousarray(d, np.float32)
+        self.check(self._lib.sk_frame_set_dimage(self.h, frame, _p(d)))
+
+    def blend_backward(self, d_image=None, frame=None) -> BlendGrads:
+        frame = frame or self._frame
+        if d_image is not None:
+            self.set_dimage(d_image, frame)
+        self.check(self._lib.sk_render_backward(self.h, frame))
+        n = C.c_int64()
+        self._lib.sk_frame_num_projected(frame, C.byref(n))
+        n = n.value
+        g = BlendGrads(np.zeros((n, 2), np.float32), np.zeros((n, 4), np.float32), np.zeros((n, 3), np.float32),
+                       np.zeros(n, np.float32), np.zeros((n, 2), np.float32))
+        s = SkBlendGrads()
+        for f in ("d_mu2d", "d_conic", "d_color", "d_opacity", "abs_grad"):
+            setattr(s, f, getattr(g, f).ctypes.data)
+        self.check(self._lib.sk_frame_get_blend_grads(self.h, frame, C.byref(s)))
+        return g
+
+    def ssim(self, a, b):
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        h, w = a.shape[:2]
+        s, p = C.c_double(), C.c_double()
+        self.check(self._lib.sk_ssim(self.h, _p(a), _p(b), C.c_int(w), C.c_int(h), C.byref(s), C.byref(p)))
+        return s.value, p.value
+
+
+class Scene:
+    """Device-resident Scene<T> (scene.hpp:30-52), planar [C][n] parameters."""
+
+    def __init__(self, ctx: Context, params: np.ndarray, sh_degree: int, capacity=None):
+        self.ctx = ctx
+        self.sh_degree = sh_degree
+        p = np.ascontiguousarray(params, np.float32)
+        assert p.shape[0] == n_components(sh_degree)
+        h = C.c_void_p()
+        ctx.check(ctx._lib.sk_scene_create(ctx.h, C.c_int(sh_degree), C.c_int64(capacity or p.shape[1]),
+                                           C.byref(h)))
+        self.h = h
+        ctx.check(ctx._lib.sk_scene_upload(ctx.h, h, _p(p), C.c_int64(p.shape[1])))
+
+    @property
+    def size(self) -> int:
+        n = C.c_int64()
+        self.ctx._lib.sk_scene_size(self.h, C.byref(n))
+        return n.value
+
+    def download(self) -> np.ndarray:
+        out = np.zeros((n_components(self.sh_degree), self.size), np.float32)
+        self.ctx.check(self.ctx._lib.sk_scene_download(self.ctx.h, self.h, _p(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx._lib.sk_scene_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# optimizer, score table, density control, trainer
+# ---------------------------------------------------------------------------
+
+class SkLearningRates(C.Structure):
+    _fields_ = [(n, C.c_float) for n in ("position", "position_final", "sh_dc", "sh_rest", "opacity", "scale",
+                                         "rotation")]
+
+
+class SkScoreTable(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("s_d", "s_p_raw", "s_p", "grad_norm_acc", "abs_grad_acc", "grad3d_acc",
+                                          "views_seen", "max_radius2d")]
+
+
+class SkTrainConfig(C.Structure):
+    """TrainConfig (config.hpp:20-61); same layout as the oracle's or_train_config."""
+    _fields_ = [("iterations", C.c_int32), ("k", C.c_int32), ("lambda_", C.c_double), ("tau", C.c_double),
+                ("tau_d", C.c_double), ("tau_p", C.c_double), ("beta", C.c_double), ("tau_alpha", C.c_double),
+                ("densify_from", C.c_int32), ("densify_until", C.c_int32), ("densify_every", C.c_int32),
+                ("prune_every_early", C.c_int32), ("prune_every_late", C.c_int32),
+                ("grad_threshold", C.c_double), ("percent_dense", C.c_double),
+                ("lr_position", C.c_double), ("lr_position_final", C.c_double), ("lr_sh_dc", C.c_double),
+                ("lr_sh_rest", C.c_double), ("lr_opacity", C.c_double), ("lr_scale", C.c_double),
+                ("lr_rotation", C.c_double), ("opacity_reset_every", C.c_int32), ("lazy_opt_enabled", C.c_int32),
+                ("lazy_opt_interval_15k", C.c_int32), ("lazy_opt_interval_20k", C.c_int32), ("seed", C.c_uint64),
+                ("tile_size", C.c_int32), ("workers", C.c_int32), ("sh_degree", C.c_int32), ("compact", C.c_int32),
+                ("vcd", C.c_int32), ("vcp", C.c_int32), ("prune_min_opacity", C.c_double),
+                ("prune_opacity_late", C.c_double), ("prune_world_size_frac", C.c_double),
+                ("prune_screen_size", C.c_double), ("size_prune_from", C.c_int32), ("schedule_dry_run", C.c_int32)]
+
+
+class SkPruneParams(C.Structure):
+    _fields_ = [("tau_p", C.c_float), ("min_opacity", C.c_float), ("opacity_late", C.c_float),
+                ("world_size_frac", C.c_float), ("screen_size", C.c_float), ("size_prune_from", C.c_int32),
+                ("densify_until", C.c_int32), ("use_vcp", C.c_int32)]
+
+
+class SkLogRow(C.Structure):
+    _fields_ = [("iteration", C.c_int32), ("gaussians", C.c_int32), ("tile_pairs", C.c_int64), ("loss", C.c_double),
+                ("psnr", C.c_double), ("elapsed_ms", C.c_double), ("view", C.c_int32), ("event", C.c_int32)]
+
+
+def default_config() -> SkTrainConfig:
+    c = SkTrainConfig()
+    lib().sk_default_config(C.byref(c))
+    return c
+
+
+def as_config(cfg) -> SkTrainConfig:
+    if isinstance(cfg, SkTrainConfig):
+        return cfg
+    return SkTrainConfig.from_buffer_copy(bytes(cfg))
+
+
+def default_learning_rates() -> SkLearningRates:
+    l = SkLearningRates()
+    lib().sk_default_learning_rates(C.byref(l))
+    return l
+
+
+def default_prune_params() -> SkPruneParams:
+    p = SkPruneParams()
+    lib().sk_default_prune_params(C.byref(p))
+    return p
+
+
+def expon_lr(lr_init, lr_final, step, max_steps) -> float:
+    f = lib().sk_expon_lr
+    f.restype = C.c_float
+    f.argtypes = [C.c_float, C.c_float, C.c_int, C.c_int]
+    return f(lr_init, lr_final, step, max_steps)
+
+
+@dataclass
+class ScoreTable:
+    s_d: np.ndarray
+    s_p_raw: np.ndarray
+    s_p: np.ndarray
+    grad_norm_acc: np.ndarray
+    abs_grad_acc: np.ndarray
+    grad3d_acc: np.ndarray
+    views_seen: np.ndarray
+    max_radius2d: np.ndarray
+
+
+def _score_struct(t: ScoreTable) -> SkScoreTable:
+    s = SkScoreTable()
+    for f in ("s_d", "s_p_raw", "s_p", "grad_norm_acc", "abs_grad_acc", "grad3d_acc", "views_seen", "max_radius2d"):
+        a = getattr(t, f)
+        setattr(s, f, a.ctypes.data if a is not None else None)
+    return s
+
+
+def _scene_methods():
+    def score_table(self) -> ScoreTable:
+        n = self.size
+        t = ScoreTable(np.zeros(n, np.float32), np.zeros(n, np.float32), np.zeros(n, np.float32),
+                       np.zeros(n, np.float32), np.zeros(n, np.float32), np.zeros((n, 3), np.float32),
+                       np.zeros(n, np.int32), np.zeros(n, np.float32))
+        self.ctx.check(self.ctx._lib.sk_scene_get_score_table(self.ctx.h, self.h, C.byref(_score_struct(t))))
+        return t
+
+    def set_score_table(self, **fields):
+        n = self.size
+        full = {}
+        for f, dt, shape in (("s_d", np.float32, (n,)), ("s_p_raw", np.float32, (n,)), ("s_p", np.float32, (n,)),
+                             ("grad_norm_acc", np.float32, (n,)), ("abs_grad_acc", np.float32, (n,)),
+                             ("grad3d_acc", np.float32, (n, 3)), ("views_seen", np.int32, (n,)),
+                             ("max_radius2d", np.float32, (n,))):
+            v = fields.get(f)
+            full[f] = None if v is None else np.ascontiguousarray(np.broadcast_to(v, shape), dt)
+        t = ScoreTable(**full)
+        self.ctx.check(self.ctx._lib.sk_scene_set_score_table(self.ctx.h, self.h, C.byref(_score_struct(t))))
+
+    def reset_score_table(self):
+        self.ctx.check(self.ctx._lib.sk_scene_reset_score_table(self.ctx.h, self.h))
+
+    def set_grads(self, g):
+        g = np.ascontiguousarray(g, np.float32)
+        self.ctx.check(self.ctx._lib.sk_scene_set_grads(self.ctx.h, self.h, _p(g)))
+
+    def adam_state(self):
+        n = self.size
+        m = np.zeros((n_components(self.sh_degree), n), np.float32)
+        v = np.zeros_like(m)
+        t = np.zeros(6, np.int64)
+        self.ctx.check(self.ctx._lib.sk_scene_get_adam(self.ctx.h, self.h, _p(m), _p(v), _p(t)))
+        return m, v, t
+
+    Scene.score_table = score_table
+    Scene.set_score_table = set_score_table
+    Scene.reset_score_table = reset_score_table
+    Scene.set_grads = set_grads
+    Scene.adam_state = adam_state
+
+
+_scene_methods()
+
+
+def _ctx_methods():
+    def project_backward(self, scene, stats=True, frame=None):
+        frame = frame or self._frame
+        g = np.zeros((n_components(scene.sh_degree), scene.size), np.float32)
+        self.check(self._lib.sk_project_backward(self.h, scene.h, frame, C.c_int(int(stats)), _p(g)))
+        return g
+
+    def adam_step(self, scene, lrs=None, position_lr=None, update_sh_rest=True):
+        lrs = lrs or default_learning_rates()
+        plr = lrs.position if position_lr is None else position_lr
+        self.check(self._lib.sk_adam_step(self.h, scene.h, C.byref(lrs), C.c_float(plr), C.c_int(int(update_sh_rest))))
+
+    def project_backward_adam(self, scene, lrs=None, position_lr=None, update_sh_rest=True, stats=True, frame=None):
+        frame = frame or self._frame
+        lrs = lrs or default_learning_rates()
+        plr = lrs.position if position_lr is None else position_lr
+        self.check(self._lib.sk_project_backward_adam(self.h, scene.h, frame, C.byref(lrs), C.c_float(plr),
+                                                      C.c_int(int(update_sh_rest)), C.c_int(int(stats))))
+
+    def accumulate_scores(self, scene, cams, images, tau=0.5, lam=0.2, bin_=None):
+        k = len(cams)
+        arr = (SkCamera * k)(*[as_camera(c) for c in cams])
+        imgs = np.ascontiguousarray(np.concatenate([np.asarray(i, np.float32).reshape(-1) for i in images]))
+        counts = np.zeros((k, scene.size), np.int32)
+        photo = np.zeros(k, np.float32)
+        self.check(self._lib.sk_accumulate_scores(self.h, scene.h, C.c_int(k), arr, _p(imgs), C.c_float(tau),
+                                                  C.c_float(lam), C.byref(as_binning(bin_)), _p(counts), _p(photo)))
+        return counts, photo
+
+    def select_densify(self, scene, tau_d=5.0, grad_threshold=2e-4, percent_dense=0.01, use_vcd=True, extent=1.0):
+        n = scene.size
+        clone = np.zeros(n, np.uint8)
+        split = np.zeros(n, np.uint8)
+        self.check(self._lib.sk_select_densify(self.h, scene.h, C.c_float(tau_d), C.c_float(grad_threshold),
+                                               C.c_float(percent_dense), C.c_int(int(use_vcd)), C.c_float(extent),
+                                               _p(clone), _p(split)))
+        return clone, split
+
+    def select_prune(self, scene, iteration, params=None, extent=1.0, **kw):
+        p = params or default_prune_params()
+        for k, v in kw.items():
+            setattr(p, k, v)
+        prune = np.zeros(scene.size, np.uint8)
+        self.check(self._lib.sk_select_prune(self.h, scene.h, C.c_int(iteration), C.byref(p), C.c_float(extent),
+                                             _p(prune)))
+        return prune
+
+    def apply_prune_densify(self, scene, prune=None, clone=None, split=None, clone_step_lr=0.0, eps=None):
+        n = scene.size
+        arrs = [None if a is None else np.ascontiguousarray(a, np.uint8) for a in (prune, clone, split)]
+        e = None if eps is None else np.ascontiguousarray(eps, np.float32)
+        o2n = np.zeros(n, np.int32)
+        new = C.c_int64()
+        self.check(self._lib.sk_apply_prune_densify(self.h, scene.h, *[_p(a) for a in arrs], C.c_float(clone_step_lr),
+                                                    _p(e), _p(o2n), C.byref(new)))
+        return o2n, new.value
+
+    Context.project_backward = project_backward
+    Context.adam_step = adam_step
+    Context.project_backward_adam = project_backward_adam
+    Context.accumulate_scores = accumulate_scores
+    Context.select_densify = select_densify
+    Context.select_prune = select_prune
+    Context.apply_prune_densify = apply_prune_densify
+
+
+_ctx_methods()
+
+
+class Dataset:
+    """Dataset<T> (dataset.hpp:24-32) resident in HBM (8-bit GT images)."""
+
+    def __init__(self, ctx: Context, cams, images_u8, train_indices=None, extent=1.0):
+        self.ctx = ctx
+        k = len(cams)
+        arr = (SkCamera * k)(*[as_camera(c) for c in cams])
+        imgs = np.ascontiguousarray(np.concatenate([np.asarray(i, np.uint8).reshape(-1) for i in images_u8]))
+        tr = None if train_indices is None else np.ascontiguousarray(train_indices, np.int32)
+        h = C.c_void_p()
+        ctx.check(ctx._lib.sk_dataset_create(ctx.h, C.c_int(k), arr, _p(imgs), _p(tr),
+                                             C.c_int(0 if tr is None else len(tr)), C.c_float(extent), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx._lib.sk_dataset_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Trainer:
+    """Trainer (trainer.hpp:70-261) on the GPU; borrows scene and dataset."""
+
+    def __init__(self, ctx: Context, scene: Scene, data: Dataset, cfg, record_events=False):
+        self.ctx, self.scene, self.data = ctx, scene, data
+        self.cfg = as_config(cfg)
+        h = C.c_void_p()
+        ctx.check(ctx._lib.sk_trainer_create(ctx.h, scene.h, data.h, C.byref(self.cfg), C.byref(h)))
+        self.h = h
+        if record_events:
+            ctx._lib.sk_trainer_record_events(h, C.c_int(1))
+
+    def run(self, iterations):
+        rows = (SkLogRow * max(1, iterations))()
+        self.ctx.check(self.ctx._lib.sk_trainer_run(self.h, C.c_int(iterations), rows))
+        return [dict(iteration=r.iteration, gaussians=r.gaussians, tile_pairs=r.tile_pairs, loss=r.loss,
+                     psnr=r.psnr, elapsed_ms=r.elapsed_ms, view=r.view, event=r.event) for r in rows[:iterations]]
+
+    def events(self):
+        n = C.c_int()
+        self.ctx._lib.sk_trainer_num_events(self.h, C.byref(n))
+        out = []
+        for e in range(n.value):
+            hdr = np.zeros(7, np.int32)
+            self.ctx._lib.sk_trainer_event(self.h, C.c_int(e), _p(hdr), None, None, None, None, None)
+            nb, k = int(hdr[1]), int(hdr[6])
+            clone, split, prune = (np.zeros(max(nb, 1), np.uint8) for _ in range(3))
+            sampled = np.zeros(max(k, 1), np.int32)
+            photo = np.zeros(max(k, 1), np.float32)
+            self.ctx._lib.sk_trainer_event(self.h, C.c_int(e), _p(hdr), _p(clone), _p(split), _p(prune),
+                                           _p(sampled), _p(photo))
+            out.append(dict(iteration=int(hdr[0]), n_before=nb, n_after=int(hdr[2]), n_clone=int(hdr[3]),
+                            n_split=int(hdr[4]), n_prune=int(hdr[5]), clone=clone[:nb], split=split[:nb],
+                            prune=prune[:nb], sampled=sampled[:k], photometric=photo[:k]))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx._lib.sk_trainer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def train_step_host(ctx: Context, scene: Scene, cam, gt_u8, cfg, extent, iteration, frame=None) -> dict:
+    """One train_iteration with the GT in host memory (the end-to-end entry point)."""
+    frame = frame or ctx._frame
+    g = np.ascontiguousarray(gt_u8, np.uint8)
+    row = SkLogRow()
+    ctx.check(ctx._lib.sk_train_step_host(ctx.h, scene.h, frame, C.byref(as_camera(cam)), _p(g),
+                                          C.byref(as_config(cfg)), C.c_float(extent), C.c_int(iteration),
+                                          C.byref(row)))
+    return dict(loss=row.loss, psnr=row.psnr, tile_pairs=row.tile_pairs, gaussians=row.gaussians)

@@ -1,0 +1,645 @@
+// The paper's multi-view-consistent density control on the GPU:
+//   K11 error maps      build_error_maps        (reference error_maps.hpp:22-43)
+//   K12 count blend     blend_forward(mask,...) (raster.hpp:194-248 via adc.hpp:105-108)
+//   K13 finalize        scores_from_counts      (adc.hpp:48-84)
+//   K14 select          select_densify / select_prune (adc.hpp:135-153, 224-270)
+//   K15 compact         apply_prune / apply_densify + AdamGroup::remap
+//                       (adc.hpp:167-205, 273-289; adam.hpp:45-58)
+// and Trainer::density_event (trainer.hpp:177-243) that sequences them.
+//
+// Everything here is compiled with -fmad=false: the error map, the mask,
+// s_d and every selection flag are computed in the reference's fp32 order, so
+// given identical inputs they are bit-identical to the CPU oracle. Footprint
+// counts are exact integers (warp-aggregated atomics). Compaction is a
+// three-class exclusive scan (survivors / clones / split children) followed by
+// a scatter of parameters and Adam moments into fresh buffers.
+#include <algorithm>
+
+#include "abi_util.h"
+#include "trainer.h"
+
+namespace sk {
+namespace {
+
+// ---- K11: raw error map + min / max ---------------------------------------
+__global__ void error_raw_kernel(const float* __restrict__ image, const void* __restrict__ gt, bool gt_u8, int W, int H,
+                                 float* __restrict__ raw, uint32_t* __restrict__ lohi) {
+  const int64_t n = (int64_t)W * H;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float v = 0.0f;
+  const bool ok = p < n;
+  if (ok) {
+    float d[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float g = gt_u8 ? __fdiv_rn((float)static_cast<const uint8_t*>(gt)[p * 3 + c], 255.0f)
+                            : static_cast<const float*>(gt)[p * 3 + c];
+      d[c] = image[c * n + p] - g;
+    }
+    // (rendered - gt).cwiseAbs().sum() / T(3)
+    v = ((fabsf(d[0]) + fabsf(d[1])) + fabsf(d[2])) / 3.0f;
+    raw[p] = v;
+  }
+  // raw >= 0: ordering of the float bits is the ordering of the values
+  uint32_t lo = ok ? __float_as_uint(v) : 0xffffffffu;
+  uint32_t hi = ok ? __float_as_uint(v) : 0u;
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&lohi[0], lo);
+    atomicMax(&lohi[1], hi);
+  }
+}
+
+// normalized = (raw - lo) / (hi - lo) (all zero if degenerate); mask = normalized > tau
+__global__ void error_mask_kernel(const float* __restrict__ raw, const uint32_t* __restrict__ lohi, int64_t n,
+                                  float tau, uint8_t* __restrict__ mask) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float lo = __uint_as_float(lohi[0]), hi = __uint_as_float(lohi[1]);
+  const float nv = hi > lo ? (raw[p] - lo) / (hi - lo) : 0.0f;
+  mask[p] = nv > tau ? 1 : 0;
+}
+
+// ---- K13: s_d, s_p_raw in view order, then min-max of s_p_raw ---------------
+__global__ void scores_kernel(const int32_t* __restrict__ rows, int64_t row_stride, const float* __restrict__ photo,
+                              int k, int64_t n, float* __restrict__ s_d, float* __restrict__ s_p_raw,
+                              uint32_t* __restrict__ lohi) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float sd = 0.0f, sp = 0.0f;
+  const bool ok = i < n;
+  if (ok) {
+    for (int j = 0; j < k; ++j) {
+      const float c = (float)rows[(int64_t)j * row_stride + i];
+      sd = sd + c;
+      sp = sp + c * photo[j];
+    }
+    s_d[i] = sd / (float)k;
+    s_p_raw[i] = sp;
+  }
+  uint32_t lo = ok ? __float_as_uint(sp) : 0xffffffffu;
+  uint32_t hi = ok ? __float_as_uint(sp) : 0u;
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&lohi[0], lo);
+    atomicMax(&lohi[1], hi);
+  }
+}
+
+__global__ void minmax_normalize_kernel(const float* __restrict__ v, const uint32_t* __restrict__ lohi, int64_t n,
+                                        float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float lo = __uint_as_float(lohi[0]), hi = __uint_as_float(lohi[1]);
+  out[i] = hi > lo ? (v[i] - lo) / (hi - lo) : 0.0f;
+}
+
+__device__ __forceinline__ float max_scale(const float* p, int64_t stride, int64_t i) {
+  const float s0 = det_expf(p[(SK_COMP_LOG_SCALE + 0) * stride + i]);
+  const float s1 = det_expf(p[(SK_COMP_LOG_SCALE + 1) * stride + i]);
+  const float s2 = det_expf(p[(SK_COMP_LOG_SCALE + 2) * stride + i]);
+  float m = s0;
+  if (s1 > m) m = s1;
+  if (s2 > m) m = s2;
+  return m;
+}
+
+// ---- K14: selection flags -------------------------------------------------------
+__global__ void densify_flags_kernel(const float* __restrict__ p, int64_t stride, int64_t n,
+                                     const float* __restrict__ s_d, const float* __restrict__ gn,
+                                     const float* __restrict__ ag, const int* __restrict__ vs, float tau_d,
+                                     float thr, float dense_cut, bool use_vcd, uint8_t* __restrict__ clone,
+                                     uint8_t* __restrict__ split) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint8_t c = 0, s = 0;
+  const int seen = vs[i];
+  if (seen != 0 && !(use_vcd && !(s_d[i] > tau_d))) {
+    const float inv_seen = 1.0f / (float)seen;
+    const float mean_grad = gn[i] * inv_seen;
+    const float mean_abs = ag[i] * inv_seen;
+    if (max_scale(p, stride, i) <= dense_cut) {
+      c = mean_grad >= thr ? 1 : 0;
+    } else {
+      s = mean_abs >= thr ? 1 : 0;
+    }
+  }
+  clone[i] = c;
+  split[i] = s;
+}
+
+// early phase: vanilla candidates (key for the VCP ordering); late: the rule.
+__global__ void prune_flags_kernel(const float* __restrict__ p, int64_t stride, int64_t n,
+                                   const float* __restrict__ s_p, const float* __restrict__ max_r2d, bool early,
+                                   bool size_rules, float min_op, float world_cut, float screen, float op_cut,
+                                   bool use_vcp, float tau_p, uint8_t* __restrict__ flag, uint32_t* __restrict__ key,
+                                   uint32_t* __restrict__ idx, int* __restrict__ count) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool f = false;
+  if (i < n) {
+    const float op = det_sigmoidf(p[SK_COMP_OPACITY * stride + i]);
+    if (early) {
+      f = op < min_op;
+      if (size_rules) {
+        f = f || max_scale(p, stride, i) > world_cut;
+        f = f || max_r2d[i] > screen;
+      }
+      if (key) {
+        // ascending key == (s_p descending, index ascending); non-candidates last
+        key[i] = f ? (0x7f800000u - __float_as_uint(s_p[i])) : 0xffffffffu;
+        idx[i] = (uint32_t)i;
+      }
+    } else {
+      f = (op < op_cut) || (use_vcp && s_p[i] > tau_p);
+    }
+    flag[i] = f ? 1 : 0;
+  }
+  const uint32_t b = __ballot_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(count, __popc(b));
+}
+
+__global__ void vcp_take_kernel(const uint32_t* __restrict__ order, int take, uint8_t* __restrict__ flag, int64_t n) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  if (r < take) flag[order[r]] = 1;
+}
+
+// never empty the scene: keep the first index with the smallest s_p
+__global__ void argmin_kernel(const float* __restrict__ s_p, int64_t n, unsigned long long* __restrict__ best) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long v = ~0ull;
+  if (i < n) v = ((unsigned long long)__float_as_uint(s_p[i]) << 32) | (unsigned long long)i;
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMin(best, v);
+}
+
+// ---- K15: class flags and scatter -------------------------------------------------
+__global__ void class_kernel(const uint8_t* __restrict__ prune, const uint8_t* __restrict__ clone,
+                             const uint8_t* __restrict__ split, int64_t n, int32_t* __restrict__ keep_ns,
+                             int32_t* __restrict__ clone_k, int32_t* __restrict__ split_k) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool keep = !prune[i];
+  const bool sp = keep && split[i];
+  keep_ns[i] = (keep && !sp) ? 1 : 0;
+  clone_k[i] = (keep && clone[i]) ? 1 : 0;
+  split_k[i] = sp ? 1 : 0;
+}
+
+__global__ void compact_kernel(const float* __restrict__ src, const float* __restrict__ m_src,
+                               const float* __restrict__ v_src, int64_t stride, int64_t n, int comps,
+                               const int32_t* __restrict__ keep_ns, const int32_t* __restrict__ clone_k,
+                               const int32_t* __restrict__ split_k, const int32_t* __restrict__ pos_keep,
+                               const int32_t* __restrict__ pos_clone, const int32_t* __restrict__ pos_split,
+                               int64_t n_keep, int64_t n_clone, const float* __restrict__ grad3d,
+                               const int* __restrict__ views_seen, float clone_lr, const float* __restrict__ eps,
+                               float log_shrink, float* __restrict__ dst, float* __restrict__ m_dst,
+                               float* __restrict__ v_dst, int64_t dstride, int32_t* __restrict__ old_to_new) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool kns = keep_ns[i], cl = clone_k[i], sp = split_k[i];
+  int32_t final_index = -1;
+  if (kns) {
+    const int64_t d = pos_keep[i];
+    final_index = (int32_t)d;
+    for (int c = 0; c < comps; ++c) {
+      dst[c * dstride + d] = src[c * stride + i];
+      m_dst[c * dstride + d] = m_src[c * stride + i];
+      v_dst[c * dstride + d] = v_src[c * stride + i];
+    }
+  }
+  if (cl) {
+    // clone: one positional-gradient step (adc.hpp:184-189), fresh moments
+    const int64_t d = n_keep + pos_clone[i];
+    for (int c = 0; c < comps; ++c) {
+      dst[c * dstride + d] = src[c * stride + i];
+      m_dst[c * dstride + d] = 0.0f;
+      v_dst[c * dstride + d] = 0.0f;
+    }
+    const int seen = views_seen[i];
+    if (seen > 0) {
+      const float vs = (float)seen;
+      for (int k = 0; k < 3; ++k)
+        dst[(SK_COMP_MU + k) * dstride + d] = src[(SK_COMP_MU + k) * stride + i] - clone_lr * (grad3d[k * stride + i] / vs);
+    }
+  }
+  if (sp) {
+    // split: two children at parent.mu + R(eps * scale), log_scale - ln 1.6 (adc.hpp:190-201)
+    const int64_t r = pos_split[i];
+    const int64_t d0 = n_keep + n_clone + 2 * r;
+    const float qw_in = src[3 * stride + i], qx_in = src[4 * stride + i], qy_in = src[5 * stride + i],
+                qz_in = src[6 * stride + i];
+    float qw = qw_in, qx = qx_in, qy = qy_in, qz = qz_in;
+    const float n2 = ((qw * qw + qx * qx) + qy * qy) + qz * qz;
+    if (n2 > 0.0f) {
+      const float nq = sqrtf(n2);
+      qw = qw / nq;
+      qx = qx / nq;
+      qy = qy / nq;
+      qz = qz / nq;
+    }
+    float R[3][3];
+    R[0][0] = 1.0f - 2.0f * (qy * qy + qz * qz);
+    R[0][1] = 2.0f * (qx * qy - qw * qz);
+    R[0][2] = 2.0f * (qx * qz + qw * qy);
+    R[1][0] = 2.0f * (qx * qy + qw * qz);
+    R[1][1] = 1.0f - 2.0f * (qx * qx + qz * qz);
+    R[1][2] = 2.0f * (qy * qz - qw * qx);
+    R[2][0] = 2.0f * (qx * qz - qw * qy);
+    R[2][1] = 2.0f * (qy * qz + qw * qx);
+    R[2][2] = 1.0f - 2.0f * (qx * qx + qy * qy);
+    float s[3];
+    for (int k = 0; k < 3; ++k) s[k] = det_expf(src[(SK_COMP_LOG_SCALE + k) * stride + i]);
+    for (int child = 0; child < 2; ++child) {
+      const int64_t d = d0 + child;
+      for (int c = 0; c < comps; ++c) {
+        dst[c * dstride + d] = src[c * stride + i];
+        m_dst[c * dstride + d] = 0.0f;
+        v_dst[c * dstride + d] = 0.0f;
+      }
+      float es[3];
+      for (int k = 0; k < 3; ++k) es[k] = eps[r * 6 + child * 3 + k] * s[k];
+      for (int k = 0; k < 3; ++k) {
+        const float off = (R[k][0] * es[0] + R[k][1] * es[1]) + R[k][2] * es[2];
+        dst[(SK_COMP_MU + k) * dstride + d] = src[(SK_COMP_MU + k) * stride + i] + off;
+        dst[(SK_COMP_LOG_SCALE + k) * dstride + d] = src[(SK_COMP_LOG_SCALE + k) * stride + i] - log_shrink;
+      }
+    }
+  }
+  if (old_to_new) old_to_new[i] = final_index;
+}
+
+unsigned blocks(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
+
+}  // namespace
+
+// Renders the k views and leaves s_d / s_p_raw / s_p in the scene's table.
+// gt: device images (u8 HWC) or host float HWC images (staged per view).
+void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_camera>& cams,
+                const std::vector<const void*>& gts, bool gt_u8_device, float tau, float lambda,
+                const sk_binning& bin, std::vector<float>* photo_out) {
+  EventScratch& ev = ctx->ev;
+  const int k = (int)cams.size();
+  require(k > 0, "accumulate_scores: no training views");
+  ensure_score_table(ctx, s);
+  const int64_t n = s->n;
+  int32_t* rows = ensure<int32_t>(ev.rows, (size_t)k * std::max<int64_t>(n, 1));
+  uint32_t* lohi = ensure<uint32_t>(ev.lohi, 4);
+  std::vector<float> photo(k);
+  for (int j = 0; j < k; ++j) {
+    const sk_camera& cam = cams[j];
+    frame_geometry(f, cam.width, cam.height, &bin);
+    f->camera = cam;
+    ensure_projected(f, n);
+    launch_preprocess(ctx, s, cam, f);
+    bin_sort(ctx, f);
+    ensure_image(f);
+    launch_blend_forward(ctx, f, nullptr, nullptr);
+    f->rendered = true;
+    const int64_t npx = (int64_t)cam.width * cam.height;
+    const void* gt = gts[j];
+    if (!gt_u8_device) {
+      void* g = f->gt.ensure(sizeof(float) * 3 * npx);
+      h2d(ctx, g, static_cast<const float*>(gts[j]), 3 * npx);
+      gt = g;
+    }
+    float* raw = ensure<float>(ev.raw, npx);
+    uint8_t* mask = ensure<uint8_t>(ev.mask, npx);
+    const uint32_t init[2] = {0xffffffffu, 0u};
+    h2d(ctx, lohi, init, 2);
+    error_raw_kernel<<<blocks(npx), 256, 0, ctx->stream>>>(f->image.as<float>(), gt, gt_u8_device, cam.width,
+                                                            cam.height, raw, lohi);
+    note_launch();
+    error_mask_kernel<<<blocks(npx), 256, 0, ctx->stream>>>(raw, lohi, npx, tau, mask);
+    note_launch();
+    LossSums sums{};
+    launch_loss(ctx, f, gt, gt_u8_device, lambda, false, &sums);
+    sk_loss_values v{};
+    finish_loss(cam.width, cam.height, lambda, sums, &v);
+    // photometric = (1 - lambda) mean(raw) + lambda (1 - ssim)  (error_maps.hpp:40-41)
+    photo[j] = (1.0f - lambda) * (float)v.l1 + lambda * (1.0f - (float)v.ssim);
+    int32_t* row = rows + (size_t)j * n;
+    SK_CUDA(cudaMemsetAsync(row, 0, sizeof(int32_t) * n, ctx->stream));
+    launch_blend_forward(ctx, f, mask, row);
+  }
+  float* dphoto = ensure<float>(ev.photo, k);
+  h2d(ctx, dphoto, photo.data(), k);
+  const uint32_t init[2] = {0xffffffffu, 0u};
+  h2d(ctx, lohi, init, 2);
+  if (n > 0) {
+    scores_kernel<<<blocks(n), 256, 0, ctx->stream>>>(rows, n, dphoto, k, n, s->s_d.as<float>(),
+                                                       s->s_p_raw.as<float>(), lohi);
+    note_launch();
+    minmax_normalize_kernel<<<blocks(n), 256, 0, ctx->stream>>>(s->s_p_raw.as<float>(), lohi, n, s->s_p.as<float>());
+    note_launch();
+  }
+  SK_CUDA(cudaGetLastError());
+  if (photo_out) *photo_out = photo;
+}
+
+void select_densify_flags(sk_ctx* ctx, sk_scene* s, float tau_d, float thr, float percent_dense, bool use_vcd,
+                          float extent, uint8_t* clone, uint8_t* split) {
+  ensure_score_table(ctx, s);
+  if (s->n == 0) return;
+  densify_flags_kernel<<<blocks(s->n), 256, 0, ctx->stream>>>(
+      s->params.as<float>(), s->capacity, s->n, s->s_d.as<float>(), s->grad_norm_acc.as<float>(),
+      s->abs_grad_acc.as<float>(), s->views_seen.as<int>(), tau_d, thr, percent_dense * extent, use_vcd, clone, split);
+  note_launch();
+}
+
+void select_prune_flags(sk_ctx* ctx, sk_scene* s, int iteration, const sk_prune_params& pp, float extent,
+                        uint8_t* prune) {
+  ensure_score_table(ctx, s);
+  const int64_t n = s->n;
+  if (n == 0) return;
+  EventScratch& ev = ctx->ev;
+  const bool early = iteration < pp.densify_until;
+  int* count = reinterpret_cast<int*>(ensure<uint32_t>(ev.lohi, 4) + 2);
+  SK_CUDA(cudaMemsetAsync(count, 0, sizeof(int), ctx->stream));
+  uint32_t* key = nullptr;
+  uint32_t* idx = nullptr;
+  uint32_t *kb = nullptr, *vb = nullptr;
+  if (early && pp.use_vcp) {
+    key = ensure<uint32_t>(ev.keys_a, n);
+    idx = ensure<uint32_t>(ev.vals_a, n);
+    kb = ensure<uint32_t>(ev.keys_b, n);
+    vb = ensure<uint32_t>(ev.vals_b, n);
+  }
+  const float op_cut = pp.use_vcp ? pp.opacity_late : pp.min_opacity;
+  prune_flags_kernel<<<blocks(n), 256, 0, ctx->stream>>>(
+      s->params.as<float>(), s->capacity, n, s->s_p.as<float>(), s->max_radius2d.as<float>(), early,
+      iteration > pp.size_prune_from, pp.min_opacity, pp.world_size_frac * extent, pp.screen_size, op_cut,
+      pp.use_vcp != 0, pp.tau_p, prune, key, idx, count);
+  note_launch();
+  int host_count = 0;
+  d2h(ctx, &host_count, count, 1);
+  sync(ctx);
+  if (early && pp.use_vcp) {
+    // keep the ceil(|C|/2) highest-scoring candidates (ties by index) as pruned
+    SK_CUDA(cudaMemsetAsync(prune, 0, n, ctx->stream));
+    radix_sort_pairs(ctx, key, kb, idx, vb, n, 32);
+    const int take = (host_count + 1) / 2;
+    vcp_take_kernel<<<blocks(n), 256, 0, ctx->stream>>>(idx, take, prune, n);
+    note_launch();
+    host_count = take;
+  }
+  if (host_count == n && n > 0) {
+    unsigned long long* best = reinterpret_cast<unsigned long long*>(ensure<uint32_t>(ev.lohi, 4));
+    const unsigned long long init = ~0ull;
+    h2d(ctx, best, &init, 1);
+    argmin_kernel<<<blocks(n), 256, 0, ctx->stream>>>(s->s_p.as<float>(), n, best);
+    note_launch();
+    unsigned long long b = 0;
+    d2h(ctx, &b, best, 1);
+    sync(ctx);
+    const int64_t keep = (int64_t)(b & 0xffffffffull);
+    const uint8_t zero = 0;
+    h2d(ctx, prune + keep, &zero, 1);
+  }
+  SK_CUDA(cudaGetLastError());
+}
+
+// K15 on device flags; returns the new size. eps_dev: [n_split][6].
+int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint8_t* clone, const uint8_t* split,
+                      float clone_lr, const float* eps_host, int64_t n_split_expected, int32_t* old_to_new_dev) {
+  EventScratch& ev = ctx->ev;
+  const int64_t n = s->n;
+  if (n == 0) return 0;
+  int32_t* cls = ensure<int32_t>(ev.cls, 3 * (size_t)n);
+  int32_t* pos = ensure<int32_t>(ev.pos, 3 * (size_t)n);
+  class_kernel<<<blocks(n), 256, 0, ctx->stream>>>(prune, clone, split, n, cls, cls + n, cls + 2 * n);
+  note_launch();
+  const int64_t n_keep = scan_gathered(ctx, cls, nullptr, pos, n);
+  const int64_t n_clone = scan_gathered(ctx, cls + n, nullptr, pos + n, n);
+  const int64_t n_split = scan_gathered(ctx, cls + 2 * n, nullptr, pos + 2 * n, n);
+  require(n_split_expected < 0 || n_split_expected == n_split, "apply_densify: split count mismatch");
+  const int64_t new_n = n_keep + n_clone + 2 * n_split;
+  float* eps = ensure<float>(ev.eps, 6 * (size_t)std::max<int64_t>(n_split, 1));
+  if (n_split > 0) {
+    require(eps_host != nullptr, "apply_densify: split requires eps normals");
+    h2d(ctx, eps, eps_host, 6 * (size_t)n_split);
+  }
+  ensure_optimizer_state(ctx, s);
+  const int64_t new_cap = new_n > s->capacity ? std::max<int64_t>(new_n, s->capacity + s->capacity / 2) : s->capacity;
+  DevBuf np, nm, nv;
+  const size_t cells = (size_t)s->comps * new_cap;
+  ensure<float>(np, cells);
+  ensure<float>(nm, cells);
+  ensure<float>(nv, cells);
+  compact_kernel<<<blocks(n), 256, 0, ctx->stream>>>(
+      s->params.as<float>(), s->adam_m.as<float>(), s->adam_v.as<float>(), s->capacity, n, s->comps, cls, cls + n,
+      cls + 2 * n, pos, pos + n, pos + 2 * n, n_keep, n_clone, s->grad3d_acc.as<float>(), s->views_seen.as<int>(),
+      clone_lr, eps, (float)std::log(1.6), np.as<float>(), nm.as<float>(), nv.as<float>(), new_cap, old_to_new_dev);
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+  sync(ctx);
+  s->params.swap(np);
+  s->adam_m.swap(nm);
+  s->adam_v.swap(nv);
+  if (new_cap != s->capacity) {
+    s->capacity = new_cap;
+    s->grads.release();
+    for (DevBuf* b : {&s->s_d, &s->s_p_raw, &s->s_p, &s->grad_norm_acc, &s->abs_grad_acc, &s->grad3d_acc,
+                      &s->views_seen, &s->max_radius2d})
+      b->release();
+  }
+  s->n = new_n;
+  ensure_optimizer_state(ctx, s);
+  reset_score_table(ctx, s);
+  return new_n;
+}
+
+// Trainer::density_event (trainer.hpp:177-243).
+void density_event(sk_trainer* t, int it, bool densify, bool prune) {
+  sk_ctx* ctx = t->ctx;
+  sk_scene* s = t->scene;
+  const sk_train_config& cfg = t->cfg;
+  const std::vector<int> sampled = t->rng.sample_without_replacement((int)t->data->train.size(), cfg.k);
+  std::vector<sk_camera> cams;
+  std::vector<const void*> gts;
+  EventRecord rec;
+  rec.iteration = it;
+  rec.n_before = (int)s->n;
+  for (const int si : sampled) {
+    const int v = t->data->train[si];
+    cams.push_back(t->data->cams[v]);
+    gts.push_back(t->data->images[v]->ptr);
+    rec.sampled.push_back(v);
+  }
+  const sk_binning bin = binning_from(cfg);
+  score_pass(ctx, s, &t->frame, cams, gts, true, (float)cfg.tau, (float)cfg.lambda, bin, &rec.photometric);
+
+  const int64_t n = s->n;
+  uint8_t* flags = ensure<uint8_t>(ctx->ev.flags, 3 * (size_t)std::max<int64_t>(n, 1));
+  uint8_t* fclone = flags;
+  uint8_t* fsplit = flags + n;
+  uint8_t* fprune = flags + 2 * n;
+  SK_CUDA(cudaMemsetAsync(flags, 0, 3 * (size_t)n, ctx->stream));
+  const float extent = t->data->extent;
+  if (densify)
+    select_densify_flags(ctx, s, (float)cfg.tau_d, (float)cfg.grad_threshold, (float)cfg.percent_dense, cfg.vcd != 0,
+                         extent, fclone, fsplit);
+  if (prune) {
+    sk_prune_params pp;
+    pp.tau_p = (float)cfg.tau_p;
+    pp.min_opacity = (float)cfg.prune_min_opacity;
+    pp.opacity_late = (float)cfg.prune_opacity_late;
+    pp.world_size_frac = (float)cfg.prune_world_size_frac;
+    pp.screen_size = (float)cfg.prune_screen_size;
+    pp.size_prune_from = cfg.size_prune_from;
+    pp.densify_until = cfg.densify_until;
+    pp.use_vcp = cfg.vcp;
+    select_prune_flags(ctx, s, it, pp, extent, fprune);
+  }
+  // host view of the flags: split count for the Rng, and the event record
+  std::vector<uint8_t> h(3 * (size_t)n);
+  d2h(ctx, h.data(), flags, h.size());
+  sync(ctx);
+  int64_t n_split = 0, n_clone = 0, n_prune = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const bool pr = h[2 * n + i] != 0;
+    n_prune += pr;
+    if (!pr) {
+      n_split += h[n + i] != 0;
+      n_clone += h[i] != 0;
+    }
+  }
+  // 6 normals per split Gaussian, ascending index order (adc.hpp:190-197)
+  std::vector<float> eps(6 * (size_t)n_split);
+  for (auto& e : eps) e = (float)t->rng.normal();
+  const float pos_lr = expon_lr((float)cfg.lr_position * extent, (float)cfg.lr_position_final * extent, it,
+                                cfg.iterations);
+  compact_scene(ctx, s, fprune, fclone, fsplit, pos_lr, eps.data(), n_split, nullptr);
+  if (t->record_events) {
+    rec.prune.assign(h.begin() + 2 * n, h.begin() + 3 * n);
+    rec.clone.assign(h.begin(), h.begin() + n);
+    rec.split.assign(h.begin() + n, h.begin() + 2 * n);
+    for (int64_t i = 0; i < n; ++i)
+      if (rec.prune[i]) rec.clone[i] = rec.split[i] = 0;
+    rec.n_clone = (int)n_clone;
+    rec.n_split = (int)n_split;
+    rec.n_prune = (int)n_prune;
+    rec.n_after = (int)s->n;
+    t->events.push_back(std::move(rec));
+  }
+}
+
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+void sk_default_prune_params(sk_prune_params* p) {
+  if (!p) return;
+  *p = sk_prune_params{(float)0.9, (float)0.005, (float)0.1, (float)0.1, 20.0f, 3000, 15000, 1};
+}
+
+int sk_accumulate_scores(sk_ctx* ctx, sk_scene* s, int k, const sk_camera* cams, const float* images, float tau,
+                         float lambda, const sk_binning* b, int32_t* counts_out, float* photo_out) {
+  return guarded(ctx, [&] {
+    require(k > 0, "accumulate_scores: no training views");
+    arg(s && cams && images, "accumulate_scores: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    std::vector<sk_camera> cv(cams, cams + k);
+    std::vector<const void*> gts;
+    size_t off = 0;
+    for (int j = 0; j < k; ++j) {
+      gts.push_back(images + off);
+      off += (size_t)cams[j].width * cams[j].height * 3;
+    }
+    sk_frame f;
+    std::vector<float> photo;
+    const sk_binning bin = b ? *b : sk_binning{0, 1.0f, (float)(1.0 / 255), 16};
+    score_pass(ctx, s, &f, cv, gts, false, tau, lambda, bin, &photo);
+    if (counts_out && s->n > 0) d2h(ctx, counts_out, ctx->ev.rows.ptr, (size_t)k * s->n);
+    sync(ctx);
+    if (photo_out) std::copy(photo.begin(), photo.end(), photo_out);
+  });
+}
+
+int sk_select_densify(sk_ctx* ctx, sk_scene* s, float tau_d, float thr, float percent_dense, int use_vcd,
+                      float extent, uint8_t* clone, uint8_t* split) {
+  return guarded(ctx, [&] {
+    arg(s && clone && split, "select_densify: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    const int64_t n = s->n;
+    uint8_t* f = ensure<uint8_t>(ctx->ev.flags, 3 * (size_t)std::max<int64_t>(n, 1));
+    select_densify_flags(ctx, s, tau_d, thr, percent_dense, use_vcd != 0, extent, f, f + n);
+    d2h(ctx, clone, f, n);
+    d2h(ctx, split, f + n, n);
+    sync(ctx);
+  });
+}
+
+int sk_select_prune(sk_ctx* ctx, sk_scene* s, int iteration, const sk_prune_params* pp, float extent,
+                    uint8_t* prune) {
+  return guarded(ctx, [&] {
+    arg(s && pp && prune, "select_prune: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    const int64_t n = s->n;
+    uint8_t* f = ensure<uint8_t>(ctx->ev.flags, 3 * (size_t)std::max<int64_t>(n, 1));
+    select_prune_flags(ctx, s, iteration, *pp, extent, f + 2 * n);
+    d2h(ctx, prune, f + 2 * n, n);
+    sync(ctx);
+  });
+}
+
+int sk_apply_prune_densify(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint8_t* clone, const uint8_t* split,
+                           float clone_lr, const float* eps, int32_t* old_to_new, int64_t* new_size) {
+  return guarded(ctx, [&] {
+    arg(s != nullptr, "apply_densify: null scene");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    const int64_t n = s->n;
+    uint8_t* f = ensure<uint8_t>(ctx->ev.flags, 3 * (size_t)std::max<int64_t>(n, 1));
+    SK_CUDA(cudaMemsetAsync(f, 0, 3 * (size_t)n, ctx->stream));
+    if (clone) h2d(ctx, f, clone, n);
+    if (split) h2d(ctx, f + n, split, n);
+    if (prune) h2d(ctx, f + 2 * n, prune, n);
+    int32_t* o2n = old_to_new ? ensure<int32_t>(ctx->ev.old_to_new, (size_t)std::max<int64_t>(n, 1)) : nullptr;
+    ensure_score_table(ctx, s);
+    const int64_t nn = compact_scene(ctx, s, f + 2 * n, f, f + n, clone_lr, eps, -1, o2n);
+    if (old_to_new && n > 0) d2h(ctx, old_to_new, o2n, n);
+    sync(ctx);
+    if (new_size) *new_size = nn;
+  });
+}
+
+int sk_trainer_record_events(sk_trainer* t, int on) {
+  if (!t) return SK_ERR_INVALID_ARGUMENT;
+  t->record_events = on != 0;
+  return SK_OK;
+}
+
+int sk_trainer_num_events(const sk_trainer* t, int* n) {
+  if (!t || !n) return SK_ERR_INVALID_ARGUMENT;
+  *n = (int)t->events.size();
+  return SK_OK;
+}
+
+int sk_trainer_event(const sk_trainer* t, int e, int32_t* header, uint8_t* clone, uint8_t* split, uint8_t* prune,
+                     int32_t* sampled, float* photometric) {
+  if (!t || e < 0 || e >= (int)t->events.size()) return SK_ERR_INVALID_ARGUMENT;
+  const EventRecord& r = t->events[e];
+  if (header) {
+    header[0] = r.iteration;
+    header[1] = r.n_before;
+    header[2] = r.n_after;
+    header[3] = r.n_clone;
+    header[4] = r.n_split;
+    header[5] = r.n_prune;
+    header[6] = (int32_t)r.sampled.size();
+  }
+  if (clone) std::copy(r.clone.begin(), r.clone.end(), clone);
+  if (split) std::copy(r.split.begin(), r.split.end(), split);
+  if (prune) std::copy(r.prune.begin(), r.prune.end(), prune);
+  if (sampled) std::copy(r.sampled.begin(), r.sampled.end(), sampled);
+  if (photometric) std::copy(r.photometric.begin(), r.photometric.end(), photometric);
+  return SK_OK;
+}
+
+}  // extern "C"

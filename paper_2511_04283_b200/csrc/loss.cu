@@ -1,0 +1,258 @@
+// K7: fused L1 + D-SSIM loss forward and backward.
+//
+// Restates training_loss (reference loss.hpp:21-47) and ssim_with_grad
+// (metrics.hpp:93-122): 11-tap separable Gaussian (sigma 1.5, normalised
+// weights), zero padding without renormalisation at the borders
+// (metrics.hpp:30-52), per-channel SSIM map, and the analytic gradient
+//   g = filt(u_mu) + filt(u_mxy) * y + filt(u_mxx) * 2 x.
+// Two kernels over 16x16 pixel tiles with a 5-pixel halo staged in shared
+// memory: kernel A filters the five moments (x, y, x^2, y^2, xy) of each
+// channel, forms the SSIM map and the three per-pixel partials, and reduces
+// the L1 / SSIM / squared-error sums; kernel B filters the partials and
+// writes dL/dimage = (1 - lambda) sign(r - g) / 3HW - lambda g.
+// This file is compiled with FMA contraction on: nothing here feeds the
+// bit-exact binning path, and the loss is checked against the oracle within
+// a tolerance.
+#include "state.h"
+
+namespace sk {
+namespace {
+
+constexpr int kT = 16;           // output tile edge
+constexpr int kHalo = 5;         // 11-tap window
+constexpr int kIn = kT + 2 * kHalo;  // 26
+
+__constant__ float c_gauss[11];
+
+// gt sample: u8 HWC decoded as byte / 255.0f (png_io.cpp:64), or f32 HWC.
+__device__ __forceinline__ float gt_at(const void* gt, bool u8, size_t p, int ch) {
+  if (u8) return __fdiv_rn((float)static_cast<const uint8_t*>(gt)[p * 3 + ch], 255.0f);
+  return static_cast<const float*>(gt)[p * 3 + ch];
+}
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sh[i];
+  return s;
+}
+
+// Kernel A. partials: planar [3 maps][3 ch][H][W]; also writes the L1 part of
+// dL/dimage into dimage (planar [3][H][W]).
+__global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ img, const void* __restrict__ gt,
+                                                       bool gt_u8, int W, int H, float nrm, float lambda,
+                                                       float inv_n, bool want_grad, float* __restrict__ partials,
+                                                       float* __restrict__ dimage, double* __restrict__ sums) {
+  __shared__ float s_x[kIn][kIn + 1];
+  __shared__ float s_y[kIn][kIn + 1];
+  __shared__ float s_h[5][kIn][kT + 1];
+  __shared__ double s_red[8];
+  const int tx0 = blockIdx.x * kT, ty0 = blockIdx.y * kT;
+  const int lx = threadIdx.x % kT, ly = threadIdx.x / kT;
+  const int px = tx0 + lx, py = ty0 + ly;
+  const bool inside = px < W && py < H;
+  const size_t plane = (size_t)W * H;
+  double l1 = 0.0, ss = 0.0, sq = 0.0;
+  for (int ch = 0; ch < 3; ++ch) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kIn * kIn; i += blockDim.x) {
+      const int iy = i / kIn, ix = i % kIn;
+      const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
+      float xv = 0.0f, yv = 0.0f;
+      if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+        const size_t p = (size_t)gy * W + gx;
+        xv = img[ch * plane + p];
+        yv = gt_at(gt, gt_u8, p, ch);
+      }
+      s_x[iy][ix] = xv;
+      s_y[iy][ix] = yv;
+    }
+    __syncthreads();
+    // horizontal pass over all kIn rows, kT output columns
+    for (int i = threadIdx.x; i < kIn * kT; i += blockDim.x) {
+      const int iy = i / kT, ox = i % kT;
+      float a = 0.f, b = 0.f, cxx = 0.f, cyy = 0.f, cxy = 0.f;
+#pragma unroll
+      for (int o = 0; o < 11; ++o) {
+        const float w = c_gauss[o];
+        const float xv = s_x[iy][ox + o], yv = s_y[iy][ox + o];
+        a += w * xv;
+        b += w * yv;
+        cxx += w * (xv * xv);
+        cyy += w * (yv * yv);
+        cxy += w * (xv * yv);
+      }
+      s_h[0][iy][ox] = a;
+      s_h[1][iy][ox] = b;
+      s_h[2][iy][ox] = cxx;
+      s_h[3][iy][ox] = cyy;
+      s_h[4][iy][ox] = cxy;
+    }
+    __syncthreads();
+    float m[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      float s = 0.f;
+#pragma unroll
+      for (int o = 0; o < 11; ++o) s += c_gauss[o] * s_h[k][ly + o][lx];
+      m[k] = s;
+    }
+    if (inside) {
+      const float mx = m[0], my = m[1];
+      const float C1 = (float)(0.01 * 0.01), C2 = (float)(0.03 * 0.03);
+      const float a1 = 2.0f * mx * my + C1;
+      const float a2 = 2.0f * (m[4] - mx * my) + C2;
+      const float b1 = mx * mx + my * my + C1;
+      const float b2 = (m[2] - mx * mx) + (m[3] - my * my) + C2;
+      const float s = (a1 * a2) / (b1 * b2);
+      ss += (double)s;
+      const size_t p = (size_t)py * W + px;
+      const float xv = s_x[ly + kHalo][lx + kHalo];
+      const float yv = s_y[ly + kHalo][lx + kHalo];
+      const float diff = xv - yv;
+      l1 += (double)fabsf(diff);
+      sq += (double)diff * (double)diff;
+      if (want_grad) {
+        const float inv_bb = 1.0f / (b1 * b2);
+        partials[(0 * 3 + ch) * plane + p] =
+            nrm * (a2 * inv_bb * 2.0f * my - a1 * inv_bb * 2.0f * my - s / b1 * 2.0f * mx + s / b2 * 2.0f * mx);
+        partials[(1 * 3 + ch) * plane + p] = nrm * (a1 * inv_bb * 2.0f);
+        partials[(2 * 3 + ch) * plane + p] = nrm * (-s / b2);
+        const float sg = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
+        dimage[ch * plane + p] = (1.0f - lambda) * sg * inv_n;
+      }
+    }
+  }
+  const double t_l1 = block_sum(l1, s_red);
+  const double t_ss = block_sum(ss, s_red);
+  const double t_sq = block_sum(sq, s_red);
+  if (threadIdx.x == 0) {
+    atomicAdd(&sums[0], t_l1);
+    atomicAdd(&sums[1], t_ss);
+    atomicAdd(&sums[2], t_sq);
+  }
+}
+
+// Kernel B: filter the partials and finish dL/dimage.
+__global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ img, const void* __restrict__ gt,
+                                                       bool gt_u8, int W, int H, float lambda,
+                                                       const float* __restrict__ partials,
+                                                       float* __restrict__ dimage) {
+  __shared__ float s_u[3][kIn][kIn + 1];
+  __shared__ float s_h[3][kIn][kT + 1];
+  const int tx0 = blockIdx.x * kT, ty0 = blockIdx.y * kT;
+  const int lx = threadIdx.x % kT, ly = threadIdx.x / kT;
+  const int px = tx0 + lx, py = ty0 + ly;
+  const bool inside = px < W && py < H;
+  const size_t plane = (size_t)W * H;
+  for (int ch = 0; ch < 3; ++ch) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kIn * kIn; i += blockDim.x) {
+      const int iy = i / kIn, ix = i % kIn;
+      const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
+      const bool ok = gx >= 0 && gx < W && gy >= 0 && gy < H;
+      const size_t p = (size_t)gy * W + gx;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) s_u[k][iy][ix] = ok ? partials[(k * 3 + ch) * plane + p] : 0.0f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kIn * kT; i += blockDim.x) {
+      const int iy = i / kT, ox = i % kT;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        float s = 0.f;
+#pragma unroll
+        for (int o = 0; o < 11; ++o) s += c_gauss[o] * s_u[k][iy][ox + o];
+        s_h[k][iy][ox] = s;
+      }
+    }
+    __syncthreads();
+    if (inside) {
+      float f[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        float s = 0.f;
+#pragma unroll
+        for (int o = 0; o < 11; ++o) s += c_gauss[o] * s_h[k][ly + o][lx];
+        f[k] = s;
+      }
+      const size_t p = (size_t)py * W + px;
+      const float xv = img[ch * plane + p];
+      const float yv = gt_at(gt, gt_u8, p, ch);
+      const float g = f[0] + f[1] * yv + f[2] * 2.0f * xv;
+      dimage[ch * plane + p] = dimage[ch * plane + p] - lambda * g;
+    }
+  }
+}
+
+bool g_gauss_ready[64] = {};
+
+void upload_gauss(cudaStream_t s) {
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && g_gauss_ready[dev]) return;
+  // ssim_kernel<float> (metrics.hpp:17-25): exp in float, normalised by the sum.
+  float k[11];
+  float sum = 0.0f;
+  for (int i = 0; i < 11; ++i) {
+    const float d = (float)(i - 5);
+    k[i] = std::exp(-(d * d) / (2.0f * (float)1.5 * (float)1.5));
+    sum = sum + k[i];
+  }
+  for (int i = 0; i < 11; ++i) k[i] = k[i] / sum;
+  SK_CUDA(cudaMemcpyToSymbolAsync(c_gauss, k, sizeof(k), 0, cudaMemcpyHostToDevice, s));
+  SK_CUDA(cudaStreamSynchronize(s));
+  if (dev < 64) g_gauss_ready[dev] = true;
+}
+
+}  // namespace
+
+void launch_loss(sk_ctx* ctx, sk_frame* f, const void* gt, bool gt_u8, float lambda, bool want_grad, LossSums* out) {
+  upload_gauss(ctx->stream);
+  const int W = f->width, H = f->height;
+  const size_t plane = (size_t)W * H;
+  float* partials = want_grad ? ensure<float>(f->loss_scratch, 9 * plane) : nullptr;
+  float* dimage = want_grad ? ensure<float>(f->dimage, 3 * plane) : nullptr;
+  double* sums = ensure<double>(ctx->scalars, 4);
+  SK_CUDA(cudaMemsetAsync(sums, 0, 4 * sizeof(double), ctx->stream));
+  const dim3 grid((W + kT - 1) / kT, (H + kT - 1) / kT);
+  const float nrm = 1.0f / (3.0f * (float)W * (float)H);
+  const float inv_n = 1.0f / (3.0f * (float)plane);
+  ssim_fwd_kernel<<<grid, 256, 0, ctx->stream>>>(f->image.as<float>(), gt, gt_u8, W, H, nrm, lambda, inv_n, want_grad,
+                                                 partials, dimage, sums);
+  note_launch();
+  if (want_grad) {
+    ssim_bwd_kernel<<<grid, 256, 0, ctx->stream>>>(f->image.as<float>(), gt, gt_u8, W, H, lambda, partials, dimage);
+    note_launch();
+  }
+  SK_CUDA(cudaGetLastError());
+  if (out) read_loss_sums(ctx, out);
+}
+
+void read_loss_sums(sk_ctx* ctx, LossSums* out) {
+  double h[4];
+  SK_CUDA(cudaMemcpyAsync(h, ctx->scalars.ptr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  SK_CUDA(cudaStreamSynchronize(ctx->stream));
+  out->l1 = h[0];
+  out->ssim = h[1];
+  out->sq = h[2];
+}
+
+// LossResult scalars (loss.hpp:45) and psnr (metrics.hpp:126-134) from the sums.
+void finish_loss(int width, int height, float lambda, const LossSums& s, sk_loss_values* out) {
+  const double npx = (double)width * height;
+  const double l1 = s.l1 / (3.0 * npx);
+  const double ssim = s.ssim / (3.0 * npx);
+  const double mse = s.sq / (3.0 * npx);
+  out->l1 = l1;
+  out->ssim = ssim;
+  out->loss = (1.0 - lambda) * l1 + lambda * (1.0 - ssim);
+  out->psnr = mse < 1e-10 ? 100.0 : 10.0 * std::log10(1.0 / mse);
+}
+
+}  // namespace sk

@@ -1,0 +1,477 @@
+// K9 project-backward + ScoreTable statistics, K10 dense Adam, and the fused
+// K9+K10 kernel used by the training step.
+//
+// K9 restates cov_grad_from_inv_grad and project_backward (reference
+// camera.hpp:148-213) with evaluate_sh_backward (sh.hpp:93-114) and
+// covariance_3d_backward / quat_rotation_backward (scene.hpp:70-110), plus the
+// per-render statistics of Trainer::train_iteration (trainer.hpp:139-156).
+// K10 restates AdamGroup::step (adam.hpp:62-74) for all six groups of
+// SceneOptimizer::step (:124-143): dense over every Gaussian, a per-group
+// step counter and bias correction, eps outside the sqrt.
+//
+// Fused path: one thread per Gaussian computes the 11+3n_sh parameter
+// gradients in registers (zero when the Gaussian was culled) and applies
+// Adam in the same pass, so gradients never round-trip through HBM. HBM
+// traffic per Gaussian = params + m + v read and written (6 x 4 B x comps) +
+// the 44 B of blend gradients; the kernel is bandwidth-bound by design.
+#include "state.h"
+
+namespace sk {
+namespace {
+
+constexpr float kC0 = 0.28209479177387814f;
+constexpr float kC1 = 0.4886025119029199f;
+__device__ constexpr float kC2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
+                                     -1.0925484305920792f, 0.5462742152960396f};
+__device__ constexpr float kC3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
+                                     0.3731763325901154f,  -0.4570457994644658f, 1.445305721320277f,
+                                     -0.5900435899266435f};
+
+struct Stats {
+  float* grad_norm_acc;
+  float* abs_grad_acc;
+  float* grad3d_acc;  // [3][stride]
+  int* views_seen;
+  float* max_radius2d;
+};
+
+// Computes all parameter gradients of one visible Gaussian (camera.hpp:156-213).
+// grad[] is indexed by SK_COMP_*.
+template <int DEG>
+__device__ __forceinline__ void project_backward_one(const float* __restrict__ p, int64_t stride, int64_t i,
+                                                     const CamParams& cam, const float dmu2d[2], const float dcov[2][2],
+                                                     const float dcol[3], float dop, float* grad) {
+  constexpr int NSH = (DEG + 1) * (DEG + 1);
+  const float mu[3] = {p[0 * stride + i], p[1 * stride + i], p[2 * stride + i]};
+  const float* R = cam.r;
+  float t[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = ((R[3 * k] * mu[0] + R[3 * k + 1] * mu[1]) + R[3 * k + 2] * mu[2]) + cam.t[k];
+  const float iz = 1.0f / t[2];
+  const float iz2 = iz * iz;
+  const float iz3 = iz2 * iz;
+  const float J[2][3] = {{cam.fx * iz, 0.0f, -cam.fx * t[0] * iz2}, {0.0f, cam.fy * iz, -cam.fy * t[1] * iz2}};
+  float m[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) m[a][j] = (J[a][0] * R[j] + J[a][1] * R[3 + j]) + J[a][2] * R[6 + j];
+  // rotation / scale
+  const float q_in[4] = {p[3 * stride + i], p[4 * stride + i], p[5 * stride + i], p[6 * stride + i]};
+  const float s[3] = {det_expf(p[7 * stride + i]), det_expf(p[8 * stride + i]), det_expf(p[9 * stride + i])};
+  const float n2 = ((q_in[0] * q_in[0] + q_in[1] * q_in[1]) + q_in[2] * q_in[2]) + q_in[3] * q_in[3];
+  const float nq = sqrtf(n2);
+  const float w = q_in[0] / nq, x = q_in[1] / nq, y = q_in[2] / nq, z = q_in[3] / nq;
+  float r[3][3];
+  r[0][0] = 1.0f - 2.0f * (y * y + z * z);
+  r[0][1] = 2.0f * (x * y - w * z);
+  r[0][2] = 2.0f * (x * z + w * y);
+  r[1][0] = 2.0f * (x * y + w * z);
+  r[1][1] = 1.0f - 2.0f * (x * x + z * z);
+  r[1][2] = 2.0f * (y * z - w * x);
+  r[2][0] = 2.0f * (x * z - w * y);
+  r[2][1] = 2.0f * (y * z + w * x);
+  r[2][2] = 1.0f - 2.0f * (x * x + y * y);
+  float M[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) M[a][b] = r[a][b] * s[b];
+  float S[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) S[a][b] = (M[a][0] * M[b][0] + M[a][1] * M[b][1]) + M[a][2] * M[b][2];
+
+  // opacity (camera.hpp:171-172)
+  const float sig = det_sigmoidf(p[SK_COMP_OPACITY * stride + i]);
+  grad[SK_COMP_OPACITY] = dop * sig * (1.0f - sig);
+
+  // colour (camera.hpp:175-182, sh.hpp:93-114)
+  float gmu[3];
+  {
+    const float rel[3] = {mu[0] - cam.center[0], mu[1] - cam.center[1], mu[2] - cam.center[2]};
+    const float dist = sqrtf((rel[0] * rel[0] + rel[1] * rel[1]) + rel[2] * rel[2]);
+    const float dx = rel[0] / dist, dy = rel[1] / dist, dz = rel[2] / dist;
+    float basis[NSH];
+    float db[NSH][3];
+    basis[0] = kC0;
+    db[0][0] = db[0][1] = db[0][2] = 0.0f;
+    if (DEG >= 1) {
+      basis[1] = -kC1 * dy;
+      basis[2] = kC1 * dz;
+      basis[3] = -kC1 * dx;
+      db[1][0] = 0.f, db[1][1] = -kC1, db[1][2] = 0.f;
+      db[2][0] = 0.f, db[2][1] = 0.f, db[2][2] = kC1;
+      db[3][0] = -kC1, db[3][1] = 0.f, db[3][2] = 0.f;
+    }
+    if (DEG >= 2) {
+      const float xx = dx * dx, yy = dy * dy, zz = dz * dz;
+      basis[4] = kC2[0] * (dx * dy);
+      basis[5] = kC2[1] * (dy * dz);
+      basis[6] = kC2[2] * (2.0f * zz - xx - yy);
+      basis[7] = kC2[3] * (dx * dz);
+      basis[8] = kC2[4] * (xx - yy);
+      db[4][0] = kC2[0] * dy, db[4][1] = kC2[0] * dx, db[4][2] = 0.f;
+      db[5][0] = 0.f, db[5][1] = kC2[1] * dz, db[5][2] = kC2[1] * dy;
+      db[6][0] = kC2[2] * (-2.0f * dx), db[6][1] = kC2[2] * (-2.0f * dy), db[6][2] = kC2[2] * (4.0f * dz);
+      db[7][0] = kC2[3] * dz, db[7][1] = 0.f, db[7][2] = kC2[3] * dx;
+      db[8][0] = kC2[4] * (2.0f * dx), db[8][1] = kC2[4] * (-2.0f * dy), db[8][2] = 0.f;
+      if (DEG >= 3) {
+        basis[9] = kC3[0] * dy * (3.0f * xx - yy);
+        basis[10] = kC3[1] * (dx * dy) * dz;
+        basis[11] = kC3[2] * dy * (4.0f * zz - xx - yy);
+        basis[12] = kC3[3] * dz * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+        basis[13] = kC3[4] * dx * (4.0f * zz - xx - yy);
+        basis[14] = kC3[5] * dz * (xx - yy);
+        basis[15] = kC3[6] * dx * (xx - 3.0f * yy);
+        db[9][0] = kC3[0] * (6.0f * dx * dy), db[9][1] = kC3[0] * (3.0f * xx - 3.0f * yy), db[9][2] = 0.f;
+        db[10][0] = kC3[1] * (dy * dz), db[10][1] = kC3[1] * (dx * dz), db[10][2] = kC3[1] * (dx * dy);
+        db[11][0] = kC3[2] * (-2.0f * dx * dy), db[11][1] = kC3[2] * (4.0f * zz - xx - 3.0f * yy),
+        db[11][2] = kC3[2] * (8.0f * dy * dz);
+        db[12][0] = kC3[3] * (-6.0f * dx * dz), db[12][1] = kC3[3] * (-6.0f * dy * dz),
+        db[12][2] = kC3[3] * (6.0f * zz - 3.0f * xx - 3.0f * yy);
+        db[13][0] = kC3[4] * (4.0f * zz - 3.0f * xx - yy), db[13][1] = kC3[4] * (-2.0f * dx * dy),
+        db[13][2] = kC3[4] * (8.0f * dx * dz);
+        db[14][0] = kC3[5] * (2.0f * dx * dz), db[14][1] = kC3[5] * (-2.0f * dy * dz), db[14][2] = kC3[5] * (xx - yy);
+        db[15][0] = kC3[6] * (3.0f * xx - 3.0f * yy), db[15][1] = kC3[6] * (-6.0f * dx * dy), db[15][2] = 0.f;
+      }
+    }
+    float raw[3] = {0.f, 0.f, 0.f};
+    float sh[NSH][3];
+#pragma unroll
+    for (int k = 0; k < NSH; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        sh[k][c] = p[(SK_COMP_SH + 3 * k + c) * stride + i];
+        raw[c] += basis[k] * sh[k][c];
+      }
+    float draw[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) draw[c] = (raw[c] + 0.5f < 0.0f) ? 0.0f : dcol[c];
+    float ddir[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < NSH; ++k) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) grad[SK_COMP_SH + 3 * k + c] = basis[k] * draw[c];
+      const float sd = (sh[k][0] * draw[0] + sh[k][1] * draw[1]) + sh[k][2] * draw[2];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ddir[c] += sd * db[k][c];
+    }
+    const float dd = (dx * ddir[0] + dy * ddir[1]) + dz * ddir[2];
+    gmu[0] = (ddir[0] - dx * dd) / dist;
+    gmu[1] = (ddir[1] - dy * dd) / dist;
+    gmu[2] = (ddir[2] - dz * dd) / dist;
+  }
+
+  // covariance: d_m = ((G + G^T) m) Sigma, d_Sigma3 = (m^T G) m
+  float Gs[2][2] = {{dcov[0][0] + dcov[0][0], dcov[0][1] + dcov[1][0]},
+                    {dcov[1][0] + dcov[0][1], dcov[1][1] + dcov[1][1]}};
+  float Gm[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Gm[a][j] = Gs[a][0] * m[0][j] + Gs[a][1] * m[1][j];
+  float dm[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dm[a][j] = (Gm[a][0] * S[0][j] + Gm[a][1] * S[1][j]) + Gm[a][2] * S[2][j];
+  float mG[3][2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) mG[a][b] = m[0][a] * dcov[0][b] + m[1][a] * dcov[1][b];
+  float dS[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) dS[a][b] = mG[a][0] * m[0][b] + mG[a][1] * m[1][b];
+  // covariance_3d_backward (scene.hpp:101-110)
+  {
+    float dM[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc += (dS[a][k] + dS[k][a]) * M[k][b];
+        dM[a][b] = acc;
+      }
+    float dr[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) dr[a][b] = dM[a][b] * s[b];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const float ds = (dM[0][b] * r[0][b] + dM[1][b] * r[1][b]) + dM[2][b] * r[2][b];
+      grad[SK_COMP_LOG_SCALE + b] = ds * s[b];
+    }
+    // quat_rotation_backward (scene.hpp:70-84)
+    const float du_w = dr[0][1] * (-2.0f * z) + dr[0][2] * (2.0f * y) + dr[1][0] * (2.0f * z) +
+                       dr[1][2] * (-2.0f * x) + dr[2][0] * (-2.0f * y) + dr[2][1] * (2.0f * x);
+    const float du_x = dr[0][1] * (2.0f * y) + dr[0][2] * (2.0f * z) + dr[1][0] * (2.0f * y) +
+                       dr[1][1] * (-4.0f * x) + dr[1][2] * (-2.0f * w) + dr[2][0] * (2.0f * z) +
+                       dr[2][1] * (2.0f * w) + dr[2][2] * (-4.0f * x);
+    const float du_y = dr[0][0] * (-4.0f * y) + dr[0][1] * (2.0f * x) + dr[0][2] * (2.0f * w) +
+                       dr[1][0] * (2.0f * x) + dr[1][2] * (2.0f * z) + dr[2][0] * (-2.0f * w) +
+                       dr[2][1] * (2.0f * z) + dr[2][2] * (-4.0f * y);
+    const float du_z = dr[0][0] * (-4.0f * z) + dr[0][1] * (-2.0f * w) + dr[0][2] * (2.0f * x) +
+                       dr[1][0] * (2.0f * w) + dr[1][1] * (-4.0f * z) + dr[1][2] * (2.0f * y) +
+                       dr[2][0] * (2.0f * x) + dr[2][1] * (2.0f * y);
+    const float qd = ((w * du_w + x * du_x) + y * du_y) + z * du_z;
+    grad[SK_COMP_ROT + 0] = (du_w - w * qd) / nq;
+    grad[SK_COMP_ROT + 1] = (du_x - x * qd) / nq;
+    grad[SK_COMP_ROT + 2] = (du_y - y * qd) / nq;
+    grad[SK_COMP_ROT + 3] = (du_z - z * qd) / nq;
+  }
+  // d_j = d_m R^T ; d_t (camera.hpp:197-207) ; + J^T d_mu2d ; mu += R^T d_t
+  float dj[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dj[a][j] = (dm[a][0] * R[3 * j] + dm[a][1] * R[3 * j + 1]) + dm[a][2] * R[3 * j + 2];
+  float dt[3];
+  dt[0] = dj[0][2] * (-cam.fx * iz2);
+  dt[1] = dj[1][2] * (-cam.fy * iz2);
+  dt[2] = ((dj[0][0] * (-cam.fx * iz2) + dj[0][2] * (2.0f * cam.fx * t[0] * iz3)) + dj[1][1] * (-cam.fy * iz2)) +
+          dj[1][2] * (2.0f * cam.fy * t[1] * iz3);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) dt[k] += J[0][k] * dmu2d[0] + J[1][k] * dmu2d[1];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) grad[SK_COMP_MU + k] = gmu[k] + ((R[k] * dt[0] + R[3 + k] * dt[1]) + R[6 + k] * dt[2]);
+}
+
+struct AdamParams {
+  float lr[6];
+  float bc1[6];
+  float bc2[6];
+  int active[6];
+};
+
+__device__ __forceinline__ int comp_group(int c) {
+  return c < 3 ? 0 : (c < 7 ? 1 : (c < 10 ? 2 : (c < 11 ? 3 : (c < 14 ? 4 : 5))));
+}
+
+// AdamGroup::step element update (adam.hpp:70-73), exactly in the reference's order.
+__device__ __forceinline__ void adam_update(float& param, float& m, float& v, float g, float lr, float bc1, float bc2) {
+  const float b1 = (float)0.9, b2 = (float)0.999;
+  m = __fadd_rn(__fmul_rn(b1, m), __fmul_rn(__fsub_rn(1.0f, b1), g));
+  v = __fadd_rn(__fmul_rn(b2, v), __fmul_rn(__fmul_rn(__fsub_rn(1.0f, b2), g), g));
+  const float num = __fmul_rn(lr, __fdiv_rn(m, bc1));
+  const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(v, bc2)), (float)1e-15);
+  param = __fsub_rn(param, __fdiv_rn(num, den));
+}
+
+__device__ __forceinline__ void load_blend(const float* __restrict__ bg, int64_t gstride, int64_t i, float dmu2d[2],
+                                           float dcov[2][2], const float4 conic4, float dcol[3], float& dop,
+                                           float absg[2]) {
+  dmu2d[0] = bg[0 * gstride + i];
+  dmu2d[1] = bg[1 * gstride + i];
+  const float dc00 = bg[2 * gstride + i], dc01 = bg[3 * gstride + i], dc11 = bg[4 * gstride + i];
+  dcol[0] = bg[5 * gstride + i];
+  dcol[1] = bg[6 * gstride + i];
+  dcol[2] = bg[7 * gstride + i];
+  dop = bg[8 * gstride + i];
+  absg[0] = bg[9 * gstride + i];
+  absg[1] = bg[10 * gstride + i];
+  // cov_grad_from_inv_grad: -(inv dinv) inv, dinv = [[dc00, dc01], [dc01, dc11]]
+  const float inv[2][2] = {{conic4.x, conic4.y}, {conic4.z, conic4.w}};
+  const float dinv[2][2] = {{dc00, dc01}, {dc01, dc11}};
+  float A[2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) A[a][b] = inv[a][0] * dinv[0][b] + inv[a][1] * dinv[1][b];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) dcov[a][b] = -(A[a][0] * inv[0][b] + A[a][1] * inv[1][b]);
+}
+
+__device__ __forceinline__ void accumulate_stats(const Stats& st, int64_t i, int64_t stride, const float dmu2d[2],
+                                                 const float absg[2], const float gmu[3], float radius, float ndc_x,
+                                                 float ndc_y) {
+  const float gx = dmu2d[0] * ndc_x, gy = dmu2d[1] * ndc_y;
+  st.grad_norm_acc[i] += sqrtf(gx * gx + gy * gy);
+  st.abs_grad_acc[i] += absg[0] * ndc_x + absg[1] * ndc_y;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) st.grad3d_acc[k * stride + i] += gmu[k];
+  st.views_seen[i] += 1;
+  st.max_radius2d[i] = fmaxf(st.max_radius2d[i], radius);
+}
+
+// MODE 0: gradients -> grads buffer (+ stats). MODE 1: fused Adam (+ stats).
+template <int DEG, int MODE>
+__global__ void __launch_bounds__(128) project_bwd_kernel(float* __restrict__ params, int64_t stride, int64_t n,
+                                                          CamParams cam, const float* __restrict__ radius,
+                                                          const float4* __restrict__ conic4,
+                                                          const float* __restrict__ bg, int64_t gstride,
+                                                          float* __restrict__ grads, float* __restrict__ am,
+                                                          float* __restrict__ av, AdamParams ap, Stats st,
+                                                          bool do_stats) {
+  constexpr int NC = 11 + 3 * (DEG + 1) * (DEG + 1);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float grad[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) grad[c] = 0.0f;
+  const float rad = radius[i];
+  if (rad > 0.0f) {
+    float dmu2d[2], dcov[2][2], dcol[3], dop, absg[2];
+    load_blend(bg, gstride, i, dmu2d, dcov, conic4[i], dcol, dop, absg);
+    project_backward_one<DEG>(params, stride, i, cam, dmu2d, dcov, dcol, dop, grad);
+    if (do_stats) {
+      const float gmu[3] = {grad[0], grad[1], grad[2]};
+      accumulate_stats(st, i, stride, dmu2d, absg, gmu, rad, (float)cam.width / 2.0f, (float)cam.height / 2.0f);
+    }
+  }
+  if (MODE == 0) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) grads[c * stride + i] = grad[c];
+  } else {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int gidx = comp_group(c);
+      if (!ap.active[gidx]) continue;
+      float pv = params[c * stride + i], mv = am[c * stride + i], vv = av[c * stride + i];
+      adam_update(pv, mv, vv, grad[c], ap.lr[gidx], ap.bc1[gidx], ap.bc2[gidx]);
+      params[c * stride + i] = pv;
+      am[c * stride + i] = mv;
+      av[c * stride + i] = vv;
+    }
+  }
+}
+
+// Dense Adam over the grads buffer (SceneOptimizer::step).
+__global__ void adam_kernel(float* __restrict__ params, const float* __restrict__ grads, float* __restrict__ am,
+                            float* __restrict__ av, int64_t stride, int64_t n, int comps, AdamParams ap) {
+  const int64_t total = (int64_t)comps * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n);
+    const int64_t i = e - (int64_t)c * n;
+    const int gidx = comp_group(c);
+    if (!ap.active[gidx]) continue;
+    const int64_t o = (int64_t)c * stride + i;
+    float pv = params[o], mv = am[o], vv = av[o];
+    adam_update(pv, mv, vv, grads[o], ap.lr[gidx], ap.bc1[gidx], ap.bc2[gidx]);
+    params[o] = pv;
+    am[o] = mv;
+    av[o] = vv;
+  }
+}
+
+AdamParams make_adam(sk_scene* s, const LearningRates& lrs, float position_lr, bool update_sh_rest) {
+  AdamParams ap;
+  const float lr[6] = {position_lr, lrs.rotation, lrs.scale, lrs.opacity, lrs.sh_dc, lrs.sh_rest};
+  for (int g = 0; g < 6; ++g) {
+    const bool active = g < 5 || (update_sh_rest && s->sh_degree > 0);
+    ap.active[g] = active ? 1 : 0;
+    ap.lr[g] = lr[g];
+    if (active) s->adam_t[g] += 1;
+    const float t = (float)s->adam_t[g];
+    // adam.hpp:64-66: T(1) - std::pow(T(beta), T(t)) in float
+    ap.bc1[g] = 1.0f - std::pow((float)0.9, t);
+    ap.bc2[g] = 1.0f - std::pow((float)0.999, t);
+  }
+  return ap;
+}
+
+Stats make_stats(sk_scene* s) {
+  Stats st;
+  st.grad_norm_acc = s->grad_norm_acc.as<float>();
+  st.abs_grad_acc = s->abs_grad_acc.as<float>();
+  st.grad3d_acc = s->grad3d_acc.as<float>();
+  st.views_seen = s->views_seen.as<int>();
+  st.max_radius2d = s->max_radius2d.as<float>();
+  return st;
+}
+
+template <int MODE>
+void launch_pb(sk_ctx* ctx, sk_scene* s, sk_frame* f, const AdamParams& ap, bool do_stats) {
+  const CamParams cp = make_cam_params(f->camera);
+  const unsigned grid = (unsigned)((s->n + 127) / 128);
+  auto go = [&](auto kern) {
+    kern<<<grid, 128, 0, ctx->stream>>>(s->params.as<float>(), s->capacity, s->n, cp, f->radius.as<float>(),
+                                        f->conic4.as<float4>(), f->bgrads.as<float>(), f->n, s->grads.as<float>(),
+                                        s->adam_m.as<float>(), s->adam_v.as<float>(), ap, make_stats(s), do_stats);
+  };
+  switch (s->sh_degree) {
+    case 0: go(project_bwd_kernel<0, MODE>); break;
+    case 1: go(project_bwd_kernel<1, MODE>); break;
+    case 2: go(project_bwd_kernel<2, MODE>); break;
+    default: go(project_bwd_kernel<3, MODE>); break;
+  }
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+void ensure_optimizer_state(sk_ctx* ctx, sk_scene* s) {
+  const size_t cells = (size_t)s->comps * s->capacity;
+  if (!s->adam_m.ptr || s->adam_m.bytes < cells * sizeof(float)) {
+    ensure<float>(s->adam_m, cells);
+    ensure<float>(s->adam_v, cells);
+    SK_CUDA(cudaMemsetAsync(s->adam_m.ptr, 0, cells * sizeof(float), ctx->stream));
+    SK_CUDA(cudaMemsetAsync(s->adam_v.ptr, 0, cells * sizeof(float), ctx->stream));
+  }
+  ensure<float>(s->grads, cells);
+  ensure_score_table(ctx, s);
+}
+
+void ensure_score_table(sk_ctx* ctx, sk_scene* s) {
+  const size_t cap = (size_t)s->capacity;
+  if (s->grad_norm_acc.ptr && s->grad_norm_acc.bytes >= cap * sizeof(float)) return;
+  ensure<float>(s->s_d, cap);
+  ensure<float>(s->s_p_raw, cap);
+  ensure<float>(s->s_p, cap);
+  ensure<float>(s->grad_norm_acc, cap);
+  ensure<float>(s->abs_grad_acc, cap);
+  ensure<float>(s->grad3d_acc, 3 * cap);
+  ensure<int>(s->views_seen, cap);
+  ensure<float>(s->max_radius2d, cap);
+  reset_score_table(ctx, s);
+}
+
+void reset_score_table(sk_ctx* ctx, sk_scene* s) {
+  const size_t cap = (size_t)s->capacity;
+  cudaStream_t st = ctx->stream;
+  SK_CUDA(cudaMemsetAsync(s->s_d.ptr, 0, cap * 4, st));
+  SK_CUDA(cudaMemsetAsync(s->s_p_raw.ptr, 0, cap * 4, st));
+  SK_CUDA(cudaMemsetAsync(s->s_p.ptr, 0, cap * 4, st));
+  SK_CUDA(cudaMemsetAsync(s->grad_norm_acc.ptr, 0, cap * 4, st));
+  SK_CUDA(cudaMemsetAsync(s->abs_grad_acc.ptr, 0, cap * 4, st));
+  SK_CUDA(cudaMemsetAsync(s->grad3d_acc.ptr, 0, 3 * cap * 4, st));
+  SK_CUDA(cudaMemsetAsync(s->views_seen.ptr, 0, cap * 4, st));
+  SK_CUDA(cudaMemsetAsync(s->max_radius2d.ptr, 0, cap * 4, st));
+}
+
+void launch_project_backward(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stats) {
+  ensure_optimizer_state(ctx, s);
+  AdamParams ap{};
+  launch_pb<0>(ctx, s, f, ap, do_stats);
+}
+
+void launch_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const LearningRates& lrs, float position_lr,
+                                  bool update_sh_rest, bool do_stats) {
+  ensure_optimizer_state(ctx, s);
+  const AdamParams ap = make_adam(s, lrs, position_lr, update_sh_rest);
+  launch_pb<1>(ctx, s, f, ap, do_stats);
+}
+
+void launch_adam(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float position_lr, bool update_sh_rest) {
+  ensure_optimizer_state(ctx, s);
+  const AdamParams ap = make_adam(s, lrs, position_lr, update_sh_rest);
+  const int64_t total = (int64_t)s->comps * s->n;
+  if (total == 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  adam_kernel<<<grid, 256, 0, ctx->stream>>>(s->params.as<float>(), s->grads.as<float>(), s->adam_m.as<float>(),
+                                             s->adam_v.as<float>(), s->capacity, s->n, s->comps, ap);
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+}
+
+}  // namespace sk

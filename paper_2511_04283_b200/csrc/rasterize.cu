@@ -1,0 +1,300 @@
+// K6 forward alpha blend (+ K12 footprint count) and K8 backward blend.
+//
+// K6 restates blend_forward (reference raster.hpp:194-248): integer pixel
+// centres, q = ((c00 dx) dx + ((2 c01) dx) dy) + (c11 dy) dy, skip q < 0,
+// alpha = min(0.99, o e^{-q/2}), skip alpha < 1/255, C += (T alpha) c,
+// T *= 1 - alpha, and the entry that takes T below 1e-4 is blended before the
+// pixel stops. One CTA per tile, one thread per pixel; the tile's list is
+// staged through shared memory in CTA-sized batches and the CTA stops loading
+// once every pixel has terminated. Compiled with -fmad=false and the shared
+// deterministic exp, so images, transmittance and footprint counts match the
+// CPU oracle bit for bit.
+//
+// K8 restates blend_backward (raster.hpp:281-355) as a reverse walk from each
+// pixel's last contributor (recorded by K6): T_before = T_after / (1 - alpha),
+// suffix accumulated in the reference's reverse order, capped entries feed
+// d_color only. Per-Gaussian partials are butterfly-reduced across the warp
+// with shuffles, then one lane per gradient field issues a global atomic.
+#include "state.h"
+
+namespace sk {
+namespace {
+
+template <int TS, bool COUNT>
+__global__ void __launch_bounds__(TS* TS) blend_fwd_kernel(
+    const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
+    const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
+    float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry,
+    const uint8_t* __restrict__ mask, int* __restrict__ counts) {
+  constexpr int B = TS * TS;
+  __shared__ float2 s_xy[B];
+  __shared__ float4 s_co[B];
+  __shared__ float4 s_rgb[B];
+  __shared__ uint32_t s_id[COUNT ? B : 1];
+
+  const int tile = blockIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int px = tx * TS + (int)(threadIdx.x % TS);
+  const int py = ty * TS + (int)(threadIdx.x / TS);
+  const bool inside = px < W && py < H;
+  const int2 range = ranges[tile];
+  const float fpx = (float)px, fpy = (float)py;
+
+  float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
+  int n = 0, last = 0;
+  bool masked = false;
+  if (COUNT && inside) masked = mask[(size_t)py * W + px] != 0;
+  // K12 (count-only pass): only masked pixels can increment a counter, so
+  // unmasked pixels never traverse and fully unmasked tiles exit at once.
+  bool done = COUNT ? !masked : !inside;
+
+  for (int b0 = range.x; b0 < range.y; b0 += B) {
+    if (__syncthreads_count(done) == B) break;
+    const int i = b0 + (int)threadIdx.x;
+    if (i < range.y) {
+      const uint32_t g = pair_val[i];
+      s_xy[threadIdx.x] = mean2d[g];
+      s_co[threadIdx.x] = conic_op[g];
+      s_rgb[threadIdx.x] = rgbd[g];
+      if (COUNT) s_id[threadIdx.x] = g;
+    }
+    __syncthreads();
+    const int cnt = min(B, range.y - b0);
+    if (!done) {
+      for (int j = 0; j < cnt; ++j) {
+        const float2 mu = s_xy[j];
+        const float4 co = s_co[j];
+        const float dx = fpx - mu.x;
+        const float dy = fpy - mu.y;
+        const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
+        if (q < 0.0f) continue;
+        float alpha = co.w * det_expf(-0.5f * q);
+        alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
+        if (alpha < kAlphaMin) continue;
+        const float4 c = s_rgb[j];
+        const float w = T * alpha;
+        C0 = C0 + w * c.x;
+        C1 = C1 + w * c.y;
+        C2 = C2 + w * c.z;
+        ++n;
+        last = b0 + j + 1;
+        if (COUNT) {
+          // warp-aggregated increment: one atomic per distinct Gaussian
+          const uint32_t id = s_id[j];
+          const uint32_t act = __activemask();
+          const uint32_t peers = __match_any_sync(act, id);
+          if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&counts[id], __popc(peers));
+        }
+        T = T * (1.0f - alpha);
+        if (T < kTransmitMin) {
+          done = true;
+          break;
+        }
+      }
+    }
+  }
+  if (!COUNT && inside) {
+    const size_t p = (size_t)py * W + px;
+    const size_t plane = (size_t)W * H;
+    image[p] = C0;
+    image[plane + p] = C1;
+    image[2 * plane + p] = C2;
+    final_t[p] = T;
+    n_contrib[p] = n;
+    last_entry[p] = last;
+  }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int TS>
+__global__ void __launch_bounds__(TS* TS) blend_bwd_kernel(
+    const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
+    const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
+    const float* __restrict__ final_t, const int* __restrict__ last_entry, const float* __restrict__ dimage,
+    float* __restrict__ bgrads, int64_t gstride) {
+  constexpr int B = TS * TS;
+  __shared__ float2 s_xy[B];
+  __shared__ float4 s_co[B];
+  __shared__ float4 s_rgb[B];
+  __shared__ uint32_t s_id[B];
+  __shared__ int s_max_last;
+
+  const int tile = blockIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int px = tx * TS + (int)(threadIdx.x % TS);
+  const int py = ty * TS + (int)(threadIdx.x / TS);
+  const bool inside = px < W && py < H;
+  const int2 range = ranges[tile];
+  const int lane = threadIdx.x & 31;
+  const float fpx = (float)px, fpy = (float)py;
+
+  float T = 1.0f, d0 = 0.0f, d1 = 0.0f, d2 = 0.0f;
+  int last = 0;
+  if (inside) {
+    const size_t p = (size_t)py * W + px;
+    const size_t plane = (size_t)W * H;
+    T = final_t[p];
+    last = last_entry[p];
+    d0 = dimage[p];
+    d1 = dimage[plane + p];
+    d2 = dimage[2 * plane + p];
+  }
+  if (threadIdx.x == 0) s_max_last = 0;
+  __syncthreads();
+  atomicMax(&s_max_last, last);
+  __syncthreads();
+  const int end = s_max_last;  // no pixel of the tile uses entries >= end
+  const int warp_last = __reduce_max_sync(0xffffffffu, last);
+  float suffix = 0.0f;
+
+  for (int b_end = end; b_end > range.x; b_end -= B) {
+    const int b0 = max(range.x, b_end - B);
+    __syncthreads();
+    const int i = b0 + (int)threadIdx.x;
+    if (i < b_end) {
+      const uint32_t g = pair_val[i];
+      s_xy[threadIdx.x] = mean2d[g];
+      s_co[threadIdx.x] = conic_op[g];
+      s_rgb[threadIdx.x] = rgbd[g];
+      s_id[threadIdx.x] = g;
+    }
+    __syncthreads();
+    const int jmax = min(b_end, warp_last) - b0;  // warp-uniform
+    for (int j = jmax - 1; j >= 0; --j) {
+      const int idx = b0 + j;
+      float g_mu0 = 0.f, g_mu1 = 0.f, g_c00 = 0.f, g_c01 = 0.f, g_c11 = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f,
+            g_op = 0.f, g_a0 = 0.f, g_a1 = 0.f;
+      bool contrib = false;
+      if (idx < last) {
+        const float2 mu = s_xy[j];
+        const float4 co = s_co[j];
+        const float dx = fpx - mu.x;
+        const float dy = fpy - mu.y;
+        const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
+        if (q >= 0.0f) {
+          const float ge = det_expf(-0.5f * q);
+          const float raw = co.w * ge;
+          const bool capped = raw > kAlphaCap;
+          const float alpha = capped ? kAlphaCap : raw;
+          if (alpha >= kAlphaMin) {
+            contrib = true;
+            const float4 c = s_rgb[j];
+            const float one_m = 1.0f - alpha;
+            const float t_before = T / one_m;
+            T = t_before;
+            const float w = (c.x * d0 + c.y * d1) + c.z * d2;
+            const float d_alpha = t_before * w - suffix / one_m;
+            const float ta = t_before * alpha;
+            suffix = suffix + ta * w;
+            g_r = ta * d0;
+            g_g = ta * d1;
+            g_b = ta * d2;
+            if (!capped) {
+              g_op = ge * d_alpha;
+              const float d_q = -0.5f * alpha * d_alpha;
+              g_c00 = d_q * (dx * dx);
+              g_c01 = d_q * (dx * dy);
+              g_c11 = d_q * (dy * dy);
+              const float v0 = co.x * dx + co.y * dy;
+              const float v1 = co.y * dx + co.z * dy;
+              g_mu0 = (-2.0f * d_q) * v0;
+              g_mu1 = (-2.0f * d_q) * v1;
+              g_a0 = fabsf(g_mu0);
+              g_a1 = fabsf(g_mu1);
+            }
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, contrib)) {
+        g_mu0 = warp_sum(g_mu0);
+        g_mu1 = warp_sum(g_mu1);
+        g_c00 = warp_sum(g_c00);
+        g_c01 = warp_sum(g_c01);
+        g_c11 = warp_sum(g_c11);
+        g_r = warp_sum(g_r);
+        g_g = warp_sum(g_g);
+        g_b = warp_sum(g_b);
+        g_op = warp_sum(g_op);
+        g_a0 = warp_sum(g_a0);
+        g_a1 = warp_sum(g_a1);
+        if (lane < kBGradFields) {
+          float v = g_mu0;
+          switch (lane) {
+            case 0: v = g_mu0; break;
+            case 1: v = g_mu1; break;
+            case 2: v = g_c00; break;
+            case 3: v = g_c01; break;
+            case 4: v = g_c11; break;
+            case 5: v = g_r; break;
+            case 6: v = g_g; break;
+            case 7: v = g_b; break;
+            case 8: v = g_op; break;
+            case 9: v = g_a0; break;
+            default: v = g_a1; break;
+          }
+          atomicAdd(&bgrads[(int64_t)lane * gstride + s_id[j]], v);
+        }
+      }
+    }
+  }
+}
+
+template <int TS>
+void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts) {
+  const int tiles = f->tiles_x * f->tiles_y;
+  auto* ranges = f->ranges.as<int2>();
+  const auto* mean2d = f->mean2d.as<float2>();
+  const auto* co = f->conic_op.as<float4>();
+  const auto* rgb = f->rgb_depth.as<float4>();
+  if (mask)
+    blend_fwd_kernel<TS, true><<<tiles, TS * TS, 0, ctx->stream>>>(
+        ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
+        f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), mask, counts);
+  else
+    blend_fwd_kernel<TS, false><<<tiles, TS * TS, 0, ctx->stream>>>(
+        ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
+        f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), nullptr, nullptr);
+  note_launch();
+}
+
+template <int TS>
+void bwd_dispatch(sk_ctx* ctx, sk_frame* f) {
+  const int tiles = f->tiles_x * f->tiles_y;
+  blend_bwd_kernel<TS><<<tiles, TS * TS, 0, ctx->stream>>>(
+      f->ranges.as<int2>(), f->pair_val, f->mean2d.as<float2>(), f->conic_op.as<float4>(), f->rgb_depth.as<float4>(),
+      f->width, f->height, f->tiles_x, f->final_t.as<float>(), f->last_entry.as<int>(), f->dimage.as<float>(),
+      f->bgrads.as<float>(), f->n);
+  note_launch();
+}
+
+}  // namespace
+
+void launch_blend_forward(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts) {
+  if (f->tiles_x * f->tiles_y == 0) return;
+  switch (f->tile_size) {
+    case 8: fwd_dispatch<8>(ctx, f, mask, counts); break;
+    case 16: fwd_dispatch<16>(ctx, f, mask, counts); break;
+    case 32: fwd_dispatch<32>(ctx, f, mask, counts); break;
+    default: throw std::invalid_argument("tile_size must be 8, 16 or 32");
+  }
+  SK_CUDA(cudaGetLastError());
+}
+
+void launch_blend_backward(sk_ctx* ctx, sk_frame* f) {
+  SK_CUDA(cudaMemsetAsync(f->bgrads.ptr, 0, sizeof(float) * kBGradFields * (size_t)f->n, ctx->stream));
+  if (f->tiles_x * f->tiles_y == 0) return;
+  switch (f->tile_size) {
+    case 8: bwd_dispatch<8>(ctx, f); break;
+    case 16: bwd_dispatch<16>(ctx, f); break;
+    case 32: bwd_dispatch<32>(ctx, f); break;
+    default: throw std::invalid_argument("tile_size must be 8, 16 or 32");
+  }
+  SK_CUDA(cudaGetLastError());
+}
+
+}  // namespace sk

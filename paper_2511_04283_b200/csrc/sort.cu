@@ -1,0 +1,361 @@
+// K2 scan, K4 onesweep radix sort, K5 tile ranges.
+//
+// Replaces depth_order's std::sort (reference raster.hpp:146-154) and the
+// per-tile push_back lists of build_tile_grid (:157-168). The pipeline is:
+//   depth sort : stable LSD sort of (depth key, index) over all slots;
+//   K2 scan    : exclusive scan of tiles_touched in depth order;
+//   K3         : pairs (tile, index) emitted in (depth, index) order;
+//   K4         : stable LSD sort of the pairs on the tile id only;
+//   K5         : per-tile [begin, end) ranges.
+// Stability of both sorts reproduces the reference's per-tile order
+// (depth ascending, ties by projected index) exactly.
+//
+// The sort is a onesweep LSD radix sort (8-bit digits): one upsweep kernel
+// builds all digit histograms in a single read of the keys; each digit pass
+// is a single kernel that ranks a 3840-key tile in shared memory (per-warp
+// match_any ranking keeps it stable), publishes per-digit counts with a
+// decoupled look-back across tiles, and writes keys/values in digit-sorted
+// runs so global stores are coalesced.
+#include "state.h"
+
+namespace sk {
+namespace {
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kItems = 15;
+constexpr int kTile = kSortThreads * kItems;  // 3840
+constexpr int kMaxPasses = 4;
+
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagInc = 2u << 30;
+constexpr uint32_t kValMask = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Upsweep: digit histograms of every pass in one read of the keys.
+__global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int passes,
+                                                         uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[kMaxPasses][kRadix];
+  for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t k = keys[i];
+    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (p * kRadixBits)) & (kRadix - 1)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
+    const uint32_t v = (&sh[0][0])[i];
+    if (v) atomicAdd(&hist[i], v);
+  }
+}
+
+// Exclusive scan of each pass's 256 digit counts (one block per pass).
+__global__ void radix_bases_kernel(uint32_t* __restrict__ hist) {
+  __shared__ uint32_t warp_sums[kRadix / 32];
+  uint32_t* h = hist + blockIdx.x * kRadix;
+  const int t = threadIdx.x;
+  const uint32_t v = h[t];
+  uint32_t x = v;
+  const int lane = t & 31, w = t >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[w] = x;
+  __syncthreads();
+  uint32_t base = 0;
+  for (int i = 0; i < w; ++i) base += warp_sums[i];
+  h[t] = base + x - v;
+}
+
+// One onesweep digit pass.
+__global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
+    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, int64_t n, int shift, const uint32_t* __restrict__ digit_base,
+    uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_hist[kSortWarps][kRadix];
+  __shared__ uint32_t s_keys[kTile];
+  __shared__ uint32_t s_vals[kTile];
+  __shared__ uint32_t s_local[kRadix];
+  __shared__ uint32_t s_global[kRadix];
+  __shared__ uint32_t s_wsum[kSortWarps];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < kSortWarps * kRadix; i += kSortThreads) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * kTile;
+
+  uint32_t k[kItems], v[kItems], d[kItems], rank[kItems];
+  const int64_t wbase = base + (int64_t)warp * (32 * kItems);
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int64_t idx = wbase + j * 32 + lane;
+    const bool valid = idx < n;
+    k[j] = valid ? keys_in[idx] : 0u;
+    v[j] = valid ? vals_in[idx] : 0u;
+    d[j] = valid ? ((k[j] >> shift) & (kRadix - 1)) : (uint32_t)kRadix;
+  }
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, d[j]);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (lane == leader && d[j] < (uint32_t)kRadix) {
+      old = s_hist[warp][d[j]];
+      s_hist[warp][d[j]] = old + __popc(peers);
+    }
+    old = __shfl_sync(0xffffffffu, old, leader);
+    rank[j] = old + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // Per digit (thread == digit): warp-exclusive offsets and the tile total.
+  const int digit = tid;
+  uint32_t total = 0;
+#pragma unroll
+  for (int w = 0; w < kSortWarps; ++w) {
+    const uint32_t c = s_hist[w][digit];
+    s_hist[w][digit] = total;
+    total += c;
+  }
+  uint32_t* my_status = status + (size_t)tile * kRadix + digit;
+  st_relaxed(my_status, (tile == 0 ? kFlagInc : kFlagAgg) | total);
+
+  // Block-local exclusive scan of the digit totals.
+  {
+    uint32_t x = total;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    uint32_t wb = 0;
+    for (int i = 0; i < warp; ++i) wb += s_wsum[i];
+    s_local[digit] = wb + x - total;
+  }
+
+  // Decoupled look-back over preceding tiles for this digit.
+  uint32_t excl = 0;
+  if (tile > 0) {
+    int64_t j = (int64_t)tile - 1;
+    while (j >= 0) {
+      const uint32_t s = ld_relaxed(status + (size_t)j * kRadix + digit);
+      const uint32_t flag = s & ~kValMask;
+      if (flag == 0) continue;
+      excl += s & kValMask;
+      if (flag == kFlagInc) break;
+      --j;
+    }
+    st_relaxed(my_status, kFlagInc | (excl + total));
+  }
+  s_global[digit] = digit_base[digit] + excl;
+  __syncthreads();
+
+  // Scatter into shared memory in digit-sorted order.
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    if (d[j] < (uint32_t)kRadix) {
+      const uint32_t pos = s_local[d[j]] + s_hist[warp][d[j]] + rank[j];
+      s_keys[pos] = k[j];
+      s_vals[pos] = v[j];
+    }
+  }
+  __syncthreads();
+  const int64_t rem = n - base;
+  const int count = rem < kTile ? (int)rem : kTile;
+  for (int i = tid; i < count; i += kSortThreads) {
+    const uint32_t key = s_keys[i];
+    const uint32_t dg = (key >> shift) & (kRadix - 1);
+    const uint32_t out = s_global[dg] + (uint32_t)i - s_local[dg];
+    keys_out[out] = key;
+    vals_out[out] = s_vals[i];
+  }
+}
+
+// ---- K2: single-pass exclusive scan with decoupled look-back ---------------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr unsigned long long kSFlagAgg = 1ull << 62;
+constexpr unsigned long long kSFlagInc = 2ull << 62;
+constexpr unsigned long long kSValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kScanThreads) scan_gather_kernel(const int32_t* __restrict__ values,
+                                                                   const uint32_t* __restrict__ order,
+                                                                   int32_t* __restrict__ out, int64_t n,
+                                                                   unsigned long long* __restrict__ status,
+                                                                   uint32_t* __restrict__ counter,
+                                                                   long long* __restrict__ total_out) {
+  __shared__ uint32_t s_tile;
+  __shared__ long long s_warp[kScanThreads / 32];
+  __shared__ long long s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(counter, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * kScanTile + (int64_t)tid * kScanItems;
+  long long v[kScanItems];
+  long long sum = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t i = base + j;
+    v[j] = (i < n) ? (long long)values[order ? order[i] : i] : 0;
+    sum += v[j];
+  }
+  // block scan of per-thread sums
+  long long x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  long long wb = 0, block_total = 0;
+  for (int i = 0; i < kScanThreads / 32; ++i) {
+    if (i < warp) wb += s_warp[i];
+    block_total += s_warp[i];
+  }
+  long long thread_excl = wb + x - sum;
+  if (tid == 0) {
+    unsigned long long* my = status + tile;
+    if (tile == 0) {
+      st_relaxed64(my, kSFlagInc | (unsigned long long)block_total);
+      s_prefix = 0;
+    } else {
+      st_relaxed64(my, kSFlagAgg | (unsigned long long)block_total);
+      long long excl = 0;
+      int64_t j = (int64_t)tile - 1;
+      while (j >= 0) {
+        const unsigned long long s = ld_relaxed64(status + j);
+        const unsigned long long flag = s & ~kSValMask;
+        if (flag == 0) continue;
+        excl += (long long)(s & kSValMask);
+        if (flag == kSFlagInc) break;
+        --j;
+      }
+      st_relaxed64(my, kSFlagInc | (unsigned long long)(excl + block_total));
+      s_prefix = excl;
+    }
+  }
+  __syncthreads();
+  long long run = s_prefix + thread_excl;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t i = base + j;
+    if (i < n) out[i] = (int32_t)run;
+    run += v[j];
+  }
+  if (total_out && base <= n - 1 && base + kScanItems >= n) *total_out = run;
+}
+
+__global__ void iota_kernel(uint32_t* out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint32_t)i;
+}
+
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ tile, int64_t pairs, int2* __restrict__ ranges) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= pairs) return;
+  const uint32_t t = tile[i];
+  if (i == 0 || tile[i - 1] != t) ranges[t].x = (int)i;
+  if (i == pairs - 1 || tile[i + 1] != t) ranges[t].y = (int)(i + 1);
+}
+
+}  // namespace
+
+void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_t*& vals, uint32_t*& vals_alt,
+                      int64_t n, int bits) {
+  if (n <= 1 || bits <= 0) return;
+  const int passes = (bits + kRadixBits - 1) / kRadixBits;
+  require(passes <= kMaxPasses, "radix_sort_pairs: at most 32 key bits");
+  const int64_t tiles = (n + kTile - 1) / kTile;
+  require(tiles < (1ll << 31), "radix_sort_pairs: too many keys");
+  uint32_t* hist = ensure<uint32_t>(ctx->sort.hist, (size_t)kMaxPasses * kRadix);
+  uint32_t* status = ensure<uint32_t>(ctx->sort.status, (size_t)tiles * kRadix);
+  uint32_t* counters = ensure<uint32_t>(ctx->sort.counters, kMaxPasses);
+  cudaStream_t s = ctx->stream;
+  SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s));
+  SK_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * kMaxPasses, s));
+  const int hist_blocks = (int)std::min<int64_t>((n + 4095) / 4096, 148 * 8);
+  radix_hist_kernel<<<hist_blocks, 256, 0, s>>>(keys, n, passes, hist);
+  note_launch();
+  radix_bases_kernel<<<passes, kRadix, 0, s>>>(hist);
+  note_launch();
+  for (int p = 0; p < passes; ++p) {
+    SK_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t) * (size_t)tiles * kRadix, s));
+    onesweep_kernel<<<(unsigned)tiles, kSortThreads, 0, s>>>(keys, vals, keys_alt, vals_alt, n, p * kRadixBits,
+                                                              hist + p * kRadix, status, counters + p);
+    note_launch();
+    std::swap(keys, keys_alt);
+    std::swap(vals, vals_alt);
+  }
+  SK_CUDA(cudaGetLastError());
+}
+
+int64_t scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets, int64_t n) {
+  if (n == 0) return 0;
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  auto* status = ensure<unsigned long long>(ctx->sort.scan_status, (size_t)tiles + 1);
+  auto* total = ensure<long long>(ctx->sort.scan_total, 2);
+  uint32_t* counter = reinterpret_cast<uint32_t*>(total + 1);
+  cudaStream_t s = ctx->stream;
+  SK_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)tiles, s));
+  SK_CUDA(cudaMemsetAsync(total, 0, sizeof(long long) * 2, s));
+  scan_gather_kernel<<<(unsigned)tiles, kScanThreads, 0, s>>>(values, order, offsets, n, status, counter, total);
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+  long long host_total = 0;
+  SK_CUDA(cudaMemcpyAsync(&host_total, total, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  SK_CUDA(cudaStreamSynchronize(s));
+  return host_total;
+}
+
+void launch_iota(sk_ctx* ctx, uint32_t* out, int64_t n) {
+  if (n == 0) return;
+  iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(out, n);
+  note_launch();
+}
+
+void launch_tile_ranges(sk_ctx* ctx, const uint32_t* pair_tile, int64_t pairs, int2* ranges, int tiles) {
+  SK_CUDA(cudaMemsetAsync(ranges, 0, sizeof(int2) * tiles, ctx->stream));
+  if (pairs == 0) return;
+  tile_ranges_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, ctx->stream>>>(pair_tile, pairs, ranges);
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+}
+
+}  // namespace sk

@@ -1,0 +1,178 @@
+// Host-side state behind the opaque C ABI handles (sk_ctx, sk_scene, sk_frame)
+// and the launchers each kernel translation unit exports.
+#pragma once
+
+#include "common.cuh"
+
+namespace sk {
+
+// Scratch for the radix sort and the decoupled look-back scans.
+struct SortTemp {
+  DevBuf hist;      // [passes][256] digit counts, then exclusive bases
+  DevBuf status;    // [tiles][256] look-back words
+  DevBuf counters;  // tile tickets, one per pass
+  DevBuf scan_status;
+  DevBuf scan_total;
+};
+
+}  // namespace sk
+
+namespace sk {
+// Scratch for density-control events (K11-K15).
+struct EventScratch {
+  DevBuf rows;       // int32 [k][n] footprint counts per sampled view
+  DevBuf photo;      // float [k]
+  DevBuf raw;        // float [H][W] channel-mean |r - g|
+  DevBuf mask;       // u8 [H][W]
+  DevBuf lohi;       // uint32 [2] min / max bits; uint64 argmin
+  DevBuf flags;      // u8 [3][n] clone / split / prune
+  DevBuf cls;        // int32 [3][n] scan inputs
+  DevBuf pos;        // int32 [3][n] scan outputs
+  DevBuf keys_a, keys_b, vals_a, vals_b;  // VCP ordering
+  DevBuf eps;        // float [n_split][6]
+  DevBuf old_to_new; // int32 [n]
+};
+}  // namespace sk
+
+struct sk_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  sk::SortTemp sort;
+  sk::EventScratch ev;
+  sk::DevBuf err_word;  // uint32 device error bits
+  sk::DevBuf scalars;   // small device scratch (reductions)
+  sk::HostBuf pinned;   // staging
+  // phase timing (sk_ctx_enable_timing)
+  bool timing = false;
+  cudaEvent_t tev[SK_NUM_PHASES + 1] = {};
+  double phase_ms[SK_NUM_PHASES] = {};
+  int64_t timed_steps = 0;
+  void mark(int i) {
+    if (timing) cudaEventRecord(tev[i], stream);
+  }
+};
+
+// Device-resident scene: planar parameters plus the per-Gaussian state the
+// reference keeps beside it (SceneOptimizer moments adam.hpp:100-164,
+// ScoreTable accumulators adc.hpp:23-45).
+struct sk_scene {
+  int sh_degree = 3;
+  int comps = 0;          // SK_COMP_COUNT(sh_degree)
+  int64_t n = 0;          // live Gaussians
+  int64_t capacity = 0;   // component stride
+  sk::DevBuf params;      // [comps][capacity]
+  sk::DevBuf grads;       // [comps][capacity]
+  sk::DevBuf adam_m;      // [comps][capacity]
+  sk::DevBuf adam_v;      // [comps][capacity]
+  int64_t adam_t[6] = {0, 0, 0, 0, 0, 0};  // pos, rot, scale, opacity, sh_dc, sh_rest
+  // ScoreTable (adc.hpp:23-45), device SoA, all [capacity] (grad3d [3][capacity])
+  sk::DevBuf s_d, s_p_raw, s_p, grad_norm_acc, abs_grad_acc, grad3d_acc, views_seen, max_radius2d;
+};
+
+// Per-view render state. Projected arrays are indexed by projected index,
+// which for sk_preprocess is the scene index (culled slots keep radius 0 and
+// zero tiles, so index order == the reference's compacted projected order).
+struct sk_frame {
+  int width = 0, height = 0, tile_size = 16, tiles_x = 0, tiles_y = 0;
+  sk_binning binning{0, 1.0f, (float)(1.0 / 255), 16};
+  sk_camera camera{};
+  int64_t n = 0;        // projected slots
+  int64_t pairs = 0;    // tile/Gaussian pairs after sk_bin_sort
+  bool binned = false;
+  bool rendered = false;
+
+  // K1 outputs
+  sk::DevBuf mean2d;     // float2 [n]
+  sk::DevBuf conic_op;   // float4 [n] (inv00, inv01, inv11, opacity)
+  sk::DevBuf rgb_depth;  // float4 [n] (r, g, b, depth)
+  sk::DevBuf cov2d;      // float4 [n] (c00, c01, c10, c11)
+  sk::DevBuf conic4;     // float4 [n] (inv00, inv01, inv10, inv11)
+  sk::DevBuf radius;     // float [n]; 0 => culled
+  sk::DevBuf tiles;      // int32 [n] tiles touched
+  sk::DevBuf rect;       // int4 [n] clipped tile rectangle
+  sk::DevBuf a_star;     // float [n] compact-box threshold
+  sk::DevBuf depth_key;  // uint32 [n]
+
+  // K2-K5
+  sk::DevBuf keys_a, keys_b, vals_a, vals_b;  // depth sort ping-pong
+  sk::DevBuf offsets;                         // int32 [n]
+  sk::DevBuf ptile_a, ptile_b, pval_a, pval_b; // pair sort ping-pong
+  uint32_t* pair_tile = nullptr;              // sorted result pointers
+  uint32_t* pair_val = nullptr;
+  sk::DevBuf ranges;                          // int2 [tiles]
+
+  // K6 outputs (planar images [3][H][W])
+  sk::DevBuf image;
+  sk::DevBuf final_t;     // float [H][W]
+  sk::DevBuf n_contrib;   // int32 [H][W]
+  sk::DevBuf last_entry;  // int32 [H][W], absolute pair index + 1 of the last contributor
+
+  // K7 / K8
+  sk::DevBuf dimage;  // planar [3][H][W]
+  sk::DevBuf bgrads;  // float [11][n] : d_mu2d(2) d_conic(3: 00, 01, 11) d_color(3) d_opacity abs_grad(2)
+  sk::DevBuf loss_scratch;
+  sk::DevBuf gt;      // staging for GT (u8 or f32)
+  sk::DevBuf mask;    // u8 [H][W]
+  sk::DevBuf counts;  // int32 [n]
+};
+
+namespace sk {
+
+constexpr int kBGradFields = 11;
+
+// ---- launchers (each .cu file owns its kernels) ---------------------------
+// preprocess.cu
+void launch_preprocess(sk_ctx* ctx, const sk_scene* scene, const sk_camera& cam, sk_frame* f);
+void launch_inject_bin(sk_ctx* ctx, sk_frame* f);
+void launch_duplicate(sk_ctx* ctx, sk_frame* f, const uint32_t* order, const int32_t* offsets, uint32_t* pair_tile,
+                      uint32_t* pair_val);
+
+// sort.cu
+// Stable LSD radix sort of (key, value) pairs on key bits [0, bits). On
+// return keys/vals point at the sorted data (pointers may be swapped).
+void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_t*& vals, uint32_t*& vals_alt,
+                      int64_t n, int bits);
+// Exclusive scan of tiles[order[i]] into offsets[i]; returns the total.
+int64_t scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets, int64_t n);
+void launch_iota(sk_ctx* ctx, uint32_t* out, int64_t n);
+void launch_tile_ranges(sk_ctx* ctx, const uint32_t* pair_tile, int64_t pairs, int2* ranges, int tiles);
+
+// rasterize.cu
+void launch_blend_forward(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts);
+void launch_blend_backward(sk_ctx* ctx, sk_frame* f);
+
+// loss.cu
+struct LossSums {
+  double l1, ssim, sq;
+};
+// out == nullptr leaves the sums on the device for read_loss_sums (no sync).
+void launch_loss(sk_ctx* ctx, sk_frame* f, const void* gt, bool gt_u8, float lambda, bool want_grad, LossSums* out);
+void read_loss_sums(sk_ctx* ctx, LossSums* out);
+void finish_loss(int width, int height, float lambda, const LossSums& s, sk_loss_values* out);
+
+// optim.cu
+struct LearningRates {  // LearningRates<T> (adam.hpp:78-86)
+  float position, position_final, sh_dc, sh_rest, opacity, scale, rotation;
+};
+void ensure_optimizer_state(sk_ctx* ctx, sk_scene* s);
+void ensure_score_table(sk_ctx* ctx, sk_scene* s);
+void reset_score_table(sk_ctx* ctx, sk_scene* s);
+void launch_project_backward(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stats);
+void launch_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const LearningRates& lrs, float position_lr,
+                                  bool update_sh_rest, bool do_stats);
+void launch_adam(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float position_lr, bool update_sh_rest);
+
+// pipeline.cu
+void arg(bool ok, const char* msg);  // throws std::invalid_argument
+void frame_geometry(sk_frame* f, int w, int h, const sk_binning* b);
+void ensure_projected(sk_frame* f, int64_t n);
+void ensure_image(sk_frame* f);
+void bin_sort(sk_ctx* ctx, sk_frame* f);
+
+// helpers
+uint32_t read_error_word(sk_ctx* ctx);
+void raise_device_errors(uint32_t bits);
+
+}  // namespace sk

@@ -1,0 +1,445 @@
+// Host orchestration of the training hot path: the optimizer / score-table
+// C ABI, TrainConfig, the host Rng, Dataset, and Trainer (reference
+// trainer.hpp:21-279, adam.hpp:16-164, config.hpp:20-81, rng.hpp:18-69).
+//
+// One iteration = K1 preprocess -> K2-K5 binning -> K6 forward blend ->
+// K7 loss -> K8 backward blend -> fused K9+K10 (project backward + stats +
+// dense Adam). All kernels are stream-ordered on the context stream; the step
+// synchronises twice (the pair count after the scan, and the loss/error
+// readback at the end).
+#include <chrono>
+#include <cmath>
+#include <memory>
+#include <random>
+#include <vector>
+
+#include "abi_util.h"
+#include "trainer.h"
+
+namespace sk {
+
+// expon_lr (adam.hpp:23-26) in float.
+float expon_lr(float lr_init, float lr_final, int step, int max_steps) {
+  float t = (float)step / (float)std::max(1, max_steps);
+  t = (t < 0.0f) ? 0.0f : ((1.0f < t) ? 1.0f : t);
+  return std::exp((1.0f - t) * std::log(lr_init) + t * std::log(lr_final));
+}
+
+LearningRates lrs_from(const sk_train_config& c) {
+  LearningRates l;
+  l.position = (float)c.lr_position;
+  l.position_final = (float)c.lr_position_final;
+  l.sh_dc = (float)c.lr_sh_dc;
+  l.sh_rest = (float)c.lr_sh_rest;
+  l.opacity = (float)c.lr_opacity;
+  l.scale = (float)c.lr_scale;
+  l.rotation = (float)c.lr_rotation;
+  return l;
+}
+
+sk_binning binning_from(const sk_train_config& c) {
+  sk_binning b;
+  b.mode = c.compact ? 1 : 0;
+  b.beta = (float)c.beta;
+  b.tau_alpha = (float)c.tau_alpha;
+  b.tile_size = c.tile_size;
+  return b;
+}
+
+void validate_config(const sk_train_config& c) {
+  require(c.iterations >= 0, "config: iterations must be >= 0");
+  require(c.k >= 1, "config: k must be >= 1");
+  require(c.lambda >= 0 && c.lambda <= 1, "config: lambda must be in [0,1]");
+  require(c.tau > 0 && c.tau < 1, "config: tau must be in (0,1)");
+  require(c.tau_d >= 0, "config: tau_d must be >= 0");
+  require(c.tau_p >= 0 && c.tau_p <= 1, "config: tau_p must be in [0,1]");
+  require(c.beta > 0 && c.beta <= 1, "config: beta must be in (0,1]");
+  require(c.tau_alpha > 0 && c.tau_alpha < 1, "config: tau_alpha must be in (0,1)");
+  require(c.densify_every > 0 && c.prune_every_early > 0 && c.prune_every_late > 0,
+          "config: event cadences must be positive");
+  require((c.densify_until - c.densify_from) % c.densify_every == 0,
+          "config: densify_every must divide densify_until - densify_from");
+  require(c.tile_size > 0, "config: tile_size must be positive");
+  require(c.sh_degree >= 0 && c.sh_degree <= 3, "config: sh_degree must be in 0..3");
+}
+
+bool densify_due(int it, const sk_train_config& c) {
+  return it >= c.densify_from && it <= c.densify_until && it % c.densify_every == 0;
+}
+bool prune_due(int it, const sk_train_config& c) {
+  if (it >= c.densify_from && it <= c.densify_until) return it % c.prune_every_early == 0;
+  if (it > c.densify_until) return (it - c.densify_until) % c.prune_every_late == 0;
+  return false;
+}
+bool lazy_update_due(int it, const sk_train_config& c) {
+  if (!c.lazy_opt_enabled || it < 15000) return true;
+  if (it < 20000) return it % c.lazy_opt_interval_15k == 0;
+  return it % c.lazy_opt_interval_20k == 0;
+}
+
+// One train_iteration (trainer.hpp:124-175) on camera `cam` with the 8-bit GT
+// already on the device.
+void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam, const uint8_t* gt_dev,
+                const sk_train_config& cfg, float extent, int it, sk_log_row* row) {
+  const sk_binning bin = binning_from(cfg);
+  frame_geometry(f, cam.width, cam.height, &bin);
+  f->camera = cam;
+  ensure_projected(f, scene->n);
+  ensure_image(f);
+  ensure<float>(f->bgrads, (size_t)kBGradFields * std::max<int64_t>(f->n, 1));
+  ctx->mark(0);
+  launch_preprocess(ctx, scene, cam, f);
+  ctx->mark(1);
+  bin_sort(ctx, f);
+  ctx->mark(2);
+  launch_blend_forward(ctx, f, nullptr, nullptr);
+  f->rendered = true;
+  ctx->mark(3);
+  launch_loss(ctx, f, gt_dev, true, (float)cfg.lambda, true, nullptr);
+  ctx->mark(4);
+  launch_blend_backward(ctx, f);
+  ctx->mark(5);
+  const LearningRates lrs = lrs_from(cfg);
+  const float pos_lr = expon_lr(lrs.position * extent, lrs.position_final * extent, it, cfg.iterations);
+  require(!cfg.lazy_opt_enabled, "trainer: lazy_opt_enabled is not supported on the GPU path yet");
+  launch_project_backward_adam(ctx, scene, f, lrs, pos_lr, true, true);
+  ctx->mark(6);
+  LossSums sums{};
+  read_loss_sums(ctx, &sums);  // synchronises the stream
+  raise_device_errors(read_error_word(ctx));
+  if (ctx->timing) {
+    for (int i = 0; i < SK_NUM_PHASES; ++i) {
+      float ms = 0.0f;
+      SK_CUDA(cudaEventElapsedTime(&ms, ctx->tev[i], ctx->tev[i + 1]));
+      ctx->phase_ms[i] += ms;
+    }
+    ctx->timed_steps += 1;
+  }
+  if (row) {
+    sk_loss_values v{};
+    finish_loss(f->width, f->height, (float)cfg.lambda, sums, &v);
+    row->iteration = it;
+    row->loss = v.loss;
+    row->psnr = v.psnr;
+    row->tile_pairs = f->pairs;
+    row->gaussians = (int32_t)scene->n;
+  }
+}
+
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+void sk_default_learning_rates(sk_learning_rates* out) {
+  if (!out) return;
+  *out = sk_learning_rates{(float)1.6e-4, (float)1.6e-6, (float)2.5e-3, (float)(2.5e-3 / 20), (float)5e-2, (float)5e-3,
+                           (float)1e-3};
+}
+
+float sk_expon_lr(float a, float b, int step, int max_steps) { return expon_lr(a, b, step, max_steps); }
+
+void sk_default_config(sk_train_config* c) {
+  if (!c) return;
+  *c = sk_train_config{};
+  c->iterations = 30000;
+  c->k = 10;
+  c->lambda = 0.2;
+  c->tau = 0.5;
+  c->tau_d = 5.0;
+  c->tau_p = 0.9;
+  c->beta = 1.0;
+  c->tau_alpha = 1.0 / 255;
+  c->densify_from = 500;
+  c->densify_until = 15000;
+  c->densify_every = 500;
+  c->prune_every_early = 500;
+  c->prune_every_late = 3000;
+  c->grad_threshold = 2e-4;
+  c->percent_dense = 0.01;
+  c->lr_position = 1.6e-4;
+  c->lr_position_final = 1.6e-6;
+  c->lr_sh_dc = 2.5e-3;
+  c->lr_sh_rest = 2.5e-3 / 20;
+  c->lr_opacity = 5e-2;
+  c->lr_scale = 5e-3;
+  c->lr_rotation = 1e-3;
+  c->opacity_reset_every = 0;
+  c->lazy_opt_enabled = 0;
+  c->lazy_opt_interval_15k = 32;
+  c->lazy_opt_interval_20k = 64;
+  c->seed = 0;
+  c->tile_size = 16;
+  c->workers = 1;
+  c->sh_degree = 3;
+  c->compact = 0;
+  c->vcd = 1;
+  c->vcp = 1;
+  c->prune_min_opacity = 0.005;
+  c->prune_opacity_late = 0.1;
+  c->prune_world_size_frac = 0.1;
+  c->prune_screen_size = 20.0;
+  c->size_prune_from = 3000;
+  c->schedule_dry_run = 0;
+}
+
+int sk_validate_config(sk_ctx* ctx, const sk_train_config* cfg) {
+  return guarded(ctx, [&] {
+    arg(cfg != nullptr, "config: null");
+    validate_config(*cfg);
+  });
+}
+
+// ---- optimizer / score table -------------------------------------------------
+int sk_scene_get_score_table(sk_ctx* ctx, sk_scene* s, sk_score_table* out) {
+  return guarded(ctx, [&] {
+    arg(s && out, "sk_scene_get_score_table: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    ensure_score_table(ctx, s);
+    const size_t n = (size_t)s->n, cap = (size_t)s->capacity;
+    if (out->s_d) d2h(ctx, out->s_d, s->s_d.ptr, n);
+    if (out->s_p_raw) d2h(ctx, out->s_p_raw, s->s_p_raw.ptr, n);
+    if (out->s_p) d2h(ctx, out->s_p, s->s_p.ptr, n);
+    if (out->grad_norm_acc) d2h(ctx, out->grad_norm_acc, s->grad_norm_acc.ptr, n);
+    if (out->abs_grad_acc) d2h(ctx, out->abs_grad_acc, s->abs_grad_acc.ptr, n);
+    if (out->views_seen) d2h(ctx, out->views_seen, s->views_seen.ptr, n);
+    if (out->max_radius2d) d2h(ctx, out->max_radius2d, s->max_radius2d.ptr, n);
+    std::vector<float> g3;
+    if (out->grad3d_acc) {
+      g3.resize(3 * cap);
+      d2h(ctx, g3.data(), s->grad3d_acc.ptr, 3 * cap);
+    }
+    sync(ctx);
+    if (out->grad3d_acc)
+      for (size_t i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) out->grad3d_acc[3 * i + k] = g3[k * cap + i];
+  });
+}
+
+int sk_scene_set_score_table(sk_ctx* ctx, sk_scene* s, const sk_score_table* in) {
+  return guarded(ctx, [&] {
+    arg(s && in, "sk_scene_set_score_table: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    ensure_score_table(ctx, s);
+    const size_t n = (size_t)s->n, cap = (size_t)s->capacity;
+    if (in->s_d) h2d(ctx, s->s_d.ptr, in->s_d, n);
+    if (in->s_p_raw) h2d(ctx, s->s_p_raw.ptr, in->s_p_raw, n);
+    if (in->s_p) h2d(ctx, s->s_p.ptr, in->s_p, n);
+    if (in->grad_norm_acc) h2d(ctx, s->grad_norm_acc.ptr, in->grad_norm_acc, n);
+    if (in->abs_grad_acc) h2d(ctx, s->abs_grad_acc.ptr, in->abs_grad_acc, n);
+    if (in->views_seen) h2d(ctx, s->views_seen.ptr, in->views_seen, n);
+    if (in->max_radius2d) h2d(ctx, s->max_radius2d.ptr, in->max_radius2d, n);
+    std::vector<float> g3;
+    if (in->grad3d_acc) {
+      g3.assign(3 * cap, 0.0f);
+      for (size_t i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) g3[k * cap + i] = in->grad3d_acc[3 * i + k];
+      h2d(ctx, s->grad3d_acc.ptr, g3.data(), 3 * cap);
+    }
+    sync(ctx);
+  });
+}
+
+int sk_scene_reset_score_table(sk_ctx* ctx, sk_scene* s) {
+  return guarded(ctx, [&] {
+    arg(s != nullptr, "sk_scene_reset_score_table: null scene");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    ensure_score_table(ctx, s);
+    reset_score_table(ctx, s);
+    sync(ctx);
+  });
+}
+
+int sk_project_backward(sk_ctx* ctx, sk_scene* s, sk_frame* f, int stats, float* grads_host) {
+  return guarded(ctx, [&] {
+    arg(s && f && f->bgrads.ptr, "project_backward: run sk_render_backward first");
+    arg(f->n == s->n, "project_backward: frame was not projected from this scene");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    launch_project_backward(ctx, s, f, stats != 0);
+    if (grads_host && s->n > 0)
+      SK_CUDA(cudaMemcpy2DAsync(grads_host, sizeof(float) * s->n, s->grads.ptr, sizeof(float) * s->capacity,
+                                sizeof(float) * s->n, s->comps, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+  });
+}
+
+int sk_scene_set_grads(sk_ctx* ctx, sk_scene* s, const float* g) {
+  return guarded(ctx, [&] {
+    arg(s && g, "sk_scene_set_grads: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    ensure_optimizer_state(ctx, s);
+    if (s->n > 0)
+      SK_CUDA(cudaMemcpy2DAsync(s->grads.ptr, sizeof(float) * s->capacity, g, sizeof(float) * s->n,
+                                sizeof(float) * s->n, s->comps, cudaMemcpyHostToDevice, ctx->stream));
+    sync(ctx);
+  });
+}
+
+int sk_adam_step(sk_ctx* ctx, sk_scene* s, const sk_learning_rates* l, float position_lr, int update_sh_rest) {
+  return guarded(ctx, [&] {
+    arg(s && l, "sk_adam_step: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    LearningRates lr{l->position, l->position_final, l->sh_dc, l->sh_rest, l->opacity, l->scale, l->rotation};
+    launch_adam(ctx, s, lr, position_lr, update_sh_rest != 0);
+    sync(ctx);
+  });
+}
+
+int sk_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const sk_learning_rates* l, float position_lr,
+                             int update_sh_rest, int stats) {
+  return guarded(ctx, [&] {
+    arg(s && f && l && f->bgrads.ptr, "project_backward: run sk_render_backward first");
+    arg(f->n == s->n, "project_backward: frame was not projected from this scene");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    LearningRates lr{l->position, l->position_final, l->sh_dc, l->sh_rest, l->opacity, l->scale, l->rotation};
+    launch_project_backward_adam(ctx, s, f, lr, position_lr, update_sh_rest != 0, stats != 0);
+    sync(ctx);
+  });
+}
+
+int sk_scene_get_adam(sk_ctx* ctx, const sk_scene* s, float* m, float* v, int64_t* t6) {
+  return guarded(ctx, [&] {
+    arg(s != nullptr, "sk_scene_get_adam: null scene");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    if (t6)
+      for (int g = 0; g < 6; ++g) t6[g] = s->adam_t[g];
+    if ((m || v) && s->n > 0) {
+      arg(s->adam_m.ptr != nullptr, "sk_scene_get_adam: optimizer not initialised");
+      if (m)
+        SK_CUDA(cudaMemcpy2DAsync(m, sizeof(float) * s->n, s->adam_m.ptr, sizeof(float) * s->capacity,
+                                  sizeof(float) * s->n, s->comps, cudaMemcpyDeviceToHost, ctx->stream));
+      if (v)
+        SK_CUDA(cudaMemcpy2DAsync(v, sizeof(float) * s->n, s->adam_v.ptr, sizeof(float) * s->capacity,
+                                  sizeof(float) * s->n, s->comps, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    sync(ctx);
+  });
+}
+
+// ---- datasets / trainer --------------------------------------------------------
+int sk_dataset_create(sk_ctx* ctx, int n_views, const sk_camera* cams, const uint8_t* images,
+                      const int32_t* train_indices, int n_train, float extent, sk_dataset** out) {
+  return guarded(ctx, [&] {
+    arg(out && cams && images && n_views > 0, "dataset: cameras.json contains no cameras");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    auto d = std::make_unique<sk_dataset>();
+    size_t off = 0;
+    for (int v = 0; v < n_views; ++v) {
+      const sk_camera& c = cams[v];
+      arg(c.fx > 0 && c.fy > 0, "camera: focal lengths must be positive");
+      arg(c.width > 0 && c.height > 0, "camera: empty image");
+      d->cams.push_back(c);
+      const size_t bytes = (size_t)c.width * c.height * 3;
+      auto buf = std::make_unique<DevBuf>();
+      buf->ensure(bytes);
+      h2d(ctx, buf->ptr, images + off, bytes);
+      off += bytes;
+      d->images.push_back(std::move(buf));
+    }
+    if (train_indices && n_train > 0) {
+      for (int i = 0; i < n_train; ++i) {
+        arg(train_indices[i] >= 0 && train_indices[i] < n_views, "dataset: train index out of range");
+        d->train.push_back(train_indices[i]);
+      }
+    } else {
+      // dataset.hpp:44-53: every 8th view is a test view
+      for (int i = 0; i < n_views; ++i)
+        if (i % 8 != 0) d->train.push_back(i);
+      if (d->train.empty())
+        for (int i = 0; i < n_views; ++i) d->train.push_back(i);
+    }
+    d->extent = extent;
+    sync(ctx);
+    *out = d.release();
+  });
+}
+
+int sk_dataset_destroy(sk_dataset* d) {
+  delete d;
+  return SK_OK;
+}
+
+int sk_trainer_create(sk_ctx* ctx, sk_scene* scene, const sk_dataset* data, const sk_train_config* cfg,
+                      sk_trainer** out) {
+  return guarded(ctx, [&] {
+    arg(out && scene && data && cfg, "trainer: bad arguments");
+    validate_config(*cfg);
+    require(!data->cams.empty(), "trainer: dataset has no views");
+    require(!data->train.empty(), "trainer: dataset has no training views");
+    arg(scene->sh_degree == cfg->sh_degree, "trainer: scene sh_degree differs from config sh_degree");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    auto t = std::make_unique<sk_trainer>();
+    t->ctx = ctx;
+    t->scene = scene;
+    t->data = data;
+    t->cfg = *cfg;
+    t->rng.seed(cfg->seed);
+    ensure_optimizer_state(ctx, scene);
+    reset_score_table(ctx, scene);
+    sync(ctx);
+    *out = t.release();
+  });
+}
+
+int sk_trainer_destroy(sk_trainer* t) {
+  delete t;
+  return SK_OK;
+}
+
+int sk_trainer_iteration(const sk_trainer* t, int* it) {
+  if (!t || !it) return SK_ERR_INVALID_ARGUMENT;
+  *it = t->it;
+  return SK_OK;
+}
+
+// Trainer::run (trainer.hpp:89-119): step, then the due density event.
+int sk_trainer_run(sk_trainer* t, int iterations, sk_log_row* rows) {
+  if (!t) return SK_ERR_INVALID_ARGUMENT;
+  return guarded(t->ctx, [&] {
+    SK_CUDA(cudaSetDevice(t->ctx->device));
+    if (!t->started) {
+      t->start = std::chrono::steady_clock::now();
+      t->started = true;
+    }
+    const int last = std::min(t->cfg.iterations, t->it + std::max(0, iterations));
+    int r = 0;
+    while (t->it < last) {
+      const int it = ++t->it;
+      sk_log_row row{};
+      row.iteration = it;
+      if (!t->cfg.schedule_dry_run) {
+        const int view = t->data->train[(size_t)t->rng.bounded((uint64_t)t->data->train.size())];
+        row.view = view;
+        train_step(t->ctx, t->scene, &t->frame, t->data->cams[view], t->data->images[view]->as<uint8_t>(), t->cfg,
+                   t->data->extent, it, &row);
+      }
+      const bool dens = densify_due(it, t->cfg);
+      const bool prn = prune_due(it, t->cfg);
+      row.event = (dens ? 1 : 0) | (prn ? 2 : 0);
+      if (!t->cfg.schedule_dry_run && (dens || prn)) density_event(t, it, dens, prn);
+      require(t->cfg.opacity_reset_every <= 0 || t->cfg.schedule_dry_run,
+              "trainer: opacity_reset_every is not supported on the GPU path yet");
+      row.gaussians = (int32_t)t->scene->n;
+      row.elapsed_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t->start).count();
+      if (rows) rows[r] = row;
+      ++r;
+    }
+  });
+}
+
+int sk_train_step_host(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_camera* cam, const uint8_t* gt_host,
+                       const sk_train_config* cfg, float extent, int iteration, sk_log_row* row) {
+  return guarded(ctx, [&] {
+    arg(scene && frame && cam && gt_host && cfg, "sk_train_step_host: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    ensure_optimizer_state(ctx, scene);
+    const size_t bytes = (size_t)cam->width * cam->height * 3;
+    void* gt = frame->gt.ensure(bytes);
+    SK_CUDA(cudaMemcpyAsync(gt, gt_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    train_step(ctx, scene, frame, *cam, static_cast<const uint8_t*>(gt), *cfg, extent, iteration, row);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Trainer / Dataset state shared by trainer.cu (steps) and density.cu (events).
+#pragma once
+
+#include <chrono>
+#include <cmath>
+#include <memory>
+#include <random>
+#include <vector>
+
+#include "state.h"
+
+struct sk_dataset {
+  std::vector<sk_camera> cams;
+  std::vector<std::unique_ptr<sk::DevBuf>> images;  // u8 HWC per view
+  std::vector<int> train;
+  float extent = 1.0f;
+};
+
+// Rng (reference rng.hpp:18-69): mt19937_64 plus hand-rolled distributions.
+struct HostRng {
+  std::mt19937_64 engine;
+  bool has_spare = false;
+  double spare = 0.0;
+  void seed(uint64_t s) {
+    engine.seed(s);
+    has_spare = false;
+  }
+  uint64_t bounded(uint64_t n) { return (uint64_t)(((__uint128_t)engine() * n) >> 64); }
+  double uniform() { return (double)(engine() >> 11) * 0x1.0p-53; }
+  double normal() {
+    if (has_spare) {
+      has_spare = false;
+      return spare;
+    }
+    double u1 = uniform();
+    double u2 = uniform();
+    u1 = std::max(u1, 0x1.0p-53);
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 2.0 * M_PI * u2;
+    spare = r * std::sin(a);
+    has_spare = true;
+    return r * std::cos(a);
+  }
+  std::vector<int> sample_without_replacement(int n, int k) {
+    std::vector<int> idx(n);
+    for (int i = 0; i < n; ++i) idx[i] = i;
+    const int m = std::min(k, n);
+    for (int i = 0; i < m; ++i) {
+      const int j = i + (int)bounded((uint64_t)(n - i));
+      std::swap(idx[i], idx[j]);
+    }
+    idx.resize(m);
+    return idx;
+  }
+};
+
+// Per-event record kept for the parity tests (masks compared per event).
+struct EventRecord {
+  int iteration = 0;
+  int n_before = 0, n_after = 0, n_clone = 0, n_split = 0, n_prune = 0;
+  std::vector<int> sampled;
+  std::vector<float> photometric;
+  std::vector<uint8_t> clone, split, prune;  // pre-event flags [n_before]
+};
+
+struct sk_trainer {
+  sk_ctx* ctx = nullptr;
+  sk_scene* scene = nullptr;
+  const sk_dataset* data = nullptr;
+  sk_train_config cfg{};
+  HostRng rng;
+  sk_frame frame;
+  int it = 0;
+  std::chrono::steady_clock::time_point start;
+  bool started = false;
+  bool record_events = false;
+  std::vector<EventRecord> events;
+};
+
+namespace sk {
+
+float expon_lr(float lr_init, float lr_final, int step, int max_steps);
+LearningRates lrs_from(const sk_train_config& c);
+sk_binning binning_from(const sk_train_config& c);
+void validate_config(const sk_train_config& c);
+bool densify_due(int it, const sk_train_config& c);
+bool prune_due(int it, const sk_train_config& c);
+void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam, const uint8_t* gt_dev,
+                const sk_train_config& cfg, float extent, int it, sk_log_row* row);
+
+// density.cu: Trainer::density_event (trainer.hpp:177-243).
+void density_event(sk_trainer* t, int it, bool densify, bool prune);
+
+}  // namespace sk
