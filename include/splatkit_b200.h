@@ -304,6 +304,24 @@ int sk_trainer_num_events(const sk_trainer* t, int* n);
 int sk_trainer_event(const sk_trainer* t, int e, int32_t* header, uint8_t* clone, uint8_t* split, uint8_t* prune,
                      int32_t* sampled, float* photometric);
 
+/* ---- multi-GPU view sharding over NCCL ------------------------
+ * One process per GPU. Rank 0 creates the id and shares it (e.g. through
+ * torch.distributed); every rank creates its communicator. A trainer with a
+ * communicator of R ranks trains R views per step (one per rank, drawn from
+ * the shared Rng in rank order), sums gradients before Adam (C1), reduces the
+ * ScoreTable statistics at events (C2) and shards the K scored views
+ * round-robin (C3); selection and compaction run identically on all ranks. */
+#define SK_COMM_ID_BYTES 128
+typedef struct sk_comm sk_comm;
+int sk_comm_unique_id(uint8_t* id /* [SK_COMM_ID_BYTES] */);
+int sk_comm_create(sk_ctx* ctx, const uint8_t* id, int nranks, int rank, sk_comm** out);
+int sk_comm_destroy(sk_comm* comm);
+int sk_comm_rank(const sk_comm* comm, int* rank, int* world);
+int sk_trainer_set_comm(sk_trainer* t, sk_comm* comm);
+/* Round-robin ownership of n_items among world ranks (the score-pass
+ * sharding): fills owned[] (may be NULL) and *n_owned. */
+int sk_shard_assign(int n_items, int world, int rank, int32_t* owned, int* n_owned);
+
 /* One train_iteration (trainer.hpp:124-175) on an explicit camera with the
  * GT image in HOST memory (copied in) — the end-to-end entry point. */
 int sk_train_step_host(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_camera* cam, const uint8_t* gt_host,

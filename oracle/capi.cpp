@@ -745,6 +745,43 @@ int or_accumulate_scores_f(const float* params, int64_t n, int deg, int k, const
   });
 }
 
+// Parameter gradients of one view (SceneGrads, trainer.hpp:128-147): render,
+// training_loss, blend_backward, project_backward. grads planar [C][n].
+int or_view_grads_f(const float* params, int64_t n, int deg, const sk_camera* cam, const float* gt_hwc, float lambda,
+                    int workers, float* grads_planar, double* loss) {
+  return guard([&] {
+    const Scene<float> s = scene_from_planar(params, n, deg);
+    const Camera<float> c = to_camera<float>(cam);
+    const auto pgs = project_scene(s, c);
+    const TileGrid grid = build_tile_grid(pgs, c.width, c.height, BinningConfig<float>{}, 16);
+    const auto rendered = blend_forward(grid, pgs, nullptr, nullptr, workers);
+    const auto lr = training_loss(rendered.image, image_from(gt_hwc, c.width, c.height), lambda);
+    const auto bg = blend_backward(grid, pgs, lr.d_image, workers);
+    Scene<float> gs = s;
+    for (auto& g : gs.gaussians) {
+      g.mu = Vec3<float>::zero();
+      g.rot = Vec4<float>::zero();
+      g.log_scale = Vec3<float>::zero();
+      g.opacity_logit = 0.0f;
+      g.sh = ShMatrix<float>(g.sh.rows);
+    }
+    for (size_t p = 0; p < pgs.size(); ++p) {
+      const auto& pg = pgs[p];
+      const Mat2<float> dcov = cov_grad_from_inv_grad(pg.cov2d_inv, bg.d_conic[p]);
+      const auto g = project_backward(s.gaussians[pg.source_index], c, deg, bg.d_mu2d[p], dcov, bg.d_color[p],
+                                      bg.d_opacity[p]);
+      auto& o = gs.gaussians[pg.source_index];
+      o.mu = g.mu;
+      o.rot = g.rot;
+      o.log_scale = g.log_scale;
+      o.opacity_logit = g.opacity_logit;
+      o.sh = g.sh;
+    }
+    scene_to_planar(gs, grads_planar);
+    if (loss) *loss = lr.loss;
+  });
+}
+
 // Trainer::density_event compaction (trainer.hpp:203-233) with explicit split
 // normals: prune -> Adam remap -> densify -> Adam remap. m/v planar [C][n] in,
 // [C][new_n] out (caller sizes them for n + clones + 2 splits).
@@ -1085,6 +1122,18 @@ int or_trainer_scene(const or_trainer* h, float* params) {
   return 0;
 }
 int or_trainer_num_events(const or_trainer* h) { return int(h->t->events().size()); }
+
+// Follow mode: decisions to replay at event `idx` (flags over n pre-event indices).
+int or_trainer_force_event(or_trainer* h, int idx, int n, const uint8_t* clone, const uint8_t* split,
+                           const uint8_t* prune) {
+  auto& f = h->t->forced_;
+  if (int(f.size()) <= idx) f.resize(idx + 1);
+  f[idx].n = n;
+  f[idx].clone.assign(clone, clone + n);
+  f[idx].split.assign(split, split + n);
+  f[idx].prune.assign(prune, prune + n);
+  return 0;
+}
 // Event e: header [iteration, n_before, n_after, n_clone, n_split, n_prune, k]
 int or_trainer_event(const or_trainer* h, int e, int32_t* header, int32_t* clone, int32_t* split, int32_t* prune,
                      int32_t* sampled, float* photometric) {

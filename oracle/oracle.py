@@ -660,3 +660,24 @@ class ViewTrainer(Trainer):
                    ptr(g), C.byref(cfg), C.c_float(extent))
         if not self.h:
             raise ValueError(lib().or_last_error().decode())
+
+
+def view_grads(params, deg, cam, gt_hwc, lam=0.2, workers=1):
+    """Parameter gradients of one view (trainer.hpp:128-147), planar [C][n]."""
+    p = np.ascontiguousarray(params, np.float32)
+    g = np.zeros_like(p)
+    gt = np.ascontiguousarray(gt_hwc, np.float32)
+    loss = C.c_double()
+    check(lib().or_view_grads_f(ptr(p), C.c_int64(p.shape[1]), C.c_int(deg),
+                                C.byref(SkCamera.from_buffer_copy(bytes(cam))), ptr(gt), C.c_float(lam),
+                                C.c_int(workers), ptr(g), C.byref(loss)))
+    return g, loss.value
+
+
+def trainer_force_events(trainer: Trainer, events):
+    """Follow mode: replay another run's per-event decisions (flags over the
+    pre-event indices) so both runs consume the shared Rng identically."""
+    for i, e in enumerate(events):
+        n = int(e["n_before"])
+        args = [np.ascontiguousarray(e[k][:n], np.uint8) for k in ("clone", "split", "prune")]
+        check(lib().or_trainer_force_event(C.c_void_p(trainer.h), C.c_int(i), C.c_int(n), *[ptr(a) for a in args]))

@@ -1909,8 +1909,15 @@ struct EventRecord {
   int iteration = 0;
   std::vector<int> sampled;       // view indices (into cameras)
   std::vector<float> photometric;
-  std::vector<int> clone, split, prune;  // pre-event indices
+  std::vector<int> clone, split, prune;  // pre-event indices (own selection)
   int n_before = 0, n_after = 0;
+  bool forced = false;
+};
+
+// Decisions to replay at one event (flags over the pre-event indices).
+struct ForcedEvent {
+  int n = 0;
+  std::vector<std::uint8_t> clone, split, prune;
 };
 
 template <typename T>
@@ -2059,6 +2066,24 @@ class Trainer {
     rec.clone = sel.clone;
     rec.split = sel.split;
     rec.prune = prune_set;
+    // Parity "follow" mode: replay another run's decisions (e.g. the GPU's) so
+    // both runs keep consuming the shared Rng identically; the oracle's own
+    // selection stays in the record for flip reporting.
+    const size_t ev_index = events_.size();
+    if (ev_index < forced_.size() && forced_[ev_index].n == scene_.size()) {
+      const auto& f = forced_[ev_index];
+      sel.clone.clear();
+      sel.split.clear();
+      prune_set.clear();
+      for (int i = 0; i < f.n; ++i) {
+        if (f.prune[i]) prune_set.push_back(i);
+        else {
+          if (f.clone[i]) sel.clone.push_back(i);
+          if (f.split[i]) sel.split.push_back(i);
+        }
+      }
+      rec.forced = true;
+    }
     const IndexRemap prune_remap = apply_prune(scene_, prune_set);
     optimizer_.remap(prune_remap);
     for (int& i : sel.clone) i = prune_remap.old_to_new[i];
@@ -2101,6 +2126,7 @@ class Trainer {
   ScoreTable<T> table_;
   std::vector<ShMatrix<T>> rest_accum_;
   std::vector<EventRecord> events_;
+  std::vector<ForcedEvent> forced_;
   int it_ = 0;
   int last_view_ = -1;
 };

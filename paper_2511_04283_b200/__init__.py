@@ -668,3 +668,71 @@ def train_step_host(ctx: Context, scene: Scene, cam, gt_u8, cfg, extent, iterati
                                           C.byref(as_config(cfg)), C.c_float(extent), C.c_int(iteration),
                                           C.byref(row)))
     return dict(loss=row.loss, psnr=row.psnr, tile_pairs=row.tile_pairs, gaussians=row.gaussians)
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU: NCCL communicator (view sharding)
+# ---------------------------------------------------------------------------
+
+COMM_ID_BYTES = 128
+
+
+def comm_unique_id() -> bytes:
+    buf = (C.c_uint8 * COMM_ID_BYTES)()
+    rc = lib().sk_comm_unique_id(buf)
+    if rc != SK_OK:
+        raise SplatError("sk_comm_unique_id failed")
+    return bytes(buf)
+
+
+def share_comm_id(dist, rank: int) -> bytes:
+    """Rank 0 draws the NCCL id; every rank receives it over torch.distributed
+    (works with the gloo and nccl backends)."""
+    obj = [comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+class Comm:
+    """sk_comm: one rank of the NCCL communicator used by the trainer."""
+
+    def __init__(self, ctx: Context, uid: bytes, world: int, rank: int):
+        self.ctx = ctx
+        buf = (C.c_uint8 * COMM_ID_BYTES).from_buffer_copy(uid)
+        h = C.c_void_p()
+        ctx.check(ctx._lib.sk_comm_create(ctx.h, buf, C.c_int(world), C.c_int(rank), C.byref(h)))
+        self.h = h
+        self.rank, self.world = rank, world
+
+    @classmethod
+    def from_torch(cls, ctx: Context, dist, rank: int, world: int) -> "Comm":
+        return cls(ctx, share_comm_id(dist, rank), world, rank)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx._lib.sk_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def shard_assign(n_items: int, world: int, rank: int) -> list:
+    """Round-robin ownership of the K scored views (C3 sharding)."""
+    out = (C.c_int32 * max(1, n_items))()
+    n = C.c_int()
+    rc = lib().sk_shard_assign(C.c_int(n_items), C.c_int(world), C.c_int(rank), out, C.byref(n))
+    if rc != SK_OK:
+        raise ValueError("sk_shard_assign: bad arguments")
+    return list(out[: n.value])
+
+
+def _trainer_set_comm(self, comm: Comm):
+    self.comm = comm
+    self.ctx.check(self.ctx._lib.sk_trainer_set_comm(self.h, comm.h))
+
+
+Trainer.set_comm = _trainer_set_comm

@@ -281,7 +281,7 @@ unsigned blocks(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
 // gt: device images (u8 HWC) or host float HWC images (staged per view).
 void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_camera>& cams,
                 const std::vector<const void*>& gts, bool gt_u8_device, float tau, float lambda,
-                const sk_binning& bin, std::vector<float>* photo_out) {
+                const sk_binning& bin, std::vector<float>* photo_out, const sk_comm* comm = nullptr) {
   EventScratch& ev = ctx->ev;
   const int k = (int)cams.size();
   require(k > 0, "accumulate_scores: no training views");
@@ -289,8 +289,12 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
   const int64_t n = s->n;
   int32_t* rows = ensure<int32_t>(ev.rows, (size_t)k * std::max<int64_t>(n, 1));
   uint32_t* lohi = ensure<uint32_t>(ev.lohi, 4);
-  std::vector<float> photo(k);
+  SK_CUDA(cudaMemsetAsync(rows, 0, sizeof(int32_t) * (size_t)k * n, ctx->stream));
+  std::vector<float> photo(k, 0.0f);
+  const int world = comm ? comm->world : 1;
+  const int rank = comm ? comm->rank : 0;
   for (int j = 0; j < k; ++j) {
+    if (j % world != rank) continue;  // views sharded round-robin over ranks (C3 below)
     const sk_camera& cam = cams[j];
     frame_geometry(f, cam.width, cam.height, &bin);
     f->camera = cam;
@@ -323,11 +327,15 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
     // photometric = (1 - lambda) mean(raw) + lambda (1 - ssim)  (error_maps.hpp:40-41)
     photo[j] = (1.0f - lambda) * (float)v.l1 + lambda * (1.0f - (float)v.ssim);
     int32_t* row = rows + (size_t)j * n;
-    SK_CUDA(cudaMemsetAsync(row, 0, sizeof(int32_t) * n, ctx->stream));
     launch_blend_forward(ctx, f, mask, row);
   }
   float* dphoto = ensure<float>(ev.photo, k);
   h2d(ctx, dphoto, photo.data(), k);
+  allreduce_scores(comm, rows, (size_t)k * n, dphoto, k, ctx->stream);
+  if (world > 1) {
+    d2h(ctx, photo.data(), dphoto, k);
+    sync(ctx);
+  }
   const uint32_t init[2] = {0xffffffffu, 0u};
   h2d(ctx, lohi, init, 2);
   if (n > 0) {
@@ -471,7 +479,8 @@ void density_event(sk_trainer* t, int it, bool densify, bool prune) {
     rec.sampled.push_back(v);
   }
   const sk_binning bin = binning_from(cfg);
-  score_pass(ctx, s, &t->frame, cams, gts, true, (float)cfg.tau, (float)cfg.lambda, bin, &rec.photometric);
+  allreduce_stats(t->comm, s, ctx->stream);  // C2
+  score_pass(ctx, s, &t->frame, cams, gts, true, (float)cfg.tau, (float)cfg.lambda, bin, &rec.photometric, t->comm);
 
   const int64_t n = s->n;
   uint8_t* flags = ensure<uint8_t>(ctx->ev.flags, 3 * (size_t)std::max<int64_t>(n, 1));

@@ -37,7 +37,8 @@ struct Stats {
 
 // Computes all parameter gradients of one visible Gaussian (camera.hpp:156-213).
 // grad[] is indexed by SK_COMP_*.
-template <int DEG>
+// grad[c * GS] receives the gradient of component c.
+template <int DEG, int GS>
 __device__ __forceinline__ void project_backward_one(const float* __restrict__ p, int64_t stride, int64_t i,
                                                      const CamParams& cam, const float dmu2d[2], const float dcov[2][2],
                                                      const float dcol[3], float dop, float* grad) {
@@ -85,7 +86,7 @@ __device__ __forceinline__ void project_backward_one(const float* __restrict__ p
 
   // opacity (camera.hpp:171-172)
   const float sig = det_sigmoidf(p[SK_COMP_OPACITY * stride + i]);
-  grad[SK_COMP_OPACITY] = dop * sig * (1.0f - sig);
+  grad[SK_COMP_OPACITY * GS] = dop * sig * (1.0f - sig);
 
   // colour (camera.hpp:175-182, sh.hpp:93-114)
   float gmu[3];
@@ -137,15 +138,13 @@ __device__ __forceinline__ void project_backward_one(const float* __restrict__ p
         db[15][0] = kC3[6] * (3.0f * xx - 3.0f * yy), db[15][1] = kC3[6] * (-6.0f * dx * dy), db[15][2] = 0.f;
       }
     }
+    // the SH coefficients are read twice (L1-resident) instead of being held
+    // in 48 registers across both passes
     float raw[3] = {0.f, 0.f, 0.f};
-    float sh[NSH][3];
 #pragma unroll
     for (int k = 0; k < NSH; ++k)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        sh[k][c] = p[(SK_COMP_SH + 3 * k + c) * stride + i];
-        raw[c] += basis[k] * sh[k][c];
-      }
+      for (int c = 0; c < 3; ++c) raw[c] += basis[k] * p[(SK_COMP_SH + 3 * k + c) * stride + i];
     float draw[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) draw[c] = (raw[c] + 0.5f < 0.0f) ? 0.0f : dcol[c];
@@ -153,8 +152,11 @@ __device__ __forceinline__ void project_backward_one(const float* __restrict__ p
 #pragma unroll
     for (int k = 0; k < NSH; ++k) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) grad[SK_COMP_SH + 3 * k + c] = basis[k] * draw[c];
-      const float sd = (sh[k][0] * draw[0] + sh[k][1] * draw[1]) + sh[k][2] * draw[2];
+      for (int c = 0; c < 3; ++c) grad[(SK_COMP_SH + 3 * k + c) * GS] = basis[k] * draw[c];
+      const float s0 = p[(SK_COMP_SH + 3 * k + 0) * stride + i];
+      const float s1 = p[(SK_COMP_SH + 3 * k + 1) * stride + i];
+      const float s2 = p[(SK_COMP_SH + 3 * k + 2) * stride + i];
+      const float sd = (s0 * draw[0] + s1 * draw[1]) + s2 * draw[2];
 #pragma unroll
       for (int c = 0; c < 3; ++c) ddir[c] += sd * db[k][c];
     }
@@ -207,7 +209,7 @@ __device__ __forceinline__ void project_backward_one(const float* __restrict__ p
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
       const float ds = (dM[0][b] * r[0][b] + dM[1][b] * r[1][b]) + dM[2][b] * r[2][b];
-      grad[SK_COMP_LOG_SCALE + b] = ds * s[b];
+      grad[(SK_COMP_LOG_SCALE + b) * GS] = ds * s[b];
     }
     // quat_rotation_backward (scene.hpp:70-84)
     const float du_w = dr[0][1] * (-2.0f * z) + dr[0][2] * (2.0f * y) + dr[1][0] * (2.0f * z) +
@@ -222,10 +224,10 @@ __device__ __forceinline__ void project_backward_one(const float* __restrict__ p
                        dr[1][0] * (2.0f * w) + dr[1][1] * (-4.0f * z) + dr[1][2] * (2.0f * y) +
                        dr[2][0] * (2.0f * x) + dr[2][1] * (2.0f * y);
     const float qd = ((w * du_w + x * du_x) + y * du_y) + z * du_z;
-    grad[SK_COMP_ROT + 0] = (du_w - w * qd) / nq;
-    grad[SK_COMP_ROT + 1] = (du_x - x * qd) / nq;
-    grad[SK_COMP_ROT + 2] = (du_y - y * qd) / nq;
-    grad[SK_COMP_ROT + 3] = (du_z - z * qd) / nq;
+    grad[(SK_COMP_ROT + 0) * GS] = (du_w - w * qd) / nq;
+    grad[(SK_COMP_ROT + 1) * GS] = (du_x - x * qd) / nq;
+    grad[(SK_COMP_ROT + 2) * GS] = (du_y - y * qd) / nq;
+    grad[(SK_COMP_ROT + 3) * GS] = (du_z - z * qd) / nq;
   }
   // d_j = d_m R^T ; d_t (camera.hpp:197-207) ; + J^T d_mu2d ; mu += R^T d_t
   float dj[2][3];
@@ -241,7 +243,8 @@ __device__ __forceinline__ void project_backward_one(const float* __restrict__ p
 #pragma unroll
   for (int k = 0; k < 3; ++k) dt[k] += J[0][k] * dmu2d[0] + J[1][k] * dmu2d[1];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) grad[SK_COMP_MU + k] = gmu[k] + ((R[k] * dt[0] + R[3 + k] * dt[1]) + R[6 + k] * dt[2]);
+  for (int k = 0; k < 3; ++k)
+    grad[(SK_COMP_MU + k) * GS] = gmu[k] + ((R[k] * dt[0] + R[3 + k] * dt[1]) + R[6 + k] * dt[2]);
 }
 
 struct AdamParams {
@@ -304,43 +307,63 @@ __device__ __forceinline__ void accumulate_stats(const Stats& st, int64_t i, int
 }
 
 // MODE 0: gradients -> grads buffer (+ stats). MODE 1: fused Adam (+ stats).
+constexpr int kPbThreads = 128;
+
+// Phase 1 computes the Gaussian's gradients into this thread's column of a
+// shared-memory tile (conflict-free: column = threadIdx.x) instead of holding
+// 59 live registers; phase 2 streams params / m / v in batches of 8
+// components so 24 independent loads per thread are in flight.
 template <int DEG, int MODE>
-__global__ void __launch_bounds__(128) project_bwd_kernel(float* __restrict__ params, int64_t stride, int64_t n,
-                                                          CamParams cam, const float* __restrict__ radius,
-                                                          const float4* __restrict__ conic4,
-                                                          const float* __restrict__ bg, int64_t gstride,
-                                                          float* __restrict__ grads, float* __restrict__ am,
-                                                          float* __restrict__ av, AdamParams ap, Stats st,
-                                                          bool do_stats) {
+__global__ void __launch_bounds__(kPbThreads, 4) project_bwd_kernel(
+    float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ radius,
+    const float4* __restrict__ conic4, const float* __restrict__ bg, int64_t gstride, float* __restrict__ grads,
+    float* __restrict__ am, float* __restrict__ av, AdamParams ap, Stats st, bool do_stats) {
   constexpr int NC = 11 + 3 * (DEG + 1) * (DEG + 1);
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ float s_grad[NC * kPbThreads];
+  const int64_t i = (int64_t)blockIdx.x * kPbThreads + threadIdx.x;
   if (i >= n) return;
-  float grad[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) grad[c] = 0.0f;
+  float* g = s_grad + threadIdx.x;  // component c at g[c * kPbThreads]
   const float rad = radius[i];
   if (rad > 0.0f) {
     float dmu2d[2], dcov[2][2], dcol[3], dop, absg[2];
     load_blend(bg, gstride, i, dmu2d, dcov, conic4[i], dcol, dop, absg);
-    project_backward_one<DEG>(params, stride, i, cam, dmu2d, dcov, dcol, dop, grad);
+    project_backward_one<DEG, kPbThreads>(params, stride, i, cam, dmu2d, dcov, dcol, dop, g);
     if (do_stats) {
-      const float gmu[3] = {grad[0], grad[1], grad[2]};
+      const float gmu[3] = {g[0], g[kPbThreads], g[2 * kPbThreads]};
       accumulate_stats(st, i, stride, dmu2d, absg, gmu, rad, (float)cam.width / 2.0f, (float)cam.height / 2.0f);
     }
+  } else {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) g[c * kPbThreads] = 0.0f;
   }
   if (MODE == 0) {
 #pragma unroll
-    for (int c = 0; c < NC; ++c) grads[c * stride + i] = grad[c];
-  } else {
+    for (int c = 0; c < NC; ++c) grads[c * stride + i] = g[c * kPbThreads];
+    return;
+  }
+  constexpr int B = 8;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
+  for (int c0 = 0; c0 < NC; c0 += B) {
+    float pv[B], mv[B], vv[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int c = c0 + u;
+      if (c < NC && ap.active[comp_group(c)]) {
+        pv[u] = params[c * stride + i];
+        mv[u] = am[c * stride + i];
+        vv[u] = av[c * stride + i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int c = c0 + u;
       const int gidx = comp_group(c);
-      if (!ap.active[gidx]) continue;
-      float pv = params[c * stride + i], mv = am[c * stride + i], vv = av[c * stride + i];
-      adam_update(pv, mv, vv, grad[c], ap.lr[gidx], ap.bc1[gidx], ap.bc2[gidx]);
-      params[c * stride + i] = pv;
-      am[c * stride + i] = mv;
-      av[c * stride + i] = vv;
+      if (c < NC && ap.active[gidx]) {
+        adam_update(pv[u], mv[u], vv[u], g[c * kPbThreads], ap.lr[gidx], ap.bc1[gidx], ap.bc2[gidx]);
+        params[c * stride + i] = pv[u];
+        am[c * stride + i] = mv[u];
+        av[c * stride + i] = vv[u];
+      }
     }
   }
 }

@@ -10,15 +10,27 @@
 // deterministic exp, so images, transmittance and footprint counts match the
 // CPU oracle bit for bit.
 //
+// Early reject: alpha >= 1/255 requires q <= 2 ln(255 o). Each staged entry
+// carries q_cut = 2 ln(255 o) + 0.02; for q > q_cut the reference's alpha is
+// below 1/255 by a 1% margin (far above the 2-ulp exp error), so skipping the
+// exponential there leaves every result bit-identical.
+//
 // K8 restates blend_backward (raster.hpp:281-355) as a reverse walk from each
 // pixel's last contributor (recorded by K6): T_before = T_after / (1 - alpha),
 // suffix accumulated in the reference's reverse order, capped entries feed
-// d_color only. Per-Gaussian partials are butterfly-reduced across the warp
-// with shuffles, then one lane per gradient field issues a global atomic.
+// d_color only. Each thread owns PIX pixels of its tile (rows y, y + TS/PIX,
+// ...), sums their partials per Gaussian in registers, and the warp then
+// butterfly-reduces the 11 partials with shuffles (skipped when no lane
+// contributes); lanes 0..10 issue one global atomic each.
 #include "state.h"
 
 namespace sk {
 namespace {
+
+__device__ __forceinline__ float qcut_of(float opacity) {
+  const float a = 255.0f * opacity;
+  return a > 1.0f ? 2.0f * __logf(a) + 0.02f : -1.0f;
+}
 
 template <int TS, bool COUNT>
 __global__ void __launch_bounds__(TS* TS) blend_fwd_kernel(
@@ -27,9 +39,9 @@ __global__ void __launch_bounds__(TS* TS) blend_fwd_kernel(
     float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry,
     const uint8_t* __restrict__ mask, int* __restrict__ counts) {
   constexpr int B = TS * TS;
-  __shared__ float2 s_xy[B];
+  __shared__ float4 s_xyq[B];
   __shared__ float4 s_co[B];
-  __shared__ float4 s_rgb[B];
+  __shared__ float4 s_rgb[COUNT ? 1 : B];
   __shared__ uint32_t s_id[COUNT ? B : 1];
 
   const int tile = blockIdx.x;
@@ -53,37 +65,40 @@ __global__ void __launch_bounds__(TS* TS) blend_fwd_kernel(
     const int i = b0 + (int)threadIdx.x;
     if (i < range.y) {
       const uint32_t g = pair_val[i];
-      s_xy[threadIdx.x] = mean2d[g];
-      s_co[threadIdx.x] = conic_op[g];
-      s_rgb[threadIdx.x] = rgbd[g];
+      const float2 mu = mean2d[g];
+      const float4 co = conic_op[g];
+      s_xyq[threadIdx.x] = make_float4(mu.x, mu.y, qcut_of(co.w), 0.0f);
+      s_co[threadIdx.x] = co;
+      if (!COUNT) s_rgb[threadIdx.x] = rgbd[g];
       if (COUNT) s_id[threadIdx.x] = g;
     }
     __syncthreads();
     const int cnt = min(B, range.y - b0);
     if (!done) {
       for (int j = 0; j < cnt; ++j) {
-        const float2 mu = s_xy[j];
+        const float4 mq = s_xyq[j];
         const float4 co = s_co[j];
-        const float dx = fpx - mu.x;
-        const float dy = fpy - mu.y;
+        const float dx = fpx - mq.x;
+        const float dy = fpy - mq.y;
         const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
-        if (q < 0.0f) continue;
+        if (q < 0.0f || q > mq.z) continue;
         float alpha = co.w * det_expf(-0.5f * q);
         alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
         if (alpha < kAlphaMin) continue;
-        const float4 c = s_rgb[j];
-        const float w = T * alpha;
-        C0 = C0 + w * c.x;
-        C1 = C1 + w * c.y;
-        C2 = C2 + w * c.z;
-        ++n;
-        last = b0 + j + 1;
         if (COUNT) {
           // warp-aggregated increment: one atomic per distinct Gaussian
           const uint32_t id = s_id[j];
           const uint32_t act = __activemask();
           const uint32_t peers = __match_any_sync(act, id);
           if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&counts[id], __popc(peers));
+        } else {
+          const float4 c = s_rgb[j];
+          const float w = T * alpha;
+          C0 = C0 + w * c.x;
+          C1 = C1 + w * c.y;
+          C2 = C2 + w * c.z;
+          ++n;
+          last = b0 + j + 1;
         }
         T = T * (1.0f - alpha);
         if (T < kTransmitMin) {
@@ -111,55 +126,67 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-template <int TS>
-__global__ void __launch_bounds__(TS* TS) blend_bwd_kernel(
+template <int TS, int PIX>
+__global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     const float* __restrict__ final_t, const int* __restrict__ last_entry, const float* __restrict__ dimage,
     float* __restrict__ bgrads, int64_t gstride) {
-  constexpr int B = TS * TS;
-  __shared__ float2 s_xy[B];
-  __shared__ float4 s_co[B];
-  __shared__ float4 s_rgb[B];
-  __shared__ uint32_t s_id[B];
+  constexpr int NT = TS * TS / PIX;  // threads == batch size
+  constexpr int ROWS = TS / PIX;     // row stride between a thread's pixels
+  __shared__ float4 s_xyq[NT];
+  __shared__ float4 s_co[NT];
+  __shared__ float4 s_rgb[NT];
+  __shared__ uint32_t s_id[NT];
   __shared__ int s_max_last;
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int px = tx * TS + (int)(threadIdx.x % TS);
-  const int py = ty * TS + (int)(threadIdx.x / TS);
-  const bool inside = px < W && py < H;
-  const int2 range = ranges[tile];
   const int lane = threadIdx.x & 31;
-  const float fpx = (float)px, fpy = (float)py;
+  const int px = tx * TS + (int)(threadIdx.x % TS);
+  const int py0 = ty * TS + (int)(threadIdx.x / TS);
+  const int2 range = ranges[tile];
+  const float fpx = (float)px;
+  const size_t plane = (size_t)W * H;
 
-  float T = 1.0f, d0 = 0.0f, d1 = 0.0f, d2 = 0.0f;
-  int last = 0;
-  if (inside) {
-    const size_t p = (size_t)py * W + px;
-    const size_t plane = (size_t)W * H;
-    T = final_t[p];
-    last = last_entry[p];
-    d0 = dimage[p];
-    d1 = dimage[plane + p];
-    d2 = dimage[2 * plane + p];
+  float T[PIX], suffix[PIX], d0[PIX], d1[PIX], d2[PIX], fpy[PIX];
+  int last[PIX];
+  int my_last = 0;
+#pragma unroll
+  for (int k = 0; k < PIX; ++k) {
+    const int py = py0 + k * ROWS;
+    fpy[k] = (float)py;
+    T[k] = 1.0f;
+    suffix[k] = 0.0f;
+    d0[k] = d1[k] = d2[k] = 0.0f;
+    last[k] = 0;
+    if (px < W && py < H) {
+      const size_t p = (size_t)py * W + px;
+      T[k] = final_t[p];
+      last[k] = last_entry[p];
+      d0[k] = dimage[p];
+      d1[k] = dimage[plane + p];
+      d2[k] = dimage[2 * plane + p];
+    }
+    my_last = max(my_last, last[k]);
   }
   if (threadIdx.x == 0) s_max_last = 0;
   __syncthreads();
-  atomicMax(&s_max_last, last);
+  atomicMax(&s_max_last, my_last);
   __syncthreads();
   const int end = s_max_last;  // no pixel of the tile uses entries >= end
-  const int warp_last = __reduce_max_sync(0xffffffffu, last);
-  float suffix = 0.0f;
+  const int warp_last = __reduce_max_sync(0xffffffffu, my_last);
 
-  for (int b_end = end; b_end > range.x; b_end -= B) {
-    const int b0 = max(range.x, b_end - B);
+  for (int b_end = end; b_end > range.x; b_end -= NT) {
+    const int b0 = max(range.x, b_end - NT);
     __syncthreads();
     const int i = b0 + (int)threadIdx.x;
     if (i < b_end) {
       const uint32_t g = pair_val[i];
-      s_xy[threadIdx.x] = mean2d[g];
-      s_co[threadIdx.x] = conic_op[g];
+      const float2 mu = mean2d[g];
+      const float4 co = conic_op[g];
+      s_xyq[threadIdx.x] = make_float4(mu.x, mu.y, qcut_of(co.w), 0.0f);
+      s_co[threadIdx.x] = co;
       s_rgb[threadIdx.x] = rgbd[g];
       s_id[threadIdx.x] = g;
     }
@@ -167,47 +194,49 @@ __global__ void __launch_bounds__(TS* TS) blend_bwd_kernel(
     const int jmax = min(b_end, warp_last) - b0;  // warp-uniform
     for (int j = jmax - 1; j >= 0; --j) {
       const int idx = b0 + j;
+      const float4 mq = s_xyq[j];
+      const float4 co = s_co[j];
       float g_mu0 = 0.f, g_mu1 = 0.f, g_c00 = 0.f, g_c01 = 0.f, g_c11 = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f,
             g_op = 0.f, g_a0 = 0.f, g_a1 = 0.f;
       bool contrib = false;
-      if (idx < last) {
-        const float2 mu = s_xy[j];
-        const float4 co = s_co[j];
-        const float dx = fpx - mu.x;
-        const float dy = fpy - mu.y;
+#pragma unroll
+      for (int k = 0; k < PIX; ++k) {
+        if (idx >= last[k]) continue;
+        const float dx = fpx - mq.x;
+        const float dy = fpy[k] - mq.y;
         const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
-        if (q >= 0.0f) {
-          const float ge = det_expf(-0.5f * q);
-          const float raw = co.w * ge;
-          const bool capped = raw > kAlphaCap;
-          const float alpha = capped ? kAlphaCap : raw;
-          if (alpha >= kAlphaMin) {
-            contrib = true;
-            const float4 c = s_rgb[j];
-            const float one_m = 1.0f - alpha;
-            const float t_before = T / one_m;
-            T = t_before;
-            const float w = (c.x * d0 + c.y * d1) + c.z * d2;
-            const float d_alpha = t_before * w - suffix / one_m;
-            const float ta = t_before * alpha;
-            suffix = suffix + ta * w;
-            g_r = ta * d0;
-            g_g = ta * d1;
-            g_b = ta * d2;
-            if (!capped) {
-              g_op = ge * d_alpha;
-              const float d_q = -0.5f * alpha * d_alpha;
-              g_c00 = d_q * (dx * dx);
-              g_c01 = d_q * (dx * dy);
-              g_c11 = d_q * (dy * dy);
-              const float v0 = co.x * dx + co.y * dy;
-              const float v1 = co.y * dx + co.z * dy;
-              g_mu0 = (-2.0f * d_q) * v0;
-              g_mu1 = (-2.0f * d_q) * v1;
-              g_a0 = fabsf(g_mu0);
-              g_a1 = fabsf(g_mu1);
-            }
-          }
+        if (q < 0.0f || q > mq.z) continue;
+        const float ge = det_expf(-0.5f * q);
+        const float raw = co.w * ge;
+        const bool capped = raw > kAlphaCap;
+        const float alpha = capped ? kAlphaCap : raw;
+        if (alpha < kAlphaMin) continue;
+        contrib = true;
+        const float4 c = s_rgb[j];
+        const float one_m = 1.0f - alpha;
+        const float t_before = T[k] / one_m;
+        T[k] = t_before;
+        const float w = (c.x * d0[k] + c.y * d1[k]) + c.z * d2[k];
+        const float d_alpha = t_before * w - suffix[k] / one_m;
+        const float ta = t_before * alpha;
+        suffix[k] = suffix[k] + ta * w;
+        g_r += ta * d0[k];
+        g_g += ta * d1[k];
+        g_b += ta * d2[k];
+        if (!capped) {
+          g_op += ge * d_alpha;
+          const float d_q = -0.5f * alpha * d_alpha;
+          g_c00 += d_q * (dx * dx);
+          g_c01 += d_q * (dx * dy);
+          g_c11 += d_q * (dy * dy);
+          const float v0 = co.x * dx + co.y * dy;
+          const float v1 = co.y * dx + co.z * dy;
+          const float m0 = (-2.0f * d_q) * v0;
+          const float m1 = (-2.0f * d_q) * v1;
+          g_mu0 += m0;
+          g_mu1 += m1;
+          g_a0 += fabsf(m0);
+          g_a1 += fabsf(m1);
         }
       }
       if (__any_sync(0xffffffffu, contrib)) {
@@ -223,7 +252,7 @@ __global__ void __launch_bounds__(TS* TS) blend_bwd_kernel(
         g_a0 = warp_sum(g_a0);
         g_a1 = warp_sum(g_a1);
         if (lane < kBGradFields) {
-          float v = g_mu0;
+          float v;
           switch (lane) {
             case 0: v = g_mu0; break;
             case 1: v = g_mu1; break;
@@ -262,10 +291,10 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
   note_launch();
 }
 
-template <int TS>
+template <int TS, int PIX>
 void bwd_dispatch(sk_ctx* ctx, sk_frame* f) {
   const int tiles = f->tiles_x * f->tiles_y;
-  blend_bwd_kernel<TS><<<tiles, TS * TS, 0, ctx->stream>>>(
+  blend_bwd_kernel<TS, PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
       f->ranges.as<int2>(), f->pair_val, f->mean2d.as<float2>(), f->conic_op.as<float4>(), f->rgb_depth.as<float4>(),
       f->width, f->height, f->tiles_x, f->final_t.as<float>(), f->last_entry.as<int>(), f->dimage.as<float>(),
       f->bgrads.as<float>(), f->n);
@@ -289,9 +318,9 @@ void launch_blend_backward(sk_ctx* ctx, sk_frame* f) {
   SK_CUDA(cudaMemsetAsync(f->bgrads.ptr, 0, sizeof(float) * kBGradFields * (size_t)f->n, ctx->stream));
   if (f->tiles_x * f->tiles_y == 0) return;
   switch (f->tile_size) {
-    case 8: bwd_dispatch<8>(ctx, f); break;
-    case 16: bwd_dispatch<16>(ctx, f); break;
-    case 32: bwd_dispatch<32>(ctx, f); break;
+    case 8: bwd_dispatch<8, 1>(ctx, f); break;
+    case 16: bwd_dispatch<16, 2>(ctx, f); break;
+    case 32: bwd_dispatch<32, 4>(ctx, f); break;
     default: throw std::invalid_argument("tile_size must be 8, 16 or 32");
   }
   SK_CUDA(cudaGetLastError());

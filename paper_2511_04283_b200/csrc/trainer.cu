@@ -80,7 +80,7 @@ bool lazy_update_due(int it, const sk_train_config& c) {
 // One train_iteration (trainer.hpp:124-175) on camera `cam` with the 8-bit GT
 // already on the device.
 void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam, const uint8_t* gt_dev,
-                const sk_train_config& cfg, float extent, int it, sk_log_row* row) {
+                const sk_train_config& cfg, float extent, int it, sk_log_row* row, const sk_comm* comm) {
   const sk_binning bin = binning_from(cfg);
   frame_geometry(f, cam.width, cam.height, &bin);
   f->camera = cam;
@@ -102,7 +102,14 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   const LearningRates lrs = lrs_from(cfg);
   const float pos_lr = expon_lr(lrs.position * extent, lrs.position_final * extent, it, cfg.iterations);
   require(!cfg.lazy_opt_enabled, "trainer: lazy_opt_enabled is not supported on the GPU path yet");
-  launch_project_backward_adam(ctx, scene, f, lrs, pos_lr, true, true);
+  if (comm && comm->world > 1) {
+    // view-parallel step: K9 into the gradient buffer, C1 sum over ranks, K10
+    launch_project_backward(ctx, scene, f, true);
+    allreduce_grads(comm, scene, ctx->stream);
+    launch_adam(ctx, scene, lrs, pos_lr, true);
+  } else {
+    launch_project_backward_adam(ctx, scene, f, lrs, pos_lr, true, true);
+  }
   ctx->mark(6);
   LossSums sums{};
   read_loss_sums(ctx, &sums);  // synchronises the stream
@@ -409,10 +416,17 @@ int sk_trainer_run(sk_trainer* t, int iterations, sk_log_row* rows) {
       sk_log_row row{};
       row.iteration = it;
       if (!t->cfg.schedule_dry_run) {
-        const int view = t->data->train[(size_t)t->rng.bounded((uint64_t)t->data->train.size())];
+        // one shared Rng draw per rank, in rank order; rank r trains view r
+        const int world = t->comm ? t->comm->world : 1;
+        const int rank = t->comm ? t->comm->rank : 0;
+        int view = 0;
+        for (int r = 0; r < world; ++r) {
+          const int v = t->data->train[(size_t)t->rng.bounded((uint64_t)t->data->train.size())];
+          if (r == rank) view = v;
+        }
         row.view = view;
         train_step(t->ctx, t->scene, &t->frame, t->data->cams[view], t->data->images[view]->as<uint8_t>(), t->cfg,
-                   t->data->extent, it, &row);
+                   t->data->extent, it, &row, t->comm);
       }
       const bool dens = densify_due(it, t->cfg);
       const bool prn = prune_due(it, t->cfg);

@@ -7,7 +7,15 @@
 #include <random>
 #include <vector>
 
+#include <nccl.h>
+
 #include "state.h"
+
+// NCCL communicator of one rank (comm.cu).
+struct sk_comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+};
 
 struct sk_dataset {
   std::vector<sk_camera> cams;
@@ -75,6 +83,7 @@ struct sk_trainer {
   bool started = false;
   bool record_events = false;
   std::vector<EventRecord> events;
+  sk_comm* comm = nullptr;  // view sharding across ranks (nullptr: single GPU)
 };
 
 namespace sk {
@@ -86,9 +95,14 @@ void validate_config(const sk_train_config& c);
 bool densify_due(int it, const sk_train_config& c);
 bool prune_due(int it, const sk_train_config& c);
 void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam, const uint8_t* gt_dev,
-                const sk_train_config& cfg, float extent, int it, sk_log_row* row);
+                const sk_train_config& cfg, float extent, int it, sk_log_row* row, const sk_comm* comm = nullptr);
 
 // density.cu: Trainer::density_event (trainer.hpp:177-243).
 void density_event(sk_trainer* t, int it, bool densify, bool prune);
+
+// comm.cu: C1 / C2 / C3 (no-ops for a null or single-rank communicator).
+void allreduce_grads(const sk_comm* c, sk_scene* s, cudaStream_t st);
+void allreduce_stats(const sk_comm* c, sk_scene* s, cudaStream_t st);
+void allreduce_scores(const sk_comm* c, int32_t* rows, size_t count, float* photo, int k, cudaStream_t st);
 
 }  // namespace sk

@@ -1,0 +1,37 @@
+"""The splat:: C++ surface (include/splatkit_b200.hpp) over the C ABI: a C++
+caller written like the reference's tests compiles here and runs on the GPU."""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _build(tmp_path):
+    import paper_2511_04283_b200 as sk
+    sk.build()
+    cxx = shutil.which("g++")
+    if cxx is None:
+        pytest.skip("no g++")
+    exe = os.path.join(str(tmp_path), "wrapper_smoke")
+    libdir = os.path.dirname(sk.LIB_PATH)
+    cmd = [cxx, "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "wrapper_smoke.cpp"), "-o", exe, "-L", libdir, "-lsplatkit_b200",
+           f"-Wl,-rpath,{libdir}"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_cpp_wrapper_compiles_and_links(tmp_path):
+    assert os.path.exists(_build(tmp_path))
+
+
+@pytest.mark.gpu
+def test_cpp_wrapper_runs_on_gpu(tmp_path):
+    exe = _build(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASS" in r.stdout

@@ -193,25 +193,38 @@ def test_config1_training_parity(ctx, orc):
     gpu_events = tr.events()
     final_gpu = scene.download()
 
+    # The oracle replays the GPU's decisions ("follow" mode) so that a single
+    # near-threshold flip does not desynchronise the shared Rng (the split
+    # noise count depends on the split set); its own selection is kept in its
+    # event records and every disagreement is reported as a flip.
     otr = orc.Trainer(p0, 3, ds, cfg)
+    orc.trainer_force_events(otr, gpu_events)
     orows, secs = otr.run(500)
     final_cpu = otr.scene()
     cpu_events = otr.events()
 
-    # test view 0 PSNR of both final scenes, rendered by the oracle
     test_gt = imgs[0].astype(np.float32) / np.float32(255)
     ps_gpu = orc.psnr(orc.render_scene(final_gpu, 3, cams[0]).image, test_gt)
     ps_cpu = orc.psnr(orc.render_scene(final_cpu, 3, cams[0]).image, test_gt)
-    print(f"config1: test PSNR gpu {ps_gpu:.3f} dB cpu {ps_cpu:.3f} dB; N gpu {final_gpu.shape[1]} "
+    print(f"config1: test-view PSNR gpu {ps_gpu:.3f} dB cpu {ps_cpu:.3f} dB; N gpu {final_gpu.shape[1]} "
           f"cpu {final_cpu.shape[1]}; oracle {secs:.1f} s")
     assert len(gpu_events) == len(cpu_events)
-    # the Rng sequence is shared until the first split-count difference
-    assert list(gpu_events[0]["sampled"]) == list(cpu_events[0]["sampled"])
+    total_flips = 0
     for ge, ce in zip(gpu_events, cpu_events):
         assert ge["iteration"] == ce["iteration"]
-        print(f"  event {ge['iteration']}: N {ge['n_before']}->{ge['n_after']} (cpu {ce['n_before']}->"
-              f"{ce['n_after']}) clone {ge['n_clone']}/{len(ce['clone'])} split {ge['n_split']}/{len(ce['split'])}"
-              f" prune {ge['n_prune']}/{len(ce['prune'])}")
+        assert list(ge["sampled"]) == list(ce["sampled"])
+        n = ge["n_before"]
+        assert ce["n_before"] == n and ce["n_after"] == ge["n_after"]
+        flips = {}
+        for key in ("clone", "split", "prune"):
+            own = np.zeros(n, np.uint8)
+            own[ce[key]] = 1
+            flips[key] = int((own != ge[key]).sum())
+        total_flips += sum(flips.values())
+        print(f"  event {ge['iteration']}: N {n}->{ge['n_after']} clone {ge['n_clone']} split {ge['n_split']} "
+              f"prune {ge['n_prune']} | near-threshold flips {flips}")
+        # flips come from near-threshold statistics (atomic summation order,
+        # Adam sign flips on near-zero gradients); they stay a small fraction
+        assert sum(flips.values()) <= max(3, n // 100)
     assert abs(ps_gpu - ps_cpu) <= 0.05
-    # training losses track each other
     assert abs(rows[-1]["loss"] - orows[-1, 0]) < 0.05 * abs(orows[-1, 0]) + 1e-3
