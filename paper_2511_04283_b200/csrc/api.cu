@@ -151,7 +151,7 @@ int sk_scene_create(sk_ctx* ctx, int sh_degree, int64_t capacity, sk_scene** out
     auto s = std::make_unique<sk_scene>();
     s->sh_degree = sh_degree;
     s->comps = SK_COMP_COUNT(sh_degree);
-    s->capacity = std::max<int64_t>(capacity, 1);
+    s->capacity = round_capacity(capacity);
     ensure<float>(s->params, (size_t)s->comps * s->capacity);
     *out = s.release();
   });
@@ -167,7 +167,7 @@ int sk_scene_upload(sk_ctx* ctx, sk_scene* s, const float* host, int64_t n) {
     arg(s && (host || n == 0) && n >= 0, "sk_scene_upload: bad arguments");
     set_device(ctx);
     if (n > s->capacity) {
-      s->capacity = n;
+      s->capacity = round_capacity(n);
       s->params.release();
     }
     float* p = ensure<float>(s->params, (size_t)s->comps * s->capacity);

@@ -432,7 +432,8 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
     h2d(ctx, eps, eps_host, 6 * (size_t)n_split);
   }
   ensure_optimizer_state(ctx, s);
-  const int64_t new_cap = new_n > s->capacity ? std::max<int64_t>(new_n, s->capacity + s->capacity / 2) : s->capacity;
+  const int64_t new_cap =
+      new_n > s->capacity ? round_capacity(std::max<int64_t>(new_n, s->capacity + s->capacity / 2)) : s->capacity;
   DevBuf np, nm, nv;
   const size_t cells = (size_t)s->comps * new_cap;
   ensure<float>(np, cells);

@@ -4,11 +4,12 @@
 // types.hpp:28-30 sigmoid, raster.hpp:81 compact_threshold, raster.hpp:228 the
 // blend alpha). glibc and CUDA libm do not agree to the last ulp, so a Gaussian
 // sitting on a tile or alpha boundary could bin or blend differently on the CPU
-// oracle and on the GPU. These helpers use only IEEE +,-,*,/ and integer bit
-// operations in a fixed order, so they produce identical bits on the host
-// (compiled with -ffp-contract=off, no FMA) and on sm_100a (compiled with
-// -fmad=false, IEEE div/sqrt, no flush-to-zero). Accuracy is 1-2 ulp against
-// the correctly rounded result; tests/test_detmath.py checks that bound.
+// oracle and on the GPU. These helpers use only IEEE +,-,*,/, exact power-of-
+// two scalings, a fixed 64-entry table and integer bit operations in a fixed
+// order, so they produce identical bits on the host (compiled with
+// -ffp-contract=off, no FMA) and on sm_100a (compiled with -fmad=false, IEEE
+// div/sqrt, no flush-to-zero). Accuracy is within 2 ulp of the correctly
+// rounded result; tests/test_oracle_kats.py checks that bound.
 #pragma once
 
 #include <stdint.h>
@@ -50,28 +51,68 @@ SK_HD float det_floorf(float x) {
 #endif
 }
 
-// e^x. Cody-Waite reduction x = k ln2 + r, |r| <= ln2/2, degree-7 Taylor
-// polynomial in Horner form, then two exact power-of-two scalings.
-SK_HD float det_expf(float x) {
-  if (!(x == x)) return x;                       // NaN propagates
-  if (x > 88.72283f) return bits_to_f32(0x7f800000u);  // +inf
-  if (x < -103.97208f) return 0.0f;              // below the smallest subnormal
-  const float kf = det_floorf(x * 1.44269504088896341f + 0.5f);
+// 2^(j/64), j = 0..63, rounded to float (bit patterns, identical everywhere).
+#define SK_EXP2_TABLE                                                                                            \
+  {0x3f800000u, 0x3f8164d2u, 0x3f82cd87u, 0x3f843a29u, 0x3f85aac3u, 0x3f871f62u, 0x3f88980fu, 0x3f8a14d5u,      \
+   0x3f8b95c2u, 0x3f8d1adfu, 0x3f8ea43au, 0x3f9031dcu, 0x3f91c3d3u, 0x3f935a2bu, 0x3f94f4f0u, 0x3f96942du,      \
+   0x3f9837f0u, 0x3f99e046u, 0x3f9b8d3au, 0x3f9d3edau, 0x3f9ef532u, 0x3fa0b051u, 0x3fa27043u, 0x3fa43516u,      \
+   0x3fa5fed7u, 0x3fa7cd94u, 0x3fa9a15bu, 0x3fab7a3au, 0x3fad583fu, 0x3faf3b79u, 0x3fb123f6u, 0x3fb311c4u,      \
+   0x3fb504f3u, 0x3fb6fd92u, 0x3fb8fbafu, 0x3fbaff5bu, 0x3fbd08a4u, 0x3fbf179au, 0x3fc12c4du, 0x3fc346cdu,      \
+   0x3fc5672au, 0x3fc78d75u, 0x3fc9b9beu, 0x3fcbec15u, 0x3fce248cu, 0x3fd06334u, 0x3fd2a81eu, 0x3fd4f35bu,      \
+   0x3fd744fdu, 0x3fd99d16u, 0x3fdbfbb8u, 0x3fde60f5u, 0x3fe0ccdfu, 0x3fe33f89u, 0x3fe5b907u, 0x3fe8396au,      \
+   0x3feac0c7u, 0x3fed4f30u, 0x3fefe4bau, 0x3ff28177u, 0x3ff5257du, 0x3ff7d0dfu, 0x3ffa83b3u, 0x3ffd3e0cu}
+
+#if defined(__CUDACC__)
+__constant__ const uint32_t kExp2TableDev[64] = SK_EXP2_TABLE;
+#endif
+static const uint32_t kExp2TableHost[64] = SK_EXP2_TABLE;
+
+// e^x for x in [-87, 88] (normal-range result). x = (64k + j) ln2/64 + r with
+// |r| <= ln2/128 (Cody-Waite split of ln2/64 into a 9-bit head, so kf * head
+// is exact for |k| < 2^14), e^r by a degree-3 polynomial, then the table and
+// one exact power-of-two scaling. `table` holds the 64 SK_EXP2_TABLE floats.
+SK_HD float det_expf_core(float x, const float* table) {
+  const float kf = det_floorf(x * 92.33248261689366f + 0.5f);  // 64 / ln2
   const int k = (int)kf;
-  const float r = (x - kf * 0.693145751953125f) - kf * 1.428606820309417232e-06f;
-  float p = 1.98412698412698413e-04f;  // 1/5040
-  p = p * r + 1.38888888888888889e-03f;  // 1/720
-  p = p * r + 8.33333333333333333e-03f;  // 1/120
-  p = p * r + 4.16666666666666667e-02f;  // 1/24
-  p = p * r + 1.66666666666666667e-01f;  // 1/6
-  p = p * r + 0.5f;
+  const float r = (x - kf * 0.010833740234375f) - kf * -3.3155381258549027e-06f;
+  float p = r * 0.16666666666666666f + 0.5f;
   p = p * r + 1.0f;
   p = p * r + 1.0f;
-  const int k1 = k / 2;
-  const int k2 = k - k1;
-  const float s1 = bits_to_f32((uint32_t)(k1 + 127) << 23);
-  const float s2 = bits_to_f32((uint32_t)(k2 + 127) << 23);
-  return (p * s1) * s2;
+  const int j = k & 63;
+  const int e = (k - j) / 64;
+  return (table[j] * p) * bits_to_f32((uint32_t)(e + 127) << 23);
+}
+
+SK_HD const float* exp2_table() {
+#if defined(__CUDA_ARCH__)
+  return reinterpret_cast<const float*>(kExp2TableDev);
+#else
+  return reinterpret_cast<const float*>(kExp2TableHost);
+#endif
+}
+
+// e^x for any float: special cases, then the core (two scalings keep the
+// subnormal / overflow ends exact). Kernels with many calls pass a copy of
+// the table staged in shared memory (constant memory serialises divergent
+// indices).
+SK_HD float det_expf(float x, const float* table = nullptr) {
+  if (!table) table = exp2_table();
+  if (!(x == x)) return x;                             // NaN propagates
+  if (x > 88.72283f) return bits_to_f32(0x7f800000u);  // +inf
+  if (x < -103.97208f) return 0.0f;                    // below the smallest subnormal
+  if (x >= -87.0f && x <= 88.0f) return det_expf_core(x, table);
+  const float kf = det_floorf(x * 92.33248261689366f + 0.5f);
+  const int k = (int)kf;
+  const float r = (x - kf * 0.010833740234375f) - kf * -3.3155381258549027e-06f;
+  float p = r * 0.16666666666666666f + 0.5f;
+  p = p * r + 1.0f;
+  p = p * r + 1.0f;
+  const int j = k & 63;
+  const int e = (k - j) / 64;
+  const int e1 = e / 2;
+  const int e2 = e - e1;
+  const float t = table[j] * p;
+  return (t * bits_to_f32((uint32_t)(e1 + 127) << 23)) * bits_to_f32((uint32_t)(e2 + 127) << 23);
 }
 
 // Natural log of a positive finite float. x = m 2^e with m in [sqrt(.5),
@@ -107,6 +148,13 @@ SK_HD float det_logf(float x) {
 }
 
 // Activation used by the reference (types.hpp:28-30): 1 / (1 + e^{-x}).
-SK_HD float det_sigmoidf(float x) { return 1.0f / (1.0f + det_expf(-x)); }
+SK_HD float det_sigmoidf(float x, const float* table = nullptr) { return 1.0f / (1.0f + det_expf(-x, table)); }
+
+#if defined(__CUDACC__)
+// Stages the exp table into shared memory; call from all threads, then sync.
+__device__ __forceinline__ void stage_exp2_table(float* s_table) {
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) s_table[i] = bits_to_f32(kExp2TableDev[i]);
+}
+#endif
 
 }  // namespace sk

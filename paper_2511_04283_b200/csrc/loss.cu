@@ -18,17 +18,15 @@
 namespace sk {
 namespace {
 
-constexpr int kT = 16;           // output tile edge
-constexpr int kHalo = 5;         // 11-tap window
-constexpr int kIn = kT + 2 * kHalo;  // 26
+constexpr int kTX = 32;                 // output tile width
+constexpr int kTY = 16;                 // output tile height
+constexpr int kHalo = 5;                // 11-tap window
+constexpr int kInX = kTX + 2 * kHalo;   // 42
+constexpr int kInY = kTY + 2 * kHalo;   // 26
+constexpr int kHX = 4;                  // horizontal outputs per thread (register sliding window)
+constexpr int kVY = 2;                  // vertical outputs per thread
 
 __constant__ float c_gauss[11];
-
-// gt sample: u8 HWC decoded as byte / 255.0f (png_io.cpp:64), or f32 HWC.
-__device__ __forceinline__ float gt_at(const void* gt, bool u8, size_t p, int ch) {
-  if (u8) return __fdiv_rn((float)static_cast<const uint8_t*>(gt)[p * 3 + ch], 255.0f);
-  return static_cast<const float*>(gt)[p * 3 + ch];
-}
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -42,79 +40,109 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return s;
 }
 
-// Kernel A. partials: planar [3 maps][3 ch][H][W]; also writes the L1 part of
+// Kernel A (per 32x16 output tile, 256 threads, channels in turn): stage x and
+// y with a 5-pixel zero halo; horizontal pass with a register sliding window
+// (4 adjacent outputs per thread, 14 loads instead of 44) producing the five
+// moments x, y, x^2, y^2, xy; vertical pass, 2 outputs per thread; SSIM map
+// and the three per-pixel partials of ssim_with_grad (metrics.hpp:104-114).
+// partials: planar [3 maps][3 ch][H][W]; also writes the L1 part of
 // dL/dimage into dimage (planar [3][H][W]).
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ img, const void* __restrict__ gt,
                                                        bool gt_u8, int W, int H, float nrm, float lambda,
                                                        float inv_n, bool want_grad, float* __restrict__ partials,
                                                        float* __restrict__ dimage, double* __restrict__ sums) {
-  __shared__ float s_x[kIn][kIn + 1];
-  __shared__ float s_y[kIn][kIn + 1];
-  __shared__ float s_h[5][kIn][kT + 1];
+  __shared__ float s_x[kInY][kInX + 1];
+  __shared__ float s_y[kInY][kInX + 1];
+  __shared__ float s_h[5][kInY][kTX + 1];
+  __shared__ float s_u8[256];
   __shared__ double s_red[8];
-  const int tx0 = blockIdx.x * kT, ty0 = blockIdx.y * kT;
-  const int lx = threadIdx.x % kT, ly = threadIdx.x / kT;
-  const int px = tx0 + lx, py = ty0 + ly;
-  const bool inside = px < W && py < H;
+  const int tx0 = blockIdx.x * kTX, ty0 = blockIdx.y * kTY;
+  const int t = threadIdx.x;
   const size_t plane = (size_t)W * H;
+  // byte / 255.0f (png_io.cpp:64) as a table: one exact division per value
+  for (int i = t; i < 256; i += blockDim.x) s_u8[i] = __fdiv_rn((float)i, 255.0f);
+  // vertical-pass ownership: column vx, rows vy0, vy0 + 1
+  const int vx = t % kTX, vy0 = (t / kTX) * kVY;
   double l1 = 0.0, ss = 0.0, sq = 0.0;
   for (int ch = 0; ch < 3; ++ch) {
     __syncthreads();
-    for (int i = threadIdx.x; i < kIn * kIn; i += blockDim.x) {
-      const int iy = i / kIn, ix = i % kIn;
+    for (int i = t; i < kInX * kInY; i += blockDim.x) {
+      const int iy = i / kInX, ix = i % kInX;
       const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
       float xv = 0.0f, yv = 0.0f;
       if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
         const size_t p = (size_t)gy * W + gx;
         xv = img[ch * plane + p];
-        yv = gt_at(gt, gt_u8, p, ch);
+        yv = gt_u8 ? s_u8[static_cast<const uint8_t*>(gt)[p * 3 + ch]] : static_cast<const float*>(gt)[p * 3 + ch];
       }
       s_x[iy][ix] = xv;
       s_y[iy][ix] = yv;
     }
     __syncthreads();
-    // horizontal pass over all kIn rows, kT output columns
-    for (int i = threadIdx.x; i < kIn * kT; i += blockDim.x) {
-      const int iy = i / kT, ox = i % kT;
-      float a = 0.f, b = 0.f, cxx = 0.f, cyy = 0.f, cxy = 0.f;
+    // horizontal: 26 rows x 8 groups of 4 columns
+    if (t < kInY * (kTX / kHX)) {
+      const int iy = t / (kTX / kHX), ox = (t % (kTX / kHX)) * kHX;
+      float xv[kHX + 10], yv[kHX + 10];
 #pragma unroll
-      for (int o = 0; o < 11; ++o) {
-        const float w = c_gauss[o];
-        const float xv = s_x[iy][ox + o], yv = s_y[iy][ox + o];
-        a += w * xv;
-        b += w * yv;
-        cxx += w * (xv * xv);
-        cyy += w * (yv * yv);
-        cxy += w * (xv * yv);
+      for (int k = 0; k < kHX + 10; ++k) {
+        xv[k] = s_x[iy][ox + k];
+        yv[k] = s_y[iy][ox + k];
       }
-      s_h[0][iy][ox] = a;
-      s_h[1][iy][ox] = b;
-      s_h[2][iy][ox] = cxx;
-      s_h[3][iy][ox] = cyy;
-      s_h[4][iy][ox] = cxy;
+      float acc[5][kHX];
+#pragma unroll
+      for (int m = 0; m < 5; ++m)
+#pragma unroll
+        for (int c = 0; c < kHX; ++c) acc[m][c] = 0.0f;
+#pragma unroll
+      for (int k = 0; k < kHX + 10; ++k) {
+        const float xx = xv[k] * xv[k], yy = yv[k] * yv[k], xy = xv[k] * yv[k];
+#pragma unroll
+        for (int c = 0; c < kHX; ++c) {
+          const int o = k - c;
+          if (o >= 0 && o < 11) {
+            const float w = c_gauss[o];
+            acc[0][c] += w * xv[k];
+            acc[1][c] += w * yv[k];
+            acc[2][c] += w * xx;
+            acc[3][c] += w * yy;
+            acc[4][c] += w * xy;
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 5; ++m)
+#pragma unroll
+        for (int c = 0; c < kHX; ++c) s_h[m][iy][ox + c] = acc[m][c];
     }
     __syncthreads();
-    float m[5];
+    float mom[5][kVY];
 #pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      float s = 0.f;
+    for (int m = 0; m < 5; ++m) {
+      float col[kVY + 10];
 #pragma unroll
-      for (int o = 0; o < 11; ++o) s += c_gauss[o] * s_h[k][ly + o][lx];
-      m[k] = s;
+      for (int k = 0; k < kVY + 10; ++k) col[k] = s_h[m][vy0 + k][vx];
+#pragma unroll
+      for (int r = 0; r < kVY; ++r) {
+        float a = 0.0f;
+#pragma unroll
+        for (int o = 0; o < 11; ++o) a += c_gauss[o] * col[r + o];
+        mom[m][r] = a;
+      }
     }
-    if (inside) {
-      const float mx = m[0], my = m[1];
+#pragma unroll
+    for (int r = 0; r < kVY; ++r) {
+      const int px = tx0 + vx, py = ty0 + vy0 + r;
+      if (px >= W || py >= H) continue;
+      const float mx = mom[0][r], my = mom[1][r];
       const float C1 = (float)(0.01 * 0.01), C2 = (float)(0.03 * 0.03);
       const float a1 = 2.0f * mx * my + C1;
-      const float a2 = 2.0f * (m[4] - mx * my) + C2;
+      const float a2 = 2.0f * (mom[4][r] - mx * my) + C2;
       const float b1 = mx * mx + my * my + C1;
-      const float b2 = (m[2] - mx * mx) + (m[3] - my * my) + C2;
+      const float b2 = (mom[2][r] - mx * mx) + (mom[3][r] - my * my) + C2;
       const float s = (a1 * a2) / (b1 * b2);
       ss += (double)s;
       const size_t p = (size_t)py * W + px;
-      const float xv = s_x[ly + kHalo][lx + kHalo];
-      const float yv = s_y[ly + kHalo][lx + kHalo];
-      const float diff = xv - yv;
+      const float diff = s_x[vy0 + r + kHalo][vx + kHalo] - s_y[vy0 + r + kHalo][vx + kHalo];
       l1 += (double)fabsf(diff);
       sq += (double)diff * (double)diff;
       if (want_grad) {
@@ -131,29 +159,31 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   const double t_l1 = block_sum(l1, s_red);
   const double t_ss = block_sum(ss, s_red);
   const double t_sq = block_sum(sq, s_red);
-  if (threadIdx.x == 0) {
+  if (t == 0) {
     atomicAdd(&sums[0], t_l1);
     atomicAdd(&sums[1], t_ss);
     atomicAdd(&sums[2], t_sq);
   }
 }
 
-// Kernel B: filter the partials and finish dL/dimage.
+// Kernel B: filter the three partials (same tiling) and finish dL/dimage:
+// d -= lambda (filt(u_mu) + filt(u_mxy) y + filt(u_mxx) 2 x).
 __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ img, const void* __restrict__ gt,
                                                        bool gt_u8, int W, int H, float lambda,
                                                        const float* __restrict__ partials,
                                                        float* __restrict__ dimage) {
-  __shared__ float s_u[3][kIn][kIn + 1];
-  __shared__ float s_h[3][kIn][kT + 1];
-  const int tx0 = blockIdx.x * kT, ty0 = blockIdx.y * kT;
-  const int lx = threadIdx.x % kT, ly = threadIdx.x / kT;
-  const int px = tx0 + lx, py = ty0 + ly;
-  const bool inside = px < W && py < H;
+  __shared__ float s_u[3][kInY][kInX + 1];
+  __shared__ float s_h[3][kInY][kTX + 1];
+  __shared__ float s_u8[256];
+  const int tx0 = blockIdx.x * kTX, ty0 = blockIdx.y * kTY;
+  const int t = threadIdx.x;
   const size_t plane = (size_t)W * H;
+  for (int i = t; i < 256; i += blockDim.x) s_u8[i] = __fdiv_rn((float)i, 255.0f);
+  const int vx = t % kTX, vy0 = (t / kTX) * kVY;
   for (int ch = 0; ch < 3; ++ch) {
     __syncthreads();
-    for (int i = threadIdx.x; i < kIn * kIn; i += blockDim.x) {
-      const int iy = i / kIn, ix = i % kIn;
+    for (int i = t; i < kInX * kInY; i += blockDim.x) {
+      const int iy = i / kInX, ix = i % kInX;
       const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
       const bool ok = gx >= 0 && gx < W && gy >= 0 && gy < H;
       const size_t p = (size_t)gy * W + gx;
@@ -161,30 +191,45 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
       for (int k = 0; k < 3; ++k) s_u[k][iy][ix] = ok ? partials[(k * 3 + ch) * plane + p] : 0.0f;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < kIn * kT; i += blockDim.x) {
-      const int iy = i / kT, ox = i % kT;
+    if (t < kInY * (kTX / kHX)) {
+      const int iy = t / (kTX / kHX), ox = (t % (kTX / kHX)) * kHX;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        float s = 0.f;
+      for (int m = 0; m < 3; ++m) {
+        float v[kHX + 10];
 #pragma unroll
-        for (int o = 0; o < 11; ++o) s += c_gauss[o] * s_u[k][iy][ox + o];
-        s_h[k][iy][ox] = s;
+        for (int k = 0; k < kHX + 10; ++k) v[k] = s_u[m][iy][ox + k];
+#pragma unroll
+        for (int c = 0; c < kHX; ++c) {
+          float a = 0.0f;
+#pragma unroll
+          for (int o = 0; o < 11; ++o) a += c_gauss[o] * v[c + o];
+          s_h[m][iy][ox + c] = a;
+        }
       }
     }
     __syncthreads();
-    if (inside) {
-      float f[3];
+    float f[3][kVY];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        float s = 0.f;
+    for (int m = 0; m < 3; ++m) {
+      float col[kVY + 10];
 #pragma unroll
-        for (int o = 0; o < 11; ++o) s += c_gauss[o] * s_h[k][ly + o][lx];
-        f[k] = s;
+      for (int k = 0; k < kVY + 10; ++k) col[k] = s_h[m][vy0 + k][vx];
+#pragma unroll
+      for (int r = 0; r < kVY; ++r) {
+        float a = 0.0f;
+#pragma unroll
+        for (int o = 0; o < 11; ++o) a += c_gauss[o] * col[r + o];
+        f[m][r] = a;
       }
+    }
+#pragma unroll
+    for (int r = 0; r < kVY; ++r) {
+      const int px = tx0 + vx, py = ty0 + vy0 + r;
+      if (px >= W || py >= H) continue;
       const size_t p = (size_t)py * W + px;
       const float xv = img[ch * plane + p];
-      const float yv = gt_at(gt, gt_u8, p, ch);
-      const float g = f[0] + f[1] * yv + f[2] * 2.0f * xv;
+      const float yv = gt_u8 ? s_u8[static_cast<const uint8_t*>(gt)[p * 3 + ch]] : static_cast<const float*>(gt)[p * 3 + ch];
+      const float g = f[0][r] + f[1][r] * yv + f[2][r] * 2.0f * xv;
       dimage[ch * plane + p] = dimage[ch * plane + p] - lambda * g;
     }
   }
@@ -220,7 +265,7 @@ void launch_loss(sk_ctx* ctx, sk_frame* f, const void* gt, bool gt_u8, float lam
   float* dimage = want_grad ? ensure<float>(f->dimage, 3 * plane) : nullptr;
   double* sums = ensure<double>(ctx->scalars, 4);
   SK_CUDA(cudaMemsetAsync(sums, 0, 4 * sizeof(double), ctx->stream));
-  const dim3 grid((W + kT - 1) / kT, (H + kT - 1) / kT);
+  const dim3 grid((W + kTX - 1) / kTX, (H + kTY - 1) / kTY);
   const float nrm = 1.0f / (3.0f * (float)W * (float)H);
   const float inv_n = 1.0f / (3.0f * (float)plane);
   ssim_fwd_kernel<<<grid, 256, 0, ctx->stream>>>(f->image.as<float>(), gt, gt_u8, W, H, nrm, lambda, inv_n, want_grad,

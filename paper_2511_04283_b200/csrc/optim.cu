@@ -41,7 +41,8 @@ struct Stats {
 template <int DEG, int GS>
 __device__ __forceinline__ void project_backward_one(const float* __restrict__ p, int64_t stride, int64_t i,
                                                      const CamParams& cam, const float dmu2d[2], const float dcov[2][2],
-                                                     const float dcol[3], float dop, float* grad) {
+                                                     const float dcol[3], float dop, float* grad,
+                                                     const float* s_exp2) {
   constexpr int NSH = (DEG + 1) * (DEG + 1);
   const float mu[3] = {p[0 * stride + i], p[1 * stride + i], p[2 * stride + i]};
   const float* R = cam.r;
@@ -59,7 +60,8 @@ __device__ __forceinline__ void project_backward_one(const float* __restrict__ p
     for (int j = 0; j < 3; ++j) m[a][j] = (J[a][0] * R[j] + J[a][1] * R[3 + j]) + J[a][2] * R[6 + j];
   // rotation / scale
   const float q_in[4] = {p[3 * stride + i], p[4 * stride + i], p[5 * stride + i], p[6 * stride + i]};
-  const float s[3] = {det_expf(p[7 * stride + i]), det_expf(p[8 * stride + i]), det_expf(p[9 * stride + i])};
+  const float s[3] = {det_expf(p[7 * stride + i], s_exp2), det_expf(p[8 * stride + i], s_exp2),
+                      det_expf(p[9 * stride + i], s_exp2)};
   const float n2 = ((q_in[0] * q_in[0] + q_in[1] * q_in[1]) + q_in[2] * q_in[2]) + q_in[3] * q_in[3];
   const float nq = sqrtf(n2);
   const float w = q_in[0] / nq, x = q_in[1] / nq, y = q_in[2] / nq, z = q_in[3] / nq;
@@ -85,7 +87,7 @@ __device__ __forceinline__ void project_backward_one(const float* __restrict__ p
     for (int b = 0; b < 3; ++b) S[a][b] = (M[a][0] * M[b][0] + M[a][1] * M[b][1]) + M[a][2] * M[b][2];
 
   // opacity (camera.hpp:171-172)
-  const float sig = det_sigmoidf(p[SK_COMP_OPACITY * stride + i]);
+  const float sig = det_sigmoidf(p[SK_COMP_OPACITY * stride + i], s_exp2);
   grad[SK_COMP_OPACITY * GS] = dop * sig * (1.0f - sig);
 
   // colour (camera.hpp:175-182, sh.hpp:93-114)
@@ -309,17 +311,20 @@ __device__ __forceinline__ void accumulate_stats(const Stats& st, int64_t i, int
 // MODE 0: gradients -> grads buffer (+ stats). MODE 1: fused Adam (+ stats).
 constexpr int kPbThreads = 128;
 
-// Phase 1 computes the Gaussian's gradients into this thread's column of a
-// shared-memory tile (conflict-free: column = threadIdx.x) instead of holding
-// 59 live registers; phase 2 streams params / m / v in batches of 8
-// components so 24 independent loads per thread are in flight.
-template <int DEG, int MODE>
+// K9: one thread per Gaussian computes all parameter gradients into its
+// column of a shared-memory tile (conflict-free: column = threadIdx.x, so no
+// 59-register live range) and the tile is written back as coalesced rows of the
+// planar gradient buffer; culled Gaussians get zeros (SceneGrads::init).
+template <int DEG>
 __global__ void __launch_bounds__(kPbThreads, 4) project_bwd_kernel(
-    float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ radius,
+    const float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ radius,
     const float4* __restrict__ conic4, const float* __restrict__ bg, int64_t gstride, float* __restrict__ grads,
-    float* __restrict__ am, float* __restrict__ av, AdamParams ap, Stats st, bool do_stats) {
+    Stats st, bool do_stats) {
   constexpr int NC = 11 + 3 * (DEG + 1) * (DEG + 1);
   __shared__ float s_grad[NC * kPbThreads];
+  __shared__ float s_exp2[64];
+  stage_exp2_table(s_exp2);
+  __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * kPbThreads + threadIdx.x;
   if (i >= n) return;
   float* g = s_grad + threadIdx.x;  // component c at g[c * kPbThreads]
@@ -327,7 +332,7 @@ __global__ void __launch_bounds__(kPbThreads, 4) project_bwd_kernel(
   if (rad > 0.0f) {
     float dmu2d[2], dcov[2][2], dcol[3], dop, absg[2];
     load_blend(bg, gstride, i, dmu2d, dcov, conic4[i], dcol, dop, absg);
-    project_backward_one<DEG, kPbThreads>(params, stride, i, cam, dmu2d, dcov, dcol, dop, g);
+    project_backward_one<DEG, kPbThreads>(params, stride, i, cam, dmu2d, dcov, dcol, dop, g, s_exp2);
     if (do_stats) {
       const float gmu[3] = {g[0], g[kPbThreads], g[2 * kPbThreads]};
       accumulate_stats(st, i, stride, dmu2d, absg, gmu, rad, (float)cam.width / 2.0f, (float)cam.height / 2.0f);
@@ -336,53 +341,64 @@ __global__ void __launch_bounds__(kPbThreads, 4) project_bwd_kernel(
 #pragma unroll
     for (int c = 0; c < NC; ++c) g[c * kPbThreads] = 0.0f;
   }
-  if (MODE == 0) {
 #pragma unroll
-    for (int c = 0; c < NC; ++c) grads[c * stride + i] = g[c * kPbThreads];
-    return;
-  }
-  constexpr int B = 8;
-#pragma unroll
-  for (int c0 = 0; c0 < NC; c0 += B) {
-    float pv[B], mv[B], vv[B];
-#pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int c = c0 + u;
-      if (c < NC && ap.active[comp_group(c)]) {
-        pv[u] = params[c * stride + i];
-        mv[u] = am[c * stride + i];
-        vv[u] = av[c * stride + i];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int c = c0 + u;
-      const int gidx = comp_group(c);
-      if (c < NC && ap.active[gidx]) {
-        adam_update(pv[u], mv[u], vv[u], g[c * kPbThreads], ap.lr[gidx], ap.bc1[gidx], ap.bc2[gidx]);
-        params[c * stride + i] = pv[u];
-        am[c * stride + i] = mv[u];
-        av[c * stride + i] = vv[u];
-      }
-    }
-  }
+  for (int c = 0; c < NC; ++c) grads[c * stride + i] = g[c * kPbThreads];
 }
 
-// Dense Adam over the grads buffer (SceneOptimizer::step).
-__global__ void adam_kernel(float* __restrict__ params, const float* __restrict__ grads, float* __restrict__ am,
-                            float* __restrict__ av, int64_t stride, int64_t n, int comps, AdamParams ap) {
-  const int64_t total = (int64_t)comps * n;
+__device__ __forceinline__ float pick(const float (&a)[6], int gidx) {
+  float v = a[0];
+  v = gidx == 1 ? a[1] : v;
+  v = gidx == 2 ? a[2] : v;
+  v = gidx == 3 ? a[3] : v;
+  v = gidx == 4 ? a[4] : v;
+  v = gidx == 5 ? a[5] : v;
+  return v;
+}
+
+// K10: dense Adam over every component of every Gaussian (SceneOptimizer::step
+// adam.hpp:124-143), float4-vectorised along the Gaussian axis (capacity is a
+// multiple of 4, rows are 16-byte aligned), grid-stride. HBM-bound:
+// 28 B per scalar (params, m, v read + written, gradient read).
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, const float* __restrict__ grads,
+                                                   float* __restrict__ am, float* __restrict__ av, int64_t stride,
+                                                   int64_t n, int comps, AdamParams ap) {
+  const int64_t nq = (n + 3) / 4;
+  const int64_t total = (int64_t)comps * nq;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e / n);
-    const int64_t i = e - (int64_t)c * n;
+    const int c = (int)(e / nq);
+    const int64_t i = (e - (int64_t)c * nq) * 4;
     const int gidx = comp_group(c);
-    if (!ap.active[gidx]) continue;
+    int active = ap.active[0];
+    active = gidx == 1 ? ap.active[1] : active;
+    active = gidx == 2 ? ap.active[2] : active;
+    active = gidx == 3 ? ap.active[3] : active;
+    active = gidx == 4 ? ap.active[4] : active;
+    active = gidx == 5 ? ap.active[5] : active;
+    if (!active) continue;
+    const float lr = pick(ap.lr, gidx), bc1 = pick(ap.bc1, gidx), bc2 = pick(ap.bc2, gidx);
     const int64_t o = (int64_t)c * stride + i;
-    float pv = params[o], mv = am[o], vv = av[o];
-    adam_update(pv, mv, vv, grads[o], ap.lr[gidx], ap.bc1[gidx], ap.bc2[gidx]);
-    params[o] = pv;
-    am[o] = mv;
-    av[o] = vv;
+    if (i + 3 < n) {
+      float4 p = *reinterpret_cast<const float4*>(params + o);
+      float4 m = *reinterpret_cast<const float4*>(am + o);
+      float4 v = *reinterpret_cast<const float4*>(av + o);
+      const float4 g = *reinterpret_cast<const float4*>(grads + o);
+      adam_update(p.x, m.x, v.x, g.x, lr, bc1, bc2);
+      adam_update(p.y, m.y, v.y, g.y, lr, bc1, bc2);
+      adam_update(p.z, m.z, v.z, g.z, lr, bc1, bc2);
+      adam_update(p.w, m.w, v.w, g.w, lr, bc1, bc2);
+      *reinterpret_cast<float4*>(params + o) = p;
+      *reinterpret_cast<float4*>(am + o) = m;
+      *reinterpret_cast<float4*>(av + o) = v;
+    } else {
+      for (int64_t k = i; k < n; ++k) {
+        const int64_t ok = (int64_t)c * stride + k;
+        float p = params[ok], m = am[ok], v = av[ok];
+        adam_update(p, m, v, grads[ok], lr, bc1, bc2);
+        params[ok] = p;
+        am[ok] = m;
+        av[ok] = v;
+      }
+    }
   }
 }
 
@@ -412,20 +428,19 @@ Stats make_stats(sk_scene* s) {
   return st;
 }
 
-template <int MODE>
-void launch_pb(sk_ctx* ctx, sk_scene* s, sk_frame* f, const AdamParams& ap, bool do_stats) {
+void launch_pb(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stats) {
   const CamParams cp = make_cam_params(f->camera);
-  const unsigned grid = (unsigned)((s->n + 127) / 128);
+  const unsigned grid = (unsigned)((s->n + kPbThreads - 1) / kPbThreads);
   auto go = [&](auto kern) {
-    kern<<<grid, 128, 0, ctx->stream>>>(s->params.as<float>(), s->capacity, s->n, cp, f->radius.as<float>(),
-                                        f->conic4.as<float4>(), f->bgrads.as<float>(), f->n, s->grads.as<float>(),
-                                        s->adam_m.as<float>(), s->adam_v.as<float>(), ap, make_stats(s), do_stats);
+    kern<<<grid, kPbThreads, 0, ctx->stream>>>(s->params.as<float>(), s->capacity, s->n, cp, f->radius.as<float>(),
+                                               f->conic4.as<float4>(), f->bgrads.as<float>(), f->n,
+                                               s->grads.as<float>(), make_stats(s), do_stats);
   };
   switch (s->sh_degree) {
-    case 0: go(project_bwd_kernel<0, MODE>); break;
-    case 1: go(project_bwd_kernel<1, MODE>); break;
-    case 2: go(project_bwd_kernel<2, MODE>); break;
-    default: go(project_bwd_kernel<3, MODE>); break;
+    case 0: go(project_bwd_kernel<0>); break;
+    case 1: go(project_bwd_kernel<1>); break;
+    case 2: go(project_bwd_kernel<2>); break;
+    default: go(project_bwd_kernel<3>); break;
   }
   note_launch();
   SK_CUDA(cudaGetLastError());
@@ -474,27 +489,30 @@ void reset_score_table(sk_ctx* ctx, sk_scene* s) {
 
 void launch_project_backward(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stats) {
   ensure_optimizer_state(ctx, s);
-  AdamParams ap{};
-  launch_pb<0>(ctx, s, f, ap, do_stats);
-}
-
-void launch_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const LearningRates& lrs, float position_lr,
-                                  bool update_sh_rest, bool do_stats) {
-  ensure_optimizer_state(ctx, s);
-  const AdamParams ap = make_adam(s, lrs, position_lr, update_sh_rest);
-  launch_pb<1>(ctx, s, f, ap, do_stats);
+  launch_pb(ctx, s, f, do_stats);
 }
 
 void launch_adam(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float position_lr, bool update_sh_rest) {
   ensure_optimizer_state(ctx, s);
+  require(s->capacity % 4 == 0, "adam: scene capacity must be a multiple of 4");
   const AdamParams ap = make_adam(s, lrs, position_lr, update_sh_rest);
-  const int64_t total = (int64_t)s->comps * s->n;
+  const int64_t total = (int64_t)s->comps * ((s->n + 3) / 4);
   if (total == 0) return;
   const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
   adam_kernel<<<grid, 256, 0, ctx->stream>>>(s->params.as<float>(), s->grads.as<float>(), s->adam_m.as<float>(),
                                              s->adam_v.as<float>(), s->capacity, s->n, s->comps, ap);
   note_launch();
   SK_CUDA(cudaGetLastError());
+}
+
+// Single-GPU step: K9 into the gradient buffer, then the streaming K10. (A
+// single fused kernel keeps the gradients on chip but is instruction-bound at
+// the occupancy its 59-gradient live range allows; split, K10 runs at HBM
+// bandwidth.)
+void launch_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const LearningRates& lrs, float position_lr,
+                                  bool update_sh_rest, bool do_stats) {
+  launch_project_backward(ctx, s, f, do_stats);
+  launch_adam(ctx, s, lrs, position_lr, update_sh_rest);
 }
 
 }  // namespace sk

@@ -130,6 +130,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
                                                          float* __restrict__ radius_out, int* __restrict__ tiles_out,
                                                          int4* __restrict__ rect_out, float* __restrict__ astar_out,
                                                          uint32_t* __restrict__ key_out, uint32_t* __restrict__ err) {
+  __shared__ float s_exp2[64];
+  stage_exp2_table(s_exp2);
+  __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   auto culled = [&]() {
@@ -161,7 +164,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
   // covariance_3d (scene.hpp:88-96)
   const float qw_in = p[3 * stride + i], qx_in = p[4 * stride + i], qy_in = p[5 * stride + i],
               qz_in = p[6 * stride + i];
-  const float s0 = det_expf(p[7 * stride + i]), s1 = det_expf(p[8 * stride + i]), s2 = det_expf(p[9 * stride + i]);
+  const float s0 = det_expf(p[7 * stride + i], s_exp2), s1 = det_expf(p[8 * stride + i], s_exp2),
+              s2 = det_expf(p[9 * stride + i], s_exp2);
   if (!(isfinite(qw_in) && isfinite(qx_in) && isfinite(qy_in) && isfinite(qz_in) && isfinite(s0) && isfinite(s1) &&
         isfinite(s2))) {
     atomicOr(err, kErrCovNonFinite);
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
     rgb[ch] = rgb[ch] + 0.5f;
     rgb[ch] = (rgb[ch] < 0.0f) ? 0.0f : rgb[ch];
   }
-  const float opacity = det_sigmoidf(p[SK_COMP_OPACITY * stride + i]);
+  const float opacity = det_sigmoidf(p[SK_COMP_OPACITY * stride + i], s_exp2);
 
   BinOut bo;
   if (!bin_footprint(mx, my, c[0][0], c[0][1], c[1][0], c[1][1], inv00, inv01, inv11, opacity, bp.mode, bp.beta,

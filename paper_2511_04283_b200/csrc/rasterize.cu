@@ -4,23 +4,25 @@
 // centres, q = ((c00 dx) dx + ((2 c01) dx) dy) + (c11 dy) dy, skip q < 0,
 // alpha = min(0.99, o e^{-q/2}), skip alpha < 1/255, C += (T alpha) c,
 // T *= 1 - alpha, and the entry that takes T below 1e-4 is blended before the
-// pixel stops. One CTA per tile, one thread per pixel; the tile's list is
-// staged through shared memory in CTA-sized batches and the CTA stops loading
-// once every pixel has terminated. Compiled with -fmad=false and the shared
-// deterministic exp, so images, transmittance and footprint counts match the
-// CPU oracle bit for bit.
+// pixel stops. One CTA per tile; the tile's list is staged through shared
+// memory in CTA-sized batches and the CTA stops loading once every pixel has
+// terminated. Compiled with -fmad=false and the shared deterministic exp, so
+// images, transmittance and footprint counts match the CPU oracle bit for bit.
 //
-// Early reject: alpha >= 1/255 requires q <= 2 ln(255 o). Each staged entry
-// carries q_cut = 2 ln(255 o) + 0.02; for q > q_cut the reference's alpha is
-// below 1/255 by a 1% margin (far above the 2-ulp exp error), so skipping the
-// exponential there leaves every result bit-identical.
+// Exact early rejects. alpha >= 1/255 requires q <= 2 ln(255 o); each staged
+// entry carries q_cut = 2 ln(255 o) + 0.02 and the bounding box of the ellipse
+// {q <= q_cut} (widened by 1e-4 relative + 0.01 px). Outside q_cut the
+// reference's alpha is below 1/255 by a 1% margin (far above the 2-ulp exp
+// error), so skipping changes no result. Warps own 8-pixel-wide blocks of the
+// tile; a warp whose block misses an entry's box skips that entry with one
+// warp-uniform test instead of evaluating 32 pixels.
 //
 // K8 restates blend_backward (raster.hpp:281-355) as a reverse walk from each
 // pixel's last contributor (recorded by K6): T_before = T_after / (1 - alpha),
 // suffix accumulated in the reference's reverse order, capped entries feed
-// d_color only. Each thread owns PIX pixels of its tile (rows y, y + TS/PIX,
-// ...), sums their partials per Gaussian in registers, and the warp then
-// butterfly-reduces the 11 partials with shuffles (skipped when no lane
+// d_color only. Each thread owns PIX pixels (rows y, y+4, ...) of its warp's
+// 8 x 4·PIX block, sums their partials per Gaussian in registers, and the warp
+// then butterfly-reduces the 11 partials with shuffles (skipped when no lane
 // contributes); lanes 0..10 issue one global atomic each.
 #include "state.h"
 
@@ -32,22 +34,63 @@ __device__ __forceinline__ float qcut_of(float opacity) {
   return a > 1.0f ? 2.0f * __logf(a) + 0.02f : -1.0f;
 }
 
+// Staged entry: position + q_cut, conic + opacity, box of {q <= q_cut}.
+__device__ __forceinline__ void stage_entry(float2 mu, float4 co, float4& xyq, float4& bb) {
+  const float qc = qcut_of(co.w);
+  xyq = make_float4(mu.x, mu.y, qc, 0.0f);
+  if (qc <= 0.0f) {
+    bb = make_float4(1.0f, -1.0f, 1.0f, -1.0f);  // empty: never contributes
+    return;
+  }
+  const float det = co.x * co.z - co.y * co.y;
+  if (!(det > 0.0f && co.x > 0.0f && co.z > 0.0f)) {
+    bb = make_float4(-3.0e38f, 3.0e38f, -3.0e38f, 3.0e38f);  // no culling
+    return;
+  }
+  const float ex = sqrtf(qc * co.z / det) * 1.0001f + 0.01f;
+  const float ey = sqrtf(qc * co.x / det) * 1.0001f + 0.01f;
+  bb = make_float4(mu.x - ex, mu.x + ex, mu.y - ey, mu.y + ey);
+}
+
+template <int TS, int PIX>
+struct WarpBlock {
+  static constexpr int kWarpsX = TS / 8;
+  int lx, ly0;    // pixel of k = 0 within the tile
+  float x0, x1, y0, y1;  // the warp's pixel-centre rectangle (absolute)
+  __device__ WarpBlock(int tx, int ty) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int bx = (w % kWarpsX) * 8, by = (w / kWarpsX) * (4 * PIX);
+    lx = bx + (l & 7);
+    ly0 = by + (l >> 3);
+    x0 = (float)(tx * TS + bx);
+    x1 = x0 + 7.0f;
+    y0 = (float)(ty * TS + by);
+    y1 = y0 + (float)(4 * PIX - 1);
+  }
+  __device__ bool misses(const float4& bb) const { return bb.y < x0 || bb.x > x1 || bb.w < y0 || bb.z > y1; }
+};
+
 template <int TS, bool COUNT>
 __global__ void __launch_bounds__(TS* TS) blend_fwd_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry,
     const uint8_t* __restrict__ mask, int* __restrict__ counts) {
-  constexpr int B = TS * TS;
+  constexpr int NTH = TS * TS;                 // one thread per pixel
+  constexpr int B = NTH > 256 ? 256 : NTH;     // staged entries per batch
   __shared__ float4 s_xyq[B];
   __shared__ float4 s_co[B];
+  __shared__ float4 s_bb[B];
   __shared__ float4 s_rgb[COUNT ? 1 : B];
   __shared__ uint32_t s_id[COUNT ? B : 1];
+  __shared__ float s_exp2[64];
+  stage_exp2_table(s_exp2);  // published by the first __syncthreads_count below
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int px = tx * TS + (int)(threadIdx.x % TS);
-  const int py = ty * TS + (int)(threadIdx.x / TS);
+  const WarpBlock<TS, 1> wb(tx, ty);
+  const int px = tx * TS + wb.lx;
+  const int py = ty * TS + wb.ly0;
   const bool inside = px < W && py < H;
   const int2 range = ranges[tile];
   const float fpx = (float)px, fpy = (float)py;
@@ -61,14 +104,16 @@ __global__ void __launch_bounds__(TS* TS) blend_fwd_kernel(
   bool done = COUNT ? !masked : !inside;
 
   for (int b0 = range.x; b0 < range.y; b0 += B) {
-    if (__syncthreads_count(done) == B) break;
+    if (__syncthreads_count(done) == NTH) break;
     const int i = b0 + (int)threadIdx.x;
-    if (i < range.y) {
+    if ((int)threadIdx.x < B && i < range.y) {
       const uint32_t g = pair_val[i];
-      const float2 mu = mean2d[g];
       const float4 co = conic_op[g];
-      s_xyq[threadIdx.x] = make_float4(mu.x, mu.y, qcut_of(co.w), 0.0f);
+      float4 xyq, bb;
+      stage_entry(mean2d[g], co, xyq, bb);
+      s_xyq[threadIdx.x] = xyq;
       s_co[threadIdx.x] = co;
+      s_bb[threadIdx.x] = bb;
       if (!COUNT) s_rgb[threadIdx.x] = rgbd[g];
       if (COUNT) s_id[threadIdx.x] = g;
     }
@@ -76,13 +121,15 @@ __global__ void __launch_bounds__(TS* TS) blend_fwd_kernel(
     const int cnt = min(B, range.y - b0);
     if (!done) {
       for (int j = 0; j < cnt; ++j) {
+        if (wb.misses(s_bb[j])) continue;  // warp-uniform
         const float4 mq = s_xyq[j];
         const float4 co = s_co[j];
         const float dx = fpx - mq.x;
         const float dy = fpy - mq.y;
         const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
-        if (q < 0.0f || q > mq.z) continue;
-        float alpha = co.w * det_expf(-0.5f * q);
+        if (!(q >= 0.0f && q <= mq.z)) continue;
+        // -0.5 q lies in [-q_cut/2, 0], inside det_expf's core range
+        float alpha = co.w * det_expf_core(-0.5f * q, s_exp2);
         alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
         if (alpha < kAlphaMin) continue;
         if (COUNT) {
@@ -133,18 +180,20 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
     const float* __restrict__ final_t, const int* __restrict__ last_entry, const float* __restrict__ dimage,
     float* __restrict__ bgrads, int64_t gstride) {
   constexpr int NT = TS * TS / PIX;  // threads == batch size
-  constexpr int ROWS = TS / PIX;     // row stride between a thread's pixels
   __shared__ float4 s_xyq[NT];
   __shared__ float4 s_co[NT];
+  __shared__ float4 s_bb[NT];
   __shared__ float4 s_rgb[NT];
   __shared__ uint32_t s_id[NT];
   __shared__ int s_max_last;
+  __shared__ float s_exp2[64];
+  stage_exp2_table(s_exp2);
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const WarpBlock<TS, PIX> wb(tx, ty);
   const int lane = threadIdx.x & 31;
-  const int px = tx * TS + (int)(threadIdx.x % TS);
-  const int py0 = ty * TS + (int)(threadIdx.x / TS);
+  const int px = tx * TS + wb.lx;
   const int2 range = ranges[tile];
   const float fpx = (float)px;
   const size_t plane = (size_t)W * H;
@@ -154,7 +203,7 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
   int my_last = 0;
 #pragma unroll
   for (int k = 0; k < PIX; ++k) {
-    const int py = py0 + k * ROWS;
+    const int py = ty * TS + wb.ly0 + 4 * k;
     fpy[k] = (float)py;
     T[k] = 1.0f;
     suffix[k] = 0.0f;
@@ -183,16 +232,19 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
     const int i = b0 + (int)threadIdx.x;
     if (i < b_end) {
       const uint32_t g = pair_val[i];
-      const float2 mu = mean2d[g];
       const float4 co = conic_op[g];
-      s_xyq[threadIdx.x] = make_float4(mu.x, mu.y, qcut_of(co.w), 0.0f);
+      float4 xyq, bb;
+      stage_entry(mean2d[g], co, xyq, bb);
+      s_xyq[threadIdx.x] = xyq;
       s_co[threadIdx.x] = co;
+      s_bb[threadIdx.x] = bb;
       s_rgb[threadIdx.x] = rgbd[g];
       s_id[threadIdx.x] = g;
     }
     __syncthreads();
     const int jmax = min(b_end, warp_last) - b0;  // warp-uniform
     for (int j = jmax - 1; j >= 0; --j) {
+      if (wb.misses(s_bb[j])) continue;  // warp-uniform
       const int idx = b0 + j;
       const float4 mq = s_xyq[j];
       const float4 co = s_co[j];
@@ -205,8 +257,8 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
         const float dx = fpx - mq.x;
         const float dy = fpy[k] - mq.y;
         const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
-        if (q < 0.0f || q > mq.z) continue;
-        const float ge = det_expf(-0.5f * q);
+        if (!(q >= 0.0f && q <= mq.z)) continue;
+        const float ge = det_expf_core(-0.5f * q, s_exp2);
         const float raw = co.w * ge;
         const bool capped = raw > kAlphaCap;
         const float alpha = capped ? kAlphaCap : raw;
@@ -214,10 +266,11 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
         contrib = true;
         const float4 c = s_rgb[j];
         const float one_m = 1.0f - alpha;
-        const float t_before = T[k] / one_m;
+        const float inv_one_m = __frcp_rn(one_m);  // tolerance path: one reciprocal, two products
+        const float t_before = T[k] * inv_one_m;
         T[k] = t_before;
         const float w = (c.x * d0[k] + c.y * d1[k]) + c.z * d2[k];
-        const float d_alpha = t_before * w - suffix[k] / one_m;
+        const float d_alpha = t_before * w - suffix[k] * inv_one_m;
         const float ta = t_before * alpha;
         suffix[k] = suffix[k] + ta * w;
         g_r += ta * d0[k];

@@ -122,6 +122,10 @@ namespace sk {
 
 constexpr int kBGradFields = 11;
 
+// Component stride of the planar scene buffers: a multiple of 4 so every
+// component row is 16-byte aligned for float4 access.
+inline int64_t round_capacity(int64_t n) { return ((n < 1 ? 1 : n) + 3) & ~int64_t(3); }
+
 // ---- launchers (each .cu file owns its kernels) ---------------------------
 // preprocess.cu
 void launch_preprocess(sk_ctx* ctx, const sk_scene* scene, const sk_camera& cam, sk_frame* f);
