@@ -70,14 +70,14 @@ struct WarpBlock {
   __device__ bool misses(const float4& bb) const { return bb.y < x0 || bb.x > x1 || bb.w < y0 || bb.z > y1; }
 };
 
-template <int TS, bool COUNT>
-__global__ void __launch_bounds__(TS* TS) blend_fwd_kernel(
+template <int TS, int PIX, bool COUNT>
+__global__ void __launch_bounds__(TS* TS / PIX, 8) blend_fwd_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry,
     const uint8_t* __restrict__ mask, int* __restrict__ counts) {
-  constexpr int NTH = TS * TS;                 // one thread per pixel
-  constexpr int B = NTH > 256 ? 256 : NTH;     // staged entries per batch
+  constexpr int NTH = TS * TS / PIX;        // threads; each owns PIX pixels
+  constexpr int B = TS * TS > 256 ? 256 : TS * TS;  // staged entries per batch
   __shared__ float4 s_xyq[B];
   __shared__ float4 s_co[B];
   __shared__ float4 s_bb[B];
@@ -88,46 +88,57 @@ __global__ void __launch_bounds__(TS* TS) blend_fwd_kernel(
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const WarpBlock<TS, 1> wb(tx, ty);
+  const WarpBlock<TS, PIX> wb(tx, ty);
   const int px = tx * TS + wb.lx;
-  const int py = ty * TS + wb.ly0;
-  const bool inside = px < W && py < H;
   const int2 range = ranges[tile];
-  const float fpx = (float)px, fpy = (float)py;
+  const float fpx = (float)px;
 
-  float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-  int n = 0, last = 0;
-  bool masked = false;
-  if (COUNT && inside) masked = mask[(size_t)py * W + px] != 0;
-  // K12 (count-only pass): only masked pixels can increment a counter, so
-  // unmasked pixels never traverse and fully unmasked tiles exit at once.
-  bool done = COUNT ? !masked : !inside;
+  float T[PIX], C0[PIX], C1[PIX], C2[PIX], fpy[PIX];
+  int n[PIX], last[PIX];
+  bool done[PIX];
+  bool all_done = true;
+#pragma unroll
+  for (int k = 0; k < PIX; ++k) {
+    const int py = ty * TS + wb.ly0 + 4 * k;
+    fpy[k] = (float)py;
+    T[k] = 1.0f;
+    C0[k] = C1[k] = C2[k] = 0.0f;
+    n[k] = last[k] = 0;
+    const bool inside = px < W && py < H;
+    // K12 (count-only pass): only masked pixels can increment a counter, so
+    // unmasked pixels never traverse and fully unmasked tiles exit at once.
+    done[k] = COUNT ? !(inside && mask[(size_t)py * W + px] != 0) : !inside;
+    all_done = all_done && done[k];
+  }
 
   for (int b0 = range.x; b0 < range.y; b0 += B) {
-    if (__syncthreads_count(done) == NTH) break;
-    const int i = b0 + (int)threadIdx.x;
-    if ((int)threadIdx.x < B && i < range.y) {
-      const uint32_t g = pair_val[i];
-      const float4 co = conic_op[g];
-      float4 xyq, bb;
-      stage_entry(mean2d[g], co, xyq, bb);
-      s_xyq[threadIdx.x] = xyq;
-      s_co[threadIdx.x] = co;
-      s_bb[threadIdx.x] = bb;
-      if (!COUNT) s_rgb[threadIdx.x] = rgbd[g];
-      if (COUNT) s_id[threadIdx.x] = g;
+    if (__syncthreads_count(all_done) == NTH) break;
+    for (int e = (int)threadIdx.x; e < B; e += NTH) {
+      const int i = b0 + e;
+      if (i < range.y) {
+        const uint32_t g = pair_val[i];
+        const float4 co = conic_op[g];
+        float4 xyq, bb;
+        stage_entry(mean2d[g], co, xyq, bb);
+        s_xyq[e] = xyq;
+        s_co[e] = co;
+        s_bb[e] = bb;
+        if (!COUNT) s_rgb[e] = rgbd[g];
+        if (COUNT) s_id[e] = g;
+      }
     }
     __syncthreads();
     const int cnt = min(B, range.y - b0);
-    if (!done) {
-      for (int j = 0; j < cnt; ++j) {
-        if (wb.misses(s_bb[j])) continue;  // warp-uniform
-        const float4 mq = s_xyq[j];
-        const float4 co = s_co[j];
+    for (int j = 0; j < cnt && !all_done; ++j) {
+      if (wb.misses(s_bb[j])) continue;  // warp-uniform
+      const float4 mq = s_xyq[j];
+      const float4 co = s_co[j];
+#pragma unroll
+      for (int k = 0; k < PIX; ++k) {
         const float dx = fpx - mq.x;
-        const float dy = fpy - mq.y;
+        const float dy = fpy[k] - mq.y;
         const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
-        if (!(q >= 0.0f && q <= mq.z)) continue;
+        if (done[k] || !(q >= 0.0f && q <= mq.z)) continue;
         // -0.5 q lies in [-q_cut/2, 0], inside det_expf's core range
         float alpha = co.w * det_expf_core(-0.5f * q, s_exp2);
         alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
@@ -140,30 +151,36 @@ __global__ void __launch_bounds__(TS* TS) blend_fwd_kernel(
           if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&counts[id], __popc(peers));
         } else {
           const float4 c = s_rgb[j];
-          const float w = T * alpha;
-          C0 = C0 + w * c.x;
-          C1 = C1 + w * c.y;
-          C2 = C2 + w * c.z;
-          ++n;
-          last = b0 + j + 1;
+          const float w = T[k] * alpha;
+          C0[k] = C0[k] + w * c.x;
+          C1[k] = C1[k] + w * c.y;
+          C2[k] = C2[k] + w * c.z;
+          ++n[k];
+          last[k] = b0 + j + 1;
         }
-        T = T * (1.0f - alpha);
-        if (T < kTransmitMin) {
-          done = true;
-          break;
-        }
+        T[k] = T[k] * (1.0f - alpha);
+        if (T[k] < kTransmitMin) done[k] = true;
       }
+      bool ad = true;
+#pragma unroll
+      for (int k = 0; k < PIX; ++k) ad = ad && done[k];
+      all_done = ad;
     }
   }
-  if (!COUNT && inside) {
-    const size_t p = (size_t)py * W + px;
-    const size_t plane = (size_t)W * H;
-    image[p] = C0;
-    image[plane + p] = C1;
-    image[2 * plane + p] = C2;
-    final_t[p] = T;
-    n_contrib[p] = n;
-    last_entry[p] = last;
+  if (COUNT) return;
+#pragma unroll
+  for (int k = 0; k < PIX; ++k) {
+    const int py = ty * TS + wb.ly0 + 4 * k;
+    if (px < W && py < H) {
+      const size_t p = (size_t)py * W + px;
+      const size_t plane = (size_t)W * H;
+      image[p] = C0[k];
+      image[plane + p] = C1[k];
+      image[2 * plane + p] = C2[k];
+      final_t[p] = T[k];
+      n_contrib[p] = n[k];
+      last_entry[p] = last[k];
+    }
   }
 }
 
@@ -171,6 +188,13 @@ __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+__device__ __forceinline__ float select_field(const float (&v)[kBGradFields], int f) {
+  float r = v[0];
+#pragma unroll
+  for (int k = 1; k < kBGradFields; ++k) r = f == k ? v[k] : r;
+  return r;
 }
 
 template <int TS, int PIX>
@@ -225,6 +249,9 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
   __syncthreads();
   const int end = s_max_last;  // no pixel of the tile uses entries >= end
   const int warp_last = __reduce_max_sync(0xffffffffu, my_last);
+  float pend[kBGradFields];
+  uint32_t pend_id = 0;
+  bool has_pend = false;
 
   for (int b_end = end; b_end > range.x; b_end -= NT) {
     const int b0 = max(range.x, b_end - NT);
@@ -293,40 +320,43 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
         }
       }
       if (__any_sync(0xffffffffu, contrib)) {
-        g_mu0 = warp_sum(g_mu0);
-        g_mu1 = warp_sum(g_mu1);
-        g_c00 = warp_sum(g_c00);
-        g_c01 = warp_sum(g_c01);
-        g_c11 = warp_sum(g_c11);
-        g_r = warp_sum(g_r);
-        g_g = warp_sum(g_g);
-        g_b = warp_sum(g_b);
-        g_op = warp_sum(g_op);
-        g_a0 = warp_sum(g_a0);
-        g_a1 = warp_sum(g_a1);
-        if (lane < kBGradFields) {
-          float v;
-          switch (lane) {
-            case 0: v = g_mu0; break;
-            case 1: v = g_mu1; break;
-            case 2: v = g_c00; break;
-            case 3: v = g_c01; break;
-            case 4: v = g_c11; break;
-            case 5: v = g_r; break;
-            case 6: v = g_g; break;
-            case 7: v = g_b; break;
-            case 8: v = g_op; break;
-            case 9: v = g_a0; break;
-            default: v = g_a1; break;
+        const float gv[kBGradFields] = {g_mu0, g_mu1, g_c00, g_c01, g_c11, g_r, g_g, g_b, g_op, g_a0, g_a1};
+        if (has_pend) {
+          // Two entries per reduction: the xor-16 stage hands the pending
+          // entry to lanes 0-15 and the current one to lanes 16-31, then four
+          // butterfly stages finish both (55 shuffles for 22 values).
+          float keep[kBGradFields];
+#pragma unroll
+          for (int f = 0; f < kBGradFields; ++f) {
+            const float give = lane < 16 ? gv[f] : pend[f];
+            const float mine = lane < 16 ? pend[f] : gv[f];
+            keep[f] = mine + __shfl_xor_sync(0xffffffffu, give, 16);
           }
-          atomicAdd(&bgrads[(int64_t)lane * gstride + s_id[j]], v);
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+            for (int f = 0; f < kBGradFields; ++f) keep[f] += __shfl_xor_sync(0xffffffffu, keep[f], o);
+          const int fl = lane & 15;
+          if (fl < kBGradFields)
+            atomicAdd(&bgrads[(int64_t)fl * gstride + (lane < 16 ? pend_id : s_id[j])], select_field(keep, fl));
+          has_pend = false;
+        } else {
+#pragma unroll
+          for (int f = 0; f < kBGradFields; ++f) pend[f] = gv[f];
+          pend_id = s_id[j];
+          has_pend = true;
         }
       }
     }
   }
+  if (has_pend) {  // warp-uniform: flush the last unpaired entry
+#pragma unroll
+    for (int f = 0; f < kBGradFields; ++f) pend[f] = warp_sum(pend[f]);
+    if (lane < kBGradFields) atomicAdd(&bgrads[(int64_t)lane * gstride + pend_id], select_field(pend, lane));
+  }
 }
 
-template <int TS>
+template <int TS, int PIX>
 void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts) {
   const int tiles = f->tiles_x * f->tiles_y;
   auto* ranges = f->ranges.as<int2>();
@@ -334,11 +364,11 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
   const auto* co = f->conic_op.as<float4>();
   const auto* rgb = f->rgb_depth.as<float4>();
   if (mask)
-    blend_fwd_kernel<TS, true><<<tiles, TS * TS, 0, ctx->stream>>>(
+    blend_fwd_kernel<TS, PIX, true><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
         ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
         f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), mask, counts);
   else
-    blend_fwd_kernel<TS, false><<<tiles, TS * TS, 0, ctx->stream>>>(
+    blend_fwd_kernel<TS, PIX, false><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
         ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
         f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), nullptr, nullptr);
   note_launch();
@@ -359,9 +389,9 @@ void bwd_dispatch(sk_ctx* ctx, sk_frame* f) {
 void launch_blend_forward(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts) {
   if (f->tiles_x * f->tiles_y == 0) return;
   switch (f->tile_size) {
-    case 8: fwd_dispatch<8>(ctx, f, mask, counts); break;
-    case 16: fwd_dispatch<16>(ctx, f, mask, counts); break;
-    case 32: fwd_dispatch<32>(ctx, f, mask, counts); break;
+    case 8: fwd_dispatch<8, 1>(ctx, f, mask, counts); break;
+    case 16: fwd_dispatch<16, 2>(ctx, f, mask, counts); break;
+    case 32: fwd_dispatch<32, 4>(ctx, f, mask, counts); break;
     default: throw std::invalid_argument("tile_size must be 8, 16 or 32");
   }
   SK_CUDA(cudaGetLastError());
