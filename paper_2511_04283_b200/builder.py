@@ -22,7 +22,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
           "-I", INCLUDE, "-I", CSRC]
-FMA_OK = {"loss.cu", "optim.cu"}
+FMA_OK = {"loss.cu", "optim.cu", "rasterize_bwd.cu"}
 
 
 def nvcc() -> str:

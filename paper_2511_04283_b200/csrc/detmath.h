@@ -51,6 +51,31 @@ SK_HD float det_floorf(float x) {
 #endif
 }
 
+// Round-to-nearest products and sums that the device compiler never fuses
+// into FMAs, so functions written with them give the same bits in
+// translation units compiled with or without -fmad=false.
+SK_HD float rn_mul(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+SK_HD float rn_add(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+SK_HD float rn_sub(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fsub_rn(a, b);
+#else
+  return a - b;
+#endif
+}
+
 // 2^(j/64), j = 0..63, rounded to float (bit patterns, identical everywhere).
 #define SK_EXP2_TABLE                                                                                            \
   {0x3f800000u, 0x3f8164d2u, 0x3f82cd87u, 0x3f843a29u, 0x3f85aac3u, 0x3f871f62u, 0x3f88980fu, 0x3f8a14d5u,      \
@@ -72,15 +97,15 @@ static const uint32_t kExp2TableHost[64] = SK_EXP2_TABLE;
 // is exact for |k| < 2^14), e^r by a degree-3 polynomial, then the table and
 // one exact power-of-two scaling. `table` holds the 64 SK_EXP2_TABLE floats.
 SK_HD float det_expf_core(float x, const float* table) {
-  const float kf = det_floorf(x * 92.33248261689366f + 0.5f);  // 64 / ln2
+  const float kf = det_floorf(rn_add(rn_mul(x, 92.33248261689366f), 0.5f));  // 64 / ln2
   const int k = (int)kf;
-  const float r = (x - kf * 0.010833740234375f) - kf * -3.3155381258549027e-06f;
-  float p = r * 0.16666666666666666f + 0.5f;
-  p = p * r + 1.0f;
-  p = p * r + 1.0f;
+  const float r = rn_sub(rn_sub(x, rn_mul(kf, 0.010833740234375f)), rn_mul(kf, -3.3155381258549027e-06f));
+  float p = rn_add(rn_mul(r, 0.16666666666666666f), 0.5f);
+  p = rn_add(rn_mul(p, r), 1.0f);
+  p = rn_add(rn_mul(p, r), 1.0f);
   const int j = k & 63;
   const int e = (k - j) / 64;
-  return (table[j] * p) * bits_to_f32((uint32_t)(e + 127) << 23);
+  return rn_mul(rn_mul(table[j], p), bits_to_f32((uint32_t)(e + 127) << 23));
 }
 
 SK_HD const float* exp2_table() {

@@ -260,14 +260,23 @@ __device__ __forceinline__ int comp_group(int c) {
   return c < 3 ? 0 : (c < 7 ? 1 : (c < 10 ? 2 : (c < 11 ? 3 : (c < 14 ? 4 : 5))));
 }
 
+// Correctly rounded a / b for b > 0 finite. A zero dividend takes the IEEE
+// division's slow path (FCHK) on sm_100; +-0 / b == a, so select it instead.
+__device__ __forceinline__ float div_pos(float a, float b) {
+  const float q = __fdiv_rn(a == 0.0f ? 1.0f : a, b);
+  return a == 0.0f ? a : q;
+}
+
 // AdamGroup::step element update (adam.hpp:70-73), exactly in the reference's order.
 __device__ __forceinline__ void adam_update(float& param, float& m, float& v, float g, float lr, float bc1, float bc2) {
   const float b1 = (float)0.9, b2 = (float)0.999;
   m = __fadd_rn(__fmul_rn(b1, m), __fmul_rn(__fsub_rn(1.0f, b1), g));
   v = __fadd_rn(__fmul_rn(b2, v), __fmul_rn(__fmul_rn(__fsub_rn(1.0f, b2), g), g));
-  const float num = __fmul_rn(lr, __fdiv_rn(m, bc1));
-  const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(v, bc2)), (float)1e-15);
-  param = __fsub_rn(param, __fdiv_rn(num, den));
+  const float num = __fmul_rn(lr, div_pos(m, bc1));
+  const float vh = div_pos(v, bc2);
+  const float root = __fsqrt_rn(vh == 0.0f ? 1.0f : vh);
+  const float den = __fadd_rn(vh == 0.0f ? vh : root, (float)1e-15);
+  param = __fsub_rn(param, div_pos(num, den));
 }
 
 __device__ __forceinline__ void load_blend(const float* __restrict__ bg, int64_t gstride, int64_t i, float dmu2d[2],
@@ -345,60 +354,43 @@ __global__ void __launch_bounds__(kPbThreads, 4) project_bwd_kernel(
   for (int c = 0; c < NC; ++c) grads[c * stride + i] = g[c * kPbThreads];
 }
 
-__device__ __forceinline__ float pick(const float (&a)[6], int gidx) {
-  float v = a[0];
-  v = gidx == 1 ? a[1] : v;
-  v = gidx == 2 ? a[2] : v;
-  v = gidx == 3 ? a[3] : v;
-  v = gidx == 4 ? a[4] : v;
-  v = gidx == 5 ? a[5] : v;
-  return v;
-}
-
 // K10: dense Adam over every component of every Gaussian (SceneOptimizer::step
 // adam.hpp:124-143), float4-vectorised along the Gaussian axis (capacity is a
-// multiple of 4, rows are 16-byte aligned), grid-stride. HBM-bound:
-// 28 B per scalar (params, m, v read + written, gradient read).
-__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, const float* __restrict__ grads,
-                                                   float* __restrict__ am, float* __restrict__ av, int64_t stride,
-                                                   int64_t n, int comps, AdamParams ap) {
-  const int64_t nq = (n + 3) / 4;
-  const int64_t total = (int64_t)comps * nq;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e / nq);
-    const int64_t i = (e - (int64_t)c * nq) * 4;
-    const int gidx = comp_group(c);
-    int active = ap.active[0];
-    active = gidx == 1 ? ap.active[1] : active;
-    active = gidx == 2 ? ap.active[2] : active;
-    active = gidx == 3 ? ap.active[3] : active;
-    active = gidx == 4 ? ap.active[4] : active;
-    active = gidx == 5 ? ap.active[5] : active;
-    if (!active) continue;
-    const float lr = pick(ap.lr, gidx), bc1 = pick(ap.bc1, gidx), bc2 = pick(ap.bc2, gidx);
-    const int64_t o = (int64_t)c * stride + i;
-    if (i + 3 < n) {
-      float4 p = *reinterpret_cast<const float4*>(params + o);
-      float4 m = *reinterpret_cast<const float4*>(am + o);
-      float4 v = *reinterpret_cast<const float4*>(av + o);
-      const float4 g = *reinterpret_cast<const float4*>(grads + o);
-      adam_update(p.x, m.x, v.x, g.x, lr, bc1, bc2);
-      adam_update(p.y, m.y, v.y, g.y, lr, bc1, bc2);
-      adam_update(p.z, m.z, v.z, g.z, lr, bc1, bc2);
-      adam_update(p.w, m.w, v.w, g.w, lr, bc1, bc2);
-      *reinterpret_cast<float4*>(params + o) = p;
-      *reinterpret_cast<float4*>(am + o) = m;
-      *reinterpret_cast<float4*>(av + o) = v;
-    } else {
-      for (int64_t k = i; k < n; ++k) {
-        const int64_t ok = (int64_t)c * stride + k;
-        float p = params[ok], m = am[ok], v = av[ok];
-        adam_update(p, m, v, grads[ok], lr, bc1, bc2);
-        params[ok] = p;
-        am[ok] = m;
-        av[ok] = v;
-      }
-    }
+// multiple of 4, rows are 16-byte aligned). blockIdx.y is the component, so
+// the group's learning rate and bias corrections are block-uniform.
+// HBM-bound: 28 B per scalar (params, m, v read + written, gradient read).
+constexpr int kAdamThreads = 256;
+__global__ void __launch_bounds__(kAdamThreads) adam_kernel(float* __restrict__ params, const float* __restrict__ grads,
+                                                            float* __restrict__ am, float* __restrict__ av,
+                                                            int64_t stride, int64_t n, AdamParams ap) {
+  const int c = blockIdx.y;
+  const int gidx = comp_group(c);
+  if (!ap.active[gidx]) return;
+  const float lr = ap.lr[gidx], bc1 = ap.bc1[gidx], bc2 = ap.bc2[gidx];
+  const int64_t row = (int64_t)c * stride;
+  const int64_t nq = n >> 2;
+  for (int64_t q = (int64_t)blockIdx.x * kAdamThreads + threadIdx.x; q < nq; q += (int64_t)gridDim.x * kAdamThreads) {
+    const int64_t o = row + q * 4;
+    float4 p = __ldcs(reinterpret_cast<const float4*>(params + o));
+    float4 m = __ldcs(reinterpret_cast<const float4*>(am + o));
+    float4 v = __ldcs(reinterpret_cast<const float4*>(av + o));
+    const float4 g = __ldcs(reinterpret_cast<const float4*>(grads + o));
+    adam_update(p.x, m.x, v.x, g.x, lr, bc1, bc2);
+    adam_update(p.y, m.y, v.y, g.y, lr, bc1, bc2);
+    adam_update(p.z, m.z, v.z, g.z, lr, bc1, bc2);
+    adam_update(p.w, m.w, v.w, g.w, lr, bc1, bc2);
+    __stcs(reinterpret_cast<float4*>(params + o), p);
+    __stcs(reinterpret_cast<float4*>(am + o), m);
+    __stcs(reinterpret_cast<float4*>(av + o), v);
+  }
+  // ragged tail (n % 4 scalars), one thread per component
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const int64_t o = row + nq * 4 + threadIdx.x;
+    float p = params[o], m = am[o], v = av[o];
+    adam_update(p, m, v, grads[o], lr, bc1, bc2);
+    params[o] = p;
+    am[o] = m;
+    av[o] = v;
   }
 }
 
@@ -496,11 +488,14 @@ void launch_adam(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float posit
   ensure_optimizer_state(ctx, s);
   require(s->capacity % 4 == 0, "adam: scene capacity must be a multiple of 4");
   const AdamParams ap = make_adam(s, lrs, position_lr, update_sh_rest);
-  const int64_t total = (int64_t)s->comps * ((s->n + 3) / 4);
-  if (total == 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  adam_kernel<<<grid, 256, 0, ctx->stream>>>(s->params.as<float>(), s->grads.as<float>(), s->adam_m.as<float>(),
-                                             s->adam_v.as<float>(), s->capacity, s->n, s->comps, ap);
+  if (s->n == 0) return;
+  // ~16 resident 256-thread blocks per SM spread over the components
+  const int64_t per_comp = std::max<int64_t>(1, (int64_t)148 * 16 / s->comps);
+  const int64_t need = (s->n / 4 + kAdamThreads - 1) / kAdamThreads;
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min(need, per_comp)), (unsigned)s->comps);
+  adam_kernel<<<grid, kAdamThreads, 0, ctx->stream>>>(s->params.as<float>(), s->grads.as<float>(),
+                                                      s->adam_m.as<float>(), s->adam_v.as<float>(), s->capacity,
+                                                      s->n, ap);
   note_launch();
   SK_CUDA(cudaGetLastError());
 }
