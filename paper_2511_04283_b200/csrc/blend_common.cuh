@@ -31,22 +31,36 @@ __device__ __forceinline__ void stage_entry(float2 mu, float4 co, float4& xyq, f
   bb = make_float4(mu.x - ex, mu.x + ex, mu.y - ey, mu.y + ey);
 }
 
+// Warp w of a TS x TS tile owns the 8 x 4·PIX pixel block starting at
+// ((w % (TS/8)) * 8, (w / (TS/8)) * 4·PIX); lane l holds column l & 7 and rows
+// (l >> 3) + 4k, k < PIX.
 template <int TS, int PIX>
 struct WarpBlock {
   static constexpr int kWarpsX = TS / 8;
-  int lx, ly0;    // pixel of k = 0 within the tile
-  float x0, x1, y0, y1;  // the warp's pixel-centre rectangle (absolute)
-  __device__ WarpBlock(int tx, int ty) {
+  static constexpr int kWarps = TS * TS / PIX / 32;
+  int lx, ly0;  // pixel of k = 0 within the tile
+  __device__ WarpBlock() {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const int bx = (w % kWarpsX) * 8, by = (w / kWarpsX) * (4 * PIX);
-    lx = bx + (l & 7);
-    ly0 = by + (l >> 3);
-    x0 = (float)(tx * TS + bx);
-    x1 = x0 + 7.0f;
-    y0 = (float)(ty * TS + by);
-    y1 = y0 + (float)(4 * PIX - 1);
+    lx = (w % kWarpsX) * 8 + (l & 7);
+    ly0 = (w / kWarpsX) * (4 * PIX) + (l >> 3);
   }
-  __device__ bool misses(const float4& bb) const { return bb.y < x0 || bb.x > x1 || bb.w < y0 || bb.z > y1; }
+  // true when warp w's pixel-centre rectangle misses the box bb
+  __device__ static bool misses(const float4& bb, int w, int tx, int ty) {
+    const float x0 = (float)(tx * TS + (w % kWarpsX) * 8);
+    const float y0 = (float)(ty * TS + (w / kWarpsX) * (4 * PIX));
+    return bb.y < x0 || bb.x > x0 + 7.0f || bb.w < y0 || bb.z > y0 + (float)(4 * PIX - 1);
+  }
+  // Called by every lane of a staging warp for entry `chunk * 32 + lane` of the
+  // batch: publishes, per compute warp, the 32-bit mask of the chunk's entries
+  // whose box touches that warp's block (s_mask[w * chunks + chunk]).
+  __device__ static void publish(const float4& bb, bool valid, int chunk, int chunks, int tx, int ty,
+                                 uint32_t* s_mask) {
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t bits = __ballot_sync(0xffffffffu, valid && !misses(bb, w, tx, ty));
+      if ((threadIdx.x & 31) == 0) s_mask[w * chunks + chunk] = bits;
+    }
+  }
 };
 
 }  // namespace blend

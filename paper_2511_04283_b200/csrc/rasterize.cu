@@ -26,16 +26,18 @@ namespace {
 using namespace blend;
 
 template <int TS, int PIX, bool COUNT>
-__global__ void __launch_bounds__(TS* TS / PIX, 8) blend_fwd_kernel(
+__global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fwd_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry,
     const uint8_t* __restrict__ mask, int* __restrict__ counts) {
   constexpr int NTH = TS * TS / PIX;        // threads; each owns PIX pixels
   constexpr int B = TS * TS > 256 ? 256 : TS * TS;  // staged entries per batch
+  using WB = WarpBlock<TS, PIX>;
+  constexpr int kChunks = B / 32;
   __shared__ float4 s_xyq[B];
   __shared__ float4 s_co[B];
-  __shared__ float4 s_bb[B];
+  __shared__ uint32_t s_mask[WB::kWarps * kChunks];
   __shared__ float4 s_rgb[COUNT ? 1 : B];
   __shared__ uint32_t s_id[COUNT ? B : 1];
   __shared__ float s_exp2[64];
@@ -43,7 +45,8 @@ __global__ void __launch_bounds__(TS* TS / PIX, 8) blend_fwd_kernel(
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const WarpBlock<TS, PIX> wb(tx, ty);
+  const WB wb;
+  const int warp = threadIdx.x >> 5;
   const int px = tx * TS + wb.lx;
   const int2 range = ranges[tile];
   const float fpx = (float)px;
@@ -70,22 +73,28 @@ __global__ void __launch_bounds__(TS* TS / PIX, 8) blend_fwd_kernel(
     if (__syncthreads_count(all_done) == NTH) break;
     for (int e = (int)threadIdx.x; e < B; e += NTH) {
       const int i = b0 + e;
-      if (i < range.y) {
+      const bool valid = i < range.y;
+      float4 bb = make_float4(1.0f, -1.0f, 1.0f, -1.0f);
+      if (valid) {
         const uint32_t g = pair_val[i];
         const float4 co = conic_op[g];
-        float4 xyq, bb;
+        float4 xyq;
         stage_entry(mean2d[g], co, xyq, bb);
         s_xyq[e] = xyq;
         s_co[e] = co;
-        s_bb[e] = bb;
         if (!COUNT) s_rgb[e] = rgbd[g];
         if (COUNT) s_id[e] = g;
       }
+      WB::publish(bb, valid, e >> 5, kChunks, tx, ty, s_mask);
     }
     __syncthreads();
-    const int cnt = min(B, range.y - b0);
-    for (int j = 0; j < cnt && !all_done; ++j) {
-      if (wb.misses(s_bb[j])) continue;  // warp-uniform
+    // Walk, in list order, only the entries whose box touches this warp's
+    // block (bit masks published at staging).
+    for (int c = 0; c < kChunks && !all_done; ++c) {
+      uint32_t m = s_mask[warp * kChunks + c];
+      while (m && !all_done) {
+      const int j = c * 32 + __ffs(m) - 1;
+      m &= m - 1;
       const float4 mq = s_xyq[j];
       const float4 co = s_co[j];
 #pragma unroll
@@ -120,6 +129,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, 8) blend_fwd_kernel(
 #pragma unroll
       for (int k = 0; k < PIX; ++k) ad = ad && done[k];
       all_done = ad;
+      }
     }
   }
   if (COUNT) return;

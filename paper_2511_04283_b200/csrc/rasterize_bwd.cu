@@ -38,9 +38,11 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
     const float* __restrict__ final_t, const int* __restrict__ last_entry, const float* __restrict__ dimage,
     float* __restrict__ bgrads, int64_t gstride) {
   constexpr int NT = TS * TS / PIX;  // threads == batch size
+  using WB = WarpBlock<TS, PIX>;
+  constexpr int kChunks = NT / 32;
   __shared__ float4 s_xyq[NT];
   __shared__ float4 s_co[NT];
-  __shared__ float4 s_bb[NT];
+  __shared__ uint32_t s_mask[WB::kWarps * kChunks];
   __shared__ float4 s_rgb[NT];
   __shared__ uint32_t s_id[NT];
   __shared__ int s_max_last;
@@ -49,8 +51,9 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const WarpBlock<TS, PIX> wb(tx, ty);
+  const WB wb;
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const int px = tx * TS + wb.lx;
   const int2 range = ranges[tile];
   const float fpx = (float)px;
@@ -91,21 +94,30 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
     const int b0 = max(range.x, b_end - NT);
     __syncthreads();
     const int i = b0 + (int)threadIdx.x;
-    if (i < b_end) {
+    const bool valid = i < b_end;
+    float4 bb = make_float4(1.0f, -1.0f, 1.0f, -1.0f);
+    if (valid) {
       const uint32_t g = pair_val[i];
       const float4 co = conic_op[g];
-      float4 xyq, bb;
+      float4 xyq;
       stage_entry(mean2d[g], co, xyq, bb);
       s_xyq[threadIdx.x] = xyq;
       s_co[threadIdx.x] = co;
-      s_bb[threadIdx.x] = bb;
       s_rgb[threadIdx.x] = rgbd[g];
       s_id[threadIdx.x] = g;
     }
+    WB::publish(bb, valid, warp, kChunks, tx, ty, s_mask);
     __syncthreads();
+    // Reverse walk over the entries whose box touches this warp's block.
     const int jmax = min(b_end, warp_last) - b0;  // warp-uniform
-    for (int j = jmax - 1; j >= 0; --j) {
-      if (wb.misses(s_bb[j])) continue;  // warp-uniform
+    for (int c = (jmax - 1) >> 5; c >= 0; --c) {
+      uint32_t m = s_mask[warp * kChunks + c];
+      const int lim = jmax - c * 32;
+      if (lim < 32) m &= (1u << lim) - 1u;
+      while (m) {
+      const int bit = 31 - __clz(m);
+      m ^= 1u << bit;
+      const int j = c * 32 + bit;
       const int idx = b0 + j;
       const float4 mq = s_xyq[j];
       const float4 co = s_co[j];
@@ -182,6 +194,7 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
           pend_id = s_id[j];
           has_pend = true;
         }
+      }
       }
     }
   }
