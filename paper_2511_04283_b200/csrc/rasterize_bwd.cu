@@ -222,7 +222,7 @@ void launch_blend_backward(sk_ctx* ctx, sk_frame* f) {
   if (f->tiles_x * f->tiles_y == 0) return;
   switch (f->tile_size) {
     case 8: bwd_dispatch<8, 1>(ctx, f); break;
-    case 16: bwd_dispatch<16, 2>(ctx, f); break;
+    case 16: bwd_dispatch<16, 4>(ctx, f); break;
     case 32: bwd_dispatch<32, 4>(ctx, f); break;
     default: throw std::invalid_argument("tile_size must be 8, 16 or 32");
   }

@@ -56,6 +56,25 @@ def test_injected_render_bit_exact(ctx, orc, tile_size, mode):
         assert np.array_equal(got.contrib, ref.contrib)
 
 
+@pytest.mark.parametrize("n", [90, 200, 450, 900, 1800, 3500, 7000, 14000, 24000])
+def test_tile_list_classes_bit_exact(ctx, orc, n):
+    """Tile lists of every length class of the per-tile segment sort,
+    including lists above the largest class (radix-sort fallback), with many
+    exact depth ties (order must fall back to the projected index)."""
+    rng = np.random.default_rng(1000 + n)
+    w, h = 40, 20  # 3 x 2 tiles of 16
+    pg = orc.random_projected(rng, n, w, h, 0.02, 0.004, dtype=np.float32)
+    pg.depth[:] = np.round(pg.depth * 4.0) / 4.0  # ~40 distinct depths
+    b = orc.binning("aabb", tile_size=16)
+    ref = orc.render_pg(pg, w, h, b)
+    ctx.set_projected(pg, w, h, b)
+    ctx.build_tile_grid()
+    _check_tile_lists(ctx.tile_lists(), ref)
+    got = ctx.blend_forward()
+    assert np.array_equal(got.image, ref.image)
+    assert np.array_equal(got.contrib, ref.contrib)
+
+
 def test_blend_kats_gpu(ctx, orc):
     """tests/test_raster.cpp:133-156 on the GPU path."""
     from oracle.oracle import PG
