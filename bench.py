@@ -38,7 +38,7 @@ HBM_FALLBACK_GBS = 6650.0
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=1_000_000)
@@ -72,7 +72,25 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        bits = [(0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"), (0x20, "sw_thermal_slowdown"),
+                (0x4, "sw_power_cap")]
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append([str(sm), str(mx), "0"] + ["Active" if r & b else "Not Active" for b, _ in bits])
+            self._stop.wait(0.01)
+
     def _run(self):
+        try:
+            self._run_nvml()
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -82,7 +100,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -145,20 +163,25 @@ def run_reference(args, world, rank):
     cfg = train_config(sk)
     cfg.workers = cores
     tr = orc.ViewTrainer(p, 3, cam, gt8, cfg, extent)
-    for _ in range(args.warmup):
+    # Bounded sample: one warm-up iteration, then timed iterations until either
+    # --steps or a ~60 s budget is reached (each iteration is a full config-2
+    # training iteration, ~2.5 s on 16 host threads).
+    budget_s = float(os.environ.get("SK_REF_BUDGET_S", "60"))
+    for _ in range(min(args.warmup, 1)):
         tr.run(1)
     secs = []
-    for _ in range(args.steps):
+    while len(secs) < args.steps and (not secs or sum(secs) < budget_s):
         _, s = tr.run(1)
         secs.append(s)
     ms = 1000.0 * sum(secs) / len(secs)
     value = 1000.0 / ms
     line = {"impl": "reference", "metric": "train iters/s (1M Gaussians, 1080p)", "value": value,
-            "unit": "iter/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "unit": "iter/s", "n_gpus": world, "steps": len(secs), "warmup": min(args.warmup, 1), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (numpy RNG, reference distribution)", "config": bench_config(args),
             "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} full config-2 iterations (oracle, workers={cores})"},
+                             "sample": f"{len(secs)} full config-2 training iterations after 1 warm-up "
+                                       f"(oracle, workers={cores}; bounded to ~{budget_s:.0f} s)"},
             "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -167,26 +190,47 @@ def run_reference(args, world, rank):
 # our arm
 # ---------------------------------------------------------------------------
 
-PHASES = ["K1 preprocess", "K2-K5 bin+sort", "K6 blend fwd", "K7 loss", "K8 blend bwd", "K9+K10 proj-bwd+Adam"]
+PHASES = ["K1 preprocess", "K2-K5 bin+sort", "K6 blend fwd", "K7 loss", "K8 blend bwd", "K9 proj-bwd", "K10 Adam"]
 
 
 def algorithmic_bytes(phase, n, visible, pairs, pixels, comps=59):
-    """Algorithmic HBM bytes per launch."""
-    if phase == 0:
-        return 4 * comps * n + 52 * visible
-    if phase == 5:
-        # fused K9+K10: params, m, v read + written (24 B / scalar), plus blend grads,
-        # conic, radius and the 7 statistics read-modify-write for visible Gaussians
-        return 24 * comps * n + (44 + 16 + 4 + 56) * visible
-    if phase == 2:
-        return 36 * pairs + 20 * pixels
-    if phase == 4:
-        return 36 * pairs + 32 * pixels
-    if phase == 3:
-        return 36 * pixels
-    if phase == 1:
-        return 8 * n + 12 * pairs + 8 * pairs * 2 * 2 + 4 * n * 8
+    """Algorithmic HBM bytes per launch of each phase (Roofline)."""
+    if phase == 0:  # K1: 59 parameters read, 104 B of projected record written per visible
+        return 4 * comps * n + 104 * visible
+    if phase == 1:  # K2-K5: depth sort (4 passes x 16 B/key), scan, emit, 2 tile passes, ranges
+        return 64 * n + 8 * n + 8 * pairs + 32 * pairs + 4 * pairs
+    if phase == 2:  # K6: per pair index + 40 B record; per pixel image, T, count, last (24 B)
+        return 44 * pairs + 24 * pixels
+    if phase == 3:  # K7: rendered (12 B) + GT (3 B) read, dL/dimage (12 B) written per pixel
+        return 27 * pixels
+    if phase == 4:  # K8: per pair index + 40 B record; per pixel T, last, dL/dimage (20 B);
+        return 44 * pairs + 20 * pixels + 44 * visible  # 11 gradient floats per visible
+    if phase == 5:  # K9: params + blend grads + conic/radius + stats in, grads out
+        return 4 * comps * n * 2 + (44 + 16 + 4 + 56) * visible
+    if phase == 6:  # K10: params, m, v read + written, gradient read (28 B per scalar)
+        return 28 * comps * n
     return 0
+
+
+# Algorithmic fp32 operations per contributing pixel-Gaussian pair (alpha >=
+# 1/255): the reference's per-entry arithmetic (raster.hpp:225-234 forward,
+# :306-345 backward), counting the exp as its 10-flop table evaluation.
+FLOP_FWD_PER_CONTRIB = 30
+FLOP_BWD_PER_CONTRIB = 70
+
+
+def ncu_traffic(kernel_prefix):
+    """DRAM bytes per launch of a kernel from the committed ncu capture
+    (profiles/traffic.json, written by scripts/ncu_summary.py traffic)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        for k, v in d["kernels"].items():
+            if k.startswith(kernel_prefix):
+                return v
+    except Exception:
+        pass
+    return None
 
 
 def run_ours(args, world, rank, local):
@@ -247,10 +291,10 @@ def run_ours(args, world, rank, local):
     launches = ctx.launch_count() - launches0
     ctx.check(ctx._lib.sk_ctx_enable_timing(ctx.h, 0))
     ms = e0.elapsed_time(e1) / args.steps
-    phase_ms = (sk.C.c_double * 6)()
+    phase_ms = (sk.C.c_double * len(PHASES))()
     nsteps = sk.C.c_int64()
     ctx._lib.sk_ctx_get_timing(ctx.h, phase_ms, sk.C.byref(nsteps))
-    phase_avg = [phase_ms[i] / max(1, nsteps.value) for i in range(6)]
+    phase_avg = [phase_ms[i] / max(1, nsteps.value) for i in range(len(PHASES))]
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -294,22 +338,35 @@ def run_ours(args, world, rank, local):
     visible = int(prj.visible.sum())
     pairs = int(rows[-1]["tile_pairs"]) if rows else 0
     pixels = args.width * args.height
+    # contributing pixel-Gaussian pairs of this view (sum of per-pixel counts)
+    ctx.project_scene(scene, cam)
+    ctx.build_tile_grid()
+    contribs = int(ctx.blend_forward().contrib.astype(np.int64).sum())
     dom = int(np.argmax(phase_avg))
     alg = algorithmic_bytes(dom, args.n, visible, pairs, pixels)
     achieved = alg / (phase_avg[dom] * 1e-3) / 1e9
     clocks = clock.summary()
-    # FP32 pipe roof for the blend kernels: SMs x 128 lanes x 2 flop x clock
-    fp32_peak = 148 * 128 * 2 * (clocks["sm_mhz"] or sm_max) * 1e6 / 1e12
+    kernel_of = {4: "blend_bwd_kernel", 2: "blend_fwd_kernel", 5: "project_bwd_kernel", 6: "adam_kernel",
+                 0: "preprocess_kernel"}
+    traffic = ncu_traffic(kernel_of.get(dom, "?"))
     roofline = {"bound": "hbm", "kernel": PHASES[dom], "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
-                "algorithmic_bytes": alg, "kernel_ms": phase_avg[dom]}
-    adam_bytes = algorithmic_bytes(5, args.n, visible, pairs, pixels)
-    hbm_kernels = {
-        "K9+K10 proj-bwd+Adam": {"ms": phase_avg[5], "GB/s": adam_bytes / (phase_avg[5] * 1e-3) / 1e9,
-                                 "frac": adam_bytes / (phase_avg[5] * 1e-3) / 1e9 / hbm_peak},
-        "K1 preprocess": {"ms": phase_avg[0],
-                          "GB/s": algorithmic_bytes(0, args.n, visible, pairs, pixels) / (phase_avg[0] * 1e-3) / 1e9},
-    }
+                "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                "algorithmic_bytes": alg, "kernel_ms": phase_avg[dom],
+                "note": "the blend kernels are FP32-issue-bound; see roofline_fp32"}
+    # FP32 SIMT roof: SMs x 128 lanes x 2 flop x clock under load
+    fp32_peak = 148 * 128 * 2 * (clocks.get("sm_mhz") or sm_max) * 1e6 / 1e12
+    roofline_fp32 = {}
+    for ph, fl in ((4, FLOP_BWD_PER_CONTRIB), (2, FLOP_FWD_PER_CONTRIB)):
+        tf = contribs * fl / (phase_avg[ph] * 1e-3) / 1e12
+        roofline_fp32[PHASES[ph]] = {"achieved": tf, "peak": fp32_peak, "unit": "TFLOP/s", "frac": tf / fp32_peak,
+                                     "flop_per_contrib": fl, "kernel_ms": phase_avg[ph]}
+    roofline_fp32["contributions"] = contribs
+    hbm_kernels = {}
+    for ph in (0, 1, 3, 5, 6):
+        b = algorithmic_bytes(ph, args.n, visible, pairs, pixels)
+        gbs = b / (phase_avg[ph] * 1e-3) / 1e9
+        hbm_kernels[PHASES[ph]] = {"ms": phase_avg[ph], "algorithmic_MB": b / 1e6, "GB/s": gbs,
+                                   "frac": gbs / hbm_peak}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -330,6 +387,7 @@ def run_ours(args, world, rank, local):
         "data": "synthetic (numpy RNG, reference generate_synthetic distribution; GT rendered on GPU, 8-bit)",
         "config": dict(bench_config(args), views_per_step=world,
                        parallelism=f"view-parallel dp{world} (NCCL grad all-reduce)" if world > 1 else "single GPU"),
+        # raster forward = K1..K6, raster backward = K8 + K9 (pixels / s)
         "raster_fwd_mpix_s": pixels / ((phase_avg[0] + phase_avg[1] + phase_avg[2]) * 1e-3) / 1e6,
         "raster_bwd_mpix_s": pixels / ((phase_avg[4] + phase_avg[5]) * 1e-3) / 1e6,
         "phase_ms": dict(zip(PHASES, [round(x, 4) for x in phase_avg])),
@@ -337,8 +395,8 @@ def run_ours(args, world, rank, local):
         "visible": visible,
         "loss_last": rows[-1]["loss"] if rows else None,
         "roofline": roofline,
+        "roofline_fp32": roofline_fp32,
         "hbm_kernels": hbm_kernels,
-        "fp32_peak_tflops": fp32_peak,
         "e2e": {"value": world * 1000.0 / e2e_ms, "unit": "iter/s", "h2d_bytes_per_step": int(gt8.size),
                 "d2h_bytes_per_step": 44, "ms_per_step": e2e_ms},
         "gpu_launches": launches,
@@ -369,9 +427,13 @@ def cpu_baseline(args, params, cam, gt8, extent):
         cfg = train_config(sk)
         cfg.workers = cores
         tr = orc.ViewTrainer(params, 3, cam, gt8, cfg, extent)
-        _, secs = tr.run(1)
-        return {"value": 1.0 / secs, "unit": "iter/s", "cores": cores, "kind": "port",
-                "sample": "1 full config-2 training iteration (1M Gaussians, 1920x1080), oracle workers=nproc"}
+        tr.run(1)  # warm-up (allocations)
+        secs = []
+        while not secs or (sum(secs) < 12.0 and len(secs) < 8):
+            secs.append(tr.run(1)[1])
+        return {"value": len(secs) / sum(secs), "unit": "iter/s", "cores": cores, "kind": "port",
+                "sample": f"{len(secs)} full config-2 training iterations (1M Gaussians, 1920x1080) after 1 "
+                          f"warm-up, oracle workers={cores}"}
     except Exception as e:  # the baseline is reported, never required
         return {"value": None, "unit": "iter/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
 

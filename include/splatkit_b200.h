@@ -109,9 +109,10 @@ int sk_ctx_synchronize(sk_ctx* ctx);
 int sk_ctx_launch_count(const sk_ctx* ctx, int64_t* out);
 /* Per-phase device timing of training steps (CUDA events on the context
  * stream). Phases: 0 preprocess (K1), 1 binning + sort (K2-K5), 2 forward
- * blend (K6), 3 loss (K7), 4 backward blend (K8), 5 project-backward + Adam
- * (K9+K10). ms[6] accumulates milliseconds, steps counts timed steps. */
-#define SK_NUM_PHASES 6
+ * blend (K6), 3 loss (K7), 4 backward blend (K8), 5 project-backward (K9,
+ * plus the gradient all-reduce on a view-parallel step), 6 Adam (K10).
+ * ms[SK_NUM_PHASES] accumulates milliseconds, steps counts timed steps. */
+#define SK_NUM_PHASES 7
 int sk_ctx_enable_timing(sk_ctx* ctx, int on);
 int sk_ctx_get_timing(const sk_ctx* ctx, double* ms, int64_t* steps);
 int sk_ctx_reset_timing(sk_ctx* ctx);

@@ -82,8 +82,11 @@ void bin_sort(sk_ctx* ctx, sk_frame* f) {
   uint32_t* tb = ensure<uint32_t>(f->ptile_b, pm);
   uint32_t* pa = ensure<uint32_t>(f->pval_a, pm);
   uint32_t* pb = ensure<uint32_t>(f->pval_b, pm);
-  launch_duplicate(ctx, f, va, offsets, ta, pa);
-  radix_sort_pairs(ctx, ta, tb, pa, pb, pairs, tile_bits(tiles));
+  const int bits = tile_bits(tiles);
+  uint32_t* hist = radix_hist_buffer(ctx);
+  SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * 256, ctx->stream));
+  launch_duplicate(ctx, f, va, offsets, ta, pa, radix_passes(bits), hist);
+  radix_sort_pairs(ctx, ta, tb, pa, pb, pairs, bits, /*hist_ready=*/true);
   f->pair_tile = ta;
   f->pair_val = pa;
   launch_tile_ranges(ctx, ta, pairs, f->ranges.as<int2>(), tiles);

@@ -322,45 +322,100 @@ __global__ void inject_bin_kernel(int64_t n, BinParams bp, const float2* __restr
 // (row-major within its rectangle, as bin_aabb / bin_compact enumerate them)
 // at its scanned offset. Pair order = (depth, index) order, which the
 // stable tile sort then preserves inside each tile.
-__global__ void __launch_bounds__(256) duplicate_kernel(int64_t n, BinParams bp, const uint32_t* __restrict__ order,
-                                                        const int32_t* __restrict__ offsets,
-                                                        const int* __restrict__ tiles,
-                                                        const int4* __restrict__ rect,
-                                                        const float2* __restrict__ mean2d,
-                                                        const float4* __restrict__ conic_op,
-                                                        const float* __restrict__ a_star,
-                                                        uint32_t* __restrict__ pair_tile,
-                                                        uint32_t* __restrict__ pair_val) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  const uint32_t g = order[s];
-  if (tiles[g] == 0) return;
-  int64_t off = offsets[s];
-  const int4 rc = rect[g];
-  if (bp.mode == 0) {
-    for (int ty = rc.y; ty <= rc.w; ++ty)
-      for (int tx = rc.x; tx <= rc.z; ++tx) {
-        pair_tile[off] = (uint32_t)(ty * bp.tiles_x + tx);
-        pair_val[off] = g;
-        ++off;
+// K3: pairs (tile, Gaussian) in (depth, index) order, plus the digit
+// histograms of the following tile-id radix sort (hist[p][256], p < passes).
+// A warp takes 32 consecutive depth-ordered slots; their pair runs are
+// adjacent in the output, so in AABB mode the warp writes the whole range
+// cooperatively (lane e writes pair e: owner found by a shuffle binary search
+// over the lanes' offsets, tile from the owner's rectangle) and every store
+// is coalesced. Compact mode keeps one thread per Gaussian (its tiles are a
+// filtered subset of the rectangle).
+constexpr int kDupThreads = 256;
+__global__ void __launch_bounds__(kDupThreads) duplicate_kernel(int64_t n, BinParams bp,
+                                                                const uint32_t* __restrict__ order,
+                                                                const int32_t* __restrict__ offsets,
+                                                                const int* __restrict__ tiles,
+                                                                const int4* __restrict__ rect,
+                                                                const float2* __restrict__ mean2d,
+                                                                const float4* __restrict__ conic_op,
+                                                                const float* __restrict__ a_star,
+                                                                uint32_t* __restrict__ pair_tile,
+                                                                uint32_t* __restrict__ pair_val, int passes,
+                                                                uint32_t* __restrict__ hist) {
+  __shared__ uint32_t s_hist[4][256];
+  for (int i = threadIdx.x; i < 4 * 256; i += kDupThreads) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  auto count_digits = [&](uint32_t t) {
+    for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(t >> (8 * p)) & 255u], 1u);
+  };
+  const int64_t warps = (int64_t)gridDim.x * (kDupThreads / 32);
+  for (int64_t wi = (int64_t)blockIdx.x * (kDupThreads / 32) + (threadIdx.x >> 5); wi * 32 < n; wi += warps) {
+    const int64_t s = wi * 32 + lane;
+    const bool valid = s < n;
+    const uint32_t g = valid ? order[s] : 0u;
+    const int cnt = valid ? tiles[g] : 0;
+    const int off = valid ? offsets[s] : 0x7fffffff;
+    if (bp.mode != 0) {
+      if (cnt == 0) continue;
+      int64_t o = off;
+      const float2 mu = mean2d[g];
+      const float4 co = conic_op[g];
+      const float as = a_star[g];
+      const int4 rc = rect[g];
+      for (int ty = rc.y; ty <= rc.w; ++ty) {
+        const float ry0 = (float)(ty * bp.ts);
+        const float ry1 = (float)(min((ty + 1) * bp.ts, bp.H) - 1);
+        for (int tx = rc.x; tx <= rc.z; ++tx) {
+          const float rx0 = (float)(tx * bp.ts);
+          const float rx1 = (float)(min((tx + 1) * bp.ts, bp.W) - 1);
+          if (min_mahalanobis_on_rect(co.x, co.y, co.z, mu.x, mu.y, rx0, rx1, ry0, ry1) <= as) {
+            const uint32_t t = (uint32_t)(ty * bp.tiles_x + tx);
+            pair_tile[o] = t;
+            pair_val[o] = g;
+            count_digits(t);
+            ++o;
+          }
+        }
       }
-    return;
-  }
-  const float2 mu = mean2d[g];
-  const float4 co = conic_op[g];
-  const float as = a_star[g];
-  for (int ty = rc.y; ty <= rc.w; ++ty) {
-    const float ry0 = (float)(ty * bp.ts);
-    const float ry1 = (float)(min((ty + 1) * bp.ts, bp.H) - 1);
-    for (int tx = rc.x; tx <= rc.z; ++tx) {
-      const float rx0 = (float)(tx * bp.ts);
-      const float rx1 = (float)(min((tx + 1) * bp.ts, bp.W) - 1);
-      if (min_mahalanobis_on_rect(co.x, co.y, co.z, mu.x, mu.y, rx0, rx1, ry0, ry1) <= as) {
-        pair_tile[off] = (uint32_t)(ty * bp.tiles_x + tx);
-        pair_val[off] = g;
-        ++off;
-      }
+      continue;
     }
+    const int4 rc = cnt ? rect[g] : make_int4(0, 0, 0, 0);
+    const int w = rc.z - rc.x + 1;
+    // the warp's pairs occupy [first, last) contiguously
+    const int first = __reduce_min_sync(0xffffffffu, valid ? off : 0x7fffffff);
+    const int last = __reduce_max_sync(0xffffffffu, valid ? off + cnt : 0);
+    const int total = last - first;
+    for (int e0 = 0; e0 < total; e0 += 32) {
+      const int pos = first + e0 + lane;
+      // owner = the highest lane whose offset is <= pos (zero-count lanes
+      // share the next lane's offset, so they are never chosen for a pair)
+      int L = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int o = __shfl_sync(0xffffffffu, off, L + step);
+        if (o <= pos) L += step;
+      }
+      const int k = pos - __shfl_sync(0xffffffffu, off, L);
+      const int ox = __shfl_sync(0xffffffffu, rc.x, L);
+      const int oy = __shfl_sync(0xffffffffu, rc.y, L);
+      const int ow = __shfl_sync(0xffffffffu, w, L);
+      const uint32_t og = __shfl_sync(0xffffffffu, g, L);
+      const bool active = e0 + lane < total;
+      uint32_t t = 0;
+      if (active) {
+        const int r = k / ow;
+        t = (uint32_t)((oy + r) * bp.tiles_x + ox + (k - r * ow));
+        pair_tile[pos] = t;
+        pair_val[pos] = og;
+      }
+      if (active) count_digits(t);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += kDupThreads) {
+    const uint32_t v = (&s_hist[0][0])[i];
+    if (v) atomicAdd(&hist[i], v);
   }
 }
 
@@ -416,13 +471,14 @@ void launch_inject_bin(sk_ctx* ctx, sk_frame* f) {
 }
 
 void launch_duplicate(sk_ctx* ctx, sk_frame* f, const uint32_t* order, const int32_t* offsets, uint32_t* pair_tile,
-                      uint32_t* pair_val) {
+                      uint32_t* pair_val, int passes, uint32_t* hist) {
   if (f->n == 0) return;
   const BinParams bp = make_bin_params(f);
-  const unsigned grid = (unsigned)((f->n + 255) / 256);
-  duplicate_kernel<<<grid, 256, 0, ctx->stream>>>(f->n, bp, order, offsets, f->tiles.as<int>(), f->rect.as<int4>(),
-                                                  f->mean2d.as<float2>(), f->conic_op.as<float4>(),
-                                                  f->a_star.as<float>(), pair_tile, pair_val);
+  const int64_t warps = (f->n + 31) / 32;
+  const unsigned grid = (unsigned)std::min<int64_t>((warps + kDupThreads / 32 - 1) / (kDupThreads / 32), 148 * 8);
+  duplicate_kernel<<<grid, kDupThreads, 0, ctx->stream>>>(
+      f->n, bp, order, offsets, f->tiles.as<int>(), f->rect.as<int4>(), f->mean2d.as<float2>(),
+      f->conic_op.as<float4>(), f->a_star.as<float>(), pair_tile, pair_val, passes, hist);
   note_launch();
   SK_CUDA(cudaGetLastError());
 }

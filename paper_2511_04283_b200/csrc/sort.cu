@@ -287,32 +287,62 @@ __global__ void iota_kernel(uint32_t* out, int64_t n) {
   if (i < n) out[i] = (uint32_t)i;
 }
 
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ tile, int64_t pairs, int2* __restrict__ ranges) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= pairs) return;
-  const uint32_t t = tile[i];
-  if (i == 0 || tile[i - 1] != t) ranges[t].x = (int)i;
-  if (i == pairs - 1 || tile[i + 1] != t) ranges[t].y = (int)(i + 1);
+// Tile ranges from the sorted tile ids: a run starts where the id differs
+// from its predecessor. Four ids per thread (uint4 loads), the predecessor of
+// the first from the previous lane.
+__global__ void __launch_bounds__(256) tile_ranges_kernel(const uint32_t* __restrict__ tile, int64_t pairs,
+                                                          int2* __restrict__ ranges) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i0 = q * 4;
+  const bool full = i0 + 3 < pairs;
+  uint32_t t[4];
+  if (full) {
+    const uint4 v = *reinterpret_cast<const uint4*>(tile + i0);
+    t[0] = v.x, t[1] = v.y, t[2] = v.z, t[3] = v.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = i0 + k < pairs ? tile[i0 + k] : 0xffffffffu;
+  }
+  uint32_t prev = __shfl_up_sync(0xffffffffu, t[3], 1);
+  if ((threadIdx.x & 31) == 0) prev = i0 > 0 && i0 - 1 < pairs ? tile[i0 - 1] : 0xffffffffu;
+  if (i0 >= pairs) return;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t i = i0 + k;
+    if (i >= pairs) break;
+    const uint32_t p = k == 0 ? prev : t[k - 1];
+    if (i == 0 || p != t[k]) {
+      ranges[t[k]].x = (int)i;
+      if (i > 0) ranges[p].y = (int)i;
+    }
+    if (i == pairs - 1) ranges[t[k]].y = (int)(i + 1);
+  }
 }
 
 }  // namespace
 
+uint32_t* radix_hist_buffer(sk_ctx* ctx) { return ensure<uint32_t>(ctx->sort.hist, (size_t)kMaxPasses * kRadix); }
+
+int radix_passes(int bits) { return (bits + kRadixBits - 1) / kRadixBits; }
+
 void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_t*& vals, uint32_t*& vals_alt,
-                      int64_t n, int bits) {
+                      int64_t n, int bits, bool hist_ready) {
   if (n <= 1 || bits <= 0) return;
-  const int passes = (bits + kRadixBits - 1) / kRadixBits;
+  const int passes = radix_passes(bits);
   require(passes <= kMaxPasses, "radix_sort_pairs: at most 32 key bits");
   const int64_t tiles = (n + kTile - 1) / kTile;
   require(tiles < (1ll << 31), "radix_sort_pairs: too many keys");
-  uint32_t* hist = ensure<uint32_t>(ctx->sort.hist, (size_t)kMaxPasses * kRadix);
+  uint32_t* hist = radix_hist_buffer(ctx);
   uint32_t* status = ensure<uint32_t>(ctx->sort.status, (size_t)tiles * kRadix);
   uint32_t* counters = ensure<uint32_t>(ctx->sort.counters, kMaxPasses);
   cudaStream_t s = ctx->stream;
-  SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s));
   SK_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * kMaxPasses, s));
-  const int hist_blocks = (int)std::min<int64_t>((n + 4095) / 4096, 148 * 8);
-  radix_hist_kernel<<<hist_blocks, 256, 0, s>>>(keys, n, passes, hist);
-  note_launch();
+  if (!hist_ready) {
+    SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s));
+    const int hist_blocks = (int)std::min<int64_t>((n + 4095) / 4096, 148 * 8);
+    radix_hist_kernel<<<hist_blocks, 256, 0, s>>>(keys, n, passes, hist);
+    note_launch();
+  }
   radix_bases_kernel<<<passes, kRadix, 0, s>>>(hist);
   note_launch();
   for (int p = 0; p < passes; ++p) {
@@ -353,7 +383,7 @@ void launch_iota(sk_ctx* ctx, uint32_t* out, int64_t n) {
 void launch_tile_ranges(sk_ctx* ctx, const uint32_t* pair_tile, int64_t pairs, int2* ranges, int tiles) {
   SK_CUDA(cudaMemsetAsync(ranges, 0, sizeof(int2) * tiles, ctx->stream));
   if (pairs == 0) return;
-  tile_ranges_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, ctx->stream>>>(pair_tile, pairs, ranges);
+  tile_ranges_kernel<<<(unsigned)((pairs + 1023) / 1024), 256, 0, ctx->stream>>>(pair_tile, pairs, ranges);
   note_launch();
   SK_CUDA(cudaGetLastError());
 }

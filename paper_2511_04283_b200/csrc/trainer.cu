@@ -102,15 +102,13 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   const LearningRates lrs = lrs_from(cfg);
   const float pos_lr = expon_lr(lrs.position * extent, lrs.position_final * extent, it, cfg.iterations);
   require(!cfg.lazy_opt_enabled, "trainer: lazy_opt_enabled is not supported on the GPU path yet");
-  if (comm && comm->world > 1) {
-    // view-parallel step: K9 into the gradient buffer, C1 sum over ranks, K10
-    launch_project_backward(ctx, scene, f, true);
-    allreduce_grads(comm, scene, ctx->stream);
-    launch_adam(ctx, scene, lrs, pos_lr, true);
-  } else {
-    launch_project_backward_adam(ctx, scene, f, lrs, pos_lr, true, true);
-  }
+  // K9 into the gradient buffer (+ C1 sum over ranks on a view-parallel
+  // step), then K10
+  launch_project_backward(ctx, scene, f, true);
+  if (comm && comm->world > 1) allreduce_grads(comm, scene, ctx->stream);
   ctx->mark(6);
+  launch_adam(ctx, scene, lrs, pos_lr, true);
+  ctx->mark(7);
   LossSums sums{};
   read_loss_sums(ctx, &sums);  // synchronises the stream
   raise_device_errors(read_error_word(ctx));
