@@ -50,14 +50,42 @@ struct WarpBlock {
     const float y0 = (float)(ty * TS + (w / kWarpsX) * (4 * PIX));
     return bb.y < x0 || bb.x > x0 + 7.0f || bb.w < y0 || bb.z > y0 + (float)(4 * PIX - 1);
   }
+  // Exact test: does the ellipse {q <= q_cut} (conic co, centre mq.xy, cut
+  // mq.z) reach a pixel centre of warp w's rectangle? The minimum of the
+  // convex q over the rectangle is 0 inside it, else on an edge, where the
+  // unconstrained minimiser along the edge is clamped to the edge. Slack of
+  // 1e-3 relative + 1e-3 absolute keeps the test conservative under fp32
+  // rounding. Only called for positive-definite conics with a box hit.
+  __device__ static bool ellipse_hits(const float4& mq, const float4& co, int w, int tx, int ty) {
+    const float x0 = (float)(tx * TS + (w % kWarpsX) * 8), x1 = x0 + 7.0f;
+    const float y0 = (float)(ty * TS + (w / kWarpsX) * (4 * PIX)), y1 = y0 + (float)(4 * PIX - 1);
+    if (mq.x >= x0 && mq.x <= x1 && mq.y >= y0 && mq.y <= y1) return true;
+    const float a = co.x, b = co.y, c = co.z;
+    const float ia = 1.0f / a, ic = 1.0f / c;
+    float best = 3.0e38f;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const float dx = (e ? x1 : x0) - mq.x;
+      const float dy = fminf(fmaxf(mq.y - b * dx * ic, y0), y1) - mq.y;
+      best = fminf(best, a * dx * dx + 2.0f * b * dx * dy + c * dy * dy);
+      const float ey = (e ? y1 : y0) - mq.y;
+      const float ex = fminf(fmaxf(mq.x - b * ey * ia, x0), x1) - mq.x;
+      best = fminf(best, a * ex * ex + 2.0f * b * ex * ey + c * ey * ey);
+    }
+    return best <= mq.z * 1.001f + 1e-3f;
+  }
   // Called by every lane of a staging warp for entry `chunk * 32 + lane` of the
   // batch: publishes, per compute warp, the 32-bit mask of the chunk's entries
-  // whose box touches that warp's block (s_mask[w * chunks + chunk]).
-  __device__ static void publish(const float4& bb, bool valid, int chunk, int chunks, int tx, int ty,
-                                 uint32_t* s_mask) {
+  // whose ellipse reaches that warp's block (s_mask[w * chunks + chunk]). The
+  // box test rejects most; the exact test runs on box hits of PD conics.
+  __device__ static void publish(const float4& bb, const float4& mq, const float4& co, bool valid, int chunk,
+                                 int chunks, int tx, int ty, uint32_t* s_mask) {
+    const bool pd = co.x > 0.0f && co.z > 0.0f && co.x * co.z - co.y * co.y > 0.0f;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      const uint32_t bits = __ballot_sync(0xffffffffu, valid && !misses(bb, w, tx, ty));
+      bool hit = valid && !misses(bb, w, tx, ty);
+      if (hit && pd) hit = ellipse_hits(mq, co, w, tx, ty);
+      const uint32_t bits = __ballot_sync(0xffffffffu, hit);
       if ((threadIdx.x & 31) == 0) s_mask[w * chunks + chunk] = bits;
     }
   }

@@ -74,18 +74,17 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
     for (int e = (int)threadIdx.x; e < B; e += NTH) {
       const int i = b0 + e;
       const bool valid = i < range.y;
-      float4 bb = make_float4(1.0f, -1.0f, 1.0f, -1.0f);
+      float4 bb = make_float4(1.0f, -1.0f, 1.0f, -1.0f), xyq = bb, co = bb;
       if (valid) {
         const uint32_t g = pair_val[i];
-        const float4 co = conic_op[g];
-        float4 xyq;
+        co = conic_op[g];
         stage_entry(mean2d[g], co, xyq, bb);
         s_xyq[e] = xyq;
         s_co[e] = co;
         if (!COUNT) s_rgb[e] = rgbd[g];
         if (COUNT) s_id[e] = g;
       }
-      WB::publish(bb, valid, e >> 5, kChunks, tx, ty, s_mask);
+      WB::publish(bb, xyq, co, valid, e >> 5, kChunks, tx, ty, s_mask);
     }
     __syncthreads();
     // Walk, in list order, only the entries whose box touches this warp's

@@ -7,10 +7,12 @@
 // of two entries at a time with shuffles; lanes issue one global atomic each.
 //
 // Gradients are checked against the oracle within a tolerance, so this file
-// is compiled with FMA contraction. The per-pixel contribution decision (q,
-// the deterministic exp, alpha) is written with non-contracting round-to-
-// nearest intrinsics so it reproduces the forward's bits exactly and the
-// walk visits exactly the entries K6 blended.
+// is compiled with FMA contraction. The per-pixel contribution decision must
+// still be K6's exactly (the walk must visit exactly the entries K6 blended):
+// q is written with non-contracting round-to-nearest intrinsics (bit-equal
+// to K6), alpha comes from the fast hardware exp, and only alphas within
+// 1e-5 relative of the 1/255 and 0.99 thresholds (the fast exp is within
+// ~1e-6) are recomputed with the shared deterministic exp.
 #include "blend_common.cuh"
 
 namespace sk {
@@ -31,7 +33,7 @@ __device__ __forceinline__ float select_field(const float (&v)[kBGradFields], in
   return r;
 }
 
-template <int TS, int PIX>
+template <int TS, int PIX, bool FASTEXP = true>
 __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
@@ -95,18 +97,17 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
     __syncthreads();
     const int i = b0 + (int)threadIdx.x;
     const bool valid = i < b_end;
-    float4 bb = make_float4(1.0f, -1.0f, 1.0f, -1.0f);
+    float4 bb = make_float4(1.0f, -1.0f, 1.0f, -1.0f), xyq = bb, co = bb;
     if (valid) {
       const uint32_t g = pair_val[i];
-      const float4 co = conic_op[g];
-      float4 xyq;
+      co = conic_op[g];
       stage_entry(mean2d[g], co, xyq, bb);
       s_xyq[threadIdx.x] = xyq;
       s_co[threadIdx.x] = co;
       s_rgb[threadIdx.x] = rgbd[g];
       s_id[threadIdx.x] = g;
     }
-    WB::publish(bb, valid, warp, kChunks, tx, ty, s_mask);
+    WB::publish(bb, xyq, co, valid, warp, kChunks, tx, ty, s_mask);
     __syncthreads();
     // Reverse walk over the entries whose box touches this warp's block.
     const int jmax = min(b_end, warp_last) - b0;  // warp-uniform
@@ -133,8 +134,15 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
         const float q = rn_add(rn_add(rn_mul(rn_mul(co.x, dx), dx), rn_mul(rn_mul(rn_mul(2.0f, co.y), dx), dy)),
                                rn_mul(rn_mul(co.z, dy), dy));
         if (!(q >= 0.0f && q <= mq.z)) continue;
-        const float ge = det_expf_core(rn_mul(-0.5f, q), s_exp2);
-        const float raw = rn_mul(co.w, ge);
+        // Fast exp (MUFU ex2, ~1e-6 relative); the exact deterministic exp
+        // only where alpha is within 1e-5 (relative) of a decision threshold,
+        // so the skip / cap decisions are exactly K6's.
+        float ge = FASTEXP ? __expf(-0.5f * q) : 0.0f;
+        float raw = co.w * ge;
+        if (!FASTEXP || fabsf(raw - kAlphaMin) <= 1e-5f * kAlphaMin || fabsf(raw - kAlphaCap) <= 1e-5f * kAlphaCap) {
+          ge = det_expf_core(rn_mul(-0.5f, q), s_exp2);
+          raw = rn_mul(co.w, ge);
+        }
         const bool capped = raw > kAlphaCap;
         const float alpha = capped ? kAlphaCap : raw;
         if (alpha < kAlphaMin) continue;
