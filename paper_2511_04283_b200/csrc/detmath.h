@@ -96,7 +96,8 @@ static const uint32_t kExp2TableHost[64] = SK_EXP2_TABLE;
 // |r| <= ln2/128 (Cody-Waite split of ln2/64 into a 9-bit head, so kf * head
 // is exact for |k| < 2^14), e^r by a degree-3 polynomial, then the table and
 // one exact power-of-two scaling. `table` holds the 64 SK_EXP2_TABLE floats.
-SK_HD float det_expf_core(float x, const float* table) {
+template <class Tab>
+SK_HD float det_expf_core_t(float x, const Tab& table) {
   const float kf = det_floorf(rn_add(rn_mul(x, 92.33248261689366f), 0.5f));  // 64 / ln2
   const int k = (int)kf;
   const float r = rn_sub(rn_sub(x, rn_mul(kf, 0.010833740234375f)), rn_mul(kf, -3.3155381258549027e-06f));
@@ -107,6 +108,24 @@ SK_HD float det_expf_core(float x, const float* table) {
   const int e = (k - j) / 64;
   return rn_mul(rn_mul(table[j], p), bits_to_f32((uint32_t)(e + 127) << 23));
 }
+
+SK_HD float det_expf_core(float x, const float* table) { return det_expf_core_t(x, table); }
+
+#if defined(__CUDACC__)
+// The exp table staged in shared memory, read with ld.shared through a
+// 32-bit shared-window address computed once per kernel (indexing a generic
+// pointer to shared memory re-derives the CTA's window base on every access).
+struct SmemTable {
+  uint32_t base;
+  __device__ explicit SmemTable(const float* s) : base((uint32_t)__cvta_generic_to_shared(s)) {}
+  __device__ __forceinline__ float operator[](int j) const {
+    float v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(base + 4u * (uint32_t)j));
+    return v;
+  }
+};
+SK_HD float det_expf_core(float x, const SmemTable& table) { return det_expf_core_t(x, table); }
+#endif
 
 SK_HD const float* exp2_table() {
 #if defined(__CUDA_ARCH__)
@@ -120,12 +139,12 @@ SK_HD const float* exp2_table() {
 // subnormal / overflow ends exact). Kernels with many calls pass a copy of
 // the table staged in shared memory (constant memory serialises divergent
 // indices).
-SK_HD float det_expf(float x, const float* table = nullptr) {
-  if (!table) table = exp2_table();
+template <class Tab>
+SK_HD float det_expf_t(float x, const Tab& table) {
   if (!(x == x)) return x;                             // NaN propagates
   if (x > 88.72283f) return bits_to_f32(0x7f800000u);  // +inf
   if (x < -103.97208f) return 0.0f;                    // below the smallest subnormal
-  if (x >= -87.0f && x <= 88.0f) return det_expf_core(x, table);
+  if (x >= -87.0f && x <= 88.0f) return det_expf_core_t(x, table);
   const float kf = det_floorf(x * 92.33248261689366f + 0.5f);
   const int k = (int)kf;
   const float r = (x - kf * 0.010833740234375f) - kf * -3.3155381258549027e-06f;
@@ -139,6 +158,11 @@ SK_HD float det_expf(float x, const float* table = nullptr) {
   const float t = table[j] * p;
   return (t * bits_to_f32((uint32_t)(e1 + 127) << 23)) * bits_to_f32((uint32_t)(e2 + 127) << 23);
 }
+
+SK_HD float det_expf(float x, const float* table = nullptr) { return det_expf_t(x, table ? table : exp2_table()); }
+#if defined(__CUDACC__)
+SK_HD float det_expf(float x, const SmemTable& table) { return det_expf_t(x, table); }
+#endif
 
 // Natural log of a positive finite float. x = m 2^e with m in [sqrt(.5),
 // sqrt(2)); log m = 2 atanh(s), s = (m-1)/(m+1), odd series to s^9.
@@ -174,6 +198,9 @@ SK_HD float det_logf(float x) {
 
 // Activation used by the reference (types.hpp:28-30): 1 / (1 + e^{-x}).
 SK_HD float det_sigmoidf(float x, const float* table = nullptr) { return 1.0f / (1.0f + det_expf(-x, table)); }
+#if defined(__CUDACC__)
+SK_HD float det_sigmoidf(float x, const SmemTable& table) { return 1.0f / (1.0f + det_expf(-x, table)); }
+#endif
 
 #if defined(__CUDACC__)
 // Stages the exp table into shared memory; call from all threads, then sync.

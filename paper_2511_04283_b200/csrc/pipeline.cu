@@ -85,7 +85,7 @@ void bin_sort(sk_ctx* ctx, sk_frame* f) {
   const int bits = tile_bits(tiles);
   uint32_t* hist = radix_hist_buffer(ctx);
   SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * 256, ctx->stream));
-  launch_duplicate(ctx, f, va, offsets, ta, pa, radix_passes(bits), hist);
+  launch_duplicate(ctx, f, va, offsets, ta, pa, radix_passes(bits), radix_digit_width(bits), hist);
   radix_sort_pairs(ctx, ta, tb, pa, pb, pairs, bits, /*hist_ready=*/true);
   f->pair_tile = ta;
   f->pair_val = pa;

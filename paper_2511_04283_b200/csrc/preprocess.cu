@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
                                                          uint32_t* __restrict__ key_out, uint32_t* __restrict__ err) {
   __shared__ float s_exp2[64];
   stage_exp2_table(s_exp2);
+  const SmemTable tab(s_exp2);
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -164,8 +165,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
   // covariance_3d (scene.hpp:88-96)
   const float qw_in = p[3 * stride + i], qx_in = p[4 * stride + i], qy_in = p[5 * stride + i],
               qz_in = p[6 * stride + i];
-  const float s0 = det_expf(p[7 * stride + i], s_exp2), s1 = det_expf(p[8 * stride + i], s_exp2),
-              s2 = det_expf(p[9 * stride + i], s_exp2);
+  const float s0 = det_expf(p[7 * stride + i], tab), s1 = det_expf(p[8 * stride + i], tab),
+              s2 = det_expf(p[9 * stride + i], tab);
   if (!(isfinite(qw_in) && isfinite(qx_in) && isfinite(qy_in) && isfinite(qz_in) && isfinite(s0) && isfinite(s1) &&
         isfinite(s2))) {
     atomicOr(err, kErrCovNonFinite);
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
     rgb[ch] = rgb[ch] + 0.5f;
     rgb[ch] = (rgb[ch] < 0.0f) ? 0.0f : rgb[ch];
   }
-  const float opacity = det_sigmoidf(p[SK_COMP_OPACITY * stride + i], s_exp2);
+  const float opacity = det_sigmoidf(p[SK_COMP_OPACITY * stride + i], tab);
 
   BinOut bo;
   if (!bin_footprint(mx, my, c[0][0], c[0][1], c[1][0], c[1][1], inv00, inv01, inv11, opacity, bp.mode, bp.beta,
@@ -341,13 +342,13 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(int64_t n, BinPa
                                                                 const float* __restrict__ a_star,
                                                                 uint32_t* __restrict__ pair_tile,
                                                                 uint32_t* __restrict__ pair_val, int passes,
-                                                                uint32_t* __restrict__ hist) {
+                                                                int width, uint32_t* __restrict__ hist) {
   __shared__ uint32_t s_hist[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += kDupThreads) (&s_hist[0][0])[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   auto count_digits = [&](uint32_t t) {
-    for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(t >> (8 * p)) & 255u], 1u);
+    for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(t >> (width * p)) & ((1u << width) - 1u)], 1u);
   };
   const int64_t warps = (int64_t)gridDim.x * (kDupThreads / 32);
   for (int64_t wi = (int64_t)blockIdx.x * (kDupThreads / 32) + (threadIdx.x >> 5); wi * 32 < n; wi += warps) {
@@ -471,14 +472,14 @@ void launch_inject_bin(sk_ctx* ctx, sk_frame* f) {
 }
 
 void launch_duplicate(sk_ctx* ctx, sk_frame* f, const uint32_t* order, const int32_t* offsets, uint32_t* pair_tile,
-                      uint32_t* pair_val, int passes, uint32_t* hist) {
+                      uint32_t* pair_val, int passes, int width, uint32_t* hist) {
   if (f->n == 0) return;
   const BinParams bp = make_bin_params(f);
   const int64_t warps = (f->n + 31) / 32;
   const unsigned grid = (unsigned)std::min<int64_t>((warps + kDupThreads / 32 - 1) / (kDupThreads / 32), 148 * 8);
   duplicate_kernel<<<grid, kDupThreads, 0, ctx->stream>>>(
       f->n, bp, order, offsets, f->tiles.as<int>(), f->rect.as<int4>(), f->mean2d.as<float2>(),
-      f->conic_op.as<float4>(), f->a_star.as<float>(), pair_tile, pair_val, passes, hist);
+      f->conic_op.as<float4>(), f->a_star.as<float>(), pair_tile, pair_val, passes, width, hist);
   note_launch();
   SK_CUDA(cudaGetLastError());
 }

@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
   __shared__ int s_max_last;
   __shared__ float s_exp2[64];
   stage_exp2_table(s_exp2);
+  const SmemTable tab(s_exp2);
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
         float ge = FASTEXP ? __expf(-0.5f * q) : 0.0f;
         float raw = co.w * ge;
         if (!FASTEXP || fabsf(raw - kAlphaMin) <= 1e-5f * kAlphaMin || fabsf(raw - kAlphaCap) <= 1e-5f * kAlphaCap) {
-          ge = det_expf_core(rn_mul(-0.5f, q), s_exp2);
+          ge = det_expf_core(rn_mul(-0.5f, q), tab);
           raw = rn_mul(co.w, ge);
         }
         const bool capped = raw > kAlphaCap;

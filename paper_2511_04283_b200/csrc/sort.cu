@@ -57,14 +57,14 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // Upsweep: digit histograms of every pass in one read of the keys.
 __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int passes,
-                                                         uint32_t* __restrict__ hist) {
+                                                         int width, uint32_t* __restrict__ hist) {
   __shared__ uint32_t sh[kMaxPasses][kRadix];
   for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t k = keys[i];
-    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (p * kRadixBits)) & (kRadix - 1)], 1u);
+    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (p * width)) & ((1u << width) - 1u)], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
@@ -94,9 +94,9 @@ __global__ void radix_bases_kernel(uint32_t* __restrict__ hist) {
 }
 
 // One onesweep digit pass.
-__global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
+__global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
-    uint32_t* __restrict__ vals_out, int64_t n, int shift, const uint32_t* __restrict__ digit_base,
+    uint32_t* __restrict__ vals_out, int64_t n, int shift, uint32_t dmask, const uint32_t* __restrict__ digit_base,
     uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_hist[kSortWarps][kRadix];
@@ -114,28 +114,37 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
   const uint32_t tile = s_tile;
   const int64_t base = (int64_t)tile * kTile;
 
-  uint32_t k[kItems], v[kItems], d[kItems], rank[kItems];
+  // Out-of-range slots carry the key 0xffffffff and digit kRadix (never
+  // counted or written); the digit is recomputed from the key when needed.
+  uint32_t k[kItems], v[kItems], rank[kItems];
   const int64_t wbase = base + (int64_t)warp * (32 * kItems);
+  auto digit_of = [&](int j) -> uint32_t {
+    return wbase + j * 32 + lane < n ? ((k[j] >> shift) & dmask) : (uint32_t)kRadix;
+  };
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const int64_t idx = wbase + j * 32 + lane;
     const bool valid = idx < n;
     k[j] = valid ? keys_in[idx] : 0u;
     v[j] = valid ? vals_in[idx] : 0u;
-    d[j] = valid ? ((k[j] >> shift) & (kRadix - 1)) : (uint32_t)kRadix;
   }
   const uint32_t lt = lanemask_lt();
+  // All match_any results first (independent, so their latencies overlap),
+  // then the per-warp histogram updates in item order (stable ranking).
+  uint32_t peers[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) peers[j] = __match_any_sync(0xffffffffu, digit_of(j));
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
-    const uint32_t peers = __match_any_sync(0xffffffffu, d[j]);
-    const int leader = __ffs(peers) - 1;
+    const uint32_t dj = digit_of(j);
+    const int leader = __ffs(peers[j]) - 1;
     uint32_t old = 0;
-    if (lane == leader && d[j] < (uint32_t)kRadix) {
-      old = s_hist[warp][d[j]];
-      s_hist[warp][d[j]] = old + __popc(peers);
+    if (lane == leader && dj < (uint32_t)kRadix) {
+      old = s_hist[warp][dj];
+      s_hist[warp][dj] = old + __popc(peers[j]);
     }
     old = __shfl_sync(0xffffffffu, old, leader);
-    rank[j] = old + __popc(peers & lt);
+    rank[j] = old + __popc(peers[j] & lt);
     __syncwarp();
   }
   __syncthreads();
@@ -167,17 +176,32 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
     s_local[digit] = wb + x - total;
   }
 
-  // Decoupled look-back over preceding tiles for this digit.
+  // Decoupled look-back over preceding tiles for this digit, kLookback
+  // predecessors per step (independent loads in flight; slots before tile 0
+  // read as an inclusive zero). Stops at the first inclusive value, re-polls
+  // from the first slot that is not yet published.
   uint32_t excl = 0;
   if (tile > 0) {
+    constexpr int kLookback = 8;
     int64_t j = (int64_t)tile - 1;
-    while (j >= 0) {
-      const uint32_t s = ld_relaxed(status + (size_t)j * kRadix + digit);
-      const uint32_t flag = s & ~kValMask;
-      if (flag == 0) continue;
-      excl += s & kValMask;
-      if (flag == kFlagInc) break;
-      --j;
+    for (;;) {
+      uint32_t st[kLookback];
+#pragma unroll
+      for (int w = 0; w < kLookback; ++w)
+        st[w] = j - w >= 0 ? ld_relaxed(status + (size_t)(j - w) * kRadix + digit) : kFlagInc;
+      int used = 0;
+      bool found = false;
+#pragma unroll
+      for (int w = 0; w < kLookback; ++w) {
+        if (found || used < w) break;
+        const uint32_t flag = st[w] & ~kValMask;
+        if (flag == 0) break;
+        excl += st[w] & kValMask;
+        ++used;
+        found = flag == kFlagInc;
+      }
+      if (found) break;
+      j -= used;
     }
     st_relaxed(my_status, kFlagInc | (excl + total));
   }
@@ -187,8 +211,9 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
   // Scatter into shared memory in digit-sorted order.
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
-    if (d[j] < (uint32_t)kRadix) {
-      const uint32_t pos = s_local[d[j]] + s_hist[warp][d[j]] + rank[j];
+    const uint32_t dj = digit_of(j);
+    if (dj < (uint32_t)kRadix) {
+      const uint32_t pos = s_local[dj] + s_hist[warp][dj] + rank[j];
       s_keys[pos] = k[j];
       s_vals[pos] = v[j];
     }
@@ -198,7 +223,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
   const int count = rem < kTile ? (int)rem : kTile;
   for (int i = tid; i < count; i += kSortThreads) {
     const uint32_t key = s_keys[i];
-    const uint32_t dg = (key >> shift) & (kRadix - 1);
+    const uint32_t dg = (key >> shift) & dmask;
     const uint32_t out = s_global[dg] + (uint32_t)i - s_local[dg];
     keys_out[out] = key;
     vals_out[out] = s_vals[i];
@@ -250,25 +275,39 @@ __global__ void __launch_bounds__(kScanThreads) scan_gather_kernel(const int32_t
     block_total += s_warp[i];
   }
   long long thread_excl = wb + x - sum;
-  if (tid == 0) {
+  if (warp == 0) {
     unsigned long long* my = status + tile;
     if (tile == 0) {
-      st_relaxed64(my, kSFlagInc | (unsigned long long)block_total);
-      s_prefix = 0;
+      if (lane == 0) {
+        st_relaxed64(my, kSFlagInc | (unsigned long long)block_total);
+        s_prefix = 0;
+      }
     } else {
-      st_relaxed64(my, kSFlagAgg | (unsigned long long)block_total);
+      if (lane == 0) st_relaxed64(my, kSFlagAgg | (unsigned long long)block_total);
+      // warp-wide look-back: lane l reads tile j - l; slots before tile 0
+      // read as an inclusive zero
       long long excl = 0;
       int64_t j = (int64_t)tile - 1;
-      while (j >= 0) {
-        const unsigned long long s = ld_relaxed64(status + j);
+      for (;;) {
+        const int64_t jj = j - lane;
+        const unsigned long long s = jj >= 0 ? ld_relaxed64(status + jj) : kSFlagInc;
         const unsigned long long flag = s & ~kSValMask;
-        if (flag == 0) continue;
-        excl += (long long)(s & kSValMask);
-        if (flag == kSFlagInc) break;
-        --j;
+        const uint32_t zero = __ballot_sync(0xffffffffu, flag == 0);
+        const uint32_t inc = __ballot_sync(0xffffffffu, flag == kSFlagInc);
+        const int fz = zero ? __ffs(zero) - 1 : 32;
+        const int fi = inc ? __ffs(inc) - 1 : 32;
+        const int take = fi < fz ? fi + 1 : fz;  // lanes [0, take) are consumed
+        long long v = lane < take ? (long long)(s & kSValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (fi < fz) break;
+        j -= take;
       }
-      st_relaxed64(my, kSFlagInc | (unsigned long long)(excl + block_total));
-      s_prefix = excl;
+      if (lane == 0) {
+        st_relaxed64(my, kSFlagInc | (unsigned long long)(excl + block_total));
+        s_prefix = excl;
+      }
     }
   }
   __syncthreads();
@@ -325,10 +364,19 @@ uint32_t* radix_hist_buffer(sk_ctx* ctx) { return ensure<uint32_t>(ctx->sort.his
 
 int radix_passes(int bits) { return (bits + kRadixBits - 1) / kRadixBits; }
 
+// Digits are split evenly over the passes (13 tile bits -> 7 + 6): fewer
+// buckets per pass means longer digit runs and better-coalesced scatters.
+int radix_digit_width(int bits) {
+  const int passes = radix_passes(bits);
+  return (bits + passes - 1) / passes;
+}
+
 void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_t*& vals, uint32_t*& vals_alt,
                       int64_t n, int bits, bool hist_ready) {
   if (n <= 1 || bits <= 0) return;
   const int passes = radix_passes(bits);
+  const int width = radix_digit_width(bits);
+  const uint32_t dmask = (1u << width) - 1u;
   require(passes <= kMaxPasses, "radix_sort_pairs: at most 32 key bits");
   const int64_t tiles = (n + kTile - 1) / kTile;
   require(tiles < (1ll << 31), "radix_sort_pairs: too many keys");
@@ -340,14 +388,14 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
   if (!hist_ready) {
     SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s));
     const int hist_blocks = (int)std::min<int64_t>((n + 4095) / 4096, 148 * 8);
-    radix_hist_kernel<<<hist_blocks, 256, 0, s>>>(keys, n, passes, hist);
+    radix_hist_kernel<<<hist_blocks, 256, 0, s>>>(keys, n, passes, width, hist);
     note_launch();
   }
   radix_bases_kernel<<<passes, kRadix, 0, s>>>(hist);
   note_launch();
   for (int p = 0; p < passes; ++p) {
     SK_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t) * (size_t)tiles * kRadix, s));
-    onesweep_kernel<<<(unsigned)tiles, kSortThreads, 0, s>>>(keys, vals, keys_alt, vals_alt, n, p * kRadixBits,
+    onesweep_kernel<<<(unsigned)tiles, kSortThreads, 0, s>>>(keys, vals, keys_alt, vals_alt, n, p * width, dmask,
                                                               hist + p * kRadix, status, counters + p);
     note_launch();
     std::swap(keys, keys_alt);

@@ -133,7 +133,7 @@ void launch_inject_bin(sk_ctx* ctx, sk_frame* f);
 // Also accumulates the digit counts of the tile-id radix sort (passes digit
 // passes) into hist (see radix_hist_buffer), so the sort can skip its upsweep.
 void launch_duplicate(sk_ctx* ctx, sk_frame* f, const uint32_t* order, const int32_t* offsets, uint32_t* pair_tile,
-                      uint32_t* pair_val, int passes, uint32_t* hist);
+                      uint32_t* pair_val, int passes, int width, uint32_t* hist);
 
 // sort.cu
 // Stable LSD radix sort of (key, value) pairs on key bits [0, bits). On
@@ -143,6 +143,7 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
                       int64_t n, int bits, bool hist_ready = false);
 uint32_t* radix_hist_buffer(sk_ctx* ctx);  // [4][256] digit counts
 int radix_passes(int bits);
+int radix_digit_width(int bits);  // bits per digit pass (even split)
 // Exclusive scan of tiles[order[i]] into offsets[i]; returns the total.
 int64_t scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets, int64_t n);
 void launch_iota(sk_ctx* ctx, uint32_t* out, int64_t n);
