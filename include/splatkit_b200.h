@@ -287,6 +287,40 @@ typedef struct sk_dataset sk_dataset;
 int sk_dataset_create(sk_ctx* ctx, int n_views, const sk_camera* cams, const uint8_t* images,
                       const int32_t* train_indices, int n_train, float extent, sk_dataset** out);
 int sk_dataset_destroy(sk_dataset* d);
+int sk_dataset_num_views(const sk_dataset* d, int* n);
+int sk_dataset_camera(const sk_dataset* d, int view, sk_camera* out);
+/* Copies view `view`'s 8-bit GT image ([H][W][3]) to host memory. */
+int sk_dataset_image_u8(sk_ctx* ctx, const sk_dataset* d, int view, uint8_t* out);
+/* Train split (every 8th view is a test view, dataset.hpp:44-53). out may be
+ * NULL to query the count. */
+int sk_dataset_train_indices(const sk_dataset* d, int32_t* out, int* count);
+int sk_dataset_extent(const sk_dataset* d, float* extent);
+
+/* ---- scene construction on the device ----------------- */
+/* SynthSpec of generate_synthetic (dataset.hpp:178-250). width == height and
+ * scale_mult = 1, focal <= 0 reproduce the reference generator; the
+ * non-square size, (500/N)^(1/3) scale multiplier and focal override are the
+ * large-config extensions of SURVEY §8(d). */
+typedef struct sk_synth_spec {
+  int32_t n_gaussians, n_views, width, height;
+  uint64_t seed;
+  double scale_mult;
+  double focal; /* <= 0: 1.1 * height */
+} sk_synth_spec;
+/* generate_synthetic: GT Gaussians drawn with the reference Rng on the host
+ * (same draw order), camera ring, every GT view rendered by K1-K6 on the GPU
+ * and quantised through 8 bits into the dataset (device-resident), then the
+ * init point cloud (GT mu + noise, DC colour) and the scene extent.
+ * gt_out (SH degree 1), init_xyz / init_rgb ([n][3]) and extent_out may be
+ * NULL. */
+int sk_synthetic_create(sk_ctx* ctx, const sk_synth_spec* spec, sk_scene** gt_out, sk_dataset** data_out,
+                        float* init_xyz, float* init_rgb, float* extent_out);
+/* init_from_points (scene.hpp:117-141): log of the mean distance to the three
+ * nearest neighbours as isotropic log-scale, identity rotation, opacity
+ * logit(0.1), DC from the point colour, higher SH zero. Raises
+ * "init_from_points: empty point cloud" for n == 0. */
+int sk_init_from_points(sk_ctx* ctx, int64_t n, const float* xyz, const float* rgb, int sh_degree, int64_t capacity,
+                        sk_scene** out);
 
 typedef struct sk_trainer sk_trainer;
 /* Trainer(scene, data, cfg) (trainer.hpp:70-87). The trainer borrows scene and

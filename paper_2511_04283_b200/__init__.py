@@ -62,7 +62,7 @@ def lib():
     global _lib
     if _lib is None:
         if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} is missing: run paper_2511_04283_b200/build.py (no CPU fallback)")
+            raise ImportError(f"{LIB_PATH} is missing: run paper_2511_04283_b200.build() (no CPU fallback)")
         _lib = C.CDLL(LIB_PATH)
         _lib.sk_last_error.restype = C.c_char_p
         _lib.sk_last_error.argtypes = [C.c_void_p]
@@ -354,6 +354,22 @@ class Scene:
         self.h = h
         ctx.check(ctx._lib.sk_scene_upload(ctx.h, h, _p(p), C.c_int64(p.shape[1])))
 
+    @classmethod
+    def _wrap(cls, ctx: Context, handle, sh_degree: int) -> "Scene":
+        s = cls.__new__(cls)
+        s.ctx, s.sh_degree, s.h = ctx, sh_degree, handle
+        return s
+
+    @classmethod
+    def from_points(cls, ctx: Context, xyz, rgb, sh_degree: int, capacity=None) -> "Scene":
+        """init_from_points (scene.hpp:117-141); 3-NN distances on the GPU."""
+        xyz = np.ascontiguousarray(xyz, np.float32).reshape(-1, 3)
+        rgb = np.ascontiguousarray(rgb, np.float32).reshape(-1, 3)
+        h = C.c_void_p()
+        ctx.check(ctx._lib.sk_init_from_points(ctx.h, C.c_int64(xyz.shape[0]), _p(xyz), _p(rgb), C.c_int(sh_degree),
+                                               C.c_int64(capacity or xyz.shape[0]), C.byref(h)))
+        return cls._wrap(ctx, h, sh_degree)
+
     @property
     def size(self) -> int:
         n = C.c_int64()
@@ -585,8 +601,61 @@ def _ctx_methods():
 _ctx_methods()
 
 
+class SkSynthSpec(C.Structure):
+    _fields_ = [("n_gaussians", C.c_int32), ("n_views", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
+                ("seed", C.c_uint64), ("scale_mult", C.c_double), ("focal", C.c_double)]
+
+
 class Dataset:
     """Dataset<T> (dataset.hpp:24-32) resident in HBM (8-bit GT images)."""
+
+    @classmethod
+    def synthetic(cls, ctx: Context, n_gaussians=500, n_views=64, width=128, height=None, seed=1, scale_mult=1.0,
+                  focal=-1.0):
+        """generate_synthetic (dataset.hpp:178-250) with the GT views rendered
+        on the GPU. Returns (dataset, gt_scene (SH degree 1), init_xyz,
+        init_rgb)."""
+        height = width if height is None else height
+        spec = SkSynthSpec(n_gaussians, n_views, width, height, seed, scale_mult, focal)
+        xyz = np.zeros((n_gaussians, 3), np.float32)
+        rgb = np.zeros((n_gaussians, 3), np.float32)
+        ext = C.c_float()
+        g, d = C.c_void_p(), C.c_void_p()
+        ctx.check(ctx._lib.sk_synthetic_create(ctx.h, C.byref(spec), C.byref(g), C.byref(d), _p(xyz), _p(rgb),
+                                               C.byref(ext)))
+        ds = cls.__new__(cls)
+        ds.ctx, ds.h = ctx, d
+        return ds, Scene._wrap(ctx, g, 1), xyz, rgb
+
+    @property
+    def num_views(self) -> int:
+        n = C.c_int()
+        self.ctx._lib.sk_dataset_num_views(self.h, C.byref(n))
+        return n.value
+
+    @property
+    def extent(self) -> float:
+        e = C.c_float()
+        self.ctx._lib.sk_dataset_extent(self.h, C.byref(e))
+        return e.value
+
+    def camera(self, v) -> "SkCamera":
+        c = SkCamera()
+        self.ctx.check(self.ctx._lib.sk_dataset_camera(self.h, C.c_int(v), C.byref(c)))
+        return c
+
+    def image_u8(self, v) -> np.ndarray:
+        c = self.camera(v)
+        out = np.zeros((c.height, c.width, 3), np.uint8)
+        self.ctx.check(self.ctx._lib.sk_dataset_image_u8(self.ctx.h, self.h, C.c_int(v), _p(out)))
+        return out
+
+    def train_indices(self) -> np.ndarray:
+        cnt = C.c_int()
+        self.ctx._lib.sk_dataset_train_indices(self.h, None, C.byref(cnt))
+        out = np.zeros(cnt.value, np.int32)
+        self.ctx._lib.sk_dataset_train_indices(self.h, _p(out), C.byref(cnt))
+        return out
 
     def __init__(self, ctx: Context, cams, images_u8, train_indices=None, extent=1.0):
         self.ctx = ctx

@@ -365,6 +365,41 @@ int sk_dataset_destroy(sk_dataset* d) {
   return SK_OK;
 }
 
+int sk_dataset_num_views(const sk_dataset* d, int* n) {
+  if (!d || !n) return SK_ERR_INVALID_ARGUMENT;
+  *n = (int)d->cams.size();
+  return SK_OK;
+}
+
+int sk_dataset_camera(const sk_dataset* d, int view, sk_camera* out) {
+  if (!d || !out || view < 0 || view >= (int)d->cams.size()) return SK_ERR_INVALID_ARGUMENT;
+  *out = d->cams[view];
+  return SK_OK;
+}
+
+int sk_dataset_image_u8(sk_ctx* ctx, const sk_dataset* d, int view, uint8_t* out) {
+  return guarded(ctx, [&] {
+    arg(d && out && view >= 0 && view < (int)d->cams.size(), "sk_dataset_image_u8: bad arguments");
+    const sk_camera& c = d->cams[view];
+    d2h(ctx, out, d->images[view]->ptr, (size_t)c.width * c.height * 3);
+    sync(ctx);
+  });
+}
+
+int sk_dataset_train_indices(const sk_dataset* d, int32_t* out, int* count) {
+  if (!d || !count) return SK_ERR_INVALID_ARGUMENT;
+  if (out)
+    for (size_t i = 0; i < d->train.size(); ++i) out[i] = d->train[i];
+  *count = (int)d->train.size();
+  return SK_OK;
+}
+
+int sk_dataset_extent(const sk_dataset* d, float* extent) {
+  if (!d || !extent) return SK_ERR_INVALID_ARGUMENT;
+  *extent = d->extent;
+  return SK_OK;
+}
+
 int sk_trainer_create(sk_ctx* ctx, sk_scene* scene, const sk_dataset* data, const sk_train_config* cfg,
                       sk_trainer** out) {
   return guarded(ctx, [&] {
