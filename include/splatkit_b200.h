@@ -332,6 +332,11 @@ int sk_trainer_destroy(sk_trainer* t);
  * to cfg.iterations); rows may be NULL. */
 int sk_trainer_run(sk_trainer* t, int iterations, sk_log_row* rows);
 int sk_trainer_iteration(const sk_trainer* t, int* it);
+/* Resumes the schedule at iteration `it` (the next run() trains it + 1). */
+int sk_trainer_set_iteration(sk_trainer* t, int it);
+/* Trainer::density_event (trainer.hpp:177-243) now, outside the schedule:
+ * samples cfg.k training views, scores, selects and compacts. */
+int sk_trainer_density_event(sk_trainer* t, int iteration, int densify, int prune);
 /* Density-event records (for parity checks): header [7] = iteration,
  * n_before, n_after, n_clone, n_split, n_prune, k; flags are [n_before] u8. */
 int sk_trainer_record_events(sk_trainer* t, int on);

@@ -1117,6 +1117,7 @@ int or_trainer_run(or_trainer* h, int iters, double* log_rows, double* seconds) 
   });
 }
 int64_t or_trainer_size(const or_trainer* h) { return h->t->scene().size(); }
+void or_trainer_set_iteration(or_trainer* h, int it) { h->t->set_iteration(it); }
 int or_trainer_scene(const or_trainer* h, float* params) {
   scene_to_planar(h->t->scene(), params);
   return 0;

@@ -556,6 +556,9 @@ class Trainer:
         check(lib().or_trainer_run(C.c_void_p(self.h), C.c_int(iters), ptr(rows), C.byref(secs)))
         return rows, secs.value
 
+    def set_iteration(self, it):
+        lib().or_trainer_set_iteration(C.c_void_p(self.h), C.c_int(it))
+
     def scene(self):
         n = lib().or_trainer_size(self.h)
         p = np.zeros((n_components(self.deg), n), np.float32)

@@ -1965,6 +1965,9 @@ class Trainer {
   const ScoreTable<T>& table() const { return table_; }
   const std::vector<EventRecord>& events() const { return events_; }
   int iteration() const { return it_; }
+  // Test hook: resume the schedule at iteration `it` (exercises the late
+  // lazy SH-rest intervals without running 15000 iterations).
+  void set_iteration(int it) { it_ = it; }
   const SceneOptimizer<T>& optimizer() const { return optimizer_; }
 
   LogRow train_iteration(int it) {

@@ -692,6 +692,14 @@ class Trainer:
         if record_events:
             ctx._lib.sk_trainer_record_events(h, C.c_int(1))
 
+    def set_iteration(self, it):
+        self.ctx.check(self.ctx._lib.sk_trainer_set_iteration(self.h, C.c_int(it)))
+
+    def density_event(self, iteration, densify=True, prune=True):
+        """Trainer::density_event (trainer.hpp:177-243) outside the schedule."""
+        self.ctx.check(self.ctx._lib.sk_trainer_density_event(self.h, C.c_int(iteration), C.c_int(int(densify)),
+                                                              C.c_int(int(prune))))
+
     def run(self, iterations):
         rows = (SkLogRow * max(1, iterations))()
         self.ctx.check(self.ctx._lib.sk_trainer_run(self.h, C.c_int(iterations), rows))

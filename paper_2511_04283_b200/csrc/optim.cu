@@ -500,6 +500,77 @@ void launch_adam(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float posit
   SK_CUDA(cudaGetLastError());
 }
 
+__global__ void accumulate_rest_kernel(float* __restrict__ acc, const float* __restrict__ g, int64_t stride,
+                                       int64_t n, int c0, int c1) {
+  const int c = c0 + blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (int64_t)c * stride + i;
+    acc[o] = acc[o] + g[o];
+  }
+}
+
+__global__ void reset_opacity_kernel(float* __restrict__ op, float* __restrict__ m, float* __restrict__ v, int64_t n,
+                                     float cap) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float x = op[i];
+  op[i] = (cap < x) ? cap : x;  // std::min(x, cap)
+  m[i] = 0.0f;
+  v[i] = 0.0f;
+}
+
+void lazy_sh_rest(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, bool due) {
+  if (s->sh_degree == 0 || s->n == 0) return;
+  const int c0 = SK_COMP_SH + 3, c1 = s->comps;
+  const size_t bytes = sizeof(float) * (size_t)s->comps * s->capacity;
+  if (s->rest_n != s->n) {  // clear_rest() when the scene size changed
+    s->rest_accum.ensure(bytes);
+    SK_CUDA(cudaMemsetAsync(s->rest_accum.ptr, 0, bytes, ctx->stream));
+    s->rest_n = s->n;
+    s->rest_stride = s->capacity;
+  } else if (s->rest_stride != s->capacity) {  // same size, re-strided buffers: keep the values
+    DevBuf nb;
+    nb.ensure(bytes);
+    SK_CUDA(cudaMemsetAsync(nb.ptr, 0, bytes, ctx->stream));
+    SK_CUDA(cudaMemcpy2DAsync(nb.ptr, sizeof(float) * s->capacity, s->rest_accum.ptr, sizeof(float) * s->rest_stride,
+                              sizeof(float) * s->n, s->comps, cudaMemcpyDeviceToDevice, ctx->stream));
+    s->rest_accum.swap(nb);
+    s->rest_stride = s->capacity;
+  }
+  const dim3 grid((unsigned)std::min<int64_t>((s->n + 255) / 256, 64), (unsigned)(c1 - c0));
+  accumulate_rest_kernel<<<grid, 256, 0, ctx->stream>>>(s->rest_accum.as<float>(), s->grads.as<float>(), s->capacity,
+                                                        s->n, c0, c1);
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+  if (!due) return;
+  // SceneOptimizer::step_sh_rest: the SH-rest group alone, on the accumulator
+  AdamParams ap = make_adam(s, lrs, 0.0f, true);
+  for (int g = 0; g < 5; ++g) {
+    if (ap.active[g]) s->adam_t[g] -= 1;  // make_adam counted every group; only SH-rest steps here
+    ap.active[g] = 0;
+  }
+  const int64_t per_comp = std::max<int64_t>(1, (int64_t)148 * 16 / s->comps);
+  const int64_t need = (s->n / 4 + kAdamThreads - 1) / kAdamThreads;
+  const dim3 agrid((unsigned)std::max<int64_t>(1, std::min(need, per_comp)), (unsigned)s->comps);
+  adam_kernel<<<agrid, kAdamThreads, 0, ctx->stream>>>(s->params.as<float>(), s->rest_accum.as<float>(),
+                                                       s->adam_m.as<float>(), s->adam_v.as<float>(), s->capacity,
+                                                       s->n, ap);
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+  SK_CUDA(cudaMemsetAsync(s->rest_accum.ptr, 0, bytes, ctx->stream));
+}
+
+void reset_opacity(sk_ctx* ctx, sk_scene* s) {
+  ensure_optimizer_state(ctx, s);
+  if (s->n == 0) return;
+  const float cap = std::log(0.01f / (1.0f - 0.01f));  // logit(T(0.01)), host libm as the reference
+  const int64_t o = (int64_t)SK_COMP_OPACITY * s->capacity;
+  reset_opacity_kernel<<<(unsigned)((s->n + 255) / 256), 256, 0, ctx->stream>>>(
+      s->params.as<float>() + o, s->adam_m.as<float>() + o, s->adam_v.as<float>() + o, s->n, cap);
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+}
+
 // Single-GPU step: K9 into the gradient buffer, then the streaming K10. (A
 // single fused kernel keeps the gradients on chip but is instruction-bound at
 // the occupancy its 59-gradient live range allows; split, K10 runs at HBM

@@ -67,6 +67,10 @@ struct sk_scene {
   sk::DevBuf adam_m;      // [comps][capacity]
   sk::DevBuf adam_v;      // [comps][capacity]
   int64_t adam_t[6] = {0, 0, 0, 0, 0, 0};  // pos, rot, scale, opacity, sh_dc, sh_rest
+  // Lazy SH-rest accumulator of the Trainer (trainer.hpp:160-169): [comps][capacity]
+  // (only the SH-rest rows are used); rest_n = scene size it was cleared for.
+  sk::DevBuf rest_accum;
+  int64_t rest_n = -1, rest_stride = 0;
   // ScoreTable (adc.hpp:23-45), device SoA, all [capacity] (grad3d [3][capacity])
   sk::DevBuf s_d, s_p_raw, s_p, grad_norm_acc, abs_grad_acc, grad3d_acc, views_seen, max_radius2d;
 };
@@ -173,6 +177,13 @@ void launch_project_backward(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stat
 void launch_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const LearningRates& lrs, float position_lr,
                                   bool update_sh_rest, bool do_stats);
 void launch_adam(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float position_lr, bool update_sh_rest);
+// Lazy SH-rest (trainer.hpp:160-169, adam.hpp:146-159): rest_accum += the SH-rest
+// gradients; when due, an Adam step of the SH-rest group on the accumulator,
+// which is then cleared.
+void lazy_sh_rest(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, bool due);
+// Trainer::reset_opacity (trainer.hpp:245-249): opacity_logit = min(.,
+// logit(0.01)), the opacity group's Adam moments zeroed.
+void reset_opacity(sk_ctx* ctx, sk_scene* s);
 
 // pipeline.cu
 void arg(bool ok, const char* msg);  // throws std::invalid_argument

@@ -101,13 +101,19 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   ctx->mark(5);
   const LearningRates lrs = lrs_from(cfg);
   const float pos_lr = expon_lr(lrs.position * extent, lrs.position_final * extent, it, cfg.iterations);
-  require(!cfg.lazy_opt_enabled, "trainer: lazy_opt_enabled is not supported on the GPU path yet");
   // K9 into the gradient buffer (+ C1 sum over ranks on a view-parallel
   // step), then K10
   launch_project_backward(ctx, scene, f, true);
   if (comm && comm->world > 1) allreduce_grads(comm, scene, ctx->stream);
   ctx->mark(6);
-  launch_adam(ctx, scene, lrs, pos_lr, true);
+  if (!cfg.lazy_opt_enabled) {
+    launch_adam(ctx, scene, lrs, pos_lr, true);
+  } else {
+    // trainer.hpp:160-169: SH-rest excluded from the step, accumulated, and
+    // stepped on the accumulated gradient when lazy_update_due
+    launch_adam(ctx, scene, lrs, pos_lr, false);
+    lazy_sh_rest(ctx, scene, lrs, lazy_update_due(it, cfg));
+  }
   ctx->mark(7);
   LossSums sums{};
   read_loss_sums(ctx, &sums);  // synchronises the stream
@@ -433,6 +439,21 @@ int sk_trainer_iteration(const sk_trainer* t, int* it) {
   return SK_OK;
 }
 
+int sk_trainer_set_iteration(sk_trainer* t, int it) {
+  if (!t || it < 0) return SK_ERR_INVALID_ARGUMENT;
+  t->it = it;
+  return SK_OK;
+}
+
+int sk_trainer_density_event(sk_trainer* t, int iteration, int densify, int prune) {
+  if (!t) return SK_ERR_INVALID_ARGUMENT;
+  return guarded(t->ctx, [&] {
+    SK_CUDA(cudaSetDevice(t->ctx->device));
+    require(!t->data->train.empty(), "accumulate_scores: no training views");
+    density_event(t, iteration, densify != 0, prune != 0);
+  });
+}
+
 // Trainer::run (trainer.hpp:89-119): step, then the due density event.
 int sk_trainer_run(sk_trainer* t, int iterations, sk_log_row* rows) {
   if (!t) return SK_ERR_INVALID_ARGUMENT;
@@ -465,8 +486,8 @@ int sk_trainer_run(sk_trainer* t, int iterations, sk_log_row* rows) {
       const bool prn = prune_due(it, t->cfg);
       row.event = (dens ? 1 : 0) | (prn ? 2 : 0);
       if (!t->cfg.schedule_dry_run && (dens || prn)) density_event(t, it, dens, prn);
-      require(t->cfg.opacity_reset_every <= 0 || t->cfg.schedule_dry_run,
-              "trainer: opacity_reset_every is not supported on the GPU path yet");
+      if (!t->cfg.schedule_dry_run && t->cfg.opacity_reset_every > 0 && it % t->cfg.opacity_reset_every == 0)
+        reset_opacity(t->ctx, t->scene);  // Trainer::reset_opacity (trainer.hpp:104-106, 245-249)
       row.gaussians = (int32_t)t->scene->n;
       row.elapsed_ms =
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t->start).count();
