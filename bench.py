@@ -46,6 +46,9 @@ def parse_args():
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no baselines, no clocks)")
+    ap.add_argument("--workload", choices=["train", "event"], default="train",
+                    help="train: config-2 training iteration (default); event: config-3 density event")
+    ap.add_argument("--views", type=int, default=64, help="event workload: scored views (K)")
     return ap.parse_args()
 
 
@@ -438,11 +441,111 @@ def cpu_baseline(args, params, cam, gt8, extent):
         return {"value": None, "unit": "iter/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
 
 
+# ---------------------------------------------------------------------------
+# config 3: the multi-view importance pass + densify / prune compaction
+# ---------------------------------------------------------------------------
+
+def run_event(args, world, rank, local):
+    """BASELINE config 3: 1M Gaussians scored over K=64 1080p views
+    (K6 + K11 + K12 per view, K13 scores), then K14 selection and K15
+    compaction, through Trainer::density_event. Scene: the GT of the GPU
+    synthetic generator padded to SH degree 3, with 20% of the Gaussians' DC
+    and opacity perturbed (seed 3); accumulators synthetic (grad ~ U(0, 6e-4),
+    views_seen in [1, 10]). Timed at iteration 1000 (densify + prune) and
+    20000 (late prune); the scene is restored before every timed event."""
+    import torch
+
+    import paper_2511_04283_b200 as sk
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = sk.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.check(ctx._lib.sk_ctx_set_stream(ctx.h, sk.C.c_void_p(stream.cuda_stream)))
+    n, k = args.n, args.views
+    t0 = time.perf_counter()
+    ds, gt, xyz, rgb = sk.Dataset.synthetic(ctx, n_gaussians=n, n_views=k, width=args.width, height=args.height,
+                                            seed=1, scale_mult=(500.0 / n) ** (1.0 / 3.0) if n >= 100_000 else 1.0,
+                                            focal=1.1 * args.height * 2.6)
+    gen_s = time.perf_counter() - t0
+    ds.set_train_indices(np.arange(k))  # K = all views
+    p1 = gt.download()
+    p = np.zeros((sk.n_components(3), n), np.float32)
+    p[: p1.shape[0]] = p1
+    rng = np.random.default_rng(3)
+    sel = rng.random(n) < 0.2
+    p[10, sel] += rng.normal(0.0, 1.0, int(sel.sum())).astype(np.float32)
+    p[11:14, sel] += rng.normal(0.0, 0.5, (3, int(sel.sum()))).astype(np.float32)
+    vs = rng.integers(1, 11, n).astype(np.int32)
+    grad = rng.uniform(0, 6e-4, n).astype(np.float32)
+    absg = rng.uniform(0, 6e-4, n).astype(np.float32)
+    g3 = rng.normal(0, 1e-4, (n, 3)).astype(np.float32)
+    rad = rng.uniform(0, 30, n).astype(np.float32)
+    cfg = train_config(sk)
+    cfg.k = k
+    scene = ctx.scene(p, 3, capacity=2 * n)
+    tr = sk.Trainer(ctx, scene, ds, cfg)
+    comm = None
+    if world > 1:
+        comm = sk.Comm.from_torch(ctx, dist, rank, world)
+        tr.set_comm(comm)
+
+    def restore():
+        ctx.check(ctx._lib.sk_scene_upload(ctx.h, scene.h, sk._p(p), sk.C.c_int64(n)))
+        scene.set_score_table(grad_norm_acc=grad * vs, abs_grad_acc=absg * vs, grad3d_acc=g3, views_seen=vs,
+                              max_radius2d=rad)
+
+    def timed(iteration, densify, prune):
+        restore()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        tr.density_event(iteration, densify, prune)
+        torch.cuda.synchronize()
+        ms = 1000.0 * (time.perf_counter() - a)
+        if dist is not None:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, scene.size
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        timed(1000, True, True)
+    reps = max(1, min(args.steps, 5))
+    early = [timed(1000, True, True) for _ in range(reps)]
+    late = [timed(20000, False, True) for _ in range(reps)]
+    if rank != 0:
+        return
+    e_ms = statistics.median(x[0] for x in early)
+    l_ms = statistics.median(x[0] for x in late)
+    line = {
+        "metric": "density event ms (config 3: 1M Gaussians, 64 views 1080p, score + select + compact)",
+        "value": e_ms, "unit": "ms/event", "n_gpus": world, "steps": reps, "warmup": max(1, min(args.warmup, 2)),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (GPU generator, reference Rng draw order); scene restored before each event",
+        "config": {"workload": "config3: multi-view importance pass over K views + densify/prune compaction",
+                   "n_gaussians": n, "views": k, "width": args.width, "height": args.height,
+                   "timing": "wall clock around Trainer::density_event with device syncs, median"},
+        "early_event_ms": e_ms, "late_event_ms": l_ms,
+        "views_scored_per_s": k / (e_ms * 1e-3),
+        "n_after_early": early[-1][1], "n_after_late": late[-1][1],
+        "generator_s": gen_s,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, world, rank)
+        return
+    if args.workload == "event":
+        run_event(args, world, rank, local)
         return
     run_ours(args, world, rank, local)
 

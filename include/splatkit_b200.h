@@ -295,6 +295,7 @@ int sk_dataset_image_u8(sk_ctx* ctx, const sk_dataset* d, int view, uint8_t* out
  * NULL to query the count. */
 int sk_dataset_train_indices(const sk_dataset* d, int32_t* out, int* count);
 int sk_dataset_extent(const sk_dataset* d, float* extent);
+int sk_dataset_set_train_indices(sk_dataset* d, const int32_t* idx, int count);
 
 /* ---- scene construction on the device ----------------- */
 /* SynthSpec of generate_synthetic (dataset.hpp:178-250). width == height and

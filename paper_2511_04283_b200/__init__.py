@@ -650,6 +650,12 @@ class Dataset:
         self.ctx.check(self.ctx._lib.sk_dataset_image_u8(self.ctx.h, self.h, C.c_int(v), _p(out)))
         return out
 
+    def set_train_indices(self, idx):
+        idx = np.ascontiguousarray(idx, np.int32)
+        rc = self.ctx._lib.sk_dataset_set_train_indices(self.h, _p(idx), C.c_int(len(idx)))
+        if rc != SK_OK:
+            raise ValueError("dataset: train index out of range")
+
     def train_indices(self) -> np.ndarray:
         cnt = C.c_int()
         self.ctx._lib.sk_dataset_train_indices(self.h, None, C.byref(cnt))

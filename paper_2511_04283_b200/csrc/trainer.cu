@@ -400,6 +400,14 @@ int sk_dataset_train_indices(const sk_dataset* d, int32_t* out, int* count) {
   return SK_OK;
 }
 
+int sk_dataset_set_train_indices(sk_dataset* d, const int32_t* idx, int count) {
+  if (!d || !idx || count <= 0) return SK_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < count; ++i)
+    if (idx[i] < 0 || idx[i] >= (int)d->cams.size()) return SK_ERR_INVALID_ARGUMENT;
+  d->train.assign(idx, idx + count);
+  return SK_OK;
+}
+
 int sk_dataset_extent(const sk_dataset* d, float* extent) {
   if (!d || !extent) return SK_ERR_INVALID_ARGUMENT;
   *extent = d->extent;
