@@ -120,8 +120,9 @@ int sk_ctx_launch_count(const sk_ctx*, int64_t* out) {
 int sk_ctx_enable_timing(sk_ctx* ctx, int on) {
   return guarded(ctx, [&] {
     set_device(ctx);
-    if (on && !ctx->tev[0])
-      for (auto& e : ctx->tev) SK_CUDA(cudaEventCreate(&e));
+    if (on && !ctx->tev[0][0])
+      for (auto& set : ctx->tev)
+        for (auto& e : set) SK_CUDA(cudaEventCreate(&e));
     ctx->timing = on != 0;
   });
 }

@@ -46,11 +46,12 @@ struct sk_ctx {
   sk::HostBuf pinned;   // staging
   // phase timing (sk_ctx_enable_timing)
   bool timing = false;
-  cudaEvent_t tev[SK_NUM_PHASES + 1] = {};
+  cudaEvent_t tev[2][SK_NUM_PHASES + 1] = {};  // two sets: a deferred step is read while the next records
+  int tev_set = 0;
   double phase_ms[SK_NUM_PHASES] = {};
   int64_t timed_steps = 0;
   void mark(int i) {
-    if (timing) cudaEventRecord(tev[i], stream);
+    if (timing) cudaEventRecord(tev[tev_set][i], stream);
   }
 };
 

@@ -79,16 +79,54 @@ bool lazy_update_due(int it, const sk_train_config& c) {
 
 // One train_iteration (trainer.hpp:124-175) on camera `cam` with the 8-bit GT
 // already on the device.
+void finish_pending(sk_ctx* ctx, PendingStep* pend) {
+  if (!pend || !pend->active) return;
+  pend->active = false;
+  SK_CUDA(cudaEventSynchronize(pend->done));
+  const double* h = static_cast<const double*>(pend->pinned.ptr) + 5 * pend->slot;
+  uint32_t bits = 0;
+  memcpy(&bits, h + 4, sizeof(bits));
+  if (bits) {
+    SK_CUDA(cudaMemsetAsync(ctx->err_word.ptr, 0, sizeof(uint32_t), ctx->stream));
+    raise_device_errors(bits);
+  }
+  if (ctx->timing) {
+    for (int i = 0; i < SK_NUM_PHASES; ++i) {
+      float ms = 0.0f;
+      SK_CUDA(cudaEventElapsedTime(&ms, ctx->tev[pend->tev_set][i], ctx->tev[pend->tev_set][i + 1]));
+      ctx->phase_ms[i] += ms;
+    }
+    ctx->timed_steps += 1;
+  }
+  if (pend->row) {
+    const LossSums sums{h[0], h[1], h[2]};
+    sk_loss_values v{};
+    finish_loss(pend->width, pend->height, pend->lambda, sums, &v);
+    pend->row->iteration = pend->it;
+    pend->row->loss = v.loss;
+    pend->row->psnr = v.psnr;
+    pend->row->tile_pairs = pend->pairs;
+    pend->row->gaussians = (int32_t)pend->n;
+  }
+}
+
+// One train_iteration (trainer.hpp:124-175) on camera `cam` with the 8-bit GT
+// already on the device.
 void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam, const uint8_t* gt_dev,
-                const sk_train_config& cfg, float extent, int it, sk_log_row* row, const sk_comm* comm) {
+                const sk_train_config& cfg, float extent, int it, sk_log_row* row, const sk_comm* comm,
+                PendingStep* pend) {
   const sk_binning bin = binning_from(cfg);
   frame_geometry(f, cam.width, cam.height, &bin);
   f->camera = cam;
   ensure_projected(f, scene->n);
   ensure_image(f);
   ensure<float>(f->bgrads, (size_t)kBGradFields * std::max<int64_t>(f->n, 1));
+  if (pend) ctx->tev_set ^= 1;  // the pending step's events stay intact
   ctx->mark(0);
   launch_preprocess(ctx, scene, cam, f);
+  // the previous step's readback completes while K1 of this step runs (the
+  // scene it reports is final: K1 only reads it)
+  if (pend) finish_pending(ctx, pend);
   ctx->mark(1);
   bin_sort(ctx, f);
   ctx->mark(2);
@@ -115,13 +153,33 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
     lazy_sh_rest(ctx, scene, lrs, lazy_update_due(it, cfg));
   }
   ctx->mark(7);
+  if (pend) {
+    if (!pend->done) SK_CUDA(cudaEventCreateWithFlags(&pend->done, cudaEventDisableTiming));
+    double* h = static_cast<double*>(pend->pinned.ensure(2 * 5 * sizeof(double)));
+    pend->slot ^= 1;
+    SK_CUDA(cudaMemcpyAsync(h + 5 * pend->slot, ctx->scalars.ptr, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    SK_CUDA(cudaMemcpyAsync(h + 5 * pend->slot + 4, ctx->err_word.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    SK_CUDA(cudaEventRecord(pend->done, ctx->stream));
+    pend->active = true;
+    pend->it = it;
+    pend->width = f->width;
+    pend->height = f->height;
+    pend->lambda = (float)cfg.lambda;
+    pend->pairs = f->pairs;
+    pend->n = scene->n;
+    pend->row = row;
+    pend->tev_set = ctx->tev_set;
+    return;
+  }
   LossSums sums{};
   read_loss_sums(ctx, &sums);  // synchronises the stream
   raise_device_errors(read_error_word(ctx));
   if (ctx->timing) {
     for (int i = 0; i < SK_NUM_PHASES; ++i) {
       float ms = 0.0f;
-      SK_CUDA(cudaEventElapsedTime(&ms, ctx->tev[i], ctx->tev[i + 1]));
+      SK_CUDA(cudaEventElapsedTime(&ms, ctx->tev[ctx->tev_set][i], ctx->tev[ctx->tev_set][i + 1]));
       ctx->phase_ms[i] += ms;
     }
     ctx->timed_steps += 1;
@@ -473,9 +531,16 @@ int sk_trainer_run(sk_trainer* t, int iterations, sk_log_row* rows) {
     }
     const int last = std::min(t->cfg.iterations, t->it + std::max(0, iterations));
     int r = 0;
+    std::vector<sk_log_row> scratch(rows ? 0 : 2);
+    // a failed run must not leave a step pending against the caller's rows
+    struct Flush {
+      sk_trainer* t;
+      ~Flush() { t->pending.active = false; }
+    } flush{t};
     while (t->it < last) {
       const int it = ++t->it;
-      sk_log_row row{};
+      sk_log_row& row = rows ? rows[r] : scratch[r & 1];
+      row = sk_log_row{};
       row.iteration = it;
       if (!t->cfg.schedule_dry_run) {
         // one shared Rng draw per rank, in rank order; rank r trains view r
@@ -487,21 +552,25 @@ int sk_trainer_run(sk_trainer* t, int iterations, sk_log_row* rows) {
           if (r == rank) view = v;
         }
         row.view = view;
+        // the row's loss / PSNR arrive one step late (PendingStep)
         train_step(t->ctx, t->scene, &t->frame, t->data->cams[view], t->data->images[view]->as<uint8_t>(), t->cfg,
-                   t->data->extent, it, &row, t->comm);
+                   t->data->extent, it, &row, t->comm, &t->pending);
       }
       const bool dens = densify_due(it, t->cfg);
       const bool prn = prune_due(it, t->cfg);
       row.event = (dens ? 1 : 0) | (prn ? 2 : 0);
-      if (!t->cfg.schedule_dry_run && (dens || prn)) density_event(t, it, dens, prn);
+      if (!t->cfg.schedule_dry_run && (dens || prn)) {
+        finish_pending(t->ctx, &t->pending);
+        density_event(t, it, dens, prn);
+      }
       if (!t->cfg.schedule_dry_run && t->cfg.opacity_reset_every > 0 && it % t->cfg.opacity_reset_every == 0)
         reset_opacity(t->ctx, t->scene);  // Trainer::reset_opacity (trainer.hpp:104-106, 245-249)
       row.gaussians = (int32_t)t->scene->n;
       row.elapsed_ms =
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t->start).count();
-      if (rows) rows[r] = row;
       ++r;
     }
+    finish_pending(t->ctx, &t->pending);
   });
 }
 

@@ -71,6 +71,25 @@ struct EventRecord {
   std::vector<uint8_t> clone, split, prune;  // pre-event flags [n_before]
 };
 
+namespace sk {
+// A training step whose loss / error-word readback is deferred: the host
+// reads it while the next step's first kernels run, so the GPU does not idle
+// on the end-of-step synchronisation (Trainer::run only).
+struct PendingStep {
+  bool active = false;
+  int it = 0, width = 0, height = 0, tev_set = 0;
+  float lambda = 0.2f;
+  int64_t pairs = 0, n = 0;
+  sk_log_row* row = nullptr;
+  cudaEvent_t done = nullptr;
+  HostBuf pinned;  // [2 slots][4 doubles + error word]
+  int slot = 0;
+  ~PendingStep() {
+    if (done) cudaEventDestroy(done);
+  }
+};
+}  // namespace sk
+
 struct sk_trainer {
   sk_ctx* ctx = nullptr;
   sk_scene* scene = nullptr;
@@ -84,6 +103,7 @@ struct sk_trainer {
   bool record_events = false;
   std::vector<EventRecord> events;
   sk_comm* comm = nullptr;  // view sharding across ranks (nullptr: single GPU)
+  sk::PendingStep pending;
 };
 
 namespace sk {
@@ -94,8 +114,15 @@ sk_binning binning_from(const sk_train_config& c);
 void validate_config(const sk_train_config& c);
 bool densify_due(int it, const sk_train_config& c);
 bool prune_due(int it, const sk_train_config& c);
+// pend == nullptr: synchronous (the row is complete on return). Otherwise the
+// step's readback is left pending in *pend and the previous pending step is
+// completed right after this step's first kernel is queued.
 void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam, const uint8_t* gt_dev,
-                const sk_train_config& cfg, float extent, int it, sk_log_row* row, const sk_comm* comm = nullptr);
+                const sk_train_config& cfg, float extent, int it, sk_log_row* row, const sk_comm* comm = nullptr,
+                PendingStep* pend = nullptr);
+// Completes a pending step: waits for it, fills its row, adds its phase
+// times, raises its device errors.
+void finish_pending(sk_ctx* ctx, PendingStep* pend);
 
 // density.cu: Trainer::density_event (trainer.hpp:177-243).
 void density_event(sk_trainer* t, int it, bool densify, bool prune);
