@@ -139,18 +139,21 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
       const float a2 = 2.0f * (mom[4][r] - mx * my) + C2;
       const float b1 = mx * mx + my * my + C1;
       const float b2 = (mom[2][r] - mx * mx) + (mom[3][r] - my * my) + C2;
-      const float s = (a1 * a2) / (b1 * b2);
+      // fast reciprocals (2 ulp): the loss is checked against the oracle
+      // within a tolerance; the IEEE divisions cost ~4x the instructions
+      const float inv_bb = __fdividef(1.0f, b1 * b2);
+      const float s = (a1 * a2) * inv_bb;
       ss += (double)s;
       const size_t p = (size_t)py * W + px;
       const float diff = s_x[vy0 + r + kHalo][vx + kHalo] - s_y[vy0 + r + kHalo][vx + kHalo];
       l1 += (double)fabsf(diff);
       sq += (double)diff * (double)diff;
       if (want_grad) {
-        const float inv_bb = 1.0f / (b1 * b2);
+        const float s_b1 = s * __fdividef(1.0f, b1), s_b2 = s * __fdividef(1.0f, b2);
         partials[(0 * 3 + ch) * plane + p] =
-            nrm * (a2 * inv_bb * 2.0f * my - a1 * inv_bb * 2.0f * my - s / b1 * 2.0f * mx + s / b2 * 2.0f * mx);
+            nrm * (a2 * inv_bb * 2.0f * my - a1 * inv_bb * 2.0f * my - s_b1 * 2.0f * mx + s_b2 * 2.0f * mx);
         partials[(1 * 3 + ch) * plane + p] = nrm * (a1 * inv_bb * 2.0f);
-        partials[(2 * 3 + ch) * plane + p] = nrm * (-s / b2);
+        partials[(2 * 3 + ch) * plane + p] = nrm * (-s_b2);
         const float sg = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
         dimage[ch * plane + p] = (1.0f - lambda) * sg * inv_n;
       }
