@@ -196,30 +196,45 @@ def run_reference(args, world, rank):
 PHASES = ["K1 preprocess", "K2-K5 bin+sort", "K6 blend fwd", "K7 loss", "K8 blend bwd", "K9 proj-bwd", "K10 Adam"]
 
 
-def algorithmic_bytes(phase, n, visible, pairs, pixels, comps=59):
-    """Algorithmic HBM bytes per launch of each phase (Roofline)."""
-    if phase == 0:  # K1: 59 parameters read, 104 B of projected record written per visible
-        return 4 * comps * n + 104 * visible
-    if phase == 1:  # K2-K5: depth sort (4 passes x 16 B/key), scan, emit, 2 tile passes, ranges
-        return 64 * n + 8 * n + 8 * pairs + 32 * pairs + 4 * pairs
-    if phase == 2:  # K6: per pair index + 40 B record; per pixel image, T, count, last (24 B)
-        return 44 * pairs + 24 * pixels
-    if phase == 3:  # K7: rendered (12 B) + GT (3 B) read, dL/dimage (12 B) written per pixel
-        return 27 * pixels
-    if phase == 4:  # K8: per pair index + 40 B record; per pixel T, last, dL/dimage (20 B);
-        return 44 * pairs + 20 * pixels + 44 * visible  # 11 gradient floats per visible
-    if phase == 5:  # K9: params + blend grads + conic/radius + stats in, grads out
-        return 4 * comps * n * 2 + (44 + 16 + 4 + 56) * visible
-    if phase == 6:  # K10: params, m, v read + written, gradient read (28 B per scalar)
+def algorithmic_bytes(phase, n, visible, pairs, pixels, tiles, comps=59):
+    """Algorithmic HBM bytes per launch of each phase, SURVEY.md §8(d)'s
+    per-unit figures x the units one launch processes."""
+    culled = n - visible
+    if phase == 0:  # K1: 236 B params read + 52 B projected record written per visible, 44 B per culled
+        return (4 * comps + 52) * visible + 44 * culled
+    if phase == 1:  # K2 scan 8 B/Gaussian; K3 12 B/pair + 20 B/visible; K4 8 + 6x24 B/pair; K5 8 B/pair + 8 B/tile
+        return 8 * n + 12 * pairs + 20 * visible + 152 * pairs + 8 * pairs + 8 * tiles
+    if phase == 2:  # K6 HBM side: 36 B per pair + 20 B per pixel
+        return 36 * pairs + 20 * pixels
+    if phase == 3:  # K7: 36 B per pixel minimum (read r, g; write dL)
+        return 36 * pixels
+    if phase == 4:  # K8 HBM side: per pair record + per pixel T, last, dL/dimage + 11 gradient floats per visible
+        return 36 * pairs + 20 * pixels + 44 * visible
+    if phase == 5:  # K9: 236 B read + 44 B blend grads + 236 B written + 56 B stats RMW per visible
+        return (4 * comps * 2 + 44 + 56) * visible
+    if phase == 6:  # K10 Adam: 59 x 28 B per Gaussian
         return 28 * comps * n
     return 0
 
 
-# Algorithmic fp32 operations per contributing pixel-Gaussian pair (alpha >=
-# 1/255): the reference's per-entry arithmetic (raster.hpp:225-234 forward,
-# :306-345 backward), counting the exp as its 10-flop table evaluation.
-FLOP_FWD_PER_CONTRIB = 30
-FLOP_BWD_PER_CONTRIB = 70
+def implementation_bytes(phase, n, visible, pairs, pixels):
+    """Bytes the kernels of this implementation must move at minimum (the
+    B200 design moves less than the SURVEY's per-pair sort figure: one 4-pass
+    depth sort over N slots + a 2-pass 32-bit tile sort)."""
+    if phase == 0:
+        return 4 * 59 * n + 104 * visible
+    if phase == 1:
+        return 64 * n + 8 * n + 8 * pairs + 32 * pairs + 4 * pairs
+    return None
+
+
+# SURVEY §8(d) FP32 work of the blend kernels per pixel-Gaussian evaluation:
+# forward 14 flop per visited + 9 per contributing (+1 ex2 per visited);
+# backward 14 per visited + 52 per contributing (+1 ex2 per visited, +1 ex2
+# and 1 division per contributing). "Visited" = the entries the reference's
+# per-pixel loop examines (raster.hpp:219-235), measured by sk_frame_pge_counts.
+FLOP_FWD = (14, 9)
+FLOP_BWD = (14, 52)
 
 
 def ncu_traffic(kernel_prefix):
@@ -341,35 +356,57 @@ def run_ours(args, world, rank, local):
     visible = int(prj.visible.sum())
     pairs = int(rows[-1]["tile_pairs"]) if rows else 0
     pixels = args.width * args.height
-    # contributing pixel-Gaussian pairs of this view (sum of per-pixel counts)
+    tiles = ((args.width + 15) // 16) * ((args.height + 15) // 16)
+    # workload units of this view: the reference loop's visited
+    # and contributing pixel-Gaussian evaluations
     ctx.project_scene(scene, cam)
     ctx.build_tile_grid()
-    contribs = int(ctx.blend_forward().contrib.astype(np.int64).sum())
-    dom = int(np.argmax(phase_avg))
-    alg = algorithmic_bytes(dom, args.n, visible, pairs, pixels)
-    achieved = alg / (phase_avg[dom] * 1e-3) / 1e9
+    ctx.blend_forward()
+    visited, contribs = ctx.pge_counts()
     clocks = clock.summary()
-    kernel_of = {4: "blend_bwd_kernel", 2: "blend_fwd_kernel", 5: "project_bwd_kernel", 6: "adam_kernel",
-                 0: "preprocess_kernel"}
-    traffic = ncu_traffic(kernel_of.get(dom, "?"))
-    roofline = {"bound": "hbm", "kernel": PHASES[dom], "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                "algorithmic_bytes": alg, "kernel_ms": phase_avg[dom],
-                "note": "the blend kernels are FP32-issue-bound; see roofline_fp32"}
-    # FP32 SIMT roof: SMs x 128 lanes x 2 flop x clock under load
-    fp32_peak = 148 * 128 * 2 * (clocks.get("sm_mhz") or sm_max) * 1e6 / 1e12
-    roofline_fp32 = {}
-    for ph, fl in ((4, FLOP_BWD_PER_CONTRIB), (2, FLOP_FWD_PER_CONTRIB)):
-        tf = contribs * fl / (phase_avg[ph] * 1e-3) / 1e12
-        roofline_fp32[PHASES[ph]] = {"achieved": tf, "peak": fp32_peak, "unit": "TFLOP/s", "frac": tf / fp32_peak,
-                                     "flop_per_contrib": fl, "kernel_ms": phase_avg[ph]}
-    roofline_fp32["contributions"] = contribs
+    # FP32 SIMT roof: 148 SMs x 128 lanes x 2 flop (FFMA) x SM clock. The SM
+    # clock is the max clock (MEASURED_PEAKS sm_max_mhz), which the run held.
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    mufu_peak = 148 * 16 * sm_max * 1e6 / 1e12  # ex2 per s (T/s)
+    blend = {}
+    for ph, (fv, fc), ex in ((4, FLOP_BWD, (1, 1)), (2, FLOP_FWD, (1, 0))):
+        fl = fv * visited + fc * contribs
+        t = phase_avg[ph] * 1e-3
+        blend[ph] = {"achieved": fl / t / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
+                     "frac": fl / t / 1e12 / fp32_peak, "flop": fl,
+                     "flop_per_visited": fv, "flop_per_contributing": fc, "kernel_ms": phase_avg[ph],
+                     "ex2_frac_of_mufu": (ex[0] * visited + ex[1] * contribs) / t / 1e12 / mufu_peak,
+                     "hbm_GB/s": algorithmic_bytes(ph, args.n, visible, pairs, pixels, tiles) / t / 1e9}
+    phase_kernel = {4: "blend_bwd_kernel", 2: "blend_fwd_kernel", 5: "project_bwd_kernel", 6: "adam_kernel",
+                    0: "preprocess_kernel"}
+    dom = int(np.argmax(phase_avg))
+    if dom in blend:
+        r = blend[dom]
+        roofline = {"bound": "fp32", "kernel": PHASES[dom], "achieved": r["achieved"], "peak": r["peak"],
+                    "unit": "TFLOP/s", "frac": r["frac"], "traffic": ncu_traffic(phase_kernel[dom]),
+                    "peak_kind": "computed: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS)",
+                    "algorithmic_flop": r["flop"], "kernel_ms": r["kernel_ms"],
+                    "note": "blend kernels are FP32/issue-bound (SURVEY 8(d)); HBM side in hbm_GB/s of roofline_fp32; "
+                            "traffic = ncu DRAM bytes per launch"}
+    else:
+        alg = algorithmic_bytes(dom, args.n, visible, pairs, pixels, tiles)
+        ach = alg / (phase_avg[dom] * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": PHASES[dom], "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": ach / hbm_peak, "traffic": ncu_traffic(phase_kernel.get(dom, "?")),
+                    "peak_kind": peak_kind, "algorithmic_bytes": alg, "kernel_ms": phase_avg[dom]}
+    roofline_fp32 = {PHASES[ph]: blend[ph] for ph in (4, 2)}
+    roofline_fp32["pge_visited"] = visited
+    roofline_fp32["pge_contributing"] = contribs
     hbm_kernels = {}
     for ph in (0, 1, 3, 5, 6):
-        b = algorithmic_bytes(ph, args.n, visible, pairs, pixels)
+        b = algorithmic_bytes(ph, args.n, visible, pairs, pixels, tiles)
         gbs = b / (phase_avg[ph] * 1e-3) / 1e9
         hbm_kernels[PHASES[ph]] = {"ms": phase_avg[ph], "algorithmic_MB": b / 1e6, "GB/s": gbs,
                                    "frac": gbs / hbm_peak}
+        ib = implementation_bytes(ph, args.n, visible, pairs, pixels)
+        if ib is not None:
+            hbm_kernels[PHASES[ph]]["implementation_min_MB"] = ib / 1e6
+            hbm_kernels[PHASES[ph]]["implementation_frac"] = ib / (phase_avg[ph] * 1e-3) / 1e9 / hbm_peak
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -513,15 +550,44 @@ def run_event(args, world, rank, local):
             ms = float(t.item())
         return ms, scene.size
 
+    def phases():
+        ms = (sk.C.c_double * 4)()
+        cnt = sk.C.c_int64()
+        ctx._lib.sk_ctx_get_event_timing(ctx.h, ms, sk.C.byref(cnt))
+        return [ms[i] / max(1, cnt.value) for i in range(4)]
+
     for _ in range(max(1, min(args.warmup, 2))):
         timed(1000, True, True)
     reps = max(1, min(args.steps, 5))
+    ctx.check(ctx._lib.sk_ctx_enable_timing(ctx.h, 1))
+    ctx.check(ctx._lib.sk_ctx_reset_timing(ctx.h))
     early = [timed(1000, True, True) for _ in range(reps)]
+    ph_early = phases()
+    ctx.check(ctx._lib.sk_ctx_reset_timing(ctx.h))
     late = [timed(20000, False, True) for _ in range(reps)]
+    ph_late = phases()
+    ctx.check(ctx._lib.sk_ctx_enable_timing(ctx.h, 0))
     if rank != 0:
         return
     e_ms = statistics.median(x[0] for x in early)
     l_ms = statistics.median(x[0] for x in late)
+    hbm_peak, _, peak_kind = measured_peaks()
+    comps = sk.n_components(3)
+
+    def event_roofline(ph, n_out):
+        # K13: int32 count rows (4 B x K x N) read, s_d / s_p_raw / s_p written
+        # and s_p_raw re-read by the min-max pass (16 B x N).
+        k13 = 4 * k * n + 16 * n
+        # K14 + K15: params + m + v, 3 x 4 x 59 = 708 B read and
+        # written per output Gaussian, plus the three flag bytes per input.
+        k1415 = 2 * 3 * 4 * comps * n_out + 3 * n
+        t13, t1415 = ph[1] * 1e-3, (ph[2] + ph[3]) * 1e-3
+        return {"phase_ms": dict(zip(["K6+K11+K12 views (+K1-K5, K7 fwd)", "K13 scores", "K14 select",
+                                      "K15 compact"], [round(x, 4) for x in ph])),
+                "K13": {"algorithmic_MB": k13 / 1e6, "GB/s": k13 / t13 / 1e9, "frac": k13 / t13 / 1e9 / hbm_peak},
+                "K14+K15": {"algorithmic_MB": k1415 / 1e6, "GB/s": k1415 / t1415 / 1e9,
+                            "frac": k1415 / t1415 / 1e9 / hbm_peak},
+                "view_ms": ph[0] / k, "peak_GB/s": hbm_peak, "peak_kind": peak_kind}
     line = {
         "metric": "density event ms (config 3: 1M Gaussians, 64 views 1080p, score + select + compact)",
         "value": e_ms, "unit": "ms/event", "n_gpus": world, "steps": reps, "warmup": max(1, min(args.warmup, 2)),
@@ -533,6 +599,7 @@ def run_event(args, world, rank, local):
         "early_event_ms": e_ms, "late_event_ms": l_ms,
         "views_scored_per_s": k / (e_ms * 1e-3),
         "n_after_early": early[-1][1], "n_after_late": late[-1][1],
+        "early": event_roofline(ph_early, early[-1][1]), "late": event_roofline(ph_late, late[-1][1]),
         "generator_s": gen_s,
     }
     print(json.dumps(line), flush=True)

@@ -116,6 +116,12 @@ int sk_ctx_launch_count(const sk_ctx* ctx, int64_t* out);
 int sk_ctx_enable_timing(sk_ctx* ctx, int on);
 int sk_ctx_get_timing(const sk_ctx* ctx, double* ms, int64_t* steps);
 int sk_ctx_reset_timing(sk_ctx* ctx);
+/* Phase timing of density events (Trainer::density_event trainer.hpp:177-243)
+ * while timing is on: 0 the K scored views (K1-K6 + K11 error maps + K7 SSIM
+ * + K12 masked count blend per view, plus the C3 exchange), 1 K13 scores,
+ * 2 K14 selection, 3 K15 compaction (+ Adam moment remap). */
+#define SK_NUM_EVENT_PHASES 4
+int sk_ctx_get_event_timing(const sk_ctx* ctx, double* ms, int64_t* events);
 const char* sk_version(void);
 
 /* ---- scene (Scene<T>, scene.hpp:30-52) ---------------------------------- */
@@ -152,6 +158,12 @@ int sk_bin_sort(sk_ctx* ctx, sk_frame* frame, int64_t* pairs);
  * given the other must be too. */
 int sk_render_forward(sk_ctx* ctx, sk_frame* frame, const uint8_t* mask_host,
                       int32_t* counts_host);
+
+/* Workload counters of the last forward render (SURVEY 8(d) roofline units):
+ * visited = pixel-Gaussian evaluations the reference loop performs
+ * (raster.hpp:219-235: list entries up to and including the terminating one),
+ * contributing = entries with alpha >= 1/255 (sum of contrib_count). */
+int sk_frame_pge_counts(sk_ctx* ctx, sk_frame* frame, int64_t* visited, int64_t* contributing);
 
 /* frame readback */
 int sk_frame_num_projected(const sk_frame* frame, int64_t* n);

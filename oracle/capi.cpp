@@ -14,6 +14,8 @@ using namespace oracle;
 namespace {
 
 thread_local std::string g_err;
+// pixel-Gaussian evaluations visited by the last or_render_* call (RenderOutputs::pge_visited)
+thread_local int64_t g_pge_visited = 0;
 
 template <typename F>
 int guard(F&& f) {
@@ -263,6 +265,7 @@ int render_scene_t(const T* params, int64_t n, int deg, const sk_camera* c, cons
     const auto out = blend_forward(grid, pgs, mm.get(), fc.get(), workers);
     if (fc)
       for (int64_t i = 0; i < n; ++i) counts[i] += fc->counts[i];
+    g_pge_visited = out.pge_visited;
     write_render(grid, pgs, out, o);
   });
 }
@@ -282,6 +285,7 @@ int render_pg_t(const PgIn<T>& in, int64_t n, int w, int h, const sk_binning* b,
     const auto out = blend_forward(grid, pgs, mm.get(), fc.get(), workers);
     if (fc)
       for (int64_t i = 0; i < n; ++i) counts[i] += fc->counts[i];
+    g_pge_visited = out.pge_visited;
     write_render(grid, pgs, out, o);
   });
 }
@@ -391,6 +395,7 @@ int project_backward_t(const T* params, int64_t n, int deg, const sk_camera* c, 
 extern "C" {
 
 const char* or_last_error() { return g_err.c_str(); }
+int64_t or_last_pge_visited() { return g_pge_visited; }
 void or_set_detmath(int on) { g_detmath = on != 0; }
 float or_expf(float x) { return sk::det_expf(x); }
 float or_logf(float x) { return sk::det_logf(x); }

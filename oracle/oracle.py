@@ -216,6 +216,14 @@ def render_scene(params, deg, cam: SkCamera, bin_: SkBinning | None = None, mask
     return Render(img, tr, cc, ranges, vals[: pairs.value].copy(), pairs.value, counts)
 
 
+def last_pge_visited() -> int:
+    """Pixel-Gaussian evaluations the reference loop visited in the last
+    render_scene / render_pg call on this thread (RenderOutputs::pge_visited)."""
+    f = lib().or_last_pge_visited
+    f.restype = C.c_int64
+    return int(f())
+
+
 @dataclass
 class PG:
     """Projected Gaussians (camera.hpp:60-68) in projected order."""

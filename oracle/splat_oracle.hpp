@@ -919,6 +919,9 @@ struct RenderOutputs {
   Image<T> image;
   Map2D<T> transmittance;
   Map2D<int> contrib_count;
+  // Workload counter (not in the reference; SURVEY 8(d) roofline units):
+  // list entries the per-pixel loop examined, the terminating one included.
+  std::int64_t pge_visited = 0;
 };
 
 struct FootprintCounter {
@@ -940,8 +943,10 @@ inline RenderOutputs<T> blend_forward(const TileGrid& grid, const std::vector<Pr
   const int n_workers = std::max(1, workers);
   std::vector<std::vector<int>> worker_counts;
   if (counter) worker_counts.assign(n_workers, std::vector<int>(counter->counts.size(), 0));
+  std::vector<std::int64_t> worker_visited(n_workers, 0);
   parallel_chunks(grid.tile_count(), n_workers, [&](int worker, int begin, int end) {
     std::vector<int>* local = counter ? &worker_counts[worker] : nullptr;
+    std::int64_t visited = 0;
     for (int tile = begin; tile < end; ++tile) {
       const auto& list = grid.tiles[tile];
       const int tx = tile % grid.tiles_x;
@@ -955,6 +960,7 @@ inline RenderOutputs<T> blend_forward(const TileGrid& grid, const std::vector<Pr
           int n = 0;
           const bool masked = mask && (*mask)(py, px) != 0;
           for (const int idx : list) {
+            ++visited;
             const ProjectedGaussian<T>& pg = pgs[idx];
             const T dx = T(px) - pg.mu2d[0];
             const T dy = T(py) - pg.mu2d[1];
@@ -975,7 +981,9 @@ inline RenderOutputs<T> blend_forward(const TileGrid& grid, const std::vector<Pr
           out.contrib_count(py, px) = n;
         }
     }
+    worker_visited[worker] += visited;
   });
+  for (const std::int64_t v : worker_visited) out.pge_visited += v;
   if (counter)
     for (const auto& wc : worker_counts)
       for (size_t i = 0; i < wc.size(); ++i) counter->counts[i] += wc[i];

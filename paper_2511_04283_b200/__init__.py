@@ -276,6 +276,14 @@ class Context:
         self.check(self._lib.sk_render_forward(self.h, frame, _p(m), _p(counts)))
         return self.get_render(frame, counts)
 
+    def pge_counts(self, frame=None):
+        """(visited, contributing) pixel-Gaussian evaluations of the last
+        forward render, in the reference loop's terms (sk_frame_pge_counts)."""
+        frame = frame or self._frame
+        v, c = C.c_int64(), C.c_int64()
+        self.check(self._lib.sk_frame_pge_counts(self.h, frame, C.byref(v), C.byref(c)))
+        return v.value, c.value
+
     def get_render(self, frame=None, counts=None) -> Render:
         frame = frame or self._frame
         w, h = self._frame_dims(frame)

@@ -120,9 +120,11 @@ int sk_ctx_launch_count(const sk_ctx*, int64_t* out) {
 int sk_ctx_enable_timing(sk_ctx* ctx, int on) {
   return guarded(ctx, [&] {
     set_device(ctx);
-    if (on && !ctx->tev[0][0])
+    if (on && !ctx->tev[0][0]) {
       for (auto& set : ctx->tev)
         for (auto& e : set) SK_CUDA(cudaEventCreate(&e));
+      for (auto& e : ctx->ev.tev) SK_CUDA(cudaEventCreate(&e));
+    }
     ctx->timing = on != 0;
   });
 }
@@ -135,10 +137,20 @@ int sk_ctx_get_timing(const sk_ctx* ctx, double* ms, int64_t* steps) {
   return SK_OK;
 }
 
+int sk_ctx_get_event_timing(const sk_ctx* ctx, double* ms, int64_t* events) {
+  if (!ctx) return SK_ERR_INVALID_ARGUMENT;
+  if (ms)
+    for (int i = 0; i < SK_NUM_EVENT_PHASES; ++i) ms[i] = ctx->ev.phase_ms[i];
+  if (events) *events = ctx->ev.timed_events;
+  return SK_OK;
+}
+
 int sk_ctx_reset_timing(sk_ctx* ctx) {
   if (!ctx) return SK_ERR_INVALID_ARGUMENT;
   for (auto& v : ctx->phase_ms) v = 0.0;
   ctx->timed_steps = 0;
+  for (auto& v : ctx->ev.phase_ms) v = 0.0;
+  ctx->ev.timed_events = 0;
   return SK_OK;
 }
 
@@ -379,6 +391,14 @@ int sk_frame_get_image(sk_ctx* ctx, const sk_frame* f, float* hwc) {
     arg(f && hwc && f->rendered, "sk_frame_get_image: frame not rendered");
     set_device(ctx);
     planar_to_hwc(ctx, f->image.ptr, hwc, f->width, f->height);
+  });
+}
+
+int sk_frame_pge_counts(sk_ctx* ctx, sk_frame* f, int64_t* visited, int64_t* contributing) {
+  return guarded(ctx, [&] {
+    arg(f && visited && contributing && f->rendered, "sk_frame_pge_counts: frame not rendered");
+    set_device(ctx);
+    frame_pge_counts(ctx, f, visited, contributing);
   });
 }
 

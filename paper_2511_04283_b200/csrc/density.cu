@@ -291,6 +291,7 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
   uint32_t* lohi = ensure<uint32_t>(ev.lohi, 4);
   SK_CUDA(cudaMemsetAsync(rows, 0, sizeof(int32_t) * (size_t)k * n, ctx->stream));
   std::vector<float> photo(k, 0.0f);
+  ctx->event_mark(0);
   const int world = comm ? comm->world : 1;
   const int rank = comm ? comm->rank : 0;
   for (int j = 0; j < k; ++j) {
@@ -336,6 +337,7 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
     d2h(ctx, photo.data(), dphoto, k);
     sync(ctx);
   }
+  ctx->event_mark(1);
   const uint32_t init[2] = {0xffffffffu, 0u};
   h2d(ctx, lohi, init, 2);
   if (n > 0) {
@@ -346,6 +348,7 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
     note_launch();
   }
   SK_CUDA(cudaGetLastError());
+  ctx->event_mark(2);
   if (photo_out) *photo_out = photo;
 }
 
@@ -505,6 +508,7 @@ void density_event(sk_trainer* t, int it, bool densify, bool prune) {
     pp.use_vcp = cfg.vcp;
     select_prune_flags(ctx, s, it, pp, extent, fprune);
   }
+  ctx->event_mark(3);
   // host view of the flags: split count for the Rng, and the event record
   std::vector<uint8_t> h(3 * (size_t)n);
   d2h(ctx, h.data(), flags, h.size());
@@ -524,6 +528,16 @@ void density_event(sk_trainer* t, int it, bool densify, bool prune) {
   const float pos_lr = expon_lr((float)cfg.lr_position * extent, (float)cfg.lr_position_final * extent, it,
                                 cfg.iterations);
   compact_scene(ctx, s, fprune, fclone, fsplit, pos_lr, eps.data(), n_split, nullptr);
+  ctx->event_mark(4);
+  if (ctx->timing && ctx->ev.tev[0]) {
+    SK_CUDA(cudaEventSynchronize(ctx->ev.tev[4]));
+    for (int i = 0; i < SK_NUM_EVENT_PHASES; ++i) {
+      float ms = 0.0f;
+      SK_CUDA(cudaEventElapsedTime(&ms, ctx->ev.tev[i], ctx->ev.tev[i + 1]));
+      ctx->ev.phase_ms[i] += ms;
+    }
+    ++ctx->ev.timed_events;
+  }
   if (t->record_events) {
     rec.prune.assign(h.begin() + 2 * n, h.begin() + 3 * n);
     rec.clone.assign(h.begin(), h.begin() + n);

@@ -149,6 +149,34 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
   }
 }
 
+// Workload counters of a rendered frame: pixel-Gaussian
+// evaluations the reference's blend_forward loop visits (raster.hpp:219-235:
+// every list entry up to and including the one that takes T below 1e-4, or
+// the whole list) and the contributing ones (alpha >= 1/255). The terminating
+// entry is always the pixel's last contributor, so visited = last_entry -
+// range start for terminated pixels (final T < 1e-4), else the list length.
+__global__ void pge_counts_kernel(const int2* __restrict__ ranges, const float* __restrict__ final_t,
+                                  const int* __restrict__ n_contrib, const int* __restrict__ last_entry, int W,
+                                  int H, int TS, int tiles_x, unsigned long long* __restrict__ out) {
+  unsigned long long vis = 0, con = 0;
+  const int64_t HW = (int64_t)W * H;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < HW; p += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(p / W), x = (int)(p % W);
+    const int2 r = ranges[(y / TS) * tiles_x + x / TS];
+    vis += (unsigned long long)(final_t[p] < kTransmitMin ? last_entry[p] - r.x : r.y - r.x);
+    con += (unsigned long long)n_contrib[p];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    vis += __shfl_xor_sync(0xffffffffu, vis, o);
+    con += __shfl_xor_sync(0xffffffffu, con, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&out[0], vis);
+    atomicAdd(&out[1], con);
+  }
+}
+
 template <int TS, int PIX>
 void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts) {
   const int tiles = f->tiles_x * f->tiles_y;
@@ -168,6 +196,21 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
 }
 
 }  // namespace
+
+void frame_pge_counts(sk_ctx* ctx, sk_frame* f, int64_t* visited, int64_t* contributing) {
+  auto* out = ensure<unsigned long long>(ctx->pge, 2);
+  SK_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  pge_counts_kernel<<<148 * 4, 256, 0, ctx->stream>>>(f->ranges.as<int2>(), f->final_t.as<float>(),
+                                                      f->n_contrib.as<int>(), f->last_entry.as<int>(), f->width,
+                                                      f->height, f->tile_size, f->tiles_x, out);
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+  unsigned long long h[2];
+  SK_CUDA(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  SK_CUDA(cudaStreamSynchronize(ctx->stream));
+  *visited = (int64_t)h[0];
+  *contributing = (int64_t)h[1];
+}
 
 void launch_blend_forward(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts) {
   if (f->tiles_x * f->tiles_y == 0) return;

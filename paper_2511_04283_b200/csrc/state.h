@@ -31,6 +31,11 @@ struct EventScratch {
   DevBuf keys_a, keys_b, vals_a, vals_b;  // VCP ordering
   DevBuf eps;        // float [n_split][6]
   DevBuf old_to_new; // int32 [n]
+  // phase timing of density events (sk_ctx_get_event_timing): marks at the
+  // start of the score pass, after the K views, after K13, K14 and K15
+  cudaEvent_t tev[SK_NUM_EVENT_PHASES + 1] = {};
+  double phase_ms[SK_NUM_EVENT_PHASES] = {};
+  int64_t timed_events = 0;
 };
 }  // namespace sk
 
@@ -43,6 +48,7 @@ struct sk_ctx {
   sk::EventScratch ev;
   sk::DevBuf err_word;  // uint32 device error bits
   sk::DevBuf scalars;   // small device scratch (reductions)
+  sk::DevBuf pge;       // uint64 [2] workload counters (sk_frame_pge_counts)
   sk::HostBuf pinned;   // staging
   // phase timing (sk_ctx_enable_timing)
   bool timing = false;
@@ -52,6 +58,9 @@ struct sk_ctx {
   int64_t timed_steps = 0;
   void mark(int i) {
     if (timing) cudaEventRecord(tev[tev_set][i], stream);
+  }
+  void event_mark(int i) {
+    if (timing && ev.tev[i]) cudaEventRecord(ev.tev[i], stream);
   }
 };
 
@@ -157,6 +166,8 @@ void launch_tile_ranges(sk_ctx* ctx, const uint32_t* pair_tile, int64_t pairs, i
 // rasterize.cu
 void launch_blend_forward(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts);
 void launch_blend_backward(sk_ctx* ctx, sk_frame* f);
+// Reference-loop workload of the last forward render (synchronises).
+void frame_pge_counts(sk_ctx* ctx, sk_frame* f, int64_t* visited, int64_t* contributing);
 
 // loss.cu
 struct LossSums {

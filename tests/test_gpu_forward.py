@@ -133,6 +133,7 @@ def test_scene_render_bit_exact_ring(ctx, orc):
         cam = ring_camera(orc, 160, 120, angle)
         b = orc.binning("compact" if v % 2 else "aabb")
         ref = orc.render_scene(p, 3, cam, b)
+        ref_visited = orc.last_pge_visited()
         scene = ctx.scene(p, 3)
         ctx.preprocess(scene, cam, b)
         ctx.build_tile_grid()
@@ -141,6 +142,10 @@ def test_scene_render_bit_exact_ring(ctx, orc):
         assert np.array_equal(got.image, ref.image)
         assert np.array_equal(got.transmittance, ref.transmittance)
         assert np.array_equal(got.contrib, ref.contrib)
+        # roofline workload units: the reference loop's visits
+        visited, contributing = ctx.pge_counts()
+        assert visited == ref_visited
+        assert contributing == int(ref.contrib.astype(np.int64).sum())
 
 
 def test_invalid_scale_raises_like_reference(ctx, orc):

@@ -456,3 +456,25 @@ def test_detmath_vs_std_exp_render_close(orc):
     finally:
         orc.set_detmath(True)
     assert np.abs(a.image - b.image).max() < 1e-4
+
+
+def test_pge_visited_counter(orc):
+    """The oracle's visited counter: every list entry up to and including the
+    terminating one (raster.hpp:219-235); workers do not change it."""
+    rng = np.random.default_rng(77)
+    pg = orc.random_projected(rng, 40, 40, 24, 0.95, dtype=np.float32)
+    r1 = orc.render_pg(pg, 40, 24, orc.binning(tile_size=8), workers=1)
+    v1 = orc.last_pge_visited()
+    r3 = orc.render_pg(pg, 40, 24, orc.binning(tile_size=8), workers=3)
+    assert orc.last_pge_visited() == v1
+    tiles_x = (40 + 7) // 8
+    lo = hi = 0
+    for y in range(24):
+        for x in range(40):
+            b, e = r1.ranges[(y // 8) * tiles_x + x // 8]
+            hi += int(e - b)
+            # unterminated pixels visit their whole list; terminated ones at
+            # least every contributor
+            lo += int(e - b) if r1.transmittance[y, x] >= 1e-4 else int(r1.contrib[y, x])
+    assert lo <= v1 <= hi and v1 > int(r1.contrib.sum())
+    assert np.array_equal(r1.image, r3.image)
