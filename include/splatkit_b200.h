@@ -335,6 +335,42 @@ int sk_synthetic_create(sk_ctx* ctx, const sk_synth_spec* spec, sk_scene** gt_ou
 int sk_init_from_points(sk_ctx* ctx, int64_t n, const float* xyz, const float* rgb, int sh_degree, int64_t capacity,
                         sk_scene** out);
 
+/* ---- on-disk formats ----------------------------------
+ * Host-side file I/O. ctx may be NULL for the pure file functions (points,
+ * PNG, cameras.json); errors are then reported by status only. */
+/* save_checkpoint (ply.hpp:217-248): binary little-endian PLY, float32 rows
+ * x y z nx ny nz f_dc_0..2 f_rest_* (channel-major) opacity scale_0..2
+ * rot_0..3. The planar device scene is gathered into rows on the GPU. */
+int sk_checkpoint_save(sk_ctx* ctx, const sk_scene* scene, const char* path);
+/* load_checkpoint (ply.hpp:251-315): SH degree from the f_rest count; missing
+ * fields raise "checkpoint: missing property '<name>'". */
+int sk_checkpoint_load(sk_ctx* ctx, const char* path, int64_t capacity, sk_scene** out);
+/* read_points_ply (ply.hpp:179-196): xyz / rgb [count][3]; colours rescaled
+ * by 1/255 when integer-typed. Pass xyz = rgb = NULL to query *count; else
+ * *count is the buffer capacity on entry and the point count on return. */
+int sk_points_read(sk_ctx* ctx, const char* path, float* xyz, float* rgb, int64_t* count);
+/* write_points_ply (ply.hpp:198-212): float xyz + uchar rgb (lround). */
+int sk_points_write(sk_ctx* ctx, const char* path, const float* xyz, const float* rgb, int64_t n);
+/* read_png (png_io.cpp:25-72) as 8-bit RGB [H][W][3] (the reference's float
+ * image is byte / 255.0f). rgb = NULL queries *width / *height. */
+int sk_png_read(sk_ctx* ctx, const char* path, uint8_t* rgb, int* width, int* height);
+/* write_png (png_io.cpp:74-104): lround(clamp(v, 0, 1) * 255) per channel. */
+int sk_png_write(sk_ctx* ctx, const char* path, const float* rgb, int width, int height);
+int sk_png_write_u8(sk_ctx* ctx, const char* path, const uint8_t* rgb, int width, int height);
+/* cameras.json records (dataset.hpp:80-100, 127-150). cams = NULL queries
+ * *count; cameras are validated (Camera::validate camera.hpp:34-42). */
+int sk_cameras_read(sk_ctx* ctx, const char* path, sk_camera* cams, int32_t* ids, int* count);
+int sk_cameras_write(sk_ctx* ctx, const char* path, const sk_camera* cams, const int32_t* ids, int n);
+/* load_dataset (dataset.hpp:73-125): cameras.json, images/%05d.png and
+ * points3d.ply into a device-resident dataset; every-8th test split; extent =
+ * 1.1 x the radius around the mean camera centre. */
+int sk_dataset_load(sk_ctx* ctx, const char* dir, sk_dataset** out);
+/* Init point cloud of a loaded or synthetic dataset (Dataset::init_points). */
+int sk_dataset_init_points(const sk_dataset* d, float* xyz, float* rgb, int64_t* count);
+/* The files generate_synthetic writes (dataset.hpp:221-247): cameras.json,
+ * images/%05d.png (device images, 8-bit) and points3d.ply. */
+int sk_dataset_save(sk_ctx* ctx, const sk_dataset* d, const char* dir);
+
 typedef struct sk_trainer sk_trainer;
 /* Trainer(scene, data, cfg) (trainer.hpp:70-87). The trainer borrows scene and
  * dataset; both must outlive it. */

@@ -13,6 +13,7 @@
 #pragma once
 
 #include <array>
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -406,10 +407,159 @@ inline TrainConfig default_train_config() {
 // Dataset (dataset.hpp:24-32): cameras + 8-bit GT images.
 struct Dataset {
   std::vector<Camera> cameras;
+  std::vector<int> camera_ids;
   std::vector<std::vector<std::uint8_t>> images_u8;  // HWC per view
+  std::vector<std::pair<Vec3, Vec3>> init_points;    // xyz, rgb in 0..1
   std::vector<int> train_indices;
+  std::vector<int> test_indices;
   T extent = 1;
 };
+
+// ---- on-disk formats (ply.hpp, png_io.cpp, dataset.hpp) ------------------
+namespace detail {
+inline void io_check(const Device* dev, int rc, const char* what) {
+  if (dev) dev->check(rc);
+  else raise(rc, what);
+}
+inline Camera from_c(const sk_camera& c) {
+  Camera o;
+  o.width = c.width;
+  o.height = c.height;
+  o.fx = c.fx;
+  o.fy = c.fy;
+  o.cx = c.cx;
+  o.cy = c.cy;
+  for (int i = 0; i < 16; ++i) o.world_to_cam.m[i] = c.world_to_cam[i];
+  o.near = c.near_plane;
+  return o;
+}
+}  // namespace detail
+
+// save_checkpoint (ply.hpp:217-248)
+inline void save_checkpoint(const Device& dev, const Scene& scene, const std::string& path) {
+  DeviceScene ds(dev, scene);
+  dev.check(sk_checkpoint_save(dev.ctx(), ds.handle(), path.c_str()));
+}
+
+// load_checkpoint (ply.hpp:251-315)
+inline Scene load_checkpoint(const Device& dev, const std::string& path) {
+  sk_scene* h = nullptr;
+  dev.check(sk_checkpoint_load(dev.ctx(), path.c_str(), 0, &h));
+  std::unique_ptr<sk_scene, int (*)(sk_scene*)> guard(h, sk_scene_destroy);
+  int deg = 0;
+  int64_t n = 0;
+  sk_scene_sh_degree(h, &deg);
+  sk_scene_size(h, &n);
+  std::vector<float> p(size_t(SK_COMP_COUNT(deg)) * n);
+  dev.check(sk_scene_download(dev.ctx(), h, p.data()));
+  Scene s;
+  s.sh_degree = deg;
+  detail::from_planar(p, int(n), s);
+  return s;
+}
+
+// read_png (png_io.cpp:25-72): float image = byte / 255.0f.
+inline Image read_png(const std::string& path) {
+  int w = 0, h = 0;
+  detail::io_check(nullptr, sk_png_read(nullptr, path.c_str(), nullptr, &w, &h), ("png: cannot read " + path).c_str());
+  std::vector<std::uint8_t> rgb(size_t(w) * h * 3);
+  detail::io_check(nullptr, sk_png_read(nullptr, path.c_str(), rgb.data(), &w, &h), ("png: cannot read " + path).c_str());
+  Image img(w, h);
+  for (size_t i = 0; i < size_t(w) * h; ++i)
+    for (int c = 0; c < 3; ++c) img.pixels[i][c] = rgb[3 * i + c] / 255.0f;
+  return img;
+}
+
+// write_png (png_io.cpp:74-104)
+inline void write_png(const std::string& path, const Image& image) {
+  std::vector<float> rgb(size_t(image.width) * image.height * 3);
+  for (size_t i = 0; i < image.pixels.size(); ++i)
+    for (int c = 0; c < 3; ++c) rgb[3 * i + c] = image.pixels[i][c];
+  detail::io_check(nullptr, sk_png_write(nullptr, path.c_str(), rgb.data(), image.width, image.height),
+                   ("png: cannot write " + path).c_str());
+}
+
+// read_points_ply / write_points_ply (ply.hpp:179-212)
+inline std::vector<std::pair<Vec3, Vec3>> read_points_ply(const std::string& path) {
+  int64_t n = 0;
+  detail::io_check(nullptr, sk_points_read(nullptr, path.c_str(), nullptr, nullptr, &n),
+                   ("ply: cannot read " + path).c_str());
+  std::vector<float> xyz(size_t(n) * 3), rgb(size_t(n) * 3);
+  detail::io_check(nullptr, sk_points_read(nullptr, path.c_str(), xyz.data(), rgb.data(), &n),
+                   ("ply: cannot read " + path).c_str());
+  std::vector<std::pair<Vec3, Vec3>> out(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i)
+    for (int d = 0; d < 3; ++d) {
+      out[i].first[d] = xyz[3 * i + d];
+      out[i].second[d] = rgb[3 * i + d];
+    }
+  return out;
+}
+
+inline void write_points_ply(const std::string& path, const std::vector<std::pair<Vec3, Vec3>>& points) {
+  std::vector<float> xyz, rgb;
+  for (const auto& [p, c] : points)
+    for (int d = 0; d < 3; ++d) {
+      xyz.push_back(p[d]);
+      rgb.push_back(c[d]);
+    }
+  detail::io_check(nullptr, sk_points_write(nullptr, path.c_str(), xyz.data(), rgb.data(), int64_t(points.size())),
+                   ("ply: cannot write " + path).c_str());
+}
+
+// load_dataset (dataset.hpp:73-125)
+inline Dataset load_dataset(const Device& dev, const std::string& path) {
+  sk_dataset* d = nullptr;
+  dev.check(sk_dataset_load(dev.ctx(), path.c_str(), &d));
+  std::unique_ptr<sk_dataset, int (*)(sk_dataset*)> guard(d, sk_dataset_destroy);
+  Dataset out;
+  int nv = 0;
+  sk_dataset_num_views(d, &nv);
+  for (int v = 0; v < nv; ++v) {
+    sk_camera c;
+    sk_dataset_camera(d, v, &c);
+    out.cameras.push_back(detail::from_c(c));
+    std::vector<std::uint8_t> img(size_t(c.width) * c.height * 3);
+    dev.check(sk_dataset_image_u8(dev.ctx(), d, v, img.data()));
+    out.images_u8.push_back(std::move(img));
+  }
+  int cnt = 0;
+  sk_dataset_train_indices(d, nullptr, &cnt);
+  std::vector<int32_t> tr(static_cast<size_t>(cnt));
+  sk_dataset_train_indices(d, tr.data(), &cnt);
+  out.train_indices.assign(tr.begin(), tr.end());
+  for (int v = 0; v < nv; ++v)
+    if (std::find(tr.begin(), tr.end(), v) == tr.end()) out.test_indices.push_back(v);
+  int64_t np = 0;
+  sk_dataset_init_points(d, nullptr, nullptr, &np);
+  std::vector<float> xyz(size_t(np) * 3), rgb(size_t(np) * 3);
+  sk_dataset_init_points(d, xyz.data(), rgb.data(), &np);
+  for (int64_t i = 0; i < np; ++i) {
+    std::pair<Vec3, Vec3> pr;
+    for (int k = 0; k < 3; ++k) {
+      pr.first[k] = xyz[3 * i + k];
+      pr.second[k] = rgb[3 * i + k];
+    }
+    out.init_points.push_back(pr);
+  }
+  std::vector<sk_camera> cams(static_cast<size_t>(nv));
+  std::vector<int32_t> ids(static_cast<size_t>(nv));
+  int cc = nv;
+  if (nv > 0 && sk_cameras_read(nullptr, (path + "/cameras.json").c_str(), cams.data(), ids.data(), &cc) == SK_OK)
+    out.camera_ids.assign(ids.begin(), ids.end());
+  sk_dataset_extent(d, &out.extent);
+  return out;
+}
+
+// save_cameras_json (dataset.hpp:127-150)
+inline void save_cameras_json(const std::string& path, const std::vector<Camera>& cameras,
+                              const std::vector<int>& ids) {
+  std::vector<sk_camera> c;
+  for (const auto& cam : cameras) c.push_back(detail::to_c(cam));
+  std::vector<int32_t> i(ids.begin(), ids.end());
+  detail::io_check(nullptr, sk_cameras_write(nullptr, path.c_str(), c.data(), i.data(), int(c.size())),
+                   ("dataset: cannot write " + path).c_str());
+}
 
 struct LogRow {
   int iteration = 0;

@@ -378,6 +378,19 @@ class Scene:
                                                C.c_int64(capacity or xyz.shape[0]), C.byref(h)))
         return cls._wrap(ctx, h, sh_degree)
 
+    @classmethod
+    def load_checkpoint(cls, ctx: Context, path, capacity=None) -> "Scene":
+        """load_checkpoint (ply.hpp:251-315) straight into HBM."""
+        h = C.c_void_p()
+        ctx.check(ctx._lib.sk_checkpoint_load(ctx.h, os.fsencode(path), C.c_int64(capacity or 0), C.byref(h)))
+        deg = C.c_int()
+        ctx._lib.sk_scene_sh_degree(h, C.byref(deg))
+        return cls._wrap(ctx, h, deg.value)
+
+    def save_checkpoint(self, path):
+        """save_checkpoint (ply.hpp:217-248)."""
+        self.ctx.check(self.ctx._lib.sk_checkpoint_save(self.ctx.h, self.h, os.fsencode(path)))
+
     @property
     def size(self) -> int:
         n = C.c_int64()
@@ -635,6 +648,29 @@ class Dataset:
         ds.ctx, ds.h = ctx, d
         return ds, Scene._wrap(ctx, g, 1), xyz, rgb
 
+    @classmethod
+    def load(cls, ctx: Context, directory: str) -> "Dataset":
+        """load_dataset (dataset.hpp:73-125): cameras.json + images/%05d.png +
+        points3d.ply into HBM."""
+        d = C.c_void_p()
+        ctx.check(ctx._lib.sk_dataset_load(ctx.h, os.fsencode(directory), C.byref(d)))
+        ds = cls.__new__(cls)
+        ds.ctx, ds.h = ctx, d
+        return ds
+
+    def save(self, directory: str):
+        """The files generate_synthetic writes (dataset.hpp:221-247)."""
+        self.ctx.check(self.ctx._lib.sk_dataset_save(self.ctx.h, self.h, os.fsencode(directory)))
+
+    def init_points(self):
+        n = C.c_int64()
+        self.ctx._lib.sk_dataset_init_points(self.h, None, None, C.byref(n))
+        xyz = np.zeros((n.value, 3), np.float32)
+        rgb = np.zeros((n.value, 3), np.float32)
+        if n.value:
+            self.ctx.check(self.ctx._lib.sk_dataset_init_points(self.h, _p(xyz), _p(rgb), C.byref(n)))
+        return xyz, rgb
+
     @property
     def num_views(self) -> int:
         n = C.c_int()
@@ -748,6 +784,85 @@ class Trainer:
             self.close()
         except Exception:
             pass
+
+
+# ---- on-disk formats; host-only, no GPU needed ----------
+
+def _io_check(rc, what):
+    if rc != SK_OK:
+        raise (ValueError if rc == SK_ERR_INVALID_ARGUMENT else SplatError)(f"{what} failed (status {rc})")
+
+
+def _io_call(ctx, fn, *args, what=""):
+    """Runs a file-format entry point; with a Context the library's message is
+    raised, without one the status."""
+    rc = fn(ctx.h if ctx is not None else None, *args)
+    if ctx is not None:
+        ctx.check(rc)
+    else:
+        _io_check(rc, what)
+
+
+def read_points_ply(path, ctx: Context | None = None):
+    """read_points_ply (ply.hpp:179-196) -> (xyz [n,3], rgb [n,3]) float32."""
+    L = lib()
+    n = C.c_int64()
+    _io_call(ctx, L.sk_points_read, os.fsencode(path), None, None, C.byref(n), what=f"ply read {path}")
+    xyz = np.zeros((n.value, 3), np.float32)
+    rgb = np.zeros((n.value, 3), np.float32)
+    _io_call(ctx, L.sk_points_read, os.fsencode(path), _p(xyz), _p(rgb), C.byref(n), what=f"ply read {path}")
+    return xyz, rgb
+
+
+def write_points_ply(path, xyz, rgb, ctx: Context | None = None):
+    xyz = np.ascontiguousarray(xyz, np.float32)
+    rgb = np.ascontiguousarray(rgb, np.float32)
+    _io_call(ctx, lib().sk_points_write, os.fsencode(path), _p(xyz), _p(rgb), C.c_int64(xyz.shape[0]),
+             what=f"ply write {path}")
+
+
+def read_png(path, ctx: Context | None = None) -> np.ndarray:
+    """read_png (png_io.cpp:25-72) as uint8 [H][W][3]; the reference's float
+    image is this / 255.0f."""
+    L = lib()
+    w, h = C.c_int(), C.c_int()
+    _io_call(ctx, L.sk_png_read, os.fsencode(path), None, C.byref(w), C.byref(h), what=f"png read {path}")
+    img = np.zeros((h.value, w.value, 3), np.uint8)
+    _io_call(ctx, L.sk_png_read, os.fsencode(path), _p(img), C.byref(w), C.byref(h), what=f"png read {path}")
+    return img
+
+
+def write_png(path, image, ctx: Context | None = None):
+    """write_png (png_io.cpp:74-104): float [H][W][3] quantised with
+    lround(clamp(v)·255), or uint8 written as is."""
+    L = lib()
+    if image.dtype == np.uint8:
+        img = np.ascontiguousarray(image)
+        fn = L.sk_png_write_u8
+    else:
+        img = np.ascontiguousarray(image, np.float32)
+        fn = L.sk_png_write
+    _io_call(ctx, fn, os.fsencode(path), _p(img), C.c_int(img.shape[1]), C.c_int(img.shape[0]),
+             what=f"png write {path}")
+
+
+def read_cameras_json(path, ctx: Context | None = None):
+    """cameras.json records (dataset.hpp:80-100) -> (list of SkCamera, ids)."""
+    L = lib()
+    n = C.c_int()
+    _io_call(ctx, L.sk_cameras_read, os.fsencode(path), None, None, C.byref(n), what=f"cameras read {path}")
+    cams = (SkCamera * max(1, n.value))()
+    ids = np.zeros(max(1, n.value), np.int32)
+    _io_call(ctx, L.sk_cameras_read, os.fsencode(path), cams, _p(ids), C.byref(n), what=f"cameras read {path}")
+    return [cams[i] for i in range(n.value)], ids[: n.value]
+
+
+def write_cameras_json(path, cams, ids=None, ctx: Context | None = None):
+    """save_cameras_json (dataset.hpp:127-150)."""
+    arr = (SkCamera * max(1, len(cams)))(*[as_camera(c) for c in cams])
+    ids = np.ascontiguousarray(np.arange(len(cams)) if ids is None else ids, np.int32)
+    _io_call(ctx, lib().sk_cameras_write, os.fsencode(path), arr, _p(ids), C.c_int(len(cams)),
+             what=f"cameras write {path}")
 
 
 def train_step_host(ctx: Context, scene: Scene, cam, gt_u8, cfg, extent, iteration, frame=None) -> dict:

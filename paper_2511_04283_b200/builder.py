@@ -48,6 +48,7 @@ def _compile(src: str, hdr_mtime: float, verbose: bool) -> str:
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(path), hdr_mtime):
         return obj
     flags = [] if src in FMA_OK else ["-fmad=false"]
+    flags += os.environ.get("SK_NVCC_EXTRA", "").split()  # A/B experiments (rebuild with force=True)
     cmd = [nvcc(), *ARCH, *COMMON, *flags, "-c", path, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
@@ -70,7 +71,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, hdr, verbose), srcs))
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl"]
+        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl", "-lz"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

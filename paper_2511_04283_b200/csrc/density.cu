@@ -15,6 +15,8 @@
 // a scatter of parameters and Adam moments into fresh buffers.
 #include <algorithm>
 
+#include <functional>
+
 #include "abi_util.h"
 #include "trainer.h"
 
@@ -415,8 +417,11 @@ void select_prune_flags(sk_ctx* ctx, sk_scene* s, int iteration, const sk_prune_
 }
 
 // K15 on device flags; returns the new size. eps_dev: [n_split][6].
+// eps_source(n_split) returns the 6·n_split split normals (host memory),
+// called once the split count is known from the device scans.
 int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint8_t* clone, const uint8_t* split,
-                      float clone_lr, const float* eps_host, int64_t n_split_expected, int32_t* old_to_new_dev) {
+                      float clone_lr, const std::function<const float*(int64_t)>& eps_source,
+                      int32_t* old_to_new_dev) {
   EventScratch& ev = ctx->ev;
   const int64_t n = s->n;
   if (n == 0) return 0;
@@ -427,9 +432,9 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
   const int64_t n_keep = scan_gathered(ctx, cls, nullptr, pos, n);
   const int64_t n_clone = scan_gathered(ctx, cls + n, nullptr, pos + n, n);
   const int64_t n_split = scan_gathered(ctx, cls + 2 * n, nullptr, pos + 2 * n, n);
-  require(n_split_expected < 0 || n_split_expected == n_split, "apply_densify: split count mismatch");
   const int64_t new_n = n_keep + n_clone + 2 * n_split;
   float* eps = ensure<float>(ev.eps, 6 * (size_t)std::max<int64_t>(n_split, 1));
+  const float* eps_host = eps_source(n_split);
   if (n_split > 0) {
     require(eps_host != nullptr, "apply_densify: split requires eps normals");
     h2d(ctx, eps, eps_host, 6 * (size_t)n_split);
@@ -437,7 +442,11 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
   ensure_optimizer_state(ctx, s);
   const int64_t new_cap =
       new_n > s->capacity ? round_capacity(std::max<int64_t>(new_n, s->capacity + s->capacity / 2)) : s->capacity;
-  DevBuf np, nm, nv;
+  // Output into the scene's persistent spare buffers (grow-only), swapped in
+  // below: no cudaMalloc / cudaFree of the ~0.7 GB-per-1M state per event.
+  DevBuf& np = s->params_alt;
+  DevBuf& nm = s->adam_m_alt;
+  DevBuf& nv = s->adam_v_alt;
   const size_t cells = (size_t)s->comps * new_cap;
   ensure<float>(np, cells);
   ensure<float>(nm, cells);
@@ -509,25 +518,26 @@ void density_event(sk_trainer* t, int it, bool densify, bool prune) {
     select_prune_flags(ctx, s, it, pp, extent, fprune);
   }
   ctx->event_mark(3);
-  // host view of the flags: split count for the Rng, and the event record
-  std::vector<uint8_t> h(3 * (size_t)n);
-  d2h(ctx, h.data(), flags, h.size());
-  sync(ctx);
-  int64_t n_split = 0, n_clone = 0, n_prune = 0;
-  for (int64_t i = 0; i < n; ++i) {
-    const bool pr = h[2 * n + i] != 0;
-    n_prune += pr;
-    if (!pr) {
-      n_split += h[n + i] != 0;
-      n_clone += h[i] != 0;
-    }
-  }
-  // 6 normals per split Gaussian, ascending index order (adc.hpp:190-197)
-  std::vector<float> eps(6 * (size_t)n_split);
-  for (auto& e : eps) e = (float)t->rng.normal();
+  // The split count (for the Rng) comes from the device scans inside
+  // compact_scene; the flags are only downloaded for the event record.
   const float pos_lr = expon_lr((float)cfg.lr_position * extent, (float)cfg.lr_position_final * extent, it,
                                 cfg.iterations);
-  compact_scene(ctx, s, fprune, fclone, fsplit, pos_lr, eps.data(), n_split, nullptr);
+  std::vector<uint8_t> h;
+  if (t->record_events) {
+    h.resize(3 * (size_t)n);
+    d2h(ctx, h.data(), flags, h.size());
+  }
+  std::vector<float> eps;
+  int64_t n_split = 0;
+  compact_scene(ctx, s, fprune, fclone, fsplit, pos_lr,
+                [&](int64_t ns) -> const float* {
+                  // 6 normals per split Gaussian, ascending index order (adc.hpp:190-197)
+                  n_split = ns;
+                  eps.resize(6 * (size_t)ns);
+                  t->rng.normals(eps.data(), eps.size());
+                  return eps.data();
+                },
+                nullptr);
   ctx->event_mark(4);
   if (ctx->timing && ctx->ev.tev[0]) {
     SK_CUDA(cudaEventSynchronize(ctx->ev.tev[4]));
@@ -542,8 +552,12 @@ void density_event(sk_trainer* t, int it, bool densify, bool prune) {
     rec.prune.assign(h.begin() + 2 * n, h.begin() + 3 * n);
     rec.clone.assign(h.begin(), h.begin() + n);
     rec.split.assign(h.begin() + n, h.begin() + 2 * n);
-    for (int64_t i = 0; i < n; ++i)
+    int64_t n_clone = 0, n_prune = 0;
+    for (int64_t i = 0; i < n; ++i) {
       if (rec.prune[i]) rec.clone[i] = rec.split[i] = 0;
+      n_prune += rec.prune[i] != 0;
+      n_clone += rec.clone[i] != 0;
+    }
     rec.n_clone = (int)n_clone;
     rec.n_split = (int)n_split;
     rec.n_prune = (int)n_prune;
@@ -626,7 +640,7 @@ int sk_apply_prune_densify(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const
     if (prune) h2d(ctx, f + 2 * n, prune, n);
     int32_t* o2n = old_to_new ? ensure<int32_t>(ctx->ev.old_to_new, (size_t)std::max<int64_t>(n, 1)) : nullptr;
     ensure_score_table(ctx, s);
-    const int64_t nn = compact_scene(ctx, s, f + 2 * n, f, f + n, clone_lr, eps, -1, o2n);
+    const int64_t nn = compact_scene(ctx, s, f + 2 * n, f, f + n, clone_lr, [&](int64_t) { return eps; }, o2n);
     if (old_to_new && n > 0) d2h(ctx, old_to_new, o2n, n);
     sync(ctx);
     if (new_size) *new_size = nn;

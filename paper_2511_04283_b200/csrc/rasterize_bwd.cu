@@ -4,7 +4,8 @@
 // reverse order, capped entries feed d_color only. Each thread owns PIX
 // pixels (rows y, y+4, ...) of its warp's 8 x 4·PIX block, sums their partials
 // per Gaussian in registers, and the warp butterfly-reduces the 11 partials
-// of two entries at a time with shuffles; lanes issue one global atomic each.
+// of two entries at a time with a shuffle reduce-scatter (23 shuffles per
+// pair); lanes issue one global atomic each.
 //
 // Gradients are checked against the oracle within a tolerance, so this file
 // is compiled with FMA contraction. The per-pixel contribution decision must
@@ -20,21 +21,57 @@ namespace {
 
 using namespace blend;
 
-__device__ __forceinline__ float warp_sum(float v) {
+// Reduce-scatter of the 11 gradient partials of two entries (a: lanes 0-15
+// after the first stage, b: lanes 16-31) over the warp: each butterfly stage
+// hands half of the remaining values to the partner lane, so 11 + 6 + 3 + 2 + 1
+// = 23 shuffles leave lane l holding the warp sum of one (entry, field):
+// field = 6·bit3 + 3·bit2 + 2·bit1 + bit0 of entry (lane < 16 ? a : b), or
+// nothing for the padding slots (bit1 & bit0, and field 11). Then every lane
+// with a value issues one global atomic.
+__device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradFields], const float (&b)[kBGradFields],
+                                                    uint32_t id_a, uint32_t id_b, bool write_b,
+                                                    float* __restrict__ bgrads, int64_t gstride) {
+  const int lane = threadIdx.x & 31;
+  float k1[kBGradFields];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+  for (int f = 0; f < kBGradFields; ++f) {
+    const float give = lane < 16 ? b[f] : a[f];
+    const float mine = lane < 16 ? a[f] : b[f];
+    k1[f] = mine + __shfl_xor_sync(0xffffffffu, give, 16);
+  }
+  const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+  float k2[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const float lo = k1[i], hi = i + 6 < kBGradFields ? k1[i + 6] : 0.0f;
+    k2[i] = (b3 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b3 ? lo : hi, 8);
+  }
+  float k3[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float lo = k2[i], hi = k2[i + 3];
+    k3[i] = (b2 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b2 ? lo : hi, 4);
+  }
+  float k4[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float lo = k3[i], hi = i == 0 ? k3[2] : 0.0f;
+    k4[i] = (b1 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b1 ? lo : hi, 2);
+  }
+  const float v = (b0 ? k4[1] : k4[0]) + __shfl_xor_sync(0xffffffffu, b0 ? k4[0] : k4[1], 1);
+  const int field = (b3 ? 6 : 0) + (b2 ? 3 : 0) + (b1 ? 2 : 0) + (b0 ? 1 : 0);
+  const bool valid = !(b1 && b0) && field < kBGradFields && (lane < 16 || write_b);
+  if (valid) atomicAdd(&bgrads[(int64_t)field * gstride + (lane < 16 ? id_a : id_b)], v);
 }
 
-__device__ __forceinline__ float select_field(const float (&v)[kBGradFields], int f) {
-  float r = v[0];
-#pragma unroll
-  for (int k = 1; k < kBGradFields; ++k) r = f == k ? v[k] : r;
-  return r;
-}
+// 10 resident CTAs (20 warps) per SM: caps the kernel at 96 registers
+// without spills (measured 7.6% faster than the unconstrained 106).
+#ifndef SK_BWD_MINB
+#define SK_BWD_MINB 10
+#endif
 
 template <int TS, int PIX, bool FASTEXP = true>
-__global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
+__global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB) blend_bwd_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     const float* __restrict__ final_t, const int* __restrict__ last_entry, const float* __restrict__ dimage,
@@ -150,7 +187,7 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
         contrib = true;
         const float4 c = s_rgb[j];
         const float one_m = 1.0f - alpha;
-        const float inv_one_m = __frcp_rn(one_m);  // tolerance path: one reciprocal, two products
+        const float inv_one_m = __fdividef(1.0f, one_m);  // tolerance path: MUFU reciprocal, two products
         const float t_before = T[k] * inv_one_m;
         T[k] = t_before;
         const float w = (c.x * d0[k] + c.y * d1[k]) + c.z * d2[k];
@@ -179,23 +216,7 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
       if (__any_sync(0xffffffffu, contrib)) {
         const float gv[kBGradFields] = {g_mu0, g_mu1, g_c00, g_c01, g_c11, g_r, g_g, g_b, g_op, g_a0, g_a1};
         if (has_pend) {
-          // Two entries per reduction: the xor-16 stage hands the pending
-          // entry to lanes 0-15 and the current one to lanes 16-31, then four
-          // butterfly stages finish both (55 shuffles for 22 values).
-          float keep[kBGradFields];
-#pragma unroll
-          for (int f = 0; f < kBGradFields; ++f) {
-            const float give = lane < 16 ? gv[f] : pend[f];
-            const float mine = lane < 16 ? pend[f] : gv[f];
-            keep[f] = mine + __shfl_xor_sync(0xffffffffu, give, 16);
-          }
-#pragma unroll
-          for (int o = 8; o > 0; o >>= 1)
-#pragma unroll
-            for (int f = 0; f < kBGradFields; ++f) keep[f] += __shfl_xor_sync(0xffffffffu, keep[f], o);
-          const int fl = lane & 15;
-          if (fl < kBGradFields)
-            atomicAdd(&bgrads[(int64_t)fl * gstride + (lane < 16 ? pend_id : s_id[j])], select_field(keep, fl));
+          reduce_scatter_2x11(pend, gv, pend_id, s_id[j], true, bgrads, gstride);
           has_pend = false;
         } else {
 #pragma unroll
@@ -208,9 +229,10 @@ __global__ void __launch_bounds__(TS* TS / PIX) blend_bwd_kernel(
     }
   }
   if (has_pend) {  // warp-uniform: flush the last unpaired entry
+    float zero[kBGradFields];
 #pragma unroll
-    for (int f = 0; f < kBGradFields; ++f) pend[f] = warp_sum(pend[f]);
-    if (lane < kBGradFields) atomicAdd(&bgrads[(int64_t)lane * gstride + pend_id], select_field(pend, lane));
+    for (int f = 0; f < kBGradFields; ++f) zero[f] = 0.0f;
+    reduce_scatter_2x11(pend, zero, pend_id, 0u, false, bgrads, gstride);
   }
 }
 

@@ -76,6 +76,8 @@ struct sk_scene {
   sk::DevBuf grads;       // [comps][capacity]
   sk::DevBuf adam_m;      // [comps][capacity]
   sk::DevBuf adam_v;      // [comps][capacity]
+  // spare buffers the density-event compaction writes into (then swapped)
+  sk::DevBuf params_alt, adam_m_alt, adam_v_alt;
   int64_t adam_t[6] = {0, 0, 0, 0, 0, 0};  // pos, rot, scale, opacity, sh_dc, sh_rest
   // Lazy SH-rest accumulator of the Trainer (trainer.hpp:160-169): [comps][capacity]
   // (only the SH-rest rows are used); rest_n = scene size it was cleared for.

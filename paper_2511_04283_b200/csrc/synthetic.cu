@@ -289,12 +289,16 @@ int sk_synthetic_create(sk_ctx* ctx, const sk_synth_spec* spec, sk_scene** gt_ou
       V3 q3 = v3(at(SK_COMP_MU, i), at(SK_COMP_MU + 1, i), at(SK_COMP_MU + 2, i));
       for (int k = 0; k < 3; ++k) q3[k] = q3[k] + noise * (float)rng.normal();
       pts[i] = q3;
+      for (int k = 0; k < 3; ++k) d->init_xyz.push_back(q3[k]);
+      for (int c = 0; c < 3; ++c)
+        d->init_rgb.push_back(std::min(1.0f, std::max(0.0f, 0.5f + (float)kShC0 * at(SK_COMP_SH + c, i))));
       if (init_xyz)
         for (int k = 0; k < 3; ++k) init_xyz[3 * i + k] = q3[k];
       if (init_rgb)
         for (int c = 0; c < 3; ++c)
           init_rgb[3 * i + c] = std::min(1.0f, std::max(0.0f, 0.5f + (float)kShC0 * at(SK_COMP_SH + c, i)));
     }
+    for (int i = 0; i < spec->n_views; ++i) d->ids.push_back(i);
     for (int i = 0; i < spec->n_views; ++i)
       if (i % 8 != 0) d->train.push_back(i);
     if (d->train.empty())

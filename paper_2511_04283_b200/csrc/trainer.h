@@ -5,6 +5,7 @@
 #include <cmath>
 #include <memory>
 #include <random>
+#include <thread>
 #include <vector>
 
 #include <nccl.h>
@@ -22,6 +23,10 @@ struct sk_dataset {
   std::vector<std::unique_ptr<sk::DevBuf>> images;  // u8 HWC per view
   std::vector<int> train;
   float extent = 1.0f;
+  // load_dataset / generate_synthetic extras (dataset.hpp:24-32): camera ids
+  // (image file names) and the init point cloud ([n][3] xyz, rgb in 0..1)
+  std::vector<int> ids;
+  std::vector<float> init_xyz, init_rgb;
 };
 
 // Rng (reference rng.hpp:18-69): mt19937_64 plus hand-rolled distributions.
@@ -48,6 +53,43 @@ struct HostRng {
     spare = r * std::sin(a);
     has_spare = true;
     return r * std::cos(a);
+  }
+  // count successive normal() values into out. The uniforms are drawn in
+  // order on this thread; the Box-Muller transcendentals (same libm calls)
+  // run on worker threads, so the values are bit-identical to count
+  // sequential normal() calls.
+  void normals(float* out, size_t count) {
+    size_t o = 0;
+    if (count == 0) return;
+    if (has_spare) {
+      out[o++] = (float)spare;
+      has_spare = false;
+    }
+    const size_t pairs = (count - o + 1) / 2;
+    std::vector<double> u(2 * pairs);
+    for (auto& x : u) x = uniform();
+    std::vector<double> sp(pairs);
+    auto work = [&](size_t b, size_t e) {
+      for (size_t p = b; p < e; ++p) {
+        const double u1 = std::max(u[2 * p], 0x1.0p-53);
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double a = 2.0 * M_PI * u[2 * p + 1];
+        sp[p] = r * std::sin(a);
+        const double c = r * std::cos(a);
+        const size_t i0 = o + 2 * p;
+        out[i0] = (float)c;
+        if (i0 + 1 < count) out[i0 + 1] = (float)sp[p];
+      }
+    };
+    const size_t nt = pairs < 4096 ? 1 : std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (size_t k = 1; k < nt; ++k) th.emplace_back(work, pairs * k / nt, pairs * (k + 1) / nt);
+    work(0, pairs / nt);
+    for (auto& x : th) x.join();
+    if (o + 2 * pairs > count) {  // odd tail: the last pair's sine is the cached spare
+      spare = sp[pairs - 1];
+      has_spare = true;
+    }
   }
   std::vector<int> sample_without_replacement(int n, int k) {
     std::vector<int> idx(n);

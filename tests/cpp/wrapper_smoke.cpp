@@ -3,6 +3,8 @@
 // tests/test_camera.cpp:23-36). Exit code 0 = all checks passed.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 
 #include "splatkit_b200.hpp"
 
@@ -67,6 +69,27 @@ int main() {
     threw = std::string(e.what()).find("covariance_3d") != std::string::npos;
   }
   CHECK(threw);
+
+  // on-disk formats (tests/test_dataset.cpp:64-84, 109-128, 182-197)
+  const std::string tmp = std::string(std::getenv("SK_TMP") ? std::getenv("SK_TMP") : "/tmp");
+  Image img(5, 3);
+  for (size_t i = 0; i < img.pixels.size(); ++i)
+    for (int c = 0; c < 3; ++c) img.pixels[i][c] = float((i * 3 + c) % 11) / 10.0f;
+  write_png(tmp + "/wrapper.png", img);
+  const Image back = read_png(tmp + "/wrapper.png");
+  CHECK(back.width == 5 && back.height == 3);
+  for (size_t i = 0; i < img.pixels.size(); ++i)
+    for (int c = 0; c < 3; ++c) CHECK(std::fabs(back.pixels[i][c] - img.pixels[i][c]) <= 0.5f / 255 + 1e-6f);
+  std::vector<std::pair<Vec3, Vec3>> pts(1);
+  pts[0].first[0] = 1.5f;
+  pts[0].second[1] = 1.0f;
+  write_points_ply(tmp + "/wrapper_points.ply", pts);
+  const auto pb = read_points_ply(tmp + "/wrapper_points.ply");
+  CHECK(pb.size() == 1 && pb[0].first[0] == 1.5f && pb[0].second[1] == 1.0f);
+  save_checkpoint(dev, scene, tmp + "/wrapper_ckpt.ply");
+  const Scene sb = load_checkpoint(dev, tmp + "/wrapper_ckpt.ply");
+  CHECK(sb.sh_degree == 1 && sb.size() == 1);
+  CHECK(sb.gaussians[0].mu[2] == 5.0f && sb.gaussians[0].sh(0, 1) == 0.5f);
   std::printf("%s (%d failures)\n", failures ? "FAIL" : "PASS", failures);
   return failures ? 1 : 0;
 }

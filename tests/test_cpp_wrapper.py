@@ -32,6 +32,6 @@ def test_cpp_wrapper_compiles_and_links(tmp_path):
 @pytest.mark.gpu
 def test_cpp_wrapper_runs_on_gpu(tmp_path):
     exe = _build(tmp_path)
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120, env=dict(os.environ, SK_TMP=str(tmp_path)))
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASS" in r.stdout
