@@ -282,6 +282,12 @@ typedef struct sk_train_config {
   int32_t size_prune_from, schedule_dry_run;
 } sk_train_config;
 void sk_default_config(sk_train_config* out);
+/* set_config_value (config.hpp:139-163): one `key = value` pair with the
+ * reference's key names ("bin_mode" = aabb|compact sets `compact`); unknown
+ * keys raise "config: unknown key '<key>'". ctx may be NULL. */
+int sk_config_set(sk_ctx* ctx, sk_train_config* cfg, const char* key, const char* value);
+/* load_config_file (config.hpp:167-196): flat key = value lines, '#' comments. */
+int sk_config_load_file(sk_ctx* ctx, sk_train_config* cfg, const char* path);
 /* TrainConfig::validate (config.hpp:63-80), same messages. */
 int sk_validate_config(sk_ctx* ctx, const sk_train_config* cfg);
 

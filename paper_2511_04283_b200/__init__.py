@@ -462,6 +462,25 @@ def default_config() -> SkTrainConfig:
     return c
 
 
+def load_config_file(path, cfg: SkTrainConfig | None = None) -> SkTrainConfig:
+    """load_config_file (config.hpp:167-196) onto cfg (default: defaults)."""
+    cfg = cfg if cfg is not None else default_config()
+    rc = lib().sk_config_load_file(None, C.byref(cfg), os.fsencode(path))
+    _io_check(rc, f"config file {path}")
+    return cfg
+
+
+def set_config_value(cfg: SkTrainConfig, key: str, value: str):
+    """set_config_value (config.hpp:139-163)."""
+    rc = lib().sk_config_set(None, C.byref(cfg), key.encode(), str(value).encode())
+    _io_check(rc, f"config: key '{key}' = '{value}'")
+
+
+def validate_config(cfg: SkTrainConfig):
+    """TrainConfig::validate (config.hpp:63-80)."""
+    _io_check(lib().sk_validate_config(None, C.byref(cfg)), "config: invalid")
+
+
 def as_config(cfg) -> SkTrainConfig:
     if isinstance(cfg, SkTrainConfig):
         return cfg

@@ -75,7 +75,28 @@ def build(verbose: bool = False, force: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_cli(verbose)
     return LIB
+
+
+CLI_SRC = os.path.join(HERE, "tools", "splatkit_cli.cpp")
+CLI = os.path.join(HERE, "splatkit_b200")
+
+
+def build_cli(verbose: bool = False) -> str:
+    """The splatkit_b200 command-line tool (host C++ over the C ABI)."""
+    if os.path.exists(CLI) and os.path.getmtime(CLI) >= max(os.path.getmtime(CLI_SRC), os.path.getmtime(LIB),
+                                                            _headers_mtime()):
+        return CLI
+    cxx = shutil.which("g++") or "g++"
+    cmd = [cxx, "-std=c++17", "-O2", "-Wall", "-I", INCLUDE, CLI_SRC, "-o", CLI, "-L", HERE, "-lsplatkit_b200",
+           "-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":

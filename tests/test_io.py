@@ -228,3 +228,33 @@ def test_cameras_json_errors(tmp_path):
                  '"world_to_cam": [1,0,0,0, 0,1,0,0, 0,0,1,0, 0,0,0,1]}]')
     cams, ids = sk.read_cameras_json(p)
     assert len(cams) == 1 and ids.tolist() == [0]
+
+
+def test_config_files_parse_override_and_reject_unknown_keys(tmp_path):
+    """test_dataset.cpp:253-285 (load_config_file, config.hpp:139-196)."""
+    p = tmp_path / "train.cfg"
+    p.write_text("# comment line\niterations = 1234\ntau = 0.25\nbin_mode = compact\nvcd = false\n")
+    cfg = sk.load_config_file(p)
+    assert cfg.iterations == 1234 and cfg.tau == pytest.approx(0.25)
+    assert cfg.compact == 1 and cfg.vcd == 0 and cfg.k == 10  # untouched keys keep their defaults
+    bad = tmp_path / "bad.cfg"
+    bad.write_text("not_a_real_key = 3\n")
+    with pytest.raises(sk.SplatError):
+        sk.load_config_file(bad)
+    rc = sk.lib().sk_config_set(None, sk.C.byref(cfg), b"vcp", b"maybe")
+    assert rc != 0
+    for k, v in (("seed", "18446744073709551615"), ("lambda", "0.3"), ("lazy_opt_enabled", "1"),
+                 ("bin_mode", "aabb")):
+        sk.set_config_value(cfg, k, v)
+    assert cfg.seed == 2 ** 64 - 1 and cfg.lambda_ == pytest.approx(0.3)
+    assert cfg.lazy_opt_enabled == 1 and cfg.compact == 0
+    with pytest.raises(sk.SplatError):
+        sk.set_config_value(cfg, "iterations", "many")
+    malformed = tmp_path / "m.cfg"
+    malformed.write_text("iterations 5\n")
+    with pytest.raises(sk.SplatError):
+        sk.load_config_file(malformed)
+    invalid = sk.default_config()
+    invalid.densify_every = 600  # does not divide 14500
+    with pytest.raises((sk.SplatError, ValueError)):
+        sk.validate_config(invalid)
