@@ -203,6 +203,31 @@ SK_HD float det_sigmoidf(float x, const SmemTable& table) { return 1.0f / (1.0f 
 #endif
 
 #if defined(__CUDACC__)
+// e^x on [-5.71, 0] for the blend kernels (x = -q/2 with q <= q_cut < 11.11).
+// Same Cody-Waite reduction and polynomial as det_expf_core, but the table
+// is indexed by m = -k and already carries the power of two:
+// T[m] = table[k & 63] * 2^((k - (k & 63)) / 64), built by adding the exponent
+// to the table bits (exact). Since the scaling by 2^e is exact in the normal
+// range, rn(T[m] * p) == rn(rn(table[j] * p) * 2^e): bit-identical to
+// det_expf_core, with the index / exponent integer work removed.
+constexpr int kNegExpTable = 528;
+__device__ __forceinline__ void stage_neg_exp_table(float* s_table) {
+  for (int m = threadIdx.x; m < kNegExpTable; m += blockDim.x) {
+    const int k = -m, j = k & 63, e = (k - j) / 64;
+    s_table[m] = bits_to_f32(kExp2TableDev[j] + ((uint32_t)e << 23));
+  }
+}
+__device__ __forceinline__ float det_expf_neg(float x, const SmemTable& neg_table) {
+  const float kf = det_floorf(rn_add(rn_mul(x, 92.33248261689366f), 0.5f));  // 64 / ln2
+  const float r = rn_sub(rn_sub(x, rn_mul(kf, 0.010833740234375f)), rn_mul(kf, -3.3155381258549027e-06f));
+  float p = rn_add(rn_mul(r, 0.16666666666666666f), 0.5f);
+  p = rn_add(rn_mul(p, r), 1.0f);
+  p = rn_add(rn_mul(p, r), 1.0f);
+  return rn_mul(neg_table[-(int)kf], p);
+}
+#endif
+
+#if defined(__CUDACC__)
 // Stages the exp table into shared memory; call from all threads, then sync.
 __device__ __forceinline__ void stage_exp2_table(float* s_table) {
   for (int i = threadIdx.x; i < 64; i += blockDim.x) s_table[i] = bits_to_f32(kExp2TableDev[i]);

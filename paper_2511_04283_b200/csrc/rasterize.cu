@@ -40,9 +40,9 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
   __shared__ uint32_t s_mask[WB::kWarps * kChunks];
   __shared__ float4 s_rgb[COUNT ? 1 : B];
   __shared__ uint32_t s_id[COUNT ? B : 1];
-  __shared__ float s_exp2[64];
-  stage_exp2_table(s_exp2);  // published by the first __syncthreads_count below
-  const SmemTable tab(s_exp2);
+  __shared__ float s_exp[kNegExpTable];
+  stage_neg_exp_table(s_exp);  // published by the first __syncthreads_count below
+  const SmemTable tab(s_exp);
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
         const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
         if (done[k] || !(q >= 0.0f && q <= mq.z)) continue;
         // -0.5 q lies in [-q_cut/2, 0], inside det_expf's core range
-        float alpha = co.w * det_expf_core(-0.5f * q, tab);
+        float alpha = co.w * det_expf_neg(-0.5f * q, tab);
         alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
         if (alpha < kAlphaMin) continue;
         if (COUNT) {
