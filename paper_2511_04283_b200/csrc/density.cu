@@ -15,6 +15,9 @@
 // a scatter of parameters and Adam moments into fresh buffers.
 #include <algorithm>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <functional>
 
 #include "abi_util.h"
@@ -277,6 +280,18 @@ __global__ void compact_kernel(const float* __restrict__ src, const float* __res
 
 unsigned blocks(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
 
+// SK_TRACE_EVENTS=1: synchronising host timestamps of the density-event
+// sub-steps on stderr (diagnostics only; off by default).
+void trace_point(sk_ctx* ctx, const char* what) {
+  static const bool on = std::getenv("SK_TRACE_EVENTS") != nullptr;
+  if (!on) return;
+  static auto last = std::chrono::steady_clock::now();
+  SK_CUDA(cudaStreamSynchronize(ctx->stream));
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[event] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
+
 }  // namespace
 
 // Renders the k views and leaves s_d / s_p_raw / s_p in the scene's table.
@@ -427,6 +442,7 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
   if (n == 0) return 0;
   int32_t* cls = ensure<int32_t>(ev.cls, 3 * (size_t)n);
   int32_t* pos = ensure<int32_t>(ev.pos, 3 * (size_t)n);
+  trace_point(ctx, "compact: enter");
   class_kernel<<<blocks(n), 256, 0, ctx->stream>>>(prune, clone, split, n, cls, cls + n, cls + 2 * n);
   note_launch();
   const int64_t n_keep = scan_gathered(ctx, cls, nullptr, pos, n);
@@ -434,7 +450,9 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
   const int64_t n_split = scan_gathered(ctx, cls + 2 * n, nullptr, pos + 2 * n, n);
   const int64_t new_n = n_keep + n_clone + 2 * n_split;
   float* eps = ensure<float>(ev.eps, 6 * (size_t)std::max<int64_t>(n_split, 1));
+  trace_point(ctx, "compact: class + 3 scans");
   const float* eps_host = eps_source(n_split);
+  trace_point(ctx, "compact: split normals");
   if (n_split > 0) {
     require(eps_host != nullptr, "apply_densify: split requires eps normals");
     h2d(ctx, eps, eps_host, 6 * (size_t)n_split);
@@ -458,6 +476,7 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
   note_launch();
   SK_CUDA(cudaGetLastError());
   sync(ctx);
+  trace_point(ctx, "compact: eps upload + kernel");
   s->params.swap(np);
   s->adam_m.swap(nm);
   s->adam_v.swap(nv);
@@ -471,6 +490,7 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
   s->n = new_n;
   ensure_optimizer_state(ctx, s);
   reset_score_table(ctx, s);
+  trace_point(ctx, "compact: state reset");
   return new_n;
 }
 
@@ -492,8 +512,10 @@ void density_event(sk_trainer* t, int it, bool densify, bool prune) {
     rec.sampled.push_back(v);
   }
   const sk_binning bin = binning_from(cfg);
+  trace_point(ctx, "event: enter");
   allreduce_stats(t->comm, s, ctx->stream);  // C2
   score_pass(ctx, s, &t->frame, cams, gts, true, (float)cfg.tau, (float)cfg.lambda, bin, &rec.photometric, t->comm);
+  trace_point(ctx, "score pass (K views, K13)");
 
   const int64_t n = s->n;
   uint8_t* flags = ensure<uint8_t>(ctx->ev.flags, 3 * (size_t)std::max<int64_t>(n, 1));
@@ -518,6 +540,7 @@ void density_event(sk_trainer* t, int it, bool densify, bool prune) {
     select_prune_flags(ctx, s, it, pp, extent, fprune);
   }
   ctx->event_mark(3);
+  trace_point(ctx, "select (K14)");
   // The split count (for the Rng) comes from the device scans inside
   // compact_scene; the flags are only downloaded for the event record.
   const float pos_lr = expon_lr((float)cfg.lr_position * extent, (float)cfg.lr_position_final * extent, it,

@@ -20,6 +20,13 @@
 // K8 (the backward walk) lives in rasterize_bwd.cu.
 #include "blend_common.cuh"
 
+#ifndef SK_FWD_WARP_STAGED
+#define SK_FWD_WARP_STAGED 0
+#endif
+#ifndef SK_FWD_PIX16
+#define SK_FWD_PIX16 2
+#endif
+
 namespace sk {
 namespace {
 
@@ -149,6 +156,119 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
   }
 }
 
+// K6, warp-staged variant: each warp walks the tile's list for its own
+// 8 x 4·PIX pixel block independently — it stages 32 entries at a time (one
+// per lane: gather, q-cut box, exact ellipse test against its own block),
+// keeps only the hits (ballot) in its private shared slots and walks them. No
+// CTA barrier inside the list walk, so warps neither wait for each other at
+// batch boundaries nor keep staging after their own pixels have terminated;
+// the price is that each warp gathers every entry (L1 serves the repeats).
+// Per-pixel arithmetic is identical to blend_fwd_kernel (bit-exact).
+template <int TS, int PIX>
+__global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fwd_warp_kernel(
+    const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
+    const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
+    float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry) {
+  using WB = WarpBlock<TS, PIX>;
+  constexpr int kWarps = WB::kWarps;
+  __shared__ float4 s_xyq[kWarps][32];
+  __shared__ float4 s_co[kWarps][32];
+  __shared__ float4 s_rgb[kWarps][32];
+  __shared__ float s_exp[kNegExpTable];
+  stage_neg_exp_table(s_exp);
+  __syncthreads();
+  const SmemTable tab(s_exp);
+
+  const int tile = blockIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const WB wb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int px = tx * TS + wb.lx;
+  const int2 range = ranges[tile];
+  const float fpx = (float)px;
+
+  float T[PIX], C0[PIX], C1[PIX], C2[PIX], fpy[PIX];
+  int n[PIX], last[PIX];
+  bool done[PIX];
+  bool all_done = true;
+#pragma unroll
+  for (int k = 0; k < PIX; ++k) {
+    const int py = ty * TS + wb.ly0 + 4 * k;
+    fpy[k] = (float)py;
+    T[k] = 1.0f;
+    C0[k] = C1[k] = C2[k] = 0.0f;
+    n[k] = last[k] = 0;
+    done[k] = !(px < W && py < H);
+    all_done = all_done && done[k];
+  }
+
+  for (int b0 = range.x; b0 < range.y; b0 += 32) {
+    if (__all_sync(0xffffffffu, all_done)) break;
+    const int i = b0 + lane;
+    bool hit = false;
+    if (i < range.y) {
+      const uint32_t g = pair_val[i];
+      const float4 co = conic_op[g];
+      float4 xyq, bb;
+      stage_entry(mean2d[g], co, xyq, bb);
+      hit = !WB::misses(bb, warp, tx, ty);
+      const bool pd = co.x > 0.0f && co.z > 0.0f && co.x * co.z - co.y * co.y > 0.0f;
+      if (hit && pd) hit = WB::ellipse_hits(xyq, co, warp, tx, ty);
+      if (hit) {
+        s_xyq[warp][lane] = xyq;
+        s_co[warp][lane] = co;
+        s_rgb[warp][lane] = rgbd[g];
+      }
+    }
+    uint32_t m = __ballot_sync(0xffffffffu, hit);
+    __syncwarp();
+    while (m && !all_done) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const float4 mq = s_xyq[warp][j];
+      const float4 co = s_co[warp][j];
+#pragma unroll
+      for (int k = 0; k < PIX; ++k) {
+        const float dx = fpx - mq.x;
+        const float dy = fpy[k] - mq.y;
+        const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
+        if (done[k] || !(q >= 0.0f && q <= mq.z)) continue;
+        float alpha = co.w * det_expf_neg(-0.5f * q, tab);
+        alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
+        if (alpha < kAlphaMin) continue;
+        const float4 c = s_rgb[warp][j];
+        const float w = T[k] * alpha;
+        C0[k] = C0[k] + w * c.x;
+        C1[k] = C1[k] + w * c.y;
+        C2[k] = C2[k] + w * c.z;
+        ++n[k];
+        last[k] = b0 + j + 1;
+        T[k] = T[k] * (1.0f - alpha);
+        if (T[k] < kTransmitMin) done[k] = true;
+      }
+      bool ad = true;
+#pragma unroll
+      for (int k = 0; k < PIX; ++k) ad = ad && done[k];
+      all_done = ad;
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int k = 0; k < PIX; ++k) {
+    const int py = ty * TS + wb.ly0 + 4 * k;
+    if (px < W && py < H) {
+      const size_t p = (size_t)py * W + px;
+      const size_t plane = (size_t)W * H;
+      image[p] = C0[k];
+      image[plane + p] = C1[k];
+      image[2 * plane + p] = C2[k];
+      final_t[p] = T[k];
+      n_contrib[p] = n[k];
+      last_entry[p] = last[k];
+    }
+  }
+}
+
 // Workload counters of a rendered frame: pixel-Gaussian
 // evaluations the reference's blend_forward loop visits (raster.hpp:219-235:
 // every list entry up to and including the one that takes T below 1e-4, or
@@ -188,6 +308,10 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
     blend_fwd_kernel<TS, PIX, true><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
         ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
         f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), mask, counts);
+  else if (SK_FWD_WARP_STAGED)
+    blend_fwd_warp_kernel<TS, PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
+        ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
+        f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>());
   else
     blend_fwd_kernel<TS, PIX, false><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
         ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
@@ -216,7 +340,7 @@ void launch_blend_forward(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t
   if (f->tiles_x * f->tiles_y == 0) return;
   switch (f->tile_size) {
     case 8: fwd_dispatch<8, 1>(ctx, f, mask, counts); break;
-    case 16: fwd_dispatch<16, 2>(ctx, f, mask, counts); break;
+    case 16: fwd_dispatch<16, SK_FWD_PIX16>(ctx, f, mask, counts); break;
     case 32: fwd_dispatch<32, 4>(ctx, f, mask, counts); break;
     default: throw std::invalid_argument("tile_size must be 8, 16 or 32");
   }

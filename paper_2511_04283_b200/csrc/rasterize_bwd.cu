@@ -70,7 +70,11 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 #define SK_BWD_MINB 10
 #endif
 
-template <int TS, int PIX, bool FASTEXP = true>
+#ifndef SK_BWD_WARP_STAGED
+#define SK_BWD_WARP_STAGED 0
+#endif
+
+template <int TS, int PIX, bool WS = SK_BWD_WARP_STAGED != 0, bool FASTEXP = true>
 __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB) blend_bwd_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
@@ -121,8 +125,8 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB) blend_bwd_kernel(
     my_last = max(my_last, last[k]);
   }
   if (threadIdx.x == 0) s_max_last = 0;
-  __syncthreads();
-  atomicMax(&s_max_last, my_last);
+  __syncthreads();  // also publishes the exp table
+  if (!WS) atomicMax(&s_max_last, my_last);
   __syncthreads();
   const int end = s_max_last;  // no pixel of the tile uses entries >= end
   const int warp_last = __reduce_max_sync(0xffffffffu, my_last);
@@ -130,6 +134,111 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB) blend_bwd_kernel(
   uint32_t pend_id = 0;
   bool has_pend = false;
 
+  // Per-entry reverse-walk step for staged slot j (list position idx).
+  auto walk_entry = [&](int j, int idx) {
+    const float4 mq = s_xyq[j];
+    const float4 co = s_co[j];
+    float g_mu0 = 0.f, g_mu1 = 0.f, g_c00 = 0.f, g_c01 = 0.f, g_c11 = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f,
+          g_op = 0.f, g_a0 = 0.f, g_a1 = 0.f;
+    bool contrib = false;
+#pragma unroll
+    for (int k = 0; k < PIX; ++k) {
+      if (idx >= last[k]) continue;
+      const float dx = fpx - mq.x;
+      const float dy = fpy[k] - mq.y;
+      // same association as K6: ((c00 dx) dx + ((2 c01) dx) dy) + (c11 dy) dy
+      const float q = rn_add(rn_add(rn_mul(rn_mul(co.x, dx), dx), rn_mul(rn_mul(rn_mul(2.0f, co.y), dx), dy)),
+                             rn_mul(rn_mul(co.z, dy), dy));
+      if (!(q >= 0.0f && q <= mq.z)) continue;
+      // Fast exp (MUFU ex2, ~1e-6 relative); the exact deterministic exp
+      // only where alpha is within 1e-5 (relative) of a decision threshold,
+      // so the skip / cap decisions are exactly K6's.
+      float ge = FASTEXP ? __expf(-0.5f * q) : 0.0f;
+      float raw = co.w * ge;
+      if (!FASTEXP || fabsf(raw - kAlphaMin) <= 1e-5f * kAlphaMin || fabsf(raw - kAlphaCap) <= 1e-5f * kAlphaCap) {
+        ge = det_expf_core(rn_mul(-0.5f, q), tab);
+        raw = rn_mul(co.w, ge);
+      }
+      const bool capped = raw > kAlphaCap;
+      const float alpha = capped ? kAlphaCap : raw;
+      if (alpha < kAlphaMin) continue;
+      contrib = true;
+      const float4 c = s_rgb[j];
+      const float one_m = 1.0f - alpha;
+      const float inv_one_m = __fdividef(1.0f, one_m);  // tolerance path: MUFU reciprocal, two products
+      const float t_before = T[k] * inv_one_m;
+      T[k] = t_before;
+      const float w = (c.x * d0[k] + c.y * d1[k]) + c.z * d2[k];
+      const float d_alpha = t_before * w - suffix[k] * inv_one_m;
+      const float ta = t_before * alpha;
+      suffix[k] = suffix[k] + ta * w;
+      g_r += ta * d0[k];
+      g_g += ta * d1[k];
+      g_b += ta * d2[k];
+      if (!capped) {
+        g_op += ge * d_alpha;
+        const float d_q = -0.5f * alpha * d_alpha;
+        g_c00 += d_q * (dx * dx);
+        g_c01 += d_q * (dx * dy);
+        g_c11 += d_q * (dy * dy);
+        const float v0 = co.x * dx + co.y * dy;
+        const float v1 = co.y * dx + co.z * dy;
+        const float m0 = (-2.0f * d_q) * v0;
+        const float m1 = (-2.0f * d_q) * v1;
+        g_mu0 += m0;
+        g_mu1 += m1;
+        g_a0 += fabsf(m0);
+        g_a1 += fabsf(m1);
+      }
+    }
+    if (__any_sync(0xffffffffu, contrib)) {
+      const float gv[kBGradFields] = {g_mu0, g_mu1, g_c00, g_c01, g_c11, g_r, g_g, g_b, g_op, g_a0, g_a1};
+      if (has_pend) {
+        reduce_scatter_2x11(pend, gv, pend_id, s_id[j], true, bgrads, gstride);
+        has_pend = false;
+      } else {
+#pragma unroll
+        for (int f = 0; f < kBGradFields; ++f) pend[f] = gv[f];
+        pend_id = s_id[j];
+        has_pend = true;
+      }
+    }
+  };
+
+  if (WS) {
+    // Warp-staged: each warp gathers 32 entries at a time from its own last
+    // contributor downward, keeps the hits on its block (ballot) in its
+    // private slots and walks them; no CTA barrier inside the walk.
+    const int base = warp * 32;
+    for (int b_end = warp_last; b_end > range.x; b_end -= 32) {
+      const int b0 = max(range.x, b_end - 32);
+      const int i = b0 + lane;
+      bool hit = false;
+      if (i < b_end) {
+        const uint32_t g = pair_val[i];
+        const float4 co = conic_op[g];
+        float4 xyq, bb;
+        stage_entry(mean2d[g], co, xyq, bb);
+        hit = !WB::misses(bb, warp, tx, ty);
+        const bool pd = co.x > 0.0f && co.z > 0.0f && co.x * co.z - co.y * co.y > 0.0f;
+        if (hit && pd) hit = WB::ellipse_hits(xyq, co, warp, tx, ty);
+        if (hit) {
+          s_xyq[base + lane] = xyq;
+          s_co[base + lane] = co;
+          s_rgb[base + lane] = rgbd[g];
+          s_id[base + lane] = g;
+        }
+      }
+      uint32_t m = __ballot_sync(0xffffffffu, hit);
+      __syncwarp();
+      while (m) {
+        const int bit = 31 - __clz(m);
+        m ^= 1u << bit;
+        walk_entry(base + bit, b0 + bit);
+      }
+      __syncwarp();
+    }
+  } else {
   for (int b_end = end; b_end > range.x; b_end -= NT) {
     const int b0 = max(range.x, b_end - NT);
     __syncthreads();
@@ -154,79 +263,12 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB) blend_bwd_kernel(
       const int lim = jmax - c * 32;
       if (lim < 32) m &= (1u << lim) - 1u;
       while (m) {
-      const int bit = 31 - __clz(m);
-      m ^= 1u << bit;
-      const int j = c * 32 + bit;
-      const int idx = b0 + j;
-      const float4 mq = s_xyq[j];
-      const float4 co = s_co[j];
-      float g_mu0 = 0.f, g_mu1 = 0.f, g_c00 = 0.f, g_c01 = 0.f, g_c11 = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f,
-            g_op = 0.f, g_a0 = 0.f, g_a1 = 0.f;
-      bool contrib = false;
-#pragma unroll
-      for (int k = 0; k < PIX; ++k) {
-        if (idx >= last[k]) continue;
-        const float dx = fpx - mq.x;
-        const float dy = fpy[k] - mq.y;
-        // same association as K6: ((c00 dx) dx + ((2 c01) dx) dy) + (c11 dy) dy
-        const float q = rn_add(rn_add(rn_mul(rn_mul(co.x, dx), dx), rn_mul(rn_mul(rn_mul(2.0f, co.y), dx), dy)),
-                               rn_mul(rn_mul(co.z, dy), dy));
-        if (!(q >= 0.0f && q <= mq.z)) continue;
-        // Fast exp (MUFU ex2, ~1e-6 relative); the exact deterministic exp
-        // only where alpha is within 1e-5 (relative) of a decision threshold,
-        // so the skip / cap decisions are exactly K6's.
-        float ge = FASTEXP ? __expf(-0.5f * q) : 0.0f;
-        float raw = co.w * ge;
-        if (!FASTEXP || fabsf(raw - kAlphaMin) <= 1e-5f * kAlphaMin || fabsf(raw - kAlphaCap) <= 1e-5f * kAlphaCap) {
-          ge = det_expf_core(rn_mul(-0.5f, q), tab);
-          raw = rn_mul(co.w, ge);
-        }
-        const bool capped = raw > kAlphaCap;
-        const float alpha = capped ? kAlphaCap : raw;
-        if (alpha < kAlphaMin) continue;
-        contrib = true;
-        const float4 c = s_rgb[j];
-        const float one_m = 1.0f - alpha;
-        const float inv_one_m = __fdividef(1.0f, one_m);  // tolerance path: MUFU reciprocal, two products
-        const float t_before = T[k] * inv_one_m;
-        T[k] = t_before;
-        const float w = (c.x * d0[k] + c.y * d1[k]) + c.z * d2[k];
-        const float d_alpha = t_before * w - suffix[k] * inv_one_m;
-        const float ta = t_before * alpha;
-        suffix[k] = suffix[k] + ta * w;
-        g_r += ta * d0[k];
-        g_g += ta * d1[k];
-        g_b += ta * d2[k];
-        if (!capped) {
-          g_op += ge * d_alpha;
-          const float d_q = -0.5f * alpha * d_alpha;
-          g_c00 += d_q * (dx * dx);
-          g_c01 += d_q * (dx * dy);
-          g_c11 += d_q * (dy * dy);
-          const float v0 = co.x * dx + co.y * dy;
-          const float v1 = co.y * dx + co.z * dy;
-          const float m0 = (-2.0f * d_q) * v0;
-          const float m1 = (-2.0f * d_q) * v1;
-          g_mu0 += m0;
-          g_mu1 += m1;
-          g_a0 += fabsf(m0);
-          g_a1 += fabsf(m1);
-        }
-      }
-      if (__any_sync(0xffffffffu, contrib)) {
-        const float gv[kBGradFields] = {g_mu0, g_mu1, g_c00, g_c01, g_c11, g_r, g_g, g_b, g_op, g_a0, g_a1};
-        if (has_pend) {
-          reduce_scatter_2x11(pend, gv, pend_id, s_id[j], true, bgrads, gstride);
-          has_pend = false;
-        } else {
-#pragma unroll
-          for (int f = 0; f < kBGradFields; ++f) pend[f] = gv[f];
-          pend_id = s_id[j];
-          has_pend = true;
-        }
-      }
+        const int bit = 31 - __clz(m);
+        m ^= 1u << bit;
+        walk_entry(c * 32 + bit, b0 + c * 32 + bit);
       }
     }
+  }
   }
   if (has_pend) {  // warp-uniform: flush the last unpaired entry
     float zero[kBGradFields];

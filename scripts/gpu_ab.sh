@@ -6,7 +6,10 @@ mkdir -p gpurun_out
 for spec in "$@"; do
   name=${spec%%=*}; flags=${spec#*=}
   SK_NVCC_EXTRA="$flags" python -c "import paper_2511_04283_b200 as sk; sk.build(force=True)" || continue
-  timeout 300 python bench.py --steps 60 --warmup 20 --no-cpu-baseline > gpurun_out/ab_${TAG}_$name.json 2>/dev/null
+  if [ -n "$AB_TEST" ]; then
+    timeout 600 python -m pytest $AB_TEST -m gpu -x -q 2>&1 | tail -1 | sed "s/^/$name tests: /"
+  fi
+  timeout 300 python bench.py --steps ${AB_STEPS:-100} --warmup ${AB_WARM:-100} --no-cpu-baseline > gpurun_out/ab_${TAG}_$name.json 2>/dev/null
   python - "$name" gpurun_out/ab_${TAG}_$name.json <<'PY'
 import json, sys
 try:
