@@ -421,6 +421,18 @@ int sk_shard_assign(int n_items, int world, int rank, int32_t* owned, int* n_own
  * GT image in HOST memory (copied in) — the end-to-end entry point. */
 int sk_train_step_host(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_camera* cam, const uint8_t* gt_host,
                        const sk_train_config* cfg, float extent, int iteration, sk_log_row* row);
+/* Pipelined variant for streaming inputs: the GT upload runs on a copy
+ * stream into one of two device buffers (overlapping the previous step), and
+ * `row` (loss / PSNR / pairs) is written when the step completes — during the
+ * next call on this frame, or at sk_train_step_host_flush. `row` and
+ * `gt_host` (pinned memory for a truly asynchronous copy) must stay valid
+ * until then. Parameters and results are those of sk_train_step_host; with
+ * a communicator (view-parallel steps) the gradients are summed
+ * over its ranks before Adam (C1), as in sk_trainer_run. comm may be NULL. */
+int sk_train_step_host_async(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_camera* cam,
+                             const uint8_t* gt_host, const sk_train_config* cfg, float extent, int iteration,
+                             sk_log_row* row, const sk_comm* comm);
+int sk_train_step_host_flush(sk_ctx* ctx, sk_frame* frame);
 
 #ifdef __cplusplus
 }

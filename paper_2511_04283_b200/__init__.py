@@ -895,6 +895,32 @@ def train_step_host(ctx: Context, scene: Scene, cam, gt_u8, cfg, extent, iterati
     return dict(loss=row.loss, psnr=row.psnr, tile_pairs=row.tile_pairs, gaussians=row.gaussians)
 
 
+class HostStepPipeline:
+    """Pipelined end-to-end steps (sk_train_step_host_async): the GT upload of
+    each step overlaps the previous step on a copy stream and each step's
+    loss is read back when the next step is issued (or at flush()). Rows are
+    kept alive here until they are filled."""
+
+    def __init__(self, ctx: Context, frame=None, comm=None):
+        self.ctx = ctx
+        self.frame = frame or ctx._frame
+        self.comm = comm
+        self.rows = []
+
+    def step(self, scene: Scene, cam, gt_u8_pinned: np.ndarray, cfg, extent, iteration):
+        row = SkLogRow()
+        self.rows.append(row)
+        self.ctx.check(self.ctx._lib.sk_train_step_host_async(
+            self.ctx.h, scene.h, self.frame, C.byref(as_camera(cam)), _p(gt_u8_pinned), C.byref(as_config(cfg)),
+            C.c_float(extent), C.c_int(iteration), C.byref(row), self.comm.h if self.comm is not None else None))
+
+    def flush(self):
+        self.ctx.check(self.ctx._lib.sk_train_step_host_flush(self.ctx.h, self.frame))
+        out = [dict(iteration=r.iteration, loss=r.loss, psnr=r.psnr, tile_pairs=r.tile_pairs) for r in self.rows]
+        self.rows = []
+        return out
+
+
 # ---------------------------------------------------------------------------
 # multi-GPU: NCCL communicator (view sharding, SURVEY §8e)
 # ---------------------------------------------------------------------------

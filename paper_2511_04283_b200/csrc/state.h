@@ -2,6 +2,8 @@
 // and the launchers each kernel translation unit exports.
 #pragma once
 
+#include <memory>
+
 #include "common.cuh"
 
 namespace sk {
@@ -18,6 +20,41 @@ struct SortTemp {
 }  // namespace sk
 
 namespace sk {
+// A training step whose loss / error-word readback is deferred: completed
+// (event wait + host arithmetic) while the next step's K1 runs.
+struct PendingStep {
+  bool active = false;
+  int it = 0, width = 0, height = 0, tev_set = 0;
+  float lambda = 0.2f;
+  int64_t pairs = 0, n = 0;
+  sk_log_row* row = nullptr;
+  cudaEvent_t done = nullptr;
+  HostBuf pinned;  // [2 slots][4 doubles + error word]
+  int slot = 0;
+  ~PendingStep() {
+    if (done) cudaEventDestroy(done);
+  }
+};
+
+// Pipelined host-input steps (sk_train_step_host_async): the GT upload of
+// step k runs on a copy stream into one of two device buffers, overlapping
+// step k-1; a buffer is refilled only after the step that read it is done.
+struct HostPipe {
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ready[2] = {}, consumed[2] = {};
+  bool consumed_recorded[2] = {false, false};
+  DevBuf gt[2];
+  int slot = 0;
+  PendingStep pend;
+  ~HostPipe() {
+    for (int i = 0; i < 2; ++i) {
+      if (ready[i]) cudaEventDestroy(ready[i]);
+      if (consumed[i]) cudaEventDestroy(consumed[i]);
+    }
+    if (copy) cudaStreamDestroy(copy);
+  }
+};
+
 // Scratch for density-control events (K11-K15).
 struct EventScratch {
   DevBuf rows;       // int32 [k][n] footprint counts per sampled view
@@ -132,6 +169,7 @@ struct sk_frame {
   sk::DevBuf gt;      // staging for GT (u8 or f32)
   sk::DevBuf mask;    // u8 [H][W]
   sk::DevBuf counts;  // int32 [n]
+  std::unique_ptr<sk::HostPipe> pipe;  // sk_train_step_host_async state
 };
 
 namespace sk {

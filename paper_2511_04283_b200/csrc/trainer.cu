@@ -579,11 +579,50 @@ int sk_train_step_host(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_c
   return guarded(ctx, [&] {
     arg(scene && frame && cam && gt_host && cfg, "sk_train_step_host: bad arguments");
     SK_CUDA(cudaSetDevice(ctx->device));
+    if (frame->pipe) finish_pending(ctx, &frame->pipe->pend);  // an async step in flight completes first
     ensure_optimizer_state(ctx, scene);
     const size_t bytes = (size_t)cam->width * cam->height * 3;
     void* gt = frame->gt.ensure(bytes);
     SK_CUDA(cudaMemcpyAsync(gt, gt_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
     train_step(ctx, scene, frame, *cam, static_cast<const uint8_t*>(gt), *cfg, extent, iteration, row);
+  });
+}
+
+int sk_train_step_host_async(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_camera* cam,
+                             const uint8_t* gt_host, const sk_train_config* cfg, float extent, int iteration,
+                             sk_log_row* row, const sk_comm* comm) {
+  return guarded(ctx, [&] {
+    arg(scene && frame && cam && gt_host && cfg, "sk_train_step_host_async: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    ensure_optimizer_state(ctx, scene);
+    if (!frame->pipe) {
+      auto p = std::make_unique<HostPipe>();
+      SK_CUDA(cudaStreamCreateWithFlags(&p->copy, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        SK_CUDA(cudaEventCreateWithFlags(&p->ready[i], cudaEventDisableTiming));
+        SK_CUDA(cudaEventCreateWithFlags(&p->consumed[i], cudaEventDisableTiming));
+      }
+      frame->pipe = std::move(p);
+    }
+    HostPipe& p = *frame->pipe;
+    const int slot = p.slot ^= 1;
+    const size_t bytes = (size_t)cam->width * cam->height * 3;
+    void* gt = p.gt[slot].ensure(bytes);
+    if (p.consumed_recorded[slot]) SK_CUDA(cudaStreamWaitEvent(p.copy, p.consumed[slot], 0));
+    SK_CUDA(cudaMemcpyAsync(gt, gt_host, bytes, cudaMemcpyHostToDevice, p.copy));
+    SK_CUDA(cudaEventRecord(p.ready[slot], p.copy));
+    SK_CUDA(cudaStreamWaitEvent(ctx->stream, p.ready[slot], 0));
+    train_step(ctx, scene, frame, *cam, static_cast<const uint8_t*>(gt), *cfg, extent, iteration, row, comm,
+               &p.pend);
+    SK_CUDA(cudaEventRecord(p.consumed[slot], ctx->stream));
+    p.consumed_recorded[slot] = true;
+  });
+}
+
+int sk_train_step_host_flush(sk_ctx* ctx, sk_frame* frame) {
+  return guarded(ctx, [&] {
+    arg(frame != nullptr, "sk_train_step_host_flush: null frame");
+    if (frame->pipe) finish_pending(ctx, &frame->pipe->pend);
   });
 }
 

@@ -117,19 +117,6 @@ namespace sk {
 // A training step whose loss / error-word readback is deferred: the host
 // reads it while the next step's first kernels run, so the GPU does not idle
 // on the end-of-step synchronisation (Trainer::run only).
-struct PendingStep {
-  bool active = false;
-  int it = 0, width = 0, height = 0, tev_set = 0;
-  float lambda = 0.2f;
-  int64_t pairs = 0, n = 0;
-  sk_log_row* row = nullptr;
-  cudaEvent_t done = nullptr;
-  HostBuf pinned;  // [2 slots][4 doubles + error word]
-  int slot = 0;
-  ~PendingStep() {
-    if (done) cudaEventDestroy(done);
-  }
-};
 }  // namespace sk
 
 struct sk_trainer {

@@ -1,0 +1,44 @@
+"""The pipelined end-to-end entry point (sk_train_step_host_async): the same
+training steps as the synchronous sk_train_step_host, with the GT uploads on a
+copy stream and each step's loss delivered one call later."""
+import numpy as np
+import pytest
+
+from tests.util import ring_camera, synthetic_scene
+
+pytestmark = pytest.mark.gpu
+
+
+def test_async_host_steps_match_sync(orc):
+    import torch
+
+    import paper_2511_04283_b200 as sk
+    sk.build()
+    ctx = sk.Context(0)
+    p = synthetic_scene(4000, deg=3, seed=21)
+    cams = [ring_camera(orc, 128, 96, a) for a in (0.0, 0.9, 2.1)]
+    gts = []
+    for v, cam in enumerate(cams):
+        r = orc.render_scene(synthetic_scene(4000, deg=3, seed=22), 3, cam)
+        g = torch.empty(r.image.size, dtype=torch.uint8, pin_memory=True).numpy().reshape(r.image.shape)
+        g[...] = np.clip(np.rint(r.image * 255), 0, 255).astype(np.uint8)
+        gts.append(g)
+    cfg = sk.default_config()
+    cfg.densify_from = cfg.densify_until = 1 << 30
+    a = ctx.scene(p, 3)
+    b = ctx.scene(p, 3)
+    sync_rows = [sk.train_step_host(ctx, a, cams[k % 3], gts[k % 3], cfg, 3.0, k + 1) for k in range(9)]
+    pipe = sk.HostStepPipeline(ctx)
+    for k in range(9):
+        pipe.step(b, cams[k % 3], gts[k % 3], cfg, 3.0, k + 1)
+    rows = pipe.flush()
+    assert [r["iteration"] for r in rows] == list(range(1, 10))
+    for s, r in zip(sync_rows, rows):
+        assert r["tile_pairs"] == s["tile_pairs"]
+        assert r["loss"] == pytest.approx(s["loss"], rel=1e-4)
+    np.testing.assert_allclose(b.download(), a.download(), rtol=1e-4, atol=1e-5)
+    # a synchronous step after async ones completes the pending step first
+    pipe.step(b, cams[0], gts[0], cfg, 3.0, 10)
+    sk.train_step_host(ctx, b, cams[1], gts[1], cfg, 3.0, 11)
+    assert pipe.flush()[0]["iteration"] == 10
+    ctx.close()
