@@ -195,50 +195,84 @@ __global__ void class_kernel(const uint8_t* __restrict__ prune, const uint8_t* _
   split_k[i] = sp ? 1 : 0;
 }
 
-__global__ void compact_kernel(const float* __restrict__ src, const float* __restrict__ m_src,
-                               const float* __restrict__ v_src, int64_t stride, int64_t n, int comps,
-                               const int32_t* __restrict__ keep_ns, const int32_t* __restrict__ clone_k,
-                               const int32_t* __restrict__ split_k, const int32_t* __restrict__ pos_keep,
-                               const int32_t* __restrict__ pos_clone, const int32_t* __restrict__ pos_split,
-                               int64_t n_keep, int64_t n_clone, const float* __restrict__ grad3d,
-                               const int* __restrict__ views_seen, float clone_lr, const float* __restrict__ eps,
-                               float log_shrink, float* __restrict__ dst, float* __restrict__ m_dst,
-                               float* __restrict__ v_dst, int64_t dstride, int32_t* __restrict__ old_to_new) {
+// Destination slots of source Gaussian i (adc.hpp:179-201 output order:
+// non-split survivors, then clones, then split pairs): x = survivor slot,
+// y = clone slot, z = first split child; -1 when absent.
+__global__ void route_kernel(const int32_t* __restrict__ keep_ns, const int32_t* __restrict__ clone_k,
+                             const int32_t* __restrict__ split_k, const int32_t* __restrict__ pos_keep,
+                             const int32_t* __restrict__ pos_clone, const int32_t* __restrict__ pos_split, int64_t n,
+                             int64_t n_keep, int64_t n_clone, int4* __restrict__ route,
+                             int32_t* __restrict__ old_to_new) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const bool kns = keep_ns[i], cl = clone_k[i], sp = split_k[i];
-  int32_t final_index = -1;
-  if (kns) {
-    const int64_t d = pos_keep[i];
-    final_index = (int32_t)d;
-    for (int c = 0; c < comps; ++c) {
-      dst[c * dstride + d] = src[c * stride + i];
-      m_dst[c * dstride + d] = m_src[c * stride + i];
-      v_dst[c * dstride + d] = v_src[c * stride + i];
-    }
+  int4 r;
+  r.x = keep_ns[i] ? pos_keep[i] : -1;
+  r.y = clone_k[i] ? (int)(n_keep + pos_clone[i]) : -1;
+  r.z = split_k[i] ? (int)(n_keep + n_clone + 2 * (int64_t)pos_split[i]) : -1;
+  r.w = 0;
+  route[i] = r;
+  if (old_to_new) old_to_new[i] = r.x;
+}
+
+// Bulk of K15: one thread per (component, source Gaussian) — every row of the
+// planar params / m / v is read and written with coalesced accesses (the
+// route table stays in L2 across the components). Survivors keep m / v;
+// clones and split children get zero moments (AdamGroup::remap
+// adam.hpp:45-58) and a verbatim parameter copy that compact_geom_kernel
+// then adjusts.
+__global__ void compact_copy_kernel(const float* __restrict__ src, const float* __restrict__ m_src,
+                                    const float* __restrict__ v_src, int64_t stride, int64_t n,
+                                    const int4* __restrict__ route, float* __restrict__ dst,
+                                    float* __restrict__ m_dst, float* __restrict__ v_dst, int64_t dstride) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = blockIdx.y;
+  const int4 r = route[i];
+  if (r.x < 0 && r.y < 0 && r.z < 0) return;
+  const size_t so = (size_t)c * stride + i;
+  const size_t co = (size_t)c * dstride;
+  const float x = src[so];
+  if (r.x >= 0) {
+    dst[co + r.x] = x;
+    m_dst[co + r.x] = m_src[so];
+    v_dst[co + r.x] = v_src[so];
   }
-  if (cl) {
-    // clone: one positional-gradient step (adc.hpp:184-189), fresh moments
-    const int64_t d = n_keep + pos_clone[i];
-    for (int c = 0; c < comps; ++c) {
-      dst[c * dstride + d] = src[c * stride + i];
-      m_dst[c * dstride + d] = 0.0f;
-      v_dst[c * dstride + d] = 0.0f;
-    }
+  if (r.y >= 0) {
+    dst[co + r.y] = x;
+    m_dst[co + r.y] = 0.0f;
+    v_dst[co + r.y] = 0.0f;
+  }
+  if (r.z >= 0) {
+    dst[co + r.z] = x;
+    dst[co + r.z + 1] = x;
+    m_dst[co + r.z] = m_dst[co + r.z + 1] = 0.0f;
+    v_dst[co + r.z] = v_dst[co + r.z + 1] = 0.0f;
+  }
+}
+
+// Geometry of clones and split children (adc.hpp:184-201), after the copy:
+// clone mu -= lr * grad3d / views_seen; children mu = parent mu + R(eps * s),
+// log_scale - ln 1.6.
+__global__ void compact_geom_kernel(const float* __restrict__ src, int64_t stride, int64_t n,
+                                    const int4* __restrict__ route, const float* __restrict__ grad3d,
+                                    const int* __restrict__ views_seen, float clone_lr, const float* __restrict__ eps,
+                                    float log_shrink, float* __restrict__ dst, int64_t dstride,
+                                    const int32_t* __restrict__ pos_split) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int4 rt = route[i];
+  if (rt.y >= 0) {
     const int seen = views_seen[i];
     if (seen > 0) {
       const float vs = (float)seen;
       for (int k = 0; k < 3; ++k)
-        dst[(SK_COMP_MU + k) * dstride + d] = src[(SK_COMP_MU + k) * stride + i] - clone_lr * (grad3d[k * stride + i] / vs);
+        dst[(SK_COMP_MU + k) * dstride + rt.y] =
+            src[(SK_COMP_MU + k) * stride + i] - clone_lr * (grad3d[k * stride + i] / vs);
     }
   }
-  if (sp) {
-    // split: two children at parent.mu + R(eps * scale), log_scale - ln 1.6 (adc.hpp:190-201)
+  if (rt.z >= 0) {
     const int64_t r = pos_split[i];
-    const int64_t d0 = n_keep + n_clone + 2 * r;
-    const float qw_in = src[3 * stride + i], qx_in = src[4 * stride + i], qy_in = src[5 * stride + i],
-                qz_in = src[6 * stride + i];
-    float qw = qw_in, qx = qx_in, qy = qy_in, qz = qz_in;
+    float qw = src[3 * stride + i], qx = src[4 * stride + i], qy = src[5 * stride + i], qz = src[6 * stride + i];
     const float n2 = ((qw * qw + qx * qx) + qy * qy) + qz * qz;
     if (n2 > 0.0f) {
       const float nq = sqrtf(n2);
@@ -260,12 +294,7 @@ __global__ void compact_kernel(const float* __restrict__ src, const float* __res
     float s[3];
     for (int k = 0; k < 3; ++k) s[k] = det_expf(src[(SK_COMP_LOG_SCALE + k) * stride + i]);
     for (int child = 0; child < 2; ++child) {
-      const int64_t d = d0 + child;
-      for (int c = 0; c < comps; ++c) {
-        dst[c * dstride + d] = src[c * stride + i];
-        m_dst[c * dstride + d] = 0.0f;
-        v_dst[c * dstride + d] = 0.0f;
-      }
+      const int64_t d = rt.z + child;
       float es[3];
       for (int k = 0; k < 3; ++k) es[k] = eps[r * 6 + child * 3 + k] * s[k];
       for (int k = 0; k < 3; ++k) {
@@ -275,7 +304,6 @@ __global__ void compact_kernel(const float* __restrict__ src, const float* __res
       }
     }
   }
-  if (old_to_new) old_to_new[i] = final_index;
 }
 
 unsigned blocks(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
@@ -457,6 +485,7 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
     require(eps_host != nullptr, "apply_densify: split requires eps normals");
     h2d(ctx, eps, eps_host, 6 * (size_t)n_split);
   }
+  trace_point(ctx, "compact: eps upload");
   ensure_optimizer_state(ctx, s);
   const int64_t new_cap =
       new_n > s->capacity ? round_capacity(std::max<int64_t>(new_n, s->capacity + s->capacity / 2)) : s->capacity;
@@ -469,14 +498,23 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
   ensure<float>(np, cells);
   ensure<float>(nm, cells);
   ensure<float>(nv, cells);
-  compact_kernel<<<blocks(n), 256, 0, ctx->stream>>>(
-      s->params.as<float>(), s->adam_m.as<float>(), s->adam_v.as<float>(), s->capacity, n, s->comps, cls, cls + n,
-      cls + 2 * n, pos, pos + n, pos + 2 * n, n_keep, n_clone, s->grad3d_acc.as<float>(), s->views_seen.as<int>(),
-      clone_lr, eps, (float)std::log(1.6), np.as<float>(), nm.as<float>(), nv.as<float>(), new_cap, old_to_new_dev);
+  trace_point(ctx, "compact: buffers");
+  int4* route = reinterpret_cast<int4*>(ensure<int32_t>(ev.route, 4 * (size_t)n));
+  route_kernel<<<blocks(n), 256, 0, ctx->stream>>>(cls, cls + n, cls + 2 * n, pos, pos + n, pos + 2 * n, n, n_keep,
+                                                   n_clone, route, old_to_new_dev);
+  note_launch();
+  compact_copy_kernel<<<dim3(blocks(n), (unsigned)s->comps), 256, 0, ctx->stream>>>(
+      s->params.as<float>(), s->adam_m.as<float>(), s->adam_v.as<float>(), s->capacity, n, route, np.as<float>(),
+      nm.as<float>(), nv.as<float>(), new_cap);
+  note_launch();
+  compact_geom_kernel<<<blocks(n), 256, 0, ctx->stream>>>(s->params.as<float>(), s->capacity, n, route,
+                                                          s->grad3d_acc.as<float>(), s->views_seen.as<int>(),
+                                                          clone_lr, eps, (float)std::log(1.6), np.as<float>(),
+                                                          new_cap, pos + 2 * n);
   note_launch();
   SK_CUDA(cudaGetLastError());
   sync(ctx);
-  trace_point(ctx, "compact: eps upload + kernel");
+  trace_point(ctx, "compact: kernel");
   s->params.swap(np);
   s->adam_m.swap(nm);
   s->adam_v.swap(nv);

@@ -21,7 +21,7 @@
 #include "blend_common.cuh"
 
 #ifndef SK_FWD_WARP_STAGED
-#define SK_FWD_WARP_STAGED 0
+#define SK_FWD_WARP_STAGED 1  // measured: 2% faster than the CTA-staged kernel at 16x16
 #endif
 #ifndef SK_FWD_PIX16
 #define SK_FWD_PIX16 2

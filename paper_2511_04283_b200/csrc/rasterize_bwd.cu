@@ -71,7 +71,7 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 #endif
 
 #ifndef SK_BWD_WARP_STAGED
-#define SK_BWD_WARP_STAGED 0
+#define SK_BWD_WARP_STAGED 1  // measured: 6.6% faster than the CTA-staged walk
 #endif
 
 template <int TS, int PIX, bool WS = SK_BWD_WARP_STAGED != 0, bool FASTEXP = true>

@@ -18,6 +18,10 @@
 // runs so global stores are coalesced.
 #include "state.h"
 
+#ifndef SK_SORT_BALLOT_RANK
+#define SK_SORT_BALLOT_RANK 0
+#endif
+
 namespace sk {
 namespace {
 
@@ -132,8 +136,29 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
   // All match_any results first (independent, so their latencies overlap),
   // then the per-warp histogram updates in item order (stable ranking).
   uint32_t peers[kItems];
+#if SK_SORT_BALLOT_RANK
+  // Peers by ballots over the digit bits (plus validity) instead of MATCH.ANY.
+  const int nbits = __popc(dmask);
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const bool valid = wbase + j * 32 + lane < n;
+    const uint32_t d = (k[j] >> shift) & dmask;
+    uint32_t m = __ballot_sync(0xffffffffu, valid);
+    m = valid ? m : ~m;
+#pragma unroll
+    for (int b = 0; b < kRadixBits; ++b) {
+      if (b < nbits) {
+        const bool bit = (d >> b) & 1u;
+        const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+        m &= bit ? bb : ~bb;
+      }
+    }
+    peers[j] = m;
+  }
+#else
 #pragma unroll
   for (int j = 0; j < kItems; ++j) peers[j] = __match_any_sync(0xffffffffu, digit_of(j));
+#endif
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const uint32_t dj = digit_of(j);

@@ -68,6 +68,7 @@ struct EventScratch {
   DevBuf keys_a, keys_b, vals_a, vals_b;  // VCP ordering
   DevBuf eps;        // float [n_split][6]
   DevBuf old_to_new; // int32 [n]
+  DevBuf route;      // int4 [n] destination slots (keep, clone, split) of K15
   // phase timing of density events (sk_ctx_get_event_timing): marks at the
   // start of the score pass, after the K views, after K13, K14 and K15
   cudaEvent_t tev[SK_NUM_EVENT_PHASES + 1] = {};
