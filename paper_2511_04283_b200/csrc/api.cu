@@ -189,12 +189,25 @@ int sk_scene_upload(sk_ctx* ctx, sk_scene* s, const float* host, int64_t n) {
                                 cudaMemcpyHostToDevice, ctx->stream));
     s->n = n;
     for (auto& t : s->adam_t) t = 0;
-    s->grads.release();
-    s->adam_m.release();
-    s->adam_v.release();
-    for (DevBuf* b : {&s->s_d, &s->s_p_raw, &s->s_p, &s->grad_norm_acc, &s->abs_grad_acc, &s->grad3d_acc,
-                      &s->views_seen, &s->max_radius2d})
-      b->release();
+    const size_t cells = (size_t)s->comps * s->capacity;
+    if (s->adam_m.ptr && s->adam_m.bytes >= cells * sizeof(float)) {
+      // same capacity: zero the moments / statistics in place instead of
+      // freeing and re-allocating them (SceneOptimizer::init, ScoreTable::reset)
+      SK_CUDA(cudaMemsetAsync(s->adam_m.ptr, 0, cells * sizeof(float), ctx->stream));
+      SK_CUDA(cudaMemsetAsync(s->adam_v.ptr, 0, cells * sizeof(float), ctx->stream));
+    } else {
+      s->grads.release();
+      s->adam_m.release();
+      s->adam_v.release();
+    }
+    if (s->grad_norm_acc.ptr && s->grad_norm_acc.bytes >= (size_t)s->capacity * sizeof(float)) {
+      reset_score_table(ctx, s);
+    } else {
+      for (DevBuf* b : {&s->s_d, &s->s_p_raw, &s->s_p, &s->grad_norm_acc, &s->abs_grad_acc, &s->grad3d_acc,
+                        &s->views_seen, &s->max_radius2d})
+        b->release();
+    }
+    s->rest_n = -1;
     sync(ctx);
   });
 }

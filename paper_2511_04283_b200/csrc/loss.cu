@@ -50,7 +50,9 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ img, const void* __restrict__ gt,
                                                        bool gt_u8, int W, int H, float nrm, float lambda,
                                                        float inv_n, bool want_grad, float* __restrict__ partials,
-                                                       float* __restrict__ dimage, double* __restrict__ sums) {
+                                                       float* __restrict__ dimage, double* __restrict__ sums,
+                                                       double* __restrict__ block_sums,
+                                                       unsigned int* __restrict__ ticket) {
   __shared__ float s_x[kInY][kInX + 1];
   __shared__ float s_y[kInY][kInX + 1];
   __shared__ float s_h[5][kInY][kTX + 1];
@@ -162,10 +164,32 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   const double t_l1 = block_sum(l1, s_red);
   const double t_ss = block_sum(ss, s_red);
   const double t_sq = block_sum(sq, s_red);
+  // Deterministic total: block sums are stored per block and the last block
+  // to finish adds them in block order (no order-dependent atomics, so the
+  // loss / SSIM / PSNR are bit-reproducible run to run).
+  const unsigned nb = gridDim.x * gridDim.y;
+  const unsigned b = blockIdx.y * gridDim.x + blockIdx.x;
+  __shared__ bool s_last;
   if (t == 0) {
-    atomicAdd(&sums[0], t_l1);
-    atomicAdd(&sums[1], t_ss);
-    atomicAdd(&sums[2], t_sq);
+    block_sums[3 * b + 0] = t_l1;
+    block_sums[3 * b + 1] = t_ss;
+    block_sums[3 * b + 2] = t_sq;
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == nb - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (unsigned j = t; j < nb; j += blockDim.x)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) acc[k] += __ldcg(&block_sums[3 * j + k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double tot = block_sum(acc[k], s_red);
+      if (t == 0) sums[k] = tot;
+    }
+    if (t == 0) *ticket = 0u;
   }
 }
 
@@ -266,13 +290,15 @@ void launch_loss(sk_ctx* ctx, sk_frame* f, const void* gt, bool gt_u8, float lam
   const size_t plane = (size_t)W * H;
   float* partials = want_grad ? ensure<float>(f->loss_scratch, 9 * plane) : nullptr;
   float* dimage = want_grad ? ensure<float>(f->dimage, 3 * plane) : nullptr;
-  double* sums = ensure<double>(ctx->scalars, 4);
-  SK_CUDA(cudaMemsetAsync(sums, 0, 4 * sizeof(double), ctx->stream));
+  double* sums = ensure<double>(ctx->scalars, 5);
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(sums + 4);
+  SK_CUDA(cudaMemsetAsync(sums, 0, 5 * sizeof(double), ctx->stream));
   const dim3 grid((W + kTX - 1) / kTX, (H + kTY - 1) / kTY);
+  double* block_sums = ensure<double>(ctx->loss_blocks, 3 * (size_t)grid.x * grid.y);
   const float nrm = 1.0f / (3.0f * (float)W * (float)H);
   const float inv_n = 1.0f / (3.0f * (float)plane);
   ssim_fwd_kernel<<<grid, 256, 0, ctx->stream>>>(f->image.as<float>(), gt, gt_u8, W, H, nrm, lambda, inv_n, want_grad,
-                                                 partials, dimage, sums);
+                                                 partials, dimage, sums, block_sums, ticket);
   note_launch();
   if (want_grad) {
     ssim_bwd_kernel<<<grid, 256, 0, ctx->stream>>>(f->image.as<float>(), gt, gt_u8, W, H, lambda, partials, dimage);

@@ -87,6 +87,7 @@ struct sk_ctx {
   sk::DevBuf err_word;  // uint32 device error bits
   sk::DevBuf scalars;   // small device scratch (reductions)
   sk::DevBuf pge;       // uint64 [2] workload counters (sk_frame_pge_counts)
+  sk::DevBuf loss_blocks;  // double [blocks][3] per-block loss sums (deterministic reduction)
   sk::HostBuf pinned;   // staging
   // phase timing (sk_ctx_enable_timing)
   bool timing = false;
