@@ -406,18 +406,7 @@ def run_ours(args, world, rank, local):
     roofline_fp32["pge_visited"] = visited
     roofline_fp32["pge_contributing"] = contribs
     hbm_kernels = {}
-    fused = phase_avg[6] < 0.02 * phase_avg[5]  # single GPU: K9 + K10 run as one kernel (phase 6 empty)
-    if fused:
-        b = algorithmic_bytes(5, args.n, visible, pairs, pixels, tiles) + algorithmic_bytes(6, args.n, visible,
-                                                                                             pairs, pixels, tiles)
-        ib = 1416 * args.n + 100 * visible  # params + m + v in/out, blend grads, stats; no gradient round trip
-        t = (phase_avg[5] + phase_avg[6]) * 1e-3
-        hbm_kernels["K9+K10 proj-bwd + Adam (fused)"] = {
-            "ms": phase_avg[5] + phase_avg[6], "algorithmic_MB": b / 1e6, "GB/s": b / t / 1e9,
-            "frac": b / t / 1e9 / hbm_peak, "implementation_min_MB": ib / 1e6,
-            "implementation_frac": ib / t / 1e9 / hbm_peak,
-            "note": "algorithmic = SURVEY K9 + K10 figures; the fused kernel never writes / re-reads the gradients"}
-    for ph in ((0, 1, 3) if fused else (0, 1, 3, 5, 6)):
+    for ph in (0, 1, 3, 5, 6):
         b = algorithmic_bytes(ph, args.n, visible, pairs, pixels, tiles)
         gbs = b / (phase_avg[ph] * 1e-3) / 1e9
         hbm_kernels[PHASES[ph]] = {"ms": phase_avg[ph], "algorithmic_MB": b / 1e6, "GB/s": gbs,

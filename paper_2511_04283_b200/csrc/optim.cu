@@ -324,17 +324,11 @@ constexpr int kPbThreads = 128;
 // column of a shared-memory tile (conflict-free: column = threadIdx.x, so no
 // 59-register live range) and the tile is written back as coalesced rows of the
 // planar gradient buffer; culled Gaussians get zeros (SceneGrads::init).
-// FUSED: K9 + K10 in one pass (single-GPU steps without the lazy SH-rest
-// schedule): the 59 gradients stay in the shared tile and each thread applies
-// the dense Adam update of its own Gaussian, component by component
-// (coalesced rows of params / m / v, same adam_update as K10, so bit-identical
-// to the two-kernel path); the gradient buffer is not written. Saves the
-// gradient's write + read (472 B per Gaussian at SH degree 3).
-template <int DEG, bool FUSED = false>
+template <int DEG>
 __global__ void __launch_bounds__(kPbThreads, 4) project_bwd_kernel(
-    float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ radius,
+    const float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ radius,
     const float4* __restrict__ conic4, const float* __restrict__ bg, int64_t gstride, float* __restrict__ grads,
-    Stats st, bool do_stats, float* __restrict__ am, float* __restrict__ av, AdamParams ap) {
+    Stats st, bool do_stats) {
   constexpr int NC = 11 + 3 * (DEG + 1) * (DEG + 1);
   __shared__ float s_grad[NC * kPbThreads];
   __shared__ float s_exp2[64];
@@ -356,22 +350,8 @@ __global__ void __launch_bounds__(kPbThreads, 4) project_bwd_kernel(
 #pragma unroll
     for (int c = 0; c < NC; ++c) g[c * kPbThreads] = 0.0f;
   }
-  if (FUSED) {
-#pragma unroll 4
-    for (int c = 0; c < NC; ++c) {
-      const int gi = comp_group(c);
-      if (!ap.active[gi]) continue;
-      const int64_t o = c * stride + i;
-      float p = params[o], m = am[o], v = av[o];
-      adam_update(p, m, v, g[c * kPbThreads], ap.lr[gi], ap.bc1[gi], ap.bc2[gi]);
-      __stcs(params + o, p);
-      __stcs(am + o, m);
-      __stcs(av + o, v);
-    }
-  } else {
 #pragma unroll
-    for (int c = 0; c < NC; ++c) grads[c * stride + i] = g[c * kPbThreads];
-  }
+  for (int c = 0; c < NC; ++c) grads[c * stride + i] = g[c * kPbThreads];
 }
 
 // K10: dense Adam over every component of every Gaussian (SceneOptimizer::step
@@ -440,30 +420,19 @@ Stats make_stats(sk_scene* s) {
   return st;
 }
 
-void launch_pb(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stats, const AdamParams* fused = nullptr) {
+void launch_pb(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stats) {
   const CamParams cp = make_cam_params(f->camera);
   const unsigned grid = (unsigned)((s->n + kPbThreads - 1) / kPbThreads);
-  const AdamParams ap = fused ? *fused : AdamParams{};
   auto go = [&](auto kern) {
     kern<<<grid, kPbThreads, 0, ctx->stream>>>(s->params.as<float>(), s->capacity, s->n, cp, f->radius.as<float>(),
                                                f->conic4.as<float4>(), f->bgrads.as<float>(), f->n,
-                                               s->grads.as<float>(), make_stats(s), do_stats,
-                                               s->adam_m.as<float>(), s->adam_v.as<float>(), ap);
+                                               s->grads.as<float>(), make_stats(s), do_stats);
   };
-  if (fused) {
-    switch (s->sh_degree) {
-      case 0: go(project_bwd_kernel<0, true>); break;
-      case 1: go(project_bwd_kernel<1, true>); break;
-      case 2: go(project_bwd_kernel<2, true>); break;
-      default: go(project_bwd_kernel<3, true>); break;
-    }
-  } else {
-    switch (s->sh_degree) {
-      case 0: go(project_bwd_kernel<0>); break;
-      case 1: go(project_bwd_kernel<1>); break;
-      case 2: go(project_bwd_kernel<2>); break;
-      default: go(project_bwd_kernel<3>); break;
-    }
+  switch (s->sh_degree) {
+    case 0: go(project_bwd_kernel<0>); break;
+    case 1: go(project_bwd_kernel<1>); break;
+    case 2: go(project_bwd_kernel<2>); break;
+    default: go(project_bwd_kernel<3>); break;
   }
   note_launch();
   SK_CUDA(cudaGetLastError());
@@ -608,9 +577,8 @@ void reset_opacity(sk_ctx* ctx, sk_scene* s) {
 // bandwidth.)
 void launch_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const LearningRates& lrs, float position_lr,
                                   bool update_sh_rest, bool do_stats) {
-  ensure_optimizer_state(ctx, s);
-  const AdamParams ap = make_adam(s, lrs, position_lr, update_sh_rest);
-  launch_pb(ctx, s, f, do_stats, &ap);
+  launch_project_backward(ctx, s, f, do_stats);
+  launch_adam(ctx, s, lrs, position_lr, update_sh_rest);
 }
 
 }  // namespace sk

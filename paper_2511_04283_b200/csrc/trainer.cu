@@ -139,24 +139,18 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   ctx->mark(5);
   const LearningRates lrs = lrs_from(cfg);
   const float pos_lr = expon_lr(lrs.position * extent, lrs.position_final * extent, it, cfg.iterations);
-  if (!(comm && comm->world > 1) && !cfg.lazy_opt_enabled) {
-    // single GPU: K9 and K10 fused (the gradients never leave the SM)
-    launch_project_backward_adam(ctx, scene, f, lrs, pos_lr, true, true);
-    ctx->mark(6);
+  // K9 into the gradient buffer (+ C1 sum over ranks on a view-parallel
+  // step), then K10
+  launch_project_backward(ctx, scene, f, true);
+  if (comm && comm->world > 1) allreduce_grads(comm, scene, ctx->stream);
+  ctx->mark(6);
+  if (!cfg.lazy_opt_enabled) {
+    launch_adam(ctx, scene, lrs, pos_lr, true);
   } else {
-    // K9 into the gradient buffer (+ C1 sum over ranks on a view-parallel
-    // step), then K10
-    launch_project_backward(ctx, scene, f, true);
-    if (comm && comm->world > 1) allreduce_grads(comm, scene, ctx->stream);
-    ctx->mark(6);
-    if (!cfg.lazy_opt_enabled) {
-      launch_adam(ctx, scene, lrs, pos_lr, true);
-    } else {
-      // trainer.hpp:160-169: SH-rest excluded from the step, accumulated, and
-      // stepped on the accumulated gradient when lazy_update_due
-      launch_adam(ctx, scene, lrs, pos_lr, false);
-      lazy_sh_rest(ctx, scene, lrs, lazy_update_due(it, cfg));
-    }
+    // trainer.hpp:160-169: SH-rest excluded from the step, accumulated, and
+    // stepped on the accumulated gradient when lazy_update_due
+    launch_adam(ctx, scene, lrs, pos_lr, false);
+    lazy_sh_rest(ctx, scene, lrs, lazy_update_due(it, cfg));
   }
   ctx->mark(7);
   if (pend) {
