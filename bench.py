@@ -327,9 +327,12 @@ def run_ours(args, world, rank, local):
     pinned = torch.empty(gt8.size, dtype=torch.uint8, pin_memory=True)
     gt_host = pinned.numpy().reshape(gt8.shape)
     gt_host[...] = gt8
-    e2e_scene = scene  # keep training the same scene
+    # Same training trajectory as the device-timed run (the per-step workload
+    # drifts as the scene trains): restart from the initial scene and step 1.
+    e2e_scene = scene
+    ctx.check(ctx._lib.sk_scene_upload(ctx.h, scene.h, sk._p(params), sk.C.c_int64(args.n)))
     pipe = sk.HostStepPipeline(ctx, comm=comm)
-    it0 = rows[-1]["iteration"] if rows else 0
+    it0 = 0
     for k in range(args.warmup):  # the e2e frame allocates its buffers on first use
         pipe.step(e2e_scene, cam, gt_host, cfg, extent, it0 + 1 + k)
     pipe.flush()

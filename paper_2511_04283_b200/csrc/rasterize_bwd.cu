@@ -70,6 +70,9 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 #define SK_BWD_MINB 10
 #endif
 
+#ifndef SK_BWD_PIX16
+#define SK_BWD_PIX16 4
+#endif
 #ifndef SK_BWD_WARP_STAGED
 #define SK_BWD_WARP_STAGED 1  // measured: 6.6% faster than the CTA-staged walk
 #endif
@@ -295,7 +298,7 @@ void launch_blend_backward(sk_ctx* ctx, sk_frame* f) {
   if (f->tiles_x * f->tiles_y == 0) return;
   switch (f->tile_size) {
     case 8: bwd_dispatch<8, 1>(ctx, f); break;
-    case 16: bwd_dispatch<16, 4>(ctx, f); break;
+    case 16: bwd_dispatch<16, SK_BWD_PIX16>(ctx, f); break;
     case 32: bwd_dispatch<32, 4>(ctx, f); break;
     default: throw std::invalid_argument("tile_size must be 8, 16 or 32");
   }
