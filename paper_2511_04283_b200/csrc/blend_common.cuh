@@ -8,6 +8,13 @@
 namespace sk {
 namespace blend {
 
+// Contribution-mask words (K6 -> K8): batch b of tile t (entries
+// [range.x + 32 b, +32)) lives at word cmask_word(range.x, t) + b, times the
+// number of K6 warps per tile. floor(begin / 32) + t never collides between
+// tiles: tile t has at most floor(L / 32) + 1 batches.
+__host__ __device__ __forceinline__ int64_t cmask_word(int begin, int tile) { return (int64_t)(begin >> 5) + tile; }
+inline size_t cmask_words(int64_t pairs, int tiles) { return (size_t)(pairs >> 5) + (size_t)tiles + 2; }
+
 __device__ __forceinline__ float qcut_of(float opacity) {
   const float a = 255.0f * opacity;
   return a > 1.0f ? 2.0f * __logf(a) + 0.02f : -1.0f;

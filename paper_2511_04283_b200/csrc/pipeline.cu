@@ -24,6 +24,7 @@ void frame_geometry(sk_frame* f, int w, int h, const sk_binning* b) {
   f->tiles_y = (h + bin.tile_size - 1) / bin.tile_size;
   f->binned = false;
   f->rendered = false;
+  f->cmask_valid = false;
 }
 
 void ensure_projected(sk_frame* f, int64_t n) {
@@ -58,6 +59,7 @@ int tile_bits(int tiles) {
 // K2-K5 (build_tile_grid raster.hpp:157-168).
 void bin_sort(sk_ctx* ctx, sk_frame* f) {
   const int64_t n = f->n;
+  f->cmask_valid = false;
   const int tiles = f->tiles_x * f->tiles_y;
   ensure<int2>(f->ranges, (size_t)std::max(tiles, 1));
   f->pairs = 0;

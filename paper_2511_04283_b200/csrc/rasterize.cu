@@ -168,7 +168,8 @@ template <int TS, int PIX>
 __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fwd_warp_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
-    float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry) {
+    float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry,
+    uint32_t* __restrict__ cmask) {
   using WB = WarpBlock<TS, PIX>;
   constexpr int kWarps = WB::kWarps;
   __shared__ float4 s_xyq[kWarps][32];
@@ -222,6 +223,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
     }
     uint32_t m = __ballot_sync(0xffffffffu, hit);
     __syncwarp();
+    uint32_t lane_bits = 0;  // entries of this batch one of my pixels blended
     while (m && !all_done) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
@@ -236,6 +238,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
         float alpha = co.w * det_expf_neg(-0.5f * q, tab);
         alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
         if (alpha < kAlphaMin) continue;
+        lane_bits |= 1u << j;
         const float4 c = s_rgb[warp][j];
         const float w = T[k] * alpha;
         C0[k] = C0[k] + w * c.x;
@@ -251,6 +254,11 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
       for (int k = 0; k < PIX; ++k) ad = ad && done[k];
       all_done = ad;
     }
+    // contribution mask of this warp block for the batch (read by K8, which
+    // then skips entries no pixel of its block blended); unwalked batches
+    // keep the frame-start zeros
+    const uint32_t bits = __reduce_or_sync(0xffffffffu, lane_bits);
+    if (cmask && lane == 0) cmask[(size_t)(cmask_word(range.x, tile) + ((b0 - range.x) >> 5)) * kWarps + warp] = bits;
     __syncwarp();
   }
 #pragma unroll
@@ -304,14 +312,23 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
   const auto* mean2d = f->mean2d.as<float2>();
   const auto* co = f->conic_op.as<float4>();
   const auto* rgb = f->rgb_depth.as<float4>();
+  if (!mask && !SK_FWD_WARP_STAGED) f->cmask_valid = false;
   if (mask)
     blend_fwd_kernel<TS, PIX, true><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
         ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
         f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), mask, counts);
-  else if (SK_FWD_WARP_STAGED)
+  else if (SK_FWD_WARP_STAGED) {
+    uint32_t* cm = nullptr;
+    if (TS == 16 && PIX == 2) {  // K8 consumes the masks at 16x16 tiles
+      const size_t words = cmask_words(f->pairs, tiles) * (size_t)(TS * TS / PIX / 32);
+      cm = ensure<uint32_t>(f->cmask, words);
+      SK_CUDA(cudaMemsetAsync(cm, 0, words * sizeof(uint32_t), ctx->stream));
+    }
+    f->cmask_valid = cm != nullptr;
     blend_fwd_warp_kernel<TS, PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
         ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
-        f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>());
+        f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), cm);
+  }
   else
     blend_fwd_kernel<TS, PIX, false><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
         ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),

@@ -70,6 +70,9 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 #define SK_BWD_MINB 10
 #endif
 
+#ifndef SK_BWD_USE_CMASK
+#define SK_BWD_USE_CMASK 1
+#endif
 #ifndef SK_BWD_PIX16
 #define SK_BWD_PIX16 4
 #endif
@@ -82,7 +85,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB) blend_bwd_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     const float* __restrict__ final_t, const int* __restrict__ last_entry, const float* __restrict__ dimage,
-    float* __restrict__ bgrads, int64_t gstride) {
+    float* __restrict__ bgrads, int64_t gstride, const uint32_t* __restrict__ cmask) {
   constexpr int NT = TS * TS / PIX;  // threads == batch size
   using WB = WarpBlock<TS, PIX>;
   constexpr int kChunks = NT / 32;
@@ -208,7 +211,42 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB) blend_bwd_kernel(
     }
   };
 
-  if (WS) {
+  if (WS && TS == 16 && cmask) {
+    // Warp-staged over K6's batches with K6's contribution masks: only the
+    // entries a pixel of this block blended in the forward pass are gathered
+    // and walked (the others contribute nothing here), no ellipse tests.
+    // K8 warp w covers K6 warps (8x8 blocks) x8 = w % 2, y8 in [y8a, y8b).
+    const int base = warp * 32;
+    const int x8 = warp % 2, y8a = (warp / 2) * (4 * PIX) / 8, y8b = ((warp / 2) * (4 * PIX) + 4 * PIX + 7) / 8;
+    if (warp_last > range.x) {
+      const int64_t wbase = cmask_word(range.x, tile);
+      for (int kb = (warp_last - 1 - range.x) >> 5; kb >= 0; --kb) {
+        const int b0 = range.x + 32 * kb;
+        uint32_t m = 0;
+        for (int y8 = y8a; y8 < y8b; ++y8) m |= __ldg(&cmask[(size_t)(wbase + kb) * 4 + y8 * 2 + x8]);
+        const int lim = warp_last - b0;
+        if (lim < 32) m &= (1u << lim) - 1u;
+        if (!m) continue;
+        if ((m >> lane) & 1u) {
+          const uint32_t g = pair_val[b0 + lane];
+          float4 xyq, bb;
+          const float4 co = conic_op[g];
+          stage_entry(mean2d[g], co, xyq, bb);
+          s_xyq[base + lane] = xyq;
+          s_co[base + lane] = co;
+          s_rgb[base + lane] = rgbd[g];
+          s_id[base + lane] = g;
+        }
+        __syncwarp();
+        while (m) {
+          const int bit = 31 - __clz(m);
+          m ^= 1u << bit;
+          walk_entry(base + bit, b0 + bit);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (WS) {
     // Warp-staged: each warp gathers 32 entries at a time from its own last
     // contributor downward, keeps the hits on its block (ballot) in its
     // private slots and walks them; no CTA barrier inside the walk.
@@ -287,7 +325,8 @@ void bwd_dispatch(sk_ctx* ctx, sk_frame* f) {
   blend_bwd_kernel<TS, PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
       f->ranges.as<int2>(), f->pair_val, f->mean2d.as<float2>(), f->conic_op.as<float4>(), f->rgb_depth.as<float4>(),
       f->width, f->height, f->tiles_x, f->final_t.as<float>(), f->last_entry.as<int>(), f->dimage.as<float>(),
-      f->bgrads.as<float>(), f->n);
+      f->bgrads.as<float>(), f->n,
+      (SK_BWD_USE_CMASK && TS == 16 && f->cmask_valid) ? f->cmask.as<uint32_t>() : nullptr);
   note_launch();
 }
 

@@ -163,6 +163,8 @@ struct sk_frame {
   sk::DevBuf final_t;     // float [H][W]
   sk::DevBuf n_contrib;   // int32 [H][W]
   sk::DevBuf last_entry;  // int32 [H][W], absolute pair index + 1 of the last contributor
+  sk::DevBuf cmask;       // uint32 per (batch of 32 entries, K6 warp): entries a pixel of the warp blended
+  bool cmask_valid = false;
 
   // K7 / K8
   sk::DevBuf dimage;  // planar [3][H][W]

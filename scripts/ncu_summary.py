@@ -59,10 +59,13 @@ def full(path: str) -> str:
     ki = h.index("Kernel Name")
     out = ["| kernel | us | DRAM rd MB | DRAM wr MB | DRAM GB/s | SM % | mem % | issue % | warps % | regs | top stalls (cycles/issue) |",
            "|---|---|---|---|---|---|---|---|---|---|---|"]
+    units = rows[1]
+    tscale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+    bscale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
     for r in rows[2:]:
-        t = float(r[col["gpu__time_duration.sum"]]) * 1000.0  # ms -> us
-        rd = float(r[col["dram__bytes_read.sum"]])
-        wr = float(r[col["dram__bytes_write.sum"]])
+        t = float(r[col["gpu__time_duration.sum"]]) * tscale.get(units[col["gpu__time_duration.sum"]], 1e3)
+        rd = float(r[col["dram__bytes_read.sum"]]) * bscale.get(units[col["dram__bytes_read.sum"]], 1.0)
+        wr = float(r[col["dram__bytes_write.sum"]]) * bscale.get(units[col["dram__bytes_write.sum"]], 1.0)
         gbs = (rd + wr) * 1e6 / (t * 1e-6) / 1e9 if t > 0 else 0.0
         st = sorted(((float(r[col[f"smsp__average_warps_issue_stalled_{s}_per_issue_active.ratio"]] or 0), s)
                      for s in STALLS), reverse=True)[:3]
