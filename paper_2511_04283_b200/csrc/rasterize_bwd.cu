@@ -64,17 +64,19 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
   if (valid) atomicAdd(&bgrads[(int64_t)field * gstride + (lane < 16 ? id_a : id_b)], v);
 }
 
-// 10 resident CTAs (20 warps) per SM: caps the kernel at 96 registers
-// without spills (measured 7.6% faster than the unconstrained 106).
+// 16x16 tiles: 128 threads (8x8 pixel block per warp, 2 pixels per thread,
+// the same blocks as K6) and 6 resident CTAs (24 warps) per SM, which caps
+// the kernel at 80 registers without spills. Measured against 64 threads x 4
+// pixels (8x16 blocks): -12% K8 time.
 #ifndef SK_BWD_MINB
-#define SK_BWD_MINB 10
+#define SK_BWD_MINB 6
 #endif
 
 #ifndef SK_BWD_USE_CMASK
 #define SK_BWD_USE_CMASK 1
 #endif
 #ifndef SK_BWD_PIX16
-#define SK_BWD_PIX16 4
+#define SK_BWD_PIX16 2
 #endif
 #ifndef SK_BWD_WARP_STAGED
 #define SK_BWD_WARP_STAGED 1  // measured: 6.6% faster than the CTA-staged walk
