@@ -65,11 +65,11 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 }
 
 // 16x16 tiles: 128 threads (8x8 pixel block per warp, 2 pixels per thread,
-// the same blocks as K6) and 6 resident CTAs (24 warps) per SM, which caps
-// the kernel at 80 registers without spills. Measured against 64 threads x 4
-// pixels (8x16 blocks): -12% K8 time.
+// the same blocks as K6) and 7 resident CTAs (28 warps) per SM, which caps
+// the kernel at 72 registers without spills. Measured against 64 threads x 4
+// pixels (8x16 blocks): -12% K8 time; 7 CTAs/SM instead of 6: -4% more.
 #ifndef SK_BWD_MINB
-#define SK_BWD_MINB 6
+#define SK_BWD_MINB 7
 #endif
 
 #ifndef SK_BWD_USE_CMASK
