@@ -8,6 +8,24 @@
 namespace sk {
 namespace blend {
 
+// cp.async (LDGSTS) helpers: global -> shared copies that hold no registers
+// while in flight.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Contribution-mask words (K6 -> K8): batch b of tile t (entries
 // [range.x + 32 b, +32)) lives at word cmask_word(range.x, t) + b, times the
 // number of K6 warps per tile. floor(begin / 32) + t never collides between
