@@ -72,6 +72,9 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 #define SK_BWD_MINB 7
 #endif
 
+#ifndef SK_BWD_ASYNC_GATHER
+#define SK_BWD_ASYNC_GATHER 1
+#endif
 #ifndef SK_BWD_USE_CMASK
 #define SK_BWD_USE_CMASK 1
 #endif
@@ -83,7 +86,7 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 #endif
 
 template <int TS, int PIX, bool WS = SK_BWD_WARP_STAGED != 0, bool FASTEXP = true>
-__global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB) blend_bwd_kernel(
+__global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / PIX)) blend_bwd_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     const float* __restrict__ final_t, const int* __restrict__ last_entry, const float* __restrict__ dimage,
@@ -91,11 +94,15 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB) blend_bwd_kernel(
   constexpr int NT = TS * TS / PIX;  // threads == batch size
   using WB = WarpBlock<TS, PIX>;
   constexpr int kChunks = NT / 32;
-  __shared__ float4 s_xyq[NT];
-  __shared__ float4 s_co[NT];
+  // two buffers of NT slots for the asynchronous gather (slot buf * NT + j);
+  // the other paths use the first NT
+  constexpr int NB = SK_BWD_ASYNC_GATHER ? 2 * NT : NT;
+  __shared__ float4 s_xyq[NB];
+  __shared__ float4 s_co[NB];
   __shared__ uint32_t s_mask[WB::kWarps * kChunks];
-  __shared__ float4 s_rgb[NT];
-  __shared__ uint32_t s_id[NT];
+  __shared__ float4 s_rgb[NB];
+  __shared__ uint32_t s_id[NB];
+  __shared__ float2 s_mu[SK_BWD_ASYNC_GATHER ? NB : 1];
   __shared__ int s_max_last;
   __shared__ float s_exp2[64];
   stage_exp2_table(s_exp2);
@@ -222,12 +229,70 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB) blend_bwd_kernel(
     const int x8 = warp % 2, y8a = (warp / 2) * (4 * PIX) / 8, y8b = ((warp / 2) * (4 * PIX) + 4 * PIX + 7) / 8;
     if (warp_last > range.x) {
       const int64_t wbase = cmask_word(range.x, tile);
-      for (int kb = (warp_last - 1 - range.x) >> 5; kb >= 0; --kb) {
-        const int b0 = range.x + 32 * kb;
+      auto mask_of = [&](int kb) -> uint32_t {
+        if (kb < 0) return 0u;
         uint32_t m = 0;
         for (int y8 = y8a; y8 < y8b; ++y8) m |= __ldg(&cmask[(size_t)(wbase + kb) * 4 + y8 * 2 + x8]);
-        const int lim = warp_last - b0;
+        const int lim = warp_last - (range.x + 32 * kb);
         if (lim < 32) m &= (1u << lim) - 1u;
+        return m;
+      };
+#if SK_BWD_ASYNC_GATHER
+      // Batches in descending order; the records of batch kb-1 are copied
+      // with cp.async while kb is walked, and the mask + pair index of kb-2
+      // are loaded one batch ahead.
+      auto issue = [&](int buf, int kb, uint32_t m, uint32_t g) {
+        if ((m >> lane) & 1u) {
+          const int slot = buf * NT + base + lane;
+          cp_async16(&s_co[slot], &conic_op[g]);
+          cp_async8(&s_mu[slot], &mean2d[g]);
+          cp_async16(&s_rgb[slot], &rgbd[g]);
+          s_id[slot] = g;
+        }
+        cp_async_commit();
+      };
+      auto gidx = [&](int kb, uint32_t m) -> uint32_t {
+        return ((m >> lane) & 1u) ? pair_val[range.x + 32 * kb + lane] : 0u;
+      };
+      int kb = (warp_last - 1 - range.x) >> 5;
+      uint32_t m_cur = mask_of(kb);
+      issue(0, kb, m_cur, gidx(kb, m_cur));
+      uint32_t m_next = mask_of(kb - 1);
+      uint32_t g_next = gidx(kb - 1, m_next);
+      int buf = 0;
+      for (; kb >= 0; --kb) {
+        const uint32_t m_prev = m_next;  // mask of batch kb - 1
+        if (kb >= 1) {
+          issue(buf ^ 1, kb - 1, m_next, g_next);
+          m_next = mask_of(kb - 2);
+          g_next = gidx(kb - 2, m_next);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncwarp();
+        const int b0 = range.x + 32 * kb;
+        uint32_t m = m_cur;
+        if ((m >> lane) & 1u) {
+          const int slot = buf * NT + base + lane;
+          float4 xyq, bb;
+          stage_entry(s_mu[slot], s_co[slot], xyq, bb);
+          s_xyq[slot] = xyq;
+        }
+        __syncwarp();
+        while (m) {
+          const int bit = 31 - __clz(m);
+          m ^= 1u << bit;
+          walk_entry(buf * NT + base + bit, b0 + bit);
+        }
+        __syncwarp();
+        m_cur = m_prev;
+        buf ^= 1;
+      }
+#else
+      for (int kb = (warp_last - 1 - range.x) >> 5; kb >= 0; --kb) {
+        const int b0 = range.x + 32 * kb;
+        uint32_t m = mask_of(kb);
         if (!m) continue;
         if ((m >> lane) & 1u) {
           const uint32_t g = pair_val[b0 + lane];
@@ -247,6 +312,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB) blend_bwd_kernel(
         }
         __syncwarp();
       }
+#endif
     }
   } else if (WS) {
     // Warp-staged: each warp gathers 32 entries at a time from its own last
