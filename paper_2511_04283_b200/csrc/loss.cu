@@ -18,13 +18,16 @@
 namespace sk {
 namespace {
 
+#ifndef SK_SSIM_TY
+#define SK_SSIM_TY 16
+#endif
 constexpr int kTX = 32;                 // output tile width
-constexpr int kTY = 16;                 // output tile height
+constexpr int kTY = SK_SSIM_TY;         // output tile height (16 or 32)
 constexpr int kHalo = 5;                // 11-tap window
 constexpr int kInX = kTX + 2 * kHalo;   // 42
 constexpr int kInY = kTY + 2 * kHalo;   // 26
 constexpr int kHX = 4;                  // horizontal outputs per thread (register sliding window)
-constexpr int kVY = 2;                  // vertical outputs per thread
+constexpr int kVY = kTX * kTY / 256;    // vertical outputs per thread (256 threads)
 
 __constant__ float c_gauss[11];
 
@@ -82,8 +85,8 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
     }
     __syncthreads();
     // horizontal: 26 rows x 8 groups of 4 columns
-    if (t < kInY * (kTX / kHX)) {
-      const int iy = t / (kTX / kHX), ox = (t % (kTX / kHX)) * kHX;
+    for (int hw = t; hw < kInY * (kTX / kHX); hw += blockDim.x) {
+      const int iy = hw / (kTX / kHX), ox = (hw % (kTX / kHX)) * kHX;
       float xv[kHX + 10], yv[kHX + 10];
 #pragma unroll
       for (int k = 0; k < kHX + 10; ++k) {
@@ -218,8 +221,8 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
       for (int k = 0; k < 3; ++k) s_u[k][iy][ix] = ok ? partials[(k * 3 + ch) * plane + p] : 0.0f;
     }
     __syncthreads();
-    if (t < kInY * (kTX / kHX)) {
-      const int iy = t / (kTX / kHX), ox = (t % (kTX / kHX)) * kHX;
+    for (int hw = t; hw < kInY * (kTX / kHX); hw += blockDim.x) {
+      const int iy = hw / (kTX / kHX), ox = (hw % (kTX / kHX)) * kHX;
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
         float v[kHX + 10];
