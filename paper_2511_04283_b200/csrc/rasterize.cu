@@ -23,6 +23,9 @@
 #ifndef SK_FWD_WARP_STAGED
 #define SK_FWD_WARP_STAGED 1  // measured: 2% faster than the CTA-staged kernel at 16x16
 #endif
+#ifndef SK_FWD_MINB
+#define SK_FWD_MINB 8  // resident 128-thread CTAs per SM (64 registers)
+#endif
 #ifndef SK_FWD_ASYNC_GATHER
 #define SK_FWD_ASYNC_GATHER 1
 #endif
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
 // the price is that each warp gathers every entry (L1 serves the repeats).
 // Per-pixel arithmetic is identical to blend_fwd_kernel (bit-exact).
 template <int TS, int PIX>
-__global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fwd_warp_kernel(
+__global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / PIX)) blend_fwd_warp_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry,
