@@ -19,4 +19,4 @@ timeout 1200 ncu --set full --import-source on --clock-control none \
 timeout 1200 ncu --set full --import-source on --clock-control none \
   -k regex:"preprocess|duplicate|onesweep|ssim|project_bwd|adam|scan_gather|tile_ranges" -s $((14 * WARM + 10)) -c 14 \
   -o gpurun_out/fullb_$TAG -f python bench.py --profile --steps 1 --warmup $WARM > gpurun_out/ncu_fullb_$TAG.log 2>&1
-tail -2 gpurun_out/ncu_full_$TAG.log gpurun_out/ncu_fullb_$TAG.log
+tail -n 2 gpurun_out/ncu_full_$TAG.log gpurun_out/ncu_fullb_$TAG.log
