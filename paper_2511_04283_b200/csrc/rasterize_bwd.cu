@@ -75,6 +75,12 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 // cp.async double-buffered gather on the mask path: measured 3% slower than
 // the direct gather (it needs the extra buffer registers / smem and K8's
 // gathers are already sparse), so off by default.
+#ifndef SK_BWD_SINGLE_LANE
+#define SK_BWD_SINGLE_LANE 1
+#endif
+#ifndef SK_BWD_DIRECT_MAX
+#define SK_BWD_DIRECT_MAX 1
+#endif
 #ifndef SK_BWD_ASYNC_GATHER
 #define SK_BWD_ASYNC_GATHER 0
 #endif
@@ -209,7 +215,20 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
         g_a1 += fabsf(m1);
       }
     }
-    if (__any_sync(0xffffffffu, contrib)) {
+    const uint32_t cb = __ballot_sync(0xffffffffu, contrib);
+#if SK_BWD_SINGLE_LANE
+    if (__popc(cb) <= SK_BWD_DIRECT_MAX) {
+      // few contributing lanes: each adds its own partials (one lane: they
+      // are the warp sum), no shuffle reduction
+      if (contrib) {
+        const float gv[kBGradFields] = {g_mu0, g_mu1, g_c00, g_c01, g_c11, g_r, g_g, g_b, g_op, g_a0, g_a1};
+        const uint32_t id = s_id[j];
+#pragma unroll
+        for (int f = 0; f < kBGradFields; ++f) atomicAdd(&bgrads[(int64_t)f * gstride + id], gv[f]);
+      }
+    } else
+#endif
+    if (cb) {
       const float gv[kBGradFields] = {g_mu0, g_mu1, g_c00, g_c01, g_c11, g_r, g_g, g_b, g_op, g_a0, g_a1};
       if (has_pend) {
         reduce_scatter_2x11(pend, gv, pend_id, s_id[j], true, bgrads, gstride);
