@@ -18,6 +18,12 @@
 // runs so global stores are coalesced.
 #include "state.h"
 
+#ifndef SK_SORT_SMALL_ITEMS
+#define SK_SORT_SMALL_ITEMS 7
+#endif
+#ifndef SK_SORT_SMALL_N
+#define SK_SORT_SMALL_N 4000000
+#endif
 #ifndef SK_SORT_BALLOT_RANK
 #define SK_SORT_BALLOT_RANK 0
 #endif
@@ -97,15 +103,17 @@ __global__ void radix_bases_kernel(uint32_t* __restrict__ hist) {
   h[t] = base + x - v;
 }
 
-// One onesweep digit pass.
+// One onesweep digit pass over tiles of kSortThreads * ITEMS keys.
+template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int64_t n, int shift, uint32_t dmask, const uint32_t* __restrict__ digit_base,
     uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
+  constexpr int kTileT = kSortThreads * ITEMS;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_hist[kSortWarps][kRadix];
-  __shared__ uint32_t s_keys[kTile];
-  __shared__ uint32_t s_vals[kTile];
+  __shared__ uint32_t s_keys[kTileT];
+  __shared__ uint32_t s_vals[kTileT];
   __shared__ uint32_t s_local[kRadix];
   __shared__ uint32_t s_global[kRadix];
   __shared__ uint32_t s_wsum[kSortWarps];
@@ -116,17 +124,17 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
   for (int i = tid; i < kSortWarps * kRadix; i += kSortThreads) (&s_hist[0][0])[i] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
-  const int64_t base = (int64_t)tile * kTile;
+  const int64_t base = (int64_t)tile * kTileT;
 
   // Out-of-range slots carry the key 0xffffffff and digit kRadix (never
   // counted or written); the digit is recomputed from the key when needed.
-  uint32_t k[kItems], v[kItems], rank[kItems];
-  const int64_t wbase = base + (int64_t)warp * (32 * kItems);
+  uint32_t k[ITEMS], v[ITEMS], rank[ITEMS];
+  const int64_t wbase = base + (int64_t)warp * (32 * ITEMS);
   auto digit_of = [&](int j) -> uint32_t {
     return wbase + j * 32 + lane < n ? ((k[j] >> shift) & dmask) : (uint32_t)kRadix;
   };
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
+  for (int j = 0; j < ITEMS; ++j) {
     const int64_t idx = wbase + j * 32 + lane;
     const bool valid = idx < n;
     k[j] = valid ? keys_in[idx] : 0u;
@@ -135,12 +143,12 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
   const uint32_t lt = lanemask_lt();
   // All match_any results first (independent, so their latencies overlap),
   // then the per-warp histogram updates in item order (stable ranking).
-  uint32_t peers[kItems];
+  uint32_t peers[ITEMS];
 #if SK_SORT_BALLOT_RANK
   // Peers by ballots over the digit bits (plus validity) instead of MATCH.ANY.
   const int nbits = __popc(dmask);
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
+  for (int j = 0; j < ITEMS; ++j) {
     const bool valid = wbase + j * 32 + lane < n;
     const uint32_t d = (k[j] >> shift) & dmask;
     uint32_t m = __ballot_sync(0xffffffffu, valid);
@@ -157,10 +165,10 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
   }
 #else
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) peers[j] = __match_any_sync(0xffffffffu, digit_of(j));
+  for (int j = 0; j < ITEMS; ++j) peers[j] = __match_any_sync(0xffffffffu, digit_of(j));
 #endif
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
+  for (int j = 0; j < ITEMS; ++j) {
     const uint32_t dj = digit_of(j);
     const int leader = __ffs(peers[j]) - 1;
     uint32_t old = 0;
@@ -235,7 +243,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
 
   // Scatter into shared memory in digit-sorted order.
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
+  for (int j = 0; j < ITEMS; ++j) {
     const uint32_t dj = digit_of(j);
     if (dj < (uint32_t)kRadix) {
       const uint32_t pos = s_local[dj] + s_hist[warp][dj] + rank[j];
@@ -245,7 +253,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
   }
   __syncthreads();
   const int64_t rem = n - base;
-  const int count = rem < kTile ? (int)rem : kTile;
+  const int count = rem < kTileT ? (int)rem : kTileT;
   for (int i = tid; i < count; i += kSortThreads) {
     const uint32_t key = s_keys[i];
     const uint32_t dg = (key >> shift) & dmask;
@@ -403,7 +411,11 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
   const int width = radix_digit_width(bits);
   const uint32_t dmask = (1u << width) - 1u;
   require(passes <= kMaxPasses, "radix_sort_pairs: at most 32 key bits");
-  const int64_t tiles = (n + kTile - 1) / kTile;
+  // Small sorts (the depth order over N slots) use 7 keys per thread so the
+  // pass spans more CTAs than SMs; large ones (tile ids over P pairs) 15.
+  const bool small = n <= (int64_t)SK_SORT_SMALL_N;
+  const int tile_keys = kSortThreads * (small ? SK_SORT_SMALL_ITEMS : kItems);
+  const int64_t tiles = (n + tile_keys - 1) / tile_keys;
   require(tiles < (1ll << 31), "radix_sort_pairs: too many keys");
   uint32_t* hist = radix_hist_buffer(ctx);
   uint32_t* status = ensure<uint32_t>(ctx->sort.status, (size_t)tiles * kRadix);
@@ -420,8 +432,12 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
   note_launch();
   for (int p = 0; p < passes; ++p) {
     SK_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t) * (size_t)tiles * kRadix, s));
-    onesweep_kernel<<<(unsigned)tiles, kSortThreads, 0, s>>>(keys, vals, keys_alt, vals_alt, n, p * width, dmask,
-                                                              hist + p * kRadix, status, counters + p);
+    if (small)
+      onesweep_kernel<SK_SORT_SMALL_ITEMS><<<(unsigned)tiles, kSortThreads, 0, s>>>(
+          keys, vals, keys_alt, vals_alt, n, p * width, dmask, hist + p * kRadix, status, counters + p);
+    else
+      onesweep_kernel<kItems><<<(unsigned)tiles, kSortThreads, 0, s>>>(
+          keys, vals, keys_alt, vals_alt, n, p * width, dmask, hist + p * kRadix, status, counters + p);
     note_launch();
     std::swap(keys, keys_alt);
     std::swap(vals, vals_alt);
