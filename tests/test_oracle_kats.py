@@ -478,3 +478,34 @@ def test_pge_visited_counter(orc):
             lo += int(e - b) if r1.transmittance[y, x] >= 1e-4 else int(r1.contrib[y, x])
     assert lo <= v1 <= hi and v1 > int(r1.contrib.sum())
     assert np.array_equal(r1.image, r3.image)
+
+
+def test_project_backward_fd(orc):
+    """tests/test_camera.cpp:136-219: project_backward is the exact adjoint of
+    project (mu2d, conic, colour, opacity) for every parameter, fp64, 1e-4."""
+    from tests.util import random_scene
+    rng = np.random.default_rng(136)
+    for deg in (0, 1, 3):
+        p = random_scene(rng, 3, deg).astype(np.float64)
+        cam = orc.default_camera(64, 48)
+        w_mu = rng.uniform(-1, 1, (3, 2))
+        w_co = rng.uniform(-1, 1, (3, 4))
+        w_co[:, 2] = w_co[:, 1]  # symmetric upstream (full-matrix convention)
+        w_col = rng.uniform(-1, 1, (3, 3))
+        w_op = rng.uniform(-1, 1, 3)
+
+        def loss(q):
+            pr = orc.project_scene(q, deg, cam, dtype=np.float64)
+            assert pr.visible.all()
+            return float((pr.mu2d * w_mu).sum() + (pr.conic * w_co).sum() + (pr.color * w_col).sum()
+                         + (pr.opacity * w_op).sum())
+
+        g = orc.project_backward(p, deg, cam, w_mu, w_co, w_col, w_op, dtype=np.float64)
+        eps = 1e-6
+        for c in range(p.shape[0]):
+            for i in range(p.shape[1]):
+                a, b = p.copy(), p.copy()
+                a[c, i] += eps
+                b[c, i] -= eps
+                fd = (loss(a) - loss(b)) / (2 * eps)
+                assert abs(fd - g[c, i]) <= 1e-4 * max(abs(fd), abs(g[c, i]), 1e-3), (deg, c, i, fd, g[c, i])
