@@ -307,14 +307,12 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
         ++n[k];
         last[k] = b0 + j + 1;
         T[k] = T[k] * (1.0f - alpha);
-        if (T[k] < kTransmitMin) {
-          done[k] = true;
-          bool ad = true;
-#pragma unroll
-          for (int kk = 0; kk < PIX; ++kk) ad = ad && done[kk];
-          all_done = ad;
-        }
+        if (T[k] < kTransmitMin) done[k] = true;
       }
+      bool ad = true;
+#pragma unroll
+      for (int k = 0; k < PIX; ++k) ad = ad && done[k];
+      all_done = ad;
     }
     // contribution mask of this warp block for the batch (read by K8, which
     // then skips entries no pixel of its block blended); unwalked batches
