@@ -122,6 +122,10 @@ struct BinParams {
   int ts, tiles_x, tiles_y, W, H;
 };
 
+#ifndef SK_K1_PREFETCH
+#define SK_K1_PREFETCH 0
+#endif
+
 template <int DEG>
 __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict__ p, int64_t stride, int64_t n,
                                                          CamParams cam, BinParams bp, float2* __restrict__ mean2d,
@@ -142,6 +146,16 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
     key_out[i] = 0xffffffffu;
   };
   const float mu0 = p[0 * stride + i], mu1 = p[1 * stride + i], mu2 = p[2 * stride + i];
+#if SK_K1_PREFETCH >= 1
+  // rotation / scale / opacity loads issued with mu's, before the near test,
+  // so their latency overlaps the projection arithmetic
+  const float pf_q0 = p[3 * stride + i], pf_q1 = p[4 * stride + i], pf_q2 = p[5 * stride + i],
+              pf_q3 = p[6 * stride + i], pf_s0 = p[7 * stride + i], pf_s1 = p[8 * stride + i],
+              pf_s2 = p[9 * stride + i], pf_op = p[SK_COMP_OPACITY * stride + i];
+#define SK_P(c, v) (v)
+#else
+#define SK_P(c, v) (p[(c) * stride + i])
+#endif
   const float* R = cam.r;
   // t = R mu + t  (Mat * Vec: ((R_k0 mu0 + R_k1 mu1) + R_k2 mu2), then + t_k)
   const float t0 = ((R[0] * mu0 + R[1] * mu1) + R[2] * mu2) + cam.t[0];
@@ -163,10 +177,19 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
     m[1][j] = (J10 * R[0 * 3 + j] + J11 * R[1 * 3 + j]) + J12 * R[2 * 3 + j];
   }
   // covariance_3d (scene.hpp:88-96)
-  const float qw_in = p[3 * stride + i], qx_in = p[4 * stride + i], qy_in = p[5 * stride + i],
-              qz_in = p[6 * stride + i];
-  const float s0 = det_expf(p[7 * stride + i], tab), s1 = det_expf(p[8 * stride + i], tab),
-              s2 = det_expf(p[9 * stride + i], tab);
+  const float qw_in = SK_P(3, pf_q0), qx_in = SK_P(4, pf_q1), qy_in = SK_P(5, pf_q2), qz_in = SK_P(6, pf_q3);
+  constexpr int NSH = (DEG + 1) * (DEG + 1);
+#if SK_K1_PREFETCH >= 2
+  // SH coefficients issued before the covariance / guard-cull arithmetic
+  float shv[3 * NSH];
+#pragma unroll
+  for (int k = 0; k < 3 * NSH; ++k) shv[k] = p[(SK_COMP_SH + k) * stride + i];
+#define SK_SH(k) shv[k]
+#else
+#define SK_SH(k) p[(SK_COMP_SH + (k)) * stride + i]
+#endif
+  const float s0 = det_expf(SK_P(7, pf_s0), tab), s1 = det_expf(SK_P(8, pf_s1), tab),
+              s2 = det_expf(SK_P(9, pf_s2), tab);
   if (!(isfinite(qw_in) && isfinite(qx_in) && isfinite(qy_in) && isfinite(qz_in) && isfinite(s0) && isfinite(s1) &&
         isfinite(s2))) {
     atomicOr(err, kErrCovNonFinite);
@@ -239,7 +262,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
   const float rel0 = mu0 - cam.center[0], rel1 = mu1 - cam.center[1], rel2 = mu2 - cam.center[2];
   const float dn = sqrtf((rel0 * rel0 + rel1 * rel1) + rel2 * rel2);
   const float x = rel0 / dn, y = rel1 / dn, z = rel2 / dn;
-  constexpr int NSH = (DEG + 1) * (DEG + 1);
   float basis[NSH];
   basis[0] = (float)0.28209479177387814;
   if (DEG >= 1) {
@@ -269,13 +291,15 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
 #pragma unroll
   for (int k = 0; k < NSH; ++k)
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) rgb[ch] = rgb[ch] + basis[k] * p[(SK_COMP_SH + 3 * k + ch) * stride + i];
+    for (int ch = 0; ch < 3; ++ch) rgb[ch] = rgb[ch] + basis[k] * SK_SH(3 * k + ch);
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
     rgb[ch] = rgb[ch] + 0.5f;
     rgb[ch] = (rgb[ch] < 0.0f) ? 0.0f : rgb[ch];
   }
-  const float opacity = det_sigmoidf(p[SK_COMP_OPACITY * stride + i], tab);
+  const float opacity = det_sigmoidf(SK_P(SK_COMP_OPACITY, pf_op), tab);
+#undef SK_P
+#undef SK_SH
 
   BinOut bo;
   if (!bin_footprint(mx, my, c[0][0], c[0][1], c[1][0], c[1][1], inv00, inv01, inv11, opacity, bp.mode, bp.beta,
