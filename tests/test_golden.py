@@ -2,7 +2,7 @@
 tests/golden/make_golden.py from the KAT-pinned oracle): the oracle must keep
 reproducing them (CPU), and the GPU path must match them bit for bit on the
 bit-exact outputs — tile lists, image, transmittance, contribution counts,
-visited / contributing counts — and within 1e-4 on the loss (GPU)."""
+visited / contributing counts — and within the fp32 serial-sum rounding on the loss scalars (GPU)."""
 import glob
 import json
 import os
@@ -72,11 +72,14 @@ def test_gpu_matches_golden(orc, path):
         assert digest(out.transmittance) == g["sha256"]["transmittance"]
         assert digest(out.contrib) == g["sha256"]["contrib"]
         assert ctx.pge_counts() == (g["pge_visited"], g["pge_contributing"])
-        # the reference sums the L1 term serially in fp32 (loss.hpp:29-32); the
-        # GPU reduces in fp64, so the scalars agree to the fp32 sum's rounding
+        # the reference sums the L1 term serially in fp32 over 3HW values
+        # (loss.hpp:29-32, ~1e-4 relative rounding at these sizes); the GPU
+        # reduces in fp64, so the scalars agree to that rounding
         v = ctx.training_loss(_target(out.image), 0.2)
-        assert v.loss == pytest.approx(g["loss"]["loss"], rel=1e-4)
+        assert v.loss == pytest.approx(g["loss"]["loss"], rel=1e-3)
         assert v.ssim == pytest.approx(g["loss"]["ssim"], rel=1e-4)
-        assert v.l1 == pytest.approx(g["loss"]["l1"], rel=1e-4)
+        assert v.l1 == pytest.approx(g["loss"]["l1"], rel=1e-3)
+        exact_l1 = float(np.abs(np.float64(out.image) - np.float64(_target(out.image))).mean())
+        assert v.l1 == pytest.approx(exact_l1, rel=1e-6)
     finally:
         ctx.close()
