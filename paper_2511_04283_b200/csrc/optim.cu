@@ -317,6 +317,9 @@ __device__ __forceinline__ void accumulate_stats(const Stats& st, int64_t i, int
   st.max_radius2d[i] = fmaxf(st.max_radius2d[i], radius);
 }
 
+#ifndef SK_K9_PREFETCH
+#define SK_K9_PREFETCH 1
+#endif
 // MODE 0: gradients -> grads buffer (+ stats). MODE 1: fused Adam (+ stats).
 constexpr int kPbThreads = 128;
 
@@ -337,6 +340,16 @@ __global__ void __launch_bounds__(kPbThreads, 4) project_bwd_kernel(
   const int64_t i = (int64_t)blockIdx.x * kPbThreads + threadIdx.x;
   if (i >= n) return;
   float* g = s_grad + threadIdx.x;  // component c at g[c * kPbThreads]
+#if SK_K9_PREFETCH
+  // L1 prefetches (no registers held) of everything the visible path reads
+  // first, issued before the radius test so the latency overlaps it
+#pragma unroll
+  for (int c = 0; c < 11; ++c) asm volatile("prefetch.global.L1 [%0];" ::"l"(bg + c * gstride + i));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(conic4 + i));
+#pragma unroll
+  for (int c = 0; c < (SK_K9_PREFETCH >= 2 ? NC : 11); ++c)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(params + c * stride + i));
+#endif
   const float rad = radius[i];
   if (rad > 0.0f) {
     float dmu2d[2], dcov[2][2], dcol[3], dop, absg[2];
