@@ -179,7 +179,12 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
   // covariance_3d (scene.hpp:88-96)
   const float qw_in = SK_P(3, pf_q0), qx_in = SK_P(4, pf_q1), qy_in = SK_P(5, pf_q2), qz_in = SK_P(6, pf_q3);
   constexpr int NSH = (DEG + 1) * (DEG + 1);
-#if SK_K1_PREFETCH >= 2
+#if SK_K1_PREFETCH == 3
+  // SH rows prefetched into L1 (no registers) while the covariance is formed
+#pragma unroll
+  for (int k = 0; k < 3 * NSH; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + (SK_COMP_SH + k) * stride + i));
+#endif
+#if SK_K1_PREFETCH == 2
   // SH coefficients issued before the covariance / guard-cull arithmetic
   float shv[3 * NSH];
 #pragma unroll

@@ -81,6 +81,9 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 #ifndef SK_BWD_DIRECT_MAX
 #define SK_BWD_DIRECT_MAX 1
 #endif
+#ifndef SK_BWD_L1PF
+#define SK_BWD_L1PF 0
+#endif
 #ifndef SK_BWD_ASYNC_GATHER
 #define SK_BWD_ASYNC_GATHER 0
 #endif
@@ -316,6 +319,10 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
         const int b0 = range.x + 32 * kb;
         uint32_t m = mask_of(kb);
         if (!m) continue;
+#if SK_BWD_L1PF
+        // L1 prefetch of the next batch's pair indices (no registers held)
+        if (kb > 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(pair_val + b0 - 32 + lane));
+#endif
         if ((m >> lane) & 1u) {
           const uint32_t g = pair_val[b0 + lane];
           float4 xyq, bb;
