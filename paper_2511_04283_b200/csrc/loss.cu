@@ -23,9 +23,13 @@ namespace {
 #ifndef SK_SSIM_TY
 #define SK_SSIM_TY 32
 #endif
+#ifndef SK_SSIM_UNROLL
+#define SK_SSIM_UNROLL 1
+#endif
 #ifndef SK_SSIM_HX
 #define SK_SSIM_HX 4
 #endif
+constexpr int kStageUnroll = SK_SSIM_UNROLL;  // halo-staging loop unroll (loads in flight)
 constexpr int kTX = 32;                 // output tile width
 constexpr int kTY = SK_SSIM_TY;         // output tile height (16 or 32)
 constexpr int kHalo = 5;                // 11-tap window
@@ -76,6 +80,7 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   double l1 = 0.0, ss = 0.0, sq = 0.0;
   for (int ch = 0; ch < 3; ++ch) {
     __syncthreads();
+#pragma unroll kStageUnroll
     for (int i = t; i < kInX * kInY; i += blockDim.x) {
       const int iy = i / kInX, ix = i % kInX;
       const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
@@ -217,6 +222,7 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
   const int vx = t % kTX, vy0 = (t / kTX) * kVY;
   for (int ch = 0; ch < 3; ++ch) {
     __syncthreads();
+#pragma unroll kStageUnroll
     for (int i = t; i < kInX * kInY; i += blockDim.x) {
       const int iy = i / kInX, ix = i % kInX;
       const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
