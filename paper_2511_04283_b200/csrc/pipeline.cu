@@ -38,7 +38,8 @@ void ensure_projected(sk_frame* f, int64_t n) {
   ensure<int>(f->tiles, m);
   ensure<int4>(f->rect, m);
   ensure<float>(f->a_star, m);
-  ensure<uint32_t>(f->depth_key, m);
+  ensure<uint32_t>(f->keys_a, m);  // K1 writes the depth keys and the index payload
+  ensure<uint32_t>(f->vals_a, m);  // straight into the sort's first buffers
   f->n = n;
 }
 
@@ -72,8 +73,6 @@ void bin_sort(sk_ctx* ctx, sk_frame* f) {
   uint32_t* kb = ensure<uint32_t>(f->keys_b, n);
   uint32_t* va = ensure<uint32_t>(f->vals_a, n);
   uint32_t* vb = ensure<uint32_t>(f->vals_b, n);
-  SK_CUDA(cudaMemcpyAsync(ka, f->depth_key.ptr, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
-  launch_iota(ctx, va, n);
   radix_sort_pairs(ctx, ka, kb, va, vb, n, 32);  // depth_order: (depth, index)
   int32_t* offsets = ensure<int32_t>(f->offsets, n);
   const int64_t pairs = scan_gathered(ctx, f->tiles.as<int32_t>(), va, offsets, n);

@@ -133,13 +133,15 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
                                                          float4* __restrict__ cov_out, float4* __restrict__ conic4,
                                                          float* __restrict__ radius_out, int* __restrict__ tiles_out,
                                                          int4* __restrict__ rect_out, float* __restrict__ astar_out,
-                                                         uint32_t* __restrict__ key_out, uint32_t* __restrict__ err) {
+                                                         uint32_t* __restrict__ key_out, uint32_t* __restrict__ val_out,
+                                                         uint32_t* __restrict__ err) {
   __shared__ float s_exp2[64];
   stage_exp2_table(s_exp2);
   const SmemTable tab(s_exp2);
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  val_out[i] = (uint32_t)i;  // the depth sort's payload (projected index)
   auto culled = [&]() {
     radius_out[i] = 0.0f;
     tiles_out[i] = 0;
@@ -329,9 +331,10 @@ __global__ void inject_bin_kernel(int64_t n, BinParams bp, const float2* __restr
                                   const float4* __restrict__ cov, float* __restrict__ radius_out,
                                   int* __restrict__ tiles_out, int4* __restrict__ rect_out,
                                   float* __restrict__ astar_out, uint32_t* __restrict__ key_out,
-                                  uint32_t* __restrict__ err) {
+                                  uint32_t* __restrict__ val_out, uint32_t* __restrict__ err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  val_out[i] = (uint32_t)i;
   const float2 mu = mean2d[i];
   const float4 co = conic_op[i];
   const float4 cv = cov[i];
@@ -412,6 +415,7 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(int64_t n, BinPa
     }
     const int4 rc = cnt ? rect[g] : make_int4(0, 0, 0, 0);
     const int w = rc.z - rc.x + 1;
+    const float inv_w = 1.0f / (float)w;  // row split of the pair index: estimate + exact fix-up
     // the warp's pairs occupy [first, last) contiguously
     const int first = __reduce_min_sync(0xffffffffu, valid ? off : 0x7fffffff);
     const int last = __reduce_max_sync(0xffffffffu, valid ? off + cnt : 0);
@@ -430,11 +434,14 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(int64_t n, BinPa
       const int ox = __shfl_sync(0xffffffffu, rc.x, L);
       const int oy = __shfl_sync(0xffffffffu, rc.y, L);
       const int ow = __shfl_sync(0xffffffffu, w, L);
+      const float oinv = __shfl_sync(0xffffffffu, inv_w, L);
       const uint32_t og = __shfl_sync(0xffffffffu, g, L);
       const bool active = e0 + lane < total;
       uint32_t t = 0;
       if (active) {
-        const int r = k / ow;
+        int r = (int)((float)k * oinv);  // within one of k / ow (k < 2^24)
+        r += (r + 1) * ow <= k;
+        r -= r * ow > k;
         t = (uint32_t)((oy + r) * bp.tiles_x + ox + (k - r * ow));
         pair_tile[pos] = t;
         pair_val[pos] = og;
@@ -475,8 +482,8 @@ void launch_preprocess(sk_ctx* ctx, const sk_scene* scene, const sk_camera& cam,
     kern<<<grid, block, 0, ctx->stream>>>(
         scene->params.as<float>(), scene->capacity, n, cp, bp, f->mean2d.as<float2>(), f->conic_op.as<float4>(),
         f->rgb_depth.as<float4>(), f->cov2d.as<float4>(), f->conic4.as<float4>(), f->radius.as<float>(),
-        f->tiles.as<int>(), f->rect.as<int4>(), f->a_star.as<float>(), f->depth_key.as<uint32_t>(),
-        ctx->err_word.as<uint32_t>());
+        f->tiles.as<int>(), f->rect.as<int4>(), f->a_star.as<float>(), f->keys_a.as<uint32_t>(),
+        f->vals_a.as<uint32_t>(), ctx->err_word.as<uint32_t>());
   };
   switch (scene->sh_degree) {
     case 0: args(preprocess_kernel<0>); break;
@@ -495,7 +502,7 @@ void launch_inject_bin(sk_ctx* ctx, sk_frame* f) {
   inject_bin_kernel<<<grid, 256, 0, ctx->stream>>>(
       f->n, bp, f->mean2d.as<float2>(), f->conic_op.as<float4>(), f->rgb_depth.as<float4>(), f->cov2d.as<float4>(),
       f->radius.as<float>(), f->tiles.as<int>(), f->rect.as<int4>(), f->a_star.as<float>(),
-      f->depth_key.as<uint32_t>(), ctx->err_word.as<uint32_t>());
+      f->keys_a.as<uint32_t>(), f->vals_a.as<uint32_t>(), ctx->err_word.as<uint32_t>());
   note_launch();
   SK_CUDA(cudaGetLastError());
 }

@@ -72,9 +72,17 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restr
   for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t k = keys[i];
-    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (p * width)) & ((1u << width) - 1u)], 1u);
+    const uint32_t act = __activemask();
+    for (int p = 0; p < passes; ++p) {
+      // warp-aggregated: depth keys share their high digits, so plain shared
+      // atomics would serialise up to 32 lanes on one counter
+      const uint32_t d = (k >> (p * width)) & ((1u << width) - 1u);
+      const uint32_t peers = __match_any_sync(act, d);
+      if ((peers & lt) == 0) atomicAdd(&sh[p][d], (uint32_t)__popc(peers));
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {

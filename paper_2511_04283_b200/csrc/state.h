@@ -148,10 +148,9 @@ struct sk_frame {
   sk::DevBuf tiles;      // int32 [n] tiles touched
   sk::DevBuf rect;       // int4 [n] clipped tile rectangle
   sk::DevBuf a_star;     // float [n] compact-box threshold
-  sk::DevBuf depth_key;  // uint32 [n]
 
   // K2-K5
-  sk::DevBuf keys_a, keys_b, vals_a, vals_b;  // depth sort ping-pong
+  sk::DevBuf keys_a, keys_b, vals_a, vals_b;  // depth sort ping-pong (K1 fills keys_a / vals_a)
   sk::DevBuf offsets;                         // int32 [n]
   sk::DevBuf ptile_a, ptile_b, pval_a, pval_b; // pair sort ping-pong
   uint32_t* pair_tile = nullptr;              // sorted result pointers
