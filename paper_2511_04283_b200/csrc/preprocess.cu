@@ -122,6 +122,9 @@ struct BinParams {
   int ts, tiles_x, tiles_y, W, H;
 };
 
+#ifndef SK_DUP_RCP
+#define SK_DUP_RCP 1
+#endif
 #ifndef SK_K1_PREFETCH
 #define SK_K1_PREFETCH 1  // measured: -12% K1 time (2: SH prefetch too, no better)
 #endif
@@ -439,9 +442,13 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(int64_t n, BinPa
       const bool active = e0 + lane < total;
       uint32_t t = 0;
       if (active) {
+#if SK_DUP_RCP
         int r = (int)((float)k * oinv);  // within one of k / ow (k < 2^24)
         r += (r + 1) * ow <= k;
         r -= r * ow > k;
+#else
+        const int r = k / ow;
+#endif
         t = (uint32_t)((oy + r) * bp.tiles_x + ox + (k - r * ow));
         pair_tile[pos] = t;
         pair_val[pos] = og;

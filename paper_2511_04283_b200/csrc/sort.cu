@@ -18,6 +18,9 @@
 // runs so global stores are coalesced.
 #include "state.h"
 
+#ifndef SK_HIST_AGG
+#define SK_HIST_AGG 0
+#endif
 #ifndef SK_SORT_SMALL_ITEMS
 #define SK_SORT_SMALL_ITEMS 7
 #endif
@@ -75,6 +78,7 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restr
   const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t k = keys[i];
+#if SK_HIST_AGG
     const uint32_t act = __activemask();
     for (int p = 0; p < passes; ++p) {
       // warp-aggregated: depth keys share their high digits, so plain shared
@@ -83,6 +87,9 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restr
       const uint32_t peers = __match_any_sync(act, d);
       if ((peers & lt) == 0) atomicAdd(&sh[p][d], (uint32_t)__popc(peers));
     }
+#else
+    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (p * width)) & ((1u << width) - 1u)], 1u);
+#endif
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
