@@ -369,10 +369,6 @@ __global__ void __launch_bounds__(kScanThreads) scan_gather_kernel(const int32_t
   if (total_out && base <= n - 1 && base + kScanItems >= n) *total_out = run;
 }
 
-__global__ void iota_kernel(uint32_t* out, int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = (uint32_t)i;
-}
 
 // Tile ranges from the sorted tile ids: a run starts where the id differs
 // from its predecessor. Four ids per thread (uint4 loads), the predecessor of
@@ -478,11 +474,6 @@ int64_t scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order,
   return host_total;
 }
 
-void launch_iota(sk_ctx* ctx, uint32_t* out, int64_t n) {
-  if (n == 0) return;
-  iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(out, n);
-  note_launch();
-}
 
 void launch_tile_ranges(sk_ctx* ctx, const uint32_t* pair_tile, int64_t pairs, int2* ranges, int tiles) {
   SK_CUDA(cudaMemsetAsync(ranges, 0, sizeof(int2) * tiles, ctx->stream));

@@ -203,7 +203,6 @@ int radix_passes(int bits);
 int radix_digit_width(int bits);  // bits per digit pass (even split)
 // Exclusive scan of tiles[order[i]] into offsets[i]; returns the total.
 int64_t scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets, int64_t n);
-void launch_iota(sk_ctx* ctx, uint32_t* out, int64_t n);
 void launch_tile_ranges(sk_ctx* ctx, const uint32_t* pair_tile, int64_t pairs, int2* ranges, int tiles);
 
 // rasterize.cu

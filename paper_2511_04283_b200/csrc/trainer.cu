@@ -3,10 +3,11 @@
 // trainer.hpp:21-279, adam.hpp:16-164, config.hpp:20-81, rng.hpp:18-69).
 //
 // One iteration = K1 preprocess -> K2-K5 binning -> K6 forward blend ->
-// K7 loss -> K8 backward blend -> fused K9+K10 (project backward + stats +
-// dense Adam). All kernels are stream-ordered on the context stream; the step
-// synchronises twice (the pair count after the scan, and the loss/error
-// readback at the end).
+// K7 loss -> K8 backward blend -> K9 project backward + stats (-> C1 gradient
+// all-reduce on a view-parallel step) -> K10 dense Adam. All kernels are
+// stream-ordered on the context stream; the host waits once per step (the
+// pair count after the scan) and reads the loss / error word back one step
+// later (PendingStep).
 #include <chrono>
 #include <cmath>
 #include <memory>
