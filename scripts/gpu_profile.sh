@@ -10,8 +10,8 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gp
 timeout 900 python -m pytest $SEL -m gpu -x -q > gpurun_out/pytest_$TAG.log 2>&1; tail -3 gpurun_out/pytest_$TAG.log
 timeout 600 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -c 600 gpurun_out/bench_$TAG.err
 timeout 600 python bench.py --workload event --no-cpu-baseline --steps 3 > gpurun_out/event_$TAG.json 2> gpurun_out/event_$TAG.err; tail -c 600 gpurun_out/event_$TAG.err
-# launch list around the first timed iteration after WARM warm-ups (20 launches per step)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -s $((20 * WARM)) -c 60 \
+# launch list around the first timed iteration after WARM warm-ups (19 launches per step)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -s $((19 * WARM)) -c 60 \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --profile --steps 2 --warmup $WARM > /dev/null 2>&1
 timeout 1200 ncu --set full --import-source on --clock-control none \
   -k regex:"blend_fwd|blend_bwd" -s $((2 * WARM + 1)) -c 2 \
