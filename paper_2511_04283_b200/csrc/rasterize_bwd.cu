@@ -75,6 +75,9 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 // cp.async double-buffered gather on the mask path: measured 3% slower than
 // the direct gather (it needs the extra buffer registers / smem and K8's
 // gathers are already sparse), so off by default.
+#ifndef SK_BWD_BRANCHLESS
+#define SK_BWD_BRANCHLESS 0
+#endif
 #ifndef SK_BWD_SINGLE_LANE
 #define SK_BWD_SINGLE_LANE 0  // measured: no gain (1.112 vs 1.101 ms)
 #endif
@@ -168,6 +171,57 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
     float g_mu0 = 0.f, g_mu1 = 0.f, g_c00 = 0.f, g_c01 = 0.f, g_c11 = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f,
           g_op = 0.f, g_a0 = 0.f, g_a1 = 0.f;
     bool contrib = false;
+#if SK_BWD_BRANCHLESS
+    // Predicated form: every lane evaluates both of its pixels and masks the
+    // non-contributing ones to exact zeros (alpha -> 0 leaves T and the
+    // suffix unchanged), so the warp does not diverge / reconverge per
+    // pixel; only the rare near-threshold exact-exp recompute branches.
+#pragma unroll
+    for (int k = 0; k < PIX; ++k) {
+      const float dx = fpx - mq.x;
+      const float dy = fpy[k] - mq.y;
+      const float q = rn_add(rn_add(rn_mul(rn_mul(co.x, dx), dx), rn_mul(rn_mul(rn_mul(2.0f, co.y), dx), dy)),
+                             rn_mul(rn_mul(co.z, dy), dy));
+      bool ok = idx < last[k] && q >= 0.0f && q <= mq.z;
+      float ge = __expf(-0.5f * q);
+      float raw = co.w * ge;
+      if (ok && (fabsf(raw - kAlphaMin) <= 1e-5f * kAlphaMin || fabsf(raw - kAlphaCap) <= 1e-5f * kAlphaCap)) {
+        ge = det_expf_core(rn_mul(-0.5f, q), tab);
+        raw = rn_mul(co.w, ge);
+      }
+      const bool capped = raw > kAlphaCap;
+      const float alpha_c = capped ? kAlphaCap : raw;
+      ok = ok && !(alpha_c < kAlphaMin);
+      contrib = contrib || ok;
+      const float alpha = ok ? alpha_c : 0.0f;
+      const float4 c = s_rgb[j];
+      const float one_m = 1.0f - alpha;
+      const float inv_one_m = __fdividef(1.0f, one_m);
+      const float t_before = T[k] * inv_one_m;
+      T[k] = t_before;
+      const float w = (c.x * d0[k] + c.y * d1[k]) + c.z * d2[k];
+      const float d_alpha = t_before * w - suffix[k] * inv_one_m;
+      const float ta = t_before * alpha;
+      suffix[k] = suffix[k] + ta * w;
+      g_r += ta * d0[k];
+      g_g += ta * d1[k];
+      g_b += ta * d2[k];
+      const bool geo = ok && !capped;
+      g_op += geo ? ge * d_alpha : 0.0f;
+      const float d_q = geo ? -0.5f * alpha * d_alpha : 0.0f;
+      g_c00 += d_q * (dx * dx);
+      g_c01 += d_q * (dx * dy);
+      g_c11 += d_q * (dy * dy);
+      const float v0 = co.x * dx + co.y * dy;
+      const float v1 = co.y * dx + co.z * dy;
+      const float m0 = (-2.0f * d_q) * v0;
+      const float m1 = (-2.0f * d_q) * v1;
+      g_mu0 += m0;
+      g_mu1 += m1;
+      g_a0 += fabsf(m0);
+      g_a1 += fabsf(m1);
+    }
+#else
 #pragma unroll
     for (int k = 0; k < PIX; ++k) {
       if (idx >= last[k]) continue;
@@ -218,6 +272,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
         g_a1 += fabsf(m1);
       }
     }
+#endif
     const uint32_t cb = __ballot_sync(0xffffffffu, contrib);
 #if SK_BWD_SINGLE_LANE
     if (__popc(cb) <= SK_BWD_DIRECT_MAX) {
