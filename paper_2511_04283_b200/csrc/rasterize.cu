@@ -23,6 +23,9 @@
 #ifndef SK_FWD_WARP_STAGED
 #define SK_FWD_WARP_STAGED 1  // measured: 2% faster than the CTA-staged kernel at 16x16
 #endif
+#ifndef SK_FWD_BRANCHLESS
+#define SK_FWD_BRANCHLESS 0
+#endif
 #ifndef SK_FWD_MINB
 #define SK_FWD_MINB 8  // resident 128-thread CTAs per SM (64 registers)
 #endif
@@ -289,6 +292,32 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
       m &= m - 1;
       const float4 mq = s_xyq[warp][j];
       const float4 co = s_co_w[j];
+#if SK_FWD_BRANCHLESS
+      // Predicated form: both pixels evaluated by every lane, the
+      // non-contributing ones masked to alpha = 0 (T * (1 - 0) and C + (T * 0) c
+      // are exact no-ops), so lanes do not diverge per pixel.
+#pragma unroll
+      for (int k = 0; k < PIX; ++k) {
+        const float dx = fpx - mq.x;
+        const float dy = fpy[k] - mq.y;
+        const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
+        bool ok = !done[k] && q >= 0.0f && q <= mq.z;
+        float alpha = co.w * det_expf_neg(ok ? -0.5f * q : 0.0f, tab);  // in-domain for every lane
+        alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
+        ok = ok && !(alpha < kAlphaMin);
+        lane_bits |= ok ? 1u << j : 0u;
+        const float a = ok ? alpha : 0.0f;
+        const float4 c = s_rgb_w[j];
+        const float w = T[k] * a;
+        C0[k] = C0[k] + w * c.x;
+        C1[k] = C1[k] + w * c.y;
+        C2[k] = C2[k] + w * c.z;
+        n[k] += ok ? 1 : 0;
+        last[k] = ok ? b0 + j + 1 : last[k];
+        T[k] = T[k] * (1.0f - a);
+        if (T[k] < kTransmitMin) done[k] = true;
+      }
+#else
 #pragma unroll
       for (int k = 0; k < PIX; ++k) {
         const float dx = fpx - mq.x;
@@ -309,6 +338,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
         T[k] = T[k] * (1.0f - alpha);
         if (T[k] < kTransmitMin) done[k] = true;
       }
+#endif
       bool ad = true;
 #pragma unroll
       for (int k = 0; k < PIX; ++k) ad = ad && done[k];
