@@ -56,27 +56,6 @@ __device__ __forceinline__ void stage_entry(float2 mu, float4 co, float4& xyq, f
   bb = make_float4(mu.x - ex, mu.x + ex, mu.y - ey, mu.y + ey);
 }
 
-// The same staging quantities computed once per Gaussian (K1 / injection):
-// xyq = (mu.x, mu.y, q_cut, 0) and the half-extents of the {q <= q_cut} box;
-// an empty entry gets extents -1e30 (its box misses every block), a
-// non-positive-definite conic +3e38 (no culling). K6 then stages with one
-// gather and four adds instead of the log / two divisions / two roots.
-__device__ __forceinline__ void stage_precompute(float2 mu, float4 co, float4& xyq, float2& ext) {
-  const float qc = qcut_of(co.w);
-  xyq = make_float4(mu.x, mu.y, qc, 0.0f);
-  const float det = co.x * co.z - co.y * co.y;
-  if (qc <= 0.0f) {
-    ext = make_float2(-1.0e30f, -1.0e30f);
-  } else if (!(det > 0.0f && co.x > 0.0f && co.z > 0.0f)) {
-    ext = make_float2(3.0e38f, 3.0e38f);
-  } else {
-    ext = make_float2(sqrtf(qc * co.z / det) * 1.0001f + 0.01f, sqrtf(qc * co.x / det) * 1.0001f + 0.01f);
-  }
-}
-__device__ __forceinline__ float4 box_of(const float4& xyq, const float2& ext) {
-  return make_float4(xyq.x - ext.x, xyq.x + ext.x, xyq.y - ext.y, xyq.y + ext.y);
-}
-
 // Warp w of a TS x TS tile owns the 8 x 4·PIX pixel block starting at
 // ((w % (TS/8)) * 8, (w / (TS/8)) * 4·PIX); lane l holds column l & 7 and rows
 // (l >> 3) + 4k, k < PIX.
@@ -107,8 +86,7 @@ struct WarpBlock {
     const float y0 = (float)(ty * TS + (w / kWarpsX) * (4 * PIX)), y1 = y0 + (float)(4 * PIX - 1);
     if (mq.x >= x0 && mq.x <= x1 && mq.y >= y0 && mq.y <= y1) return true;
     const float a = co.x, b = co.y, c = co.z;
-    // MUFU reciprocals: the test carries 1e-3 slack, far above their error
-    const float ia = __fdividef(1.0f, a), ic = __fdividef(1.0f, c);
+    const float ia = 1.0f / a, ic = 1.0f / c;
     float best = 3.0e38f;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {

@@ -38,8 +38,6 @@ void ensure_projected(sk_frame* f, int64_t n) {
   ensure<int>(f->tiles, m);
   ensure<int4>(f->rect, m);
   ensure<float>(f->a_star, m);
-  ensure<float4>(f->xyq, m);
-  ensure<float2>(f->ext, m);
   ensure<uint32_t>(f->keys_a, m);  // K1 writes the depth keys and the index payload
   ensure<uint32_t>(f->vals_a, m);  // straight into the sort's first buffers
   f->n = n;

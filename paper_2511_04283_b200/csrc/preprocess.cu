@@ -11,7 +11,7 @@
 // Layout: one thread per Gaussian; all parameter reads are planar
 // ([component][capacity]) and therefore fully coalesced; outputs are float2 /
 // float4 SoA records.
-#include "blend_common.cuh"
+#include "state.h"
 
 namespace sk {
 namespace {
@@ -137,7 +137,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
                                                          float* __restrict__ radius_out, int* __restrict__ tiles_out,
                                                          int4* __restrict__ rect_out, float* __restrict__ astar_out,
                                                          uint32_t* __restrict__ key_out, uint32_t* __restrict__ val_out,
-                                                         float4* __restrict__ xyq_out, float2* __restrict__ ext_out,
                                                          uint32_t* __restrict__ err) {
   __shared__ float s_exp2[64];
   stage_exp2_table(s_exp2);
@@ -320,13 +319,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
   mean2d[i] = make_float2(mx, my);
   conic_op[i] = make_float4(inv00, inv01, inv11, opacity);
   rgbd[i] = make_float4(rgb[0], rgb[1], rgb[2], t2);
-  {
-    float4 xyq;
-    float2 ext;
-    blend::stage_precompute(make_float2(mx, my), make_float4(inv00, inv01, inv11, opacity), xyq, ext);
-    xyq_out[i] = xyq;
-    ext_out[i] = ext;
-  }
   cov_out[i] = make_float4(c[0][0], c[0][1], c[1][0], c[1][1]);
   conic4[i] = make_float4(inv00, inv01, inv10, inv11);
   radius_out[i] = radius;
@@ -342,18 +334,10 @@ __global__ void inject_bin_kernel(int64_t n, BinParams bp, const float2* __restr
                                   const float4* __restrict__ cov, float* __restrict__ radius_out,
                                   int* __restrict__ tiles_out, int4* __restrict__ rect_out,
                                   float* __restrict__ astar_out, uint32_t* __restrict__ key_out,
-                                  uint32_t* __restrict__ val_out, float4* __restrict__ xyq_out,
-                                  float2* __restrict__ ext_out, uint32_t* __restrict__ err) {
+                                  uint32_t* __restrict__ val_out, uint32_t* __restrict__ err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   val_out[i] = (uint32_t)i;
-  {
-    float4 xyq;
-    float2 ext;
-    blend::stage_precompute(mean2d[i], conic_op[i], xyq, ext);
-    xyq_out[i] = xyq;
-    ext_out[i] = ext;
-  }
   const float2 mu = mean2d[i];
   const float4 co = conic_op[i];
   const float4 cv = cov[i];
@@ -506,7 +490,7 @@ void launch_preprocess(sk_ctx* ctx, const sk_scene* scene, const sk_camera& cam,
         scene->params.as<float>(), scene->capacity, n, cp, bp, f->mean2d.as<float2>(), f->conic_op.as<float4>(),
         f->rgb_depth.as<float4>(), f->cov2d.as<float4>(), f->conic4.as<float4>(), f->radius.as<float>(),
         f->tiles.as<int>(), f->rect.as<int4>(), f->a_star.as<float>(), f->keys_a.as<uint32_t>(),
-        f->vals_a.as<uint32_t>(), f->xyq.as<float4>(), f->ext.as<float2>(), ctx->err_word.as<uint32_t>());
+        f->vals_a.as<uint32_t>(), ctx->err_word.as<uint32_t>());
   };
   switch (scene->sh_degree) {
     case 0: args(preprocess_kernel<0>); break;
@@ -525,8 +509,7 @@ void launch_inject_bin(sk_ctx* ctx, sk_frame* f) {
   inject_bin_kernel<<<grid, 256, 0, ctx->stream>>>(
       f->n, bp, f->mean2d.as<float2>(), f->conic_op.as<float4>(), f->rgb_depth.as<float4>(), f->cov2d.as<float4>(),
       f->radius.as<float>(), f->tiles.as<int>(), f->rect.as<int4>(), f->a_star.as<float>(),
-      f->keys_a.as<uint32_t>(), f->vals_a.as<uint32_t>(), f->xyq.as<float4>(), f->ext.as<float2>(),
-      ctx->err_word.as<uint32_t>());
+      f->keys_a.as<uint32_t>(), f->vals_a.as<uint32_t>(), ctx->err_word.as<uint32_t>());
   note_launch();
   SK_CUDA(cudaGetLastError());
 }

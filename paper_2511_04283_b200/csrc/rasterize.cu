@@ -23,9 +23,6 @@
 #ifndef SK_FWD_WARP_STAGED
 #define SK_FWD_WARP_STAGED 1  // measured: 2% faster than the CTA-staged kernel at 16x16
 #endif
-#ifndef SK_FWD_PRESTAGE
-#define SK_FWD_PRESTAGE 1
-#endif
 #ifndef SK_FWD_BRANCHLESS
 #define SK_FWD_BRANCHLESS 0
 #endif
@@ -181,18 +178,13 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry,
-    uint32_t* __restrict__ cmask, const float4* __restrict__ pre_xyq, const float2* __restrict__ pre_ext) {
+    uint32_t* __restrict__ cmask) {
   using WB = WarpBlock<TS, PIX>;
   constexpr int kWarps = WB::kWarps;
   __shared__ float4 s_xyq[kWarps][32];
 #if SK_FWD_ASYNC_GATHER
   __shared__ float4 s_gco[2][kWarps][32];
-#if SK_FWD_PRESTAGE
-  __shared__ float4 s_gxyq[2][kWarps][32];
-  __shared__ float2 s_gext[2][kWarps][32];
-#else
   __shared__ float2 s_gmu[2][kWarps][32];
-#endif
   __shared__ float4 s_grgb[2][kWarps][32];
 #else
   __shared__ float4 s_co[kWarps][32];
@@ -236,12 +228,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
   auto issue = [&](int buf, int bb, uint32_t g) {
     if (bb + lane < range.y) {
       cp_async16(&s_gco[buf][warp][lane], &conic_op[g]);
-#if SK_FWD_PRESTAGE
-      cp_async16(&s_gxyq[buf][warp][lane], &pre_xyq[g]);
-      cp_async8(&s_gext[buf][warp][lane], &pre_ext[g]);
-#else
       cp_async8(&s_gmu[buf][warp][lane], &mean2d[g]);
-#endif
       cp_async16(&s_grgb[buf][warp][lane], &rgbd[g]);
     }
     cp_async_commit();
@@ -265,13 +252,8 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
     bool hit = false;
     if (i < range.y) {
       const float4 co = s_gco[cur][warp][lane];
-#if SK_FWD_PRESTAGE
-      const float4 xyq = s_gxyq[cur][warp][lane];
-      const float4 bb = box_of(xyq, s_gext[cur][warp][lane]);
-#else
       float4 xyq, bb;
       stage_entry(s_gmu[cur][warp][lane], co, xyq, bb);
-#endif
       hit = !WB::misses(bb, warp, tx, ty);
       const bool pd = co.x > 0.0f && co.z > 0.0f && co.x * co.z - co.y * co.y > 0.0f;
       if (hit && pd) hit = WB::ellipse_hits(xyq, co, warp, tx, ty);
@@ -435,8 +417,7 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
     f->cmask_valid = cm != nullptr;
     blend_fwd_warp_kernel<TS, PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
         ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
-        f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), cm, f->xyq.as<float4>(),
-        f->ext.as<float2>());
+        f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), cm);
   }
   else
     blend_fwd_kernel<TS, PIX, false><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(

@@ -148,8 +148,6 @@ struct sk_frame {
   sk::DevBuf tiles;      // int32 [n] tiles touched
   sk::DevBuf rect;       // int4 [n] clipped tile rectangle
   sk::DevBuf a_star;     // float [n] compact-box threshold
-  sk::DevBuf xyq;        // float4 [n] (mu.x, mu.y, q_cut, 0) for K6 staging
-  sk::DevBuf ext;        // float2 [n] half-extents of the {q <= q_cut} box
 
   // K2-K5
   sk::DevBuf keys_a, keys_b, vals_a, vals_b;  // depth sort ping-pong (K1 fills keys_a / vals_a)
