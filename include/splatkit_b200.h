@@ -421,6 +421,13 @@ int sk_shard_assign(int n_items, int world, int rank, int32_t* owned, int* n_own
  * GT image in HOST memory (copied in) — the end-to-end entry point. */
 int sk_train_step_host(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_camera* cam, const uint8_t* gt_host,
                        const sk_train_config* cfg, float extent, int iteration, sk_log_row* row);
+/* The reference Rng (rng.hpp:18-69, mt19937_64 + Box-Muller with a cached
+ * spare) as the density event draws the split noise: successive chunks of
+ * normal() values from one generator seeded with `seed`, written back to back
+ * into out. The batched draw (uniforms in order, transcendentals on worker
+ * threads) is bit-identical to sequential normal() calls. */
+int sk_rng_normals(uint64_t seed, const int64_t* chunks, int n_chunks, float* out);
+
 /* Pipelined variant for streaming inputs: the GT upload runs on a copy
  * stream into one of two device buffers (overlapping the previous step), and
  * `row` (loss / PSNR / pairs) is written when the step completes — during the

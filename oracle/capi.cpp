@@ -396,6 +396,13 @@ extern "C" {
 
 const char* or_last_error() { return g_err.c_str(); }
 int64_t or_last_pge_visited() { return g_pge_visited; }
+
+// The reference Rng's normal() stream (rng.hpp:36-49), count draws cast to float.
+int or_rng_normals(uint64_t seed, int64_t count, float* out) {
+  Rng r(seed);
+  for (int64_t k = 0; k < count; ++k) out[k] = static_cast<float>(r.normal());
+  return 0;
+}
 void or_set_detmath(int on) { g_detmath = on != 0; }
 float or_expf(float x) { return sk::det_expf(x); }
 float or_logf(float x) { return sk::det_logf(x); }

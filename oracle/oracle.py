@@ -216,6 +216,13 @@ def render_scene(params, deg, cam: SkCamera, bin_: SkBinning | None = None, mask
     return Render(img, tr, cc, ranges, vals[: pairs.value].copy(), pairs.value, counts)
 
 
+def rng_normals(seed: int, count: int) -> np.ndarray:
+    """count successive Rng::normal() draws (rng.hpp:36-49) as float32."""
+    out = np.zeros(max(1, count), np.float32)
+    check(lib().or_rng_normals(C.c_uint64(seed), C.c_int64(count), ptr(out)))
+    return out[:count]
+
+
 def last_pge_visited() -> int:
     """Pixel-Gaussian evaluations the reference loop visited in the last
     render_scene / render_pg call on this thread (RenderOutputs::pge_visited)."""

@@ -589,6 +589,19 @@ int sk_train_step_host(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_c
   });
 }
 
+int sk_rng_normals(uint64_t seed, const int64_t* chunks, int n_chunks, float* out) {
+  if (n_chunks < 0 || (n_chunks > 0 && (!chunks || !out))) return SK_ERR_INVALID_ARGUMENT;
+  HostRng r;
+  r.seed(seed);
+  int64_t off = 0;
+  for (int c = 0; c < n_chunks; ++c) {
+    if (chunks[c] < 0) return SK_ERR_INVALID_ARGUMENT;
+    r.normals(out + off, (size_t)chunks[c]);
+    off += chunks[c];
+  }
+  return SK_OK;
+}
+
 int sk_train_step_host_async(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_camera* cam,
                              const uint8_t* gt_host, const sk_train_config* cfg, float extent, int iteration,
                              sk_log_row* row, const sk_comm* comm) {

@@ -258,3 +258,17 @@ def test_config_files_parse_override_and_reject_unknown_keys(tmp_path):
     invalid.densify_every = 600  # does not divide 14500
     with pytest.raises((sk.SplatError, ValueError)):
         sk.validate_config(invalid)
+
+
+def test_rng_normals_match_reference_stream(orc):
+    """The split noise (adc.hpp:190-197) comes from the reference Rng's
+    normal() stream; the library's batched draw (parallel Box-Muller) must be
+    bit-identical to sequential draws, across chunk boundaries (odd chunks
+    carry the cached spare) and for large batches (worker threads)."""
+    chunks = [3, 4, 1, 0, 5, 100001, 6]
+    total = sum(chunks)
+    ref = orc.rng_normals(17, total)
+    arr = (sk.C.c_int64 * len(chunks))(*chunks)
+    out = np.zeros(total, np.float32)
+    assert sk.lib().sk_rng_normals(sk.C.c_uint64(17), arr, len(chunks), sk._p(out)) == 0
+    assert np.array_equal(out, ref)
