@@ -23,6 +23,9 @@ namespace {
 #ifndef SK_SSIM_TY
 #define SK_SSIM_TY 32
 #endif
+#ifndef SK_SSIM_PREFETCH
+#define SK_SSIM_PREFETCH 1
+#endif
 #ifndef SK_SSIM_UNROLL
 #define SK_SSIM_UNROLL 1  // explicit no-unroll of the halo staging: measured -5% K7 (4 or 7: slower)
 #endif
@@ -94,6 +97,17 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
       s_y[iy][ix] = yv;
     }
     __syncthreads();
+#if SK_SSIM_PREFETCH
+    if (ch < 2) {
+      for (int ln = t; ln < kInY * 2; ln += blockDim.x) {
+        const int iy = ln >> 1, half = ln & 1;
+        const int gy = ty0 - kHalo + iy;
+        const int gx = max(0, min(W - 1, tx0 - kHalo + half * 32));
+        if (gy >= 0 && gy < H)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(img + (ch + 1) * plane + (size_t)gy * W + gx));
+      }
+    }
+#endif
     // horizontal: 26 rows x 8 groups of 4 columns
     for (int hw = t; hw < kInY * (kTX / kHX); hw += blockDim.x) {
       const int iy = hw / (kTX / kHX), ox = (hw % (kTX / kHX)) * kHX;
@@ -232,6 +246,19 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
       for (int k = 0; k < 3; ++k) s_u[k][iy][ix] = ok ? partials[(k * 3 + ch) * plane + p] : 0.0f;
     }
     __syncthreads();
+#if SK_SSIM_PREFETCH
+    // L1 prefetch of the next channel's halo rows (3 maps x kInY rows, two
+    // 128-byte lines each) while this channel is filtered
+    if (ch < 2) {
+      for (int ln = t; ln < 3 * kInY * 2; ln += blockDim.x) {
+        const int k = ln / (2 * kInY), iy = (ln >> 1) % kInY, half = ln & 1;
+        const int gy = ty0 - kHalo + iy;
+        const int gx = max(0, min(W - 1, tx0 - kHalo + half * 32));
+        if (gy >= 0 && gy < H)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(partials + (k * 3 + ch + 1) * plane + (size_t)gy * W + gx));
+      }
+    }
+#endif
     for (int hw = t; hw < kInY * (kTX / kHX); hw += blockDim.x) {
       const int iy = hw / (kTX / kHX), ox = (hw % (kTX / kHX)) * kHX;
 #pragma unroll
