@@ -24,6 +24,9 @@
 #ifndef SK_SORT_SMALL_ITEMS
 #define SK_SORT_SMALL_ITEMS 7
 #endif
+#ifndef SK_SORT_LARGE_ITEMS
+#define SK_SORT_LARGE_ITEMS 15
+#endif
 #ifndef SK_SORT_SMALL_N
 #define SK_SORT_SMALL_N 0  // 7 keys per thread for small sorts measured no faster; off
 #endif
@@ -425,7 +428,7 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
   // Small sorts (the depth order over N slots) use 7 keys per thread so the
   // pass spans more CTAs than SMs; large ones (tile ids over P pairs) 15.
   const bool small = n <= (int64_t)SK_SORT_SMALL_N;
-  const int tile_keys = kSortThreads * (small ? SK_SORT_SMALL_ITEMS : kItems);
+  const int tile_keys = kSortThreads * (small ? SK_SORT_SMALL_ITEMS : SK_SORT_LARGE_ITEMS);
   const int64_t tiles = (n + tile_keys - 1) / tile_keys;
   require(tiles < (1ll << 31), "radix_sort_pairs: too many keys");
   uint32_t* hist = radix_hist_buffer(ctx);
@@ -447,7 +450,7 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
       onesweep_kernel<SK_SORT_SMALL_ITEMS><<<(unsigned)tiles, kSortThreads, 0, s>>>(
           keys, vals, keys_alt, vals_alt, n, p * width, dmask, hist + p * kRadix, status, counters + p);
     else
-      onesweep_kernel<kItems><<<(unsigned)tiles, kSortThreads, 0, s>>>(
+      onesweep_kernel<SK_SORT_LARGE_ITEMS><<<(unsigned)tiles, kSortThreads, 0, s>>>(
           keys, vals, keys_alt, vals_alt, n, p * width, dmask, hist + p * kRadix, status, counters + p);
     note_launch();
     std::swap(keys, keys_alt);
