@@ -42,3 +42,33 @@ def test_async_host_steps_match_sync(orc):
     sk.train_step_host(ctx, b, cams[1], gts[1], cfg, 3.0, 11)
     assert pipe.flush()[0]["iteration"] == 10
     ctx.close()
+
+
+def test_nccl_single_rank_communicator(orc):
+    """The NCCL plumbing on one GPU: the library resolves NCCL, a one-rank
+    communicator is created from a unique id, and a view-parallel Trainer
+    and the pipelined host step run with it (all collectives degenerate to
+    no-ops at world size 1, so results equal the communicator-free run)."""
+    import paper_2511_04283_b200 as sk
+    sk.build()
+    ctx = sk.Context(0)
+    uid = sk.comm_unique_id()
+    assert len(uid) == sk.COMM_ID_BYTES and any(uid)
+    comm = sk.Comm(ctx, uid, 1, 0)
+    p = synthetic_scene(3000, deg=3, seed=31)
+    cam = ring_camera(orc, 96, 64, 0.4)
+    gt = np.clip(orc.render_scene(synthetic_scene(3000, deg=3, seed=32), 3, cam).image * 255 + 0.5, 0, 255)
+    gt = gt.astype(np.uint8)
+    cfg = sk.default_config()
+    cfg.densify_from = cfg.densify_until = 1 << 30
+    a = ctx.scene(p, 3)
+    data = sk.Dataset(ctx, [cam], [gt], [0], 3.0)
+    tr = sk.Trainer(ctx, a, data, cfg)
+    tr.set_comm(comm)
+    rows = tr.run(3)
+    assert all(np.isfinite(r["loss"]) for r in rows)
+    pipe = sk.HostStepPipeline(ctx, comm=comm)
+    pipe.step(a, cam, gt, cfg, 3.0, 4)
+    assert np.isfinite(pipe.flush()[0]["loss"])
+    comm.close()
+    ctx.close()
