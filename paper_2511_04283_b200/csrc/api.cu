@@ -88,6 +88,12 @@ int sk_ctx_create(int device, sk_ctx** out) {
 int sk_ctx_destroy(sk_ctx* ctx) {
   if (!ctx) return SK_OK;
   cudaSetDevice(ctx->device);
+  if (ctx->helper) {
+    delete ctx->helper_frame;
+    sk_ctx_destroy(ctx->helper);
+    ctx->helper = nullptr;
+    ctx->helper_frame = nullptr;
+  }
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;

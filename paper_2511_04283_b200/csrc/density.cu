@@ -19,9 +19,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
+#include <thread>
 
 #include "abi_util.h"
 #include "trainer.h"
+
+#ifndef SK_SCORE_TWO_STREAMS
+#define SK_SCORE_TWO_STREAMS 1
+#endif
 
 namespace sk {
 namespace {
@@ -324,6 +329,66 @@ void trace_point(sk_ctx* ctx, const char* what) {
 
 // Renders the k views and leaves s_d / s_p_raw / s_p in the scene's table.
 // gt: device images (u8 HWC) or host float HWC images (staged per view).
+// One scored view (adc.hpp:101-108): render, error maps, photometric term,
+// and the masked count pass into `row`, on context c (its stream, scratch and
+// error word) with frame f.
+void score_view(sk_ctx* c, sk_scene* s, sk_frame* f, const sk_camera& cam, const void* gt_in, bool gt_u8_device,
+                float tau, float lambda, const sk_binning& bin, int32_t* row, float* photo) {
+  const int64_t n = s->n;
+  frame_geometry(f, cam.width, cam.height, &bin);
+  f->camera = cam;
+  ensure_projected(f, n);
+  launch_preprocess(c, s, cam, f);
+  bin_sort(c, f);
+  ensure_image(f);
+  launch_blend_forward(c, f, nullptr, nullptr);
+  f->rendered = true;
+  const int64_t npx = (int64_t)cam.width * cam.height;
+  const void* gt = gt_in;
+  if (!gt_u8_device) {
+    void* g = f->gt.ensure(sizeof(float) * 3 * npx);
+    h2d(c, g, static_cast<const float*>(gt_in), 3 * npx);
+    gt = g;
+  }
+  float* raw = ensure<float>(c->ev.raw, npx);
+  uint8_t* mask = ensure<uint8_t>(c->ev.mask, npx);
+  uint32_t* lohi = ensure<uint32_t>(c->ev.lohi, 4);
+  const uint32_t init[2] = {0xffffffffu, 0u};
+  h2d(c, lohi, init, 2);
+  error_raw_kernel<<<blocks(npx), 256, 0, c->stream>>>(f->image.as<float>(), gt, gt_u8_device, cam.width,
+                                                        cam.height, raw, lohi);
+  note_launch();
+  error_mask_kernel<<<blocks(npx), 256, 0, c->stream>>>(raw, lohi, npx, tau, mask);
+  note_launch();
+  LossSums sums{};
+  launch_loss(c, f, gt, gt_u8_device, lambda, false, &sums);
+  sk_loss_values v{};
+  finish_loss(cam.width, cam.height, lambda, sums, &v);
+  // photometric = (1 - lambda) mean(raw) + lambda (1 - ssim)  (error_maps.hpp:40-41)
+  *photo = (1.0f - lambda) * (float)v.l1 + lambda * (1.0f - (float)v.ssim);
+  launch_blend_forward(c, f, mask, row);
+}
+
+// The second context of the two-stream score pass (own stream, sort / event
+// scratch and error word, plus its frame), created on first use.
+sk_ctx* score_helper(sk_ctx* ctx) {
+  if (!ctx->helper) {
+    sk_ctx* h = nullptr;
+    if (sk_ctx_create(ctx->device, &h) != SK_OK) throw CudaError("score pass: cannot create the helper stream");
+    ctx->helper = h;
+    ctx->helper_frame = new sk_frame();
+  }
+  return ctx->helper;
+}
+
+// Renders the k views and leaves s_d / s_p_raw / s_p in the scene's table.
+// gt: device images (u8 HWC) or host float HWC images (staged per view).
+// With device GT (the Trainer's event) the views are split over two host
+// threads / two streams (even views on ctx, odd views on a helper context):
+// each view's host synchronisations (the pair count, the photometric sums)
+// then only stall its own stream while the other stream's kernels keep the
+// GPU busy. Views are independent (own count row, own photometric slot), so
+// the result is identical to the sequential pass.
 void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_camera>& cams,
                 const std::vector<const void*>& gts, bool gt_u8_device, float tau, float lambda,
                 const sk_binning& bin, std::vector<float>* photo_out, const sk_comm* comm = nullptr) {
@@ -339,41 +404,48 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
   ctx->event_mark(0);
   const int world = comm ? comm->world : 1;
   const int rank = comm ? comm->rank : 0;
-  for (int j = 0; j < k; ++j) {
-    if (j % world != rank) continue;  // views sharded round-robin over ranks (C3 below)
-    const sk_camera& cam = cams[j];
-    frame_geometry(f, cam.width, cam.height, &bin);
-    f->camera = cam;
-    ensure_projected(f, n);
-    launch_preprocess(ctx, s, cam, f);
-    bin_sort(ctx, f);
-    ensure_image(f);
-    launch_blend_forward(ctx, f, nullptr, nullptr);
-    f->rendered = true;
-    const int64_t npx = (int64_t)cam.width * cam.height;
-    const void* gt = gts[j];
-    if (!gt_u8_device) {
-      void* g = f->gt.ensure(sizeof(float) * 3 * npx);
-      h2d(ctx, g, static_cast<const float*>(gts[j]), 3 * npx);
-      gt = g;
+  std::vector<int> mine;  // views sharded round-robin over ranks (C3 below)
+  for (int j = 0; j < k; ++j)
+    if (j % world == rank) mine.push_back(j);
+  auto run_view = [&](sk_ctx* c, sk_frame* fr, int j) {
+    score_view(c, s, fr, cams[j], gts[j], gt_u8_device, tau, lambda, bin, rows + (size_t)j * n, &photo[j]);
+  };
+  if (!(SK_SCORE_TWO_STREAMS && gt_u8_device && mine.size() >= 2)) {
+    for (const int j : mine) run_view(ctx, f, j);
+  } else {
+    sk_ctx* h = score_helper(ctx);
+    prepare_loss(ctx);  // one-time constant upload, before two threads use it
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    SK_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    SK_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    SK_CUDA(cudaEventRecord(e0, ctx->stream));  // rows zeroed before either stream counts
+    SK_CUDA(cudaStreamWaitEvent(h->stream, e0, 0));
+    std::exception_ptr helper_err;
+    std::thread th([&] {
+      try {
+        SK_CUDA(cudaSetDevice(h->device));
+        for (size_t i = 1; i < mine.size(); i += 2) run_view(h, ctx->helper_frame, mine[i]);
+      } catch (...) {
+        helper_err = std::current_exception();
+      }
+    });
+    try {
+      for (size_t i = 0; i < mine.size(); i += 2) run_view(ctx, f, mine[i]);
+    } catch (...) {
+      th.join();
+      cudaStreamSynchronize(h->stream);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      throw;
     }
-    float* raw = ensure<float>(ev.raw, npx);
-    uint8_t* mask = ensure<uint8_t>(ev.mask, npx);
-    const uint32_t init[2] = {0xffffffffu, 0u};
-    h2d(ctx, lohi, init, 2);
-    error_raw_kernel<<<blocks(npx), 256, 0, ctx->stream>>>(f->image.as<float>(), gt, gt_u8_device, cam.width,
-                                                            cam.height, raw, lohi);
-    note_launch();
-    error_mask_kernel<<<blocks(npx), 256, 0, ctx->stream>>>(raw, lohi, npx, tau, mask);
-    note_launch();
-    LossSums sums{};
-    launch_loss(ctx, f, gt, gt_u8_device, lambda, false, &sums);
-    sk_loss_values v{};
-    finish_loss(cam.width, cam.height, lambda, sums, &v);
-    // photometric = (1 - lambda) mean(raw) + lambda (1 - ssim)  (error_maps.hpp:40-41)
-    photo[j] = (1.0f - lambda) * (float)v.l1 + lambda * (1.0f - (float)v.ssim);
-    int32_t* row = rows + (size_t)j * n;
-    launch_blend_forward(ctx, f, mask, row);
+    th.join();
+    SK_CUDA(cudaEventRecord(e1, h->stream));
+    SK_CUDA(cudaStreamWaitEvent(ctx->stream, e1, 0));
+    SK_CUDA(cudaStreamSynchronize(h->stream));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (helper_err) std::rethrow_exception(helper_err);
+    raise_device_errors(read_error_word(h));
   }
   float* dphoto = ensure<float>(ev.photo, k);
   h2d(ctx, dphoto, photo.data(), k);

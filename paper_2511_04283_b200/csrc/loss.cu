@@ -349,6 +349,8 @@ void launch_loss(sk_ctx* ctx, sk_frame* f, const void* gt, bool gt_u8, float lam
   if (out) read_loss_sums(ctx, out);
 }
 
+void prepare_loss(sk_ctx* ctx) { upload_gauss(ctx->stream); }
+
 void read_loss_sums(sk_ctx* ctx, LossSums* out) {
   double h[4];
   SK_CUDA(cudaMemcpyAsync(h, ctx->scalars.ptr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));

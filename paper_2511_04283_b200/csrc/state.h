@@ -98,6 +98,9 @@ struct sk_ctx {
   void mark(int i) {
     if (timing) cudaEventRecord(tev[tev_set][i], stream);
   }
+  // second context of the two-stream density-event score pass (density.cu)
+  sk_ctx* helper = nullptr;
+  struct sk_frame* helper_frame = nullptr;
   void event_mark(int i) {
     if (timing && ev.tev[i]) cudaEventRecord(ev.tev[i], stream);
   }
@@ -218,6 +221,8 @@ struct LossSums {
 // out == nullptr leaves the sums on the device for read_loss_sums (no sync).
 void launch_loss(sk_ctx* ctx, sk_frame* f, const void* gt, bool gt_u8, float lambda, bool want_grad, LossSums* out);
 void read_loss_sums(sk_ctx* ctx, LossSums* out);
+// One-time upload of the SSIM window constants (idempotent).
+void prepare_loss(sk_ctx* ctx);
 void finish_loss(int width, int height, float lambda, const LossSums& s, sk_loss_values* out);
 
 // optim.cu
