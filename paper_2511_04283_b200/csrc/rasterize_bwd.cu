@@ -75,6 +75,9 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 // cp.async double-buffered gather on the mask path: measured 3% slower than
 // the direct gather (it needs the extra buffer registers / smem and K8's
 // gathers are already sparse), so off by default.
+#ifndef SK_BWD_PAIRWALK
+#define SK_BWD_PAIRWALK 1
+#endif
 #ifndef SK_BWD_BRANCHLESS
 #define SK_BWD_BRANCHLESS 1  // measured: -6.8% K8 time
 #endif
@@ -165,7 +168,9 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
   bool has_pend = false;
 
   // Per-entry reverse-walk step for staged slot j (list position idx).
-  auto walk_entry = [&](int j, int idx) {
+  // The 11 gradient partials of staged slot j (list position idx) over this
+  // lane's pixels; returns whether one of them blended the entry.
+  auto partials = [&](int j, int idx, float (&gv)[kBGradFields]) -> bool {
     const float4 mq = s_xyq[j];
     const float4 co = s_co[j];
     float g_mu0 = 0.f, g_mu1 = 0.f, g_c00 = 0.f, g_c01 = 0.f, g_c11 = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f,
@@ -273,27 +278,33 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
       }
     }
 #endif
+    gv[0] = g_mu0; gv[1] = g_mu1; gv[2] = g_c00; gv[3] = g_c01; gv[4] = g_c11; gv[5] = g_r;
+    gv[6] = g_g; gv[7] = g_b; gv[8] = g_op; gv[9] = g_a0; gv[10] = g_a1;
+    return contrib;
+  };
+
+  auto walk_entry = [&](int j, int idx) {
+    float gv0[kBGradFields];
+    const bool contrib = partials(j, idx, gv0);
     const uint32_t cb = __ballot_sync(0xffffffffu, contrib);
 #if SK_BWD_SINGLE_LANE
     if (__popc(cb) <= SK_BWD_DIRECT_MAX) {
       // few contributing lanes: each adds its own partials (one lane: they
       // are the warp sum), no shuffle reduction
       if (contrib) {
-        const float gv[kBGradFields] = {g_mu0, g_mu1, g_c00, g_c01, g_c11, g_r, g_g, g_b, g_op, g_a0, g_a1};
         const uint32_t id = s_id[j];
 #pragma unroll
-        for (int f = 0; f < kBGradFields; ++f) atomicAdd(&bgrads[(int64_t)f * gstride + id], gv[f]);
+        for (int f = 0; f < kBGradFields; ++f) atomicAdd(&bgrads[(int64_t)f * gstride + id], gv0[f]);
       }
     } else
 #endif
     if (cb) {
-      const float gv[kBGradFields] = {g_mu0, g_mu1, g_c00, g_c01, g_c11, g_r, g_g, g_b, g_op, g_a0, g_a1};
       if (has_pend) {
-        reduce_scatter_2x11(pend, gv, pend_id, s_id[j], true, bgrads, gstride);
+        reduce_scatter_2x11(pend, gv0, pend_id, s_id[j], true, bgrads, gstride);
         has_pend = false;
       } else {
 #pragma unroll
-        for (int f = 0; f < kBGradFields; ++f) pend[f] = gv[f];
+        for (int f = 0; f < kBGradFields; ++f) pend[f] = gv0[f];
         pend_id = s_id[j];
         has_pend = true;
       }
@@ -389,11 +400,39 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
           s_id[base + lane] = g;
         }
         __syncwarp();
+#if SK_BWD_PAIRWALK
+        // entries taken two at a time straight into one reduce-scatter (every
+        // masked entry has a contributing lane); one entry is carried over
+        // only when a batch has an odd count
+        while (m) {
+          const int ba = 31 - __clz(m);
+          m ^= 1u << ba;
+          float ga[kBGradFields];
+          partials(base + ba, b0 + ba, ga);
+          const uint32_t ida = s_id[base + ba];
+          if (has_pend) {
+            reduce_scatter_2x11(pend, ga, pend_id, ida, true, bgrads, gstride);
+            has_pend = false;
+          } else if (m) {
+            const int bb2 = 31 - __clz(m);
+            m ^= 1u << bb2;
+            float gb[kBGradFields];
+            partials(base + bb2, b0 + bb2, gb);
+            reduce_scatter_2x11(ga, gb, ida, s_id[base + bb2], true, bgrads, gstride);
+          } else {
+#pragma unroll
+            for (int f = 0; f < kBGradFields; ++f) pend[f] = ga[f];
+            pend_id = ida;
+            has_pend = true;
+          }
+        }
+#else
         while (m) {
           const int bit = 31 - __clz(m);
           m ^= 1u << bit;
           walk_entry(base + bit, b0 + bit);
         }
+#endif
         __syncwarp();
       }
 #endif
