@@ -76,7 +76,7 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 // the direct gather (it needs the extra buffer registers / smem and K8's
 // gathers are already sparse), so off by default.
 #ifndef SK_BWD_PAIRWALK
-#define SK_BWD_PAIRWALK 1
+#define SK_BWD_PAIRWALK 0  // measured: 5% slower (register pressure)
 #endif
 #ifndef SK_BWD_BRANCHLESS
 #define SK_BWD_BRANCHLESS 1  // measured: -6.8% K8 time
