@@ -59,10 +59,14 @@ struct DevBuf {
   }
   void* ensure(size_t want) {
     if (want <= bytes) return ptr;
+    // a buffer that has to grow gets 25% headroom: per-view pair counts and
+    // scene sizes drift during training, and every cudaFree synchronises the
+    // device (stalling the other stream of a two-stream score pass)
+    const bool regrow = ptr != nullptr;
     if (ptr) SK_CUDA(cudaFree(ptr));
     ptr = nullptr;
     bytes = 0;
-    size_t alloc = want < 256 ? 256 : want;
+    size_t alloc = want < 256 ? 256 : (regrow ? want + want / 4 : want);
     SK_CUDA(cudaMalloc(&ptr, alloc));
     bytes = alloc;
     return ptr;
