@@ -23,6 +23,8 @@
 #include <zlib.h>
 
 #include <algorithm>
+#include <thread>
+#include <atomic>
 #include <cctype>
 #include <cmath>
 #include <cstdio>
@@ -964,23 +966,43 @@ int sk_dataset_load(sk_ctx* ctx, const char* dir, sk_dataset** out) {
     std::vector<int> ids;
     io::read_cameras((root / "cameras.json").string(), cams, ids);
     auto d = std::make_unique<sk_dataset>();
-    for (size_t v = 0; v < cams.size(); ++v) {
-      const io::fs::path img = root / "images" / io::image_name(ids[v]);
-      require(io::fs::exists(img), "dataset: missing image " + img.string());
-      std::vector<uint8_t> rgb;
-      int w = 0, h = 0;
-      io::read_png_u8(img.string(), rgb, w, h);
-      require(w == cams[v].width && h == cams[v].height,
-              "dataset: image " + img.string() + " is " + std::to_string(w) + "x" + std::to_string(h) +
-                  " but camera " + std::to_string(ids[v]) + " expects " + std::to_string(cams[v].width) + "x" +
-                  std::to_string(cams[v].height));
+    // decode the PNGs on host worker threads (independent files), then upload
+    // in view order; errors are reported for the first failing view, as the
+    // reference's sequential loop would
+    const size_t nv = cams.size();
+    std::vector<std::vector<uint8_t>> rgb(nv);
+    std::vector<std::string> errs(nv);
+    std::atomic<size_t> next{0};
+    auto worker = [&] {
+      for (size_t v; (v = next.fetch_add(1)) < nv;) {
+        try {
+          const io::fs::path img = root / "images" / io::image_name(ids[v]);
+          require(io::fs::exists(img), "dataset: missing image " + img.string());
+          int w = 0, h = 0;
+          io::read_png_u8(img.string(), rgb[v], w, h);
+          require(w == cams[v].width && h == cams[v].height,
+                  "dataset: image " + img.string() + " is " + std::to_string(w) + "x" + std::to_string(h) +
+                      " but camera " + std::to_string(ids[v]) + " expects " + std::to_string(cams[v].width) + "x" +
+                      std::to_string(cams[v].height));
+        } catch (const std::exception& e) {
+          errs[v] = e.what();
+        }
+      }
+    };
+    const size_t nt = std::min<size_t>(nv, std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    std::vector<std::thread> pool;
+    for (size_t t = 1; t < nt; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& t : pool) t.join();
+    for (size_t v = 0; v < nv; ++v) require(errs[v].empty(), errs[v]);
+    for (size_t v = 0; v < nv; ++v) {
       auto buf = std::make_unique<DevBuf>();
-      buf->ensure(rgb.size());
-      h2d(ctx, buf->ptr, rgb.data(), rgb.size());
-      sync(ctx);  // rgb is a pageable temporary
+      buf->ensure(rgb[v].size());
+      h2d(ctx, buf->ptr, rgb[v].data(), rgb[v].size());
       d->cams.push_back(cams[v]);
       d->images.push_back(std::move(buf));
     }
+    sync(ctx);  // the host images are pageable temporaries
     io::read_points((root / "points3d.ply").string(), d->init_xyz, d->init_rgb);
     d->ids = ids;
     // split_views (dataset.hpp:44-53)
