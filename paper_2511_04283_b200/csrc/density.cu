@@ -410,7 +410,9 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
   auto run_view = [&](sk_ctx* c, sk_frame* fr, int j) {
     score_view(c, s, fr, cams[j], gts[j], gt_u8_device, tau, lambda, bin, rows + (size_t)j * n, &photo[j]);
   };
-  if (!(SK_SCORE_TWO_STREAMS && gt_u8_device && mine.size() >= 2)) {
+  const char* one = std::getenv("SK_SCORE_ONE_STREAM");  // runtime override (tests / diagnostics)
+  const bool two = SK_SCORE_TWO_STREAMS && !(one && one[0] == '1');
+  if (!(two && gt_u8_device && mine.size() >= 2)) {
     for (const int j : mine) run_view(ctx, f, j);
   } else {
     sk_ctx* h = score_helper(ctx);

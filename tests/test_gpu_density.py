@@ -228,3 +228,39 @@ def test_config1_training_parity(ctx, orc):
         assert sum(flips.values()) <= max(3, n // 100)
     assert abs(ps_gpu - ps_cpu) <= 0.05
     assert abs(rows[-1]["loss"] - orows[-1, 0]) < 0.05 * abs(orows[-1, 0]) + 1e-3
+
+
+def test_two_stream_score_pass_identical(ctx, orc):
+    """The density event's two-stream score pass (views split over two host
+    threads / streams) gives exactly the single-stream result: same sampled
+    views, photometric scores, selections and compacted scene. No training
+    beforehand (its atomic gradient sums are not bit-reproducible); the
+    gradient statistics are a seeded table instead."""
+    import os
+
+    import paper_2511_04283_b200 as sk
+    ds, gt, xyz, rgb = sk.Dataset.synthetic(ctx, n_gaussians=4000, n_views=12, width=96, seed=7)
+    p0 = orc.init_from_points(xyz, rgb, 3)
+    cfg = sk.default_config()
+    cfg.k = 9
+    cfg.tau_d = 0.5
+    cfg.size_prune_from = 0
+    out = []
+    for one in ("1", "0"):
+        os.environ["SK_SCORE_ONE_STREAM"] = one
+        try:
+            scene = ctx.scene(p0, 3)
+            tr = sk.Trainer(ctx, scene, ds, cfg, record_events=True)
+            scene.set_score_table(**_random_table(np.random.default_rng(3), scene.size))
+            tr.density_event(600, True, True)
+            out.append((scene.download(), tr.events()[-1]))
+            tr.close()
+        finally:
+            os.environ.pop("SK_SCORE_ONE_STREAM", None)
+    (p1, e1), (p2, e2) = out
+    assert e1["n_after"] == e2["n_after"] and list(e1["sampled"]) == list(e2["sampled"])
+    assert len(e1["sampled"]) == 9
+    assert e1["n_clone"] + e1["n_split"] + e1["n_prune"] > 0
+    for key in ("clone", "split", "prune", "photometric"):
+        assert np.array_equal(np.asarray(e1[key]), np.asarray(e2[key])), key
+    assert np.array_equal(p1, p2)
