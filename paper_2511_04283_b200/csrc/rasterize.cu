@@ -32,6 +32,12 @@
 #ifndef SK_FWD_ASYNC_GATHER
 #define SK_FWD_ASYNC_GATHER 1
 #endif
+#ifndef SK_FWD_NANDONE
+// 1: a finished (or off-image) pixel's row coordinate becomes NaN, so its q is
+// NaN and one unsigned compare q_bits <= q_cut_bits replaces the done flag and
+// both range tests (q >= 0 and q <= q_cut; q + 0 maps -0 to +0)
+#define SK_FWD_NANDONE 1
+#endif
 #ifndef SK_FWD_PIX16
 #define SK_FWD_PIX16 2
 #endif
@@ -216,6 +222,9 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
     n[k] = last[k] = 0;
     done[k] = !(px < W && py < H);
     all_done = all_done && done[k];
+#if SK_FWD_NANDONE
+    if (done[k]) fpy[k] = __int_as_float(0x7fc00000);
+#endif
   }
 
 #if SK_FWD_ASYNC_GATHER
@@ -323,7 +332,11 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
         const float dx = fpx - mq.x;
         const float dy = fpy[k] - mq.y;
         const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
+#if SK_FWD_NANDONE
+        if (__float_as_uint(__fadd_rn(q, 0.0f)) > __float_as_uint(mq.z)) continue;  // -0 -> +0
+#else
         if (done[k] || !(q >= 0.0f && q <= mq.z)) continue;
+#endif
         float alpha = co.w * det_expf_neg(-0.5f * q, tab);
         alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
         if (alpha < kAlphaMin) continue;
@@ -336,7 +349,12 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
         ++n[k];
         last[k] = b0 + j + 1;
         T[k] = T[k] * (1.0f - alpha);
-        if (T[k] < kTransmitMin) done[k] = true;
+        if (T[k] < kTransmitMin) {
+          done[k] = true;
+#if SK_FWD_NANDONE
+          fpy[k] = __int_as_float(0x7fc00000);
+#endif
+        }
       }
 #endif
       bool ad = true;

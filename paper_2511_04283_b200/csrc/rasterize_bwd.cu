@@ -81,6 +81,13 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 #ifndef SK_BWD_BRANCHLESS
 #define SK_BWD_BRANCHLESS 1  // measured: -6.8% K8 time
 #endif
+#ifndef SK_BWD_UQ
+// 1: q in [0, q_cut] as one unsigned compare of (q + 0) bits (K6's test), and
+// the two near-threshold bands folded into one symmetric band around the
+// midpoint of alpha_min and the cap (absolute half-width 1e-5 * cap, which
+// contains both relative 1e-5 bands)
+#define SK_BWD_UQ 1
+#endif
 #ifndef SK_BWD_SINGLE_LANE
 #define SK_BWD_SINGLE_LANE 0  // measured: no gain (1.112 vs 1.101 ms)
 #endif
@@ -187,10 +194,18 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
       const float dy = fpy[k] - mq.y;
       const float q = rn_add(rn_add(rn_mul(rn_mul(co.x, dx), dx), rn_mul(rn_mul(rn_mul(2.0f, co.y), dx), dy)),
                              rn_mul(rn_mul(co.z, dy), dy));
+#if SK_BWD_UQ
+      bool ok = idx < last[k] && __float_as_uint(__fadd_rn(q, 0.0f)) <= __float_as_uint(mq.z);
+      float ge = __expf(-0.5f * q);
+      float raw = co.w * ge;
+      constexpr float kMid = (float)((1.0 / 255 + 0.99) / 2), kHalf = (float)((0.99 - 1.0 / 255) / 2);
+      if (ok && fabsf(fabsf(raw - kMid) - kHalf) <= 1e-5f * kAlphaCap) {
+#else
       bool ok = idx < last[k] && q >= 0.0f && q <= mq.z;
       float ge = __expf(-0.5f * q);
       float raw = co.w * ge;
       if (ok && (fabsf(raw - kAlphaMin) <= 1e-5f * kAlphaMin || fabsf(raw - kAlphaCap) <= 1e-5f * kAlphaCap)) {
+#endif
         ge = det_expf_core(rn_mul(-0.5f, q), tab);
         raw = rn_mul(co.w, ge);
       }
