@@ -38,6 +38,12 @@
 // both range tests (q >= 0 and q <= q_cut; q + 0 maps -0 to +0)
 #define SK_FWD_NANDONE 1
 #endif
+#ifndef SK_FWD_BATCH_DONE
+// 1 (needs SK_FWD_NANDONE): the walk no longer tracks per-entry "all my
+// pixels done"; finished pixels reject every entry by their NaN row, and
+// the all-done test runs once per 32-entry batch
+#define SK_FWD_BATCH_DONE 1
+#endif
 #ifndef SK_FWD_PIX16
 #define SK_FWD_PIX16 2
 #endif
@@ -296,7 +302,11 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
     uint32_t m = __ballot_sync(0xffffffffu, hit);
     __syncwarp();
     uint32_t lane_bits = 0;  // entries of this batch one of my pixels blended
+#if SK_FWD_NANDONE && SK_FWD_BATCH_DONE
+    while (m) {
+#else
     while (m && !all_done) {
+#endif
       const int j = __ffs(m) - 1;
       m &= m - 1;
       const float4 mq = s_xyq[warp][j];
@@ -349,19 +359,33 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
         ++n[k];
         last[k] = b0 + j + 1;
         T[k] = T[k] * (1.0f - alpha);
+#if SK_FWD_NANDONE && SK_FWD_BATCH_DONE
+        fpy[k] = T[k] < kTransmitMin ? __int_as_float(0x7fc00000) : fpy[k];
+#else
         if (T[k] < kTransmitMin) {
           done[k] = true;
 #if SK_FWD_NANDONE
           fpy[k] = __int_as_float(0x7fc00000);
 #endif
         }
+#endif
       }
 #endif
+#if !(SK_FWD_NANDONE && SK_FWD_BATCH_DONE)
       bool ad = true;
 #pragma unroll
       for (int k = 0; k < PIX; ++k) ad = ad && done[k];
       all_done = ad;
+#endif
     }
+#if SK_FWD_NANDONE && SK_FWD_BATCH_DONE
+    {
+      bool ad = true;
+#pragma unroll
+      for (int k = 0; k < PIX; ++k) ad = ad && isnan(fpy[k]);
+      all_done = ad;
+    }
+#endif
     // contribution mask of this warp block for the batch (read by K8, which
     // then skips entries no pixel of its block blended); unwalked batches
     // keep the frame-start zeros
