@@ -33,6 +33,29 @@ __device__ __forceinline__ void cp_async_wait() {
 __host__ __device__ __forceinline__ int64_t cmask_word(int begin, int tile) { return (int64_t)(begin >> 5) + tile; }
 inline size_t cmask_words(int64_t pairs, int tiles) { return (size_t)(pairs >> 5) + (size_t)tiles + 2; }
 
+#ifndef SK_STAGE_APPROX
+// 1: the culling geometry (ellipse box, edge minimiser) uses MUFU sqrt /
+// reciprocal instead of the IEEE sequences -fmad=false files get; culling
+// only has to be conservative and carries 1e-4 / 1e-3 slack
+#define SK_STAGE_APPROX 1
+#endif
+__device__ __forceinline__ float cull_sqrt(float x) {
+#if SK_STAGE_APPROX
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+#else
+  return sqrtf(x);
+#endif
+}
+__device__ __forceinline__ float cull_div(float a, float b) {
+#if SK_STAGE_APPROX
+  return __fdividef(a, b);
+#else
+  return a / b;
+#endif
+}
+
 __device__ __forceinline__ float qcut_of(float opacity) {
   const float a = 255.0f * opacity;
   return a > 1.0f ? 2.0f * __logf(a) + 0.02f : -1.0f;
@@ -51,8 +74,8 @@ __device__ __forceinline__ void stage_entry(float2 mu, float4 co, float4& xyq, f
     bb = make_float4(-3.0e38f, 3.0e38f, -3.0e38f, 3.0e38f);  // no culling
     return;
   }
-  const float ex = sqrtf(qc * co.z / det) * 1.0001f + 0.01f;
-  const float ey = sqrtf(qc * co.x / det) * 1.0001f + 0.01f;
+  const float ex = cull_sqrt(cull_div(qc * co.z, det)) * 1.0001f + 0.01f;
+  const float ey = cull_sqrt(cull_div(qc * co.x, det)) * 1.0001f + 0.01f;
   bb = make_float4(mu.x - ex, mu.x + ex, mu.y - ey, mu.y + ey);
 }
 
@@ -86,7 +109,7 @@ struct WarpBlock {
     const float y0 = (float)(ty * TS + (w / kWarpsX) * (4 * PIX)), y1 = y0 + (float)(4 * PIX - 1);
     if (mq.x >= x0 && mq.x <= x1 && mq.y >= y0 && mq.y <= y1) return true;
     const float a = co.x, b = co.y, c = co.z;
-    const float ia = 1.0f / a, ic = 1.0f / c;
+    const float ia = cull_div(1.0f, a), ic = cull_div(1.0f, c);
     float best = 3.0e38f;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
