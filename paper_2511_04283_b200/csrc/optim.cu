@@ -319,13 +319,16 @@ __device__ __forceinline__ void accumulate_stats(const Stats& st, int64_t i, int
 #define SK_K9_PREFETCH 2  // all parameter rows + blend grads: measured -12% K9 time
 #endif
 constexpr int kPbThreads = 128;
+#ifndef SK_K9_MINB
+#define SK_K9_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
 
 // K9: one thread per Gaussian computes all parameter gradients into its
 // column of a shared-memory tile (conflict-free: column = threadIdx.x, so no
 // 59-register live range) and the tile is written back as coalesced rows of the
 // planar gradient buffer; culled Gaussians get zeros (SceneGrads::init).
 template <int DEG>
-__global__ void __launch_bounds__(kPbThreads, 4) project_bwd_kernel(
+__global__ void __launch_bounds__(kPbThreads, SK_K9_MINB) project_bwd_kernel(
     const float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ radius,
     const float4* __restrict__ conic4, const float* __restrict__ bg, int64_t gstride, float* __restrict__ grads,
     Stats st, bool do_stats) {
