@@ -95,6 +95,11 @@ int sk_ctx_destroy(sk_ctx* ctx) {
     ctx->helper_frame = nullptr;
   }
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->count_stream) {
+    cudaStreamSynchronize(ctx->count_stream);
+    cudaStreamDestroy(ctx->count_stream);
+  }
+  if (ctx->count_ev) cudaEventDestroy(ctx->count_ev);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return SK_OK;

@@ -57,6 +57,10 @@ int tile_bits(int tiles) {
   return b;
 }
 
+#ifndef SK_SPECULATIVE_DUP
+#define SK_SPECULATIVE_DUP 1
+#endif
+
 // K2-K5 (build_tile_grid raster.hpp:157-168).
 void bin_sort(sk_ctx* ctx, sk_frame* f) {
   const int64_t n = f->n;
@@ -75,18 +79,34 @@ void bin_sort(sk_ctx* ctx, sk_frame* f) {
   uint32_t* vb = ensure<uint32_t>(f->vals_b, n);
   radix_sort_pairs(ctx, ka, kb, va, vb, n, 32);  // depth_order: (depth, index)
   int32_t* offsets = ensure<int32_t>(f->offsets, n);
-  const int64_t pairs = scan_gathered(ctx, f->tiles.as<int32_t>(), va, offsets, n);
+  const int bits = tile_bits(tiles);
+  uint32_t* hist = radix_hist_buffer(ctx);
+  const long long* d_total = launch_scan_gathered(ctx, f->tiles.as<int32_t>(), va, offsets, n);
+  // Speculative emission: the pair buffers already hold `cap` pairs from an
+  // earlier frame (DevBuf keeps 25% headroom), so K3 is launched before the
+  // host reads the pair count and the GPU emits pairs while the host waits;
+  // it is relaunched only if the count outgrew the buffers.
+  auto cap_of = [](const DevBuf& b) { return (int64_t)(b.bytes / sizeof(uint32_t)); };
+  const int64_t cap = SK_SPECULATIVE_DUP ? std::min(std::min(cap_of(f->ptile_a), cap_of(f->ptile_b)),
+                                                    std::min(cap_of(f->pval_a), cap_of(f->pval_b)))
+                                         : 0;
+  auto emit = [&](int64_t limit) {
+    SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * 256, ctx->stream));
+    launch_duplicate(ctx, f, va, offsets, f->ptile_a.as<uint32_t>(), f->pval_a.as<uint32_t>(), radix_passes(bits),
+                     radix_digit_width(bits), hist, limit);
+  };
+  if (cap > 256) emit(cap);
+  const int64_t pairs = read_scan_total(ctx, d_total);
   require(pairs < (1ll << 30), "build_tile_grid: too many tile/Gaussian pairs");
   f->pairs = pairs;
   const size_t pm = (size_t)std::max<int64_t>(pairs, 1);
+  // the speculative K3 may still be writing the buffers a regrowth frees
+  if (cap > 256 && pairs > cap) SK_CUDA(cudaStreamSynchronize(ctx->stream));
   uint32_t* ta = ensure<uint32_t>(f->ptile_a, pm);
   uint32_t* tb = ensure<uint32_t>(f->ptile_b, pm);
   uint32_t* pa = ensure<uint32_t>(f->pval_a, pm);
   uint32_t* pb = ensure<uint32_t>(f->pval_b, pm);
-  const int bits = tile_bits(tiles);
-  uint32_t* hist = radix_hist_buffer(ctx);
-  SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * 256, ctx->stream));
-  launch_duplicate(ctx, f, va, offsets, ta, pa, radix_passes(bits), radix_digit_width(bits), hist);
+  if (!(cap > 256 && pairs <= cap)) emit(pairs);
   radix_sort_pairs(ctx, ta, tb, pa, pb, pairs, bits, /*hist_ready=*/true);
   f->pair_tile = ta;
   f->pair_val = pa;

@@ -377,7 +377,8 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(int64_t n, BinPa
                                                                 const float* __restrict__ a_star,
                                                                 uint32_t* __restrict__ pair_tile,
                                                                 uint32_t* __restrict__ pair_val, int passes,
-                                                                int width, uint32_t* __restrict__ hist) {
+                                                                int width, uint32_t* __restrict__ hist,
+                                                                int64_t cap) {
   __shared__ uint32_t s_hist[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += kDupThreads) (&s_hist[0][0])[i] = 0;
   __syncthreads();
@@ -407,8 +408,10 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(int64_t n, BinPa
           const float rx1 = (float)(min((tx + 1) * bp.ts, bp.W) - 1);
           if (min_mahalanobis_on_rect(co.x, co.y, co.z, mu.x, mu.y, rx0, rx1, ry0, ry1) <= as) {
             const uint32_t t = (uint32_t)(ty * bp.tiles_x + tx);
-            pair_tile[o] = t;
-            pair_val[o] = g;
+            if (o < cap) {
+              pair_tile[o] = t;
+              pair_val[o] = g;
+            }
             count_digits(t);
             ++o;
           }
@@ -450,8 +453,10 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(int64_t n, BinPa
         const int r = k / ow;
 #endif
         t = (uint32_t)((oy + r) * bp.tiles_x + ox + (k - r * ow));
-        pair_tile[pos] = t;
-        pair_val[pos] = og;
+        if (pos < cap) {
+          pair_tile[pos] = t;
+          pair_val[pos] = og;
+        }
       }
       if (active) count_digits(t);
     }
@@ -515,14 +520,14 @@ void launch_inject_bin(sk_ctx* ctx, sk_frame* f) {
 }
 
 void launch_duplicate(sk_ctx* ctx, sk_frame* f, const uint32_t* order, const int32_t* offsets, uint32_t* pair_tile,
-                      uint32_t* pair_val, int passes, int width, uint32_t* hist) {
+                      uint32_t* pair_val, int passes, int width, uint32_t* hist, int64_t cap) {
   if (f->n == 0) return;
   const BinParams bp = make_bin_params(f);
   const int64_t warps = (f->n + 31) / 32;
   const unsigned grid = (unsigned)std::min<int64_t>((warps + kDupThreads / 32 - 1) / (kDupThreads / 32), 148 * 8);
   duplicate_kernel<<<grid, kDupThreads, 0, ctx->stream>>>(
       f->n, bp, order, offsets, f->tiles.as<int>(), f->rect.as<int4>(), f->mean2d.as<float2>(),
-      f->conic_op.as<float4>(), f->a_star.as<float>(), pair_tile, pair_val, passes, width, hist);
+      f->conic_op.as<float4>(), f->a_star.as<float>(), pair_tile, pair_val, passes, width, hist, cap);
   note_launch();
   SK_CUDA(cudaGetLastError());
 }

@@ -459,8 +459,9 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
   SK_CUDA(cudaGetLastError());
 }
 
-int64_t scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets, int64_t n) {
-  if (n == 0) return 0;
+const long long* launch_scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets,
+                                      int64_t n) {
+  if (n == 0) return nullptr;
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
   auto* status = ensure<unsigned long long>(ctx->sort.scan_status, (size_t)tiles + 1);
   auto* total = ensure<long long>(ctx->sort.scan_total, 2);
@@ -471,10 +472,25 @@ int64_t scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order,
   scan_gather_kernel<<<(unsigned)tiles, kScanThreads, 0, s>>>(values, order, offsets, n, status, counter, total);
   note_launch();
   SK_CUDA(cudaGetLastError());
-  long long host_total = 0;
-  SK_CUDA(cudaMemcpyAsync(&host_total, total, sizeof(long long), cudaMemcpyDeviceToHost, s));
-  SK_CUDA(cudaStreamSynchronize(s));
-  return host_total;
+  if (!ctx->count_stream) {
+    SK_CUDA(cudaStreamCreateWithFlags(&ctx->count_stream, cudaStreamNonBlocking));
+    SK_CUDA(cudaEventCreateWithFlags(&ctx->count_ev, cudaEventDisableTiming));
+  }
+  auto* host = static_cast<long long*>(ctx->count_pinned.ensure(sizeof(long long)));
+  SK_CUDA(cudaEventRecord(ctx->count_ev, s));
+  SK_CUDA(cudaStreamWaitEvent(ctx->count_stream, ctx->count_ev, 0));
+  SK_CUDA(cudaMemcpyAsync(host, total, sizeof(long long), cudaMemcpyDeviceToHost, ctx->count_stream));
+  return total;
+}
+
+int64_t read_scan_total(sk_ctx* ctx, const long long* total) {
+  if (!total) return 0;
+  SK_CUDA(cudaStreamSynchronize(ctx->count_stream));
+  return *static_cast<const long long*>(ctx->count_pinned.ptr);
+}
+
+int64_t scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets, int64_t n) {
+  return read_scan_total(ctx, launch_scan_gathered(ctx, values, order, offsets, n));
 }
 
 

@@ -89,6 +89,12 @@ struct sk_ctx {
   sk::DevBuf pge;       // uint64 [2] workload counters (sk_frame_pge_counts)
   sk::DevBuf loss_blocks;  // double [blocks][3] per-block loss sums (deterministic reduction)
   sk::HostBuf pinned;   // staging
+  // pair-count readback (sort.cu read_scan_total): copied on its own stream
+  // after the scan, so the host waits for the scan only, not for the
+  // speculative K3 queued behind it
+  cudaStream_t count_stream = nullptr;
+  cudaEvent_t count_ev = nullptr;
+  sk::HostBuf count_pinned;
   // phase timing (sk_ctx_enable_timing)
   bool timing = false;
   cudaEvent_t tev[2][SK_NUM_PHASES + 1] = {};  // two sets: a deferred step is read while the next records
@@ -192,8 +198,10 @@ void launch_preprocess(sk_ctx* ctx, const sk_scene* scene, const sk_camera& cam,
 void launch_inject_bin(sk_ctx* ctx, sk_frame* f);
 // Also accumulates the digit counts of the tile-id radix sort (passes digit
 // passes) into hist (see radix_hist_buffer), so the sort can skip its upsweep.
+// Pairs at positions >= cap are not written (speculative launch before the
+// pair count is known on the host; see bin_sort).
 void launch_duplicate(sk_ctx* ctx, sk_frame* f, const uint32_t* order, const int32_t* offsets, uint32_t* pair_tile,
-                      uint32_t* pair_val, int passes, int width, uint32_t* hist);
+                      uint32_t* pair_val, int passes, int width, uint32_t* hist, int64_t cap);
 
 // sort.cu
 // Stable LSD radix sort of (key, value) pairs on key bits [0, bits). On
@@ -206,6 +214,11 @@ int radix_passes(int bits);
 int radix_digit_width(int bits);  // bits per digit pass (even split)
 // Exclusive scan of tiles[order[i]] into offsets[i]; returns the total.
 int64_t scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets, int64_t n);
+// The same split in two: the launch (total left on the device) and the
+// blocking read of the total.
+const long long* launch_scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets,
+                                      int64_t n);
+int64_t read_scan_total(sk_ctx* ctx, const long long* total);
 void launch_tile_ranges(sk_ctx* ctx, const uint32_t* pair_tile, int64_t pairs, int2* ranges, int tiles);
 
 // rasterize.cu
