@@ -217,7 +217,22 @@ __device__ __forceinline__ void stage_neg_exp_table(float* s_table) {
     s_table[m] = bits_to_f32(kExp2TableDev[j] + ((uint32_t)e << 23));
   }
 }
-__device__ __forceinline__ float det_expf_neg(float x, const SmemTable& neg_table) {
+// The same table with its shared-window base pinned in a register.
+struct SmemPinnedTable {
+  uint32_t base;
+  // the asm keeps the converted address in one register (otherwise it is
+  // rematerialised with an S2R of the cluster CTA id at every lookup)
+  __device__ explicit SmemPinnedTable(const float* s) {
+    asm volatile("mov.u32 %0, %1;" : "=r"(base) : "r"((uint32_t)__cvta_generic_to_shared(s)));
+  }
+  __device__ __forceinline__ float operator[](int j) const {
+    float v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(base + 4u * (uint32_t)j));
+    return v;
+  }
+};
+template <class Tab>
+__device__ __forceinline__ float det_expf_neg(float x, const Tab& neg_table) {
   const float kf = det_floorf(rn_add(rn_mul(x, 92.33248261689366f), 0.5f));  // 64 / ln2
   const float r = rn_sub(rn_sub(x, rn_mul(kf, 0.010833740234375f)), rn_mul(kf, -3.3155381258549027e-06f));
   float p = rn_add(rn_mul(r, 0.16666666666666666f), 0.5f);

@@ -44,6 +44,9 @@
 // the all-done test runs once per 32-entry batch
 #define SK_FWD_BATCH_DONE 1
 #endif
+#ifndef SK_FWD_PTR_TABLE
+#define SK_FWD_PTR_TABLE 1  // exp table base pinned in a register
+#endif
 #ifndef SK_FWD_PIX16
 #define SK_FWD_PIX16 2
 #endif
@@ -205,7 +208,11 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
   __shared__ float s_exp[kNegExpTable];
   stage_neg_exp_table(s_exp);
   __syncthreads();
+#if SK_FWD_PTR_TABLE
+  const SmemPinnedTable tab(s_exp);
+#else
   const SmemTable tab(s_exp);
+#endif
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
