@@ -81,6 +81,9 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 #ifndef SK_BWD_BRANCHLESS
 #define SK_BWD_BRANCHLESS 1  // measured: -6.8% K8 time
 #endif
+#ifndef SK_BWD_PIN
+#define SK_BWD_PIN 1
+#endif
 #ifndef SK_BWD_UQ
 // 1: q in [0, q_cut] as one unsigned compare of (q + 0) bits (K6's test), and
 // the two near-threshold bands folded into one symmetric band around the
@@ -122,11 +125,50 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
   // two buffers of NT slots for the asynchronous gather (slot buf * NT + j);
   // the other paths use the first NT
   constexpr int NB = SK_BWD_ASYNC_GATHER ? 2 * NT : NT;
+#if SK_BWD_PIN
+  // the walk's four staged arrays in one block whose shared-window base is
+  // pinned in a register: the walk loads use it with immediate offsets
+  // (plain indexing rematerialised each array's base with an S2R of the
+  // cluster CTA id inside the loop)
+  struct alignas(16) Staged {
+    float4 xyq[NB];
+    float4 co[NB];
+    float4 rgb[NB];
+    uint32_t id[NB];
+  };
+  __shared__ Staged s_st;
+  float4(&s_xyq)[NB] = s_st.xyq;
+  float4(&s_co)[NB] = s_st.co;
+  float4(&s_rgb)[NB] = s_st.rgb;
+  uint32_t(&s_id)[NB] = s_st.id;
+  uint32_t st_base;
+  asm volatile("mov.u32 %0, %1;" : "=r"(st_base) : "r"((uint32_t)__cvta_generic_to_shared(&s_st)));
+  auto ld_f4 = [&](uint32_t off, int j) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(st_base + off + 16u * (uint32_t)j));
+    return v;
+  };
+  auto ld_xyq = [&](int j) { return ld_f4(0u, j); };
+  auto ld_co = [&](int j) { return ld_f4(16u * NB, j); };
+  auto ld_rgb = [&](int j) { return ld_f4(32u * NB, j); };
+  auto ld_id = [&](int j) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(st_base + 48u * NB + 4u * (uint32_t)j));
+    return v;
+  };
+#else
   __shared__ float4 s_xyq[NB];
   __shared__ float4 s_co[NB];
-  __shared__ uint32_t s_mask[WB::kWarps * kChunks];
   __shared__ float4 s_rgb[NB];
   __shared__ uint32_t s_id[NB];
+  auto ld_xyq = [&](int j) { return s_xyq[j]; };
+  auto ld_co = [&](int j) { return s_co[j]; };
+  auto ld_rgb = [&](int j) { return s_rgb[j]; };
+  auto ld_id = [&](int j) { return s_id[j]; };
+#endif
+  __shared__ uint32_t s_mask[WB::kWarps * kChunks];
   __shared__ float2 s_mu[SK_BWD_ASYNC_GATHER ? NB : 1];
   __shared__ int s_max_last;
   __shared__ float s_exp2[64];
@@ -178,8 +220,8 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
   // The 11 gradient partials of staged slot j (list position idx) over this
   // lane's pixels; returns whether one of them blended the entry.
   auto partials = [&](int j, int idx, float (&gv)[kBGradFields]) -> bool {
-    const float4 mq = s_xyq[j];
-    const float4 co = s_co[j];
+    const float4 mq = ld_xyq(j);
+    const float4 co = ld_co(j);
     float g_mu0 = 0.f, g_mu1 = 0.f, g_c00 = 0.f, g_c01 = 0.f, g_c11 = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f,
           g_op = 0.f, g_a0 = 0.f, g_a1 = 0.f;
     bool contrib = false;
@@ -214,7 +256,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
       ok = ok && !(alpha_c < kAlphaMin);
       contrib = contrib || ok;
       const float alpha = ok ? alpha_c : 0.0f;
-      const float4 c = s_rgb[j];
+      const float4 c = ld_rgb(j);
       const float one_m = 1.0f - alpha;
       const float inv_one_m = __fdividef(1.0f, one_m);
       const float t_before = T[k] * inv_one_m;
@@ -264,7 +306,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
       const float alpha = capped ? kAlphaCap : raw;
       if (alpha < kAlphaMin) continue;
       contrib = true;
-      const float4 c = s_rgb[j];
+      const float4 c = ld_rgb(j);
       const float one_m = 1.0f - alpha;
       const float inv_one_m = __fdividef(1.0f, one_m);  // tolerance path: MUFU reciprocal, two products
       const float t_before = T[k] * inv_one_m;
@@ -307,7 +349,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
       // few contributing lanes: each adds its own partials (one lane: they
       // are the warp sum), no shuffle reduction
       if (contrib) {
-        const uint32_t id = s_id[j];
+        const uint32_t id = ld_id(j);
 #pragma unroll
         for (int f = 0; f < kBGradFields; ++f) atomicAdd(&bgrads[(int64_t)f * gstride + id], gv0[f]);
       }
@@ -315,12 +357,12 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_BWD_MINB * 128 / (TS * TS / P
 #endif
     if (cb) {
       if (has_pend) {
-        reduce_scatter_2x11(pend, gv0, pend_id, s_id[j], true, bgrads, gstride);
+        reduce_scatter_2x11(pend, gv0, pend_id, ld_id(j), true, bgrads, gstride);
         has_pend = false;
       } else {
 #pragma unroll
         for (int f = 0; f < kBGradFields; ++f) pend[f] = gv0[f];
-        pend_id = s_id[j];
+        pend_id = ld_id(j);
         has_pend = true;
       }
     }
