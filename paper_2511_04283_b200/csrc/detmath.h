@@ -124,7 +124,22 @@ struct SmemTable {
     return v;
   }
 };
+// The same table with its shared-window base pinned in a register.
+struct SmemPinnedTable {
+  uint32_t base;
+  // the asm keeps the converted address in one register (otherwise it is
+  // rematerialised with an S2R of the cluster CTA id at every lookup)
+  __device__ explicit SmemPinnedTable(const float* s) {
+    asm volatile("mov.u32 %0, %1;" : "=r"(base) : "r"((uint32_t)__cvta_generic_to_shared(s)));
+  }
+  __device__ __forceinline__ float operator[](int j) const {
+    float v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(base + 4u * (uint32_t)j));
+    return v;
+  }
+};
 SK_HD float det_expf_core(float x, const SmemTable& table) { return det_expf_core_t(x, table); }
+SK_HD float det_expf_core(float x, const SmemPinnedTable& table) { return det_expf_core_t(x, table); }
 #endif
 
 SK_HD const float* exp2_table() {
@@ -162,6 +177,7 @@ SK_HD float det_expf_t(float x, const Tab& table) {
 SK_HD float det_expf(float x, const float* table = nullptr) { return det_expf_t(x, table ? table : exp2_table()); }
 #if defined(__CUDACC__)
 SK_HD float det_expf(float x, const SmemTable& table) { return det_expf_t(x, table); }
+SK_HD float det_expf(float x, const SmemPinnedTable& table) { return det_expf_t(x, table); }
 #endif
 
 // Natural log of a positive finite float. x = m 2^e with m in [sqrt(.5),
@@ -200,6 +216,7 @@ SK_HD float det_logf(float x) {
 SK_HD float det_sigmoidf(float x, const float* table = nullptr) { return 1.0f / (1.0f + det_expf(-x, table)); }
 #if defined(__CUDACC__)
 SK_HD float det_sigmoidf(float x, const SmemTable& table) { return 1.0f / (1.0f + det_expf(-x, table)); }
+SK_HD float det_sigmoidf(float x, const SmemPinnedTable& table) { return 1.0f / (1.0f + det_expf(-x, table)); }
 #endif
 
 #if defined(__CUDACC__)
@@ -217,20 +234,6 @@ __device__ __forceinline__ void stage_neg_exp_table(float* s_table) {
     s_table[m] = bits_to_f32(kExp2TableDev[j] + ((uint32_t)e << 23));
   }
 }
-// The same table with its shared-window base pinned in a register.
-struct SmemPinnedTable {
-  uint32_t base;
-  // the asm keeps the converted address in one register (otherwise it is
-  // rematerialised with an S2R of the cluster CTA id at every lookup)
-  __device__ explicit SmemPinnedTable(const float* s) {
-    asm volatile("mov.u32 %0, %1;" : "=r"(base) : "r"((uint32_t)__cvta_generic_to_shared(s)));
-  }
-  __device__ __forceinline__ float operator[](int j) const {
-    float v;
-    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(base + 4u * (uint32_t)j));
-    return v;
-  }
-};
 template <class Tab>
 __device__ __forceinline__ float det_expf_neg(float x, const Tab& neg_table) {
   const float kf = det_floorf(rn_add(rn_mul(x, 92.33248261689366f), 0.5f));  // 64 / ln2

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
                                                          uint32_t* __restrict__ err) {
   __shared__ float s_exp2[64];
   stage_exp2_table(s_exp2);
-  const SmemTable tab(s_exp2);
+  const SmemPinnedTable tab(s_exp2);
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
   __shared__ uint32_t s_id[COUNT ? B : 1];
   __shared__ float s_exp[kNegExpTable];
   stage_neg_exp_table(s_exp);  // published by the first __syncthreads_count below
-  const SmemTable tab(s_exp);
+  const SmemPinnedTable tab(s_exp);
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
