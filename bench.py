@@ -34,6 +34,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0
+METRIC = "train iters/s (1M Gaussians, 1080p)"
+DATA = ("synthetic (numpy RNG, reference generate_synthetic distribution; GT rendered and quantised to 8 bits; "
+        "trained scene = GT with perturbed positions)")
 
 
 def parse_args():
@@ -50,6 +53,7 @@ def parse_args():
     ap.add_argument("--workload", choices=["train", "event"], default="train",
                     help="train: config-2 training iteration (default); event: config-3 density event")
     ap.add_argument("--views", type=int, default=64, help="event workload: scored views (K)")
+    ap.add_argument("--no-event", action="store_true", help="train workload: skip the config-3 event sub-object")
     return ap.parse_args()
 
 
@@ -133,15 +137,22 @@ def dist_env():
     return world, rank, local
 
 
-def bench_config(args):
+def bench_config(args, world):
+    """The `config` object of both arms (identical by construction)."""
     return {"workload": "config2: synthetic 1M-Gaussian scene (SH deg 3), 1920x1080 ring view per rank, "
                         "train iteration K1-K10 (fwd+loss+bwd+Adam)",
             "n_gaussians": args.n, "width": args.width, "height": args.height, "sh_degree": 3,
-            "views_per_step": None, "l2": "inputs larger than L2 (944 MB params+moments+grads state per step)"}
+            "views_per_step": world,
+            "start_state": "timed steps are training iterations 1..K from the perturbed initial scene with fresh "
+                           "Adam state (warm-up steps run first, then scene and optimizer are restored)",
+            "l2": "inputs larger than L2 (944 MB params+moments+grads state per step)",
+            "parallelism": f"view-parallel dp{world} (gradient all-reduce)" if world > 1 else "single device"}
 
 
-def train_config(sk, iterations=30000):
-    cfg = sk.default_config()
+def train_config(default_config, iterations=30000):
+    """TrainConfig of the bench step; `default_config` is the arm's own
+    (sk.default_config for ours, orc.default_config for the reference)."""
+    cfg = default_config()
     cfg.iterations = iterations
     cfg.densify_from = cfg.densify_until = 1 << 30  # the bench step has no density events
     return cfg
@@ -152,40 +163,56 @@ def train_config(sk, iterations=30000):
 # ---------------------------------------------------------------------------
 
 def run_reference(args, world, rank):
+    """The reference's CPU implementation of the path (the oracle restatement,
+    oracle/; the reference itself cannot be built here)
+    on this box's host cores, on our arm's config, metric and unit. Nothing of
+    the product (libsplatkit_b200.so) is loaded in this process."""
     if rank != 0:
         return
-    import paper_2511_04283_b200.synthetic as syn
+    import paper_2511_04283_b200.synthetic as syn  # pure numpy; never loads the CUDA library
     from oracle import oracle as orc
-    import paper_2511_04283_b200 as sk  # structs / config only; no GPU calls
     cores = os.cpu_count() or 1
     gt = syn.gaussians(args.n, 1, 3)
-    cam = syn.ring_camera(0, 64, args.width, args.height)
+    cam = syn.ring_camera(0, 64, args.width, args.height, camera_fn=orc.camera)
     r = orc.render_scene(gt, 3, cam, workers=cores, values_cap=64 * args.n)
     gt8 = syn.quantize_u8(r.image)
     extent = syn.ring_extent()
     p = syn.perturb_positions(gt, 0.02 * extent, 2)
-    cfg = train_config(sk)
+    del gt, r
+    cfg = train_config(orc.default_config)
     cfg.workers = cores
+    budget_s = float(os.environ.get("SK_REF_BUDGET_S", "150"))
+    # warm-up on a throw-away trainer, then iterations 1..K from the initial
+    # scene (the same start state as our arm); bounded by a time budget
+    warm = orc.ViewTrainer(p, 3, cam, gt8, cfg, extent)
+    wsecs = [warm.run(1)[1] for _ in range(args.warmup)]
+    del warm
     tr = orc.ViewTrainer(p, 3, cam, gt8, cfg, extent)
-    # Bounded sample: one warm-up iteration, then timed iterations until either
-    # --steps or a ~60 s budget is reached (each iteration is a full config-2
-    # training iteration, ~2.5 s on 16 host threads).
-    budget_s = float(os.environ.get("SK_REF_BUDGET_S", "60"))
-    for _ in range(min(args.warmup, 1)):
-        tr.run(1)
     secs = []
-    while len(secs) < args.steps and (not secs or sum(secs) < budget_s):
-        _, s = tr.run(1)
-        secs.append(s)
+    while len(secs) < args.steps and (not secs or sum(secs) + sum(wsecs) < budget_s):
+        secs.append(tr.run(1)[1])
+    del tr
     ms = 1000.0 * sum(secs) / len(secs)
     value = 1000.0 / ms
-    line = {"impl": "reference", "metric": "train iters/s (1M Gaussians, 1080p)", "value": value,
-            "unit": "iter/s", "n_gpus": world, "steps": len(secs), "warmup": min(args.warmup, 1), "ms_per_step": ms,
+    # the reference's bit-reproducible mode (workers=1, proj/README.md:75-78):
+    # one iteration from the initial scene
+    w1 = None
+    if not os.environ.get("SK_REF_NO_W1"):
+        cfg1 = train_config(orc.default_config)
+        cfg1.workers = 1
+        t1 = orc.ViewTrainer(p, 3, cam, gt8, cfg1, extent)
+        s1 = t1.run(1)[1]
+        w1 = {"value": 1.0 / s1, "unit": "iter/s", "cores": 1, "kind": "port",
+              "sample": "1 full config-2 training iteration (iteration 1) at workers=1"}
+    line = {"impl": "reference", "metric": METRIC, "value": value,
+            "unit": "iter/s", "n_gpus": world, "steps": len(secs), "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (numpy RNG, reference distribution)", "config": bench_config(args),
+            "data": DATA, "config": bench_config(args, world),
             "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cores, "kind": "port",
-                             "sample": f"{len(secs)} full config-2 training iterations after 1 warm-up "
-                                       f"(oracle, workers={cores}; bounded to ~{budget_s:.0f} s)"},
+                             "sample": f"{len(secs)} full config-2 training iterations (1..{len(secs)}) after "
+                                       f"{args.warmup} warm-up iterations (oracle, workers={cores}; bounded to "
+                                       f"~{budget_s:.0f} s)"},
+            "cpu_baseline_workers1": w1,
             "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -273,7 +300,7 @@ def run_ours(args, world, rank, local):
     gt8 = syn.render_gt_u8(ctx, gt_params, 3, cam)
     params = syn.perturb_positions(gt_params, 0.02 * extent, 2)
     del gt_params
-    cfg = train_config(sk)
+    cfg = train_config(sk.default_config)
     scene = ctx.scene(params, 3)
     data = sk.Dataset(ctx, [cam], [gt8], [0], extent)
     trainer = sk.Trainer(ctx, scene, data, cfg)
@@ -286,11 +313,19 @@ def run_ours(args, world, rank, local):
         if dist is not None:
             dist.barrier()
 
+    def restore():
+        """The fixed start state of every timed region: the perturbed initial
+        scene, fresh Adam moments / step counters and score table
+        (sk_scene_upload resets both), iteration counter 0."""
+        ctx.check(ctx._lib.sk_scene_upload(ctx.h, scene.h, sk._p(params), sk.C.c_int64(args.n)))
+        trainer.set_iteration(0)
+
     for _ in range(args.warmup):
         trainer.run(1)
+    restore()
     torch.cuda.synchronize()
 
-    # ---- device-resident timed region ------------------------------------
+    # ---- device-resident timed region: iterations 1..K --------------------
     ctx.check(ctx._lib.sk_ctx_reset_timing(ctx.h))
     ctx.check(ctx._lib.sk_ctx_enable_timing(ctx.h, 1))
     launches0 = ctx.launch_count()
@@ -320,23 +355,24 @@ def run_ours(args, world, rank, local):
         ms = float(t.item())
     if args.profile:
         if rank == 0:
-            print(json.dumps({"profile": True, "ms_per_step": ms, "phase_ms": phase_avg}), flush=True)
+            print(json.dumps({"profile": True, "ms_per_step": ms, "phase_ms": phase_avg,
+                              "tile_pairs_last": rows[-1]["tile_pairs"] if rows else None}), flush=True)
         return
 
     # ---- end-to-end through the C ABI with host buffers -----------------
     pinned = torch.empty(gt8.size, dtype=torch.uint8, pin_memory=True)
     gt_host = pinned.numpy().reshape(gt8.shape)
     gt_host[...] = gt8
-    # Same training trajectory as the device-timed run (the per-step workload
-    # drifts as the scene trains): restart from the initial scene and step 1.
+    # Same start state and trajectory as the device-timed run: warm-up steps
+    # (the e2e frame allocates its buffers on first use), then restore and
+    # time iterations 1..K.
     e2e_scene = scene
-    ctx.check(ctx._lib.sk_scene_upload(ctx.h, scene.h, sk._p(params), sk.C.c_int64(args.n)))
     pipe = sk.HostStepPipeline(ctx, comm=comm)
-    it0 = 0
-    for k in range(args.warmup):  # the e2e frame allocates its buffers on first use
-        pipe.step(e2e_scene, cam, gt_host, cfg, extent, it0 + 1 + k)
+    for k in range(args.warmup):
+        pipe.step(e2e_scene, cam, gt_host, cfg, extent, 1 + k)
     pipe.flush()
-    it0 += args.warmup
+    restore()
+    it0 = 0
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -359,21 +395,34 @@ def run_ours(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # ---- workload units of the timed steps --------------------
+    # visible Gaussians and the reference loop's visited / contributing
+    # pixel-Gaussian evaluations, measured at the start state (iteration 1)
+    # and at the end state (after iteration K) and averaged; pairs = the
+    # mean over the timed steps' own counts.
+    def units():
+        prj = ctx.project_scene(scene, cam)
+        ctx.build_tile_grid()
+        ctx.blend_forward()
+        return (int(prj.visible.sum()),) + tuple(ctx.pge_counts())
+    end_units = units()
+    restore()
+    start_units = units()
+    visible, visited, contribs = (int(round((a + b) / 2)) for a, b in zip(start_units, end_units))
+    pairs = int(round(sum(r["tile_pairs"] for r in rows) / len(rows))) if rows else 0
+
+    # ---- the paper's contribution: one config-3 density event ---------------
+    event = None
+    if not args.no_event:
+        event = measure_event(ctx, sk, torch, dist, rank, args.n, args.views, args.width, args.height, reps=3,
+                              warm=1)
+
     if rank != 0:
         return
     # ---- roofline of the dominant kernel ------------------------------------
     hbm_peak, sm_max, peak_kind = measured_peaks()
-    prj = ctx.get_projected()
-    visible = int(prj.visible.sum())
-    pairs = int(rows[-1]["tile_pairs"]) if rows else 0
     pixels = args.width * args.height
     tiles = ((args.width + 15) // 16) * ((args.height + 15) // 16)
-    # workload units of this view: the reference loop's visited
-    # and contributing pixel-Gaussian evaluations
-    ctx.project_scene(scene, cam)
-    ctx.build_tile_grid()
-    ctx.blend_forward()
-    visited, contribs = ctx.pge_counts()
     clocks = clock.summary()
     # FP32 SIMT roof: 148 SMs x 128 lanes x 2 flop (FFMA) x SM clock. The SM
     # clock is the max clock (MEASURED_PEAKS sm_max_mhz), which the run held.
@@ -430,7 +479,7 @@ def run_ours(args, world, rank, local):
         cpu = cpu_baseline(args, params, cam, gt8, extent)
 
     line = {
-        "metric": "train iters/s (1M Gaussians, 1080p)",
+        "metric": METRIC,
         "value": world * 1000.0 / ms,
         "unit": "iter/s",
         "n_gpus": world,
@@ -441,15 +490,17 @@ def run_ours(args, world, rank, local):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": "synthetic (numpy RNG, reference generate_synthetic distribution; GT rendered on GPU, 8-bit)",
-        "config": dict(bench_config(args), views_per_step=world,
-                       parallelism=f"view-parallel dp{world} (NCCL grad all-reduce)" if world > 1 else "single GPU"),
+        "data": DATA,
+        "config": bench_config(args, world),
         # raster forward = K1..K6, raster backward = K8 + K9 (pixels / s)
         "raster_fwd_mpix_s": pixels / ((phase_avg[0] + phase_avg[1] + phase_avg[2]) * 1e-3) / 1e6,
         "raster_bwd_mpix_s": pixels / ((phase_avg[4] + phase_avg[5]) * 1e-3) / 1e6,
         "phase_ms": dict(zip(PHASES, [round(x, 4) for x in phase_avg])),
         "tile_pairs": pairs,
         "visible": visible,
+        "workload_units": {"start": dict(zip(("visible", "pge_visited", "pge_contributing"), start_units)),
+                           "end": dict(zip(("visible", "pge_visited", "pge_contributing"), end_units)),
+                           "tile_pairs_first_last": [rows[0]["tile_pairs"], rows[-1]["tile_pairs"]] if rows else None},
         "loss_last": rows[-1]["loss"] if rows else None,
         "roofline": roofline,
         "roofline_fp32": roofline_fp32,
@@ -459,6 +510,7 @@ def run_ours(args, world, rank, local):
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": cpu,
+        "event": event,
     }
     print(json.dumps(line), flush=True)
 
@@ -475,22 +527,22 @@ class _Null:
 
 
 def cpu_baseline(args, params, cam, gt8, extent):
-    """The restated reference (oracle) on the host cores, one full config-2
-    iteration as the bounded sample."""
+    """The restated reference (oracle) on the host cores: one warm-up
+    iteration on a throw-away trainer, then iterations 1..k from the initial
+    scene (our arm's start state), bounded to ~12 s."""
     try:
         from oracle import oracle as orc
-        import paper_2511_04283_b200 as sk
         cores = os.cpu_count() or 1
-        cfg = train_config(sk)
+        cfg = train_config(orc.default_config)
         cfg.workers = cores
+        orc.ViewTrainer(params, 3, cam, gt8, cfg, extent).run(1)  # warm-up (allocations, page-in)
         tr = orc.ViewTrainer(params, 3, cam, gt8, cfg, extent)
-        tr.run(1)  # warm-up (allocations)
         secs = []
         while not secs or (sum(secs) < 12.0 and len(secs) < 8):
             secs.append(tr.run(1)[1])
         return {"value": len(secs) / sum(secs), "unit": "iter/s", "cores": cores, "kind": "port",
-                "sample": f"{len(secs)} full config-2 training iterations (1M Gaussians, 1920x1080) after 1 "
-                          f"warm-up, oracle workers={cores}"}
+                "sample": f"{len(secs)} full config-2 training iterations (1..{len(secs)}, 1M Gaussians, 1920x1080) "
+                          f"from the initial scene, oracle workers={cores}"}
     except Exception as e:  # the baseline is reported, never required
         return {"value": None, "unit": "iter/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
 
@@ -499,36 +551,26 @@ def cpu_baseline(args, params, cam, gt8, extent):
 # config 3: the multi-view importance pass + densify / prune compaction
 # ---------------------------------------------------------------------------
 
-def run_event(args, world, rank, local):
-    """BASELINE config 3: 1M Gaussians scored over K=64 1080p views
-    (K6 + K11 + K12 per view, K13 scores), then K14 selection and K15
-    compaction, through Trainer::density_event. Scene: the GT of the GPU
-    synthetic generator padded to SH degree 3, with 20% of the Gaussians' DC
-    and opacity perturbed (seed 3); accumulators synthetic (grad ~ U(0, 6e-4),
-    views_seen in [1, 10]). Timed at iteration 1000 (densify + prune) and
-    20000 (late prune); the scene is restored before every timed event."""
-    import torch
-
-    import paper_2511_04283_b200 as sk
-
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    ctx = sk.Context(local)
-    stream = torch.cuda.current_stream()
-    ctx.check(ctx._lib.sk_ctx_set_stream(ctx.h, sk.C.c_void_p(stream.cuda_stream)))
-    n, k = args.n, args.views
+def measure_event(ctx, sk, torch, dist, rank, n, k, width, height, reps, warm):
+    """BASELINE config 3: n Gaussians scored over K views
+    (K1-K6 + K11 + K7-fwd + K12 per view, K13 scores), then K14 selection and
+    K15 compaction, through Trainer::density_event (trainer.hpp:177-243).
+    Scene: the GT of the GPU synthetic generator padded to SH degree 3, with
+    20% of the Gaussians' DC and opacity perturbed (seed 3); accumulators
+    synthetic (grad ~ U(0, 6e-4), views_seen in [1, 10]). Timed at iteration
+    1000 (densify + prune) and 20000 (late prune); the scene and table are
+    restored before every event. Returns the event dict (rank 0) or None."""
     t0 = time.perf_counter()
-    ds, gt, xyz, rgb = sk.Dataset.synthetic(ctx, n_gaussians=n, n_views=k, width=args.width, height=args.height,
-                                            seed=1, scale_mult=(500.0 / n) ** (1.0 / 3.0) if n >= 100_000 else 1.0,
-                                            focal=1.1 * args.height * 2.6)
+    ds, gt, _, _ = sk.Dataset.synthetic(ctx, n_gaussians=n, n_views=k, width=width, height=height, seed=1,
+                                        scale_mult=(500.0 / n) ** (1.0 / 3.0) if n >= 100_000 else 1.0,
+                                        focal=1.1 * height * 2.6)
     gen_s = time.perf_counter() - t0
     ds.set_train_indices(np.arange(k))  # K = all views
     p1 = gt.download()
+    gt.close()
     p = np.zeros((sk.n_components(3), n), np.float32)
     p[: p1.shape[0]] = p1
+    del p1
     rng = np.random.default_rng(3)
     sel = rng.random(n) < 0.2
     p[10, sel] += rng.normal(0.0, 1.0, int(sel.sum())).astype(np.float32)
@@ -538,22 +580,27 @@ def run_event(args, world, rank, local):
     absg = rng.uniform(0, 6e-4, n).astype(np.float32)
     g3 = rng.normal(0, 1e-4, (n, 3)).astype(np.float32)
     rad = rng.uniform(0, 30, n).astype(np.float32)
-    cfg = train_config(sk)
+    cfg = train_config(sk.default_config)
     cfg.k = k
     scene = ctx.scene(p, 3, capacity=2 * n)
     tr = sk.Trainer(ctx, scene, ds, cfg)
-    comm = None
-    if world > 1:
-        comm = sk.Comm.from_torch(ctx, dist, rank, world)
-        tr.set_comm(comm)
+    if dist is not None:
+        tr.set_comm(sk.Comm.from_torch(ctx, dist, rank, dist.get_world_size()))
 
     def restore():
         ctx.check(ctx._lib.sk_scene_upload(ctx.h, scene.h, sk._p(p), sk.C.c_int64(n)))
         scene.set_score_table(grad_norm_acc=grad * vs, abs_grad_acc=absg * vs, grad3d_acc=g3, views_seen=vs,
                               max_radius2d=rad)
 
+    def phases():
+        ms = (sk.C.c_double * 4)()
+        cnt = sk.C.c_int64()
+        ctx._lib.sk_ctx_get_event_timing(ctx.h, ms, sk.C.byref(cnt))
+        return [ms[i] / max(1, cnt.value) for i in range(4)]
+
     def timed(iteration, densify, prune):
         restore()
+        ctx.check(ctx._lib.sk_ctx_reset_timing(ctx.h))
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
@@ -565,34 +612,22 @@ def run_event(args, world, rank, local):
             t = torch.tensor([ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        return ms, scene.size
+        return ms, scene.size, phases()
 
-    def phases():
-        ms = (sk.C.c_double * 4)()
-        cnt = sk.C.c_int64()
-        ctx._lib.sk_ctx_get_event_timing(ctx.h, ms, sk.C.byref(cnt))
-        return [ms[i] / max(1, cnt.value) for i in range(4)]
-
-    for _ in range(max(1, min(args.warmup, 2))):
-        timed(1000, True, True)
-    reps = max(1, min(args.steps, 5))
     ctx.check(ctx._lib.sk_ctx_enable_timing(ctx.h, 1))
-
-    def timed_with_phases(iteration, densify, prune):
-        ctx.check(ctx._lib.sk_ctx_reset_timing(ctx.h))
-        ms, size = timed(iteration, densify, prune)
-        return ms, size, phases()
-
-    early = [timed_with_phases(1000, True, True) for _ in range(reps)]
-    late = [timed_with_phases(20000, False, True) for _ in range(reps)]
+    for _ in range(warm):
+        timed(1000, True, True)
+    early = [timed(1000, True, True) for _ in range(reps)]
+    late = [timed(20000, False, True) for _ in range(reps)]
     ctx.check(ctx._lib.sk_ctx_enable_timing(ctx.h, 0))
+    tr.close()
+    scene.close()
+    ds.close()
     if rank != 0:
-        return
+        return None
     # the phase split reported is that of the median event (by wall time)
     e_med = sorted(early, key=lambda x: x[0])[len(early) // 2]
     l_med = sorted(late, key=lambda x: x[0])[len(late) // 2]
-    e_ms, ph_early = e_med[0], e_med[2]
-    l_ms, ph_late = l_med[0], l_med[2]
     hbm_peak, _, peak_kind = measured_peaks()
     comps = sk.n_components(3)
 
@@ -610,21 +645,41 @@ def run_event(args, world, rank, local):
                 "K14+K15": {"algorithmic_MB": k1415 / 1e6, "GB/s": k1415 / t1415 / 1e9,
                             "frac": k1415 / t1415 / 1e9 / hbm_peak},
                 "view_ms": ph[0] / k, "peak_GB/s": hbm_peak, "peak_kind": peak_kind}
-    line = {
-        "metric": "density event ms (config 3: 1M Gaussians, 64 views 1080p, score + select + compact)",
-        "value": e_ms, "unit": "ms/event", "n_gpus": world, "steps": reps, "warmup": max(1, min(args.warmup, 2)),
-        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (GPU generator, reference Rng draw order); scene restored before each event",
+    return {
+        "metric": f"density event ms (config 3: {n} Gaussians, {k} views {width}x{height}, score + select + compact)",
+        "value": e_med[0], "unit": "ms/event", "higher_is_better": False, "reps": reps, "warmup": warm,
         "config": {"workload": "config3: multi-view importance pass over K views + densify/prune compaction",
-                   "n_gaussians": n, "views": k, "width": args.width, "height": args.height,
+                   "n_gaussians": n, "views": k, "width": width, "height": height,
                    "timing": "wall clock around Trainer::density_event with device syncs, median; phase split "
-                  "(CUDA events) of that median event"},
-        "early_event_ms": e_ms, "late_event_ms": l_ms,
-        "views_scored_per_s": k / (e_ms * 1e-3),
-        "n_after_early": early[-1][1], "n_after_late": late[-1][1],
-        "early": event_roofline(ph_early, early[-1][1]), "late": event_roofline(ph_late, late[-1][1]),
+                             "(CUDA events) of that median event"},
+        "early_event_ms": e_med[0], "late_event_ms": l_med[0],
+        "views_scored_per_s": k / (e_med[0] * 1e-3),
+        "n_after_early": e_med[1], "n_after_late": l_med[1],
+        "early": event_roofline(e_med[2], e_med[1]), "late": event_roofline(l_med[2], l_med[1]),
         "generator_s": gen_s,
     }
+
+
+def run_event(args, world, rank, local):
+    """`--workload event`: the config-3 event alone as the JSON line."""
+    import torch
+
+    import paper_2511_04283_b200 as sk
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = sk.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.check(ctx._lib.sk_ctx_set_stream(ctx.h, sk.C.c_void_p(stream.cuda_stream)))
+    ev = measure_event(ctx, sk, torch, dist, rank, args.n, args.views, args.width, args.height,
+                       reps=max(1, min(args.steps, 5)), warm=max(1, min(args.warmup, 2)))
+    if rank != 0:
+        return
+    line = dict(ev, n_gpus=world, steps=ev["reps"], scaling="strong", vs_baseline=None, dtype="f32",
+                data="synthetic (GPU generator, reference Rng draw order); scene restored before each event")
     print(json.dumps(line), flush=True)
 
 

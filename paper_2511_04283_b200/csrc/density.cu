@@ -602,6 +602,10 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
   s->n = new_n;
   ensure_optimizer_state(ctx, s);
   reset_score_table(ctx, s);
+  // clear_rest() (trainer.hpp:242): every event clears the lazy SH-rest
+  // accumulator, also when the compaction leaves the size unchanged (the
+  // indices moved, or nothing was removed).
+  s->rest_n = -1;
   trace_point(ctx, "compact: state reset");
   return new_n;
 }

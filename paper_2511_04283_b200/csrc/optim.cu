@@ -331,8 +331,12 @@ template <int DEG>
 __global__ void __launch_bounds__(kPbThreads, SK_K9_MINB) project_bwd_kernel(
     const float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ radius,
     const float4* __restrict__ conic4, const float* __restrict__ bg, int64_t gstride, float* __restrict__ grads,
-    Stats st, bool do_stats) {
+    Stats st, bool do_stats, const uint32_t* __restrict__ err) {
   constexpr int NC = 11 + 3 * (DEG + 1) * (DEG + 1);
+  // A step whose K1 raised a device error (covariance_3d's throw,
+  // scene.hpp:89-92) mutates no persistent state: the reference throws
+  // before any update. The word is block-uniform.
+  if (__ldg(err)) return;
   __shared__ float s_grad[NC * kPbThreads];
   __shared__ float s_exp2[64];
   stage_exp2_table(s_exp2);
@@ -375,7 +379,9 @@ __global__ void __launch_bounds__(kPbThreads, SK_K9_MINB) project_bwd_kernel(
 constexpr int kAdamThreads = 256;
 __global__ void __launch_bounds__(kAdamThreads) adam_kernel(float* __restrict__ params, const float* __restrict__ grads,
                                                             float* __restrict__ am, float* __restrict__ av,
-                                                            int64_t stride, int64_t n, AdamParams ap) {
+                                                            int64_t stride, int64_t n, AdamParams ap,
+                                                            const uint32_t* __restrict__ err) {
+  if (__ldg(err)) return;  // see project_bwd_kernel
   const int c = blockIdx.y;
   const int gidx = comp_group(c);
   if (!ap.active[gidx]) return;
@@ -439,7 +445,8 @@ void launch_pb(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stats) {
   auto go = [&](auto kern) {
     kern<<<grid, kPbThreads, 0, ctx->stream>>>(s->params.as<float>(), s->capacity, s->n, cp, f->radius.as<float>(),
                                                f->conic4.as<float4>(), f->bgrads.as<float>(), f->n,
-                                               s->grads.as<float>(), make_stats(s), do_stats);
+                                               s->grads.as<float>(), make_stats(s), do_stats,
+                                               ctx->err_word.as<uint32_t>());
   };
   switch (s->sh_degree) {
     case 0: go(project_bwd_kernel<0>); break;
@@ -508,13 +515,14 @@ void launch_adam(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float posit
   const dim3 grid((unsigned)std::max<int64_t>(1, std::min(need, per_comp)), (unsigned)s->comps);
   adam_kernel<<<grid, kAdamThreads, 0, ctx->stream>>>(s->params.as<float>(), s->grads.as<float>(),
                                                       s->adam_m.as<float>(), s->adam_v.as<float>(), s->capacity,
-                                                      s->n, ap);
+                                                      s->n, ap, ctx->err_word.as<uint32_t>());
   note_launch();
   SK_CUDA(cudaGetLastError());
 }
 
 __global__ void accumulate_rest_kernel(float* __restrict__ acc, const float* __restrict__ g, int64_t stride,
-                                       int64_t n, int c0, int c1) {
+                                       int64_t n, int c0, int c1, const uint32_t* __restrict__ err) {
+  if (__ldg(err)) return;  // see project_bwd_kernel
   const int c = c0 + blockIdx.y;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t o = (int64_t)c * stride + i;
@@ -552,7 +560,7 @@ void lazy_sh_rest(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, bool due) 
   }
   const dim3 grid((unsigned)std::min<int64_t>((s->n + 255) / 256, 64), (unsigned)(c1 - c0));
   accumulate_rest_kernel<<<grid, 256, 0, ctx->stream>>>(s->rest_accum.as<float>(), s->grads.as<float>(), s->capacity,
-                                                        s->n, c0, c1);
+                                                        s->n, c0, c1, ctx->err_word.as<uint32_t>());
   note_launch();
   SK_CUDA(cudaGetLastError());
   if (!due) return;
@@ -567,7 +575,7 @@ void lazy_sh_rest(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, bool due) 
   const dim3 agrid((unsigned)std::max<int64_t>(1, std::min(need, per_comp)), (unsigned)s->comps);
   adam_kernel<<<agrid, kAdamThreads, 0, ctx->stream>>>(s->params.as<float>(), s->rest_accum.as<float>(),
                                                        s->adam_m.as<float>(), s->adam_v.as<float>(), s->capacity,
-                                                       s->n, ap);
+                                                       s->n, ap, ctx->err_word.as<uint32_t>());
   note_launch();
   SK_CUDA(cudaGetLastError());
   SK_CUDA(cudaMemsetAsync(s->rest_accum.ptr, 0, bytes, ctx->stream));

@@ -58,9 +58,13 @@ def look_at(eye, target=(0.0, 0.0, 0.0), up=(0.0, 0.0, 1.0)) -> np.ndarray:
     return m
 
 
-def ring_camera(view: int, n_views: int, width: int, height: int, focal: float | None = None):
-    """Camera `view` of the reference ring (radius 2.4, height 1.0, look-at origin)."""
-    from . import camera
+def ring_camera(view: int, n_views: int, width: int, height: int, focal: float | None = None, camera_fn=None):
+    """Camera `view` of the reference ring (radius 2.4, height 1.0, look-at origin).
+    camera_fn builds the struct (default: this package's sk_camera; the
+    benchmark's reference arm passes the oracle's)."""
+    if camera_fn is None:
+        from . import camera as camera_fn
+    camera = camera_fn
     angle = 2.0 * math.pi * view / n_views
     eye = (2.4 * math.cos(angle), 2.4 * math.sin(angle), 1.0)
     f = focal if focal is not None else 1.1 * height * 2.6

@@ -67,3 +67,31 @@ def rel_err_vec(a, b, floor_frac=1e-3):
     b = np.asarray(b, np.float64)
     floor = max(floor_frac * np.abs(b).max(), 1e-12)
     return np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)
+
+
+def unfloored_report(name, got, ref, floor_frac=1e-3):
+    """Distribution of the elementwise relative error WITHOUT a floor
+    (|a-b| / max(|a|, |b|), elements where both are exactly zero excluded),
+    next to the floored maximum the assertions use. Appended as one JSON line
+    to $SK_PARITY_REPORT when that is set (the round's parity evidence)."""
+    import json
+    import os
+    a = np.asarray(got, np.float64).ravel()
+    b = np.asarray(ref, np.float64).ravel()
+    den = np.maximum(np.abs(a), np.abs(b))
+    nz = den > 0
+    e = np.abs(a - b)[nz] / den[nz]
+    rep = {"name": name, "elements": int(a.size), "nonzero": int(nz.sum()),
+           "floored_max": float(rel_err_vec(a, b, floor_frac).max()) if a.size else 0.0,
+           "unfloored_p50": float(np.percentile(e, 50)) if e.size else 0.0,
+           "unfloored_p99": float(np.percentile(e, 99)) if e.size else 0.0,
+           "unfloored_p999": float(np.percentile(e, 99.9)) if e.size else 0.0,
+           "unfloored_max": float(e.max()) if e.size else 0.0,
+           "frac_unfloored_gt_1e-3": float((e > 1e-3).mean()) if e.size else 0.0,
+           "max_abs_err": float(np.abs(a - b).max()) if a.size else 0.0,
+           "max_abs_ref": float(np.abs(b).max()) if b.size else 0.0}
+    path = os.environ.get("SK_PARITY_REPORT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rep) + "\n")
+    return rep
