@@ -410,6 +410,24 @@ int sk_trainer_event(const sk_trainer* t, int e, int32_t* header, uint8_t* clone
 typedef struct sk_comm sk_comm;
 int sk_comm_unique_id(uint8_t* id /* [SK_COMM_ID_BYTES] */);
 int sk_comm_create(sk_ctx* ctx, const uint8_t* id, int nranks, int rank, sk_comm** out);
+/* Host-callback collectives: the library stages its device buffers through
+ * pinned host memory and calls these (e.g. torch.distributed over gloo, MPI),
+ * so the same C1 / C2 / C3 code runs without NCCL (and with several ranks on
+ * one GPU). Buffers are host pointers; dtype SK_DT_*, op SK_OP_*; each
+ * returns 0 on success. reduce_scatter: send holds world * count elements
+ * (rank-major), recv gets this rank's reduced count; all_gather: send holds
+ * count elements, recv world * count (rank-major). */
+#define SK_DT_F32 0
+#define SK_DT_I32 1
+#define SK_OP_SUM 0
+#define SK_OP_MAX 1
+typedef struct sk_comm_host_ops {
+  void* user;
+  int (*all_reduce)(void* user, void* buf, int64_t count, int dtype, int op);
+  int (*reduce_scatter)(void* user, const void* send, void* recv, int64_t count, int dtype, int op);
+  int (*all_gather)(void* user, const void* send, void* recv, int64_t count, int dtype);
+} sk_comm_host_ops;
+int sk_comm_create_host(sk_ctx* ctx, int nranks, int rank, const sk_comm_host_ops* ops, sk_comm** out);
 int sk_comm_destroy(sk_comm* comm);
 int sk_comm_rank(const sk_comm* comm, int* rank, int* world);
 int sk_trainer_set_comm(sk_trainer* t, sk_comm* comm);

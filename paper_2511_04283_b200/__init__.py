@@ -971,6 +971,64 @@ class Comm:
             pass
 
 
+_AR = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int)
+_RS = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int)
+_AG = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int)
+
+
+class SkCommHostOps(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("all_reduce", _AR), ("reduce_scatter", _RS), ("all_gather", _AG)]
+
+
+class HostComm(Comm):
+    """sk_comm over torch.distributed collectives on host memory
+    (sk_comm_create_host): the library's own C1 / C2 / C3 code with any
+    torch.distributed backend (gloo on CPU; several ranks may share one GPU,
+    which NCCL refuses)."""
+
+    def __init__(self, ctx: Context, dist, rank: int, world: int):
+        import torch
+        self.ctx = ctx
+        self.rank, self.world = rank, world
+
+        def view(ptr, count, dtype):
+            ct = C.c_float if dtype == 0 else C.c_int32
+            return torch.from_numpy(np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(count,)))
+
+        def op_of(op):
+            return dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX
+
+        def all_reduce(_, buf, count, dtype, op):
+            try:
+                dist.all_reduce(view(buf, count, dtype), op=op_of(op))
+                return 0
+            except Exception:
+                return 1
+
+        def reduce_scatter(_, send, recv, count, dtype, op):
+            try:
+                t = view(send, count * world, dtype)
+                dist.all_reduce(t, op=op_of(op))  # gloo has no reduce_scatter
+                view(recv, count, dtype).copy_(t[rank * count:(rank + 1) * count])
+                return 0
+            except Exception:
+                return 1
+
+        def all_gather(_, send, recv, count, dtype):
+            try:
+                out = view(recv, count * world, dtype)
+                dist.all_gather(list(out.split(count)), view(send, count, dtype).clone())
+                return 0
+            except Exception:
+                return 1
+
+        self._ops = SkCommHostOps(None, _AR(all_reduce), _RS(reduce_scatter), _AG(all_gather))
+        h = C.c_void_p()
+        ctx.check(ctx._lib.sk_comm_create_host(ctx.h, C.c_int(world), C.c_int(rank), C.byref(self._ops),
+                                               C.byref(h)))
+        self.h = h
+
+
 def shard_assign(n_items: int, world: int, rank: int) -> list:
     """Round-robin ownership of the K scored views (C3 sharding)."""
     out = (C.c_int32 * max(1, n_items))()

@@ -219,6 +219,7 @@ int sk_scene_upload(sk_ctx* ctx, sk_scene* s, const float* host, int64_t n) {
         b->release();
     }
     s->rest_n = -1;
+    s->moments_sharded_over = nullptr;  // fresh moments: nothing left to gather
     sync(ctx);
   });
 }

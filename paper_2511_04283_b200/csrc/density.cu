@@ -72,17 +72,21 @@ __global__ void error_mask_kernel(const float* __restrict__ raw, const uint32_t*
 }
 
 // ---- K13: s_d, s_p_raw in view order, then min-max of s_p_raw ---------------
+// View j's count row / photometric value sit at slot (j % world) * kpr +
+// j / world (rank-major blocks of the sharded score pass; the identity at
+// world = 1); the sums run over j ascending as the reference's.
 __global__ void scores_kernel(const int32_t* __restrict__ rows, int64_t row_stride, const float* __restrict__ photo,
-                              int k, int64_t n, float* __restrict__ s_d, float* __restrict__ s_p_raw,
-                              uint32_t* __restrict__ lohi) {
+                              int k, int world, int kpr, int64_t n, float* __restrict__ s_d,
+                              float* __restrict__ s_p_raw, uint32_t* __restrict__ lohi) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float sd = 0.0f, sp = 0.0f;
   const bool ok = i < n;
   if (ok) {
     for (int j = 0; j < k; ++j) {
-      const float c = (float)rows[(int64_t)j * row_stride + i];
+      const int slot = (j % world) * kpr + j / world;
+      const float c = (float)rows[(int64_t)slot * row_stride + i];
       sd = sd + c;
-      sp = sp + c * photo[j];
+      sp = sp + c * photo[slot];
     }
     s_d[i] = sd / (float)k;
     s_p_raw[i] = sp;
@@ -397,18 +401,24 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
   require(k > 0, "accumulate_scores: no training views");
   ensure_score_table(ctx, s);
   const int64_t n = s->n;
-  int32_t* rows = ensure<int32_t>(ev.rows, (size_t)k * std::max<int64_t>(n, 1));
-  uint32_t* lohi = ensure<uint32_t>(ev.lohi, 4);
-  SK_CUDA(cudaMemsetAsync(rows, 0, sizeof(int32_t) * (size_t)k * n, ctx->stream));
-  std::vector<float> photo(k, 0.0f);
-  ctx->event_mark(0);
   const int world = comm ? comm->world : 1;
   const int rank = comm ? comm->rank : 0;
-  std::vector<int> mine;  // views sharded round-robin over ranks (C3 below)
+  // views sharded round-robin over ranks; rank r's views fill block r of the
+  // rank-major rows [world][kpr][n] (C3 all-gathers the blocks)
+  const int kpr = (k + world - 1) / world;
+  const int slots = world * kpr;
+  auto slot_of = [&](int j) { return (j % world) * kpr + j / world; };
+  int32_t* rows = ensure<int32_t>(ev.rows, (size_t)slots * std::max<int64_t>(n, 1));
+  uint32_t* lohi = ensure<uint32_t>(ev.lohi, 4);
+  SK_CUDA(cudaMemsetAsync(rows, 0, sizeof(int32_t) * (size_t)slots * n, ctx->stream));
+  std::vector<float> photo(slots, 0.0f);
+  ctx->event_mark(0);
+  std::vector<int> mine;
   for (int j = 0; j < k; ++j)
     if (j % world == rank) mine.push_back(j);
   auto run_view = [&](sk_ctx* c, sk_frame* fr, int j) {
-    score_view(c, s, fr, cams[j], gts[j], gt_u8_device, tau, lambda, bin, rows + (size_t)j * n, &photo[j]);
+    const int sl = slot_of(j);
+    score_view(c, s, fr, cams[j], gts[j], gt_u8_device, tau, lambda, bin, rows + (size_t)sl * n, &photo[sl]);
   };
   const char* one = std::getenv("SK_SCORE_ONE_STREAM");  // runtime override (tests / diagnostics)
   const bool two = SK_SCORE_TWO_STREAMS && !(one && one[0] == '1');
@@ -449,18 +459,18 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
     if (helper_err) std::rethrow_exception(helper_err);
     raise_device_errors(read_error_word(h));
   }
-  float* dphoto = ensure<float>(ev.photo, k);
-  h2d(ctx, dphoto, photo.data(), k);
-  allreduce_scores(comm, rows, (size_t)k * n, dphoto, k, ctx->stream);
+  float* dphoto = ensure<float>(ev.photo, slots);
+  h2d(ctx, dphoto, photo.data(), slots);
   if (world > 1) {
-    d2h(ctx, photo.data(), dphoto, k);
+    allgather_scores(const_cast<sk_comm*>(comm), rows, kpr, n, dphoto, ctx->stream);  // C3
+    d2h(ctx, photo.data(), dphoto, slots);
     sync(ctx);
   }
   ctx->event_mark(1);
   const uint32_t init[2] = {0xffffffffu, 0u};
   h2d(ctx, lohi, init, 2);
   if (n > 0) {
-    scores_kernel<<<blocks(n), 256, 0, ctx->stream>>>(rows, n, dphoto, k, n, s->s_d.as<float>(),
+    scores_kernel<<<blocks(n), 256, 0, ctx->stream>>>(rows, n, dphoto, k, world, kpr, n, s->s_d.as<float>(),
                                                        s->s_p_raw.as<float>(), lohi);
     note_launch();
     minmax_normalize_kernel<<<blocks(n), 256, 0, ctx->stream>>>(s->s_p_raw.as<float>(), lohi, n, s->s_p.as<float>());
@@ -468,7 +478,10 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
   }
   SK_CUDA(cudaGetLastError());
   ctx->event_mark(2);
-  if (photo_out) *photo_out = photo;
+  if (photo_out) {
+    photo_out->resize(k);
+    for (int j = 0; j < k; ++j) (*photo_out)[j] = photo[slot_of(j)];
+  }
 }
 
 void select_densify_flags(sk_ctx* ctx, sk_scene* s, float tau_d, float thr, float percent_dense, bool use_vcd,
@@ -540,6 +553,7 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
                       float clone_lr, const std::function<const float*(int64_t)>& eps_source,
                       int32_t* old_to_new_dev) {
   EventScratch& ev = ctx->ev;
+  gather_moments(s, ctx->stream);  // the compaction moves whole moment rows (sharded C1, comm.cu)
   const int64_t n = s->n;
   if (n == 0) return 0;
   int32_t* cls = ensure<int32_t>(ev.cls, 3 * (size_t)n);

@@ -379,21 +379,21 @@ __global__ void __launch_bounds__(kPbThreads, SK_K9_MINB) project_bwd_kernel(
 constexpr int kAdamThreads = 256;
 __global__ void __launch_bounds__(kAdamThreads) adam_kernel(float* __restrict__ params, const float* __restrict__ grads,
                                                             float* __restrict__ am, float* __restrict__ av,
-                                                            int64_t stride, int64_t n, AdamParams ap,
-                                                            const uint32_t* __restrict__ err) {
+                                                            int64_t stride, int64_t gstride, int64_t n,
+                                                            AdamParams ap, const uint32_t* __restrict__ err) {
   if (__ldg(err)) return;  // see project_bwd_kernel
   const int c = blockIdx.y;
   const int gidx = comp_group(c);
   if (!ap.active[gidx]) return;
   const float lr = ap.lr[gidx], bc1 = ap.bc1[gidx], bc2 = ap.bc2[gidx];
-  const int64_t row = (int64_t)c * stride;
+  const int64_t row = (int64_t)c * stride, grow = (int64_t)c * gstride;
   const int64_t nq = n >> 2;
   for (int64_t q = (int64_t)blockIdx.x * kAdamThreads + threadIdx.x; q < nq; q += (int64_t)gridDim.x * kAdamThreads) {
     const int64_t o = row + q * 4;
     float4 p = __ldcs(reinterpret_cast<const float4*>(params + o));
     float4 m = __ldcs(reinterpret_cast<const float4*>(am + o));
     float4 v = __ldcs(reinterpret_cast<const float4*>(av + o));
-    const float4 g = __ldcs(reinterpret_cast<const float4*>(grads + o));
+    const float4 g = __ldcs(reinterpret_cast<const float4*>(grads + grow + q * 4));
     adam_update(p.x, m.x, v.x, g.x, lr, bc1, bc2);
     adam_update(p.y, m.y, v.y, g.y, lr, bc1, bc2);
     adam_update(p.z, m.z, v.z, g.z, lr, bc1, bc2);
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(kAdamThreads) adam_kernel(float* __restrict__ 
   if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
     const int64_t o = row + nq * 4 + threadIdx.x;
     float p = params[o], m = am[o], v = av[o];
-    adam_update(p, m, v, grads[o], lr, bc1, bc2);
+    adam_update(p, m, v, grads[grow + nq * 4 + threadIdx.x], lr, bc1, bc2);
     params[o] = p;
     am[o] = m;
     av[o] = v;
@@ -504,20 +504,37 @@ void launch_project_backward(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stat
   launch_pb(ctx, s, f, do_stats);
 }
 
+namespace {
+// K10 over Gaussians [first, first + count) of every component; the
+// gradients of that range are row c of `grads` with stride gstride.
+void adam_range(sk_ctx* ctx, sk_scene* s, const AdamParams& ap, const float* grads, int64_t gstride, int64_t first,
+                int64_t count) {
+  if (count <= 0) return;
+  // ~16 resident 256-thread blocks per SM spread over the components
+  const int64_t per_comp = std::max<int64_t>(1, (int64_t)148 * 16 / s->comps);
+  const int64_t need = (count / 4 + kAdamThreads - 1) / kAdamThreads;
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min(need, per_comp)), (unsigned)s->comps);
+  adam_kernel<<<grid, kAdamThreads, 0, ctx->stream>>>(s->params.as<float>() + first, grads, s->adam_m.as<float>() + first,
+                                                      s->adam_v.as<float>() + first, s->capacity, gstride, count, ap,
+                                                      ctx->err_word.as<uint32_t>());
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+}
+}  // namespace
+
 void launch_adam(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float position_lr, bool update_sh_rest) {
   ensure_optimizer_state(ctx, s);
   require(s->capacity % 4 == 0, "adam: scene capacity must be a multiple of 4");
   const AdamParams ap = make_adam(s, lrs, position_lr, update_sh_rest);
-  if (s->n == 0) return;
-  // ~16 resident 256-thread blocks per SM spread over the components
-  const int64_t per_comp = std::max<int64_t>(1, (int64_t)148 * 16 / s->comps);
-  const int64_t need = (s->n / 4 + kAdamThreads - 1) / kAdamThreads;
-  const dim3 grid((unsigned)std::max<int64_t>(1, std::min(need, per_comp)), (unsigned)s->comps);
-  adam_kernel<<<grid, kAdamThreads, 0, ctx->stream>>>(s->params.as<float>(), s->grads.as<float>(),
-                                                      s->adam_m.as<float>(), s->adam_v.as<float>(), s->capacity,
-                                                      s->n, ap, ctx->err_word.as<uint32_t>());
-  note_launch();
-  SK_CUDA(cudaGetLastError());
+  adam_range(ctx, s, ap, s->grads.as<float>(), s->capacity, 0, s->n);
+}
+
+void launch_adam_shard(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float position_lr, bool update_sh_rest,
+                       const float* gshard, int64_t chunk, int rank) {
+  ensure_optimizer_state(ctx, s);
+  const AdamParams ap = make_adam(s, lrs, position_lr, update_sh_rest);
+  const int64_t first = (int64_t)rank * chunk;
+  adam_range(ctx, s, ap, gshard, chunk, first, std::min(chunk, s->n - first));
 }
 
 __global__ void accumulate_rest_kernel(float* __restrict__ acc, const float* __restrict__ g, int64_t stride,
@@ -570,14 +587,7 @@ void lazy_sh_rest(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, bool due) 
     if (ap.active[g]) s->adam_t[g] -= 1;  // make_adam counted every group; only SH-rest steps here
     ap.active[g] = 0;
   }
-  const int64_t per_comp = std::max<int64_t>(1, (int64_t)148 * 16 / s->comps);
-  const int64_t need = (s->n / 4 + kAdamThreads - 1) / kAdamThreads;
-  const dim3 agrid((unsigned)std::max<int64_t>(1, std::min(need, per_comp)), (unsigned)s->comps);
-  adam_kernel<<<agrid, kAdamThreads, 0, ctx->stream>>>(s->params.as<float>(), s->rest_accum.as<float>(),
-                                                       s->adam_m.as<float>(), s->adam_v.as<float>(), s->capacity,
-                                                       s->n, ap, ctx->err_word.as<uint32_t>());
-  note_launch();
-  SK_CUDA(cudaGetLastError());
+  adam_range(ctx, s, ap, s->rest_accum.as<float>(), s->capacity, 0, s->n);
   SK_CUDA(cudaMemsetAsync(s->rest_accum.ptr, 0, bytes, ctx->stream));
 }
 

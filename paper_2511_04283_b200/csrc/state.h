@@ -28,6 +28,8 @@ struct PendingStep {
   float lambda = 0.2f;
   int64_t pairs = 0, n = 0;
   sk_log_row* row = nullptr;
+  sk_scene* scene = nullptr;
+  int64_t adam_t[6] = {};  // the scene's Adam step counters before this step (restored on a device error)
   cudaEvent_t done = nullptr;
   HostBuf pinned;  // [2 slots][4 doubles + error word]
   int slot = 0;
@@ -133,6 +135,9 @@ struct sk_scene {
   int64_t rest_n = -1, rest_stride = 0;
   // ScoreTable (adc.hpp:23-45), device SoA, all [capacity] (grad3d [3][capacity])
   sk::DevBuf s_d, s_p_raw, s_p, grad_norm_acc, abs_grad_acc, grad3d_acc, views_seen, max_radius2d;
+  // Sharded C1 (comm.cu): the Adam moments are current only on this rank's
+  // slice until gather_moments() completes them over this communicator.
+  struct sk_comm* moments_sharded_over = nullptr;
 };
 
 // Per-view render state. Projected arrays are indexed by projected index,
@@ -188,9 +193,11 @@ namespace sk {
 
 constexpr int kBGradFields = 11;
 
-// Component stride of the planar scene buffers: a multiple of 4 so every
-// component row is 16-byte aligned for float4 access.
-inline int64_t round_capacity(int64_t n) { return ((n < 1 ? 1 : n) + 3) & ~int64_t(3); }
+// Component stride of the planar scene buffers: a multiple of 32, so every
+// component row is 16-byte aligned for float4 access and the stride holds
+// world x shard_chunk(n, world) entries for 1, 2, 4 and 8 ranks (the sharded
+// C1 exchanges whole 4-aligned slices in place, comm.cu).
+inline int64_t round_capacity(int64_t n) { return ((n < 1 ? 1 : n) + 31) & ~int64_t(31); }
 
 // ---- launchers (each .cu file owns its kernels) ---------------------------
 // preprocess.cu
@@ -249,6 +256,10 @@ void launch_project_backward(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stat
 void launch_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const LearningRates& lrs, float position_lr,
                                   bool update_sh_rest, bool do_stats);
 void launch_adam(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float position_lr, bool update_sh_rest);
+// K10 on Gaussians [rank x chunk, min(n, (rank + 1) x chunk)) with that
+// slice's gradients in gshard ([comps][chunk]); sharded C1 (comm.cu).
+void launch_adam_shard(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float position_lr, bool update_sh_rest,
+                       const float* gshard, int64_t chunk, int rank);
 // Lazy SH-rest (trainer.hpp:160-169, adam.hpp:146-159): rest_accum += the SH-rest
 // gradients; when due, an Adam step of the SH-rest group on the accumulator,
 // which is then cleared.

@@ -88,6 +88,10 @@ void finish_pending(sk_ctx* ctx, PendingStep* pend) {
   uint32_t bits = 0;
   memcpy(&bits, h + 4, sizeof(bits));
   if (bits) {
+    // K9 / K10 of the failed step were gated on the error word (optim.cu), so
+    // the scene is as before the step; roll the host step counters back too.
+    // The pipelined path reports the error one call late (documented).
+    if (pend->scene) std::copy(pend->adam_t, pend->adam_t + 6, pend->scene->adam_t);
     SK_CUDA(cudaMemsetAsync(ctx->err_word.ptr, 0, sizeof(uint32_t), ctx->stream));
     raise_device_errors(bits);
   }
@@ -140,12 +144,25 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   ctx->mark(5);
   const LearningRates lrs = lrs_from(cfg);
   const float pos_lr = expon_lr(lrs.position * extent, lrs.position_final * extent, it, cfg.iterations);
-  // K9 into the gradient buffer (+ C1 sum over ranks on a view-parallel
+  int64_t adam_t0[6];
+  std::copy(scene->adam_t, scene->adam_t + 6, adam_t0);
+  // K9 into the gradient buffer (+ C1 over the ranks of a view-parallel
   // step), then K10
   launch_project_backward(ctx, scene, f, true);
-  if (comm && comm->world > 1) allreduce_grads(comm, scene, ctx->stream);
+  sk_comm* c1 = const_cast<sk_comm*>(comm);
+  const bool sharded = !cfg.lazy_opt_enabled && c1_sharded(comm, scene);
+  if (sharded) {
+    reduce_scatter_grads(c1, scene, ctx->stream);
+  } else if (comm && comm->world > 1) {
+    gather_moments(scene, ctx->stream);
+    allreduce_grads(c1, scene, ctx->stream);
+  }
   ctx->mark(6);
-  if (!cfg.lazy_opt_enabled) {
+  if (sharded) {
+    launch_adam_shard(ctx, scene, lrs, pos_lr, true, c1->gshard.as<float>(), shard_chunk(scene->n, comm->world),
+                      comm->rank);
+    allgather_params(c1, scene, ctx->stream);
+  } else if (!cfg.lazy_opt_enabled) {
     launch_adam(ctx, scene, lrs, pos_lr, true);
   } else {
     // trainer.hpp:160-169: SH-rest excluded from the step, accumulated, and
@@ -172,11 +189,15 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
     pend->n = scene->n;
     pend->row = row;
     pend->tev_set = ctx->tev_set;
+    pend->scene = scene;
+    std::copy(adam_t0, adam_t0 + 6, pend->adam_t);
     return;
   }
   LossSums sums{};
   read_loss_sums(ctx, &sums);  // synchronises the stream
-  raise_device_errors(read_error_word(ctx));
+  const uint32_t bits = read_error_word(ctx);
+  if (bits) std::copy(adam_t0, adam_t0 + 6, scene->adam_t);  // K9 / K10 were gated: no update happened
+  raise_device_errors(bits);
   if (ctx->timing) {
     for (int i = 0; i < SK_NUM_PHASES; ++i) {
       float ms = 0.0f;
@@ -376,6 +397,7 @@ int sk_scene_get_adam(sk_ctx* ctx, const sk_scene* s, float* m, float* v, int64_
       for (int g = 0; g < 6; ++g) t6[g] = s->adam_t[g];
     if ((m || v) && s->n > 0) {
       arg(s->adam_m.ptr != nullptr, "sk_scene_get_adam: optimizer not initialised");
+      gather_moments(const_cast<sk_scene*>(s), ctx->stream);  // sharded C1 leaves them per-rank
       if (m)
         SK_CUDA(cudaMemcpy2DAsync(m, sizeof(float) * s->n, s->adam_m.ptr, sizeof(float) * s->capacity,
                                   sizeof(float) * s->n, s->comps, cudaMemcpyDeviceToHost, ctx->stream));

@@ -12,10 +12,16 @@
 
 #include "state.h"
 
-// NCCL communicator of one rank (comm.cu).
+// Communicator of one rank (comm.cu): NCCL over NVLink / NVSwitch, or the
+// host-callback backend (sk_comm_create_host: the library stages its buffers
+// through pinned host memory and calls the caller's collectives).
 struct sk_comm {
   ncclComm_t comm = nullptr;
+  bool is_host = false;
+  sk_comm_host_ops host{};
   int rank = 0, world = 1;
+  sk::HostBuf stage;  // host backend staging (send | recv)
+  sk::DevBuf gshard;  // C1: this rank's reduce-scattered gradient slice [comps][chunk]
 };
 
 struct sk_dataset {
@@ -156,9 +162,29 @@ void finish_pending(sk_ctx* ctx, PendingStep* pend);
 // density.cu: Trainer::density_event (trainer.hpp:177-243).
 void density_event(sk_trainer* t, int it, bool densify, bool prune);
 
-// comm.cu: C1 / C2 / C3 (no-ops for a null or single-rank communicator).
-void allreduce_grads(const sk_comm* c, sk_scene* s, cudaStream_t st);
-void allreduce_stats(const sk_comm* c, sk_scene* s, cudaStream_t st);
-void allreduce_scores(const sk_comm* c, int32_t* rows, size_t count, float* photo, int k, cudaStream_t st);
+// comm.cu: the exchanges of view sharding. All are no-ops for a
+// null or single-rank communicator.
+// C1, sharded form: the Gaussian axis is cut into `world` slices of
+// shard_chunk(n, world) entries (a multiple of 4); the summed gradients of
+// this rank's slice are reduce-scattered into c->gshard, K10 updates only
+// that slice of params / m / v, and the parameters are all-gathered in place
+// (the Adam moments stay sharded until gather_moments).
+bool c1_sharded(const sk_comm* c, const sk_scene* s);
+int64_t shard_chunk(int64_t n, int world);
+void reduce_scatter_grads(sk_comm* c, sk_scene* s, cudaStream_t st);
+void allgather_params(sk_comm* c, sk_scene* s, cudaStream_t st);
+// Completes the Adam moments on every rank (each rank owns its slice): run
+// before anything reads m / v across slices (the density-event compaction,
+// sk_scene_get_adam).
+void gather_moments(sk_scene* s, cudaStream_t st);
+// C1, replicated form (lazy SH-rest schedule or a capacity the slices do not
+// divide): the first n gradients of every component are all-reduced.
+void allreduce_grads(sk_comm* c, sk_scene* s, cudaStream_t st);
+// C2: ScoreTable statistics of the first n Gaussians, sum / max.
+void allreduce_stats(sk_comm* c, sk_scene* s, cudaStream_t st);
+// C3: every rank scored views rank, rank + world, ... into its block of the
+// rank-major rows [world][kpr][n] (kpr = ceil(k / world)) and photometric
+// [world][kpr]; the blocks are all-gathered (no reduction, exact).
+void allgather_scores(sk_comm* c, int32_t* rows, int64_t kpr, int64_t n, float* photo, cudaStream_t st);
 
 }  // namespace sk

@@ -72,3 +72,66 @@ def test_nccl_single_rank_communicator(orc):
     assert np.isfinite(pipe.flush()[0]["loss"])
     comm.close()
     ctx.close()
+
+
+def _poke_device_param(ctx, scene, comp, index, value):
+    """Writes one parameter straight into the device scene (no upload, so
+    the Adam state is kept) through __cuda_array_interface__."""
+    import torch
+
+    import paper_2511_04283_b200 as sk
+    ptr = sk.C.POINTER(sk.C.c_float)()
+    stride = sk.C.c_int64()
+    ctx.check(ctx._lib.sk_scene_device_params(scene.h, sk.C.byref(ptr), sk.C.byref(stride)))
+    addr = sk.C.cast(ptr, sk.C.c_void_p).value + 4 * (comp * stride.value + index)
+
+    class One:
+        __cuda_array_interface__ = {"shape": (1,), "typestr": "<f4", "data": (addr, False), "version": 3}
+    ctx.synchronize()
+    torch.as_tensor(One(), device="cuda").fill_(value)
+    torch.cuda.synchronize()
+
+
+def test_device_error_leaves_scene_untouched(orc):
+    """covariance_3d throws before any state changes (scene.hpp:89-92): a train
+    step whose K1 raises leaves parameters, Adam moments and step counters and
+    the score table as they were — on the synchronous path and on the
+    pipelined path (which reports the error one call late)."""
+    import paper_2511_04283_b200 as sk
+    from tests.util import random_scene
+    sk.build()
+    ctx = sk.Context(0)
+    rng = np.random.default_rng(31)
+    p = random_scene(rng, 300, 3)
+    cam = orc.default_camera(64, 48)
+    gt8 = rng.integers(0, 256, (48, 64, 3), dtype=np.uint8)
+    cfg = sk.default_config()
+    scene = ctx.scene(p, 3)
+    sk.train_step_host(ctx, scene, cam, gt8, cfg, 2.64, 1)  # one good step: non-zero moments and stats
+    _poke_device_param(ctx, scene, 7, 5, float("nan"))
+    before = scene.download()
+    assert np.isnan(before[7, 5])
+    m0, v0, t0 = scene.adam_state()
+    assert np.abs(m0).max() > 0 and list(t0) == [1] * 6
+    tab0 = scene.score_table()
+    with pytest.raises(ValueError, match="covariance_3d"):
+        sk.train_step_host(ctx, scene, cam, gt8, cfg, 2.64, 2)
+    assert np.array_equal(scene.download(), before, equal_nan=True)
+    m1, v1, t1 = scene.adam_state()
+    assert np.array_equal(m1, m0) and np.array_equal(v1, v0) and list(t1) == list(t0)
+    tab1 = scene.score_table()
+    assert np.array_equal(tab1.views_seen, tab0.views_seen)
+    assert np.array_equal(tab1.grad_norm_acc, tab0.grad_norm_acc)
+    # pipelined: the error surfaces at the next call (or flush), state untouched
+    import torch
+    pinned = torch.empty(gt8.size, dtype=torch.uint8, pin_memory=True).numpy().reshape(gt8.shape)
+    pinned[...] = gt8
+    pipe = sk.HostStepPipeline(ctx)
+    with pytest.raises(ValueError, match="covariance_3d"):
+        pipe.step(scene, cam, pinned, cfg, 2.64, 3)
+        pipe.step(scene, cam, pinned, cfg, 2.64, 4)
+        pipe.flush()
+    assert np.array_equal(scene.download(), before, equal_nan=True)
+    m2, v2, t2 = scene.adam_state()
+    assert np.array_equal(m2, m0) and np.array_equal(v2, v0) and list(t2) == list(t0)
+    ctx.close()
