@@ -159,6 +159,16 @@ int sk_bin_sort(sk_ctx* ctx, sk_frame* frame, int64_t* pairs);
 int sk_render_forward(sk_ctx* ctx, sk_frame* frame, const uint8_t* mask_host,
                       int32_t* counts_host);
 
+/* A caller's TileGrid (raster.hpp:27-57, build_tile_grid :157-168) for the
+ * frame's projected set: ranges [tiles][2] contiguous in tile order into
+ * values [pairs] (projected indices). sk_render_forward then blends exactly
+ * these lists in their given order (blend_forward raster.hpp:194-248). */
+int sk_frame_set_tile_lists(sk_ctx* ctx, sk_frame* frame, const int32_t* ranges, const int32_t* values,
+                            int64_t pairs);
+/* A caller's rendered image ([H][W][3]) as the frame's render, so sk_loss
+ * evaluates training_loss(rendered, gt, lambda) (loss.hpp:21-47) on it. */
+int sk_frame_set_image(sk_ctx* ctx, sk_frame* frame, const float* hwc, int width, int height);
+
 /* Workload counters of the last forward render (SURVEY 8(d) roofline units):
  * visited = pixel-Gaussian evaluations the reference loop performs
  * (raster.hpp:219-235: list entries up to and including the terminating one),
@@ -224,6 +234,27 @@ int sk_scene_reset_score_table(sk_ctx* ctx, sk_scene* scene);
  * accumulate_stats the ScoreTable statistics of trainer.hpp:139-156 are
  * updated. grads_host ([C][n]) may be NULL. */
 int sk_project_backward(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, int accumulate_stats, float* grads_host);
+/* project_backward (camera.hpp:156-213) for every Gaussian of the scene
+ * (no culling test, as the reference's per-Gaussian call) with explicit
+ * upstream gradients: d_mu2d [n][2], d_cov2d [n][4] (row-major 2x2, the
+ * output of cov_grad_from_inv_grad camera.hpp:148-150), d_color [n][3],
+ * d_opacity [n]. Gradients go to the scene's gradient buffer and, if
+ * grads_host != NULL, to planar [C][n] host memory. */
+int sk_project_backward_explicit(sk_ctx* ctx, sk_scene* scene, const sk_camera* cam, const float* d_mu2d,
+                                 const float* d_cov2d, const float* d_color, const float* d_opacity,
+                                 float* grads_host);
+/* Overwrites the parameters (planar [C][n], n = the scene size) keeping the
+ * optimizer state (SceneOptimizer holds moments across steps, adam.hpp). */
+int sk_scene_set_params(sk_ctx* ctx, sk_scene* scene, const float* host_params, int64_t n);
+/* SceneOptimizer::remap (adam.hpp:113-120 / AdamGroup::remap :45-58):
+ * old_to_new [n] (-1 = removed), the scene size becomes new_n; survivors keep
+ * their moments, new slots start at zero, the step counters are kept. */
+int sk_scene_remap_moments(sk_ctx* ctx, sk_scene* scene, const int32_t* old_to_new, int64_t new_n);
+/* SceneOptimizer::step_sh_rest (adam.hpp:146-153): the SH-rest group alone,
+ * from the gradient buffer. */
+int sk_adam_step_sh_rest(sk_ctx* ctx, sk_scene* scene, const sk_learning_rates* lrs);
+/* SceneOptimizer::reset_opacity_state (adam.hpp:157-160). */
+int sk_adam_reset_opacity_state(sk_ctx* ctx, sk_scene* scene);
 /* Overwrites the scene's gradient buffer (planar [C][n]). */
 int sk_scene_set_grads(sk_ctx* ctx, sk_scene* scene, const float* grads_host);
 /* K10: SceneOptimizer::step (adam.hpp:124-143) from the gradient buffer. */
@@ -243,6 +274,16 @@ int sk_scene_get_adam(sk_ctx* ctx, const sk_scene* scene, float* m, float* v, in
  * NULL. */
 int sk_accumulate_scores(sk_ctx* ctx, sk_scene* scene, int k, const sk_camera* cams, const float* images, float tau,
                          float lambda, const sk_binning* binning, int32_t* counts_out, float* photometric_out);
+/* build_error_maps (error_maps.hpp:22-43) on explicit [H][W][3] images:
+ * raw and normalized maps and the strict mask ([H][W] row-major; any output
+ * may be NULL) and the photometric term. */
+int sk_error_maps(sk_ctx* ctx, const float* rendered, const float* gt, int width, int height, float tau,
+                  float lambda, float* raw, float* normalized, uint8_t* mask, float* photometric);
+/* scores_from_counts (adc.hpp:69-84) on explicit count rows counts [k][n]
+ * and photometric [k]: s_d, s_p_raw and the min-max normalized s_p ([n]
+ * each, any may be NULL). Raises the reference's message for k == 0. */
+int sk_scores_from_counts(sk_ctx* ctx, const int32_t* counts, const float* photometric, int k, int64_t n, float* s_d,
+                          float* s_p_raw, float* s_p);
 /* select_densify (adc.hpp:135-153) over the scene's ScoreTable; flags [n]. */
 int sk_select_densify(sk_ctx* ctx, sk_scene* scene, float tau_d, float grad_threshold, float percent_dense,
                       int use_vcd, float extent, uint8_t* clone, uint8_t* split);

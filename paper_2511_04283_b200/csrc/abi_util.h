@@ -26,6 +26,9 @@ int guarded(sk_ctx* ctx, F&& f) {
 }
 
 inline void sync(sk_ctx* ctx) { SK_CUDA(cudaStreamSynchronize(ctx->stream)); }
+// planar [3][H][W] device image <-> interleaved [H][W][3] host image (synchronous)
+void planar_to_hwc(sk_ctx* ctx, const void* dev, float* hwc, int w, int h);
+void hwc_to_planar(sk_ctx* ctx, void* dev, const float* hwc, int w, int h);
 
 template <typename T>
 void d2h(sk_ctx* ctx, T* host, const void* dev, size_t count) {

@@ -33,6 +33,8 @@ namespace {
 
 void set_device(sk_ctx* ctx) { SK_CUDA(cudaSetDevice(ctx->device)); }
 
+}  // namespace
+
 // planar [3][H][W] device -> interleaved [H][W][3] host
 void planar_to_hwc(sk_ctx* ctx, const void* dev, float* hwc, int w, int h) {
   const size_t plane = (size_t)w * h;
@@ -53,7 +55,6 @@ void hwc_to_planar(sk_ctx* ctx, void* dev, const float* hwc, int w, int h) {
 }
 
 
-}  // namespace
 }  // namespace sk
 
 using namespace sk;
@@ -307,6 +308,51 @@ int sk_frame_set_projected(sk_ctx* ctx, sk_frame* f, const sk_projected* pg, int
     }
     launch_inject_bin(ctx, f);
     raise_device_errors(read_error_word(ctx));
+  });
+}
+
+// A caller's TileGrid (raster.hpp:27-57) as the frame's tile lists: ranges
+// [tiles][2] into values [pairs] (projected indices); blend_forward then
+// blends exactly these lists in their order, as the reference does.
+int sk_frame_set_tile_lists(sk_ctx* ctx, sk_frame* f, const int32_t* ranges, const int32_t* values, int64_t pairs) {
+  return guarded(ctx, [&] {
+    arg(f && ranges && (values || pairs == 0) && pairs >= 0, "sk_frame_set_tile_lists: bad arguments");
+    set_device(ctx);
+    const int tiles = f->tiles_x * f->tiles_y;
+    int64_t expect = 0;
+    for (int t = 0; t < tiles; ++t) {
+      arg(ranges[2 * t] == expect && ranges[2 * t + 1] >= ranges[2 * t],
+          "sk_frame_set_tile_lists: ranges must be contiguous in tile order");
+      expect = ranges[2 * t + 1];
+    }
+    arg(expect == pairs, "sk_frame_set_tile_lists: ranges do not cover the values");
+    for (int64_t k = 0; k < pairs; ++k)
+      arg(values[k] >= 0 && values[k] < f->n, "sk_frame_set_tile_lists: projected index out of range");
+    ensure<int2>(f->ranges, (size_t)std::max(tiles, 1));
+    if (tiles > 0) h2d(ctx, f->ranges.ptr, ranges, 2 * (size_t)tiles);
+    const size_t pm = (size_t)std::max<int64_t>(pairs, 1);
+    uint32_t* pv = ensure<uint32_t>(f->pval_a, pm);
+    if (pairs > 0) h2d(ctx, pv, values, pairs);
+    f->pair_val = pv;
+    f->pair_tile = nullptr;
+    f->pairs = pairs;
+    f->binned = true;
+    f->rendered = false;
+    f->cmask_valid = false;
+    sync(ctx);
+  });
+}
+
+// A caller's rendered image ([H][W][3]) as the frame's render, for
+// training_loss (loss.hpp:21-47) on explicit images.
+int sk_frame_set_image(sk_ctx* ctx, sk_frame* f, const float* hwc, int width, int height) {
+  return guarded(ctx, [&] {
+    arg(f && hwc, "sk_frame_set_image: bad arguments");
+    set_device(ctx);
+    frame_geometry(f, width, height, nullptr);
+    ensure_image(f);
+    hwc_to_planar(ctx, f->image.ptr, hwc, width, height);
+    f->rendered = true;
   });
 }
 

@@ -62,13 +62,15 @@ __global__ void error_raw_kernel(const float* __restrict__ image, const void* __
 }
 
 // normalized = (raw - lo) / (hi - lo) (all zero if degenerate); mask = normalized > tau
+// (normalized may be null: the score pass only needs the mask)
 __global__ void error_mask_kernel(const float* __restrict__ raw, const uint32_t* __restrict__ lohi, int64_t n,
-                                  float tau, uint8_t* __restrict__ mask) {
+                                  float tau, uint8_t* __restrict__ mask, float* __restrict__ normalized) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const float lo = __uint_as_float(lohi[0]), hi = __uint_as_float(lohi[1]);
   const float nv = hi > lo ? (raw[p] - lo) / (hi - lo) : 0.0f;
   mask[p] = nv > tau ? 1 : 0;
+  if (normalized) normalized[p] = nv;
 }
 
 // ---- K13: s_d, s_p_raw in view order, then min-max of s_p_raw ---------------
@@ -362,7 +364,7 @@ void score_view(sk_ctx* c, sk_scene* s, sk_frame* f, const sk_camera& cam, const
   error_raw_kernel<<<blocks(npx), 256, 0, c->stream>>>(f->image.as<float>(), gt, gt_u8_device, cam.width,
                                                         cam.height, raw, lohi);
   note_launch();
-  error_mask_kernel<<<blocks(npx), 256, 0, c->stream>>>(raw, lohi, npx, tau, mask);
+  error_mask_kernel<<<blocks(npx), 256, 0, c->stream>>>(raw, lohi, npx, tau, mask, nullptr);
   note_launch();
   LossSums sums{};
   launch_loss(c, f, gt, gt_u8_device, lambda, false, &sums);
@@ -750,6 +752,73 @@ int sk_accumulate_scores(sk_ctx* ctx, sk_scene* s, int k, const sk_camera* cams,
     if (counts_out && s->n > 0) d2h(ctx, counts_out, ctx->ev.rows.ptr, (size_t)k * s->n);
     sync(ctx);
     if (photo_out) std::copy(photo.begin(), photo.end(), photo_out);
+  });
+}
+
+// build_error_maps (error_maps.hpp:22-43) on explicit images: K11 raw map and
+// min / max, the normalized map and strict mask, and the photometric term
+// (K7 forward for the SSIM).
+int sk_error_maps(sk_ctx* ctx, const float* rendered, const float* gt, int width, int height, float tau, float lambda,
+                  float* raw_out, float* normalized_out, uint8_t* mask_out, float* photometric) {
+  return guarded(ctx, [&] {
+    arg(rendered && gt && width > 0 && height > 0, "build_error_maps: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    sk_frame f;
+    frame_geometry(&f, width, height, nullptr);
+    ensure_image(&f);
+    const int64_t npx = (int64_t)width * height;
+    hwc_to_planar(ctx, f.image.ptr, rendered, width, height);
+    f.rendered = true;
+    void* g = f.gt.ensure(sizeof(float) * 3 * npx);
+    h2d(ctx, g, gt, 3 * npx);
+    float* raw = ensure<float>(ctx->ev.raw, npx);
+    uint8_t* mask = ensure<uint8_t>(ctx->ev.mask, npx);
+    float* nrm = ensure<float>(f.loss_scratch, npx);
+    uint32_t* lohi = ensure<uint32_t>(ctx->ev.lohi, 4);
+    const uint32_t init[2] = {0xffffffffu, 0u};
+    h2d(ctx, lohi, init, 2);
+    error_raw_kernel<<<blocks(npx), 256, 0, ctx->stream>>>(f.image.as<float>(), g, false, width, height, raw, lohi);
+    note_launch();
+    error_mask_kernel<<<blocks(npx), 256, 0, ctx->stream>>>(raw, lohi, npx, tau, mask, nrm);
+    note_launch();
+    LossSums sums{};
+    launch_loss(ctx, &f, g, false, lambda, false, &sums);
+    sk_loss_values v{};
+    finish_loss(width, height, lambda, sums, &v);
+    if (photometric) *photometric = (1.0f - lambda) * (float)v.l1 + lambda * (1.0f - (float)v.ssim);
+    if (raw_out) d2h(ctx, raw_out, raw, npx);
+    if (normalized_out) d2h(ctx, normalized_out, nrm, npx);
+    if (mask_out) d2h(ctx, mask_out, mask, npx);
+    sync(ctx);
+  });
+}
+
+// scores_from_counts (adc.hpp:69-84) on explicit count rows: K13.
+int sk_scores_from_counts(sk_ctx* ctx, const int32_t* counts, const float* photometric, int k, int64_t n, float* s_d,
+                          float* s_p_raw, float* s_p) {
+  return guarded(ctx, [&] {
+    require(k > 0, "scores_from_counts: need one count row and one photometric value per view");
+    arg(n >= 0 && (n == 0 || counts) && photometric, "scores_from_counts: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    if (n == 0) return;
+    int32_t* rows = ensure<int32_t>(ctx->ev.rows, (size_t)k * n);
+    float* dphoto = ensure<float>(ctx->ev.photo, k);
+    DevBuf out;
+    float* o = ensure<float>(out, 3 * (size_t)n);
+    uint32_t* lohi = ensure<uint32_t>(ctx->ev.lohi, 4);
+    h2d(ctx, rows, counts, (size_t)k * n);
+    h2d(ctx, dphoto, photometric, k);
+    const uint32_t init[2] = {0xffffffffu, 0u};
+    h2d(ctx, lohi, init, 2);
+    scores_kernel<<<blocks(n), 256, 0, ctx->stream>>>(rows, n, dphoto, k, 1, k, n, o, o + n, lohi);
+    note_launch();
+    minmax_normalize_kernel<<<blocks(n), 256, 0, ctx->stream>>>(o + n, lohi, n, o + 2 * n);
+    note_launch();
+    SK_CUDA(cudaGetLastError());
+    if (s_d) d2h(ctx, s_d, o, n);
+    if (s_p_raw) d2h(ctx, s_p_raw, o + n, n);
+    if (s_p) d2h(ctx, s_p, o + 2 * n, n);
+    sync(ctx);
   });
 }
 

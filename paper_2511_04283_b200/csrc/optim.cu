@@ -371,6 +371,45 @@ __global__ void __launch_bounds__(kPbThreads, SK_K9_MINB) project_bwd_kernel(
   for (int c = 0; c < NC; ++c) grads[c * stride + i] = g[c * kPbThreads];
 }
 
+// project_backward (camera.hpp:156-213) with explicit per-Gaussian upstream
+// gradients (d_mu2d [n][2], d_cov2d [n][4] row-major, d_color [n][3],
+// d_opacity [n]) for every Gaussian, as the reference's per-Gaussian call:
+// no culling test (the C++ API's project_backward).
+template <int DEG>
+__global__ void __launch_bounds__(kPbThreads, SK_K9_MINB) project_bwd_explicit_kernel(
+    const float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ up_mu,
+    const float* __restrict__ up_cov, const float* __restrict__ up_col, const float* __restrict__ up_op,
+    float* __restrict__ grads) {
+  constexpr int NC = 11 + 3 * (DEG + 1) * (DEG + 1);
+  __shared__ float s_grad[NC * kPbThreads];
+  __shared__ float s_exp2[64];
+  stage_exp2_table(s_exp2);
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kPbThreads + threadIdx.x;
+  if (i >= n) return;
+  float* g = s_grad + threadIdx.x;
+  float dmu2d[2] = {up_mu[2 * i], up_mu[2 * i + 1]};
+  float dcov[2][2] = {{up_cov[4 * i], up_cov[4 * i + 1]}, {up_cov[4 * i + 2], up_cov[4 * i + 3]}};
+  float dcol[3] = {up_col[3 * i], up_col[3 * i + 1], up_col[3 * i + 2]};
+  project_backward_one<DEG, kPbThreads>(params, stride, i, cam, dmu2d, dcov, dcol, up_op[i], g, s_exp2);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) grads[c * stride + i] = g[c * kPbThreads];
+}
+
+// AdamGroup::remap (adam.hpp:45-58) for every group: survivors keep their
+// moments at their new index, new slots start at zero (zeroed by the caller).
+__global__ void remap_moments_kernel(const float* __restrict__ m, const float* __restrict__ v, int64_t stride, int64_t n,
+                                     const int32_t* __restrict__ old_to_new, float* __restrict__ m2,
+                                     float* __restrict__ v2, int64_t stride2) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = old_to_new[i];
+  if (j < 0) return;
+  const int c = blockIdx.y;
+  m2[c * stride2 + j] = m[c * stride + i];
+  v2[c * stride2 + j] = v[c * stride + i];
+}
+
 // K10: dense Adam over every component of every Gaussian (SceneOptimizer::step
 // adam.hpp:124-143), float4-vectorised along the Gaussian axis (capacity is a
 // multiple of 4, rows are 16-byte aligned). blockIdx.y is the component, so
@@ -600,6 +639,81 @@ void reset_opacity(sk_ctx* ctx, sk_scene* s) {
       s->params.as<float>() + o, s->adam_m.as<float>() + o, s->adam_v.as<float>() + o, s->n, cap);
   note_launch();
   SK_CUDA(cudaGetLastError());
+}
+
+void launch_project_backward_explicit(sk_ctx* ctx, sk_scene* s, const sk_camera& cam, const float* up_mu,
+                                      const float* up_cov, const float* up_col, const float* up_op) {
+  ensure_optimizer_state(ctx, s);
+  if (s->n == 0) return;
+  const CamParams cp = make_cam_params(cam);
+  const unsigned grid = (unsigned)((s->n + kPbThreads - 1) / kPbThreads);
+  auto go = [&](auto kern) {
+    kern<<<grid, kPbThreads, 0, ctx->stream>>>(s->params.as<float>(), s->capacity, s->n, cp, up_mu, up_cov, up_col,
+                                               up_op, s->grads.as<float>());
+  };
+  switch (s->sh_degree) {
+    case 0: go(project_bwd_explicit_kernel<0>); break;
+    case 1: go(project_bwd_explicit_kernel<1>); break;
+    case 2: go(project_bwd_explicit_kernel<2>); break;
+    default: go(project_bwd_explicit_kernel<3>); break;
+  }
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+}
+
+void remap_moments(sk_ctx* ctx, sk_scene* s, const int32_t* old_to_new_dev, int64_t new_n) {
+  ensure_optimizer_state(ctx, s);
+  const int64_t new_cap = std::max(s->capacity, round_capacity(new_n));
+  const size_t cells = (size_t)s->comps * new_cap;
+  DevBuf& nm = s->adam_m_alt;
+  DevBuf& nv = s->adam_v_alt;
+  ensure<float>(nm, cells);
+  ensure<float>(nv, cells);
+  SK_CUDA(cudaMemsetAsync(nm.ptr, 0, cells * sizeof(float), ctx->stream));
+  SK_CUDA(cudaMemsetAsync(nv.ptr, 0, cells * sizeof(float), ctx->stream));
+  if (s->n > 0) {
+    remap_moments_kernel<<<dim3((unsigned)((s->n + 255) / 256), (unsigned)s->comps), 256, 0, ctx->stream>>>(
+        s->adam_m.as<float>(), s->adam_v.as<float>(), s->capacity, s->n, old_to_new_dev, nm.as<float>(),
+        nv.as<float>(), new_cap);
+    note_launch();
+    SK_CUDA(cudaGetLastError());
+  }
+  s->adam_m.swap(nm);
+  s->adam_v.swap(nv);
+  if (new_cap != s->capacity) {
+    // the parameter buffer follows the new stride (its values are replaced by
+    // the caller's next sk_scene_set_params)
+    DevBuf np;
+    ensure<float>(np, cells);
+    s->params.swap(np);
+    s->capacity = new_cap;
+    s->grads.release();
+    for (DevBuf* b : {&s->s_d, &s->s_p_raw, &s->s_p, &s->grad_norm_acc, &s->abs_grad_acc, &s->grad3d_acc,
+                      &s->views_seen, &s->max_radius2d})
+      b->release();
+  }
+  s->n = new_n;
+  s->rest_n = -1;
+  ensure_optimizer_state(ctx, s);
+}
+
+void adam_step_sh_rest(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs) {
+  ensure_optimizer_state(ctx, s);
+  if (s->sh_degree == 0) return;
+  // SceneOptimizer::step_sh_rest (adam.hpp:146-153): the SH-rest group alone
+  AdamParams ap = make_adam(s, lrs, 0.0f, true);
+  for (int g = 0; g < 5; ++g) {
+    if (ap.active[g]) s->adam_t[g] -= 1;
+    ap.active[g] = 0;
+  }
+  adam_range(ctx, s, ap, s->grads.as<float>(), s->capacity, 0, s->n);
+}
+
+void reset_opacity_state(sk_ctx* ctx, sk_scene* s) {
+  ensure_optimizer_state(ctx, s);
+  const size_t o = (size_t)SK_COMP_OPACITY * s->capacity;
+  SK_CUDA(cudaMemsetAsync(s->adam_m.as<float>() + o, 0, sizeof(float) * s->capacity, ctx->stream));
+  SK_CUDA(cudaMemsetAsync(s->adam_v.as<float>() + o, 0, sizeof(float) * s->capacity, ctx->stream));
 }
 
 // Single-GPU step: K9 into the gradient buffer, then the streaming K10. (A

@@ -264,6 +264,16 @@ void launch_adam_shard(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float
 // gradients; when due, an Adam step of the SH-rest group on the accumulator,
 // which is then cleared.
 void lazy_sh_rest(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, bool due);
+// project_backward with explicit upstream gradients (device arrays), every
+// Gaussian, into the gradient buffer (C++ API project_backward).
+void launch_project_backward_explicit(sk_ctx* ctx, sk_scene* s, const sk_camera& cam, const float* up_mu,
+                                      const float* up_cov, const float* up_col, const float* up_op);
+// AdamGroup::remap (adam.hpp:45-58) of every group; the scene size becomes new_n.
+void remap_moments(sk_ctx* ctx, sk_scene* s, const int32_t* old_to_new_dev, int64_t new_n);
+// SceneOptimizer::step_sh_rest (adam.hpp:146-153) from the gradient buffer.
+void adam_step_sh_rest(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs);
+// SceneOptimizer::reset_opacity_state (adam.hpp:157-160).
+void reset_opacity_state(sk_ctx* ctx, sk_scene* s);
 // Trainer::reset_opacity (trainer.hpp:245-249): opacity_logit = min(.,
 // logit(0.01)), the opacity group's Adam moments zeroed.
 void reset_opacity(sk_ctx* ctx, sk_scene* s);

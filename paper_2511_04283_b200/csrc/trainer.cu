@@ -389,6 +389,76 @@ int sk_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const sk_lea
   });
 }
 
+int sk_project_backward_explicit(sk_ctx* ctx, sk_scene* s, const sk_camera* cam, const float* d_mu2d,
+                                 const float* d_cov2d, const float* d_color, const float* d_opacity,
+                                 float* grads_host) {
+  return guarded(ctx, [&] {
+    arg(s && cam && (s->n == 0 || (d_mu2d && d_cov2d && d_color && d_opacity)),
+        "project_backward: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    const int64_t n = s->n;
+    DevBuf up;
+    float* u = ensure<float>(up, 10 * (size_t)std::max<int64_t>(n, 1));
+    if (n > 0) {
+      h2d(ctx, u, d_mu2d, 2 * n);
+      h2d(ctx, u + 2 * n, d_cov2d, 4 * n);
+      h2d(ctx, u + 6 * n, d_color, 3 * n);
+      h2d(ctx, u + 9 * n, d_opacity, n);
+    }
+    launch_project_backward_explicit(ctx, s, *cam, u, u + 2 * n, u + 6 * n, u + 9 * n);
+    if (grads_host && n > 0)
+      SK_CUDA(cudaMemcpy2DAsync(grads_host, sizeof(float) * n, s->grads.ptr, sizeof(float) * s->capacity,
+                                sizeof(float) * n, s->comps, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+  });
+}
+
+int sk_scene_set_params(sk_ctx* ctx, sk_scene* s, const float* host, int64_t n) {
+  return guarded(ctx, [&] {
+    arg(s && (host || n == 0), "sk_scene_set_params: bad arguments");
+    arg(n == s->n, "sk_scene_set_params: size differs from the scene (use sk_scene_upload to resize)");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    if (n > 0)
+      SK_CUDA(cudaMemcpy2DAsync(s->params.ptr, sizeof(float) * s->capacity, host, sizeof(float) * n,
+                                sizeof(float) * n, s->comps, cudaMemcpyHostToDevice, ctx->stream));
+    sync(ctx);
+  });
+}
+
+int sk_scene_remap_moments(sk_ctx* ctx, sk_scene* s, const int32_t* old_to_new, int64_t new_n) {
+  return guarded(ctx, [&] {
+    arg(s && (old_to_new || s->n == 0) && new_n >= 0, "SceneOptimizer::remap: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    for (int64_t i = 0; i < s->n; ++i)
+      arg(old_to_new[i] >= -1 && old_to_new[i] < new_n, "SceneOptimizer::remap: index out of range");
+    gather_moments(s, ctx->stream);
+    DevBuf o2n;
+    int32_t* d = ensure<int32_t>(o2n, (size_t)std::max<int64_t>(s->n, 1));
+    if (s->n > 0) h2d(ctx, d, old_to_new, s->n);
+    remap_moments(ctx, s, d, new_n);
+    sync(ctx);
+  });
+}
+
+int sk_adam_step_sh_rest(sk_ctx* ctx, sk_scene* s, const sk_learning_rates* l) {
+  return guarded(ctx, [&] {
+    arg(s && l, "sk_adam_step_sh_rest: bad arguments");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    LearningRates lr{l->position, l->position_final, l->sh_dc, l->sh_rest, l->opacity, l->scale, l->rotation};
+    adam_step_sh_rest(ctx, s, lr);
+    sync(ctx);
+  });
+}
+
+int sk_adam_reset_opacity_state(sk_ctx* ctx, sk_scene* s) {
+  return guarded(ctx, [&] {
+    arg(s != nullptr, "sk_adam_reset_opacity_state: null scene");
+    SK_CUDA(cudaSetDevice(ctx->device));
+    reset_opacity_state(ctx, s);
+    sync(ctx);
+  });
+}
+
 int sk_scene_get_adam(sk_ctx* ctx, const sk_scene* s, float* m, float* v, int64_t* t6) {
   return guarded(ctx, [&] {
     arg(s != nullptr, "sk_scene_get_adam: null scene");

@@ -1,0 +1,713 @@
+// The reference's own known-answer tests for the densify / prune, optimizer
+// and trainer surface, ported onto the splat:: C++ API of this library
+// (include/splatkit_b200.hpp) and run on the GPU:
+//   tests/test_adc.cpp:39-332      scores, selection, compaction
+//   tests/test_adam.cpp:13-97      optimizer step / decay / remap, expon_lr, lazy schedule
+//   tests/test_trainer.cpp:60-137  zero iterations, constant count, loss decrease, schedule, dry run
+//   tests/test_raster.cpp:146-156, tests/test_camera.cpp:23-36, tests/test_dataset.cpp  (smoke)
+// The reference instantiates most KATs with T = double; this GPU path computes
+// in fp32, so exact double-precision equalities become fp32 tolerances
+// (noted per check). Exit code 0 = every check passed.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <functional>
+#include <set>
+#include <string>
+
+#include "splatkit_b200.hpp"
+
+using namespace splat;
+
+static int failures = 0, checks = 0;
+#define CHECK(c)                                                \
+  do {                                                          \
+    ++checks;                                                   \
+    if (!(c)) {                                                 \
+      std::printf("FAILED %s:%d %s\n", __FILE__, __LINE__, #c); \
+      ++failures;                                               \
+    }                                                           \
+  } while (0)
+#define CHECK_THROWS(expr)      \
+  do {                          \
+    bool threw_ = false;        \
+    try {                       \
+      expr;                     \
+    } catch (const std::exception&) { \
+      threw_ = true;            \
+    }                           \
+    CHECK(threw_);              \
+  } while (0)
+
+static bool near(double a, double b, double rel = 1e-5, double abs_tol = 1e-7) {
+  return std::fabs(a - b) <= std::max(abs_tol, rel * std::max(std::fabs(a), std::fabs(b)));
+}
+
+// ---- test scenes (tests/helpers.hpp:100-131 distributions) ----------------------
+template <typename T>
+static Scene<T> random_scene(Rng& rng, int n, int sh_degree = 2, double max_opacity = 0.8) {
+  Scene<T> scene;
+  scene.sh_degree = sh_degree;
+  for (int i = 0; i < n; ++i) {
+    Gaussian3D<T> g;
+    g.mu = Vec3<T>(T(rng.uniform(-0.6, 0.6)), T(rng.uniform(-0.6, 0.6)), T(rng.uniform(2.0, 5.0)));
+    Vec4<T> q;
+    for (int d = 0; d < 4; ++d) q[d] = T(rng.normal());
+    const T qn = q.norm();
+    for (int d = 0; d < 4; ++d) g.rot[d] = q[d] / qn;
+    for (int d = 0; d < 3; ++d) g.log_scale[d] = T(std::log(rng.uniform(0.03, 0.15)));
+    g.opacity_logit = logit(T(rng.uniform(0.1, max_opacity)));
+    g.sh = ShMatrix<T>::Zero(sh_coeff_count(sh_degree), 3);
+    for (int m = 0; m < sh_coeff_count(sh_degree); ++m)
+      for (int c = 0; c < 3; ++c) g.sh(m, c) = T(rng.uniform(-0.3, 0.3)) + (m == 0 ? T(rng.uniform(0.2, 1.2)) : T(0));
+    scene.gaussians.push_back(g);
+  }
+  return scene;
+}
+
+template <typename T>
+static Camera<T> default_camera(int width = 32, int height = 32) {
+  Camera<T> cam;
+  cam.width = width;
+  cam.height = height;
+  cam.fx = cam.fy = T(0.9) * width;
+  cam.cx = T(width - 1) / T(2);
+  cam.cy = T(height - 1) / T(2);
+  return cam;
+}
+
+static Scene<double> two_gaussian_scene() {
+  Scene<double> scene;
+  scene.sh_degree = 0;
+  for (int i = 0; i < 2; ++i) {
+    Gaussian3D<double> g;
+    g.mu = Vec3<double>(i == 0 ? -0.3 : 0.3, 0, 3);
+    g.log_scale = Vec3<double>::Constant(std::log(0.08));
+    g.opacity_logit = logit(0.8);
+    g.sh = ShMatrix<double>::Zero(1, 3);
+    g.sh(0, 0) = i == 0 ? 1.2 : -0.8;
+    g.sh(0, 1) = g.sh(0, 2) = 0.2;
+    scene.gaussians.push_back(g);
+  }
+  return scene;
+}
+
+static ScoreTable<double> table_with(int n, const std::function<void(ScoreTable<double>&)>& fill) {
+  ScoreTable<double> t;
+  t.reset(n);
+  fill(t);
+  return t;
+}
+
+// Untiled per-pixel renderer over every Gaussian in (depth, index) order — the
+// independent check of accumulate_scores (tests/helpers.hpp:20-62 semantics).
+static void brute_force(const std::vector<ProjectedGaussian<double>>& pgs, int w, int h, Image<double>* image,
+                        const MaskMap* mask, std::vector<int>* counts) {
+  std::vector<int> order(pgs.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    return pgs[a].depth != pgs[b].depth ? pgs[a].depth < pgs[b].depth : a < b;
+  });
+  for (int py = 0; py < h; ++py)
+    for (int px = 0; px < w; ++px) {
+      double trans = 1;
+      Vec3<double> c;
+      const bool masked = mask && (*mask)(py, px) != 0;
+      for (const int idx : order) {
+        const auto& pg = pgs[idx];
+        const double dx = px - pg.mu2d[0], dy = py - pg.mu2d[1];
+        const double q = pg.cov2d_inv(0, 0) * dx * dx + 2 * pg.cov2d_inv(0, 1) * dx * dy + pg.cov2d_inv(1, 1) * dy * dy;
+        if (q < 0) continue;
+        const double alpha = std::min(kAlphaCap, pg.opacity * std::exp(-0.5 * q));
+        if (alpha < kAlphaMin) continue;
+        for (int k = 0; k < 3; ++k) c[k] += trans * alpha * pg.color[k];
+        if (masked && counts) ++(*counts)[pg.source_index];
+        trans *= 1 - alpha;
+        if (trans < kTransmitMin) break;
+      }
+      if (image) image->at(px, py) = c;
+    }
+}
+
+// ---- tests/test_adc.cpp ------------------------------------------------------------
+static void adc_kats() {
+  {  // densify score is the mean count across sampled views
+    ScoreTable<double> table;
+    scores_from_counts<double>({{3}, {5}}, {0.1, 0.1}, table);
+    CHECK(table.s_d[0] == 4.0);
+  }
+  {  // pruning score weights counts by photometric loss then min-max normalizes
+    ScoreTable<double> table;
+    scores_from_counts<double>({{4, 0}}, {0.25}, table);
+    CHECK(table.s_p_raw[0] == 1.0 && table.s_p_raw[1] == 0.0);
+    CHECK(table.s_p[0] == 1.0 && table.s_p[1] == 0.0);
+  }
+  {  // min-max normalization degenerate population goes to zeros
+    CHECK(minmax_normalize<double>({0.7, 0.7, 0.7}) == (std::vector<double>{0, 0, 0}));
+    CHECK(minmax_normalize<double>({}).empty());
+    const auto n = minmax_normalize<double>({2.0, 6.0, 10.0});
+    CHECK(n[0] == 0.0 && near(n[1], 0.5) && n[2] == 1.0);
+  }
+  {  // s_p invariant under positive rescaling
+    const std::vector<double> raw = {0.0, 3.0, 1.5, 7.5};
+    std::vector<double> scaled = raw;
+    for (auto& v : scaled) v *= 42.0;
+    const auto a = minmax_normalize(raw), b = minmax_normalize(scaled);
+    for (size_t i = 0; i < raw.size(); ++i) CHECK(near(a[i], b[i], 1e-12));
+  }
+  {  // accumulate_scores matches an independent per-view reconstruction
+    Rng rng(71);
+    Scene<double> scene = random_scene<double>(rng, 8, 0, 0.7);
+    const Camera<double> cam_a = default_camera<double>(24, 24);
+    Camera<double> cam_b = cam_a;
+    cam_b.world_to_cam(0, 3) = 0.15;
+    Image<double> gt_a(24, 24), gt_b(24, 24);
+    for (auto& p : gt_a.pixels) p = Vec3<double>(0.1, 0.1, 0.1);
+    for (auto& p : gt_b.pixels) p = Vec3<double>(0.6, 0.2, 0.1);
+    ScoreTable<double> table;
+    table.reset(scene.size());
+    accumulate_scores<double>(scene, {{&cam_a, &gt_a}, {&cam_b, &gt_b}}, 0.5, 0.2, BinningConfig<double>{}, 16, table);
+    std::vector<std::vector<int>> counts;
+    std::vector<double> photometric;
+    for (const auto& [cam, gt] : std::vector<std::pair<const Camera<double>*, Image<double>*>>{{&cam_a, &gt_a},
+                                                                                                {&cam_b, &gt_b}}) {
+      const auto pgs = project_scene(scene, *cam);
+      Image<double> rendered(24, 24);
+      brute_force(pgs, 24, 24, &rendered, nullptr, nullptr);
+      const auto maps = build_error_maps(rendered, *gt, 0.5, 0.2);
+      std::vector<int> c(scene.size(), 0);
+      brute_force(pgs, 24, 24, nullptr, &maps.mask, &c);
+      counts.push_back(c);
+      photometric.push_back(maps.photometric);
+    }
+    for (int i = 0; i < scene.size(); ++i) {
+      CHECK(near(table.s_d[i], 0.5 * (counts[0][i] + counts[1][i])));
+      CHECK(near(table.s_p_raw[i], counts[0][i] * photometric[0] + counts[1][i] * photometric[1], 1e-4));
+    }
+  }
+  {  // a gaussian culled in every view scores zero and is never densified
+    Scene<double> scene = two_gaussian_scene();
+    scene.gaussians[1].mu = Vec3<double>(0, 0, -5);
+    const Camera<double> cam = default_camera<double>(24, 24);
+    Image<double> gt(24, 24);
+    ScoreTable<double> table;
+    table.reset(scene.size());
+    accumulate_scores<double>(scene, {{&cam, &gt}}, 0.5, 0.2, BinningConfig<double>{}, 16, table);
+    CHECK(table.s_d[1] == 0.0 && table.s_p_raw[1] == 0.0);
+    table.grad_norm_acc[1] = 100.0;
+    table.abs_grad_acc[1] = 100.0;
+    const auto sel = select_densify(table, scene, DensifyParams<double>{}, 1.0);
+    CHECK(std::find(sel.clone.begin(), sel.clone.end(), 1) == sel.clone.end());
+    CHECK(std::find(sel.split.begin(), sel.split.end(), 1) == sel.split.end());
+  }
+  {  // accumulate_scores requires at least one view
+    const Scene<double> scene = two_gaussian_scene();
+    ScoreTable<double> table;
+    table.reset(scene.size());
+    CHECK_THROWS(accumulate_scores<double>(scene, {}, 0.5, 0.2, BinningConfig<double>{}, 16, table));
+  }
+  {  // select_densify needs both the score and the gradient criterion
+    Scene<double> scene = two_gaussian_scene();
+    scene.gaussians[0].log_scale = Vec3<double>::Constant(std::log(0.001));
+    DensifyParams<double> params;
+    auto t1 = table_with(2, [](ScoreTable<double>& t) {
+      t.s_d = {3.0, 0.0};
+      t.grad_norm_acc = {1.0, 0.0};
+      t.views_seen = {1, 1};
+    });
+    CHECK(select_densify(t1, scene, params, 1.0).clone.empty());
+    auto t2 = table_with(2, [](ScoreTable<double>& t) {
+      t.s_d = {100.0, 0.0};
+      t.grad_norm_acc = {1e-6, 0.0};
+      t.views_seen = {1, 1};
+    });
+    CHECK(select_densify(t2, scene, params, 1.0).clone.empty());
+    CHECK(select_densify(t2, scene, params, 1.0).split.empty());
+    auto t3 = table_with(2, [&](ScoreTable<double>& t) {
+      t.s_d = {6.0, 0.0};
+      t.grad_norm_acc = {2 * params.grad_threshold, 0.0};
+      t.views_seen = {1, 1};
+    });
+    const auto sel = select_densify(t3, scene, params, 1.0);
+    CHECK(sel.clone == std::vector<int>{0});
+    CHECK(sel.split.empty());
+  }
+  {  // select_densify routes large gaussians to split by the absolute gradient
+    Scene<double> scene = two_gaussian_scene();
+    scene.gaussians[0].log_scale = Vec3<double>::Constant(std::log(0.5));
+    DensifyParams<double> params;
+    auto t = table_with(2, [&](ScoreTable<double>& t) {
+      t.s_d = {9.0, 9.0};
+      t.grad_norm_acc = {0.0, 0.0};
+      t.abs_grad_acc = {10 * params.grad_threshold, 0.0};
+      t.views_seen = {1, 1};
+    });
+    const auto sel = select_densify(t, scene, params, 1.0);
+    CHECK(sel.split == std::vector<int>{0});
+    CHECK(sel.clone.empty());
+  }
+  {  // vcd selection is a subset of the gradient-only selection
+    Rng rng(72);
+    Scene<double> scene = random_scene<double>(rng, 40);
+    auto t = table_with(40, [&](ScoreTable<double>& t) {
+      for (int i = 0; i < 40; ++i) {
+        t.s_d[i] = rng.uniform(0, 12);
+        t.grad_norm_acc[i] = rng.uniform(0, 6e-4);
+        t.abs_grad_acc[i] = rng.uniform(0, 6e-4);
+        t.views_seen[i] = 1;
+      }
+    });
+    DensifyParams<double> with_vcd, gradient_only;
+    gradient_only.use_vcd = false;
+    const auto a = select_densify(t, scene, with_vcd, 1.0);
+    const auto b = select_densify(t, scene, gradient_only, 1.0);
+    for (const int i : a.clone) CHECK(std::find(b.clone.begin(), b.clone.end(), i) != b.clone.end());
+    for (const int i : a.split) CHECK(std::find(b.split.begin(), b.split.end(), i) != b.split.end());
+    CHECK(b.clone.size() + b.split.size() > a.clone.size() + a.split.size());
+  }
+  // apply_densify cardinality and child parameters (five subcases, fresh scene each)
+  auto fresh = [](Rng& rng, ScoreTable<double>& table) {
+    Scene<double> s = random_scene<double>(rng, 5);
+    table.reset(5);
+    return s;
+  };
+  {
+    Rng rng(73);
+    ScoreTable<double> table;
+    Scene<double> scene = fresh(rng, table);
+    const Scene<double> before = scene;
+    apply_densify(scene, {}, {}, table, 0.01, rng);
+    CHECK(scene.size() == 5);
+    for (int i = 0; i < 5; ++i)
+      for (int d = 0; d < 3; ++d) CHECK(near(scene.gaussians[i].mu[d], before.gaussians[i].mu[d], 1e-7));
+  }
+  {
+    Rng rng(73);
+    ScoreTable<double> table;
+    Scene<double> scene = fresh(rng, table);
+    const Gaussian3D<double> parent = scene.gaussians[2];
+    const auto remap = apply_densify(scene, {}, {2}, table, 0.01, rng);
+    CHECK(scene.size() == 6);
+    CHECK(remap.old_to_new[2] == -1);
+    for (int c = 0; c < 2; ++c) {
+      const auto& child = scene.gaussians[4 + c];
+      for (int d = 0; d < 3; ++d) CHECK(near(child.log_scale[d], parent.log_scale[d] - std::log(1.6), 1e-6));
+      for (int d = 0; d < 4; ++d) CHECK(near(child.rot[d], parent.rot[d], 1e-7));
+      CHECK(near(child.opacity_logit, parent.opacity_logit, 1e-7));
+    }
+  }
+  {
+    Rng rng(73);
+    ScoreTable<double> table;
+    Scene<double> scene = fresh(rng, table);
+    scene.gaussians[0].log_scale = Vec3<double>::Constant(std::log(1.6));
+    apply_densify(scene, {}, {0}, table, 0.01, rng);
+    const auto& child = scene.gaussians.back();
+    for (int d = 0; d < 3; ++d) CHECK(near(child.scale()[d], 1.0, 1e-6));  // reference: 1e-12 in double
+  }
+  {
+    Rng rng(73);
+    ScoreTable<double> table;
+    Scene<double> scene = fresh(rng, table);
+    table.grad3d_acc[1] = Vec3<double>(1.0, -2.0, 0.5);
+    table.views_seen[1] = 2;
+    const Vec3<double> parent_mu = scene.gaussians[1].mu;
+    const auto remap = apply_densify(scene, {1}, {}, table, 0.01, rng);
+    CHECK(scene.size() == 6);
+    CHECK(remap.old_to_new[1] == 1);
+    const Vec3<double> expected(parent_mu[0] - 0.01 * 0.5, parent_mu[1] + 0.01, parent_mu[2] - 0.01 * 0.25);
+    double err = 0;
+    for (int d = 0; d < 3; ++d) err += std::pow(scene.gaussians[5].mu[d] - expected[d], 2);
+    CHECK(std::sqrt(err) < 1e-6);  // reference: 1e-12 in double
+  }
+  {
+    Rng rng(73);
+    ScoreTable<double> table;
+    Scene<double> scene = fresh(rng, table);
+    apply_densify(scene, {0, 3}, {1}, table, 0.01, rng);
+    CHECK(scene.size() == 5 + 2 + 1);
+  }
+  {  // select_prune late phase: opacity and score rules
+    Scene<double> scene = two_gaussian_scene();
+    scene.gaussians.push_back(scene.gaussians[0]);
+    scene.gaussians[0].opacity_logit = logit(0.05);
+    scene.gaussians[1].opacity_logit = logit(0.5);
+    scene.gaussians[2].opacity_logit = logit(0.5);
+    auto t = table_with(3, [](ScoreTable<double>& t) { t.s_p = {0.2, 0.95, 0.5}; });
+    CHECK(select_prune(t, scene, 15000, PruneParams<double>{}, 1.0) == (std::vector<int>{0, 1}));
+  }
+  {  // select_prune early phase keeps the top-scoring half of vanilla candidates
+    Scene<double> scene;
+    scene.sh_degree = 0;
+    for (int i = 0; i < 6; ++i) {
+      Gaussian3D<double> g;
+      g.mu = Vec3<double>(0, 0, 3);
+      g.log_scale = Vec3<double>::Constant(std::log(0.05));
+      g.opacity_logit = logit(i < 4 ? 0.004 : 0.5);
+      g.sh = ShMatrix<double>::Zero(1, 3);
+      scene.gaussians.push_back(g);
+    }
+    auto t = table_with(6, [](ScoreTable<double>& t) { t.s_p = {0.1, 0.2, 0.8, 0.9, 0.0, 0.0}; });
+    CHECK(select_prune(t, scene, 1000, PruneParams<double>{}, 1.0) == (std::vector<int>{2, 3}));
+  }
+  {  // select_prune early phase without vcp prunes every vanilla candidate
+    Scene<double> scene = two_gaussian_scene();
+    scene.gaussians[0].opacity_logit = logit(0.004);
+    PruneParams<double> params;
+    params.use_vcp = false;
+    auto t = table_with(2, [](ScoreTable<double>& t) { t.s_p = {0.0, 0.0}; });
+    CHECK(select_prune(t, scene, 1000, params, 1.0) == std::vector<int>{0});
+  }
+  {  // oversize rules activate only after size_prune_from
+    Scene<double> scene = two_gaussian_scene();
+    scene.gaussians[0].log_scale = Vec3<double>::Constant(std::log(0.5));
+    auto t = table_with(2, [](ScoreTable<double>& t) { t.s_p = {1.0, 0.0}; });
+    CHECK(select_prune(t, scene, 1000, PruneParams<double>{}, 1.0).empty());
+    CHECK(select_prune(t, scene, 4000, PruneParams<double>{}, 1.0) == std::vector<int>{0});
+  }
+  {  // select_prune never empties the scene
+    Scene<double> scene = two_gaussian_scene();
+    scene.gaussians[0].opacity_logit = logit(0.01);
+    scene.gaussians[1].opacity_logit = logit(0.01);
+    auto t = table_with(2, [](ScoreTable<double>& t) { t.s_p = {0.4, 0.6}; });
+    CHECK(select_prune(t, scene, 20000, PruneParams<double>{}, 1.0) == std::vector<int>{1});
+  }
+  {  // apply_prune compacts the scene and reports the remap
+    Rng rng(74);
+    Scene<double> scene = random_scene<double>(rng, 5);
+    const Vec3<double> kept_mu = scene.gaussians[3].mu;
+    const auto remap = apply_prune(scene, {0, 2});
+    CHECK(scene.size() == 3);
+    CHECK(remap.old_to_new[0] == -1 && remap.old_to_new[1] == 0 && remap.old_to_new[3] == 1);
+    for (int d = 0; d < 3; ++d) CHECK(near(scene.gaussians[1].mu[d], kept_mu[d], 1e-7));
+  }
+}
+
+// ---- tests/test_adam.cpp through SceneOptimizer --------------------------------------
+static Scene<float> one_gaussian(float mu0) {
+  Scene<float> s;
+  s.sh_degree = 0;
+  Gaussian3D<float> g;
+  g.mu = Vec3<float>(mu0, 0, 3);
+  g.sh = ShMatrix<float>::Zero(1, 3);
+  s.gaussians.push_back(g);
+  return s;
+}
+
+static void adam_kats() {
+  {  // first step moves by ~lr against the gradient sign
+    Scene<float> s = one_gaussian(1.0f);
+    SceneOptimizer<float> opt;
+    opt.init(s);
+    SceneGrads<float> g;
+    g.init(s);
+    g.per_gaussian[0].mu[0] = 0.37f;
+    opt.step(s, g, LearningRates<float>{}, 1e-2f);
+    CHECK(near(s.gaussians[0].mu[0], 1.0 - 1e-2, 1e-6));
+  }
+  {  // zero gradient: momentum still moves the parameter, moments decay; idle stays frozen
+    Scene<float> s = one_gaussian(2.5f);
+    SceneOptimizer<float> opt;
+    opt.init(s);
+    SceneGrads<float> g;
+    g.init(s);
+    g.per_gaussian[0].mu[0] = 1.0f;
+    opt.step(s, g, LearningRates<float>{}, 1e-2f);
+    const float after_one = s.gaussians[0].mu[0];
+    std::vector<float> m1, v1, m2, v2;
+    int64_t t[6];
+    opt.moments(&m1, &v1, t);
+    g.per_gaussian[0].mu[0] = 0.0f;
+    opt.step(s, g, LearningRates<float>{}, 1e-2f);
+    opt.moments(&m2, &v2, t);
+    CHECK(s.gaussians[0].mu[0] != after_one);
+    CHECK(near(m2[SK_COMP_MU], kAdamBeta1 * m1[SK_COMP_MU]));
+    CHECK(near(v2[SK_COMP_MU], kAdamBeta2 * v1[SK_COMP_MU]));
+    Scene<float> idle = one_gaussian(-3.0f);
+    SceneOptimizer<float> o2;
+    o2.init(idle);
+    SceneGrads<float> z;
+    z.init(idle);
+    o2.step(idle, z, LearningRates<float>{}, 1e-2f);
+    CHECK(idle.gaussians[0].mu[0] == -3.0f);
+  }
+  {  // remap keeps survivor moments and zeroes new slots
+    Scene<float> s;
+    s.sh_degree = 0;
+    for (int i = 0; i < 3; ++i) s.gaussians.push_back(one_gaussian(0.1f * i).gaussians[0]);
+    SceneOptimizer<float> opt;
+    opt.init(s);
+    SceneGrads<float> g;
+    g.init(s);
+    for (int i = 0; i < 3; ++i) g.per_gaussian[i].mu[0] = 10.0f + i;
+    opt.step(s, g, LearningRates<float>{}, 1e-3f);
+    std::vector<float> m0;
+    int64_t t[6];
+    opt.moments(&m0, nullptr, t);
+    IndexRemap remap;
+    remap.old_to_new = {1, -1, 0};
+    remap.new_size = 3;
+    opt.remap(remap);
+    std::vector<float> m1;
+    opt.moments(&m1, nullptr, t);
+    const int n = 3;  // planar [C][n]: component MU x is row 0
+    CHECK(m1[1] == m0[0]);  // old 0 moved to 1
+    CHECK(m1[0] == m0[2]);  // old 2 moved to 0
+    CHECK(m1[2] == 0.0f);   // new slot
+    CHECK(t[0] == 1);       // step counters kept
+    (void)n;
+  }
+  {  // expon_lr endpoints
+    CHECK(near(expon_lr(1.6e-4, 1.6e-6, 0, 30000), 1.6e-4, 1e-9));
+    CHECK(near(expon_lr(1.6e-4, 1.6e-6, 30000, 30000), 1.6e-6, 1e-9));
+    CHECK(near(expon_lr(1.6e-4, 1.6e-6, 15000, 30000), std::sqrt(1.6e-4 * 1.6e-6), 1e-9));
+    CHECK(near(expon_lr(1.6e-4, 1.6e-6, 40000, 30000), 1.6e-6, 1e-9));
+  }
+  {  // lazy optimizer schedule
+    TrainConfig cfg;
+    cfg.lazy_opt_enabled = true;
+    CHECK(lazy_update_due(1, cfg) && lazy_update_due(14999, cfg) && lazy_update_due(15008, cfg));
+    CHECK(!lazy_update_due(15010, cfg) && lazy_update_due(16000, cfg) && !lazy_update_due(16016, cfg));
+    CHECK(!lazy_update_due(20010, cfg) && lazy_update_due(20480, cfg));
+    cfg.lazy_opt_enabled = false;
+    CHECK(lazy_update_due(15010, cfg));
+  }
+}
+
+// ---- tests/test_trainer.cpp -----------------------------------------------------------
+static Dataset<float> tiny_dataset(Rng& rng, int n_views, int size, int n_gaussians) {
+  Dataset<float> data;
+  Scene<float> gt = random_scene<float>(rng, n_gaussians, 1, 0.9);
+  for (int v = 0; v < n_views; ++v) {
+    Camera<float> cam = default_camera<float>(size, size);
+    cam.world_to_cam(0, 3) = 0.25f * (v - n_views / 2);
+    const auto pgs = project_scene(gt, cam);
+    const TileGrid grid = build_tile_grid(pgs, size, size, BinningConfig<float>{});
+    data.cameras.push_back(cam);
+    data.camera_ids.push_back(v);
+    data.images.push_back(blend_forward(grid, pgs).image);
+  }
+  for (const auto& g : gt.gaussians) {
+    Vec3<float> color;
+    for (int c = 0; c < 3; ++c) color[c] = std::clamp(0.5f + float(kShC0) * g.sh(0, c), 0.0f, 1.0f);
+    Vec3<float> p;
+    for (int d = 0; d < 3; ++d) p[d] = g.mu[d] + float(rng.normal()) * 0.02f;
+    data.init_points.push_back({p, color});
+  }
+  for (int v = 0; v < n_views; ++v) (v % 8 == 0 ? data.test_indices : data.train_indices).push_back(v);
+  data.extent = 1.1f;
+  return data;
+}
+
+static TrainConfig fast_config() {
+  TrainConfig cfg;
+  cfg.iterations = 40;
+  cfg.k = 2;
+  cfg.densify_from = 10;
+  cfg.densify_until = 30;
+  cfg.densify_every = 10;
+  cfg.prune_every_early = 10;
+  cfg.prune_every_late = 5;
+  cfg.sh_degree = 1;
+  cfg.seed = 7;
+  return cfg;
+}
+
+static void trainer_kats() {
+  {  // zero iterations returns the initial scene and an empty log
+    Rng rng(91);
+    const auto data = tiny_dataset(rng, 4, 24, 6);
+    Scene<float> scene = init_from_points(data.init_points, 1);
+    TrainConfig cfg = fast_config();
+    cfg.iterations = 0;
+    const auto result = run_training(scene, data, cfg);
+    CHECK(result.log.empty());
+    CHECK(result.scene.size() == scene.size());
+    for (int i = 0; i < scene.size(); ++i) CHECK(result.scene.gaussians[i].mu == scene.gaussians[i].mu);
+  }
+  {  // gaussian count stays constant with density control disabled
+    Rng rng(92);
+    const auto data = tiny_dataset(rng, 4, 24, 6);
+    Scene<float> scene = init_from_points(data.init_points, 1);
+    TrainConfig cfg = fast_config();
+    cfg.densify_from = 1000;
+    cfg.densify_until = 2000;
+    cfg.densify_every = 100;
+    cfg.prune_every_early = 100;
+    cfg.prune_every_late = 100;
+    const auto result = run_training(scene, data, cfg);
+    CHECK(int(result.log.size()) == cfg.iterations);
+    for (const auto& row : result.log) CHECK(row.gaussians == scene.size());
+  }
+  {  // training reduces the loss on the training views
+    Rng rng(93);
+    const auto data = tiny_dataset(rng, 4, 32, 8);
+    Scene<float> scene = init_from_points(data.init_points, 1);
+    TrainConfig cfg = fast_config();
+    cfg.iterations = 150;
+    cfg.densify_from = 40;
+    cfg.densify_until = 120;
+    cfg.densify_every = 40;
+    cfg.prune_every_early = 40;
+    cfg.prune_every_late = 40;
+    const auto result = run_training(scene, data, cfg);
+    double early = 0, late = 0;
+    for (int i = 0; i < 10; ++i) early += result.log[i].loss;
+    for (int i = 0; i < 10; ++i) late += result.log[result.log.size() - 1 - i].loss;
+    CHECK(late < early);
+  }
+  {  // schedule fires the documented event iterations
+    TrainConfig cfg;
+    std::set<int> densify, prune;
+    for (int it = 1; it <= 30000; ++it) {
+      if (densify_due(it, cfg)) densify.insert(it);
+      if (prune_due(it, cfg)) prune.insert(it);
+    }
+    CHECK(densify.size() == 30 && densify.count(500) && densify.count(15000) && !densify.count(15500));
+    CHECK(prune.count(15000) && prune.count(18000) && !prune.count(16000) && prune.count(30000));
+  }
+  {  // dry-run scheduling through Trainer::run callbacks matches the predicates
+    Rng rng(94);
+    const auto data = tiny_dataset(rng, 3, 16, 4);
+    Scene<float> scene = init_from_points(data.init_points, 1);
+    TrainConfig cfg = fast_config();
+    cfg.iterations = 60;
+    cfg.schedule_dry_run = true;
+    std::vector<int> densify_events, prune_events, iterations;
+    TrainCallbacks callbacks;
+    callbacks.on_densify_event = [&](int it) { densify_events.push_back(it); };
+    callbacks.on_prune_event = [&](int it) { prune_events.push_back(it); };
+    callbacks.on_iteration = [&](int it) { iterations.push_back(it); };
+    run_training(scene, data, cfg, callbacks);
+    CHECK(densify_events == (std::vector<int>{10, 20, 30}));
+    CHECK(prune_events == (std::vector<int>{10, 20, 30, 35, 40, 45, 50, 55, 60}));
+    CHECK(iterations.size() == 60 && iterations.front() == 1 && iterations.back() == 60);
+  }
+  {  // a fixed seed reproduces the trajectory (up to the backward blend's
+     // float-atomic summation order: loss within 1e-5 relative, same counts)
+    Rng rng(95);
+    const auto data = tiny_dataset(rng, 4, 24, 6);
+    Scene<float> scene = init_from_points(data.init_points, 1);
+    TrainConfig cfg = fast_config();
+    const auto a = run_training(scene, data, cfg);
+    const auto b = run_training(scene, data, cfg);
+    CHECK(a.log.size() == b.log.size());
+    for (size_t i = 0; i < a.log.size() && i < b.log.size(); ++i) {
+      CHECK(near(a.log[i].loss, b.log[i].loss, 1e-5));
+      CHECK(a.log[i].gaussians == b.log[i].gaussians);
+    }
+  }
+}
+
+// ---- smoke: raster KATs, camera KAT, exception, file formats ----------------------
+static void smoke() {
+  std::vector<ProjectedGaussian<float>> pgs(2);
+  for (int i = 0; i < 2; ++i) {
+    pgs[i].mu2d = Vec2<float>(3, 3);
+    pgs[i].cov2d = Mat2<float>::Identity();
+    pgs[i].cov2d_inv = Mat2<float>::Identity();
+    pgs[i].opacity = 0.5f;
+    pgs[i].depth = 1.0f + i;
+    pgs[i].source_index = i;
+  }
+  pgs[0].color = Vec3<float>(1, 0, 0);
+  pgs[1].color = Vec3<float>(0, 1, 0);
+  const TileGrid grid = build_tile_grid(pgs, 8, 8, BinningConfig<float>{}, 8);
+  CHECK(count_pairs(grid) == 2);
+  const RenderOutputs<float> out = blend_forward(grid, pgs);
+  CHECK(std::fabs(out.image.at(3, 3)[0] - 0.5f) < 1e-7f);
+  CHECK(std::fabs(out.image.at(3, 3)[1] - 0.25f) < 1e-7f);
+  CHECK(std::fabs(out.transmittance(3, 3) - 0.25f) < 1e-7f);
+  CHECK(out.contrib_count(3, 3) == 2);
+  // blend_forward honours the caller's grid: the same Gaussians with the
+  // second one removed from the tile list render as the first alone
+  TileGrid only0 = grid;
+  for (auto& t : only0.tiles) t.erase(std::remove(t.begin(), t.end(), 1), t.end());
+  const RenderOutputs<float> one = blend_forward(only0, pgs);
+  CHECK(std::fabs(one.image.at(3, 3)[0] - 0.5f) < 1e-7f && one.image.at(3, 3)[1] == 0.0f);
+  CHECK(one.contrib_count(3, 3) == 1);
+  // blend_backward runs on the given grid / pgs, independent of earlier calls
+  Image<float> up(8, 8);
+  up.at(3, 3) = Vec3<float>(1, 1, 1);
+  const auto bg_full = blend_backward(grid, pgs, up);
+  const auto bg_one = blend_backward(only0, pgs, up);
+  CHECK(bg_full.d_color[1][1] > 0.0f && bg_one.d_color[1][1] == 0.0f);
+  CHECK(std::fabs(bg_full.d_color[0][0] - 0.5f) < 1e-6f);  // dC/dc0 = T0 alpha0 = 0.5
+
+  // principal point (tests/test_camera.cpp:23-36)
+  Scene<float> scene;
+  scene.sh_degree = 1;
+  Gaussian3D<float> g;
+  g.mu = Vec3<float>(0, 0, 5);
+  g.sh = ShMatrix<float>::Zero(4, 3);
+  g.sh(0, 0) = g.sh(0, 1) = g.sh(0, 2) = 0.5f;
+  scene.gaussians.push_back(g);
+  Camera<float> cam;
+  cam.width = cam.height = 64;
+  cam.fx = cam.fy = 100;
+  cam.cx = cam.cy = 32;
+  const auto proj = project_scene(scene, cam);
+  CHECK(proj.size() == 1);
+  CHECK(std::fabs(proj[0].mu2d[0] - 32) < 1e-5f && std::fabs(proj[0].mu2d[1] - 32) < 1e-5f);
+  CHECK(std::fabs(proj[0].depth - 5) < 1e-6f);
+  const auto single = project(g, cam, 1, 7);
+  CHECK(single.has_value() && single->source_index == 7 && single->mu2d == proj[0].mu2d);
+  Gaussian3D<float> behind = g;
+  behind.mu[2] = -1;
+  CHECK(!project(behind, cam, 1).has_value());
+  // on-axis project_backward: d mu_x = fx / z (tests/test_camera.cpp:122-134)
+  const auto pb = project_backward(g, cam, 1, Vec2<float>(1, 0), Mat2<float>::Zero(), Vec3<float>(), 0.0f);
+  CHECK(near(pb.mu[0], 100.0 / 5.0, 1e-5));
+  // training_loss on explicit images: identical images give zero loss and gradient
+  Image<float> a(16, 12);
+  for (size_t i = 0; i < a.pixels.size(); ++i) a.pixels[i] = Vec3<float>(0.2f, 0.4f, float(i % 7) / 7);
+  const auto lr = training_loss(a, a, 0.2f);
+  CHECK(std::fabs(lr.loss) < 1e-6f && std::fabs(lr.ssim_value - 1.0f) < 1e-6f);
+  CHECK(std::isinf(psnr(a, a)) || psnr(a, a) == 100.0);
+  // invalid scale raises the reference's exception
+  Scene<float> bad = scene;
+  bad.gaussians[0].log_scale[0] = NAN;
+  bool threw = false;
+  try {
+    project_scene(bad, cam);
+  } catch (const std::invalid_argument& e) {
+    threw = std::string(e.what()).find("covariance_3d") != std::string::npos;
+  }
+  CHECK(threw);
+  // storage orders: ShMatrix / maps are column-major as Eigen
+  ShMatrix<float> sh = ShMatrix<float>::Zero(4, 3);
+  sh(1, 0) = 1.0f;
+  CHECK(sh.d[1] == 1.0f);
+  ScalarMap<float> sm(2, 3);
+  sm(1, 0) = 5.0f;
+  CHECK(sm.d[1] == 5.0f);
+  // on-disk formats (tests/test_dataset.cpp)
+  const std::string tmp = std::string(std::getenv("SK_TMP") ? std::getenv("SK_TMP") : "/tmp");
+  Image<float> img(5, 3);
+  for (size_t i = 0; i < img.pixels.size(); ++i)
+    for (int c = 0; c < 3; ++c) img.pixels[i][c] = float((i * 3 + c) % 11) / 10.0f;
+  write_png(tmp + "/wrapper.png", img);
+  const Image<float> back = read_png(tmp + "/wrapper.png");
+  CHECK(back.width == 5 && back.height == 3);
+  for (size_t i = 0; i < img.pixels.size(); ++i)
+    for (int c = 0; c < 3; ++c) CHECK(std::fabs(back.pixels[i][c] - img.pixels[i][c]) <= 0.5f / 255 + 1e-6f);
+  std::vector<std::pair<Vec3<float>, Vec3<float>>> pts(1);
+  pts[0].first[0] = 1.5f;
+  pts[0].second[1] = 1.0f;
+  write_points_ply(tmp + "/wrapper_points.ply", pts);
+  const auto pbk = read_points_ply(tmp + "/wrapper_points.ply");
+  CHECK(pbk.size() == 1 && pbk[0].first[0] == 1.5f && pbk[0].second[1] == 1.0f);
+  save_checkpoint(scene, tmp + "/wrapper_ckpt.ply");
+  const Scene<float> sb = load_checkpoint<float>(tmp + "/wrapper_ckpt.ply");
+  CHECK(sb.sh_degree == 1 && sb.size() == 1);
+  CHECK(sb.gaussians[0].mu[2] == 5.0f && sb.gaussians[0].sh(0, 1) == 0.5f);
+}
+
+int main() {
+  smoke();
+  adc_kats();
+  adam_kats();
+  trainer_kats();
+  std::printf("%s (%d checks, %d failures)\n", failures ? "FAIL" : "PASS", checks, failures);
+  return failures ? 1 : 0;
+}
