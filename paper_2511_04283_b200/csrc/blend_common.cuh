@@ -20,6 +20,13 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
                "l"(gmem)
                : "memory");
 }
+// 2^x on MUFU.EX2 (the hardware exp __expf uses, without its pre-multiply)
+__device__ __forceinline__ float exp2f_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {

@@ -222,7 +222,22 @@ def test_config2_gradients_match_oracle(ctx, orc, config2):
     from oracle.oracle import PG
     pg = PG(prj.mu2d[vis], prj.cov2d[vis], prj.conic[vis], prj.depth[vis], prj.color[vis], prj.opacity[vis])
     ref_bg = orc.blend_backward_pg(pg, c["w"], c["h"], d_ref, orc.binning(), workers=WORKERS)
-    _compare_blend_grads("config2.blend", bg, ref_bg, rows=vis)
+    # At 1080p a Gaussian's gradient sums ~10^2-10^4 cancelling per-pixel
+    # terms; the fp32 reference and the GPU (different, atomic summation
+    # order) each carry ~1e-7 x sum|terms| of rounding, which exceeds 1e-3 of
+    # the few smallest elements near the floor. The bar is therefore set
+    # against the exact (fp64) blend gradients of the same projected set and
+    # dL/dimage: the GPU within 1e-3 (floored), and no further from them than
+    # the fp32 reference is, with the GPU-vs-fp32-reference distance reported.
+    ref64 = orc.blend_backward_pg(pg, c["w"], c["h"], d_ref.astype(np.float64), orc.binning(), workers=WORKERS,
+                                  dtype=np.float64)
+    for f in ("d_mu2d", "d_conic", "d_color", "d_opacity", "abs_grad"):
+        got, r32, r64 = getattr(bg, f)[vis], getattr(ref_bg, f), getattr(ref64, f)
+        unfloored_report(f"config2.blend.{f}", got, r32)
+        g64 = unfloored_report(f"config2.blend.{f}_vs_fp64", got, r64)
+        o64 = unfloored_report(f"config2.blend.{f}_fp32_reference_vs_fp64", r32, r64)
+        assert g64["floored_max"] < TOL, g64
+        assert g64["unfloored_p999"] <= max(o64["unfloored_p999"], 1e-4), (g64, o64)
     g = ctx.project_backward(scene, stats=False)
     ref_g, ref_loss = orc.view_grads(c["params"], 3, c["cam"], gt, 0.2, workers=WORKERS)
     assert ref_loss == pytest.approx(v.loss, rel=1e-3)  # fp32 serial sums (see above)
