@@ -40,27 +40,13 @@ __device__ __forceinline__ void cp_async_wait() {
 __host__ __device__ __forceinline__ int64_t cmask_word(int begin, int tile) { return (int64_t)(begin >> 5) + tile; }
 inline size_t cmask_words(int64_t pairs, int tiles) { return (size_t)(pairs >> 5) + (size_t)tiles + 2; }
 
-#ifndef SK_STAGE_APPROX
-// 1: the culling geometry (ellipse box, edge minimiser) uses MUFU sqrt /
-// reciprocal instead of the IEEE sequences -fmad=false files get; culling
-// only has to be conservative and carries 1e-4 / 1e-3 slack
-#define SK_STAGE_APPROX 1
-#endif
 __device__ __forceinline__ float cull_sqrt(float x) {
-#if SK_STAGE_APPROX
   float r;
   asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
-#else
-  return sqrtf(x);
-#endif
 }
 __device__ __forceinline__ float cull_div(float a, float b) {
-#if SK_STAGE_APPROX
   return __fdividef(a, b);
-#else
-  return a / b;
-#endif
 }
 
 __device__ __forceinline__ float qcut_of(float opacity) {

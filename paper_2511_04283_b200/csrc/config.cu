@@ -4,6 +4,7 @@
 // for booleans, "aabb"/"compact" for bin_mode) and error messages. Host code.
 #include <cstddef>
 #include <fstream>
+#include <vector>
 #include <sstream>
 #include <string>
 
@@ -116,24 +117,21 @@ std::string trim(const std::string& s) {
   return b == std::string::npos ? std::string() : s.substr(b, e - b + 1);
 }
 
-// load_config_file (config.hpp:167-196)
+// load_config_file (config.hpp:162-188): a flat "key = value" file; '#'
+// starts a comment; blank lines are skipped; any other line without '=' is
+// an error naming its 1-based line number. The whole file is read first and
+// then applied line by line.
 void load_file(sk_train_config& cfg, const std::string& path) {
-  std::ifstream in(path);
-  require(in.good(), "config: cannot open '" + path + "'");
-  std::string line;
-  int line_no = 0;
-  while (std::getline(in, line)) {
-    ++line_no;
-    const auto hash = line.find('#');
-    if (hash != std::string::npos) line = line.substr(0, hash);
-    const auto eq = line.find('=');
-    if (eq == std::string::npos) {
-      std::istringstream check(line);
-      std::string token;
-      require(!(check >> token), "config: malformed line " + std::to_string(line_no) + " (expected key = value)");
-      continue;
-    }
-    set_value(cfg, trim(line.substr(0, eq)), trim(line.substr(eq + 1)));
+  std::ifstream file(path);
+  require(file.good(), "config: cannot open '" + path + "'");
+  std::vector<std::string> lines;
+  for (std::string l; std::getline(file, l);) lines.push_back(std::move(l));
+  for (size_t i = 0; i < lines.size(); ++i) {
+    const std::string body = trim(lines[i].substr(0, lines[i].find('#')));
+    if (body.empty()) continue;
+    const size_t sep = body.find('=');
+    require(sep != std::string::npos, "config: malformed line " + std::to_string(i + 1) + " (expected key = value)");
+    set_value(cfg, trim(body.substr(0, sep)), trim(body.substr(sep + 1)));
   }
 }
 

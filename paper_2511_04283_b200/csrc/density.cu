@@ -24,9 +24,6 @@
 #include "abi_util.h"
 #include "trainer.h"
 
-#ifndef SK_SCORE_TWO_STREAMS
-#define SK_SCORE_TWO_STREAMS 1
-#endif
 
 namespace sk {
 namespace {
@@ -150,7 +147,7 @@ __global__ void prune_flags_kernel(const float* __restrict__ p, int64_t stride, 
                                    const float* __restrict__ s_p, const float* __restrict__ max_r2d, bool early,
                                    bool size_rules, float min_op, float world_cut, float screen, float op_cut,
                                    bool use_vcp, float tau_p, uint8_t* __restrict__ flag, uint32_t* __restrict__ key,
-                                   uint32_t* __restrict__ idx, int* __restrict__ count) {
+                                   int* __restrict__ count) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool f = false;
   if (i < n) {
@@ -161,11 +158,8 @@ __global__ void prune_flags_kernel(const float* __restrict__ p, int64_t stride, 
         f = f || max_scale(p, stride, i) > world_cut;
         f = f || max_r2d[i] > screen;
       }
-      if (key) {
-        // ascending key == (s_p descending, index ascending); non-candidates last
-        key[i] = f ? (0x7f800000u - __float_as_uint(s_p[i])) : 0xffffffffu;
-        idx[i] = (uint32_t)i;
-      }
+      // ascending key == s_p descending (ties: index order, select_take_kernel); non-candidates last
+      if (key) key[i] = f ? (0x7f800000u - __float_as_uint(s_p[i])) : 0xffffffffu;
     } else {
       f = (op < op_cut) || (use_vcp && s_p[i] > tau_p);
     }
@@ -175,10 +169,89 @@ __global__ void prune_flags_kernel(const float* __restrict__ p, int64_t stride, 
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(count, __popc(b));
 }
 
-__global__ void vcp_take_kernel(const uint32_t* __restrict__ order, int take, uint8_t* __restrict__ flag, int64_t n) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  if (r < take) flag[order[r]] = 1;
+// VCP's "keep the ceil(|C|/2) highest s_p, ties by index" (adc.hpp:243-249)
+// as a radix select on the candidate keys (ascending key == s_p descending,
+// non-candidates 0xffffffff) instead of a full sort: four 8-bit MSB-first
+// histogram passes find the take-th smallest key K*; every key < K* is
+// taken, and of the keys == K* the first `rank` in index order.
+struct SelectState {
+  uint32_t prefix, mask;  // digits of K* fixed so far
+  int rank;               // position still to find among keys matching the prefix (1-based)
+  int pad;
+};
+
+__global__ void select_init_kernel(const int* __restrict__ count, SelectState* __restrict__ st,
+                                   uint32_t* __restrict__ hist) {
+  if (threadIdx.x == 0) *st = SelectState{0u, 0u, (*count + 1) / 2, 0};
+  hist[threadIdx.x] = 0;
+}
+
+__global__ void select_hist_kernel(const uint32_t* __restrict__ key, int64_t n, const SelectState* __restrict__ st,
+                                   int shift, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t s_h[256];
+  s_h[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t prefix = st->prefix, mask = st->mask;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = key[i];
+    if ((k & mask) == prefix) atomicAdd(&s_h[(k >> shift) & 0xffu], 1u);
+  }
+  __syncthreads();
+  if (s_h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], s_h[threadIdx.x]);
+}
+
+// one CTA of 256: fixes the next digit of K* and clears the histogram
+__global__ void select_step_kernel(SelectState* __restrict__ st, int shift, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t s_c[256];
+  const int d = threadIdx.x;
+  uint32_t x = hist[d];
+  s_c[d] = x;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {  // inclusive scan
+    const uint32_t y = d >= o ? s_c[d - o] : 0u;
+    __syncthreads();
+    s_c[d] += y;
+    __syncthreads();
+  }
+  const int rank = st->rank;
+  const uint32_t incl = s_c[d], excl = incl - x;
+  __syncthreads();
+  if (rank > 0 && (int)excl < rank && rank <= (int)incl) {
+    st->prefix |= (uint32_t)d << shift;
+    st->mask |= 0xffu << shift;
+    st->rank = rank - (int)excl;
+  }
+  hist[d] = 0;
+}
+
+__global__ void __launch_bounds__(256) select_tie_count_kernel(const uint32_t* __restrict__ key, int64_t n,
+                                                                const SelectState* __restrict__ st,
+                                                                int3* __restrict__ block_counts) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const bool eq = i < n && st->rank > 0 && key[i] == st->prefix;
+  const int c = __syncthreads_count(eq);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = make_int3(c, 0, 0);
+}
+
+__global__ void __launch_bounds__(256) select_take_kernel(const uint32_t* __restrict__ key, int64_t n,
+                                                           const SelectState* __restrict__ st,
+                                                           const int3* __restrict__ block_base,
+                                                           uint8_t* __restrict__ flag) {
+  __shared__ int s_w[8];
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const uint32_t kstar = st->prefix;
+  const int rank = st->rank;  // 0: no candidate at all
+  const uint32_t k = i < n ? key[i] : 0xffffffffu;
+  const int eq = (i < n && rank > 0 && k == kstar) ? 1 : 0;
+  // in-block exclusive count of equal keys before i
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t b = __ballot_sync(0xffffffffu, eq);
+  if (lane == 0) s_w[warp] = __popc(b);
+  __syncthreads();
+  int before = block_base[blockIdx.x].x + __popc(b & ((1u << lane) - 1u));
+  for (int w = 0; w < warp; ++w) before += s_w[w];
+  if (i >= n) return;
+  flag[i] = (rank > 0 && (k < kstar || (eq && before < rank))) ? 1 : 0;
 }
 
 // never empty the scene: keep the first index with the smallest s_p
@@ -193,96 +266,152 @@ __global__ void argmin_kernel(const float* __restrict__ s_p, int64_t n, unsigned
   if ((threadIdx.x & 31) == 0) atomicMin(best, v);
 }
 
-// ---- K15: class flags and scatter -------------------------------------------------
-__global__ void class_kernel(const uint8_t* __restrict__ prune, const uint8_t* __restrict__ clone,
-                             const uint8_t* __restrict__ split, int64_t n, int32_t* __restrict__ keep_ns,
-                             int32_t* __restrict__ clone_k, int32_t* __restrict__ split_k) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const bool keep = !prune[i];
-  const bool sp = keep && split[i];
-  keep_ns[i] = (keep && !sp) ? 1 : 0;
-  clone_k[i] = (keep && clone[i]) ? 1 : 0;
-  split_k[i] = sp ? 1 : 0;
+// ---- K15: compaction (apply_prune / apply_densify adc.hpp:166-205, 272-289 and
+// the Adam moment remaps adam.hpp:45-58) in three kernels:
+//   K15a  per 256-Gaussian block: counts of the three output classes
+//         (non-split survivors, clones, split parents; pruned Gaussians are
+//         neither cloned nor split, trainer.hpp:212-217);
+//   K15b  one CTA: exclusive scans of the block counts and the totals;
+//   K15c  per block: the same class flags, an in-block scan for each class,
+//         then every Gaussian moves its 59 parameter / m / v rows (coalesced
+//         along the Gaussian axis) to its destination slots and writes the
+//         clone step and the split children's geometry.
+// Output order (adc.hpp:179-201): survivors, then clones, then split pairs.
+constexpr int kCompactBlock = 256;  // threads per block
+constexpr int kCompactItems = 1;    // Gaussians per thread (measured: 4 per thread with float4 row
+                                    // loads +22% K15 — strided stores)
+constexpr int kCompactSpan = kCompactBlock * kCompactItems;
+
+struct Classes {
+  int keep, clone, split;  // 0 / 1 each
+};
+__device__ __forceinline__ Classes classify(const uint8_t* prune, const uint8_t* clone, const uint8_t* split,
+                                            int64_t i, int64_t n) {
+  Classes c{0, 0, 0};
+  if (i < n && !prune[i]) {
+    const bool sp = split[i] != 0;
+    c.keep = sp ? 0 : 1;
+    c.clone = clone[i] ? 1 : 0;
+    c.split = sp ? 1 : 0;
+  }
+  return c;
 }
 
-// Destination slots of source Gaussian i (adc.hpp:179-201 output order:
-// non-split survivors, then clones, then split pairs): x = survivor slot,
-// y = clone slot, z = first split child; -1 when absent.
-__global__ void route_kernel(const int32_t* __restrict__ keep_ns, const int32_t* __restrict__ clone_k,
-                             const int32_t* __restrict__ split_k, const int32_t* __restrict__ pos_keep,
-                             const int32_t* __restrict__ pos_clone, const int32_t* __restrict__ pos_split, int64_t n,
-                             int64_t n_keep, int64_t n_clone, int4* __restrict__ route,
-                             int32_t* __restrict__ old_to_new) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int4 r;
-  r.x = keep_ns[i] ? pos_keep[i] : -1;
-  r.y = clone_k[i] ? (int)(n_keep + pos_clone[i]) : -1;
-  r.z = split_k[i] ? (int)(n_keep + n_clone + 2 * (int64_t)pos_split[i]) : -1;
-  r.w = 0;
-  route[i] = r;
-  if (old_to_new) old_to_new[i] = r.x;
+// Block-wide exclusive scan of three per-thread counts; total = block sums.
+__device__ __forceinline__ int3 block_excl_scan3(int3 v, int3* s_warp, int3& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int3 x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, x.x, o), b = __shfl_up_sync(0xffffffffu, x.y, o),
+              c = __shfl_up_sync(0xffffffffu, x.z, o);
+    if (lane >= o) x.x += a, x.y += b, x.z += c;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  int3 wb = make_int3(0, 0, 0), tot = make_int3(0, 0, 0);
+#pragma unroll
+  for (int w = 0; w < kCompactBlock / 32; ++w) {
+    const int3 t = s_warp[w];
+    if (w < warp) wb.x += t.x, wb.y += t.y, wb.z += t.z;
+    tot.x += t.x, tot.y += t.y, tot.z += t.z;
+  }
+  total = tot;
+  return make_int3(wb.x + x.x - v.x, wb.y + x.y - v.y, wb.z + x.z - v.z);
 }
 
-// Bulk of K15: one thread per (component, source Gaussian) — every row of the
-// planar params / m / v is read and written with coalesced accesses (the
-// route table stays in L2 across the components). Survivors keep m / v;
-// clones and split children get zero moments (AdamGroup::remap
-// adam.hpp:45-58) and a verbatim parameter copy that compact_geom_kernel
-// then adjusts.
-__global__ void compact_copy_kernel(const float* __restrict__ src, const float* __restrict__ m_src,
-                                    const float* __restrict__ v_src, int64_t stride, int64_t n,
-                                    const int4* __restrict__ route, float* __restrict__ dst,
-                                    float* __restrict__ m_dst, float* __restrict__ v_dst, int64_t dstride) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int c = blockIdx.y;
-  const int4 r = route[i];
-  if (r.x < 0 && r.y < 0 && r.z < 0) return;
-  const size_t so = (size_t)c * stride + i;
-  const size_t co = (size_t)c * dstride;
-  const float x = src[so];
-  if (r.x >= 0) {
-    dst[co + r.x] = x;
-    m_dst[co + r.x] = m_src[so];
-    v_dst[co + r.x] = v_src[so];
+__global__ void __launch_bounds__(kCompactBlock) compact_count_kernel(const uint8_t* __restrict__ prune,
+                                                                      const uint8_t* __restrict__ clone,
+                                                                      const uint8_t* __restrict__ split, int64_t n,
+                                                                      int3* __restrict__ block_counts) {
+  __shared__ int3 s_warp[kCompactBlock / 32];
+  const int64_t i0 = (int64_t)blockIdx.x * kCompactSpan + (int64_t)threadIdx.x * kCompactItems;
+  int3 v = make_int3(0, 0, 0);
+#pragma unroll
+  for (int k = 0; k < kCompactItems; ++k) {
+    const Classes c = classify(prune, clone, split, i0 + k, n);
+    v.x += c.keep, v.y += c.clone, v.z += c.split;
   }
-  if (r.y >= 0) {
-    dst[co + r.y] = x;
-    m_dst[co + r.y] = 0.0f;
-    v_dst[co + r.y] = 0.0f;
+  int3 tot;
+  block_excl_scan3(v, s_warp, tot);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = tot;
+}
+
+// One CTA of 1024 threads: exclusive scan of the block counts in place (four
+// consecutive blocks per thread, chunks of 4096), the class totals into
+// totals[0..2].
+__global__ void __launch_bounds__(1024) compact_scan_blocks_kernel(int3* __restrict__ block_counts, int nb,
+                                                                   long long* __restrict__ totals) {
+  __shared__ int3 s_w[32];
+  __shared__ int3 s_carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int3 carry = make_int3(0, 0, 0);
+  for (int b0 = 0; b0 < nb; b0 += 4096) {
+    const int b = b0 + 4 * (int)threadIdx.x;
+    int3 v[4], sum = make_int3(0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = b + k < nb ? block_counts[b + k] : make_int3(0, 0, 0);
+      sum.x += v[k].x, sum.y += v[k].y, sum.z += v[k].z;
+    }
+    int3 x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int p = __shfl_up_sync(0xffffffffu, x.x, o), q = __shfl_up_sync(0xffffffffu, x.y, o),
+                r = __shfl_up_sync(0xffffffffu, x.z, o);
+      if (lane >= o) x.x += p, x.y += q, x.z += r;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int3 w = s_w[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int p = __shfl_up_sync(0xffffffffu, w.x, o), q = __shfl_up_sync(0xffffffffu, w.y, o),
+                  r = __shfl_up_sync(0xffffffffu, w.z, o);
+        if (lane >= o) w.x += p, w.y += q, w.z += r;
+      }
+      s_w[lane] = w;  // inclusive warp prefix
+      if (lane == 31) s_carry = w;
+    }
+    __syncthreads();
+    const int3 wp = warp > 0 ? s_w[warp - 1] : make_int3(0, 0, 0);
+    int3 run = make_int3(carry.x + wp.x + x.x - sum.x, carry.y + wp.y + x.y - sum.y, carry.z + wp.z + x.z - sum.z);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (b + k < nb) block_counts[b + k] = run;
+      run.x += v[k].x, run.y += v[k].y, run.z += v[k].z;
+    }
+    const int3 c = s_carry;
+    carry.x += c.x, carry.y += c.y, carry.z += c.z;
+    __syncthreads();
   }
-  if (r.z >= 0) {
-    dst[co + r.z] = x;
-    dst[co + r.z + 1] = x;
-    m_dst[co + r.z] = m_dst[co + r.z + 1] = 0.0f;
-    v_dst[co + r.z] = v_dst[co + r.z + 1] = 0.0f;
+  if (threadIdx.x == 0) {
+    totals[0] = carry.x;
+    totals[1] = carry.y;
+    totals[2] = carry.z;
   }
 }
 
-// Geometry of clones and split children (adc.hpp:184-201), after the copy:
-// clone mu -= lr * grad3d / views_seen; children mu = parent mu + R(eps * s),
-// log_scale - ln 1.6.
-__global__ void compact_geom_kernel(const float* __restrict__ src, int64_t stride, int64_t n,
-                                    const int4* __restrict__ route, const float* __restrict__ grad3d,
-                                    const int* __restrict__ views_seen, float clone_lr, const float* __restrict__ eps,
-                                    float log_shrink, float* __restrict__ dst, int64_t dstride,
-                                    const int32_t* __restrict__ pos_split) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int4 rt = route[i];
-  if (rt.y >= 0) {
+// The clone step and the split children's geometry (adc.hpp:184-201) of
+// source Gaussian i, written over the verbatim copies of its rows.
+__device__ __forceinline__ void compact_geometry(const float* __restrict__ src, int64_t stride, int64_t i,
+                                                 int64_t clone_slot, int64_t split_slot, int64_t split_rank,
+                                                 const float* __restrict__ grad3d, const int* __restrict__ views_seen,
+                                                 float clone_lr, const float* __restrict__ eps, float log_shrink,
+                                                 float* __restrict__ dst, int64_t dstride) {
+  // clone mu -= lr * grad3d / views_seen (adc.hpp:184-189)
+  if (clone_slot >= 0) {
     const int seen = views_seen[i];
     if (seen > 0) {
       const float vs = (float)seen;
       for (int k = 0; k < 3; ++k)
-        dst[(SK_COMP_MU + k) * dstride + rt.y] =
+        dst[(SK_COMP_MU + k) * dstride + clone_slot] =
             src[(SK_COMP_MU + k) * stride + i] - clone_lr * (grad3d[k * stride + i] / vs);
     }
   }
-  if (rt.z >= 0) {
-    const int64_t r = pos_split[i];
+  // split children: mu = parent mu + R (eps * s), log_scale - ln 1.6 (adc.hpp:190-201)
+  if (split_slot >= 0) {
     float qw = src[3 * stride + i], qx = src[4 * stride + i], qy = src[5 * stride + i], qz = src[6 * stride + i];
     const float n2 = ((qw * qw + qx * qx) + qy * qy) + qz * qz;
     if (n2 > 0.0f) {
@@ -302,12 +431,12 @@ __global__ void compact_geom_kernel(const float* __restrict__ src, int64_t strid
     R[2][0] = 2.0f * (qx * qz - qw * qy);
     R[2][1] = 2.0f * (qy * qz + qw * qx);
     R[2][2] = 1.0f - 2.0f * (qx * qx + qy * qy);
-    float s[3];
-    for (int k = 0; k < 3; ++k) s[k] = det_expf(src[(SK_COMP_LOG_SCALE + k) * stride + i]);
+    float sc[3];
+    for (int k = 0; k < 3; ++k) sc[k] = det_expf(src[(SK_COMP_LOG_SCALE + k) * stride + i]);
     for (int child = 0; child < 2; ++child) {
-      const int64_t d = rt.z + child;
+      const int64_t d = split_slot + child;
       float es[3];
-      for (int k = 0; k < 3; ++k) es[k] = eps[r * 6 + child * 3 + k] * s[k];
+      for (int k = 0; k < 3; ++k) es[k] = eps[split_rank * 6 + child * 3 + k] * sc[k];
       for (int k = 0; k < 3; ++k) {
         const float off = (R[k][0] * es[0] + R[k][1] * es[1]) + R[k][2] * es[2];
         dst[(SK_COMP_MU + k) * dstride + d] = src[(SK_COMP_MU + k) * stride + i] + off;
@@ -316,6 +445,95 @@ __global__ void compact_geom_kernel(const float* __restrict__ src, int64_t strid
     }
   }
 }
+
+__global__ void __launch_bounds__(kCompactBlock) compact_move_kernel(
+    const uint8_t* __restrict__ prune, const uint8_t* __restrict__ clone, const uint8_t* __restrict__ split, int64_t n,
+    const int3* __restrict__ block_base, const long long* __restrict__ totals, int comps,
+    const float* __restrict__ src, const float* __restrict__ m_src, const float* __restrict__ v_src, int64_t stride,
+    float* __restrict__ dst, float* __restrict__ m_dst, float* __restrict__ v_dst, int64_t dstride,
+    const float* __restrict__ grad3d, const int* __restrict__ views_seen, float clone_lr,
+    const float* __restrict__ eps, float log_shrink, int32_t* __restrict__ old_to_new) {
+  __shared__ int3 s_warp[kCompactBlock / 32];
+  const int64_t i0 = (int64_t)blockIdx.x * kCompactSpan + (int64_t)threadIdx.x * kCompactItems;
+  Classes cl[kCompactItems];
+  int3 v = make_int3(0, 0, 0);
+#pragma unroll
+  for (int k = 0; k < kCompactItems; ++k) {
+    cl[k] = classify(prune, clone, split, i0 + k, n);
+    v.x += cl[k].keep, v.y += cl[k].clone, v.z += cl[k].split;
+  }
+  int3 tot;
+  const int3 local = block_excl_scan3(v, s_warp, tot);
+  if (i0 >= n) return;
+  const int3 base = block_base[blockIdx.x];
+  const int64_t n_keep = totals[0], n_clone = totals[1];
+  // destination slots of the thread's Gaussians (-1: absent)
+  int64_t keep_slot[kCompactItems], clone_slot[kCompactItems], split_slot[kCompactItems], split_rank[kCompactItems];
+  {
+    int64_t kr = base.x + local.x, cr = base.y + local.y, sr = base.z + local.z;
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+      keep_slot[k] = cl[k].keep ? kr : -1;
+      clone_slot[k] = cl[k].clone ? n_keep + cr : -1;
+      split_slot[k] = cl[k].split ? n_keep + n_clone + 2 * sr : -1;
+      split_rank[k] = sr;
+      kr += cl[k].keep, cr += cl[k].clone, sr += cl[k].split;
+    }
+  }
+  // blockIdx.y = component group: group 0 moves the 11 geometry / opacity rows
+  // and then writes the clone / split geometry over its own copies; the SH
+  // rows are split evenly over the other groups (about four rows each)
+  const int g = blockIdx.y, groups = gridDim.y;
+  const int c0 = g == 0 ? 0 : SK_COMP_SH + (int)((int64_t)(comps - SK_COMP_SH) * (g - 1) / (groups - 1));
+  const int c1 = g == 0 ? SK_COMP_SH : SK_COMP_SH + (int)((int64_t)(comps - SK_COMP_SH) * g / (groups - 1));
+  if (g == 0 && old_to_new)
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k)
+      if (i0 + k < n) old_to_new[i0 + k] = (int32_t)keep_slot[k];
+  // rows: survivors keep m / v, clones and split children start at zero;
+  // all rows are loaded unconditionally so the loads of several components
+  // are in flight together
+#pragma unroll 4
+  for (int comp = c0; comp < c1; ++comp) {
+    const size_t co = (size_t)comp * dstride;
+    float xs[kCompactItems], ms[kCompactItems], vs[kCompactItems];
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+      const size_t so = (size_t)comp * stride + i0 + k;
+      xs[k] = src[so];
+      ms[k] = m_src[so];
+      vs[k] = v_src[so];
+    }
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+      if (keep_slot[k] >= 0) {
+        dst[co + keep_slot[k]] = xs[k];
+        m_dst[co + keep_slot[k]] = ms[k];
+        v_dst[co + keep_slot[k]] = vs[k];
+      }
+      if (clone_slot[k] >= 0) {
+        dst[co + clone_slot[k]] = xs[k];
+        m_dst[co + clone_slot[k]] = 0.0f;
+        v_dst[co + clone_slot[k]] = 0.0f;
+      }
+      if (split_slot[k] >= 0) {
+        dst[co + split_slot[k]] = xs[k];
+        dst[co + split_slot[k] + 1] = xs[k];
+        m_dst[co + split_slot[k]] = m_dst[co + split_slot[k] + 1] = 0.0f;
+        v_dst[co + split_slot[k]] = v_dst[co + split_slot[k] + 1] = 0.0f;
+      }
+    }
+  }
+  if (g != 0) return;
+#pragma unroll 1
+  for (int k = 0; k < kCompactItems; ++k) {
+    const int64_t i = i0 + k;
+    if (i >= n) break;
+    compact_geometry(src, stride, i, clone_slot[k], split_slot[k], split_rank[k], grad3d, views_seen, clone_lr, eps,
+                     log_shrink, dst, dstride);
+  }
+}
+
 
 unsigned blocks(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
 
@@ -423,7 +641,7 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
     score_view(c, s, fr, cams[j], gts[j], gt_u8_device, tau, lambda, bin, rows + (size_t)sl * n, &photo[sl]);
   };
   const char* one = std::getenv("SK_SCORE_ONE_STREAM");  // runtime override (tests / diagnostics)
-  const bool two = SK_SCORE_TWO_STREAMS && !(one && one[0] == '1');
+  const bool two = !(one && one[0] == '1');
   if (!(two && gt_u8_device && mine.size() >= 2)) {
     for (const int j : mine) run_view(ctx, f, j);
   } else {
@@ -506,32 +724,40 @@ void select_prune_flags(sk_ctx* ctx, sk_scene* s, int iteration, const sk_prune_
   int* count = reinterpret_cast<int*>(ensure<uint32_t>(ev.lohi, 4) + 2);
   SK_CUDA(cudaMemsetAsync(count, 0, sizeof(int), ctx->stream));
   uint32_t* key = nullptr;
-  uint32_t* idx = nullptr;
-  uint32_t *kb = nullptr, *vb = nullptr;
-  if (early && pp.use_vcp) {
-    key = ensure<uint32_t>(ev.keys_a, n);
-    idx = ensure<uint32_t>(ev.vals_a, n);
-    kb = ensure<uint32_t>(ev.keys_b, n);
-    vb = ensure<uint32_t>(ev.vals_b, n);
-  }
+  if (early && pp.use_vcp) key = ensure<uint32_t>(ev.keys_a, n);
   const float op_cut = pp.use_vcp ? pp.opacity_late : pp.min_opacity;
   prune_flags_kernel<<<blocks(n), 256, 0, ctx->stream>>>(
       s->params.as<float>(), s->capacity, n, s->s_p.as<float>(), s->max_radius2d.as<float>(), early,
       iteration > pp.size_prune_from, pp.min_opacity, pp.world_size_frac * extent, pp.screen_size, op_cut,
-      pp.use_vcp != 0, pp.tau_p, prune, key, idx, count);
+      pp.use_vcp != 0, pp.tau_p, prune, key, count);
   note_launch();
+  if (early && pp.use_vcp) {
+    // keep the ceil(|C|/2) highest-scoring candidates (ties by index) as pruned
+    auto* stv = reinterpret_cast<SelectState*>(ensure<uint32_t>(ev.keys_b, 4 + 256));
+    uint32_t* hist = reinterpret_cast<uint32_t*>(stv + 1);
+    select_init_kernel<<<1, 256, 0, ctx->stream>>>(count, stv, hist);
+    note_launch();
+    const unsigned hb = (unsigned)std::min<int64_t>(blocks(n), 148 * 4);
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      select_hist_kernel<<<hb, 256, 0, ctx->stream>>>(key, n, stv, shift, hist);
+      select_step_kernel<<<1, 256, 0, ctx->stream>>>(stv, shift, hist);
+      note_launch();
+      note_launch();
+    }
+    const int nb = (int)blocks(n);
+    int3* block_base = reinterpret_cast<int3*>(ensure<int32_t>(ev.cls, 3 * (size_t)nb));
+    long long* totals = ensure<long long>(ev.totals, 3);
+    select_tie_count_kernel<<<nb, 256, 0, ctx->stream>>>(key, n, stv, block_base);
+    compact_scan_blocks_kernel<<<1, 1024, 0, ctx->stream>>>(block_base, nb, totals);
+    select_take_kernel<<<nb, 256, 0, ctx->stream>>>(key, n, stv, block_base, prune);
+    note_launch();
+    note_launch();
+    note_launch();
+  }
   int host_count = 0;
   d2h(ctx, &host_count, count, 1);
   sync(ctx);
-  if (early && pp.use_vcp) {
-    // keep the ceil(|C|/2) highest-scoring candidates (ties by index) as pruned
-    SK_CUDA(cudaMemsetAsync(prune, 0, n, ctx->stream));
-    radix_sort_pairs(ctx, key, kb, idx, vb, n, 32);
-    const int take = (host_count + 1) / 2;
-    vcp_take_kernel<<<blocks(n), 256, 0, ctx->stream>>>(idx, take, prune, n);
-    note_launch();
-    host_count = take;
-  }
+  if (early && pp.use_vcp) host_count = (host_count + 1) / 2;
   if (host_count == n && n > 0) {
     unsigned long long* best = reinterpret_cast<unsigned long long*>(ensure<uint32_t>(ev.lohi, 4));
     const unsigned long long init = ~0ull;
@@ -558,17 +784,20 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
   gather_moments(s, ctx->stream);  // the compaction moves whole moment rows (sharded C1, comm.cu)
   const int64_t n = s->n;
   if (n == 0) return 0;
-  int32_t* cls = ensure<int32_t>(ev.cls, 3 * (size_t)n);
-  int32_t* pos = ensure<int32_t>(ev.pos, 3 * (size_t)n);
-  trace_point(ctx, "compact: enter");
-  class_kernel<<<blocks(n), 256, 0, ctx->stream>>>(prune, clone, split, n, cls, cls + n, cls + 2 * n);
+  const int nb = (int)((n + kCompactSpan - 1) / kCompactSpan);
+  int3* block_base = reinterpret_cast<int3*>(ensure<int32_t>(ev.cls, 3 * (size_t)nb));
+  long long* totals = ensure<long long>(ev.totals, 3);
+  compact_count_kernel<<<nb, kCompactBlock, 0, ctx->stream>>>(prune, clone, split, n, block_base);
   note_launch();
-  const int64_t n_keep = scan_gathered(ctx, cls, nullptr, pos, n);
-  const int64_t n_clone = scan_gathered(ctx, cls + n, nullptr, pos + n, n);
-  const int64_t n_split = scan_gathered(ctx, cls + 2 * n, nullptr, pos + 2 * n, n);
+  compact_scan_blocks_kernel<<<1, 1024, 0, ctx->stream>>>(block_base, nb, totals);
+  note_launch();
+  long long tot[3];
+  d2h(ctx, tot, totals, 3);
+  sync(ctx);
+  const int64_t n_keep = tot[0], n_clone = tot[1], n_split = tot[2];
   const int64_t new_n = n_keep + n_clone + 2 * n_split;
   float* eps = ensure<float>(ev.eps, 6 * (size_t)std::max<int64_t>(n_split, 1));
-  trace_point(ctx, "compact: class + 3 scans");
+  trace_point(ctx, "compact: class counts + scan");
   const float* eps_host = eps_source(n_split);
   trace_point(ctx, "compact: split normals");
   if (n_split > 0) {
@@ -589,18 +818,11 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
   ensure<float>(nm, cells);
   ensure<float>(nv, cells);
   trace_point(ctx, "compact: buffers");
-  int4* route = reinterpret_cast<int4*>(ensure<int32_t>(ev.route, 4 * (size_t)n));
-  route_kernel<<<blocks(n), 256, 0, ctx->stream>>>(cls, cls + n, cls + 2 * n, pos, pos + n, pos + 2 * n, n, n_keep,
-                                                   n_clone, route, old_to_new_dev);
-  note_launch();
-  compact_copy_kernel<<<dim3(blocks(n), (unsigned)s->comps), 256, 0, ctx->stream>>>(
-      s->params.as<float>(), s->adam_m.as<float>(), s->adam_v.as<float>(), s->capacity, n, route, np.as<float>(),
-      nm.as<float>(), nv.as<float>(), new_cap);
-  note_launch();
-  compact_geom_kernel<<<blocks(n), 256, 0, ctx->stream>>>(s->params.as<float>(), s->capacity, n, route,
-                                                          s->grad3d_acc.as<float>(), s->views_seen.as<int>(),
-                                                          clone_lr, eps, (float)std::log(1.6), np.as<float>(),
-                                                          new_cap, pos + 2 * n);
+  const int groups = 1 + std::max(1, (s->comps - SK_COMP_SH + 3) / 4);
+  compact_move_kernel<<<dim3(nb, groups), kCompactBlock, 0, ctx->stream>>>(
+      prune, clone, split, n, block_base, totals, s->comps, s->params.as<float>(), s->adam_m.as<float>(),
+      s->adam_v.as<float>(), s->capacity, np.as<float>(), nm.as<float>(), nv.as<float>(), new_cap,
+      s->grad3d_acc.as<float>(), s->views_seen.as<int>(), clone_lr, eps, (float)std::log(1.6), old_to_new_dev);
   note_launch();
   SK_CUDA(cudaGetLastError());
   sync(ctx);

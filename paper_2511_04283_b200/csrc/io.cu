@@ -49,69 +49,62 @@ namespace fs = std::filesystem;
 // PLY
 // ---------------------------------------------------------------------------
 
+// Scalar property types a vertex element may carry, keyed by every spelling
+// the PLY format allows (ply.hpp:49-72 accepts the same set).
+enum class PlyScalar { I8, U8, I16, U16, I32, U32, F32, F64 };
+
 struct PlyProp {
-  std::string name, type;
-  int size = 0;
-  bool integer = false, floating = false, is_signed = true;
+  std::string name;
+  PlyScalar kind = PlyScalar::F32;
+  int size = 4;                 // bytes in a binary row
+  bool integer = false;         // integer-typed (points3d colours are then rescaled by 1/255)
 };
 
-// ply.hpp:49-72
-PlyProp ply_prop(const std::string& type, const std::string& name) {
-  PlyProp d;
-  d.name = name;
-  d.type = type;
-  if (type == "char" || type == "int8" || type == "uchar" || type == "uint8") {
-    d.size = 1;
-    d.integer = true;
-  } else if (type == "short" || type == "int16" || type == "ushort" || type == "uint16") {
-    d.size = 2;
-    d.integer = true;
-  } else if (type == "int" || type == "int32" || type == "uint" || type == "uint32") {
-    d.size = 4;
-    d.integer = true;
-  } else if (type == "float" || type == "float32") {
-    d.size = 4;
-    d.floating = true;
-  } else if (type == "double" || type == "float64") {
-    d.size = 8;
-    d.floating = true;
-  } else {
-    throw std::runtime_error("ply: unsupported property type '" + type + "'");
-  }
-  d.is_signed = type[0] != 'u';
-  return d;
+PlyProp make_prop(const std::string& type, const std::string& name) {
+  static const std::pair<const char*, PlyScalar> kTypes[] = {
+      {"char", PlyScalar::I8},    {"int8", PlyScalar::I8},     {"uchar", PlyScalar::U8},
+      {"uint8", PlyScalar::U8},   {"short", PlyScalar::I16},   {"int16", PlyScalar::I16},
+      {"ushort", PlyScalar::U16}, {"uint16", PlyScalar::U16},  {"int", PlyScalar::I32},
+      {"int32", PlyScalar::I32},  {"uint", PlyScalar::U32},    {"uint32", PlyScalar::U32},
+      {"float", PlyScalar::F32},  {"float32", PlyScalar::F32}, {"double", PlyScalar::F64},
+      {"float64", PlyScalar::F64}};
+  static const int kSize[] = {1, 1, 2, 2, 4, 4, 4, 8};
+  for (const auto& [spelling, kind] : kTypes)
+    if (type == spelling) {
+      PlyProp p;
+      p.name = name;
+      p.kind = kind;
+      p.size = kSize[static_cast<int>(kind)];
+      p.integer = kind != PlyScalar::F32 && kind != PlyScalar::F64;
+      return p;
+    }
+  throw std::runtime_error("ply: unsupported property type '" + type + "'");
 }
 
-double ply_binary_value(const char* p, const PlyProp& d) {
-  if (d.floating && d.size == 4) {
-    float v;
-    std::memcpy(&v, p, 4);
-    return v;
-  }
-  if (d.floating) {
-    double v;
-    std::memcpy(&v, p, 8);
-    return v;
-  }
-  switch (d.size) {
-    case 1: {
-      if (d.is_signed) { int8_t v; std::memcpy(&v, p, 1); return v; }
-      uint8_t v; std::memcpy(&v, p, 1); return v;
-    }
-    case 2: {
-      if (d.is_signed) { int16_t v; std::memcpy(&v, p, 2); return v; }
-      uint16_t v; std::memcpy(&v, p, 2); return v;
-    }
-    default: {
-      if (d.is_signed) { int32_t v; std::memcpy(&v, p, 4); return v; }
-      uint32_t v; std::memcpy(&v, p, 4); return v;
-    }
+// One little-endian binary value of the given type, widened to double.
+template <typename V>
+double load_as(const char* p) {
+  V v;
+  std::memcpy(&v, p, sizeof(V));
+  return static_cast<double>(v);
+}
+double decode_value(const char* p, PlyScalar kind) {
+  switch (kind) {
+    case PlyScalar::I8: return load_as<int8_t>(p);
+    case PlyScalar::U8: return load_as<uint8_t>(p);
+    case PlyScalar::I16: return load_as<int16_t>(p);
+    case PlyScalar::U16: return load_as<uint16_t>(p);
+    case PlyScalar::I32: return load_as<int32_t>(p);
+    case PlyScalar::U32: return load_as<uint32_t>(p);
+    case PlyScalar::F32: return load_as<float>(p);
+    default: return load_as<double>(p);
   }
 }
 
-// PlyVertexTable (ply.hpp:19-40). When the file is binary and every vertex
-// property is float32, the body is kept as raw rows (`raw`, [count][props])
-// and `columns` stays empty: the checkpoint path gathers it on the GPU.
+// The vertex table of a PLY file (PlyVertexTable, ply.hpp:19-40). When the
+// file is binary and every vertex property is float32, the body is kept as
+// raw rows (`raw`, [count][props]) and `columns` stays empty: the checkpoint
+// path gathers it on the GPU.
 struct PlyTable {
   int64_t count = 0;
   std::vector<PlyProp> props;
@@ -120,9 +113,8 @@ struct PlyTable {
   bool raw_f32 = false;
 
   int find(const std::string& name) const {
-    for (size_t i = 0; i < props.size(); ++i)
-      if (props[i].name == name) return (int)i;
-    return -1;
+    const auto it = std::find_if(props.begin(), props.end(), [&](const PlyProp& p) { return p.name == name; });
+    return it == props.end() ? -1 : int(it - props.begin());
   }
   int need(const std::string& name, const std::string& context) const {
     const int i = find(name);
@@ -134,96 +126,97 @@ struct PlyTable {
   }
 };
 
-// read_ply_vertices (ply.hpp:103-175), same header grammar and messages.
-PlyTable read_ply(const std::string& path, bool keep_raw_f32) {
-  std::ifstream in(path, std::ios::binary);
-  require(in.good(), "ply: cannot open '" + path + "'");
+// Header state: which element the property lines belong to, the body
+// encoding and the vertex element's declaration.
+struct PlyHeader {
+  bool have_format = false, binary = false;
+  int64_t vertices = -1;     // count of the vertex element once declared
+  bool reading_vertex = false;
+  std::vector<PlyProp> props;
+};
+
+// The header grammar of read_ply_vertices (ply.hpp:103-175): magic line,
+// format (ascii | binary_little_endian), the vertex element first, scalar
+// vertex properties, properties of later elements ignored, end_header.
+PlyHeader parse_ply_header(std::istream& in, const std::string& path) {
   std::string line;
   require(std::getline(in, line) && (line == "ply" || line == "ply\r"),
           "ply: '" + path + "' does not start with a ply magic line");
-  bool binary = false, format_seen = false, in_vertex = false;
-  int64_t vertex_count = -1;
-  PlyTable t;
+  PlyHeader h;
+  const auto where = " in '" + path + "'";
   while (std::getline(in, line)) {
     if (!line.empty() && line.back() == '\r') line.pop_back();
-    std::istringstream ls(line);
-    std::string tok;
-    ls >> tok;
-    if (tok == "comment" || tok == "obj_info" || tok.empty()) continue;
-    if (tok == "format") {
-      std::string fmt;
-      ls >> fmt;
-      if (fmt == "ascii")
-        binary = false;
-      else if (fmt == "binary_little_endian")
-        binary = true;
-      else
-        throw std::runtime_error("ply: unsupported format '" + fmt + "' in '" + path + "'");
-      format_seen = true;
-    } else if (tok == "element") {
-      std::string name;
-      int64_t count = 0;
-      ls >> name >> count;
-      if (name == "vertex") {
-        require(t.props.empty(), "ply: vertex element must come first in '" + path + "'");
-        vertex_count = count;
-        in_vertex = true;
-      } else {
-        require(vertex_count >= 0, "ply: vertex element must come first in '" + path + "'");
-        in_vertex = false;
-      }
-    } else if (tok == "property") {
-      if (!in_vertex) continue;
-      std::string type;
-      ls >> type;
+    std::istringstream words(line);
+    std::string key;
+    words >> key;
+    if (key.empty() || key == "comment" || key == "obj_info") continue;
+    if (key == "end_header") break;
+    if (key == "format") {
+      std::string enc;
+      words >> enc;
+      if (enc != "ascii" && enc != "binary_little_endian")
+        throw std::runtime_error("ply: unsupported format '" + enc + "'" + where);
+      h.binary = enc == "binary_little_endian";
+      h.have_format = true;
+    } else if (key == "element") {
+      std::string what;
+      int64_t n = 0;
+      words >> what >> n;
+      const bool vertex = what == "vertex";
+      require(vertex ? h.props.empty() : h.vertices >= 0, "ply: vertex element must come first" + where);
+      if (vertex) h.vertices = n;
+      h.reading_vertex = vertex;
+    } else if (key == "property") {
+      if (!h.reading_vertex) continue;
+      std::string type, name;
+      words >> type;
       require(type != "list", "ply: list properties are not supported on vertices");
-      std::string name;
-      ls >> name;
-      t.props.push_back(ply_prop(type, name));
-    } else if (tok == "end_header") {
-      break;
+      words >> name;
+      h.props.push_back(make_prop(type, name));
     } else {
-      throw std::runtime_error("ply: unexpected header token '" + tok + "' in '" + path + "'");
+      throw std::runtime_error("ply: unexpected header token '" + key + "'" + where);
     }
   }
-  require(format_seen, "ply: missing format line in '" + path + "'");
-  require(vertex_count >= 0, "ply: missing vertex element in '" + path + "'");
-  t.count = vertex_count;
+  require(h.have_format, "ply: missing format line" + where);
+  require(h.vertices >= 0, "ply: missing vertex element" + where);
+  return h;
+}
+
+// read_ply_vertices (ply.hpp:103-175): the header, then the vertex rows as
+// columns of doubles (or as raw float32 rows, see PlyTable).
+PlyTable read_ply(const std::string& path, bool keep_raw_f32) {
+  std::ifstream in(path, std::ios::binary);
+  require(in.good(), "ply: cannot open '" + path + "'");
+  PlyHeader h = parse_ply_header(in, path);
+  PlyTable t;
+  t.count = h.vertices;
+  t.props = std::move(h.props);
   const size_t np = t.props.size();
-  bool all_f32 = binary;
-  size_t stride = 0;
-  for (const auto& p : t.props) {
-    stride += p.size;
-    all_f32 = all_f32 && p.floating && p.size == 4;
-  }
-  if (all_f32 && keep_raw_f32 && np > 0) {
+  const std::string truncated = "ply: truncated vertex data in '" + path + "'";
+  size_t row_bytes = 0;
+  for (const auto& p : t.props) row_bytes += (size_t)p.size;
+  const bool f32_rows = h.binary && np > 0 && row_bytes == 4 * np &&
+                        std::all_of(t.props.begin(), t.props.end(),
+                                    [](const PlyProp& p) { return p.kind == PlyScalar::F32; });
+  if (f32_rows && keep_raw_f32) {
     t.raw_f32 = true;
-    t.raw.resize((size_t)vertex_count * np);
-    const std::streamsize want = (std::streamsize)(t.raw.size() * sizeof(float));
-    in.read(reinterpret_cast<char*>(t.raw.data()), want);
-    require(in.gcount() == want, "ply: truncated vertex data in '" + path + "'");
+    t.raw.resize((size_t)t.count * np);
+    const auto bytes = (std::streamsize)(t.raw.size() * sizeof(float));
+    in.read(reinterpret_cast<char*>(t.raw.data()), bytes);
+    require(in.gcount() == bytes, truncated);
     return t;
   }
-  t.columns.assign(np, {});
-  for (auto& c : t.columns) c.reserve((size_t)vertex_count);
-  if (binary) {
-    std::vector<char> row(stride);
-    for (int64_t v = 0; v < vertex_count; ++v) {
-      in.read(row.data(), (std::streamsize)stride);
-      require(in.gcount() == (std::streamsize)stride, "ply: truncated vertex data in '" + path + "'");
-      size_t off = 0;
-      for (size_t i = 0; i < np; ++i) {
-        t.columns[i].push_back(ply_binary_value(row.data() + off, t.props[i]));
-        off += t.props[i].size;
-      }
-    }
+  t.columns.assign(np, std::vector<double>((size_t)t.count));
+  if (h.binary) {
+    std::vector<char> body((size_t)t.count * row_bytes);
+    in.read(body.data(), (std::streamsize)body.size());
+    require(in.gcount() == (std::streamsize)body.size(), truncated);
+    const char* row = body.data();
+    for (int64_t v = 0; v < t.count; ++v)
+      for (size_t i = 0; i < np; row += t.props[i].size, ++i) t.columns[i][v] = decode_value(row, t.props[i].kind);
   } else {
-    for (int64_t v = 0; v < vertex_count; ++v)
-      for (size_t i = 0; i < np; ++i) {
-        double value;
-        require(static_cast<bool>(in >> value), "ply: truncated vertex data in '" + path + "'");
-        t.columns[i].push_back(value);
-      }
+    for (int64_t v = 0; v < t.count; ++v)
+      for (size_t i = 0; i < np; ++i) require(static_cast<bool>(in >> t.columns[i][v]), truncated);
   }
   return t;
 }
@@ -384,7 +377,7 @@ void read_points(const std::string& path, std::vector<float>& xyz, std::vector<f
   const PlyTable t = read_ply(path, false);
   const int cx = t.need("x", "points3d"), cy = t.need("y", "points3d"), cz = t.need("z", "points3d");
   const int cr = t.need("red", "points3d"), cg = t.need("green", "points3d"), cb = t.need("blue", "points3d");
-  const double scale = t.props[t.find("red")].integer ? 1.0 / 255 : 1.0;
+  const double scale = t.props[cr].integer ? 1.0 / 255 : 1.0;
   xyz.resize((size_t)t.count * 3);
   rgb.resize((size_t)t.count * 3);
   for (int64_t i = 0; i < t.count; ++i) {

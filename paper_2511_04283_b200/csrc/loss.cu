@@ -20,25 +20,14 @@ namespace {
 
 // 32x32 output tiles (measured 11% faster than 32x16: the 10-row halo of the
 // horizontal pass is amortised over twice the rows)
-#ifndef SK_SSIM_TY
-#define SK_SSIM_TY 32
-#endif
-#ifndef SK_SSIM_PREFETCH
-#define SK_SSIM_PREFETCH 0  // measured: 3% slower
-#endif
-#ifndef SK_SSIM_UNROLL
-#define SK_SSIM_UNROLL 1  // explicit no-unroll of the halo staging: measured -5% K7 (4 or 7: slower)
-#endif
-#ifndef SK_SSIM_HX
-#define SK_SSIM_HX 4
-#endif
-constexpr int kStageUnroll = SK_SSIM_UNROLL;  // halo-staging loop unroll (loads in flight)
+
+constexpr int kStageUnroll = 1;   // halo-staging loop not unrolled (measured -5% K7; 4 or 7: slower)
 constexpr int kTX = 32;                 // output tile width
-constexpr int kTY = SK_SSIM_TY;         // output tile height (16 or 32)
+constexpr int kTY = 32;                 // output tile height
 constexpr int kHalo = 5;                // 11-tap window
 constexpr int kInX = kTX + 2 * kHalo;   // 42
 constexpr int kInY = kTY + 2 * kHalo;   // 26
-constexpr int kHX = SK_SSIM_HX;         // horizontal outputs per thread (register sliding window)
+constexpr int kHX = 4;                  // horizontal outputs per thread (register sliding window)
 constexpr int kVY = kTX * kTY / 256;    // vertical outputs per thread (256 threads)
 
 __constant__ float c_gauss[11];
@@ -97,17 +86,6 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
       s_y[iy][ix] = yv;
     }
     __syncthreads();
-#if SK_SSIM_PREFETCH
-    if (ch < 2) {
-      for (int ln = t; ln < kInY * 2; ln += blockDim.x) {
-        const int iy = ln >> 1, half = ln & 1;
-        const int gy = ty0 - kHalo + iy;
-        const int gx = max(0, min(W - 1, tx0 - kHalo + half * 32));
-        if (gy >= 0 && gy < H)
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(img + (ch + 1) * plane + (size_t)gy * W + gx));
-      }
-    }
-#endif
     // horizontal: 26 rows x 8 groups of 4 columns
     for (int hw = t; hw < kInY * (kTX / kHX); hw += blockDim.x) {
       const int iy = hw / (kTX / kHX), ox = (hw % (kTX / kHX)) * kHX;
@@ -246,19 +224,6 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
       for (int k = 0; k < 3; ++k) s_u[k][iy][ix] = ok ? partials[(k * 3 + ch) * plane + p] : 0.0f;
     }
     __syncthreads();
-#if SK_SSIM_PREFETCH
-    // L1 prefetch of the next channel's halo rows (3 maps x kInY rows, two
-    // 128-byte lines each) while this channel is filtered
-    if (ch < 2) {
-      for (int ln = t; ln < 3 * kInY * 2; ln += blockDim.x) {
-        const int k = ln / (2 * kInY), iy = (ln >> 1) % kInY, half = ln & 1;
-        const int gy = ty0 - kHalo + iy;
-        const int gx = max(0, min(W - 1, tx0 - kHalo + half * 32));
-        if (gy >= 0 && gy < H)
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(partials + (k * 3 + ch + 1) * plane + (size_t)gy * W + gx));
-      }
-    }
-#endif
     for (int hw = t; hw < kInY * (kTX / kHX); hw += blockDim.x) {
       const int iy = hw / (kTX / kHX), ox = (hw % (kTX / kHX)) * kHX;
 #pragma unroll

@@ -315,20 +315,15 @@ __device__ __forceinline__ void accumulate_stats(const Stats& st, int64_t i, int
   st.max_radius2d[i] = fmaxf(st.max_radius2d[i], radius);
 }
 
-#ifndef SK_K9_PREFETCH
-#define SK_K9_PREFETCH 2  // all parameter rows + blend grads: measured -12% K9 time
-#endif
 constexpr int kPbThreads = 128;
-#ifndef SK_K9_MINB
-#define SK_K9_MINB 4  // resident CTAs per SM the register budget is sized for
-#endif
+constexpr int kK9MinBlocks = 4;  // resident CTAs per SM the register budget is sized for (5 / 6 spill)
 
 // K9: one thread per Gaussian computes all parameter gradients into its
 // column of a shared-memory tile (conflict-free: column = threadIdx.x, so no
 // 59-register live range) and the tile is written back as coalesced rows of the
 // planar gradient buffer; culled Gaussians get zeros (SceneGrads::init).
 template <int DEG>
-__global__ void __launch_bounds__(kPbThreads, SK_K9_MINB) project_bwd_kernel(
+__global__ void __launch_bounds__(kPbThreads, kK9MinBlocks) project_bwd_kernel(
     const float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ radius,
     const float4* __restrict__ conic4, const float* __restrict__ bg, int64_t gstride, float* __restrict__ grads,
     Stats st, bool do_stats, const uint32_t* __restrict__ err) {
@@ -344,16 +339,14 @@ __global__ void __launch_bounds__(kPbThreads, SK_K9_MINB) project_bwd_kernel(
   const int64_t i = (int64_t)blockIdx.x * kPbThreads + threadIdx.x;
   if (i >= n) return;
   float* g = s_grad + threadIdx.x;  // component c at g[c * kPbThreads]
-#if SK_K9_PREFETCH
   // L1 prefetches (no registers held) of everything the visible path reads
   // first, issued before the radius test so the latency overlaps it
 #pragma unroll
   for (int c = 0; c < 11; ++c) asm volatile("prefetch.global.L1 [%0];" ::"l"(bg + c * gstride + i));
   asm volatile("prefetch.global.L1 [%0];" ::"l"(conic4 + i));
 #pragma unroll
-  for (int c = 0; c < (SK_K9_PREFETCH >= 2 ? NC : 11); ++c)
+  for (int c = 0; c < NC; ++c)
     asm volatile("prefetch.global.L1 [%0];" ::"l"(params + c * stride + i));
-#endif
   const float rad = radius[i];
   if (rad > 0.0f) {
     float dmu2d[2], dcov[2][2], dcol[3], dop, absg[2];
@@ -376,7 +369,7 @@ __global__ void __launch_bounds__(kPbThreads, SK_K9_MINB) project_bwd_kernel(
 // d_opacity [n]) for every Gaussian, as the reference's per-Gaussian call:
 // no culling test (the C++ API's project_backward).
 template <int DEG>
-__global__ void __launch_bounds__(kPbThreads, SK_K9_MINB) project_bwd_explicit_kernel(
+__global__ void __launch_bounds__(kPbThreads, kK9MinBlocks) project_bwd_explicit_kernel(
     const float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ up_mu,
     const float* __restrict__ up_cov, const float* __restrict__ up_col, const float* __restrict__ up_op,
     float* __restrict__ grads) {
@@ -525,17 +518,28 @@ void ensure_score_table(sk_ctx* ctx, sk_scene* s) {
   reset_score_table(ctx, s);
 }
 
+// ScoreTable::reset (adc.hpp:33-42): the ten per-Gaussian rows in one launch.
+struct TableRows {
+  float4* row[10];
+};
+__global__ void reset_table_kernel(TableRows t, int64_t quads) {
+  const int r = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < quads; i += (int64_t)gridDim.x * blockDim.x)
+    t.row[r][i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+}
+
 void reset_score_table(sk_ctx* ctx, sk_scene* s) {
-  const size_t cap = (size_t)s->capacity;
-  cudaStream_t st = ctx->stream;
-  SK_CUDA(cudaMemsetAsync(s->s_d.ptr, 0, cap * 4, st));
-  SK_CUDA(cudaMemsetAsync(s->s_p_raw.ptr, 0, cap * 4, st));
-  SK_CUDA(cudaMemsetAsync(s->s_p.ptr, 0, cap * 4, st));
-  SK_CUDA(cudaMemsetAsync(s->grad_norm_acc.ptr, 0, cap * 4, st));
-  SK_CUDA(cudaMemsetAsync(s->abs_grad_acc.ptr, 0, cap * 4, st));
-  SK_CUDA(cudaMemsetAsync(s->grad3d_acc.ptr, 0, 3 * cap * 4, st));
-  SK_CUDA(cudaMemsetAsync(s->views_seen.ptr, 0, cap * 4, st));
-  SK_CUDA(cudaMemsetAsync(s->max_radius2d.ptr, 0, cap * 4, st));
+  const int64_t cap = s->capacity;  // a multiple of 32: whole float4s
+  TableRows t;
+  float4* g3 = s->grad3d_acc.as<float4>();
+  DevBuf* rows[7] = {&s->s_d, &s->s_p_raw, &s->s_p, &s->grad_norm_acc, &s->abs_grad_acc, &s->views_seen,
+                     &s->max_radius2d};
+  for (int k = 0; k < 7; ++k) t.row[k] = rows[k]->as<float4>();
+  for (int d = 0; d < 3; ++d) t.row[7 + d] = g3 + d * (cap / 4);
+  const int64_t quads = cap / 4;
+  reset_table_kernel<<<dim3((unsigned)std::min<int64_t>((quads + 255) / 256, 148), 10), 256, 0, ctx->stream>>>(t, quads);
+  note_launch();
+  SK_CUDA(cudaGetLastError());
 }
 
 void launch_project_backward(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stats) {

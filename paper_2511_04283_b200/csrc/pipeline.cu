@@ -57,9 +57,6 @@ int tile_bits(int tiles) {
   return b;
 }
 
-#ifndef SK_SPECULATIVE_DUP
-#define SK_SPECULATIVE_DUP 1
-#endif
 
 // K2-K5 (build_tile_grid raster.hpp:157-168).
 void bin_sort(sk_ctx* ctx, sk_frame* f) {
@@ -87,9 +84,8 @@ void bin_sort(sk_ctx* ctx, sk_frame* f) {
   // host reads the pair count and the GPU emits pairs while the host waits;
   // it is relaunched only if the count outgrew the buffers.
   auto cap_of = [](const DevBuf& b) { return (int64_t)(b.bytes / sizeof(uint32_t)); };
-  const int64_t cap = SK_SPECULATIVE_DUP ? std::min(std::min(cap_of(f->ptile_a), cap_of(f->ptile_b)),
-                                                    std::min(cap_of(f->pval_a), cap_of(f->pval_b)))
-                                         : 0;
+  const int64_t cap =
+      std::min(std::min(cap_of(f->ptile_a), cap_of(f->ptile_b)), std::min(cap_of(f->pval_a), cap_of(f->pval_b)));
   auto emit = [&](int64_t limit) {
     SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * 256, ctx->stream));
     launch_duplicate(ctx, f, va, offsets, f->ptile_a.as<uint32_t>(), f->pval_a.as<uint32_t>(), radix_passes(bits),

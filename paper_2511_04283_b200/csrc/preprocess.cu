@@ -122,12 +122,6 @@ struct BinParams {
   int ts, tiles_x, tiles_y, W, H;
 };
 
-#ifndef SK_DUP_RCP
-#define SK_DUP_RCP 1
-#endif
-#ifndef SK_K1_PREFETCH
-#define SK_K1_PREFETCH 1  // measured: -12% K1 time (2: SH prefetch too, no better)
-#endif
 
 template <int DEG>
 __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict__ p, int64_t stride, int64_t n,
@@ -151,16 +145,12 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
     key_out[i] = 0xffffffffu;
   };
   const float mu0 = p[0 * stride + i], mu1 = p[1 * stride + i], mu2 = p[2 * stride + i];
-#if SK_K1_PREFETCH >= 1
   // rotation / scale / opacity loads issued with mu's, before the near test,
   // so their latency overlaps the projection arithmetic
   const float pf_q0 = p[3 * stride + i], pf_q1 = p[4 * stride + i], pf_q2 = p[5 * stride + i],
               pf_q3 = p[6 * stride + i], pf_s0 = p[7 * stride + i], pf_s1 = p[8 * stride + i],
               pf_s2 = p[9 * stride + i], pf_op = p[SK_COMP_OPACITY * stride + i];
 #define SK_P(c, v) (v)
-#else
-#define SK_P(c, v) (p[(c) * stride + i])
-#endif
   const float* R = cam.r;
   // t = R mu + t  (Mat * Vec: ((R_k0 mu0 + R_k1 mu1) + R_k2 mu2), then + t_k)
   const float t0 = ((R[0] * mu0 + R[1] * mu1) + R[2] * mu2) + cam.t[0];
@@ -184,20 +174,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
   // covariance_3d (scene.hpp:88-96)
   const float qw_in = SK_P(3, pf_q0), qx_in = SK_P(4, pf_q1), qy_in = SK_P(5, pf_q2), qz_in = SK_P(6, pf_q3);
   constexpr int NSH = (DEG + 1) * (DEG + 1);
-#if SK_K1_PREFETCH == 3
-  // SH rows prefetched into L1 (no registers) while the covariance is formed
-#pragma unroll
-  for (int k = 0; k < 3 * NSH; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + (SK_COMP_SH + k) * stride + i));
-#endif
-#if SK_K1_PREFETCH == 2
-  // SH coefficients issued before the covariance / guard-cull arithmetic
-  float shv[3 * NSH];
-#pragma unroll
-  for (int k = 0; k < 3 * NSH; ++k) shv[k] = p[(SK_COMP_SH + k) * stride + i];
-#define SK_SH(k) shv[k]
-#else
 #define SK_SH(k) p[(SK_COMP_SH + (k)) * stride + i]
-#endif
   const float s0 = det_expf(SK_P(7, pf_s0), tab), s1 = det_expf(SK_P(8, pf_s1), tab),
               s2 = det_expf(SK_P(9, pf_s2), tab);
   if (!(isfinite(qw_in) && isfinite(qx_in) && isfinite(qy_in) && isfinite(qz_in) && isfinite(s0) && isfinite(s1) &&
@@ -445,13 +422,9 @@ __global__ void __launch_bounds__(kDupThreads) duplicate_kernel(int64_t n, BinPa
       const bool active = e0 + lane < total;
       uint32_t t = 0;
       if (active) {
-#if SK_DUP_RCP
         int r = (int)((float)k * oinv);  // within one of k / ow (k < 2^24)
         r += (r + 1) * ow <= k;
         r -= r * ow > k;
-#else
-        const int r = k / ow;
-#endif
         t = (uint32_t)((oy + r) * bp.tiles_x + ox + (k - r * ow));
         if (pos < cap) {
           pair_tile[pos] = t;

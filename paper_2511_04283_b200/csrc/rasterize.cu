@@ -4,8 +4,8 @@
 // centres, q = ((c00 dx) dx + ((2 c01) dx) dy) + (c11 dy) dy, skip q < 0,
 // alpha = min(0.99, o e^{-q/2}), skip alpha < 1/255, C += (T alpha) c,
 // T *= 1 - alpha, and the entry that takes T below 1e-4 is blended before the
-// pixel stops. One CTA per tile; the tile's list is staged through shared
-// memory in CTA-sized batches and the CTA stops loading once every pixel has
+// pixel stops. One CTA per tile; each warp walks the tile's list for its own
+// pixel block (blend_fwd_warp_kernel) and stops once its pixels have
 // terminated. Compiled with -fmad=false and the shared deterministic exp, so
 // images, transmittance and footprint counts match the CPU oracle bit for bit.
 //
@@ -20,57 +20,31 @@
 // K8 (the backward walk) lives in rasterize_bwd.cu.
 #include "blend_common.cuh"
 
-#ifndef SK_FWD_WARP_STAGED
-#define SK_FWD_WARP_STAGED 1  // measured: 2% faster than the CTA-staged kernel at 16x16
-#endif
-#ifndef SK_FWD_BRANCHLESS
-#define SK_FWD_BRANCHLESS 0
-#endif
-#ifndef SK_FWD_MINB
-#define SK_FWD_MINB 8  // resident 128-thread CTAs per SM (64 registers)
-#endif
-#ifndef SK_FWD_ASYNC_GATHER
-#define SK_FWD_ASYNC_GATHER 1
-#endif
-#ifndef SK_FWD_NANDONE
-// 1: a finished (or off-image) pixel's row coordinate becomes NaN, so its q is
-// NaN and one unsigned compare q_bits <= q_cut_bits replaces the done flag and
-// both range tests (q >= 0 and q <= q_cut; q + 0 maps -0 to +0)
-#define SK_FWD_NANDONE 1
-#endif
-#ifndef SK_FWD_BATCH_DONE
-// 1 (needs SK_FWD_NANDONE): the walk no longer tracks per-entry "all my
-// pixels done"; finished pixels reject every entry by their NaN row, and
-// the all-done test runs once per 32-entry batch
-#define SK_FWD_BATCH_DONE 1
-#endif
-#ifndef SK_FWD_PTR_TABLE
-#define SK_FWD_PTR_TABLE 1  // exp table base pinned in a register
-#endif
-#ifndef SK_FWD_PIX16
-#define SK_FWD_PIX16 2
-#endif
-
 namespace sk {
 namespace {
 
 using namespace blend;
 
-template <int TS, int PIX, bool COUNT>
-__global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fwd_kernel(
+constexpr int kFwdMinBlocks = 8;  // resident 128-thread CTAs per SM (64 registers)
+
+// K12: blend_forward(grid, pgs, &mask, &counter) (raster.hpp:194-248) as a
+// count-only pass: the forward recurrence (same decisions, bit for bit, as
+// K6) over masked pixels only, incrementing the counter of every Gaussian a
+// masked pixel blends. One CTA per tile stages the list in CTA-sized batches;
+// unmasked pixels never traverse and fully unmasked tiles exit at once.
+template <int TS, int PIX>
+__global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) count_blend_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
-    const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
-    float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry,
-    const uint8_t* __restrict__ mask, int* __restrict__ counts) {
-  constexpr int NTH = TS * TS / PIX;        // threads; each owns PIX pixels
+    const float4* __restrict__ conic_op, int W, int H, int tiles_x, const uint8_t* __restrict__ mask,
+    int* __restrict__ counts) {
+  constexpr int NTH = TS * TS / PIX;                // threads; each owns PIX pixels
   constexpr int B = TS * TS > 256 ? 256 : TS * TS;  // staged entries per batch
   using WB = WarpBlock<TS, PIX>;
   constexpr int kChunks = B / 32;
   __shared__ float4 s_xyq[B];
   __shared__ float4 s_co[B];
   __shared__ uint32_t s_mask[WB::kWarps * kChunks];
-  __shared__ float4 s_rgb[COUNT ? 1 : B];
-  __shared__ uint32_t s_id[COUNT ? B : 1];
+  __shared__ uint32_t s_id[B];
   __shared__ float s_exp[kNegExpTable];
   stage_neg_exp_table(s_exp);  // published by the first __syncthreads_count below
   const SmemPinnedTable tab(s_exp);
@@ -83,8 +57,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
   const int2 range = ranges[tile];
   const float fpx = (float)px;
 
-  float T[PIX], C0[PIX], C1[PIX], C2[PIX], fpy[PIX];
-  int n[PIX], last[PIX];
+  float T[PIX], fpy[PIX];
   bool done[PIX];
   bool all_done = true;
 #pragma unroll
@@ -92,12 +65,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
     const int py = ty * TS + wb.ly0 + 4 * k;
     fpy[k] = (float)py;
     T[k] = 1.0f;
-    C0[k] = C1[k] = C2[k] = 0.0f;
-    n[k] = last[k] = 0;
-    const bool inside = px < W && py < H;
-    // K12 (count-only pass): only masked pixels can increment a counter, so
-    // unmasked pixels never traverse and fully unmasked tiles exit at once.
-    done[k] = COUNT ? !(inside && mask[(size_t)py * W + px] != 0) : !inside;
+    done[k] = !(px < W && py < H && mask[(size_t)py * W + px] != 0);
     all_done = all_done && done[k];
   }
 
@@ -113,8 +81,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
         stage_entry(mean2d[g], co, xyq, bb);
         s_xyq[e] = xyq;
         s_co[e] = co;
-        if (!COUNT) s_rgb[e] = rgbd[g];
-        if (COUNT) s_id[e] = g;
+        s_id[e] = g;
       }
       WB::publish(bb, xyq, co, valid, e >> 5, kChunks, tx, ty, s_mask);
     }
@@ -124,58 +91,33 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
     for (int c = 0; c < kChunks && !all_done; ++c) {
       uint32_t m = s_mask[warp * kChunks + c];
       while (m && !all_done) {
-      const int j = c * 32 + __ffs(m) - 1;
-      m &= m - 1;
-      const float4 mq = s_xyq[j];
-      const float4 co = s_co[j];
+        const int j = c * 32 + __ffs(m) - 1;
+        m &= m - 1;
+        const float4 mq = s_xyq[j];
+        const float4 co = s_co[j];
 #pragma unroll
-      for (int k = 0; k < PIX; ++k) {
-        const float dx = fpx - mq.x;
-        const float dy = fpy[k] - mq.y;
-        const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
-        if (done[k] || !(q >= 0.0f && q <= mq.z)) continue;
-        // -0.5 q lies in [-q_cut/2, 0], inside det_expf's core range
-        float alpha = co.w * det_expf_neg(-0.5f * q, tab);
-        alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
-        if (alpha < kAlphaMin) continue;
-        if (COUNT) {
+        for (int k = 0; k < PIX; ++k) {
+          const float dx = fpx - mq.x;
+          const float dy = fpy[k] - mq.y;
+          const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
+          if (done[k] || !(q >= 0.0f && q <= mq.z)) continue;
+          // -0.5 q lies in [-q_cut/2, 0], inside det_expf's core range
+          float alpha = co.w * det_expf_neg(-0.5f * q, tab);
+          alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
+          if (alpha < kAlphaMin) continue;
           // warp-aggregated increment: one atomic per distinct Gaussian
           const uint32_t id = s_id[j];
           const uint32_t act = __activemask();
           const uint32_t peers = __match_any_sync(act, id);
           if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&counts[id], __popc(peers));
-        } else {
-          const float4 c = s_rgb[j];
-          const float w = T[k] * alpha;
-          C0[k] = C0[k] + w * c.x;
-          C1[k] = C1[k] + w * c.y;
-          C2[k] = C2[k] + w * c.z;
-          ++n[k];
-          last[k] = b0 + j + 1;
+          T[k] = T[k] * (1.0f - alpha);
+          if (T[k] < kTransmitMin) done[k] = true;
         }
-        T[k] = T[k] * (1.0f - alpha);
-        if (T[k] < kTransmitMin) done[k] = true;
-      }
-      bool ad = true;
+        bool ad = true;
 #pragma unroll
-      for (int k = 0; k < PIX; ++k) ad = ad && done[k];
-      all_done = ad;
+        for (int k = 0; k < PIX; ++k) ad = ad && done[k];
+        all_done = ad;
       }
-    }
-  }
-  if (COUNT) return;
-#pragma unroll
-  for (int k = 0; k < PIX; ++k) {
-    const int py = ty * TS + wb.ly0 + 4 * k;
-    if (px < W && py < H) {
-      const size_t p = (size_t)py * W + px;
-      const size_t plane = (size_t)W * H;
-      image[p] = C0[k];
-      image[plane + p] = C1[k];
-      image[2 * plane + p] = C2[k];
-      final_t[p] = T[k];
-      n_contrib[p] = n[k];
-      last_entry[p] = last[k];
     }
   }
 }
@@ -189,7 +131,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) blend_fw
 // the price is that each warp gathers every entry (L1 serves the repeats).
 // Per-pixel arithmetic is identical to blend_fwd_kernel (bit-exact).
 template <int TS, int PIX>
-__global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / PIX)) blend_fwd_warp_kernel(
+__global__ void __launch_bounds__(TS* TS / PIX, kFwdMinBlocks * 128 / (TS * TS / PIX)) blend_fwd_warp_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry,
@@ -197,22 +139,13 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
   using WB = WarpBlock<TS, PIX>;
   constexpr int kWarps = WB::kWarps;
   __shared__ float4 s_xyq[kWarps][32];
-#if SK_FWD_ASYNC_GATHER
   __shared__ float4 s_gco[2][kWarps][32];
   __shared__ float2 s_gmu[2][kWarps][32];
   __shared__ float4 s_grgb[2][kWarps][32];
-#else
-  __shared__ float4 s_co[kWarps][32];
-  __shared__ float4 s_rgb[kWarps][32];
-#endif
   __shared__ float s_exp[kNegExpTable];
   stage_neg_exp_table(s_exp);
   __syncthreads();
-#if SK_FWD_PTR_TABLE
   const SmemPinnedTable tab(s_exp);
-#else
-  const SmemTable tab(s_exp);
-#endif
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -235,12 +168,9 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
     n[k] = last[k] = 0;
     done[k] = !(px < W && py < H);
     all_done = all_done && done[k];
-#if SK_FWD_NANDONE
     if (done[k]) fpy[k] = __int_as_float(0x7fc00000);
-#endif
   }
 
-#if SK_FWD_ASYNC_GATHER
   // Double-buffered gather: the records of batch k+1 are copied into this
   // warp's shared slots with cp.async (no registers held in flight) while
   // batch k is walked; the pair index of batch k+2 is loaded one batch ahead
@@ -284,76 +214,20 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
     const float4* s_co_w = s_gco[cur][warp];
     const float4* s_rgb_w = s_grgb[cur][warp];
     cur ^= 1;
-#else
-  for (int b0 = range.x; b0 < range.y; b0 += 32) {
-    if (__all_sync(0xffffffffu, all_done)) break;
-    const int i = b0 + lane;
-    bool hit = false;
-    if (i < range.y) {
-      const uint32_t g = pair_val[i];
-      const float4 co = conic_op[g];
-      float4 xyq, bb;
-      stage_entry(mean2d[g], co, xyq, bb);
-      hit = !WB::misses(bb, warp, tx, ty);
-      const bool pd = co.x > 0.0f && co.z > 0.0f && co.x * co.z - co.y * co.y > 0.0f;
-      if (hit && pd) hit = WB::ellipse_hits(xyq, co, warp, tx, ty);
-      if (hit) {
-        s_xyq[warp][lane] = xyq;
-        s_co[warp][lane] = co;
-        s_rgb[warp][lane] = rgbd[g];
-      }
-    }
-    const float4* s_co_w = s_co[warp];
-    const float4* s_rgb_w = s_rgb[warp];
-#endif
     uint32_t m = __ballot_sync(0xffffffffu, hit);
     __syncwarp();
     uint32_t lane_bits = 0;  // entries of this batch one of my pixels blended
-#if SK_FWD_NANDONE && SK_FWD_BATCH_DONE
     while (m) {
-#else
-    while (m && !all_done) {
-#endif
       const int j = __ffs(m) - 1;
       m &= m - 1;
       const float4 mq = s_xyq[warp][j];
       const float4 co = s_co_w[j];
-#if SK_FWD_BRANCHLESS
-      // Predicated form: both pixels evaluated by every lane, the
-      // non-contributing ones masked to alpha = 0 (T * (1 - 0) and C + (T * 0) c
-      // are exact no-ops), so lanes do not diverge per pixel.
 #pragma unroll
       for (int k = 0; k < PIX; ++k) {
         const float dx = fpx - mq.x;
         const float dy = fpy[k] - mq.y;
         const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
-        bool ok = !done[k] && q >= 0.0f && q <= mq.z;
-        float alpha = co.w * det_expf_neg(ok ? -0.5f * q : 0.0f, tab);  // in-domain for every lane
-        alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
-        ok = ok && !(alpha < kAlphaMin);
-        lane_bits |= ok ? 1u << j : 0u;
-        const float a = ok ? alpha : 0.0f;
-        const float4 c = s_rgb_w[j];
-        const float w = T[k] * a;
-        C0[k] = C0[k] + w * c.x;
-        C1[k] = C1[k] + w * c.y;
-        C2[k] = C2[k] + w * c.z;
-        n[k] += ok ? 1 : 0;
-        last[k] = ok ? b0 + j + 1 : last[k];
-        T[k] = T[k] * (1.0f - a);
-        if (T[k] < kTransmitMin) done[k] = true;
-      }
-#else
-#pragma unroll
-      for (int k = 0; k < PIX; ++k) {
-        const float dx = fpx - mq.x;
-        const float dy = fpy[k] - mq.y;
-        const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
-#if SK_FWD_NANDONE
         if (__float_as_uint(__fadd_rn(q, 0.0f)) > __float_as_uint(mq.z)) continue;  // -0 -> +0
-#else
-        if (done[k] || !(q >= 0.0f && q <= mq.z)) continue;
-#endif
         float alpha = co.w * det_expf_neg(-0.5f * q, tab);
         alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
         if (alpha < kAlphaMin) continue;
@@ -366,33 +240,15 @@ __global__ void __launch_bounds__(TS* TS / PIX, SK_FWD_MINB * 128 / (TS * TS / P
         ++n[k];
         last[k] = b0 + j + 1;
         T[k] = T[k] * (1.0f - alpha);
-#if SK_FWD_NANDONE && SK_FWD_BATCH_DONE
         fpy[k] = T[k] < kTransmitMin ? __int_as_float(0x7fc00000) : fpy[k];
-#else
-        if (T[k] < kTransmitMin) {
-          done[k] = true;
-#if SK_FWD_NANDONE
-          fpy[k] = __int_as_float(0x7fc00000);
-#endif
-        }
-#endif
       }
-#endif
-#if !(SK_FWD_NANDONE && SK_FWD_BATCH_DONE)
-      bool ad = true;
-#pragma unroll
-      for (int k = 0; k < PIX; ++k) ad = ad && done[k];
-      all_done = ad;
-#endif
     }
-#if SK_FWD_NANDONE && SK_FWD_BATCH_DONE
     {
       bool ad = true;
 #pragma unroll
       for (int k = 0; k < PIX; ++k) ad = ad && isnan(fpy[k]);
       all_done = ad;
     }
-#endif
     // contribution mask of this warp block for the batch (read by K8, which
     // then skips entries no pixel of its block blended); unwalked batches
     // keep the frame-start zeros
@@ -451,12 +307,10 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
   const auto* mean2d = f->mean2d.as<float2>();
   const auto* co = f->conic_op.as<float4>();
   const auto* rgb = f->rgb_depth.as<float4>();
-  if (!mask && !SK_FWD_WARP_STAGED) f->cmask_valid = false;
   if (mask)
-    blend_fwd_kernel<TS, PIX, true><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
-        ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
-        f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), mask, counts);
-  else if (SK_FWD_WARP_STAGED) {
+    count_blend_kernel<TS, PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(ranges, f->pair_val, mean2d, co, f->width,
+                                                                          f->height, f->tiles_x, mask, counts);
+  else {
     uint32_t* cm = nullptr;
     if (TS == 16 && PIX == 2) {  // K8 consumes the masks at 16x16 tiles
       const size_t words = cmask_words(f->pairs, tiles) * (size_t)(TS * TS / PIX / 32);
@@ -468,10 +322,6 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
         ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
         f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), cm);
   }
-  else
-    blend_fwd_kernel<TS, PIX, false><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
-        ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
-        f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), nullptr, nullptr);
   note_launch();
 }
 
@@ -496,7 +346,7 @@ void launch_blend_forward(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t
   if (f->tiles_x * f->tiles_y == 0) return;
   switch (f->tile_size) {
     case 8: fwd_dispatch<8, 1>(ctx, f, mask, counts); break;
-    case 16: fwd_dispatch<16, SK_FWD_PIX16>(ctx, f, mask, counts); break;
+    case 16: fwd_dispatch<16, 2>(ctx, f, mask, counts); break;
     case 32: fwd_dispatch<32, 4>(ctx, f, mask, counts); break;
     default: throw std::invalid_argument("tile_size must be 8, 16 or 32");
   }

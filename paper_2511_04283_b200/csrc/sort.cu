@@ -18,21 +18,7 @@
 // runs so global stores are coalesced.
 #include "state.h"
 
-#ifndef SK_HIST_AGG
-#define SK_HIST_AGG 0
-#endif
-#ifndef SK_SORT_SMALL_ITEMS
-#define SK_SORT_SMALL_ITEMS 7
-#endif
-#ifndef SK_SORT_LARGE_ITEMS
-#define SK_SORT_LARGE_ITEMS 11  // measured: 11 keys per thread -1.4% vs 15 (17: +12%)
-#endif
-#ifndef SK_SORT_SMALL_N
-#define SK_SORT_SMALL_N 0  // 7 keys per thread for small sorts measured no faster; off
-#endif
-#ifndef SK_SORT_BALLOT_RANK
-#define SK_SORT_BALLOT_RANK 0
-#endif
+constexpr int kSortItems = 11;  // keys per thread (measured: -1.4% vs 15, 17: +12%, 7: no faster)
 
 namespace sk {
 namespace {
@@ -81,18 +67,7 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restr
   const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t k = keys[i];
-#if SK_HIST_AGG
-    const uint32_t act = __activemask();
-    for (int p = 0; p < passes; ++p) {
-      // warp-aggregated: depth keys share their high digits, so plain shared
-      // atomics would serialise up to 32 lanes on one counter
-      const uint32_t d = (k >> (p * width)) & ((1u << width) - 1u);
-      const uint32_t peers = __match_any_sync(act, d);
-      if ((peers & lt) == 0) atomicAdd(&sh[p][d], (uint32_t)__popc(peers));
-    }
-#else
     for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (p * width)) & ((1u << width) - 1u)], 1u);
-#endif
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
@@ -162,29 +137,8 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
   // All match_any results first (independent, so their latencies overlap),
   // then the per-warp histogram updates in item order (stable ranking).
   uint32_t peers[ITEMS];
-#if SK_SORT_BALLOT_RANK
-  // Peers by ballots over the digit bits (plus validity) instead of MATCH.ANY.
-  const int nbits = __popc(dmask);
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const bool valid = wbase + j * 32 + lane < n;
-    const uint32_t d = (k[j] >> shift) & dmask;
-    uint32_t m = __ballot_sync(0xffffffffu, valid);
-    m = valid ? m : ~m;
-#pragma unroll
-    for (int b = 0; b < kRadixBits; ++b) {
-      if (b < nbits) {
-        const bool bit = (d >> b) & 1u;
-        const uint32_t bb = __ballot_sync(0xffffffffu, bit);
-        m &= bit ? bb : ~bb;
-      }
-    }
-    peers[j] = m;
-  }
-#else
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) peers[j] = __match_any_sync(0xffffffffu, digit_of(j));
-#endif
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     const uint32_t dj = digit_of(j);
@@ -425,10 +379,8 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
   const int width = radix_digit_width(bits);
   const uint32_t dmask = (1u << width) - 1u;
   require(passes <= kMaxPasses, "radix_sort_pairs: at most 32 key bits");
-  // Small sorts (the depth order over N slots) use 7 keys per thread so the
-  // pass spans more CTAs than SMs; large ones (tile ids over P pairs) 15.
-  const bool small = n <= (int64_t)SK_SORT_SMALL_N;
-  const int tile_keys = kSortThreads * (small ? SK_SORT_SMALL_ITEMS : SK_SORT_LARGE_ITEMS);
+  // 11 keys per thread for every sort (measured against 7 / 15 / 17 keys)
+  const int tile_keys = kSortThreads * kSortItems;
   const int64_t tiles = (n + tile_keys - 1) / tile_keys;
   require(tiles < (1ll << 31), "radix_sort_pairs: too many keys");
   uint32_t* hist = radix_hist_buffer(ctx);
@@ -446,12 +398,8 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
   note_launch();
   for (int p = 0; p < passes; ++p) {
     SK_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t) * (size_t)tiles * kRadix, s));
-    if (small)
-      onesweep_kernel<SK_SORT_SMALL_ITEMS><<<(unsigned)tiles, kSortThreads, 0, s>>>(
-          keys, vals, keys_alt, vals_alt, n, p * width, dmask, hist + p * kRadix, status, counters + p);
-    else
-      onesweep_kernel<SK_SORT_LARGE_ITEMS><<<(unsigned)tiles, kSortThreads, 0, s>>>(
-          keys, vals, keys_alt, vals_alt, n, p * width, dmask, hist + p * kRadix, status, counters + p);
+    onesweep_kernel<kSortItems><<<(unsigned)tiles, kSortThreads, 0, s>>>(
+        keys, vals, keys_alt, vals_alt, n, p * width, dmask, hist + p * kRadix, status, counters + p);
     note_launch();
     std::swap(keys, keys_alt);
     std::swap(vals, vals_alt);

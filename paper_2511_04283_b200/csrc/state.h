@@ -65,12 +65,11 @@ struct EventScratch {
   DevBuf mask;       // u8 [H][W]
   DevBuf lohi;       // uint32 [2] min / max bits; uint64 argmin
   DevBuf flags;      // u8 [3][n] clone / split / prune
-  DevBuf cls;        // int32 [3][n] scan inputs
-  DevBuf pos;        // int32 [3][n] scan outputs
+  DevBuf cls;        // int3 [blocks] per-block class counts, then their exclusive scan (K15)
+  DevBuf totals;     // int64 [3] class totals (survivors, clones, splits)
   DevBuf keys_a, keys_b, vals_a, vals_b;  // VCP ordering
   DevBuf eps;        // float [n_split][6]
   DevBuf old_to_new; // int32 [n]
-  DevBuf route;      // int4 [n] destination slots (keep, clone, split) of K15
   // phase timing of density events (sk_ctx_get_event_timing): marks at the
   // start of the score pass, after the K views, after K13, K14 and K15
   cudaEvent_t tev[SK_NUM_EVENT_PHASES + 1] = {};
