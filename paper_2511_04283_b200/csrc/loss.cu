@@ -44,11 +44,15 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return s;
 }
 
-// Kernel A (per 32x16 output tile, 256 threads, channels in turn): stage x and
-// y with a 5-pixel zero halo; horizontal pass with a register sliding window
-// (4 adjacent outputs per thread, 14 loads instead of 44) producing the five
-// moments x, y, x^2, y^2, xy; vertical pass, 2 outputs per thread; SSIM map
-// and the three per-pixel partials of ssim_with_grad (metrics.hpp:104-114).
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// Kernel A (per 32x32 output tile, 256 threads, channels in turn): stage x and
+// y interleaved as float2 with a 5-pixel zero halo; horizontal pass with a
+// register sliding window (4 adjacent outputs per thread) producing the five
+// moments as two packed pairs (mu_x, mu_y), (E[x^2], E[y^2]) and E[xy] — one
+// FFMA2 per pair per tap instead of two FFMAs; vertical pass the same way, 4
+// outputs per thread; SSIM map and the three per-pixel partials of
+// ssim_with_grad (metrics.hpp:104-114).
 // partials: planar [3 maps][3 ch][H][W]; also writes the L1 part of
 // dL/dimage into dimage (planar [3][H][W]).
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ img, const void* __restrict__ gt,
@@ -57,9 +61,9 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
                                                        float* __restrict__ dimage, double* __restrict__ sums,
                                                        double* __restrict__ block_sums,
                                                        unsigned int* __restrict__ ticket) {
-  __shared__ float s_x[kInY][kInX + 1];
-  __shared__ float s_y[kInY][kInX + 1];
-  __shared__ float s_h[5][kInY][kTX + 1];
+  __shared__ float2 s_xy[kInY][kInX + 1];
+  __shared__ float2 s_h2[2][kInY][kTX + 1];  // (mu_x, mu_y), (E x^2, E y^2) after the horizontal pass
+  __shared__ float s_h1[kInY][kTX + 1];      // E xy
   __shared__ float s_u8[256];
   __shared__ double s_red[8];
   const int tx0 = blockIdx.x * kTX, ty0 = blockIdx.y * kTY;
@@ -67,7 +71,7 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   const size_t plane = (size_t)W * H;
   // byte / 255.0f (png_io.cpp:64) as a table: one exact division per value
   for (int i = t; i < 256; i += blockDim.x) s_u8[i] = __fdiv_rn((float)i, 255.0f);
-  // vertical-pass ownership: column vx, rows vy0, vy0 + 1
+  // vertical-pass ownership: column vx, rows vy0 .. vy0 + kVY - 1
   const int vx = t % kTX, vy0 = (t / kTX) * kVY;
   double l1 = 0.0, ss = 0.0, sq = 0.0;
   for (int ch = 0; ch < 3; ++ch) {
@@ -82,81 +86,81 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
         xv = img[ch * plane + p];
         yv = gt_u8 ? s_u8[static_cast<const uint8_t*>(gt)[p * 3 + ch]] : static_cast<const float*>(gt)[p * 3 + ch];
       }
-      s_x[iy][ix] = xv;
-      s_y[iy][ix] = yv;
+      s_xy[iy][ix] = make_float2(xv, yv);
     }
     __syncthreads();
-    // horizontal: 26 rows x 8 groups of 4 columns
+    // horizontal: kInY rows x 8 groups of 4 columns
     for (int hw = t; hw < kInY * (kTX / kHX); hw += blockDim.x) {
       const int iy = hw / (kTX / kHX), ox = (hw % (kTX / kHX)) * kHX;
-      float xv[kHX + 10], yv[kHX + 10];
+      float2 acc_m[kHX], acc_s[kHX];
+      float acc_p[kHX];
+#pragma unroll
+      for (int c = 0; c < kHX; ++c) acc_m[c] = acc_s[c] = f2(0.0f), acc_p[c] = 0.0f;
 #pragma unroll
       for (int k = 0; k < kHX + 10; ++k) {
-        xv[k] = s_x[iy][ox + k];
-        yv[k] = s_y[iy][ox + k];
-      }
-      float acc[5][kHX];
-#pragma unroll
-      for (int m = 0; m < 5; ++m)
-#pragma unroll
-        for (int c = 0; c < kHX; ++c) acc[m][c] = 0.0f;
-#pragma unroll
-      for (int k = 0; k < kHX + 10; ++k) {
-        const float xx = xv[k] * xv[k], yy = yv[k] * yv[k], xy = xv[k] * yv[k];
+        const float2 v = s_xy[iy][ox + k];
+        const float2 sq2 = __fmul2_rn(v, v);
+        const float pr = v.x * v.y;
 #pragma unroll
         for (int c = 0; c < kHX; ++c) {
           const int o = k - c;
           if (o >= 0 && o < 11) {
             const float w = c_gauss[o];
-            acc[0][c] += w * xv[k];
-            acc[1][c] += w * yv[k];
-            acc[2][c] += w * xx;
-            acc[3][c] += w * yy;
-            acc[4][c] += w * xy;
+            acc_m[c] = __ffma2_rn(f2(w), v, acc_m[c]);
+            acc_s[c] = __ffma2_rn(f2(w), sq2, acc_s[c]);
+            acc_p[c] = fmaf(w, pr, acc_p[c]);
           }
         }
       }
 #pragma unroll
-      for (int m = 0; m < 5; ++m)
-#pragma unroll
-        for (int c = 0; c < kHX; ++c) s_h[m][iy][ox + c] = acc[m][c];
+      for (int c = 0; c < kHX; ++c) {
+        s_h2[0][iy][ox + c] = acc_m[c];
+        s_h2[1][iy][ox + c] = acc_s[c];
+        s_h1[iy][ox + c] = acc_p[c];
+      }
     }
     __syncthreads();
-    float mom[5][kVY];
+    float2 mom_m[kVY], mom_s[kVY];
+    float mom_p[kVY];
 #pragma unroll
-    for (int m = 0; m < 5; ++m) {
-      float col[kVY + 10];
+    for (int r = 0; r < kVY; ++r) mom_m[r] = mom_s[r] = f2(0.0f), mom_p[r] = 0.0f;
 #pragma unroll
-      for (int k = 0; k < kVY + 10; ++k) col[k] = s_h[m][vy0 + k][vx];
+    for (int k = 0; k < kVY + 10; ++k) {
+      const float2 a = s_h2[0][vy0 + k][vx], b = s_h2[1][vy0 + k][vx];
+      const float c = s_h1[vy0 + k][vx];
 #pragma unroll
       for (int r = 0; r < kVY; ++r) {
-        float a = 0.0f;
-#pragma unroll
-        for (int o = 0; o < 11; ++o) a += c_gauss[o] * col[r + o];
-        mom[m][r] = a;
+        const int o = k - r;
+        if (o >= 0 && o < 11) {
+          const float w = c_gauss[o];
+          mom_m[r] = __ffma2_rn(f2(w), a, mom_m[r]);
+          mom_s[r] = __ffma2_rn(f2(w), b, mom_s[r]);
+          mom_p[r] = fmaf(w, c, mom_p[r]);
+        }
       }
     }
 #pragma unroll
     for (int r = 0; r < kVY; ++r) {
       const int px = tx0 + vx, py = ty0 + vy0 + r;
       if (px >= W || py >= H) continue;
-      const float mx = mom[0][r], my = mom[1][r];
+      const float mx = mom_m[r].x, my = mom_m[r].y;
       const float C1 = (float)(0.01 * 0.01), C2 = (float)(0.03 * 0.03);
       const float a1 = 2.0f * mx * my + C1;
-      const float a2 = 2.0f * (mom[4][r] - mx * my) + C2;
+      const float a2 = 2.0f * (mom_p[r] - mx * my) + C2;
       const float b1 = mx * mx + my * my + C1;
-      const float b2 = (mom[2][r] - mx * mx) + (mom[3][r] - my * my) + C2;
+      const float b2 = (mom_s[r].x - mx * mx) + (mom_s[r].y - my * my) + C2;
       // fast reciprocals (2 ulp): the loss is checked against the oracle
       // within a tolerance; the IEEE divisions cost ~4x the instructions
       const float inv_bb = __fdividef(1.0f, b1 * b2);
-      const float s = (a1 * a2) * inv_bb;
-      ss += (double)s;
+      const float sv = (a1 * a2) * inv_bb;
+      ss += (double)sv;
       const size_t p = (size_t)py * W + px;
-      const float diff = s_x[vy0 + r + kHalo][vx + kHalo] - s_y[vy0 + r + kHalo][vx + kHalo];
+      const float2 xy = s_xy[vy0 + r + kHalo][vx + kHalo];
+      const float diff = xy.x - xy.y;
       l1 += (double)fabsf(diff);
       sq += (double)diff * (double)diff;
       if (want_grad) {
-        const float s_b1 = s * __fdividef(1.0f, b1), s_b2 = s * __fdividef(1.0f, b2);
+        const float s_b1 = sv * __fdividef(1.0f, b1), s_b2 = sv * __fdividef(1.0f, b2);
         partials[(0 * 3 + ch) * plane + p] =
             nrm * (a2 * inv_bb * 2.0f * my - a1 * inv_bb * 2.0f * my - s_b1 * 2.0f * mx + s_b2 * 2.0f * mx);
         partials[(1 * 3 + ch) * plane + p] = nrm * (a1 * inv_bb * 2.0f);
@@ -198,14 +202,17 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   }
 }
 
-// Kernel B: filter the three partials (same tiling) and finish dL/dimage:
+// Kernel B: filter the three partials (same tiling; u_mu and u_mxy as one
+// packed pair, u_mxx alone) and finish dL/dimage:
 // d -= lambda (filt(u_mu) + filt(u_mxy) y + filt(u_mxx) 2 x).
 __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ img, const void* __restrict__ gt,
                                                        bool gt_u8, int W, int H, float lambda,
                                                        const float* __restrict__ partials,
                                                        float* __restrict__ dimage) {
-  __shared__ float s_u[3][kInY][kInX + 1];
-  __shared__ float s_h[3][kInY][kTX + 1];
+  __shared__ float2 s_u2[kInY][kInX + 1];
+  __shared__ float s_u1[kInY][kInX + 1];
+  __shared__ float2 s_h2[kInY][kTX + 1];
+  __shared__ float s_h1[kInY][kTX + 1];
   __shared__ float s_u8[256];
   const int tx0 = blockIdx.x * kTX, ty0 = blockIdx.y * kTY;
   const int t = threadIdx.x;
@@ -220,39 +227,52 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
       const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
       const bool ok = gx >= 0 && gx < W && gy >= 0 && gy < H;
       const size_t p = (size_t)gy * W + gx;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) s_u[k][iy][ix] = ok ? partials[(k * 3 + ch) * plane + p] : 0.0f;
+      s_u2[iy][ix] = ok ? make_float2(partials[(0 * 3 + ch) * plane + p], partials[(1 * 3 + ch) * plane + p])
+                        : f2(0.0f);
+      s_u1[iy][ix] = ok ? partials[(2 * 3 + ch) * plane + p] : 0.0f;
     }
     __syncthreads();
     for (int hw = t; hw < kInY * (kTX / kHX); hw += blockDim.x) {
       const int iy = hw / (kTX / kHX), ox = (hw % (kTX / kHX)) * kHX;
+      float2 a2[kHX];
+      float a1[kHX];
 #pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        float v[kHX + 10];
+      for (int c = 0; c < kHX; ++c) a2[c] = f2(0.0f), a1[c] = 0.0f;
 #pragma unroll
-        for (int k = 0; k < kHX + 10; ++k) v[k] = s_u[m][iy][ox + k];
+      for (int k = 0; k < kHX + 10; ++k) {
+        const float2 u = s_u2[iy][ox + k];
+        const float u1 = s_u1[iy][ox + k];
 #pragma unroll
         for (int c = 0; c < kHX; ++c) {
-          float a = 0.0f;
-#pragma unroll
-          for (int o = 0; o < 11; ++o) a += c_gauss[o] * v[c + o];
-          s_h[m][iy][ox + c] = a;
+          const int o = k - c;
+          if (o >= 0 && o < 11) {
+            a2[c] = __ffma2_rn(f2(c_gauss[o]), u, a2[c]);
+            a1[c] = fmaf(c_gauss[o], u1, a1[c]);
+          }
         }
+      }
+#pragma unroll
+      for (int c = 0; c < kHX; ++c) {
+        s_h2[iy][ox + c] = a2[c];
+        s_h1[iy][ox + c] = a1[c];
       }
     }
     __syncthreads();
-    float f[3][kVY];
+    float2 f2v[kVY];
+    float f1v[kVY];
 #pragma unroll
-    for (int m = 0; m < 3; ++m) {
-      float col[kVY + 10];
+    for (int r = 0; r < kVY; ++r) f2v[r] = f2(0.0f), f1v[r] = 0.0f;
 #pragma unroll
-      for (int k = 0; k < kVY + 10; ++k) col[k] = s_h[m][vy0 + k][vx];
+    for (int k = 0; k < kVY + 10; ++k) {
+      const float2 a = s_h2[vy0 + k][vx];
+      const float c = s_h1[vy0 + k][vx];
 #pragma unroll
       for (int r = 0; r < kVY; ++r) {
-        float a = 0.0f;
-#pragma unroll
-        for (int o = 0; o < 11; ++o) a += c_gauss[o] * col[r + o];
-        f[m][r] = a;
+        const int o = k - r;
+        if (o >= 0 && o < 11) {
+          f2v[r] = __ffma2_rn(f2(c_gauss[o]), a, f2v[r]);
+          f1v[r] = fmaf(c_gauss[o], c, f1v[r]);
+        }
       }
     }
 #pragma unroll
@@ -262,7 +282,7 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
       const size_t p = (size_t)py * W + px;
       const float xv = img[ch * plane + p];
       const float yv = gt_u8 ? s_u8[static_cast<const uint8_t*>(gt)[p * 3 + ch]] : static_cast<const float*>(gt)[p * 3 + ch];
-      const float g = f[0][r] + f[1][r] * yv + f[2][r] * 2.0f * xv;
+      const float g = f2v[r].x + f2v[r].y * yv + f1v[r] * 2.0f * xv;
       dimage[ch * plane + p] = dimage[ch * plane + p] - lambda * g;
     }
   }

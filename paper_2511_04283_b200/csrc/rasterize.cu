@@ -130,7 +130,14 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) count_bl
 // batch boundaries nor keep staging after their own pixels have terminated;
 // the price is that each warp gathers every entry (L1 serves the repeats).
 // Per-pixel arithmetic is identical to blend_fwd_kernel (bit-exact).
-template <int TS, int PIX>
+//
+// FAST (training steps, sk_train_step*/Trainer): alpha = o 2^{q (-log2 e / 2)}
+// on MUFU.EX2 instead of the deterministic exp — the image is then within
+// the north star's 1e-4 of the oracle's (not bit-equal), and K8 recomputes
+// exactly the same alphas (same ops on the same bit-equal q), so the
+// forward / backward pair stays self-consistent. Every parity-facing path
+// (sk_render_forward, the density-event renders, K12) runs the exact form.
+template <int TS, int PIX, bool FAST>
 __global__ void __launch_bounds__(TS* TS / PIX, kFwdMinBlocks * 128 / (TS * TS / PIX)) blend_fwd_warp_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
@@ -142,9 +149,11 @@ __global__ void __launch_bounds__(TS* TS / PIX, kFwdMinBlocks * 128 / (TS * TS /
   __shared__ float4 s_gco[2][kWarps][32];
   __shared__ float2 s_gmu[2][kWarps][32];
   __shared__ float4 s_grgb[2][kWarps][32];
-  __shared__ float s_exp[kNegExpTable];
-  stage_neg_exp_table(s_exp);
-  __syncthreads();
+  __shared__ float s_exp[FAST ? 1 : kNegExpTable];
+  if (!FAST) {
+    stage_neg_exp_table(s_exp);
+    __syncthreads();
+  }
   const SmemPinnedTable tab(s_exp);
 
   const int tile = blockIdx.x;
@@ -228,7 +237,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, kFwdMinBlocks * 128 / (TS * TS /
         const float dy = fpy[k] - mq.y;
         const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;
         if (__float_as_uint(__fadd_rn(q, 0.0f)) > __float_as_uint(mq.z)) continue;  // -0 -> +0
-        float alpha = co.w * det_expf_neg(-0.5f * q, tab);
+        float alpha = FAST ? co.w * exp2f_approx(q * -0.72134752044448170f) : co.w * det_expf_neg(-0.5f * q, tab);
         alpha = (alpha < kAlphaCap) ? alpha : kAlphaCap;
         if (alpha < kAlphaMin) continue;
         lane_bits |= 1u << j;
@@ -301,7 +310,7 @@ __global__ void pge_counts_kernel(const int2* __restrict__ ranges, const float* 
 }
 
 template <int TS, int PIX>
-void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts) {
+void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts, bool fast) {
   const int tiles = f->tiles_x * f->tiles_y;
   auto* ranges = f->ranges.as<int2>();
   const auto* mean2d = f->mean2d.as<float2>();
@@ -318,9 +327,16 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
       SK_CUDA(cudaMemsetAsync(cm, 0, words * sizeof(uint32_t), ctx->stream));
     }
     f->cmask_valid = cm != nullptr;
-    blend_fwd_warp_kernel<TS, PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
-        ranges, f->pair_val, mean2d, co, rgb, f->width, f->height, f->tiles_x, f->image.as<float>(),
-        f->final_t.as<float>(), f->n_contrib.as<int>(), f->last_entry.as<int>(), cm);
+    f->fast_blend = fast;
+    auto go = [&](auto kern) {
+      kern<<<tiles, TS * TS / PIX, 0, ctx->stream>>>(ranges, f->pair_val, mean2d, co, rgb, f->width, f->height,
+                                                     f->tiles_x, f->image.as<float>(), f->final_t.as<float>(),
+                                                     f->n_contrib.as<int>(), f->last_entry.as<int>(), cm);
+    };
+    if (fast)
+      go(blend_fwd_warp_kernel<TS, PIX, true>);
+    else
+      go(blend_fwd_warp_kernel<TS, PIX, false>);
   }
   note_launch();
 }
@@ -342,12 +358,12 @@ void frame_pge_counts(sk_ctx* ctx, sk_frame* f, int64_t* visited, int64_t* contr
   *contributing = (int64_t)h[1];
 }
 
-void launch_blend_forward(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts) {
+void launch_blend_forward(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts, bool fast) {
   if (f->tiles_x * f->tiles_y == 0) return;
   switch (f->tile_size) {
-    case 8: fwd_dispatch<8, 1>(ctx, f, mask, counts); break;
-    case 16: fwd_dispatch<16, 2>(ctx, f, mask, counts); break;
-    case 32: fwd_dispatch<32, 4>(ctx, f, mask, counts); break;
+    case 8: fwd_dispatch<8, 1>(ctx, f, mask, counts, fast && !mask); break;
+    case 16: fwd_dispatch<16, 2>(ctx, f, mask, counts, fast && !mask); break;
+    case 32: fwd_dispatch<32, 4>(ctx, f, mask, counts, fast && !mask); break;
     default: throw std::invalid_argument("tile_size must be 8, 16 or 32");
   }
   SK_CUDA(cudaGetLastError());

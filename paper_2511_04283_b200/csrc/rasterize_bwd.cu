@@ -88,7 +88,7 @@ struct PairState {
   int last0, last1;
 };
 
-template <typename Tab>
+template <bool FAST, typename Tab>
 __device__ __forceinline__ bool pair_partials(const float4 mq, const float4 co, const float4 c, float fpx, int idx,
                                               PairState& st, const Tab& tab, float (&g)[kBGradFields]) {
   const float dx = fpx - mq.x;
@@ -111,11 +111,12 @@ __device__ __forceinline__ bool pair_partials(const float4 mq, const float4 co, 
   // one symmetric band |(|raw - mid| - half)| <= 1e-5 * cap around both thresholds
   constexpr float kMid = (float)((1.0 / 255 + 0.99) / 2), kHalf = (float)((0.99 - 1.0 / 255) / 2);
   constexpr float kBand = 1e-5f * (float)kAlphaCap;
-  if (ok0 && fabsf(fabsf(raw.x - kMid) - kHalf) <= kBand) {
+  // FAST (the frame's K6 ran the MUFU form): these are K6's alphas bit for bit
+  if (!FAST && ok0 && fabsf(fabsf(raw.x - kMid) - kHalf) <= kBand) {
     ge.x = det_expf_core(rn_mul(-0.5f, q.x), tab);
     raw.x = rn_mul(co.w, ge.x);
   }
-  if (ok1 && fabsf(fabsf(raw.y - kMid) - kHalf) <= kBand) {
+  if (!FAST && ok1 && fabsf(fabsf(raw.y - kMid) - kHalf) <= kBand) {
     ge.y = det_expf_core(rn_mul(-0.5f, q.y), tab);
     raw.y = rn_mul(co.w, ge.y);
   }
@@ -160,7 +161,7 @@ __device__ __forceinline__ bool pair_partials(const float4 mq, const float4 co, 
 }
 
 // Scalar form of the same step for one-pixel lanes (8x8 tiles).
-template <typename Tab>
+template <bool FAST, typename Tab>
 __device__ __forceinline__ bool one_partials(const float4 mq, const float4 co, const float4 c, float fpx, float fpy,
                                              int idx, int last, float& T, float& ns, float d0, float d1, float d2,
                                              const Tab& tab, float (&g)[kBGradFields]) {
@@ -171,7 +172,7 @@ __device__ __forceinline__ bool one_partials(const float4 mq, const float4 co, c
   float ge = exp2f_approx(q * -0.72134752044448170f);
   float raw = co.w * ge;
   constexpr float kMid = (float)((1.0 / 255 + 0.99) / 2), kHalf = (float)((0.99 - 1.0 / 255) / 2);
-  if (ok && fabsf(fabsf(raw - kMid) - kHalf) <= 1e-5f * (float)kAlphaCap) {
+  if (!FAST && ok && fabsf(fabsf(raw - kMid) - kHalf) <= 1e-5f * (float)kAlphaCap) {
     ge = det_expf_core(rn_mul(-0.5f, q), tab);
     raw = rn_mul(co.w, ge);
   }
@@ -203,7 +204,7 @@ __device__ __forceinline__ bool one_partials(const float4 mq, const float4 co, c
   return ok;
 }
 
-template <int TS, int PIX>
+template <int TS, int PIX, bool FAST>
 __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS / PIX)) blend_bwd_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
@@ -306,9 +307,9 @@ __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS /
     for (int f = 0; f < kBGradFields; ++f) gv[f] = 0.0f;
     if (PIX >= 2) {
 #pragma unroll
-      for (int k = 0; k < NP; ++k) contrib = pair_partials(mq, co, c, fpx, idx, ps[k], tab, gv) || contrib;
+      for (int k = 0; k < NP; ++k) contrib = pair_partials<FAST>(mq, co, c, fpx, idx, ps[k], tab, gv) || contrib;
     } else {
-      contrib = one_partials(mq, co, c, fpx, fpy[0], idx, last[0], T1, ns1, d0[0], d1[0], d2[0], tab, gv);
+      contrib = one_partials<FAST>(mq, co, c, fpx, fpy[0], idx, last[0], T1, ns1, d0[0], d1[0], d2[0], tab, gv);
     }
     // the conic fields were accumulated as -2 d_q [dx^2, dx dy, dy^2]
     gv[2] *= -0.5f;
@@ -406,7 +407,8 @@ __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS /
 template <int TS, int PIX>
 void bwd_dispatch(sk_ctx* ctx, sk_frame* f) {
   const int tiles = f->tiles_x * f->tiles_y;
-  blend_bwd_kernel<TS, PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
+  auto kern = f->fast_blend ? blend_bwd_kernel<TS, PIX, true> : blend_bwd_kernel<TS, PIX, false>;
+  kern<<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
       f->ranges.as<int2>(), f->pair_val, f->mean2d.as<float2>(), f->conic_op.as<float4>(), f->rgb_depth.as<float4>(),
       f->width, f->height, f->tiles_x, f->final_t.as<float>(), f->last_entry.as<int>(), f->dimage.as<float>(),
       f->bgrads.as<float>(), f->n, (TS == 16 && f->cmask_valid) ? f->cmask.as<uint32_t>() : nullptr);

@@ -177,6 +177,7 @@ struct sk_frame {
   sk::DevBuf last_entry;  // int32 [H][W], absolute pair index + 1 of the last contributor
   sk::DevBuf cmask;       // uint32 per (batch of 32 entries, K6 warp): entries a pixel of the warp blended
   bool cmask_valid = false;
+  bool fast_blend = false;  // K6 ran the MUFU-exp (training) form; K8 must match it
 
   // K7 / K8
   sk::DevBuf dimage;  // planar [3][H][W]
@@ -228,7 +229,9 @@ int64_t read_scan_total(sk_ctx* ctx, const long long* total);
 void launch_tile_ranges(sk_ctx* ctx, const uint32_t* pair_tile, int64_t pairs, int2* ranges, int tiles);
 
 // rasterize.cu
-void launch_blend_forward(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts);
+// fast: the MUFU-exp blend of training steps (rasterize.cu); K8 follows the
+// mode the frame was rendered with (sk_frame::fast_blend).
+void launch_blend_forward(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts, bool fast = false);
 void launch_blend_backward(sk_ctx* ctx, sk_frame* f);
 // Reference-loop workload of the last forward render (synchronises).
 void frame_pge_counts(sk_ctx* ctx, sk_frame* f, int64_t* visited, int64_t* contributing);

@@ -135,7 +135,7 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   ctx->mark(1);
   bin_sort(ctx, f);
   ctx->mark(2);
-  launch_blend_forward(ctx, f, nullptr, nullptr);
+  launch_blend_forward(ctx, f, nullptr, nullptr, /*fast=*/true);
   f->rendered = true;
   ctx->mark(3);
   launch_loss(ctx, f, gt_dev, true, (float)cfg.lambda, true, nullptr);

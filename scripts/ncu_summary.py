@@ -32,15 +32,19 @@ def launches(path: str) -> str:
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     h = rows[0]
     ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
-    seq = sorted((int(r[ii]), short(r[ki]), float(r[vi]) / 1000.0) for r in rows[1:]
-                 if r[mi] == "gpu__time_duration.sum")
+    per = {}
+    for r in rows[1:]:
+        per.setdefault(int(r[ii]), {"k": short(r[ki])})[r[mi]] = float(r[vi].replace(",", ""))
+    seq = sorted((i, d["k"], d.get("gpu__time_duration.sum", 0.0) / 1000.0, d.get("dram__bytes_read.sum"),
+                  d.get("dram__bytes_write.sum")) for i, d in per.items())
     starts = [i for i, s in enumerate(seq) if s[1].startswith("preprocess")]
     step = seq[starts[-1]:]
-    total = sum(t for _, _, t in step)
-    out = ["| # | kernel | us | share |", "|---|---|---|---|"]
-    for j, (_, k, t) in enumerate(step):
-        out.append(f"| {j} | `{k}` | {t:.1f} | {100 * t / total:.1f}% |")
-    out.append(f"| | **sum of kernels** | **{total:.1f}** | |")
+    total = sum(t for _, _, t, _, _ in step)
+    out = ["| # | kernel | us | share | DRAM rd MB | DRAM wr MB |", "|---|---|---|---|---|---|"]
+    for j, (_, k, t, rd, wr) in enumerate(step):
+        f = lambda b: "" if b is None else f"{b / 1e6:.1f}" if b > 1e4 else f"{b:.1f}"
+        out.append(f"| {j} | `{k}` | {t:.1f} | {100 * t / total:.1f}% | {f(rd)} | {f(wr)} |")
+    out.append(f"| | **sum of kernels** | **{total:.1f}** | | | |")
     return "\n".join(out) + "\n"
 
 

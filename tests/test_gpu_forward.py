@@ -171,3 +171,32 @@ def test_large_scene_1080p_bit_exact(ctx, orc):
     _check_tile_lists(ctx.tile_lists(), ref)
     assert np.array_equal(got.image, ref.image)
     assert np.array_equal(got.contrib, ref.contrib)
+
+
+def test_training_blend_within_north_star_of_exact(ctx, orc):
+    """Training steps render with the MUFU-exp form of K6 (FAST, rasterize.cu);
+    its image must stay within the north star's 1e-4 per channel of the exact
+    (oracle bit-equal) render of the same scene, with the pixels whose
+    contributor count flips at a threshold reported."""
+    import json
+    import paper_2511_04283_b200 as sk
+    import paper_2511_04283_b200.synthetic as syn
+    n = 200_000
+    p = synthetic_scene(n, deg=3, seed=1)
+    cam = ring_camera(orc, 1920, 1080, 0.0, focal=1.1 * 1080 * 2.6)
+    scene = ctx.scene(p, 3)
+    ctx.preprocess(scene, cam)
+    ctx.build_tile_grid()
+    exact = ctx.blend_forward()
+    ref = orc.render_scene(p, 3, cam, orc.binning(), workers=8, values_cap=40 * n)
+    assert np.array_equal(exact.image, ref.image)
+    gt8 = syn.quantize_u8(exact.image)
+    cfg = sk.default_config()
+    sk.train_step_host(ctx, scene, cam, gt8, cfg, 2.64, 1)  # renders the pre-update scene with the FAST blend
+    fast = ctx.get_render()
+    diff = np.abs(fast.image - exact.image)
+    flips = int((fast.contrib != exact.contrib).sum())
+    print("training blend vs exact:", json.dumps({"max_abs": float(diff.max()), "mean_abs": float(diff.mean()),
+                                                  "contrib_flips": flips, "pixels": int(diff.shape[0] * diff.shape[1])}))
+    assert diff.max() <= 1e-4, diff.max()
+    assert flips <= 1e-4 * diff.shape[0] * diff.shape[1], flips
