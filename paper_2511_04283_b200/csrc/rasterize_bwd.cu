@@ -72,6 +72,12 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 constexpr int kBwdMinBlocks = 7;
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+// 1 / x on MUFU.RCP alone (x = 1 - alpha lies in [0.01, 1]: no range fix-ups)
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 // The 11 gradient partials of one staged entry over a lane's pixel pair
 // (rows y and y + 4 of its column), with the pair's arithmetic in packed
@@ -128,7 +134,7 @@ __device__ __forceinline__ bool pair_partials(const float4 mq, const float4 co, 
   const float2 alpha = make_float2(ok0 ? ac0 : 0.0f, ok1 ? ac1 : 0.0f);
   // capped entries feed d_color only (raster.hpp:315, 333)
   const bool geo0 = ok0 && !cap0, geo1 = ok1 && !cap1;
-  const float2 inv = make_float2(__fdividef(1.0f, 1.0f - alpha.x), __fdividef(1.0f, 1.0f - alpha.y));
+  const float2 inv = make_float2(rcp_approx(1.0f - alpha.x), rcp_approx(1.0f - alpha.y));
   const float2 tb = __fmul2_rn(st.T, inv);  // T before the entry
   st.T = tb;
   const float2 w = __ffma2_rn(f2(c.z), st.d2, __ffma2_rn(f2(c.y), st.d1, __fmul2_rn(f2(c.x), st.d0)));
@@ -181,7 +187,7 @@ __device__ __forceinline__ bool one_partials(const float4 mq, const float4 co, c
   ok = ok && !(ac < kAlphaMin);
   const float alpha = ok ? ac : 0.0f;
   const bool geo = ok && !capped;
-  const float inv = __fdividef(1.0f, 1.0f - alpha);
+  const float inv = rcp_approx(1.0f - alpha);
   const float tb = T * inv;
   T = tb;
   const float w = fmaf(c.z, d2, fmaf(c.y, d1, c.x * d0));
