@@ -347,6 +347,14 @@ __global__ void __launch_bounds__(kPbThreads, kK9MinBlocks) project_bwd_kernel(
 #pragma unroll
   for (int c = 0; c < NC; ++c)
     asm volatile("prefetch.global.L1 [%0];" ::"l"(params + c * stride + i));
+  if (do_stats) {  // the statistics read-modify-write at the end
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(st.grad_norm_acc + i));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(st.abs_grad_acc + i));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(st.views_seen + i));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(st.max_radius2d + i));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(st.grad3d_acc + k * stride + i));
+  }
   const float rad = radius[i];
   if (rad > 0.0f) {
     float dmu2d[2], dcov[2][2], dcol[3], dop, absg[2];
