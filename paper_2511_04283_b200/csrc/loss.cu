@@ -21,7 +21,7 @@ namespace {
 // 32x32 output tiles (measured 11% faster than 32x16: the 10-row halo of the
 // horizontal pass is amortised over twice the rows)
 
-constexpr int kStageUnroll = 1;   // halo-staging loop not unrolled (measured -5% K7; 4 or 7: slower)
+
 constexpr int kTX = 32;                 // output tile width
 constexpr int kTY = 32;                 // output tile height
 constexpr int kHalo = 5;                // 11-tap window
@@ -46,7 +46,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
-// Kernel A (per 32x32 output tile, 256 threads, channels in turn): stage x and
+// Kernel A (per 32x32 output tile and channel, 256 threads): stage x and
 // y interleaved as float2 with a 5-pixel zero halo; horizontal pass with a
 // register sliding window (4 adjacent outputs per thread) producing the five
 // moments as two packed pairs (mu_x, mu_y), (E[x^2], E[y^2]) and E[xy] — one
@@ -74,9 +74,9 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   // vertical-pass ownership: column vx, rows vy0 .. vy0 + kVY - 1
   const int vx = t % kTX, vy0 = (t / kTX) * kVY;
   double l1 = 0.0, ss = 0.0, sq = 0.0;
-  for (int ch = 0; ch < 3; ++ch) {
+  {
+    const int ch = blockIdx.z;  // one channel per CTA: three times the CTAs in flight
     __syncthreads();
-#pragma unroll kStageUnroll
     for (int i = t; i < kInX * kInY; i += blockDim.x) {
       const int iy = i / kInX, ix = i % kInX;
       const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
@@ -176,8 +176,8 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   // Deterministic total: block sums are stored per block and the last block
   // to finish adds them in block order (no order-dependent atomics, so the
   // loss / SSIM / PSNR are bit-reproducible run to run).
-  const unsigned nb = gridDim.x * gridDim.y;
-  const unsigned b = blockIdx.y * gridDim.x + blockIdx.x;
+  const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+  const unsigned b = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   __shared__ bool s_last;
   if (t == 0) {
     block_sums[3 * b + 0] = t_l1;
@@ -219,9 +219,9 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
   const size_t plane = (size_t)W * H;
   for (int i = t; i < 256; i += blockDim.x) s_u8[i] = __fdiv_rn((float)i, 255.0f);
   const int vx = t % kTX, vy0 = (t / kTX) * kVY;
-  for (int ch = 0; ch < 3; ++ch) {
+  {
+    const int ch = blockIdx.z;  // one channel per CTA
     __syncthreads();
-#pragma unroll kStageUnroll
     for (int i = t; i < kInX * kInY; i += blockDim.x) {
       const int iy = i / kInX, ix = i % kInX;
       const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
@@ -319,8 +319,8 @@ void launch_loss(sk_ctx* ctx, sk_frame* f, const void* gt, bool gt_u8, float lam
   double* sums = ensure<double>(ctx->scalars, 5);
   unsigned int* ticket = reinterpret_cast<unsigned int*>(sums + 4);
   SK_CUDA(cudaMemsetAsync(sums, 0, 5 * sizeof(double), ctx->stream));
-  const dim3 grid((W + kTX - 1) / kTX, (H + kTY - 1) / kTY);
-  double* block_sums = ensure<double>(ctx->loss_blocks, 3 * (size_t)grid.x * grid.y);
+  const dim3 grid((W + kTX - 1) / kTX, (H + kTY - 1) / kTY, 3);
+  double* block_sums = ensure<double>(ctx->loss_blocks, 3 * (size_t)grid.x * grid.y * grid.z);
   const float nrm = 1.0f / (3.0f * (float)W * (float)H);
   const float inv_n = 1.0f / (3.0f * (float)plane);
   ssim_fwd_kernel<<<grid, 256, 0, ctx->stream>>>(f->image.as<float>(), gt, gt_u8, W, H, nrm, lambda, inv_n, want_grad,
