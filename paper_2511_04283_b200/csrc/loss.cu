@@ -29,6 +29,10 @@ constexpr int kInX = kTX + 2 * kHalo;   // 42
 constexpr int kInY = kTY + 2 * kHalo;   // 26
 constexpr int kHX = 4;                  // horizontal outputs per thread (register sliding window)
 constexpr int kVY = kTX * kTY / 256;    // vertical outputs per thread (256 threads)
+// Vectorised halo staging: the 4-aligned window [x0 - 8, x0 + 40) covers the
+// halo [x0 - 5, x0 + 37) in 12 quads per row.
+constexpr int kQuadLead = 8;
+constexpr int kQuads = (kTX + 2 * kQuadLead) / 4;
 
 __constant__ float c_gauss[11];
 
@@ -77,16 +81,45 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   {
     const int ch = blockIdx.z;  // one channel per CTA: three times the CTAs in flight
     __syncthreads();
-    for (int i = t; i < kInX * kInY; i += blockDim.x) {
-      const int iy = i / kInX, ix = i % kInX;
-      const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
-      float xv = 0.0f, yv = 0.0f;
-      if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
-        const size_t p = (size_t)gy * W + gx;
-        xv = img[ch * plane + p];
-        yv = gt_u8 ? s_u8[static_cast<const uint8_t*>(gt)[p * 3 + ch]] : static_cast<const float*>(gt)[p * 3 + ch];
+    if ((W & 3) == 0 && gt_u8) {
+      // Rows of four pixels at a time: with W % 4 == 0 every 4-aligned quad
+      // lies entirely inside or outside the image (zero padding), the image
+      // quad is one float4 and the GT quad's 12 bytes three aligned words.
+      for (int i = t; i < kInY * kQuads; i += blockDim.x) {
+        const int iy = i / kQuads, q = i % kQuads;
+        const int gy = ty0 - kHalo + iy, gx0 = tx0 - kQuadLead + 4 * q;
+        float4 xv = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        float yv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        if (gy >= 0 && gy < H && gx0 >= 0 && gx0 < W) {
+          const size_t p = (size_t)gy * W + gx0;
+          xv = *reinterpret_cast<const float4*>(img + ch * plane + p);
+          const uint32_t* wq = reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(gt) + p * 3);
+          const uint32_t w3[3] = {wq[0], wq[1], wq[2]};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int b = 3 * j + ch;
+            yv[j] = s_u8[(w3[b >> 2] >> (8 * (b & 3))) & 0xffu];
+          }
+        }
+        const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ix = 4 * q + j - (kQuadLead - kHalo);
+          if (ix >= 0 && ix < kInX) s_xy[iy][ix] = make_float2(xs[j], yv[j]);
+        }
       }
-      s_xy[iy][ix] = make_float2(xv, yv);
+    } else {
+      for (int i = t; i < kInX * kInY; i += blockDim.x) {
+        const int iy = i / kInX, ix = i % kInX;
+        const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
+        float xv = 0.0f, yv = 0.0f;
+        if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+          const size_t p = (size_t)gy * W + gx;
+          xv = img[ch * plane + p];
+          yv = gt_u8 ? s_u8[static_cast<const uint8_t*>(gt)[p * 3 + ch]] : static_cast<const float*>(gt)[p * 3 + ch];
+        }
+        s_xy[iy][ix] = make_float2(xv, yv);
+      }
     }
     __syncthreads();
     // horizontal: kInY rows x 8 groups of 4 columns
@@ -222,14 +255,38 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
   {
     const int ch = blockIdx.z;  // one channel per CTA
     __syncthreads();
-    for (int i = t; i < kInX * kInY; i += blockDim.x) {
-      const int iy = i / kInX, ix = i % kInX;
-      const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
-      const bool ok = gx >= 0 && gx < W && gy >= 0 && gy < H;
-      const size_t p = (size_t)gy * W + gx;
-      s_u2[iy][ix] = ok ? make_float2(partials[(0 * 3 + ch) * plane + p], partials[(1 * 3 + ch) * plane + p])
-                        : f2(0.0f);
-      s_u1[iy][ix] = ok ? partials[(2 * 3 + ch) * plane + p] : 0.0f;
+    if ((W & 3) == 0) {
+      // float4 quads of the three partial planes (see ssim_fwd_kernel)
+      for (int i = t; i < kInY * kQuads; i += blockDim.x) {
+        const int iy = i / kQuads, q = i % kQuads;
+        const int gy = ty0 - kHalo + iy, gx0 = tx0 - kQuadLead + 4 * q;
+        float4 a = make_float4(0.0f, 0.0f, 0.0f, 0.0f), b = a, c = a;
+        if (gy >= 0 && gy < H && gx0 >= 0 && gx0 < W) {
+          const size_t p = (size_t)gy * W + gx0;
+          a = *reinterpret_cast<const float4*>(partials + (0 * 3 + ch) * plane + p);
+          b = *reinterpret_cast<const float4*>(partials + (1 * 3 + ch) * plane + p);
+          c = *reinterpret_cast<const float4*>(partials + (2 * 3 + ch) * plane + p);
+        }
+        const float as[4] = {a.x, a.y, a.z, a.w}, bs[4] = {b.x, b.y, b.z, b.w}, cs[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ix = 4 * q + j - (kQuadLead - kHalo);
+          if (ix >= 0 && ix < kInX) {
+            s_u2[iy][ix] = make_float2(as[j], bs[j]);
+            s_u1[iy][ix] = cs[j];
+          }
+        }
+      }
+    } else {
+      for (int i = t; i < kInX * kInY; i += blockDim.x) {
+        const int iy = i / kInX, ix = i % kInX;
+        const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
+        const bool ok = gx >= 0 && gx < W && gy >= 0 && gy < H;
+        const size_t p = (size_t)gy * W + gx;
+        s_u2[iy][ix] = ok ? make_float2(partials[(0 * 3 + ch) * plane + p], partials[(1 * 3 + ch) * plane + p])
+                          : f2(0.0f);
+        s_u1[iy][ix] = ok ? partials[(2 * 3 + ch) * plane + p] : 0.0f;
+      }
     }
     __syncthreads();
     for (int hw = t; hw < kInY * (kTX / kHX); hw += blockDim.x) {
