@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
 
 // ---- K2: single-pass exclusive scan with decoupled look-back ---------------
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
+constexpr int kScanItems = 4;  // 1024-entry tiles: ~4x the CTAs of 16 items, -4 us on 1M slots
 constexpr int kScanTile = kScanThreads * kScanItems;
 constexpr unsigned long long kSFlagAgg = 1ull << 62;
 constexpr unsigned long long kSFlagInc = 2ull << 62;
