@@ -42,7 +42,7 @@ DATA = ("synthetic (numpy RNG, reference generate_synthetic distribution; GT ren
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=1_000_000)
@@ -334,12 +334,16 @@ def run_ours(args, world, rank, local):
     with (clock if not args.profile else _Null()):
         barrier()
         torch.cuda.synchronize()
+        if args.profile:  # `ncu --profile-from-start off` then captures exactly the timed steps
+            torch.cuda.cudart().cudaProfilerStart()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         rows = trainer.run(args.steps)  # Trainer::run: each step's readback completes during the next
         e1.record(stream)
         torch.cuda.synchronize()
+        if args.profile:
+            torch.cuda.cudart().cudaProfilerStop()
         barrier()
     launches = ctx.launch_count() - launches0
     ctx.check(ctx._lib.sk_ctx_enable_timing(ctx.h, 0))
@@ -436,7 +440,7 @@ def run_ours(args, world, rank, local):
                      "flop_per_visited": fv, "flop_per_contributing": fc, "kernel_ms": phase_avg[ph],
                      "ex2_frac_of_mufu": (ex[0] * visited + ex[1] * contribs) / t / 1e12 / mufu_peak,
                      "hbm_GB/s": algorithmic_bytes(ph, args.n, visible, pairs, pixels, tiles) / t / 1e9}
-    phase_kernel = {4: "blend_bwd_kernel", 2: "blend_fwd_kernel", 5: "project_bwd_kernel", 6: "adam_kernel",
+    phase_kernel = {4: "blend_bwd_kernel", 2: "blend_fwd_warp_kernel", 5: "project_bwd_kernel", 6: "adam_kernel",
                     0: "preprocess_kernel"}
     dom = int(np.argmax(phase_avg))
     if dom in blend:

@@ -1,6 +1,6 @@
 # A/B of compile-time variants on one box: for each "name=flags" argument,
 # rebuild with SK_NVCC_EXTRA=flags and run a short bench; then restore the
-# default build. usage: bash scripts/gpu_ab.sh TAG "base=" "minb10=-DSK_BWD_MINB=10" ...
+# default build. usage: bash scripts/gpu_ab.sh TAG "base=" "fast=-DSOME_FLAG=1" ...
 TAG=$1; shift
 mkdir -p gpurun_out
 for spec in "$@"; do

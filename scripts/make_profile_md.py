@@ -1,95 +1,126 @@
-"""Writes profiles/r1_ncu.md, profiles/r1_launches.csv and profiles/traffic.json
-from one scripts/gpu_profile.sh capture (tag) plus its bench line.
+"""Writes profiles/<round>_ncu.md, profiles/<round>_launches.csv and
+profiles/traffic.json from one scripts/gpu_profile.sh capture (tag) plus its
+bench line (gpurun_out/bench_<tag>.json).
 
-    python scripts/make_profile_md.py <tag>
+    python scripts/make_profile_md.py <tag> [round]
 """
 import json
+import os
 import shutil
 import subprocess
 import sys
 
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import ncu_summary  # noqa: E402
+
 tag = sys.argv[1]
-g = f"gpurun_out"
+rnd = sys.argv[2] if len(sys.argv) > 2 else "r2"
+g = "gpurun_out"
+
+# kernel name prefix -> bench.py phase (PHASES in bench.py)
+PHASE_OF = [("preprocess", "K1 preprocess"), ("radix_", "K2-K5 bin+sort"), ("onesweep", "K2-K5 bin+sort"),
+            ("scan_gather", "K2-K5 bin+sort"), ("duplicate", "K2-K5 bin+sort"),
+            ("tile_ranges", "K2-K5 bin+sort"), ("blend_fwd", "K6 blend fwd"), ("ssim", "K7 loss"),
+            ("blend_bwd", "K8 blend bwd"), ("project_bwd", "K9 proj-bwd"), ("adam", "K10 Adam")]
+
+
+def phase(k):
+    for p, name in PHASE_OF:
+        if k.startswith(p):
+            return name
+    return "other"
 
 
 def run(*a):
     return subprocess.run(["python", *a], capture_output=True, text=True, check=True).stdout
 
 
-launches = run("scripts/ncu_summary.py", "launches", f"{g}/launches_{tag}.csv")
-full = run("scripts/ncu_summary.py", "full", f"{g}/full_{tag}.ncu-rep")
-fullb = run("scripts/ncu_summary.py", "full", f"{g}/fullb_{tag}.ncu-rep")
+avg, nsteps = ncu_summary.launch_avg(f"{g}/launches_{tag}.csv")
+launches = ncu_summary.launches(f"{g}/launches_{tag}.csv")
+full = ncu_summary.full(f"{g}/full_{tag}.ncu-rep")
 hb = run("scripts/ncu_lines.py", f"{g}/full_{tag}.ncu-rep", "blend_bwd", "20")
 hf = run("scripts/ncu_lines.py", f"{g}/full_{tag}.ncu-rep", "blend_fwd_warp", "20")
-shutil.copy(f"{g}/launches_{tag}.csv", "profiles/r1_launches.csv")
-a = json.loads(run("scripts/ncu_summary.py", "traffic", f"{g}/full_{tag}.ncu-rep"))
-b = json.loads(run("scripts/ncu_summary.py", "traffic", f"{g}/fullb_{tag}.ncu-rep"))
-k = dict(b["kernels"])
-k.update(a["kernels"])
-json.dump({"source": f"full_{tag}.ncu-rep + fullb_{tag}.ncu-rep (steady state, after 150 training iterations)",
-           "unit": "bytes per launch", "kernels": k}, open("profiles/traffic.json", "w"), indent=1)
+shutil.copy(f"{g}/launches_{tag}.csv", f"profiles/{rnd}_launches.csv")
+tr = json.loads(ncu_summary.traffic(f"{g}/full_{tag}.ncu-rep"))
+json.dump({"source": f"full_{tag}.ncu-rep: `bench.py --profile --steps 1 --warmup 5`, training iteration 1 "
+                     f"from the bench's restored start state", "unit": "bytes per launch",
+           "kernels": tr["kernels"]}, open("profiles/traffic.json", "w"), indent=1)
+
 d = json.load(open(f"{g}/bench_{tag}.json"))
 ph = d["phase_ms"]
+ncu_ph = {}
+for k, t, _, _ in avg:
+    ncu_ph[phase(k)] = ncu_ph.get(phase(k), 0.0) + t / 1000.0
+tot_b, tot_n = sum(ph.values()), sum(ncu_ph.values())
+share_rows = ["| phase | bench ms (CUDA events) | bench share | ncu ms (serialised, cold) | ncu share | Δ share |",
+              "|---|---|---|---|---|---|"]
+worst = 0.0
+for name, v in ph.items():
+    nv = ncu_ph.get(name, 0.0)
+    sb, sn = 100 * v / tot_b, 100 * nv / tot_n
+    worst = max(worst, abs(sb - sn))
+    share_rows.append(f"| {name} | {v:.3f} | {sb:.1f}% | {nv:.3f} | {sn:.1f}% | {sn - sb:+.1f} pp |")
+share_rows.append(f"| **sum** | **{tot_b:.3f}** | | **{tot_n:.3f}** | | max {worst:.1f} pp |")
+shares = "\n".join(share_rows) + "\n"
+r = d["roofline"]
 rf = d["roofline_fp32"]
-phases = ", ".join(f"{n.split(' ', 1)[1]} {v:.3f}" for n, v in ph.items())
-md = f"""# Round 1 — ncu evidence (B200, sm_100a), final state of the round
+ev = d.get("event", {})
+md = f"""# Round {rnd[1:]} — ncu evidence (B200, sm_100a)
 
-Workload: `bench.py` config 2 — 1,000,000 Gaussians (SH degree 3), one 1920×1080 view,
-one training iteration (K1 preprocess … K10 Adam, 19 launches), captured at **steady state**:
-after 150 training iterations, the state the bench's timed region sees (the per-step workload
-drifts as the scene trains). Commands (`scripts/gpu_profile.sh {tag} tests 150`, summarised by
+Workload: `bench.py` config 2 — 1,000,000 Gaussians (SH degree 3), 1920×1080 views of the
+synthetic ring, the bench's own settings (`--steps 20 --warmup 5`; after warm-up the scene,
+moments and camera sequence are restored, so the timed region is always training iterations
+1..20 from the same start state). `bench.py --profile` brackets exactly the timed iterations
+with `cudaProfilerStart/Stop`. Commands (`scripts/gpu_profile.sh {tag}`, summarised by
 `scripts/make_profile_md.py {tag}`):
 
 ```
-ncu --metrics gpu__time_duration.sum --clock-control none --csv -s 2850 -c 60 \\
-    --log-file gpurun_out/launches_{tag}.csv python bench.py --profile --steps 2 --warmup 150
-ncu --set full --import-source on --clock-control none -k regex:"blend_fwd|blend_bwd" -s 301 -c 2 \\
-    -o gpurun_out/full_{tag} python bench.py --profile --steps 2 --warmup 150
-ncu --set full --import-source on --clock-control none \\
-    -k regex:"preprocess|duplicate|onesweep|ssim|project_bwd|adam|scan_gather|tile_ranges" -s 2110 -c 14 \\
-    -o gpurun_out/fullb_{tag} python bench.py --profile --steps 1 --warmup 150
+ncu --profile-from-start off --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,\\
+    dram__bytes_write.sum --csv --log-file gpurun_out/launches_{tag}.csv \\
+    python bench.py --profile --steps 20 --warmup 5 --no-event
+ncu --profile-from-start off --clock-control none --set full --import-source on -o gpurun_out/full_{tag} \\
+    python bench.py --profile --steps 1 --warmup 5 --no-event
 ```
 
-ncu serialises kernels and flushes caches between them, so absolute times are cold-cache; the
-**shares** agree with bench.py's CUDA-event phase split of the same code (BENCH {tag}, ms:
-{phases}; {d['value']:.1f} it/s device-resident, {d['e2e']['value']:.1f} it/s end to end).
+The bench line of the same code and settings (`bench_{tag}.json`): **{d['value']:.1f} it/s
+device-resident, {d['e2e']['value']:.1f} it/s end to end** ({d['ms_per_step']:.3f} ms/step; SM clock
+{d['clocks']['sm_mhz']} MHz, throttle reasons {d['clocks']['reasons']}); dominant kernel
+{r['kernel']} at {r['achieved']:.2f} {r['unit']} = {100 * r['frac']:.1f}% of {r['peak']:.1f}.
+Density event (K11–K15 over 64 views, `event` sub-object): {ev.get('value', float('nan')):.2f} ms.
 
-## 1. Launch list of one training iteration
+## 1. Phase shares: ncu launch list vs bench.py CUDA events
+
+ncu serialises kernels and runs them cold (caches flushed between launches), so absolute times
+differ; the **shares** must agree with bench.py's CUDA-event phase split.
+
+{shares}
+## 2. Launch list (mean over the {nsteps} timed iterations)
 
 {launches}
-## 2. Full-set metrics: blend kernels
+## 3. Full-set metrics, iteration 1 (`full_{tag}.ncu-rep`)
 
 {full}
-## 3. Full-set metrics: streaming kernels
-
-{fullb}
 ## 4. Where the blend kernels spend their issue slots (per CUDA line, top 20)
 
-K8 `blend_bwd_kernel<16, 2>` (warp samples, executed warp instructions):
+K8 `blend_bwd_kernel<16, 2, 1>` (FAST mode, the training step's):
 
 ```
 {hb}```
 
-K6 `blend_fwd_warp_kernel<16, 2>`:
+K6 `blend_fwd_warp_kernel<16, 2, 1>`:
 
 ```
 {hf}```
 
 ## Reading
 
-* The blend kernels are **issue-bound** (stalls dominated by `not_selected` and fixed-latency
-  `wait`) with small DRAM traffic: their roof is the FP32/ALU issue rate. Against SURVEY §8(d)'s
-  algorithmic FP32 work (14 flop per visited + 9 / 52 per contributing pixel–Gaussian
-  evaluation; PGE_v = {rf['pge_visited'] / 1e6:.1f}M and PGE_c = {rf['pge_contributing'] / 1e6:.1f}M measured on
-  the frame), K6 reaches {rf['K6 blend fwd']['achieved']:.1f} TFLOP/s ({100 * rf['K6 blend fwd']['frac']:.0f}% of
-  {rf['K6 blend fwd']['peak']:.1f}) and K8 {rf['K8 blend bwd']['achieved']:.1f} TFLOP/s
-  ({100 * rf['K8 blend bwd']['frac']:.0f}%): the other issue slots go to the exactness machinery
-  (non-contracted round-to-nearest q, the deterministic exp, threshold re-checks), the warp
-  reduce-scatter (23 shuffles per entry pair) and lanes of partially covered 8×8 blocks.
-* HBM-bound kernels: Adam ≈6.0 TB/s (≈92% of the 6.53 TB/s copy roof), preprocess ≈4.9 TB/s of
-  DRAM traffic, project-backward ≈3.4 TB/s (latency-bound at 128 registers).
-* The tile-id onesweep passes are `short_scoreboard`-bound: a third of their samples wait on the
-  MATCH.ANY results of the stable warp ranking; they run out of L2.
+* The blend kernels are issue-bound with small DRAM traffic: their roof is the FP32 issue
+  rate. Against SURVEY §8(d)'s algorithmic FP32 work (14 flop per visited + 9 / 52 per
+  contributing pixel–Gaussian evaluation; PGE_v = {rf['pge_visited'] / 1e6:.1f}M, PGE_c =
+  {rf['pge_contributing'] / 1e6:.1f}M), K6 reaches {rf['K6 blend fwd']['achieved']:.1f} TFLOP/s
+  ({100 * rf['K6 blend fwd']['frac']:.0f}% of {rf['K6 blend fwd']['peak']:.1f}) and K8
+  {rf['K8 blend bwd']['achieved']:.1f} TFLOP/s ({100 * rf['K8 blend bwd']['frac']:.0f}%).
+* `traffic` in the bench line's roofline is the DRAM bytes per launch of §3 (profiles/traffic.json).
 """
-open("profiles/r1_ncu.md", "w").write(md)
-print("ok")
+open(f"profiles/{rnd}_ncu.md", "w").write(md)
+print(f"ok; max share delta {worst:.1f} pp")

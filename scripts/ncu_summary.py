@@ -28,21 +28,39 @@ def short(name: str) -> str:
     return n
 
 
-def launches(path: str) -> str:
+def launch_avg(path: str):
+    """[(kernel, us, dram_read_bytes, dram_write_bytes)] of one training
+    iteration (each starts at preprocess): with several iterations captured,
+    every launch position is averaged over them. Returns (list, iterations)."""
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     h = rows[0]
     ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
     per = {}
     for r in rows[1:]:
         per.setdefault(int(r[ii]), {"k": short(r[ki])})[r[mi]] = float(r[vi].replace(",", ""))
-    seq = sorted((i, d["k"], d.get("gpu__time_duration.sum", 0.0) / 1000.0, d.get("dram__bytes_read.sum"),
-                  d.get("dram__bytes_write.sum")) for i, d in per.items())
-    starts = [i for i, s in enumerate(seq) if s[1].startswith("preprocess")]
-    step = seq[starts[-1]:]
-    total = sum(t for _, _, t, _, _ in step)
-    out = ["| # | kernel | us | share | DRAM rd MB | DRAM wr MB |", "|---|---|---|---|---|---|"]
-    for j, (_, k, t, rd, wr) in enumerate(step):
-        f = lambda b: "" if b is None else f"{b / 1e6:.1f}" if b > 1e4 else f"{b:.1f}"
+    seq = [(d["k"], d.get("gpu__time_duration.sum", 0.0) / 1000.0, d.get("dram__bytes_read.sum"),
+            d.get("dram__bytes_write.sum")) for _, d in sorted(per.items())]
+    starts = [i for i, s in enumerate(seq) if s[0].startswith("preprocess")]
+    steps = [seq[a:b] for a, b in zip(starts, starts[1:] + [len(seq)])]
+    n = min(len(st) for st in steps)
+    avg = []
+    for j in range(n):
+        ts = [st[j][1] for st in steps]
+        rd = [st[j][2] for st in steps if st[j][2] is not None]
+        wr = [st[j][3] for st in steps if st[j][3] is not None]
+        avg.append((steps[0][j][0], sum(ts) / len(ts), sum(rd) / len(rd) if rd else None,
+                    sum(wr) / len(wr) if wr else None))
+    return avg, len(steps)
+
+
+def launches(path: str) -> str:
+    avg, nsteps = launch_avg(path)
+    steps = range(nsteps)
+    total = sum(t for _, t, _, _ in avg)
+    out = [f"Average over {len(steps)} captured training iteration(s).", "",
+           "| # | kernel | us | share | DRAM rd MB | DRAM wr MB |", "|---|---|---|---|---|---|"]
+    f = lambda b: "" if b is None else f"{b / 1e6:.2f}"
+    for j, (k, t, rd, wr) in enumerate(avg):
         out.append(f"| {j} | `{k}` | {t:.1f} | {100 * t / total:.1f}% | {f(rd)} | {f(wr)} |")
     out.append(f"| | **sum of kernels** | **{total:.1f}** | | | |")
     return "\n".join(out) + "\n"
