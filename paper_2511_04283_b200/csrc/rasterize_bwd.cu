@@ -94,7 +94,9 @@ struct PairState {
   int last0, last1;
 };
 
-template <bool FAST, typename Tab>
+// FIRST: the partials are assigned rather than accumulated (the lane's
+// first pixel pair of the entry; saves the adds of zero).
+template <bool FAST, bool FIRST, typename Tab>
 __device__ __forceinline__ bool pair_partials(const float4 mq, const float4 co, const float4 c, float fpx, int idx,
                                               PairState& st, const Tab& tab, float (&g)[kBGradFields]) {
   const float dx = fpx - mq.x;
@@ -145,28 +147,39 @@ __device__ __forceinline__ bool pair_partials(const float4 mq, const float4 co, 
   // product fused (fma(p1, q1, p0 q0 + g)): one rounding fewer than summing
   // two rounded products, which matters on the cancelling sums of small
   // gradients.
-  auto acc = [](float& gf, float2 a, float2 b) { gf = fmaf(a.y, b.y, fmaf(a.x, b.x, gf)); };
+  auto acc = [](float& gf, float2 a, float2 b) {
+    gf = FIRST ? fmaf(a.y, b.y, a.x * b.x) : fmaf(a.y, b.y, fmaf(a.x, b.x, gf));
+  };
   acc(g[5], ta, st.d0);
   acc(g[6], ta, st.d1);
   acc(g[7], ta, st.d2);
   acc(g[8], make_float2(geo0 ? ge.x : 0.0f, geo1 ? ge.y : 0.0f), d_alpha);  // e^{-q/2} d_alpha
   // ad = alpha d_alpha = -2 d_q on geometric entries (d_q = -alpha d_alpha / 2)
   const float2 ad = __fmul2_rn(make_float2(geo0 ? alpha.x : 0.0f, geo1 ? alpha.y : 0.0f), d_alpha);
-  // d_conic (full-matrix convention) accumulates -2 d_q [dx^2, dx dy, dy^2]; scaled by -1/2 at the end
-  acc(g[2], ad, f2(dx * dx));
-  acc(g[3], ad, __fmul2_rn(f2(dx), dy));
-  acc(g[4], ad, __fmul2_rn(dy, dy));
+  // d_conic (full-matrix convention) = d_q [dx^2, dx dy, dy^2] = -ad / 2 [..]
+  // (the power-of-two scale commutes with the rounding)
+  const float2 adh = __fmul2_rn(ad, f2(-0.5f));
+  acc(g[2], adh, f2(dx * dx));
+  acc(g[3], adh, __fmul2_rn(f2(dx), dy));
+  acc(g[4], adh, __fmul2_rn(dy, dy));
   // d_mu = -2 d_q conic d
   const float2 m0 = __fmul2_rn(ad, __ffma2_rn(f2(co.y), dy, f2(co.x * dx)));
   const float2 m1 = __fmul2_rn(ad, __ffma2_rn(f2(co.z), dy, f2(co.y * dx)));
-  g[0] = (g[0] + m0.x) + m0.y;
-  g[1] = (g[1] + m1.x) + m1.y;
-  g[9] = (g[9] + fabsf(m0.x)) + fabsf(m0.y);
-  g[10] = (g[10] + fabsf(m1.x)) + fabsf(m1.y);
+  if (FIRST) {
+    g[0] = m0.x + m0.y;
+    g[1] = m1.x + m1.y;
+    g[9] = fabsf(m0.x) + fabsf(m0.y);
+    g[10] = fabsf(m1.x) + fabsf(m1.y);
+  } else {
+    g[0] = (g[0] + m0.x) + m0.y;
+    g[1] = (g[1] + m1.x) + m1.y;
+    g[9] = (g[9] + fabsf(m0.x)) + fabsf(m0.y);
+    g[10] = (g[10] + fabsf(m1.x)) + fabsf(m1.y);
+  }
   return ok0 || ok1;
 }
 
-// Scalar form of the same step for one-pixel lanes (8x8 tiles).
+// Scalar form of the same step for one-pixel lanes (8x8 tiles); assigns g.
 template <bool FAST, typename Tab>
 __device__ __forceinline__ bool one_partials(const float4 mq, const float4 co, const float4 c, float fpx, float fpy,
                                              int idx, int last, float& T, float& ns, float d0, float d1, float d2,
@@ -194,19 +207,20 @@ __device__ __forceinline__ bool one_partials(const float4 mq, const float4 co, c
   const float d_alpha = fmaf(ns, inv, tb * w);
   const float ta = tb * alpha;
   ns = fmaf(-ta, w, ns);
-  g[5] = fmaf(ta, d0, g[5]);
-  g[6] = fmaf(ta, d1, g[6]);
-  g[7] = fmaf(ta, d2, g[7]);
-  g[8] = fmaf(geo ? ge : 0.0f, d_alpha, g[8]);
+  g[5] = ta * d0;
+  g[6] = ta * d1;
+  g[7] = ta * d2;
+  g[8] = (geo ? ge : 0.0f) * d_alpha;
   const float ad = geo ? alpha * d_alpha : 0.0f;
-  g[2] = fmaf(ad, dx * dx, g[2]);
-  g[3] = fmaf(ad, dx * dy, g[3]);
-  g[4] = fmaf(ad, dy * dy, g[4]);
+  const float adh = -0.5f * ad;
+  g[2] = adh * (dx * dx);
+  g[3] = adh * (dx * dy);
+  g[4] = adh * (dy * dy);
   const float m0 = ad * fmaf(co.y, dy, co.x * dx), m1 = ad * fmaf(co.z, dy, co.y * dx);
-  g[0] += m0;
-  g[1] += m1;
-  g[9] += fabsf(m0);
-  g[10] += fabsf(m1);
+  g[0] = m0;
+  g[1] = m1;
+  g[9] = fabsf(m0);
+  g[10] = fabsf(m1);
   return ok;
 }
 
@@ -296,45 +310,56 @@ __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS /
   }
   __syncthreads();  // publishes the exp table
   const int warp_last = __reduce_max_sync(0xffffffffu, my_last);
-  float pend[kBGradFields];
-  uint32_t pend_id = 0;
-  bool has_pend = false;
 
-  // Reverse-walk step for staged slot j (list position idx): this lane's
-  // partials, then (two entries at a time) the warp reduce-scatter and the
-  // global atomics.
-  auto walk_entry = [&](int j, int idx) {
+  // This lane's 11 partials of staged slot j (list position idx), the
+  // -2 d_q scale folded in; returns whether some lane of the warp
+  // contributed (warp-uniform).
+  auto partials = [&](int j, int idx, float (&gv)[kBGradFields]) {
     const float4 mq = ld_f4(0u, j);
     const float4 co = ld_f4(16u * NT, j);
     const float4 c = ld_f4(32u * NT, j);
-    float gv[kBGradFields];
-    bool contrib = false;
-#pragma unroll
-    for (int f = 0; f < kBGradFields; ++f) gv[f] = 0.0f;
+    bool contrib;
     if (PIX >= 2) {
+      contrib = pair_partials<FAST, true>(mq, co, c, fpx, idx, ps[0], tab, gv);
 #pragma unroll
-      for (int k = 0; k < NP; ++k) contrib = pair_partials<FAST>(mq, co, c, fpx, idx, ps[k], tab, gv) || contrib;
+      for (int k = 1; k < NP; ++k) contrib = pair_partials<FAST, false>(mq, co, c, fpx, idx, ps[k], tab, gv) || contrib;
     } else {
       contrib = one_partials<FAST>(mq, co, c, fpx, fpy[0], idx, last[0], T1, ns1, d0[0], d1[0], d2[0], tab, gv);
     }
-    // the conic fields were accumulated as -2 d_q [dx^2, dx dy, dy^2]
-    gv[2] *= -0.5f;
-    gv[3] *= -0.5f;
-    gv[4] *= -0.5f;
-    if (__ballot_sync(0xffffffffu, contrib)) {
-      if (has_pend) {
-        reduce_scatter_2x11(pend, gv, pend_id, ld_id(j), true, bgrads, gstride);
-        has_pend = false;
+    return __any_sync(0xffffffffu, contrib);
+  };
+  // Entries are reduced two at a time (reduce_scatter_2x11): the walk
+  // alternates between computing into ga (the pending entry, kept across
+  // batches) and gb, then reduces the pair, so no partials are copied.
+  float ga[kBGradFields], gb[kBGradFields];
+  uint32_t id_a = 0;
+  bool has_a = false;
+  // pops the highest set bit of m (reverse list order)
+  auto pop = [](uint32_t& m) {
+    uint32_t bit;
+    asm("bfind.u32 %0, %1;" : "=r"(bit) : "r"(m));
+    m ^= 1u << bit;
+    return (int)bit;
+  };
+  const int base = warp * 32;
+  auto walk = [&](uint32_t m, int b0) {
+    while (m) {
+      if (!has_a) {
+        const int bit = pop(m);
+        if (partials(base + bit, b0 + bit, ga)) {
+          has_a = true;
+          id_a = ld_id(base + bit);
+        }
       } else {
-#pragma unroll
-        for (int f = 0; f < kBGradFields; ++f) pend[f] = gv[f];
-        pend_id = ld_id(j);
-        has_pend = true;
+        const int bit = pop(m);
+        if (partials(base + bit, b0 + bit, gb)) {
+          reduce_scatter_2x11(ga, gb, id_a, ld_id(base + bit), true, bgrads, gstride);
+          has_a = false;
+        }
       }
     }
   };
 
-  const int base = warp * 32;
   if (TS == 16 && cmask) {
     // Over K6's 32-entry batches with K6's contribution masks: only the
     // entries a pixel of this block blended in the forward pass are gathered
@@ -361,11 +386,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS /
           s_st.id[base + lane] = g;
         }
         __syncwarp();
-        while (m) {
-          const int bit = 31 - __clz(m);
-          m ^= 1u << bit;
-          walk_entry(base + bit, b0 + bit);
-        }
+        walk(m, b0);
         __syncwarp();
       }
     }
@@ -392,21 +413,16 @@ __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS /
           s_st.id[base + lane] = g;
         }
       }
-      uint32_t m = __ballot_sync(0xffffffffu, hit);
+      const uint32_t m = __ballot_sync(0xffffffffu, hit);
       __syncwarp();
-      while (m) {
-        const int bit = 31 - __clz(m);
-        m ^= 1u << bit;
-        walk_entry(base + bit, b0 + bit);
-      }
+      walk(m, b0);
       __syncwarp();
     }
   }
-  if (has_pend) {  // warp-uniform: flush the last unpaired entry
-    float zero[kBGradFields];
+  if (has_a) {  // warp-uniform: flush the last unpaired entry
 #pragma unroll
-    for (int f = 0; f < kBGradFields; ++f) zero[f] = 0.0f;
-    reduce_scatter_2x11(pend, zero, pend_id, 0u, false, bgrads, gstride);
+    for (int f = 0; f < kBGradFields; ++f) gb[f] = 0.0f;
+    reduce_scatter_2x11(ga, gb, id_a, 0u, false, bgrads, gstride);
   }
 }
 
