@@ -334,7 +334,6 @@ int sk_frame_set_tile_lists(sk_ctx* ctx, sk_frame* f, const int32_t* ranges, con
     uint32_t* pv = ensure<uint32_t>(f->pval_a, pm);
     if (pairs > 0) h2d(ctx, pv, values, pairs);
     f->pair_val = pv;
-    f->pair_tile = nullptr;
     f->pairs = pairs;
     f->binned = true;
     f->rendered = false;

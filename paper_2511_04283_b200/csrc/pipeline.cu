@@ -51,14 +51,9 @@ void ensure_image(sk_frame* f) {
   ensure<int>(f->last_entry, plane);
 }
 
-int tile_bits(int tiles) {
-  int b = 1;
-  while ((1ll << b) < tiles) ++b;
-  return b;
-}
-
-
-// K2-K5 (build_tile_grid raster.hpp:157-168).
+// K2-K5 (build_tile_grid raster.hpp:157-168): depth sort of the slots, then
+// the tile lists by the counting scatter of preprocess.cu (count, prefix over
+// chunks + tile scan, stable scatter).
 void bin_sort(sk_ctx* ctx, sk_frame* f) {
   const int64_t n = f->n;
   f->cmask_valid = false;
@@ -70,43 +65,48 @@ void bin_sort(sk_ctx* ctx, sk_frame* f) {
     f->binned = true;
     return;
   }
+  cudaStream_t s = ctx->stream;
   uint32_t* ka = ensure<uint32_t>(f->keys_a, n);
   uint32_t* kb = ensure<uint32_t>(f->keys_b, n);
   uint32_t* va = ensure<uint32_t>(f->vals_a, n);
   uint32_t* vb = ensure<uint32_t>(f->vals_b, n);
   radix_sort_pairs(ctx, ka, kb, va, vb, n, 32);  // depth_order: (depth, index)
-  int32_t* offsets = ensure<int32_t>(f->offsets, n);
-  const int bits = tile_bits(tiles);
-  uint32_t* hist = radix_hist_buffer(ctx);
-  const long long* d_total = launch_scan_gathered(ctx, f->tiles.as<int32_t>(), va, offsets, n);
-  // Speculative emission: the pair buffers already hold `cap` pairs from an
-  // earlier frame (DevBuf keeps 25% headroom), so K3 is launched before the
-  // host reads the pair count and the GPU emits pairs while the host waits;
-  // it is relaunched only if the count outgrew the buffers.
-  auto cap_of = [](const DevBuf& b) { return (int64_t)(b.bytes / sizeof(uint32_t)); };
-  const int64_t cap =
-      std::min(std::min(cap_of(f->ptile_a), cap_of(f->ptile_b)), std::min(cap_of(f->pval_a), cap_of(f->pval_b)));
-  auto emit = [&](int64_t limit) {
-    SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * 256, ctx->stream));
-    launch_duplicate(ctx, f, va, offsets, f->ptile_a.as<uint32_t>(), f->pval_a.as<uint32_t>(), radix_passes(bits),
-                     radix_digit_width(bits), hist, limit);
-  };
-  if (cap > 256) emit(cap);
-  const int64_t pairs = read_scan_total(ctx, d_total);
+  int32_t* counts = ensure<int32_t>(ctx->sort.bin_counts, (size_t)bin_chunks(f) * tiles);
+  int32_t* totals = ensure<int32_t>(ctx->sort.bin_totals, (size_t)tiles);
+  if (!ctx->sort.bin_total.ptr) {
+    ensure<long long>(ctx->sort.bin_total, 2);
+    SK_CUDA(cudaMemsetAsync(ctx->sort.bin_total.ptr, 0, 2 * sizeof(long long), s));
+  }
+  auto* total = ctx->sort.bin_total.as<long long>();
+  auto* done = reinterpret_cast<unsigned int*>(total + 1);
+  launch_bin_tiles(ctx, f, va, counts, nullptr, 0);
+  launch_bin_prefix(ctx, f, counts, totals, done, total);
+  // P on the host: copied on a side stream right after the prefix kernel, so
+  // the host wakes while the scatter queued behind it still runs. The scatter
+  // is launched speculatively into the pair buffer left by an earlier frame
+  // (DevBuf keeps 25% headroom; slots past the capacity are not written) and
+  // relaunched only if P outgrew it.
+  if (!ctx->count_stream) {
+    SK_CUDA(cudaStreamCreateWithFlags(&ctx->count_stream, cudaStreamNonBlocking));
+    SK_CUDA(cudaEventCreateWithFlags(&ctx->count_ev, cudaEventDisableTiming));
+  }
+  auto* host = static_cast<long long*>(ctx->count_pinned.ensure(sizeof(long long)));
+  SK_CUDA(cudaEventRecord(ctx->count_ev, s));
+  SK_CUDA(cudaStreamWaitEvent(ctx->count_stream, ctx->count_ev, 0));
+  SK_CUDA(cudaMemcpyAsync(host, total, sizeof(long long), cudaMemcpyDeviceToHost, ctx->count_stream));
+  const int64_t cap = (int64_t)(f->pval_a.bytes / sizeof(uint32_t));
+  if (cap > 256) launch_bin_tiles(ctx, f, va, counts, f->pval_a.as<uint32_t>(), cap);
+  SK_CUDA(cudaStreamSynchronize(ctx->count_stream));
+  const int64_t pairs = *host;
   require(pairs < (1ll << 30), "build_tile_grid: too many tile/Gaussian pairs");
   f->pairs = pairs;
-  const size_t pm = (size_t)std::max<int64_t>(pairs, 1);
-  // the speculative K3 may still be writing the buffers a regrowth frees
-  if (cap > 256 && pairs > cap) SK_CUDA(cudaStreamSynchronize(ctx->stream));
-  uint32_t* ta = ensure<uint32_t>(f->ptile_a, pm);
-  uint32_t* tb = ensure<uint32_t>(f->ptile_b, pm);
-  uint32_t* pa = ensure<uint32_t>(f->pval_a, pm);
-  uint32_t* pb = ensure<uint32_t>(f->pval_b, pm);
-  if (!(cap > 256 && pairs <= cap)) emit(pairs);
-  radix_sort_pairs(ctx, ta, tb, pa, pb, pairs, bits, /*hist_ready=*/true);
-  f->pair_tile = ta;
-  f->pair_val = pa;
-  launch_tile_ranges(ctx, ta, pairs, f->ranges.as<int2>(), tiles);
+  if (!(cap > 256 && pairs <= cap)) {
+    // the speculative scatter may still be writing the buffer a regrowth frees
+    if (cap > 256) SK_CUDA(cudaStreamSynchronize(s));
+    uint32_t* pv = ensure<uint32_t>(f->pval_a, (size_t)std::max<int64_t>(pairs, 1));
+    launch_bin_tiles(ctx, f, va, counts, pv, pairs);
+  }
+  f->pair_val = f->pval_a.as<uint32_t>();
   f->binned = true;
 }
 

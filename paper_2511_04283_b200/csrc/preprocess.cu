@@ -1,4 +1,4 @@
-// K1 preprocess and K3 duplicate-with-keys.
+// K1 preprocess and K3 tile binning (counting scatter).
 //
 // K1 follows project() (reference camera.hpp:93-123) with covariance_3d
 // (scene.hpp:88-96), quat_to_rotation (scene.hpp:57-65), evaluate_sh
@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
   auto culled = [&]() {
     radius_out[i] = 0.0f;
     tiles_out[i] = 0;
+    rect_out[i] = make_int4(0, 0, -1, -1);  // K3 enumerates rectangles only
     key_out[i] = 0xffffffffu;
   };
   const float mu0 = p[0 * stride + i], mu1 = p[1 * stride + i], mu2 = p[2 * stride + i];
@@ -331,113 +332,400 @@ __global__ void inject_bin_kernel(int64_t n, BinParams bp, const float2* __restr
   key_out[i] = bo.count > 0 ? depth_key_bits(rgbd[i].w) : 0xffffffffu;
 }
 
-// K3: one thread per depth-sorted position; writes the Gaussian's tile ids
-// (row-major within its rectangle, as bin_aabb / bin_compact enumerate them)
-// at its scanned offset. Pair order = (depth, index) order, which the
-// stable tile sort then preserves inside each tile.
-// K3: pairs (tile, Gaussian) in (depth, index) order, plus the digit
-// histograms of the following tile-id radix sort (hist[p][256], p < passes).
-// A warp takes 32 consecutive depth-ordered slots; their pair runs are
-// adjacent in the output, so in AABB mode the warp writes the whole range
-// cooperatively (lane e writes pair e: owner found by a shuffle binary search
-// over the lanes' offsets, tile from the owner's rectangle) and every store
-// is coalesced. Compact mode keeps one thread per Gaussian (its tiles are a
-// filtered subset of the rectangle).
-constexpr int kDupThreads = 256;
-__global__ void __launch_bounds__(kDupThreads) duplicate_kernel(int64_t n, BinParams bp,
-                                                                const uint32_t* __restrict__ order,
-                                                                const int32_t* __restrict__ offsets,
-                                                                const int* __restrict__ tiles,
-                                                                const int4* __restrict__ rect,
-                                                                const float2* __restrict__ mean2d,
-                                                                const float4* __restrict__ conic_op,
-                                                                const float* __restrict__ a_star,
-                                                                uint32_t* __restrict__ pair_tile,
-                                                                uint32_t* __restrict__ pair_val, int passes,
-                                                                int width, uint32_t* __restrict__ hist,
-                                                                int64_t cap) {
-  __shared__ uint32_t s_hist[4][256];
-  for (int i = threadIdx.x; i < 4 * 256; i += kDupThreads) (&s_hist[0][0])[i] = 0;
+// K3: the per-tile lists as a stable counting scatter (replaces the
+// reference's per-tile push_back in build_tile_grid, raster.hpp:157-168, and
+// the sort that list order implies).
+//
+// The slots are visited in (depth, index) order — the depth sort's output —
+// cut into chunks of consecutive slots. The tile rows are split into
+// row-groups whose counters fit in shared memory (one group at 1080p / 16-px
+// tiles); a CTA handles one (chunk, row-group).
+//   bin_count_kernel    counts[chunk][tile] = pairs of the chunk per tile
+//                       (shared-memory atomics; order does not matter here)
+//   bin_prefix_kernel   counts -> exclusive prefix over chunks, per tile; the
+//                       last CTA scans the tile totals into the ranges and P
+//   bin_scatter_kernel  each warp owns a band of tile rows, so no two warps
+//                       share a tile counter. Per stage of slots the CTA
+//                       builds, with ballots, each band's list of the slots
+//                       whose rectangle reaches it (in slot order); a warp
+//                       walks its list and enumerates the band's pairs
+//                       Gaussian-major, 32 at a time (lane e takes pair e:
+//                       owner by a shuffle binary search over the lanes'
+//                       offsets, tile from the owner's rectangle). Lower lanes
+//                       therefore hold earlier Gaussians, so __match_any_sync
+//                       on the tile gives each pair its rank among the round's
+//                       same-tile pairs and the round's leader advances the
+//                       tile's counter: slot = ranges[t].x + prefix[chunk][t]
+//                       + the chunk's earlier pairs of t.
+// Every tile thus receives its Gaussians in (depth, index) order — the
+// reference's list order — with no key sort over the pairs, and only the
+// 4-byte Gaussian index is written per pair. Compact binning enumerates the
+// same rectangle and drops the tiles failing the min-Mahalanobis test
+// (bin_compact, raster.hpp:111-141), exactly as K1 counted them.
+#ifndef SK_BIN_WARPS
+#define SK_BIN_WARPS 16
+#endif
+#ifndef SK_BIN_MINB
+#define SK_BIN_MINB 2
+#endif
+constexpr int kBinWarps = SK_BIN_WARPS;  // tile-row bands per scatter CTA
+constexpr int kBinThreads = kBinWarps * 32;
+constexpr int kBinStage = 1024;  // slots staged in shared memory per step
+constexpr int kCountThreads = 256;
+constexpr int kBinMaxSmemTiles = 40960;  // 160 KB of int32 counters per row-group
+constexpr int kCountSmallArea = 48;      // larger rectangles are counted by the whole warp
+
+struct BinLayout {
+  int64_t n;           // slots in depth order
+  int64_t chunk;       // slots per chunk (multiple of kBinThreads)
+  int tiles;           // tiles_x * tiles_y
+  int rows_per_group;  // tile rows per CTA row-group
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt_u32() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Compact binning keeps a tile of the rectangle only if the footprint's
+// min-Mahalanobis distance to it is within a* (the test K1 counted with).
+__device__ __forceinline__ bool compact_keeps(const BinParams& bp, int ty, int tx, float2 mu, float4 co, float as) {
+  const float ry0 = (float)(ty * bp.ts);
+  const float ry1 = (float)(min((ty + 1) * bp.ts, bp.H) - 1);
+  const float rx0 = (float)(tx * bp.ts);
+  const float rx1 = (float)(min((tx + 1) * bp.ts, bp.W) - 1);
+  return min_mahalanobis_on_rect(co.x, co.y, co.z, mu.x, mu.y, rx0, rx1, ry0, ry1) <= as;
+}
+
+__global__ void __launch_bounds__(kCountThreads) bin_count_kernel(BinParams bp, BinLayout L,
+                                                                  const uint32_t* __restrict__ order,
+                                                                  const int4* __restrict__ rect,
+                                                                  const float2* __restrict__ mean2d,
+                                                                  const float4* __restrict__ conic_op,
+                                                                  const float* __restrict__ a_star,
+                                                                  int32_t* __restrict__ counts) {
+  extern __shared__ int32_t s_cnt[];
+  const int row0 = blockIdx.y * L.rows_per_group;
+  const int rows = min(L.rows_per_group, bp.tiles_y - row0);
+  const int t0 = row0 * bp.tiles_x;
+  const int gtiles = rows * bp.tiles_x;
+  for (int i = threadIdx.x; i < gtiles; i += kCountThreads) s_cnt[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  auto count_digits = [&](uint32_t t) {
-    for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(t >> (width * p)) & ((1u << width) - 1u)], 1u);
-  };
-  const int64_t warps = (int64_t)gridDim.x * (kDupThreads / 32);
-  for (int64_t wi = (int64_t)blockIdx.x * (kDupThreads / 32) + (threadIdx.x >> 5); wi * 32 < n; wi += warps) {
-    const int64_t s = wi * 32 + lane;
-    const bool valid = s < n;
-    const uint32_t g = valid ? order[s] : 0u;
-    const int cnt = valid ? tiles[g] : 0;
-    const int off = valid ? offsets[s] : 0x7fffffff;
-    if (bp.mode != 0) {
-      if (cnt == 0) continue;
-      int64_t o = off;
-      const float2 mu = mean2d[g];
-      const float4 co = conic_op[g];
-      const float as = a_star[g];
-      const int4 rc = rect[g];
-      for (int ty = rc.y; ty <= rc.w; ++ty) {
-        const float ry0 = (float)(ty * bp.ts);
-        const float ry1 = (float)(min((ty + 1) * bp.ts, bp.H) - 1);
-        for (int tx = rc.x; tx <= rc.z; ++tx) {
-          const float rx0 = (float)(tx * bp.ts);
-          const float rx1 = (float)(min((tx + 1) * bp.ts, bp.W) - 1);
-          if (min_mahalanobis_on_rect(co.x, co.y, co.z, mu.x, mu.y, rx0, rx1, ry0, ry1) <= as) {
-            const uint32_t t = (uint32_t)(ty * bp.tiles_x + tx);
-            if (o < cap) {
-              pair_tile[o] = t;
-              pair_val[o] = g;
-            }
-            count_digits(t);
-            ++o;
-          }
-        }
-      }
-      continue;
-    }
-    const int4 rc = cnt ? rect[g] : make_int4(0, 0, 0, 0);
-    const int w = rc.z - rc.x + 1;
-    const float inv_w = 1.0f / (float)w;  // row split of the pair index: estimate + exact fix-up
-    // the warp's pairs occupy [first, last) contiguously
-    const int first = __reduce_min_sync(0xffffffffu, valid ? off : 0x7fffffff);
-    const int last = __reduce_max_sync(0xffffffffu, valid ? off + cnt : 0);
-    const int total = last - first;
-    for (int e0 = 0; e0 < total; e0 += 32) {
-      const int pos = first + e0 + lane;
-      // owner = the highest lane whose offset is <= pos (zero-count lanes
-      // share the next lane's offset, so they are never chosen for a pair)
-      int L = 0;
+  const int64_t s_begin = (int64_t)blockIdx.x * L.chunk;
+  const int64_t s_end = s_begin + L.chunk < L.n ? s_begin + L.chunk : L.n;
+  constexpr int kPer = 4;  // slots per thread per step: their loads are issued together
+  for (int64_t sb = s_begin; sb < s_end; sb += kCountThreads * kPer) {
+    uint32_t gq[kPer];
+    int4 rq[kPer];
 #pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int o = __shfl_sync(0xffffffffu, off, L + step);
-        if (o <= pos) L += step;
+    for (int q = 0; q < kPer; ++q) {
+      const int64_t s = sb + q * kCountThreads + threadIdx.x;
+      gq[q] = s < s_end ? order[s] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) rq[q] = gq[q] != 0xffffffffu ? rect[gq[q]] : make_int4(0, 0, -1, -1);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const uint32_t g = gq[q];
+      const int4 rc = rq[q];
+      const int ya = max(rc.y, row0), yb = min(rc.w, row0 + rows - 1), xa = rc.x, w = rc.z - rc.x + 1;
+      const int area = ya <= yb ? (yb - ya + 1) * w : 0;
+      if (area > 0 && area <= kCountSmallArea) {
+        float2 mu = make_float2(0.f, 0.f);
+        float4 co = make_float4(0.f, 0.f, 0.f, 0.f);
+        float as = 0.f;
+        if (bp.mode != 0) {
+          mu = mean2d[g];
+          co = conic_op[g];
+          as = a_star[g];
+        }
+        for (int ty = ya; ty <= yb; ++ty)
+          for (int tx = xa; tx < xa + w; ++tx)
+            if (bp.mode == 0 || compact_keeps(bp, ty, tx, mu, co, as)) atomicAdd(&s_cnt[(ty - row0) * bp.tiles_x + tx], 1);
       }
-      const int k = pos - __shfl_sync(0xffffffffu, off, L);
-      const int ox = __shfl_sync(0xffffffffu, rc.x, L);
-      const int oy = __shfl_sync(0xffffffffu, rc.y, L);
-      const int ow = __shfl_sync(0xffffffffu, w, L);
-      const float oinv = __shfl_sync(0xffffffffu, inv_w, L);
-      const uint32_t og = __shfl_sync(0xffffffffu, g, L);
-      const bool active = e0 + lane < total;
-      uint32_t t = 0;
-      if (active) {
-        int r = (int)((float)k * oinv);  // within one of k / ow (k < 2^24)
-        r += (r + 1) * ow <= k;
-        r -= r * ow > k;
-        t = (uint32_t)((oy + r) * bp.tiles_x + ox + (k - r * ow));
-        if (pos < cap) {
-          pair_tile[pos] = t;
-          pair_val[pos] = og;
+      // large rectangles: the whole warp strides over one at a time
+      uint32_t big = __ballot_sync(0xffffffffu, area > kCountSmallArea);
+      while (big) {
+        const int src = __ffs(big) - 1;
+        big &= big - 1;
+        const int sya = __shfl_sync(0xffffffffu, ya, src);
+        const int sxa = __shfl_sync(0xffffffffu, xa, src);
+        const int sw = __shfl_sync(0xffffffffu, w, src);
+        const int sarea = __shfl_sync(0xffffffffu, area, src);
+        const uint32_t sg = __shfl_sync(0xffffffffu, g, src);
+        float2 mu = make_float2(0.f, 0.f);
+        float4 co = make_float4(0.f, 0.f, 0.f, 0.f);
+        float as = 0.f;
+        if (bp.mode != 0) {
+          mu = mean2d[sg];
+          co = conic_op[sg];
+          as = a_star[sg];
+        }
+        for (int k = lane; k < sarea; k += 32) {
+          const int r = k / sw;
+          const int ty = sya + r, tx = sxa + (k - r * sw);
+          if (bp.mode == 0 || compact_keeps(bp, ty, tx, mu, co, as)) atomicAdd(&s_cnt[(ty - row0) * bp.tiles_x + tx], 1);
         }
       }
-      if (active) count_digits(t);
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < passes * 256; i += kDupThreads) {
-    const uint32_t v = (&s_hist[0][0])[i];
-    if (v) atomicAdd(&hist[i], v);
+  int32_t* crow = counts + (int64_t)blockIdx.x * L.tiles + t0;
+  for (int i = threadIdx.x; i < gtiles; i += kCountThreads) crow[i] = s_cnt[i];
+}
+
+// counts[c][t] -> sum over chunks c' < c (in place), per tile column: 32
+// tiles per CTA, pages of 32 x 8 chunk rows, each warp holding its 8 rows
+// of the page in registers (one read, one write of the matrix). The last CTA
+// to finish scans the tile totals into ranges[t] = [start, start + total)
+// and writes P.
+constexpr int kPrefixWarps = 32;
+constexpr int kPrefixRows = 8;
+__global__ void __launch_bounds__(kPrefixWarps * 32) bin_prefix_kernel(int32_t* __restrict__ counts, int chunks,
+                                                                       int tiles, int32_t* __restrict__ totals,
+                                                                       int2* __restrict__ ranges,
+                                                                       unsigned int* __restrict__ done,
+                                                                       long long* __restrict__ total_out) {
+  constexpr int NT = kPrefixWarps * 32;
+  constexpr int kItems = 4;
+  __shared__ int32_t s_sum[kPrefixWarps][32];
+  __shared__ bool s_last;
+  __shared__ long long s_carry;
+  __shared__ long long s_warp[kPrefixWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
+  int carry = 0;
+  for (int page = 0; page < chunks; page += kPrefixWarps * kPrefixRows) {
+    const int c0 = page + warp * kPrefixRows;
+    int v[kPrefixRows];
+    int sum = 0;
+#pragma unroll
+    for (int r = 0; r < kPrefixRows; ++r) {
+      v[r] = c0 + r < chunks && t < tiles ? counts[(int64_t)(c0 + r) * tiles + t] : 0;
+      sum += v[r];
+    }
+    __syncthreads();  // s_sum of the previous page consumed
+    s_sum[warp][lane] = sum;
+    __syncthreads();
+    int run = carry, page_total = 0;
+#pragma unroll
+    for (int w = 0; w < kPrefixWarps; ++w) {
+      const int x = s_sum[w][lane];
+      run += w < warp ? x : 0;
+      page_total += x;
+    }
+#pragma unroll
+    for (int r = 0; r < kPrefixRows; ++r) {
+      if (c0 + r < chunks && t < tiles) counts[(int64_t)(c0 + r) * tiles + t] = run;
+      run += v[r];
+    }
+    carry += page_total;
+  }
+  if (warp == 0 && t < tiles) totals[t] = carry;
+  // the last CTA: exclusive scan of the tile totals
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) s_carry = 0;
+  for (int base = 0; base < tiles; base += NT * kItems) {
+    __syncthreads();
+    const int i0 = base + threadIdx.x * kItems;
+    int v[kItems];
+    long long loc = 0;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      v[q] = i0 + q < tiles ? __ldcg(&totals[i0 + q]) : 0;
+      loc += v[q];
+    }
+    long long x = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    long long wb = s_carry, all = 0;
+#pragma unroll
+    for (int w = 0; w < kPrefixWarps; ++w) {
+      wb += w < warp ? s_warp[w] : 0;
+      all += s_warp[w];
+    }
+    long long start = wb + x - loc;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      if (i0 + q < tiles) ranges[i0 + q] = make_int2((int)start, (int)(start + v[q]));
+      start += v[q];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += all;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *total_out = s_carry;
+    *done = 0;  // ready for the next frame
+  }
+}
+
+__global__ void __launch_bounds__(kBinThreads, SK_BIN_MINB) bin_scatter_kernel(BinParams bp, BinLayout L,
+                                                                  const uint32_t* __restrict__ order,
+                                                                  const int4* __restrict__ rect,
+                                                                  const float2* __restrict__ mean2d,
+                                                                  const float4* __restrict__ conic_op,
+                                                                  const float* __restrict__ a_star,
+                                                                  const int32_t* __restrict__ counts,
+                                                                  const int2* __restrict__ ranges,
+                                                                  uint32_t* __restrict__ pair_val, int64_t cap) {
+  extern __shared__ int32_t s_pos[];  // the row-group's tile counters
+  __shared__ uint32_t s_g[kBinStage];
+  __shared__ int4 s_rect[kBinStage];
+  __shared__ uint32_t s_cls[kBinStage];         // per slot: bit w = the rectangle reaches warp w's rows
+  __shared__ uint16_t s_queue[kBinWarps][64];  // per warp: stage slots reaching its rows, in slot order
+  const int tid = threadIdx.x;
+  const int row0 = blockIdx.y * L.rows_per_group;
+  const int rows = min(L.rows_per_group, bp.tiles_y - row0);
+  const int t0 = row0 * bp.tiles_x;
+  const int gtiles = rows * bp.tiles_x;
+  const int32_t* crow = counts + (int64_t)blockIdx.x * L.tiles + t0;
+  for (int i = tid; i < gtiles; i += kBinThreads) s_pos[i] = ranges[t0 + i].x + crow[i];
+
+  // warp w owns the group's tile rows row0 + w + q * kBinWarps (interleaved,
+  // so the pair load is balanced whatever the scene's vertical profile)
+  const int warp = tid >> 5, lane = tid & 31;
+  const uint32_t lt = lanemask_lt_u32();
+  const int64_t s_begin = (int64_t)blockIdx.x * L.chunk;
+  const int64_t s_end = s_begin + L.chunk < L.n ? s_begin + L.chunk : L.n;
+  // this warp's rows of a rectangle's clipped row span [ya, yb]: q in [qa, qb]
+  auto my_rows = [&](int ya, int yb, int& qa) {
+    const int lo = ya - row0 - warp, hi = yb - row0 - warp;
+    qa = lo <= 0 ? 0 : (lo + kBinWarps - 1) / kBinWarps;
+    const int qb = hi < 0 ? -1 : hi / kBinWarps;
+    return qb - qa + 1;
+  };
+  // one batch of up to 32 queued slots (each reaches this warp's rows): their
+  // pairs in this warp's rows, Gaussian-major, 32 per round. Per-round cost
+  // is what bounds this kernel (MATCH / SHFL are 1/2 and 1 warp-instruction
+  // per clock per SM, POPC / FLO / I2F 1/2: scripts/micro/warp_ops.cu), so a
+  // round uses 5 + 3 shuffles, one MATCH, two POPC and a multiply-high for
+  // the row split.
+  auto walk = [&](int head, int cnt) {
+    int m = 0;
+    uint32_t g = 0, packed = 0, magic = 0;
+    if (lane < cnt) {
+      const int slot = s_queue[warp][(head + lane) & 63];
+      const int4 rc = s_rect[slot];
+      g = s_g[slot];
+      int qa;
+      const int nr = my_rows(max(rc.y, row0), min(rc.w, row0 + rows - 1), qa);
+      const int w = rc.z - rc.x + 1;
+      m = nr * w;
+      packed = (uint32_t)rc.x | ((uint32_t)qa << 12) | ((uint32_t)w << 20);
+      magic = 0xffffffffu / (uint32_t)w + 1u;  // k / w == umulhi(k, magic) for k, w < 2^16
+    }
+    int incl = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int off = incl - m;  // lanes >= cnt: off == total, never an owner
+    for (int e0 = 0; e0 < total; e0 += 32) {
+      const int pos = e0 + lane;
+      // owner = the highest lane whose offset is <= pos; its offset comes
+      // out of the search (lane 0's is 0)
+      int o = 0, off_o = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, off, o + step);
+        if (v <= pos) {
+          o += step;
+          off_o = v;
+        }
+      }
+      const uint32_t og = __shfl_sync(0xffffffffu, g, o);
+      const uint32_t op = __shfl_sync(0xffffffffu, packed, o);
+      const uint32_t omag = __shfl_sync(0xffffffffu, magic, o);
+      const uint32_t k = (uint32_t)(pos - off_o);
+      const uint32_t r = __umulhi(k, omag);
+      const int ow = (int)(op >> 20);
+      const int ty = row0 + warp + ((int)((op >> 12) & 0xffu) + (int)r) * kBinWarps;
+      const int tx = (int)(op & 0xfffu) + (int)k - (int)r * ow;
+      bool take = pos < total;
+      if (take && bp.mode != 0) take = compact_keeps(bp, ty, tx, mean2d[og], conic_op[og], a_star[og]);
+      const int local = (ty - row0) * bp.tiles_x + tx;
+      const uint32_t peers = __match_any_sync(0xffffffffu, take ? (uint32_t)local : 0xffffffffu);
+      // every lane reads the tile's counter, then the round's first lane of
+      // each tile advances it (no leader search, no broadcast)
+      const int rank = __popc(peers & lt);
+      int base = 0;
+      if (take) base = s_pos[local];
+      __syncwarp();
+      if (take && rank == 0) s_pos[local] = base + __popc(peers);
+      __syncwarp();
+      const int64_t slot = (int64_t)base + rank;
+      if (take && slot < cap) pair_val[slot] = og;
+    }
+  };
+
+  // stages of kBinStage slots; each thread prefetches its slots of the next
+  // stage (Gaussian index, then rectangle) while the current one is walked
+  constexpr int kPer = kBinStage / kBinThreads;
+  uint32_t gq[kPer];
+  int4 rq[kPer];
+  auto prefetch = [&](int64_t sb) {
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int64_t s = sb + q * kBinThreads + tid;
+      gq[q] = s < s_end ? order[s] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) rq[q] = gq[q] != 0xffffffffu ? rect[gq[q]] : make_int4(0, 0, -1, -1);
+  };
+  prefetch(s_begin);
+  for (int64_t sb = s_begin; sb < s_end; sb += kBinStage) {
+    __syncthreads();  // counters initialised / the previous stage walked
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      s_g[q * kBinThreads + tid] = gq[q];
+      s_rect[q * kBinThreads + tid] = rq[q];
+      // row classes (mod kBinWarps) of the rectangle's rows in this group
+      uint32_t cls = 0;
+      const int a = max(rq[q].y, row0) - row0, b = min(rq[q].w, row0 + rows - 1) - row0;
+      if (rq[q].z >= rq[q].x && a <= b) {
+        constexpr uint32_t kAll = kBinWarps == 32 ? 0xffffffffu : (1u << kBinWarps) - 1u;
+        const int nrow = b - a + 1;
+        if (nrow >= kBinWarps) {
+          cls = kAll;
+        } else {
+          const uint64_t run = ((1ull << nrow) - 1ull) << (a % kBinWarps);
+          cls = (uint32_t)(run | (run >> kBinWarps)) & kAll;
+        }
+      }
+      s_cls[q * kBinThreads + tid] = cls;
+    }
+    __syncthreads();
+    if (sb + kBinStage < s_end) prefetch(sb + kBinStage);
+    const int nstage = (int)(s_end - sb < kBinStage ? s_end - sb : kBinStage);
+    int head = 0, queued = 0;
+    for (int j0 = 0; j0 < nstage; j0 += 32) {
+      const bool in = (s_cls[j0 + lane] >> warp) & 1u;
+      const uint32_t mb = __ballot_sync(0xffffffffu, in);
+      if (in) s_queue[warp][(head + queued + __popc(mb & lt)) & 63] = (uint16_t)(j0 + lane);
+      queued += __popc(mb);
+      __syncwarp();
+      if (queued >= 32) {
+        walk(head, 32);
+        head = (head + 32) & 63;
+        queued -= 32;
+      }
+    }
+    if (queued > 0) walk(head, queued);
   }
 }
 
@@ -492,15 +780,64 @@ void launch_inject_bin(sk_ctx* ctx, sk_frame* f) {
   SK_CUDA(cudaGetLastError());
 }
 
-void launch_duplicate(sk_ctx* ctx, sk_frame* f, const uint32_t* order, const int32_t* offsets, uint32_t* pair_tile,
-                      uint32_t* pair_val, int passes, int width, uint32_t* hist, int64_t cap) {
+BinLayout bin_layout(const sk_frame* f) {
+  BinLayout L;
+  L.n = f->n;
+  L.tiles = f->tiles_x * f->tiles_y;
+  // ~8 chunks per SM (measured at config 2); SK_BIN_CHUNK overrides (A/B)
+  static const int64_t forced = [] {
+    const char* e = std::getenv("SK_BIN_CHUNK");
+    return e ? std::atoll(e) : 0ll;
+  }();
+  int64_t chunk = forced > 0 ? forced : (L.n + 8 * 148 - 1) / (8 * 148);
+  chunk = std::max<int64_t>(chunk, 1024);
+  L.chunk = (chunk + kBinStage - 1) / kBinStage * kBinStage;
+  L.rows_per_group = std::max(1, std::min(f->tiles_y, kBinMaxSmemTiles / f->tiles_x));
+  // the scatter packs a tile column and a rectangle width into 12 bits each
+  // and a warp's row index into 8 (tile grids up to 4095 x 4095)
+  require(f->tiles_x < 4096 && f->tiles_y < 4096, "build_tile_grid: at most 4095 x 4095 tiles");
+  return L;
+}
+
+void launch_bin_tiles(sk_ctx* ctx, sk_frame* f, const uint32_t* order, int32_t* counts, uint32_t* pair_val,
+                      int64_t cap) {
   if (f->n == 0) return;
   const BinParams bp = make_bin_params(f);
-  const int64_t warps = (f->n + 31) / 32;
-  const unsigned grid = (unsigned)std::min<int64_t>((warps + kDupThreads / 32 - 1) / (kDupThreads / 32), 148 * 8);
-  duplicate_kernel<<<grid, kDupThreads, 0, ctx->stream>>>(
-      f->n, bp, order, offsets, f->tiles.as<int>(), f->rect.as<int4>(), f->mean2d.as<float2>(),
-      f->conic_op.as<float4>(), f->a_star.as<float>(), pair_tile, pair_val, passes, width, hist, cap);
+  const BinLayout L = bin_layout(f);
+  const dim3 grid((unsigned)((L.n + L.chunk - 1) / L.chunk),
+                  (unsigned)((f->tiles_y + L.rows_per_group - 1) / L.rows_per_group));
+  const size_t smem = sizeof(int32_t) * (size_t)L.rows_per_group * f->tiles_x;
+  static bool attr = false;
+  if (!attr) {
+    SK_CUDA(cudaFuncSetAttribute(bin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 sizeof(int32_t) * kBinMaxSmemTiles));
+    SK_CUDA(cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 sizeof(int32_t) * kBinMaxSmemTiles));
+    attr = true;
+  }
+  if (pair_val)
+    bin_scatter_kernel<<<grid, kBinThreads, smem, ctx->stream>>>(
+        bp, L, order, f->rect.as<int4>(), f->mean2d.as<float2>(), f->conic_op.as<float4>(),
+        f->a_star.as<float>(), counts, f->ranges.as<int2>(), pair_val, cap);
+  else
+    bin_count_kernel<<<grid, kCountThreads, smem, ctx->stream>>>(bp, L, order,
+                                                                 f->rect.as<int4>(), f->mean2d.as<float2>(),
+                                                                 f->conic_op.as<float4>(), f->a_star.as<float>(),
+                                                                 counts);
+  note_launch();
+  SK_CUDA(cudaGetLastError());
+}
+
+int64_t bin_chunks(const sk_frame* f) {
+  const BinLayout L = bin_layout(f);
+  return (L.n + L.chunk - 1) / L.chunk;
+}
+
+void launch_bin_prefix(sk_ctx* ctx, sk_frame* f, int32_t* counts, int32_t* totals, unsigned int* done,
+                       long long* total_out) {
+  const int tiles = f->tiles_x * f->tiles_y;
+  bin_prefix_kernel<<<(unsigned)((tiles + 31) / 32), kPrefixWarps * 32, 0, ctx->stream>>>(
+      counts, (int)bin_chunks(f), tiles, totals, f->ranges.as<int2>(), done, total_out);
   note_launch();
   SK_CUDA(cudaGetLastError());
 }

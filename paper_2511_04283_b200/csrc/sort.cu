@@ -1,14 +1,9 @@
-// K2 scan, K4 onesweep radix sort, K5 tile ranges.
+// K2 depth sort: a onesweep radix sort of (depth key, index) over all slots.
 //
-// Replaces depth_order's std::sort (reference raster.hpp:146-154) and the
-// per-tile push_back lists of build_tile_grid (:157-168). The pipeline is:
-//   depth sort : stable LSD sort of (depth key, index) over all slots;
-//   K2 scan    : exclusive scan of tiles_touched in depth order;
-//   K3         : pairs (tile, index) emitted in (depth, index) order;
-//   K4         : stable LSD sort of the pairs on the tile id only;
-//   K5         : per-tile [begin, end) ranges.
-// Stability of both sorts reproduces the reference's per-tile order
-// (depth ascending, ties by projected index) exactly.
+// Replaces depth_order's std::sort (reference raster.hpp:146-154). The tile
+// lists of build_tile_grid (:157-168) are then built from this order by the
+// counting scatter in preprocess.cu (K3), which keeps the order inside every
+// tile, so each list is (depth ascending, ties by projected index) exactly.
 //
 // The sort is a onesweep LSD radix sort (8-bit digits): one upsweep kernel
 // builds all digit histograms in a single read of the keys; each digit pass
@@ -235,145 +230,21 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
   }
 }
 
-// ---- K2: single-pass exclusive scan with decoupled look-back ---------------
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 4;  // 1024-entry tiles: ~4x the CTAs of 16 items, -4 us on 1M slots
-constexpr int kScanTile = kScanThreads * kScanItems;
-constexpr unsigned long long kSFlagAgg = 1ull << 62;
-constexpr unsigned long long kSFlagInc = 2ull << 62;
-constexpr unsigned long long kSValMask = (1ull << 62) - 1;
-
-__global__ void __launch_bounds__(kScanThreads) scan_gather_kernel(const int32_t* __restrict__ values,
-                                                                   const uint32_t* __restrict__ order,
-                                                                   int32_t* __restrict__ out, int64_t n,
-                                                                   unsigned long long* __restrict__ status,
-                                                                   uint32_t* __restrict__ counter,
-                                                                   long long* __restrict__ total_out) {
-  __shared__ uint32_t s_tile;
-  __shared__ long long s_warp[kScanThreads / 32];
-  __shared__ long long s_prefix;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(counter, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const int64_t base = (int64_t)tile * kScanTile + (int64_t)tid * kScanItems;
-  long long v[kScanItems];
-  long long sum = 0;
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    const int64_t i = base + j;
-    v[j] = (i < n) ? (long long)values[order ? order[i] : i] : 0;
-    sum += v[j];
-  }
-  // block scan of per-thread sums
-  long long x = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const long long y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_warp[warp] = x;
-  __syncthreads();
-  long long wb = 0, block_total = 0;
-  for (int i = 0; i < kScanThreads / 32; ++i) {
-    if (i < warp) wb += s_warp[i];
-    block_total += s_warp[i];
-  }
-  long long thread_excl = wb + x - sum;
-  if (warp == 0) {
-    unsigned long long* my = status + tile;
-    if (tile == 0) {
-      if (lane == 0) {
-        st_relaxed64(my, kSFlagInc | (unsigned long long)block_total);
-        s_prefix = 0;
-      }
-    } else {
-      if (lane == 0) st_relaxed64(my, kSFlagAgg | (unsigned long long)block_total);
-      // warp-wide look-back: lane l reads tile j - l; slots before tile 0
-      // read as an inclusive zero
-      long long excl = 0;
-      int64_t j = (int64_t)tile - 1;
-      for (;;) {
-        const int64_t jj = j - lane;
-        const unsigned long long s = jj >= 0 ? ld_relaxed64(status + jj) : kSFlagInc;
-        const unsigned long long flag = s & ~kSValMask;
-        const uint32_t zero = __ballot_sync(0xffffffffu, flag == 0);
-        const uint32_t inc = __ballot_sync(0xffffffffu, flag == kSFlagInc);
-        const int fz = zero ? __ffs(zero) - 1 : 32;
-        const int fi = inc ? __ffs(inc) - 1 : 32;
-        const int take = fi < fz ? fi + 1 : fz;  // lanes [0, take) are consumed
-        long long v = lane < take ? (long long)(s & kSValMask) : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        excl += v;
-        if (fi < fz) break;
-        j -= take;
-      }
-      if (lane == 0) {
-        st_relaxed64(my, kSFlagInc | (unsigned long long)(excl + block_total));
-        s_prefix = excl;
-      }
-    }
-  }
-  __syncthreads();
-  long long run = s_prefix + thread_excl;
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    const int64_t i = base + j;
-    if (i < n) out[i] = (int32_t)run;
-    run += v[j];
-  }
-  if (total_out && base <= n - 1 && base + kScanItems >= n) *total_out = run;
-}
-
-
-// Tile ranges from the sorted tile ids: a run starts where the id differs
-// from its predecessor. Four ids per thread (uint4 loads), the predecessor of
-// the first from the previous lane.
-__global__ void __launch_bounds__(256) tile_ranges_kernel(const uint32_t* __restrict__ tile, int64_t pairs,
-                                                          int2* __restrict__ ranges) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t i0 = q * 4;
-  const bool full = i0 + 3 < pairs;
-  uint32_t t[4];
-  if (full) {
-    const uint4 v = *reinterpret_cast<const uint4*>(tile + i0);
-    t[0] = v.x, t[1] = v.y, t[2] = v.z, t[3] = v.w;
-  } else {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = i0 + k < pairs ? tile[i0 + k] : 0xffffffffu;
-  }
-  uint32_t prev = __shfl_up_sync(0xffffffffu, t[3], 1);
-  if ((threadIdx.x & 31) == 0) prev = i0 > 0 && i0 - 1 < pairs ? tile[i0 - 1] : 0xffffffffu;
-  if (i0 >= pairs) return;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int64_t i = i0 + k;
-    if (i >= pairs) break;
-    const uint32_t p = k == 0 ? prev : t[k - 1];
-    if (i == 0 || p != t[k]) {
-      ranges[t[k]].x = (int)i;
-      if (i > 0) ranges[p].y = (int)i;
-    }
-    if (i == pairs - 1) ranges[t[k]].y = (int)(i + 1);
-  }
-}
-
 }  // namespace
 
-uint32_t* radix_hist_buffer(sk_ctx* ctx) { return ensure<uint32_t>(ctx->sort.hist, (size_t)kMaxPasses * kRadix); }
-
+namespace {
 int radix_passes(int bits) { return (bits + kRadixBits - 1) / kRadixBits; }
 
-// Digits are split evenly over the passes (13 tile bits -> 7 + 6): fewer
-// buckets per pass means longer digit runs and better-coalesced scatters.
+// Digits are split evenly over the passes: fewer buckets per pass means
+// longer digit runs and better-coalesced scatters.
 int radix_digit_width(int bits) {
   const int passes = radix_passes(bits);
   return (bits + passes - 1) / passes;
 }
+}  // namespace
 
 void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_t*& vals, uint32_t*& vals_alt,
-                      int64_t n, int bits, bool hist_ready) {
+                      int64_t n, int bits) {
   if (n <= 1 || bits <= 0) return;
   const int passes = radix_passes(bits);
   const int width = radix_digit_width(bits);
@@ -383,17 +254,15 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
   const int tile_keys = kSortThreads * kSortItems;
   const int64_t tiles = (n + tile_keys - 1) / tile_keys;
   require(tiles < (1ll << 31), "radix_sort_pairs: too many keys");
-  uint32_t* hist = radix_hist_buffer(ctx);
+  uint32_t* hist = ensure<uint32_t>(ctx->sort.hist, (size_t)kMaxPasses * kRadix);
   uint32_t* status = ensure<uint32_t>(ctx->sort.status, (size_t)tiles * kRadix);
   uint32_t* counters = ensure<uint32_t>(ctx->sort.counters, kMaxPasses);
   cudaStream_t s = ctx->stream;
   SK_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * kMaxPasses, s));
-  if (!hist_ready) {
-    SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s));
-    const int hist_blocks = (int)std::min<int64_t>((n + 4095) / 4096, 148 * 8);
-    radix_hist_kernel<<<hist_blocks, 256, 0, s>>>(keys, n, passes, width, hist);
-    note_launch();
-  }
+  SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s));
+  const int hist_blocks = (int)std::min<int64_t>((n + 4095) / 4096, 148 * 8);
+  radix_hist_kernel<<<hist_blocks, 256, 0, s>>>(keys, n, passes, width, hist);
+  note_launch();
   radix_bases_kernel<<<passes, kRadix, 0, s>>>(hist);
   note_launch();
   for (int p = 0; p < passes; ++p) {
@@ -404,49 +273,6 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
     std::swap(keys, keys_alt);
     std::swap(vals, vals_alt);
   }
-  SK_CUDA(cudaGetLastError());
-}
-
-const long long* launch_scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets,
-                                      int64_t n) {
-  if (n == 0) return nullptr;
-  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
-  auto* status = ensure<unsigned long long>(ctx->sort.scan_status, (size_t)tiles + 1);
-  auto* total = ensure<long long>(ctx->sort.scan_total, 2);
-  uint32_t* counter = reinterpret_cast<uint32_t*>(total + 1);
-  cudaStream_t s = ctx->stream;
-  SK_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)tiles, s));
-  SK_CUDA(cudaMemsetAsync(total, 0, sizeof(long long) * 2, s));
-  scan_gather_kernel<<<(unsigned)tiles, kScanThreads, 0, s>>>(values, order, offsets, n, status, counter, total);
-  note_launch();
-  SK_CUDA(cudaGetLastError());
-  if (!ctx->count_stream) {
-    SK_CUDA(cudaStreamCreateWithFlags(&ctx->count_stream, cudaStreamNonBlocking));
-    SK_CUDA(cudaEventCreateWithFlags(&ctx->count_ev, cudaEventDisableTiming));
-  }
-  auto* host = static_cast<long long*>(ctx->count_pinned.ensure(sizeof(long long)));
-  SK_CUDA(cudaEventRecord(ctx->count_ev, s));
-  SK_CUDA(cudaStreamWaitEvent(ctx->count_stream, ctx->count_ev, 0));
-  SK_CUDA(cudaMemcpyAsync(host, total, sizeof(long long), cudaMemcpyDeviceToHost, ctx->count_stream));
-  return total;
-}
-
-int64_t read_scan_total(sk_ctx* ctx, const long long* total) {
-  if (!total) return 0;
-  SK_CUDA(cudaStreamSynchronize(ctx->count_stream));
-  return *static_cast<const long long*>(ctx->count_pinned.ptr);
-}
-
-int64_t scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets, int64_t n) {
-  return read_scan_total(ctx, launch_scan_gathered(ctx, values, order, offsets, n));
-}
-
-
-void launch_tile_ranges(sk_ctx* ctx, const uint32_t* pair_tile, int64_t pairs, int2* ranges, int tiles) {
-  SK_CUDA(cudaMemsetAsync(ranges, 0, sizeof(int2) * tiles, ctx->stream));
-  if (pairs == 0) return;
-  tile_ranges_kernel<<<(unsigned)((pairs + 1023) / 1024), 256, 0, ctx->stream>>>(pair_tile, pairs, ranges);
-  note_launch();
   SK_CUDA(cudaGetLastError());
 }
 

@@ -13,8 +13,9 @@ struct SortTemp {
   DevBuf hist;      // [passes][256] digit counts, then exclusive bases
   DevBuf status;    // [tiles][256] look-back words
   DevBuf counters;  // tile tickets, one per pass
-  DevBuf scan_status;
-  DevBuf scan_total;
+  DevBuf bin_counts;  // int32 [chunks][tiles] (K3 counting scatter)
+  DevBuf bin_totals;  // int32 [tiles]
+  DevBuf bin_total;   // long long [2]: P, then the prefix kernel's done-counter
 };
 
 }  // namespace sk
@@ -90,7 +91,7 @@ struct sk_ctx {
   sk::DevBuf pge;       // uint64 [2] workload counters (sk_frame_pge_counts)
   sk::DevBuf loss_blocks;  // double [blocks][3] per-block loss sums (deterministic reduction)
   sk::HostBuf pinned;   // staging
-  // pair-count readback (sort.cu read_scan_total): copied on its own stream
+  // pair-count readback (pipeline.cu bin_sort): copied on its own stream
   // after the scan, so the host waits for the scan only, not for the
   // speculative K3 queued behind it
   cudaStream_t count_stream = nullptr;
@@ -164,9 +165,7 @@ struct sk_frame {
 
   // K2-K5
   sk::DevBuf keys_a, keys_b, vals_a, vals_b;  // depth sort ping-pong (K1 fills keys_a / vals_a)
-  sk::DevBuf offsets;                         // int32 [n]
-  sk::DevBuf ptile_a, ptile_b, pval_a, pval_b; // pair sort ping-pong
-  uint32_t* pair_tile = nullptr;              // sorted result pointers
+  sk::DevBuf pval_a;                          // uint32 [P] tile lists (Gaussian indices)
   uint32_t* pair_val = nullptr;
   sk::DevBuf ranges;                          // int2 [tiles]
 
@@ -203,30 +202,22 @@ inline int64_t round_capacity(int64_t n) { return ((n < 1 ? 1 : n) + 31) & ~int6
 // preprocess.cu
 void launch_preprocess(sk_ctx* ctx, const sk_scene* scene, const sk_camera& cam, sk_frame* f);
 void launch_inject_bin(sk_ctx* ctx, sk_frame* f);
-// Also accumulates the digit counts of the tile-id radix sort (passes digit
-// passes) into hist (see radix_hist_buffer), so the sort can skip its upsweep.
-// Pairs at positions >= cap are not written (speculative launch before the
-// pair count is known on the host; see bin_sort).
-void launch_duplicate(sk_ctx* ctx, sk_frame* f, const uint32_t* order, const int32_t* offsets, uint32_t* pair_tile,
-                      uint32_t* pair_val, int passes, int width, uint32_t* hist, int64_t cap);
+// K3 tile binning (counting scatter): pair_val == nullptr counts pairs per
+// (chunk, tile) into counts; otherwise scatters the Gaussian indices into
+// pair_val (slots >= cap are not written). Both need the depth order.
+void launch_bin_tiles(sk_ctx* ctx, sk_frame* f, const uint32_t* order, int32_t* counts, uint32_t* pair_val,
+                      int64_t cap);
+// counts -> exclusive prefix over chunks; ranges and P (*total_out) from the
+// tile totals. done: a zeroed counter (reset by the kernel).
+void launch_bin_prefix(sk_ctx* ctx, sk_frame* f, int32_t* counts, int32_t* totals, unsigned int* done,
+                       long long* total_out);
+int64_t bin_chunks(const sk_frame* f);
 
 // sort.cu
 // Stable LSD radix sort of (key, value) pairs on key bits [0, bits). On
 // return keys/vals point at the sorted data (pointers may be swapped).
-// hist_ready: the digit counts are already in radix_hist_buffer(ctx).
 void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_t*& vals, uint32_t*& vals_alt,
-                      int64_t n, int bits, bool hist_ready = false);
-uint32_t* radix_hist_buffer(sk_ctx* ctx);  // [4][256] digit counts
-int radix_passes(int bits);
-int radix_digit_width(int bits);  // bits per digit pass (even split)
-// Exclusive scan of tiles[order[i]] into offsets[i]; returns the total.
-int64_t scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets, int64_t n);
-// The same split in two: the launch (total left on the device) and the
-// blocking read of the total.
-const long long* launch_scan_gathered(sk_ctx* ctx, const int32_t* values, const uint32_t* order, int32_t* offsets,
-                                      int64_t n);
-int64_t read_scan_total(sk_ctx* ctx, const long long* total);
-void launch_tile_ranges(sk_ctx* ctx, const uint32_t* pair_tile, int64_t pairs, int2* ranges, int tiles);
+                      int64_t n, int bits);
 
 // rasterize.cu
 // fast: the MUFU-exp blend of training steps (rasterize.cu); K8 follows the
