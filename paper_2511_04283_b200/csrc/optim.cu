@@ -10,8 +10,9 @@
 //
 // K9 runs one thread per Gaussian (zero gradients when culled) and writes the
 // gradients through a shared-memory tile; K10 streams params / m / v / grads
-// with float4 accesses at ~92% of the HBM copy roof. Fusing the two was
-// measured 2.3x slower: Adam would run at K9's occupancy.
+// with float4 accesses at ~92% of the HBM copy roof. On one GPU with dense
+// Adam the two run fused (project_bwd_adam_kernel): the gradients never
+// leave the CTA's tile.
 #include "state.h"
 
 namespace sk {
@@ -453,6 +454,115 @@ __global__ void __launch_bounds__(kAdamThreads) adam_kernel(float* __restrict__ 
   }
 }
 
+// K9 + K10 fused (one GPU, dense Adam): the gradients of a CTA's 128
+// Gaussians stay in its shared-memory tile and are consumed there by the
+// Adam update of the same Gaussians, so the 59-component gradient buffer is
+// neither written nor re-read (2 x 236 B per Gaussian) and the parameters
+// the projection backward just read are re-read from L2. Phase 2 streams
+// params / m / v as float4 rows (32 lanes x 4 Gaussians = one component row
+// of the tile; the four warps take four components, kAdamUnroll rows in
+// flight each), so the Adam half runs at HBM rate while the latency-bound
+// gradient half of the other resident CTAs overlaps it. Bit-identical to
+// K9 followed by K10: the same per-Gaussian gradient code and the same
+// adam_update in the same order.
+constexpr int kAdamUnroll = 4;  // rows in flight per warp (measured: 2 and 6 slower)
+template <int DEG>
+__global__ void __launch_bounds__(kPbThreads, kK9MinBlocks) project_bwd_adam_kernel(
+    float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ radius,
+    const float4* __restrict__ conic4, const float* __restrict__ bg, int64_t gstride, float* __restrict__ am,
+    float* __restrict__ av, AdamParams ap, Stats st, bool do_stats, const uint32_t* __restrict__ err) {
+  constexpr int NC = 11 + 3 * (DEG + 1) * (DEG + 1);
+  if (__ldg(err)) return;  // see project_bwd_kernel
+  __shared__ __align__(16) float s_grad[NC * kPbThreads];
+  __shared__ float s_exp2[64];
+  // per component: (lr, bc1, bc2, active): group lookups off the param struct
+  __shared__ float4 s_adam[NC];
+  if (threadIdx.x < NC) {
+    const int gi = comp_group(threadIdx.x);
+    s_adam[threadIdx.x] = make_float4(ap.lr[gi], ap.bc1[gi], ap.bc2[gi], ap.active[gi] ? 1.0f : 0.0f);
+  }
+  const int64_t i0 = (int64_t)blockIdx.x * kPbThreads;
+  const int64_t i = i0 + threadIdx.x;
+  stage_exp2_table(s_exp2);
+  __syncthreads();
+  float* g = s_grad + threadIdx.x;
+  if (i < n) {
+#pragma unroll
+    for (int c = 0; c < 11; ++c) asm volatile("prefetch.global.L1 [%0];" ::"l"(bg + c * gstride + i));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(conic4 + i));
+#pragma unroll
+    for (int c = 0; c < NC; ++c) asm volatile("prefetch.global.L1 [%0];" ::"l"(params + c * stride + i));
+    if (do_stats) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(st.grad_norm_acc + i));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(st.abs_grad_acc + i));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(st.views_seen + i));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(st.max_radius2d + i));
+#pragma unroll
+      for (int k = 0; k < 3; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(st.grad3d_acc + k * stride + i));
+    }
+    const float rad = radius[i];
+    if (rad > 0.0f) {
+      float dmu2d[2], dcov[2][2], dcol[3], dop, absg[2];
+      load_blend(bg, gstride, i, dmu2d, dcov, conic4[i], dcol, dop, absg);
+      project_backward_one<DEG, kPbThreads>(params, stride, i, cam, dmu2d, dcov, dcol, dop, g, s_exp2);
+      if (do_stats) {
+        const float gmu[3] = {g[0], g[kPbThreads], g[2 * kPbThreads]};
+        accumulate_stats(st, i, stride, dmu2d, absg, gmu, rad, (float)cam.width / 2.0f, (float)cam.height / 2.0f);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) g[c * kPbThreads] = 0.0f;
+    }
+  }
+  __syncthreads();
+  // phase 2: Adam over the tile, component rows as float4 along the Gaussians
+  const int nloc = (int)(n - i0 < kPbThreads ? n - i0 : kPbThreads);
+  const int q = threadIdx.x & 31, wq = threadIdx.x >> 5;  // float4 column, warp
+  const int e0 = q * 4;                                     // first Gaussian of the column
+  const bool full = e0 + 3 < nloc;
+  constexpr int kWarps = kPbThreads / 32;
+  for (int cb = 0; cb < NC; cb += kWarps * kAdamUnroll) {
+    float4 P[kAdamUnroll], M[kAdamUnroll], V[kAdamUnroll];
+#pragma unroll
+    for (int u = 0; u < kAdamUnroll; ++u) {
+      const int c = cb + wq + kWarps * u;
+      if (c < NC && full && s_adam[c].w != 0.0f) {
+        const int64_t o = (int64_t)c * stride + i0 + e0;
+        P[u] = *reinterpret_cast<const float4*>(params + o);
+        M[u] = __ldcs(reinterpret_cast<const float4*>(am + o));
+        V[u] = __ldcs(reinterpret_cast<const float4*>(av + o));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kAdamUnroll; ++u) {
+      const int c = cb + wq + kWarps * u;
+      if (c >= NC) continue;
+      const float4 hp = s_adam[c];
+      if (hp.w == 0.0f) continue;
+      const float lr = hp.x, bc1 = hp.y, bc2 = hp.z;
+      const int64_t o = (int64_t)c * stride + i0 + e0;
+      if (full) {
+        const float4 G = *reinterpret_cast<const float4*>(s_grad + c * kPbThreads + e0);
+        adam_update(P[u].x, M[u].x, V[u].x, G.x, lr, bc1, bc2);
+        adam_update(P[u].y, M[u].y, V[u].y, G.y, lr, bc1, bc2);
+        adam_update(P[u].z, M[u].z, V[u].z, G.z, lr, bc1, bc2);
+        adam_update(P[u].w, M[u].w, V[u].w, G.w, lr, bc1, bc2);
+        *reinterpret_cast<float4*>(params + o) = P[u];
+        __stcs(reinterpret_cast<float4*>(am + o), M[u]);
+        __stcs(reinterpret_cast<float4*>(av + o), V[u]);
+      } else {
+        for (int e = 0; e < 4 && e0 + e < nloc; ++e) {
+          float p = params[o + e], m = am[o + e], v = av[o + e];
+          adam_update(p, m, v, s_grad[c * kPbThreads + e0 + e], lr, bc1, bc2);
+          params[o + e] = p;
+          am[o + e] = m;
+          av[o + e] = v;
+        }
+      }
+    }
+  }
+}
+
 AdamParams make_adam(sk_scene* s, const LearningRates& lrs, float position_lr, bool update_sh_rest) {
   AdamParams ap;
   const float lr[6] = {position_lr, lrs.rotation, lrs.scale, lrs.opacity, lrs.sh_dc, lrs.sh_rest};
@@ -728,14 +838,30 @@ void reset_opacity_state(sk_ctx* ctx, sk_scene* s) {
   SK_CUDA(cudaMemsetAsync(s->adam_v.as<float>() + o, 0, sizeof(float) * s->capacity, ctx->stream));
 }
 
-// Single-GPU step: K9 into the gradient buffer, then the streaming K10. (A
-// single fused kernel keeps the gradients on chip but is instruction-bound at
-// the occupancy its 59-gradient live range allows; split, K10 runs at HBM
-// bandwidth.)
+// Single-GPU step: K9 and K10 fused (project_bwd_adam_kernel). The gradient
+// buffer is not written.
 void launch_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const LearningRates& lrs, float position_lr,
                                   bool update_sh_rest, bool do_stats) {
-  launch_project_backward(ctx, s, f, do_stats);
-  launch_adam(ctx, s, lrs, position_lr, update_sh_rest);
+  ensure_optimizer_state(ctx, s);
+  require(s->capacity % 4 == 0, "adam: scene capacity must be a multiple of 4");
+  const AdamParams ap = make_adam(s, lrs, position_lr, update_sh_rest);
+  if (s->n == 0) return;
+  const CamParams cp = make_cam_params(f->camera);
+  const unsigned grid = (unsigned)((s->n + kPbThreads - 1) / kPbThreads);
+  auto go = [&](auto kern) {
+    kern<<<grid, kPbThreads, 0, ctx->stream>>>(s->params.as<float>(), s->capacity, s->n, cp, f->radius.as<float>(),
+                                               f->conic4.as<float4>(), f->bgrads.as<float>(), f->n,
+                                               s->adam_m.as<float>(), s->adam_v.as<float>(), ap, make_stats(s),
+                                               do_stats, ctx->err_word.as<uint32_t>());
+  };
+  switch (s->sh_degree) {
+    case 0: go(project_bwd_adam_kernel<0>); break;
+    case 1: go(project_bwd_adam_kernel<1>); break;
+    case 2: go(project_bwd_adam_kernel<2>); break;
+    default: go(project_bwd_adam_kernel<3>); break;
+  }
+  note_launch();
+  SK_CUDA(cudaGetLastError());
 }
 
 }  // namespace sk

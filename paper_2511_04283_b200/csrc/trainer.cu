@@ -146,10 +146,16 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   const float pos_lr = expon_lr(lrs.position * extent, lrs.position_final * extent, it, cfg.iterations);
   int64_t adam_t0[6];
   std::copy(scene->adam_t, scene->adam_t + 6, adam_t0);
-  // K9 into the gradient buffer (+ C1 over the ranks of a view-parallel
-  // step), then K10
-  launch_project_backward(ctx, scene, f, true);
+  // One GPU, dense Adam: K9 and K10 fused (the gradients stay on chip; the
+  // K9 / K10 phase boundary is then empty). Otherwise K9 into the gradient
+  // buffer (+ C1 over the ranks of a view-parallel step), then K10.
   sk_comm* c1 = const_cast<sk_comm*>(comm);
+  const bool multi = comm && comm->world > 1;
+  if (!multi && !cfg.lazy_opt_enabled) {
+    launch_project_backward_adam(ctx, scene, f, lrs, pos_lr, true, true);
+    ctx->mark(6);
+  } else {
+  launch_project_backward(ctx, scene, f, true);
   const bool sharded = !cfg.lazy_opt_enabled && c1_sharded(comm, scene);
   if (sharded) {
     reduce_scatter_grads(c1, scene, ctx->stream);
@@ -169,6 +175,7 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
     // stepped on the accumulated gradient when lazy_update_due
     launch_adam(ctx, scene, lrs, pos_lr, false);
     lazy_sh_rest(ctx, scene, lrs, lazy_update_due(it, cfg));
+  }
   }
   ctx->mark(7);
   if (pend) {

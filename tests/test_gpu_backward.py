@@ -179,6 +179,34 @@ def test_adam_bit_exact_and_fused_equivalence(ctx, orc):
     assert rel_err_vec(p2 - p, p1 - p).max() < TOL
 
 
+@pytest.mark.parametrize("deg,n,sh_rest", [(3, 301, True), (3, 1000, False), (0, 257, True), (1, 130, True)])
+def test_fused_k9_k10_bit_identical(ctx, orc, deg, n, sh_rest):
+    """The fused K9+K10 kernel (one GPU, dense Adam) against K9 then K10 from
+    the same blend gradients and state: parameters, moments, step counters and
+    ScoreTable statistics bit-identical (ragged float4 / CTA tails included)."""
+    import paper_2511_04283_b200 as sk
+    rng = np.random.default_rng(11 + n)
+    p = random_scene(rng, n, deg)
+    cam = orc.default_camera(64, 48)
+    lrs = sk.default_learning_rates()
+    a = ctx.scene(p, deg)
+    b = ctx.scene(p, deg)
+    ctx.preprocess(a, cam)
+    ctx.blend_forward()
+    ctx.blend_backward(rng.uniform(-1, 1, (48, 64, 3)).astype(np.float32))
+    for step in range(2):  # the second step starts from non-zero moments
+        ctx.project_backward(a, stats=True)
+        ctx.adam_step(a, lrs, position_lr=np.float32(1.6e-4), update_sh_rest=sh_rest)
+        ctx.project_backward_adam(b, lrs, position_lr=np.float32(1.6e-4), update_sh_rest=sh_rest, stats=True)
+    assert np.array_equal(a.download(), b.download())
+    ma, va, ta = a.adam_state()
+    mb, vb, tb = b.adam_state()
+    assert np.array_equal(ma, mb) and np.array_equal(va, vb) and list(ta) == list(tb)
+    sa, sb = a.score_table(), b.score_table()
+    for f in ("grad_norm_acc", "abs_grad_acc", "grad3d_acc", "views_seen", "max_radius2d"):
+        assert np.array_equal(getattr(sa, f), getattr(sb, f)), f
+
+
 def test_train_step_matches_oracle(ctx, orc):
     """One full train_iteration (trainer.hpp:124-175) vs the oracle on the same view."""
     import paper_2511_04283_b200 as sk
