@@ -1,15 +1,32 @@
-// K7: fused L1 + D-SSIM loss forward and backward.
+// K7: fused L1 + D-SSIM loss forward and backward, one kernel.
 //
 // Restates training_loss (reference loss.hpp:21-47) and ssim_with_grad
 // (metrics.hpp:93-122): 11-tap separable Gaussian (sigma 1.5, normalised
-// weights), zero padding without renormalisation at the borders
-// (metrics.hpp:30-52), per-channel SSIM map, and the analytic gradient
-//   g = filt(u_mu) + filt(u_mxy) * y + filt(u_mxx) * 2 x.
-// Two kernels over 32x32 pixel tiles with a 5-pixel halo staged in shared
-// memory: kernel A filters the five moments (x, y, x^2, y^2, xy) of each
-// channel, forms the SSIM map and the three per-pixel partials, and reduces
-// the L1 / SSIM / squared-error sums; kernel B filters the partials and
-// writes dL/dimage = (1 - lambda) sign(r - g) / 3HW - lambda g.
+// weights), horizontal then vertical pass, zero padding without
+// renormalisation at the borders (gauss_filter, metrics.hpp:30-52),
+// per-channel SSIM map, and the analytic gradient
+//   g = filt(u_mu) + filt(u_mxy) * y + filt(u_mxx) * 2 x,
+//   dL/dimage = (1 - lambda) sign(x - y) / 3HW - lambda g.
+//
+// Strip marching: a CTA owns one channel, a strip of kSW output columns and a
+// range of rows, and walks down the rows kRB at a time. Per step it
+//   (1) stages kRB input rows (x and the 8-bit GT decoded byte/255) over the
+//       strip plus a 10-column halo each side (prefetched into registers one
+//       step ahead),
+//   (2) filters them horizontally into the five moments (x, y, x^2, y^2, xy)
+//       of kSW + 10 columns, kept in an 18-row shared ring,
+//   (3) filters the ring vertically into the moments of kRB centre rows
+//       (5 rows behind), forms the SSIM map and the three per-pixel partials
+//       (zero outside the image: the adjoint filter zero-pads them),
+//   (4) filters the partials horizontally into a second 18-row ring, and
+//   (5) filters that ring vertically into g for kRB output rows (10 rows
+//       behind the input) and writes dL/dimage once.
+// Nothing but the image, the GT and dL/dimage touches HBM (the two-kernel
+// version wrote and re-read nine partial planes), and the only recomputation
+// is the 10-column horizontal halo of the moments (kSW + 10 of kSW) and 20
+// lead-in rows per CTA. Shared planes are planar fp32 with one pad word per
+// 32 columns, so the 4-outputs-per-thread sliding windows (lane stride 4
+// words) are bank-conflict free.
 // This file is compiled with FMA contraction on: nothing here feeds the
 // bit-exact binning path, and the loss is checked against the oracle within
 // a tolerance.
@@ -18,23 +35,40 @@
 namespace sk {
 namespace {
 
-// 32x32 output tiles (measured 11% faster than 32x16: the 10-row halo of the
-// horizontal pass is amortised over twice the rows)
-
-
-constexpr int kTX = 32;                 // output tile width
-constexpr int kTY = 32;                 // output tile height
-constexpr int kHalo = 5;                // 11-tap window
-constexpr int kInX = kTX + 2 * kHalo;   // 42
-constexpr int kInY = kTY + 2 * kHalo;   // 26
-constexpr int kHX = 4;                  // horizontal outputs per thread (register sliding window)
-constexpr int kVY = kTX * kTY / 256;    // vertical outputs per thread (256 threads)
-// Vectorised halo staging: the 4-aligned window [x0 - 8, x0 + 40) covers the
-// halo [x0 - 5, x0 + 37) in 12 quads per row.
-constexpr int kQuadLead = 8;
-constexpr int kQuads = (kTX + 2 * kQuadLead) / 4;
+constexpr int kThreads = 256;
+constexpr int kSW = 118;             // output columns per strip
+constexpr int kMW = kSW + 10;        // 128 moment / partial columns
+constexpr int kIW = kSW + 20;        // 138 input columns
+constexpr int kRB = 8;               // rows per step
+constexpr int kRing = kRB + 10;      // rows a vertical 11-tap pass over kRB outputs reads
+constexpr int kLoadIters = (kIW + 31) / 32;  // 5 column passes of a warp over one input row
+// Shared planes (no padding words). The horizontal passes give each thread 4
+// adjacent outputs (lane stride 4 elements); a warp covers 4 rows x 8 column
+// groups, and every row pitch is odd, so the 16 lanes of a half-warp (64-bit
+// accesses) and the 32 lanes of a warp (32-bit) hit distinct banks. The
+// vertical passes read consecutive columns of one row.
+constexpr int kPI = 139;   // input ring, float2 (x, y): >= kIW
+constexpr int kPM = 129;   // moment / filtered-partial rings: >= kMW
+constexpr int kPS = 139;   // partial rows: stage 4 reads up to column 4 * 31 + 13
+// shared layout in floats
+constexpr int kOffIn = 0;                                // float2 [kRing][kPI]
+constexpr int kOffMA = kOffIn + 2 * kRing * kPI;         // float4 (mu_x, mu_y, E x^2, E y^2) [kRing][kPM]
+constexpr int kOffMC = kOffMA + 4 * kRing * kPM;         // float E xy [kRing][kPM]
+constexpr int kOffPA = kOffMC + kRing * kPM;             // float2 (u_mu, u_mxy) [kRB][kPS]
+constexpr int kOffPB = kOffPA + 2 * kRB * kPS;           // float u_mxx [kRB][kPS]
+constexpr int kOffHA = kOffPB + kRB * kPS;               // float2 filtered (u_mu, u_mxy) [kRing][kPM]
+constexpr int kOffHB = kOffHA + 2 * kRing * kPM;         // float filtered u_mxx [kRing][kPM]
+constexpr int kOffU8 = kOffHB + kRing * kPM;             // [256] byte / 255
+constexpr int kSmemFloats = kOffU8 + 256;
+constexpr size_t kSmemBytes = sizeof(float) * kSmemFloats + 8 * sizeof(double);
+static_assert(kOffMA % 4 == 0 && kOffPA % 2 == 0 && kOffHA % 2 == 0, "float2 planes");
+static_assert(kSmemFloats % 2 == 0, "double reduction scratch alignment");
+static_assert(kSmemBytes <= 113 * 1024, "two CTAs per SM");
 
 __constant__ float c_gauss[11];
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ int ring(int r) { return r >= kRing ? r - kRing : r; }
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -48,161 +82,292 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return s;
 }
 
-__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+// One window of 14 consecutive ring rows starting at slot s of a plane with
+// row pitch P: rows before the wrap are addressed from lo, the rest from
+// lo - kRing rows (one compare + select per tap instead of a modulo).
+template <typename T, int P>
+struct RingWin {
+  const T* lo;
+  const T* hi;
+  int wrap;
+  __device__ __forceinline__ RingWin(const T* plane_col, int s) {
+    lo = plane_col + s * P;
+    hi = lo - kRing * P;
+    wrap = kRing - s;
+  }
+  __device__ __forceinline__ T operator()(int k) const { return (k < wrap ? lo : hi)[k * P]; }
+};
 
-// Kernel A (per 32x32 output tile and channel, 256 threads): stage x and
-// y interleaved as float2 with a 5-pixel zero halo; horizontal pass with a
-// register sliding window (4 adjacent outputs per thread) producing the five
-// moments as two packed pairs (mu_x, mu_y), (E[x^2], E[y^2]) and E[xy] — one
-// FFMA2 per pair per tap instead of two FFMAs; vertical pass the same way, 4
-// outputs per thread; SSIM map and the three per-pixel partials of
-// ssim_with_grad (metrics.hpp:104-114).
-// partials: planar [3 maps][3 ch][H][W]; also writes the L1 part of
-// dL/dimage into dimage (planar [3][H][W]).
-__global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ img, const void* __restrict__ gt,
-                                                       bool gt_u8, int W, int H, float nrm, float lambda,
-                                                       float inv_n, bool want_grad, float* __restrict__ partials,
-                                                       float* __restrict__ dimage, double* __restrict__ sums,
-                                                       double* __restrict__ block_sums,
-                                                       unsigned int* __restrict__ ticket) {
-  __shared__ float2 s_xy[kInY][kInX + 1];
-  __shared__ float2 s_h2[2][kInY][kTX + 1];  // (mu_x, mu_y), (E x^2, E y^2) after the horizontal pass
-  __shared__ float s_h1[kInY][kTX + 1];      // E xy
-  __shared__ float s_u8[256];
-  __shared__ double s_red[8];
-  const int tx0 = blockIdx.x * kTX, ty0 = blockIdx.y * kTY;
+// GRAD = false: loss / SSIM / PSNR sums only (stages 1-3). U8: GT is 8-bit
+// HWC (decoded byte / 255, png_io.cpp:64), else fp32 HWC.
+// grid (strips, row ranges, 3 channels); rows_per_cta output rows per CTA.
+template <bool GRAD, bool U8>
+__global__ void __launch_bounds__(kThreads, 2)
+    ssim_march_kernel(const float* __restrict__ img, const void* __restrict__ gt, int W, int H,
+                      int rows_per_cta, float nrm, float lambda, float inv_n, float* __restrict__ dimage,
+                      double* __restrict__ sums, double* __restrict__ block_sums, unsigned int* __restrict__ ticket) {
+  extern __shared__ float4 smem_f4[];
+  float* sm = reinterpret_cast<float*>(smem_f4);
+  float2* s_in = reinterpret_cast<float2*>(sm + kOffIn);
+  float4* m_ab = reinterpret_cast<float4*>(sm + kOffMA);
+  float* m_c = sm + kOffMC;
+  float2* p_a = reinterpret_cast<float2*>(sm + kOffPA);
+  float* p_b = sm + kOffPB;
+  float2* h_a = reinterpret_cast<float2*>(sm + kOffHA);
+  float* h_b = sm + kOffHB;
+  float* s_u8 = sm + kOffU8;
+  double* s_red = reinterpret_cast<double*>(sm + kSmemFloats);
   const int t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
+  const int ch = blockIdx.z;
+  const int x0 = blockIdx.x * kSW;
+  const int r0 = blockIdx.y * rows_per_cta;
+  const int r_end = min(r0 + rows_per_cta, H);
+  constexpr int kLag = GRAD ? 10 : 5;  // input rows ahead of the last stage's output rows
+  const int rs = r0 - kLag;            // first input row (ring slot 0)
   const size_t plane = (size_t)W * H;
-  // byte / 255.0f (png_io.cpp:64) as a table: one exact division per value
-  for (int i = t; i < 256; i += blockDim.x) s_u8[i] = __fdiv_rn((float)i, 255.0f);
-  // vertical-pass ownership: column vx, rows vy0 .. vy0 + kVY - 1
-  const int vx = t % kTX, vy0 = (t / kTX) * kVY;
+  const float* xin = img + ch * plane;
+  const uint8_t* gt8 = static_cast<const uint8_t*>(gt);
+  const float* gtf = static_cast<const float*>(gt);
+  for (int i = t; i < 256; i += kThreads) s_u8[i] = __fdiv_rn((float)i, 255.0f);
   double l1 = 0.0, ss = 0.0, sq = 0.0;
-  {
-    const int ch = blockIdx.z;  // one channel per CTA: three times the CTAs in flight
-    __syncthreads();
-    if ((W & 3) == 0 && gt_u8) {
-      // Rows of four pixels at a time: with W % 4 == 0 every 4-aligned quad
-      // lies entirely inside or outside the image (zero padding), the image
-      // quad is one float4 and the GT quad's 12 bytes three aligned words.
-      for (int i = t; i < kInY * kQuads; i += blockDim.x) {
-        const int iy = i / kQuads, q = i % kQuads;
-        const int gy = ty0 - kHalo + iy, gx0 = tx0 - kQuadLead + 4 * q;
-        float4 xv = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        float yv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-        if (gy >= 0 && gy < H && gx0 >= 0 && gx0 < W) {
-          const size_t p = (size_t)gy * W + gx0;
-          xv = *reinterpret_cast<const float4*>(img + ch * plane + p);
-          const uint32_t* wq = reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(gt) + p * 3);
-          const uint32_t w3[3] = {wq[0], wq[1], wq[2]};
+  // horizontal passes: warp covers rows 4 (w & 1) .. + 3 x column groups
+  // 8 (w >> 1) .. + 7 (4 outputs per group)
+  const int h_row = 4 * (warp & 1) + ((lane >> 2) & 3);
+  const int h_grp = 8 * (warp >> 1) + (lane & 3) + 4 * (lane >> 4);
+
+  // (1) staging: warp w loads block row w, lane l columns l + 32k of the
+  // kIW-column window. Column validity and ownership do not change along
+  // the march.
+  unsigned col_ok = 0u, col_own = 0u;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int b = 3 * j + ch;
-            yv[j] = s_u8[(w3[b >> 2] >> (8 * (b & 3))) & 0xffu];
-          }
-        }
-        const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+  for (int k = 0; k < kLoadIters; ++k) {
+    const int gx = x0 - 10 + lane + 32 * k;
+    if (lane + 32 * k < kIW && gx >= 0 && gx < W) {
+      col_ok |= 1u << k;
+      if (gx >= x0 && gx < x0 + kSW) col_own |= 1u << k;
+    }
+  }
+  // prefetch of one block into registers (raw GT bytes: decoding them here
+  // would wait for the loads)
+  float pf_x[kLoadIters];
+  uint32_t pf_y[kLoadIters];
+  auto prefetch = [&](int y0) {
+    const int gy = y0 + warp;
+    const bool row_ok = gy >= 0 && gy < H;
+    const size_t p0 = (size_t)(row_ok ? gy : 0) * W + (x0 - 10 + lane);
+    const float* xp = xin + p0;
+    const uint8_t* yp8 = gt8 + p0 * 3 + ch;
+    const float* ypf = gtf + p0 * 3 + ch;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int ix = 4 * q + j - (kQuadLead - kHalo);
-          if (ix >= 0 && ix < kInX) s_xy[iy][ix] = make_float2(xs[j], yv[j]);
-        }
-      }
-    } else {
-      for (int i = t; i < kInX * kInY; i += blockDim.x) {
-        const int iy = i / kInX, ix = i % kInX;
-        const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
-        float xv = 0.0f, yv = 0.0f;
-        if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
-          const size_t p = (size_t)gy * W + gx;
-          xv = img[ch * plane + p];
-          yv = gt_u8 ? s_u8[static_cast<const uint8_t*>(gt)[p * 3 + ch]] : static_cast<const float*>(gt)[p * 3 + ch];
-        }
-        s_xy[iy][ix] = make_float2(xv, yv);
+    for (int k = 0; k < kLoadIters; ++k) {
+      pf_x[k] = 0.0f;
+      pf_y[k] = U8 ? 0u : __float_as_uint(0.0f);
+      if (row_ok && (col_ok >> k & 1u)) {
+        pf_x[k] = __ldg(xp + 32 * k);
+        pf_y[k] = U8 ? (uint32_t)__ldg(yp8 + 96 * k) : __float_as_uint(__ldg(ypf + 96 * k));
       }
     }
+  };
+  __syncthreads();  // s_u8
+  prefetch(rs);
+
+  // s0 = ring slot of row y0; every other row's slot is s0 + a constant
+  // offset (mod kRing): y0 - 10 -> s0 + 8, y0 - 5 -> s0 + 13, y0 - 15 -> s0 + 3
+  int s0 = 0;
+  for (int y0 = rs; y0 - kLag < r_end; y0 += kRB, s0 = ring(s0 + kRB)) {
+    // store the prefetched block (its ring slots held rows y0 - 18 .. y0 - 11,
+    // which the previous step's stage 5 read: barrier first); L1 /
+    // squared-error sums of owned pixels
+    if (GRAD) __syncthreads();
+    {
+      const int gy = y0 + warp;
+      const bool row_own = gy >= r0 && gy < r_end;
+      float2* dst = s_in + ring(s0 + warp) * kPI + lane;
+      float fl1 = 0.0f, fsq = 0.0f;
+#pragma unroll
+      for (int k = 0; k < kLoadIters; ++k) {
+        if (lane + 32 * k < kIW) {
+          const float yv = U8 ? s_u8[pf_y[k]] : __uint_as_float(pf_y[k]);
+          dst[32 * k] = make_float2(pf_x[k], yv);
+          if (row_own && (col_own >> k & 1u)) {
+            const float diff = pf_x[k] - yv;
+            fl1 += fabsf(diff);
+            fsq = fmaf(diff, diff, fsq);
+          }
+        }
+      }
+      l1 += (double)fl1;
+      sq += (double)fsq;
+    }
     __syncthreads();
-    // horizontal: kInY rows x 8 groups of 4 columns
-    for (int hw = t; hw < kInY * (kTX / kHX); hw += blockDim.x) {
-      const int iy = hw / (kTX / kHX), ox = (hw % (kTX / kHX)) * kHX;
-      float2 acc_m[kHX], acc_s[kHX];
-      float acc_p[kHX];
+    if (y0 + kRB - kLag < r_end) prefetch(y0 + kRB);
+
+    // (2) horizontal moments of the block's rows
+    {
+      const int slot = ring(s0 + h_row);
+      const float2* src = s_in + slot * kPI + 4 * h_grp;
+      float2 am[4], as[4];
+      float ap[4];
 #pragma unroll
-      for (int c = 0; c < kHX; ++c) acc_m[c] = acc_s[c] = f2(0.0f), acc_p[c] = 0.0f;
+      for (int c = 0; c < 4; ++c) am[c] = as[c] = f2(0.0f), ap[c] = 0.0f;
 #pragma unroll
-      for (int k = 0; k < kHX + 10; ++k) {
-        const float2 v = s_xy[iy][ox + k];
+      for (int k = 0; k < 14; ++k) {
+        const float2 v = src[k];
         const float2 sq2 = __fmul2_rn(v, v);
         const float pr = v.x * v.y;
 #pragma unroll
-        for (int c = 0; c < kHX; ++c) {
+        for (int c = 0; c < 4; ++c) {
           const int o = k - c;
           if (o >= 0 && o < 11) {
             const float w = c_gauss[o];
-            acc_m[c] = __ffma2_rn(f2(w), v, acc_m[c]);
-            acc_s[c] = __ffma2_rn(f2(w), sq2, acc_s[c]);
-            acc_p[c] = fmaf(w, pr, acc_p[c]);
+            am[c] = __ffma2_rn(f2(w), v, am[c]);
+            as[c] = __ffma2_rn(f2(w), sq2, as[c]);
+            ap[c] = fmaf(w, pr, ap[c]);
           }
         }
       }
+      const int o = slot * kPM + 4 * h_grp;
 #pragma unroll
-      for (int c = 0; c < kHX; ++c) {
-        s_h2[0][iy][ox + c] = acc_m[c];
-        s_h2[1][iy][ox + c] = acc_s[c];
-        s_h1[iy][ox + c] = acc_p[c];
+      for (int c = 0; c < 4; ++c) {
+        m_ab[o + c] = make_float4(am[c].x, am[c].y, as[c].x, as[c].y);
+        m_c[o + c] = ap[c];
       }
     }
     __syncthreads();
-    float2 mom_m[kVY], mom_s[kVY];
-    float mom_p[kVY];
+
+    // (3) vertical moments of centre rows y0 - 5 .. y0 + 2: column t % 128,
+    // rows 4 (t / 128) .. + 3; SSIM map and partials
+    {
+      const int m = t & (kMW - 1), rb = (t >> 7) * 4;
+      float2 mm[4], ms[4];
+      float mp[4];
 #pragma unroll
-    for (int r = 0; r < kVY; ++r) mom_m[r] = mom_s[r] = f2(0.0f), mom_p[r] = 0.0f;
+      for (int r = 0; r < 4; ++r) mm[r] = ms[r] = f2(0.0f), mp[r] = 0.0f;
+      const int sw = ring(s0 + 8 + rb);  // first row y0 - 10 + rb
+      const RingWin<float4, kPM> wa(m_ab + m, sw);
+      const RingWin<float, kPM> wc(m_c + m, sw);
 #pragma unroll
-    for (int k = 0; k < kVY + 10; ++k) {
-      const float2 a = s_h2[0][vy0 + k][vx], b = s_h2[1][vy0 + k][vx];
-      const float c = s_h1[vy0 + k][vx];
+      for (int k = 0; k < 14; ++k) {
+        const float4 ab = wa(k);
+        const float2 a2 = make_float2(ab.x, ab.y), s2 = make_float2(ab.z, ab.w);
+        const float p1 = wc(k);
 #pragma unroll
-      for (int r = 0; r < kVY; ++r) {
-        const int o = k - r;
-        if (o >= 0 && o < 11) {
-          const float w = c_gauss[o];
-          mom_m[r] = __ffma2_rn(f2(w), a, mom_m[r]);
-          mom_s[r] = __ffma2_rn(f2(w), b, mom_s[r]);
-          mom_p[r] = fmaf(w, c, mom_p[r]);
+        for (int r = 0; r < 4; ++r) {
+          const int o = k - r;
+          if (o >= 0 && o < 11) {
+            const float w = c_gauss[o];
+            mm[r] = __ffma2_rn(f2(w), a2, mm[r]);
+            ms[r] = __ffma2_rn(f2(w), s2, ms[r]);
+            mp[r] = fmaf(w, p1, mp[r]);
+          }
+        }
+      }
+      const int gx = x0 - 5 + m;
+      const bool col_in = gx >= 0 && gx < W;
+      const bool col_own2 = col_in && gx >= x0 && gx < x0 + kSW;
+      float fss = 0.0f;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int gy = y0 - 5 + rb + r;
+        const float mx = mm[r].x, my = mm[r].y;
+        const float C1 = (float)(0.01 * 0.01), C2 = (float)(0.03 * 0.03);
+        const float a1 = 2.0f * mx * my + C1;
+        const float a2 = 2.0f * (mp[r] - mx * my) + C2;
+        const float b1 = mx * mx + my * my + C1;
+        const float b2 = (ms[r].x - mx * mx) + (ms[r].y - my * my) + C2;
+        // fast reciprocals (2 ulp): the loss is checked against the oracle
+        // within a tolerance; the IEEE divisions cost ~4x the instructions
+        const float inv_bb = __fdividef(1.0f, b1 * b2);
+        const float sv = (a1 * a2) * inv_bb;
+        if (col_own2 && gy >= r0 && gy < r_end) fss += sv;
+        if (GRAD) {
+          const bool in = col_in && gy >= 0 && gy < H;
+          const float s_b1 = sv * __fdividef(1.0f, b1), s_b2 = sv * __fdividef(1.0f, b2);
+          const float u_mu = nrm * (a2 * inv_bb * 2.0f * my - a1 * inv_bb * 2.0f * my - s_b1 * 2.0f * mx + s_b2 * 2.0f * mx);
+          const float u_mxy = nrm * (a1 * inv_bb * 2.0f);
+          const float u_mxx = nrm * (-s_b2);
+          p_a[(rb + r) * kPS + m] = in ? make_float2(u_mu, u_mxy) : f2(0.0f);
+          p_b[(rb + r) * kPS + m] = in ? u_mxx : 0.0f;
+        }
+      }
+      ss += (double)fss;
+    }
+    __syncthreads();
+    if (!GRAD) continue;
+
+    // (4) horizontal filter of the partial rows y0 - 5 .. y0 + 2 into the
+    // second ring (groups 30 and 31 are beyond kSW: computed, never read)
+    {
+      const float2* sa = p_a + h_row * kPS + 4 * h_grp;
+      const float* sb = p_b + h_row * kPS + 4 * h_grp;
+      float2 a2[4];
+      float a1[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) a2[c] = f2(0.0f), a1[c] = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 14; ++k) {
+        const float2 u = sa[k];
+        const float u1 = sb[k];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int o = k - c;
+          if (o >= 0 && o < 11) {
+            a2[c] = __ffma2_rn(f2(c_gauss[o]), u, a2[c]);
+            a1[c] = fmaf(c_gauss[o], u1, a1[c]);
+          }
+        }
+      }
+      const int o = ring(ring(s0 + 13) + h_row) * kPM + 4 * h_grp;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        h_a[o + c] = a2[c];
+        h_b[o + c] = a1[c];
+      }
+    }
+    __syncthreads();
+
+    // (5) vertical filter into g for output rows y0 - 10 .. y0 - 3: column
+    // t % 128 (< kSW), rows 4 (t / 128) .. + 3; dL/dimage written once
+    {
+      const int j = t & (kMW - 1), rb = (t >> 7) * 4;
+      const int gx = x0 + j;
+      if (j < kSW && gx < W) {
+        float2 f2v[4];
+        float f1v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) f2v[r] = f2(0.0f), f1v[r] = 0.0f;
+        const int sw = ring(s0 + 3 + rb);  // first row y0 - 15 + rb
+        const RingWin<float2, kPM> wa(h_a + j, sw);
+        const RingWin<float, kPM> wb(h_b + j, sw);
+#pragma unroll
+        for (int k = 0; k < 14; ++k) {
+          const float2 u = wa(k);
+          const float u1 = wb(k);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int o = k - r;
+            if (o >= 0 && o < 11) {
+              f2v[r] = __ffma2_rn(f2(c_gauss[o]), u, f2v[r]);
+              f1v[r] = fmaf(c_gauss[o], u1, f1v[r]);
+            }
+          }
+        }
+        const int sx = ring(s0 + 8 + rb);  // input slot of row y0 - 10 + rb
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int gy = y0 - 10 + rb + r;
+          if (gy < r0 || gy >= r_end) continue;
+          const float2 xy = s_in[ring(sx + r) * kPI + j + 10];
+          const float diff = xy.x - xy.y;
+          const float sg = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
+          const float g = f2v[r].x + f2v[r].y * xy.y + f1v[r] * 2.0f * xy.x;
+          dimage[ch * plane + (size_t)gy * W + gx] = (1.0f - lambda) * sg * inv_n - lambda * g;
         }
       }
     }
-#pragma unroll
-    for (int r = 0; r < kVY; ++r) {
-      const int px = tx0 + vx, py = ty0 + vy0 + r;
-      if (px >= W || py >= H) continue;
-      const float mx = mom_m[r].x, my = mom_m[r].y;
-      const float C1 = (float)(0.01 * 0.01), C2 = (float)(0.03 * 0.03);
-      const float a1 = 2.0f * mx * my + C1;
-      const float a2 = 2.0f * (mom_p[r] - mx * my) + C2;
-      const float b1 = mx * mx + my * my + C1;
-      const float b2 = (mom_s[r].x - mx * mx) + (mom_s[r].y - my * my) + C2;
-      // fast reciprocals (2 ulp): the loss is checked against the oracle
-      // within a tolerance; the IEEE divisions cost ~4x the instructions
-      const float inv_bb = __fdividef(1.0f, b1 * b2);
-      const float sv = (a1 * a2) * inv_bb;
-      ss += (double)sv;
-      const size_t p = (size_t)py * W + px;
-      const float2 xy = s_xy[vy0 + r + kHalo][vx + kHalo];
-      const float diff = xy.x - xy.y;
-      l1 += (double)fabsf(diff);
-      sq += (double)diff * (double)diff;
-      if (want_grad) {
-        const float s_b1 = sv * __fdividef(1.0f, b1), s_b2 = sv * __fdividef(1.0f, b2);
-        partials[(0 * 3 + ch) * plane + p] =
-            nrm * (a2 * inv_bb * 2.0f * my - a1 * inv_bb * 2.0f * my - s_b1 * 2.0f * mx + s_b2 * 2.0f * mx);
-        partials[(1 * 3 + ch) * plane + p] = nrm * (a1 * inv_bb * 2.0f);
-        partials[(2 * 3 + ch) * plane + p] = nrm * (-s_b2);
-        const float sg = diff > 0.0f ? 1.0f : (diff < 0.0f ? -1.0f : 0.0f);
-        dimage[ch * plane + p] = (1.0f - lambda) * sg * inv_n;
-      }
-    }
   }
+
   const double t_l1 = block_sum(l1, s_red);
   const double t_ss = block_sum(ss, s_red);
   const double t_sq = block_sum(sq, s_red);
@@ -235,116 +400,6 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
   }
 }
 
-// Kernel B: filter the three partials (same tiling; u_mu and u_mxy as one
-// packed pair, u_mxx alone) and finish dL/dimage:
-// d -= lambda (filt(u_mu) + filt(u_mxy) y + filt(u_mxx) 2 x).
-__global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ img, const void* __restrict__ gt,
-                                                       bool gt_u8, int W, int H, float lambda,
-                                                       const float* __restrict__ partials,
-                                                       float* __restrict__ dimage) {
-  __shared__ float2 s_u2[kInY][kInX + 1];
-  __shared__ float s_u1[kInY][kInX + 1];
-  __shared__ float2 s_h2[kInY][kTX + 1];
-  __shared__ float s_h1[kInY][kTX + 1];
-  __shared__ float s_u8[256];
-  const int tx0 = blockIdx.x * kTX, ty0 = blockIdx.y * kTY;
-  const int t = threadIdx.x;
-  const size_t plane = (size_t)W * H;
-  for (int i = t; i < 256; i += blockDim.x) s_u8[i] = __fdiv_rn((float)i, 255.0f);
-  const int vx = t % kTX, vy0 = (t / kTX) * kVY;
-  {
-    const int ch = blockIdx.z;  // one channel per CTA
-    __syncthreads();
-    if ((W & 3) == 0) {
-      // float4 quads of the three partial planes (see ssim_fwd_kernel)
-      for (int i = t; i < kInY * kQuads; i += blockDim.x) {
-        const int iy = i / kQuads, q = i % kQuads;
-        const int gy = ty0 - kHalo + iy, gx0 = tx0 - kQuadLead + 4 * q;
-        float4 a = make_float4(0.0f, 0.0f, 0.0f, 0.0f), b = a, c = a;
-        if (gy >= 0 && gy < H && gx0 >= 0 && gx0 < W) {
-          const size_t p = (size_t)gy * W + gx0;
-          a = *reinterpret_cast<const float4*>(partials + (0 * 3 + ch) * plane + p);
-          b = *reinterpret_cast<const float4*>(partials + (1 * 3 + ch) * plane + p);
-          c = *reinterpret_cast<const float4*>(partials + (2 * 3 + ch) * plane + p);
-        }
-        const float as[4] = {a.x, a.y, a.z, a.w}, bs[4] = {b.x, b.y, b.z, b.w}, cs[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int ix = 4 * q + j - (kQuadLead - kHalo);
-          if (ix >= 0 && ix < kInX) {
-            s_u2[iy][ix] = make_float2(as[j], bs[j]);
-            s_u1[iy][ix] = cs[j];
-          }
-        }
-      }
-    } else {
-      for (int i = t; i < kInX * kInY; i += blockDim.x) {
-        const int iy = i / kInX, ix = i % kInX;
-        const int gx = tx0 - kHalo + ix, gy = ty0 - kHalo + iy;
-        const bool ok = gx >= 0 && gx < W && gy >= 0 && gy < H;
-        const size_t p = (size_t)gy * W + gx;
-        s_u2[iy][ix] = ok ? make_float2(partials[(0 * 3 + ch) * plane + p], partials[(1 * 3 + ch) * plane + p])
-                          : f2(0.0f);
-        s_u1[iy][ix] = ok ? partials[(2 * 3 + ch) * plane + p] : 0.0f;
-      }
-    }
-    __syncthreads();
-    for (int hw = t; hw < kInY * (kTX / kHX); hw += blockDim.x) {
-      const int iy = hw / (kTX / kHX), ox = (hw % (kTX / kHX)) * kHX;
-      float2 a2[kHX];
-      float a1[kHX];
-#pragma unroll
-      for (int c = 0; c < kHX; ++c) a2[c] = f2(0.0f), a1[c] = 0.0f;
-#pragma unroll
-      for (int k = 0; k < kHX + 10; ++k) {
-        const float2 u = s_u2[iy][ox + k];
-        const float u1 = s_u1[iy][ox + k];
-#pragma unroll
-        for (int c = 0; c < kHX; ++c) {
-          const int o = k - c;
-          if (o >= 0 && o < 11) {
-            a2[c] = __ffma2_rn(f2(c_gauss[o]), u, a2[c]);
-            a1[c] = fmaf(c_gauss[o], u1, a1[c]);
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < kHX; ++c) {
-        s_h2[iy][ox + c] = a2[c];
-        s_h1[iy][ox + c] = a1[c];
-      }
-    }
-    __syncthreads();
-    float2 f2v[kVY];
-    float f1v[kVY];
-#pragma unroll
-    for (int r = 0; r < kVY; ++r) f2v[r] = f2(0.0f), f1v[r] = 0.0f;
-#pragma unroll
-    for (int k = 0; k < kVY + 10; ++k) {
-      const float2 a = s_h2[vy0 + k][vx];
-      const float c = s_h1[vy0 + k][vx];
-#pragma unroll
-      for (int r = 0; r < kVY; ++r) {
-        const int o = k - r;
-        if (o >= 0 && o < 11) {
-          f2v[r] = __ffma2_rn(f2(c_gauss[o]), a, f2v[r]);
-          f1v[r] = fmaf(c_gauss[o], c, f1v[r]);
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < kVY; ++r) {
-      const int px = tx0 + vx, py = ty0 + vy0 + r;
-      if (px >= W || py >= H) continue;
-      const size_t p = (size_t)py * W + px;
-      const float xv = img[ch * plane + p];
-      const float yv = gt_u8 ? s_u8[static_cast<const uint8_t*>(gt)[p * 3 + ch]] : static_cast<const float*>(gt)[p * 3 + ch];
-      const float g = f2v[r].x + f2v[r].y * yv + f1v[r] * 2.0f * xv;
-      dimage[ch * plane + p] = dimage[ch * plane + p] - lambda * g;
-    }
-  }
-}
-
 bool g_gauss_ready[64] = {};
 
 void upload_gauss(cudaStream_t s) {
@@ -365,28 +420,49 @@ void upload_gauss(cudaStream_t s) {
   if (dev < 64) g_gauss_ready[dev] = true;
 }
 
+// 2 resident CTAs per SM (98 KB of shared memory each): the row ranges are
+// sized so strips x ranges x 3 channels fills those slots once.
+int g_slots[64] = {};
+
+template <bool GRAD, bool U8>
+int march_slots(int dev) {
+  SK_CUDA(cudaFuncSetAttribute(ssim_march_kernel<GRAD, U8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kSmemBytes));
+  int per_sm = 0, sms = 0;
+  SK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssim_march_kernel<GRAD, U8>, kThreads, kSmemBytes));
+  SK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  return std::max(1, per_sm) * sms;
+}
+
 }  // namespace
 
 void launch_loss(sk_ctx* ctx, sk_frame* f, const void* gt, bool gt_u8, float lambda, bool want_grad, LossSums* out) {
   upload_gauss(ctx->stream);
   const int W = f->width, H = f->height;
   const size_t plane = (size_t)W * H;
-  float* partials = want_grad ? ensure<float>(f->loss_scratch, 9 * plane) : nullptr;
   float* dimage = want_grad ? ensure<float>(f->dimage, 3 * plane) : nullptr;
   double* sums = ensure<double>(ctx->scalars, 5);
   unsigned int* ticket = reinterpret_cast<unsigned int*>(sums + 4);
   SK_CUDA(cudaMemsetAsync(sums, 0, 5 * sizeof(double), ctx->stream));
-  const dim3 grid((W + kTX - 1) / kTX, (H + kTY - 1) / kTY, 3);
+  const int dev = ctx->device;
+  if (dev >= 64 || g_slots[dev] == 0) {
+    const int s = std::min(std::min(march_slots<true, true>(dev), march_slots<true, false>(dev)),
+                           std::min(march_slots<false, true>(dev), march_slots<false, false>(dev)));
+    if (dev < 64) g_slots[dev] = s;
+  }
+  const int slots = dev < 64 ? g_slots[dev] : 296;
+  const int strips = (W + kSW - 1) / kSW;
+  const int ranges = std::max(1, std::min((H + kRB - 1) / kRB, slots / (3 * strips)));
+  const int rows = (((H + ranges - 1) / ranges) + kRB - 1) / kRB * kRB;
+  const dim3 grid(strips, (H + rows - 1) / rows, 3);
   double* block_sums = ensure<double>(ctx->loss_blocks, 3 * (size_t)grid.x * grid.y * grid.z);
   const float nrm = 1.0f / (3.0f * (float)W * (float)H);
   const float inv_n = 1.0f / (3.0f * (float)plane);
-  ssim_fwd_kernel<<<grid, 256, 0, ctx->stream>>>(f->image.as<float>(), gt, gt_u8, W, H, nrm, lambda, inv_n, want_grad,
-                                                 partials, dimage, sums, block_sums, ticket);
+  auto* k = want_grad ? (gt_u8 ? ssim_march_kernel<true, true> : ssim_march_kernel<true, false>)
+                      : (gt_u8 ? ssim_march_kernel<false, true> : ssim_march_kernel<false, false>);
+  k<<<grid, kThreads, kSmemBytes, ctx->stream>>>(f->image.as<float>(), gt, W, H, rows, nrm, lambda, inv_n, dimage,
+                                                 sums, block_sums, ticket);
   note_launch();
-  if (want_grad) {
-    ssim_bwd_kernel<<<grid, 256, 0, ctx->stream>>>(f->image.as<float>(), gt, gt_u8, W, H, lambda, partials, dimage);
-    note_launch();
-  }
   SK_CUDA(cudaGetLastError());
   if (out) read_loss_sums(ctx, out);
 }

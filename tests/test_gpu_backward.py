@@ -28,8 +28,10 @@ def ctx():
 
 def test_loss_and_dimage_match_oracle(ctx, orc):
     rng = np.random.default_rng(3)
-    for (w, h) in ((37, 29), (64, 48), (128, 96)):
-        pg = orc.random_projected(rng, 60, w, h, 0.9, dtype=np.float32)
+    # strips of 118 columns x row ranges: sizes with one strip, several,
+    # ragged last strips and ranges, W % 4 != 0
+    for (w, h) in ((37, 29), (64, 48), (128, 96), (250, 131), (509, 301)):
+        pg = orc.random_projected(rng, 60 if w < 200 else 400, w, h, 0.9, dtype=np.float32)
         ctx.set_projected(pg, w, h)
         r = ctx.blend_forward()
         gt = rng.uniform(0, 1, (h, w, 3)).astype(np.float32)
@@ -37,7 +39,9 @@ def test_loss_and_dimage_match_oracle(ctx, orc):
         loss, l1, ss, d_ref = orc.training_loss(r.image, gt, 0.2)
         assert v.loss == pytest.approx(loss, rel=1e-5)
         assert v.l1 == pytest.approx(l1, rel=1e-5)
-        assert v.ssim == pytest.approx(ss, rel=1e-5)
+        # the mean SSIM of random GT is ~1e-3: an absolute floor at the
+        # oracle's own fp32 accumulation error over ~1e5 pixels
+        assert v.ssim == pytest.approx(ss, rel=1e-5, abs=1e-7)
         assert v.psnr == pytest.approx(orc.psnr(r.image, gt), rel=1e-6)
         d = ctx.get_dimage()
         assert rel_err_vec(d, d_ref, 1e-4).max() < TOL
@@ -45,13 +49,15 @@ def test_loss_and_dimage_match_oracle(ctx, orc):
 
 def test_loss_u8_gt(ctx, orc):
     rng = np.random.default_rng(4)
-    pg = orc.random_projected(rng, 40, 48, 40, 0.9, dtype=np.float32)
-    ctx.set_projected(pg, 48, 40)
-    r = ctx.blend_forward()
-    gt8 = rng.integers(0, 256, (40, 48, 3), dtype=np.uint8)
-    v = ctx.training_loss(gt8, 0.2)
-    loss, _, _, _ = orc.training_loss(r.image, gt8.astype(np.float32) / np.float32(255.0), 0.2)
-    assert v.loss == pytest.approx(loss, rel=1e-5)
+    for (w, h) in ((48, 40), (356, 203)):
+        pg = orc.random_projected(rng, 40, w, h, 0.9, dtype=np.float32)
+        ctx.set_projected(pg, w, h)
+        r = ctx.blend_forward()
+        gt8 = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        v = ctx.training_loss(gt8, 0.2)
+        loss, _, _, d_ref = orc.training_loss(r.image, gt8.astype(np.float32) / np.float32(255.0), 0.2)
+        assert v.loss == pytest.approx(loss, rel=1e-5)
+        assert rel_err_vec(ctx.get_dimage(), d_ref, 1e-4).max() < TOL
 
 
 def test_ssim_psnr_kats_gpu(ctx):
