@@ -622,7 +622,9 @@ def measure_event(ctx, sk, torch, dist, rank, n, k, width, height, reps, warm):
         ms = (sk.C.c_double * 4)()
         cnt = sk.C.c_int64()
         ctx._lib.sk_ctx_get_event_timing(ctx.h, ms, sk.C.byref(cnt))
-        return [ms[i] / max(1, cnt.value) for i in range(4)]
+        mv = sk.C.c_double()
+        ctx._lib.sk_ctx_get_compact_kernel_ms(ctx.h, sk.C.byref(mv))
+        return [ms[i] / max(1, cnt.value) for i in range(4)] + [mv.value / max(1, cnt.value)]
 
     def timed(iteration, densify, prune):
         restore()
@@ -665,8 +667,15 @@ def measure_event(ctx, sk, torch, dist, rank, n, k, width, height, reps, warm):
         # written per output Gaussian, plus the three flag bytes per input.
         k1415 = 2 * 3 * 4 * comps * n_out + 3 * n
         t13, t1415 = ph[1] * 1e-3, (ph[2] + ph[3]) * 1e-3
+        # the K15 row-move kernel alone (CUDA events around it): the same
+        # row bytes without the flags, the class scans and the host round
+        # trip for the split normals that the phase time includes
+        mv_b, t_mv = 2 * 3 * 4 * comps * n_out, ph[4] * 1e-3
         return {"phase_ms": dict(zip(["K6+K11+K12 views (+K1-K5, K7 fwd)", "K13 scores", "K14 select",
-                                      "K15 compact"], [round(x, 4) for x in ph])),
+                                      "K15 compact"], [round(x, 4) for x in ph[:4]])),
+                "K15 move kernel": {"ms": round(ph[4], 4), "algorithmic_MB": mv_b / 1e6,
+                                    "GB/s": mv_b / t_mv / 1e9 if t_mv > 0 else None,
+                                    "frac": mv_b / t_mv / 1e9 / hbm_peak if t_mv > 0 else None},
                 "K13": {"algorithmic_MB": k13 / 1e6, "GB/s": k13 / t13 / 1e9, "frac": k13 / t13 / 1e9 / hbm_peak},
                 "K14+K15": {"algorithmic_MB": k1415 / 1e6, "GB/s": k1415 / t1415 / 1e9,
                             "frac": k1415 / t1415 / 1e9 / hbm_peak},

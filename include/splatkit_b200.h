@@ -122,6 +122,10 @@ int sk_ctx_reset_timing(sk_ctx* ctx);
  * 2 K14 selection, 3 K15 compaction (+ Adam moment remap). */
 #define SK_NUM_EVENT_PHASES 4
 int sk_ctx_get_event_timing(const sk_ctx* ctx, double* ms, int64_t* events);
+/* Kernel-only time inside phase 3 (sum over timed events): the K15 row-move
+ * kernel, without the class scans and the host round trip for the split
+ * normals (the phase time includes both). */
+int sk_ctx_get_compact_kernel_ms(const sk_ctx* ctx, double* move_ms);
 const char* sk_version(void);
 
 /* ---- scene (Scene<T>, scene.hpp:30-52) ---------------------------------- */

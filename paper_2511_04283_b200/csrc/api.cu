@@ -136,6 +136,7 @@ int sk_ctx_enable_timing(sk_ctx* ctx, int on) {
       for (auto& set : ctx->tev)
         for (auto& e : set) SK_CUDA(cudaEventCreate(&e));
       for (auto& e : ctx->ev.tev) SK_CUDA(cudaEventCreate(&e));
+      for (auto& e : ctx->ev.move_ev) SK_CUDA(cudaEventCreate(&e));
     }
     ctx->timing = on != 0;
   });
@@ -157,12 +158,19 @@ int sk_ctx_get_event_timing(const sk_ctx* ctx, double* ms, int64_t* events) {
   return SK_OK;
 }
 
+int sk_ctx_get_compact_kernel_ms(const sk_ctx* ctx, double* move_ms) {
+  if (!ctx || !move_ms) return SK_ERR_INVALID_ARGUMENT;
+  *move_ms = ctx->ev.move_ms;
+  return SK_OK;
+}
+
 int sk_ctx_reset_timing(sk_ctx* ctx) {
   if (!ctx) return SK_ERR_INVALID_ARGUMENT;
   for (auto& v : ctx->phase_ms) v = 0.0;
   ctx->timed_steps = 0;
   for (auto& v : ctx->ev.phase_ms) v = 0.0;
   ctx->ev.timed_events = 0;
+  ctx->ev.move_ms = 0.0;
   return SK_OK;
 }
 

@@ -819,13 +819,21 @@ int64_t compact_scene(sk_ctx* ctx, sk_scene* s, const uint8_t* prune, const uint
   ensure<float>(nv, cells);
   trace_point(ctx, "compact: buffers");
   const int groups = 1 + std::max(1, (s->comps - SK_COMP_SH + 3) / 4);
+  const bool timed = ctx->timing && ctx->ev.move_ev[0];
+  if (timed) SK_CUDA(cudaEventRecord(ctx->ev.move_ev[0], ctx->stream));
   compact_move_kernel<<<dim3(nb, groups), kCompactBlock, 0, ctx->stream>>>(
       prune, clone, split, n, block_base, totals, s->comps, s->params.as<float>(), s->adam_m.as<float>(),
       s->adam_v.as<float>(), s->capacity, np.as<float>(), nm.as<float>(), nv.as<float>(), new_cap,
       s->grad3d_acc.as<float>(), s->views_seen.as<int>(), clone_lr, eps, (float)std::log(1.6), old_to_new_dev);
   note_launch();
   SK_CUDA(cudaGetLastError());
+  if (timed) SK_CUDA(cudaEventRecord(ctx->ev.move_ev[1], ctx->stream));
   sync(ctx);
+  if (timed) {
+    float ms = 0.0f;
+    SK_CUDA(cudaEventElapsedTime(&ms, ctx->ev.move_ev[0], ctx->ev.move_ev[1]));
+    ctx->ev.move_ms += ms;
+  }
   trace_point(ctx, "compact: kernel");
   s->params.swap(np);
   s->adam_m.swap(nm);

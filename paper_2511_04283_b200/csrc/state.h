@@ -76,6 +76,8 @@ struct EventScratch {
   cudaEvent_t tev[SK_NUM_EVENT_PHASES + 1] = {};
   double phase_ms[SK_NUM_EVENT_PHASES] = {};
   int64_t timed_events = 0;
+  cudaEvent_t move_ev[2] = {};  // around the K15 row-move kernel (created with tev)
+  double move_ms = 0.0;
 };
 }  // namespace sk
 
