@@ -19,9 +19,9 @@ g = "gpurun_out"
 
 # kernel name prefix -> bench.py phase (PHASES in bench.py)
 PHASE_OF = [("preprocess", "K1 preprocess"), ("radix_", "K2-K5 bin+sort"), ("onesweep", "K2-K5 bin+sort"),
-            ("scan_gather", "K2-K5 bin+sort"), ("duplicate", "K2-K5 bin+sort"),
-            ("tile_ranges", "K2-K5 bin+sort"), ("blend_fwd", "K6 blend fwd"), ("ssim", "K7 loss"),
-            ("blend_bwd", "K8 blend bwd"), ("project_bwd", "K9 proj-bwd"), ("adam", "K10 Adam")]
+            ("bin_", "K2-K5 bin+sort"), ("blend_fwd", "K6 blend fwd"), ("ssim", "K7 loss"),
+            ("blend_bwd", "K8 blend bwd"), ("project_bwd_adam", "K9+K10 proj-bwd+Adam (fused)"),
+            ("project_bwd", "K9 proj-bwd"), ("adam", "K10 Adam")]
 
 
 def phase(k):
