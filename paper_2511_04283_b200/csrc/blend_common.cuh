@@ -49,6 +49,14 @@ __device__ __forceinline__ float cull_div(float a, float b) {
   return __fdividef(a, b);
 }
 
+// FAST (training-step) form of q for a pixel pair sharing the column
+// (dx) and differing in row (dy = (dy0, dy1)): q = A + dy (B + c11 dy) with
+// A = (c00 dx) dx, B = (2 c01) dx, in two packed FMAs. K6 and K8 form it with
+// these same instructions, so their contribution decisions agree bit for bit.
+__device__ __forceinline__ float2 fast_pair_q(float2 dy, float c11, float A, float B) {
+  return __ffma2_rn(dy, __ffma2_rn(make_float2(c11, c11), dy, make_float2(B, B)), make_float2(A, A));
+}
+
 __device__ __forceinline__ float qcut_of(float opacity) {
   const float a = 255.0f * opacity;
   return a > 1.0f ? 2.0f * __logf(a) + 0.02f : -1.0f;

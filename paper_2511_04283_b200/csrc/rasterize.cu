@@ -231,6 +231,50 @@ __global__ void __launch_bounds__(TS* TS / PIX, kFwdMinBlocks * 128 / (TS * TS /
       m &= m - 1;
       const float4 mq = s_xyq[warp][j];
       const float4 co = s_co_w[j];
+      if (FAST && PIX % 2 == 0) {
+        // Training steps: q of the lane's pixel pairs (rows y, y + 4) in packed
+        // f32x2 FMAs, q = A + dy (B + c11 dy) with A = (c00 dx) dx and
+        // B = (2 c01) dx shared by the pair. K8's FAST walk forms q with the
+        // same instructions, so both kernels make the same contribution
+        // decisions (blend_common.cuh: fast_pair_q).
+        const float dx = fpx - mq.x;
+        const float A = __fmul_rn(__fmul_rn(co.x, dx), dx), B = __fmul_rn(__fmul_rn(2.0f, co.y), dx);
+        const uint32_t qc = __float_as_uint(mq.z);
+#pragma unroll
+        for (int kp = 0; kp < PIX / 2; ++kp) {
+          const int a = 2 * kp, b = 2 * kp + 1;
+          const float2 dy = __fadd2_rn(make_float2(fpy[a], fpy[b]), make_float2(-mq.y, -mq.y));
+          const float2 q = fast_pair_q(dy, co.z, A, B);
+          bool ok0 = __float_as_uint(__fadd_rn(q.x, 0.0f)) <= qc;
+          bool ok1 = __float_as_uint(__fadd_rn(q.y, 0.0f)) <= qc;
+          if (!(ok0 || ok1)) continue;
+          const float2 xe = __fmul2_rn(q, make_float2(-0.72134752044448170f, -0.72134752044448170f));
+          float2 al = __fmul2_rn(make_float2(co.w, co.w), make_float2(exp2f_approx(xe.x), exp2f_approx(xe.y)));
+          al.x = (al.x < kAlphaCap) ? al.x : kAlphaCap;
+          al.y = (al.y < kAlphaCap) ? al.y : kAlphaCap;
+          ok0 = ok0 && !(al.x < kAlphaMin);
+          ok1 = ok1 && !(al.y < kAlphaMin);
+          if (!(ok0 || ok1)) continue;
+          lane_bits |= 1u << j;
+          const float4 c = s_rgb_w[j];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = h == 0 ? a : b;
+            const bool ok = h == 0 ? ok0 : ok1;
+            const float alpha = h == 0 ? al.x : al.y;
+            if (!ok) continue;
+            const float w = T[k] * alpha;
+            C0[k] = C0[k] + w * c.x;
+            C1[k] = C1[k] + w * c.y;
+            C2[k] = C2[k] + w * c.z;
+            ++n[k];
+            last[k] = b0 + j + 1;
+            T[k] = T[k] * (1.0f - alpha);
+            fpy[k] = T[k] < kTransmitMin ? __int_as_float(0x7fc00000) : fpy[k];
+          }
+        }
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < PIX; ++k) {
         const float dx = fpx - mq.x;

@@ -101,13 +101,16 @@ __device__ __forceinline__ bool pair_partials(const float4 mq, const float4 co, 
                                               PairState& st, const Tab& tab, float (&g)[kBGradFields]) {
   const float dx = fpx - mq.x;
   const float2 dy = __fadd2_rn(st.fpy, f2(-mq.y));
-  // q = ((c00 dx) dx + ((2 c01) dx) dy) + (c11 dy) dy, bit-equal to K6. Scalar
-  // round-to-nearest ops: ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into
-  // FFMA2 (even under -fmad=false), which would change q's last bits.
+  // Exact frames: q = ((c00 dx) dx + ((2 c01) dx) dy) + (c11 dy) dy, bit-equal
+  // to K6's exact walk, in scalar round-to-nearest ops (ptxas contracts
+  // mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under -fmad=false, which would
+  // change q's last bits). FAST frames: K6's packed form (fast_pair_q).
   const float A = __fmul_rn(__fmul_rn(co.x, dx), dx);
   const float B = __fmul_rn(__fmul_rn(2.0f, co.y), dx);
-  const float2 q = make_float2(rn_add(rn_add(A, rn_mul(B, dy.x)), rn_mul(rn_mul(co.z, dy.x), dy.x)),
-                               rn_add(rn_add(A, rn_mul(B, dy.y)), rn_mul(rn_mul(co.z, dy.y), dy.y)));
+  // FAST frames: K6's packed form (fast_pair_q); exact frames: K6's scalar ops
+  const float2 q = FAST ? fast_pair_q(dy, co.z, A, B)
+                        : make_float2(rn_add(rn_add(A, rn_mul(B, dy.x)), rn_mul(rn_mul(co.z, dy.x), dy.x)),
+                                      rn_add(rn_add(A, rn_mul(B, dy.y)), rn_mul(rn_mul(co.z, dy.y), dy.y)));
   // q in [0, q_cut] as one unsigned compare of (q + 0) bits (-0 -> +0; NaN / negative fail)
   const uint32_t qc = __float_as_uint(mq.z);
   bool ok0 = idx < st.last0 && __float_as_uint(__fadd_rn(q.x, 0.0f)) <= qc;
