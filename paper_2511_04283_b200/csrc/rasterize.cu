@@ -263,10 +263,11 @@ __global__ void __launch_bounds__(TS* TS / PIX, kFwdMinBlocks * 128 / (TS * TS /
             const bool ok = h == 0 ? ok0 : ok1;
             const float alpha = h == 0 ? al.x : al.y;
             if (!ok) continue;
+            // (the colour sums may contract: K8 reads only T and last_entry)
             const float w = T[k] * alpha;
-            C0[k] = C0[k] + w * c.x;
-            C1[k] = C1[k] + w * c.y;
-            C2[k] = C2[k] + w * c.z;
+            C0[k] = fmaf(w, c.x, C0[k]);
+            C1[k] = fmaf(w, c.y, C1[k]);
+            C2[k] = fmaf(w, c.z, C2[k]);
             ++n[k];
             last[k] = b0 + j + 1;
             T[k] = T[k] * (1.0f - alpha);
