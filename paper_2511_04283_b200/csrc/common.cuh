@@ -146,6 +146,10 @@ enum : uint32_t {
   kErrCovNonFinite = 1u,
   kErrCovNonPositive = 2u,
   kErrCompactNotPD = 4u,
+  // not an input error: a training step's pair count outgrew the pair buffer
+  // it was launched into (device-resident P, pipeline.cu); the host regrows
+  // the buffer and replays the step
+  kErrPairOverflow = 8u,
 };
 
 // Library kernel launch accounting (sk_ctx_launch_count).

@@ -54,12 +54,13 @@ void ensure_image(sk_frame* f) {
 // K2-K5 (build_tile_grid raster.hpp:157-168): depth sort of the slots, then
 // the tile lists by the counting scatter of preprocess.cu (count, prefix over
 // chunks + tile scan, stable scatter).
-void bin_sort(sk_ctx* ctx, sk_frame* f) {
+void bin_sort(sk_ctx* ctx, sk_frame* f, bool deferred) {
   const int64_t n = f->n;
   f->cmask_valid = false;
   const int tiles = f->tiles_x * f->tiles_y;
   ensure<int2>(f->ranges, (size_t)std::max(tiles, 1));
   f->pairs = 0;
+  f->pair_cap = 0;
   if (n == 0) {
     SK_CUDA(cudaMemsetAsync(f->ranges.ptr, 0, sizeof(int2) * tiles, ctx->stream));
     f->binned = true;
@@ -79,8 +80,30 @@ void bin_sort(sk_ctx* ctx, sk_frame* f) {
   }
   auto* total = ctx->sort.bin_total.as<long long>();
   auto* done = reinterpret_cast<unsigned int*>(total + 1);
+  if (deferred) {
+    // Training steps: P stays on the device. The scatter fills the pair
+    // buffer of an earlier frame (DevBuf keeps 25% regrowth headroom; 12
+    // pairs per slot the first time); if P outgrew it, the prefix kernel
+    // raises kErrPairOverflow, K6 / K8 / K9 / K10 skip, and the host — which
+    // reads P with the step's loss — regrows the buffer and replays the step.
+    if (f->pval_a.bytes / sizeof(uint32_t) <= 256) {
+      // SK_INITIAL_PAIR_CAP: a smaller first buffer (tests drive the overflow
+      // replay with it)
+      const char* e = std::getenv("SK_INITIAL_PAIR_CAP");
+      ensure<uint32_t>(f->pval_a, e ? (size_t)std::max(257ll, std::atoll(e)) : (size_t)12 * n);
+    }
+    const int64_t cap = (int64_t)(f->pval_a.bytes / sizeof(uint32_t));
+    launch_bin_tiles(ctx, f, va, counts, nullptr, 0);
+    launch_bin_prefix(ctx, f, counts, totals, done, cap, ctx->err_word.as<uint32_t>(), total);
+    launch_bin_tiles(ctx, f, va, counts, f->pval_a.as<uint32_t>(), cap);
+    f->pairs = -1;
+    f->pair_cap = cap;
+    f->pair_val = f->pval_a.as<uint32_t>();
+    f->binned = true;
+    return;
+  }
   launch_bin_tiles(ctx, f, va, counts, nullptr, 0);
-  launch_bin_prefix(ctx, f, counts, totals, done, total);
+  launch_bin_prefix(ctx, f, counts, totals, done, -1, nullptr, total);
   // P on the host: copied on a side stream right after the prefix kernel, so
   // the host wakes while the scatter queued behind it still runs. The scatter
   // is launched speculatively into the pair buffer left by an earlier frame

@@ -487,7 +487,8 @@ __global__ void __launch_bounds__(kPrefixWarps * 32) bin_prefix_kernel(int32_t* 
                                                                        int tiles, int32_t* __restrict__ totals,
                                                                        int2* __restrict__ ranges,
                                                                        unsigned int* __restrict__ done,
-                                                                       long long* __restrict__ total_out) {
+                                                                       long long* __restrict__ total_out,
+                                                                       int64_t cap, uint32_t* __restrict__ err) {
   constexpr int NT = kPrefixWarps * 32;
   constexpr int kItems = 4;
   __shared__ int32_t s_sum[kPrefixWarps][32];
@@ -569,6 +570,7 @@ __global__ void __launch_bounds__(kPrefixWarps * 32) bin_prefix_kernel(int32_t* 
   if (threadIdx.x == 0) {
     *total_out = s_carry;
     *done = 0;  // ready for the next frame
+    if (cap >= 0 && s_carry > cap) atomicOr(err, kErrPairOverflow);
   }
 }
 
@@ -833,11 +835,11 @@ int64_t bin_chunks(const sk_frame* f) {
   return (L.n + L.chunk - 1) / L.chunk;
 }
 
-void launch_bin_prefix(sk_ctx* ctx, sk_frame* f, int32_t* counts, int32_t* totals, unsigned int* done,
-                       long long* total_out) {
+void launch_bin_prefix(sk_ctx* ctx, sk_frame* f, int32_t* counts, int32_t* totals, unsigned int* done, int64_t cap,
+                       uint32_t* err, long long* total_out) {
   const int tiles = f->tiles_x * f->tiles_y;
   bin_prefix_kernel<<<(unsigned)((tiles + 31) / 32), kPrefixWarps * 32, 0, ctx->stream>>>(
-      counts, (int)bin_chunks(f), tiles, totals, f->ranges.as<int2>(), done, total_out);
+      counts, (int)bin_chunks(f), tiles, totals, f->ranges.as<int2>(), done, total_out, cap, err);
   note_launch();
   SK_CUDA(cudaGetLastError());
 }

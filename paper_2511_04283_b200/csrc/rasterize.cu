@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(TS* TS / PIX, kFwdMinBlocks * 128 / (TS * TS /
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     float* __restrict__ image, float* __restrict__ final_t, int* __restrict__ n_contrib, int* __restrict__ last_entry,
-    uint32_t* __restrict__ cmask) {
+    uint32_t* __restrict__ cmask, const uint32_t* __restrict__ err) {
+  // a training step whose pair count outgrew its buffer (or whose K1 raised an
+  // error) skips the blend: it is replayed or fails (pipeline.cu, trainer.cu)
+  if (err && __ldg(err)) return;
   using WB = WarpBlock<TS, PIX>;
   constexpr int kWarps = WB::kWarps;
   __shared__ float4 s_xyq[kWarps][32];
@@ -367,7 +370,7 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
   else {
     uint32_t* cm = nullptr;
     if (TS == 16 && PIX == 2) {  // K8 consumes the masks at 16x16 tiles
-      const size_t words = cmask_words(f->pairs, tiles) * (size_t)(TS * TS / PIX / 32);
+      const size_t words = cmask_words(f->pairs < 0 ? f->pair_cap : f->pairs, tiles) * (size_t)(TS * TS / PIX / 32);
       cm = ensure<uint32_t>(f->cmask, words);
       SK_CUDA(cudaMemsetAsync(cm, 0, words * sizeof(uint32_t), ctx->stream));
     }
@@ -376,7 +379,8 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
     auto go = [&](auto kern) {
       kern<<<tiles, TS * TS / PIX, 0, ctx->stream>>>(ranges, f->pair_val, mean2d, co, rgb, f->width, f->height,
                                                      f->tiles_x, f->image.as<float>(), f->final_t.as<float>(),
-                                                     f->n_contrib.as<int>(), f->last_entry.as<int>(), cm);
+                                                     f->n_contrib.as<int>(), f->last_entry.as<int>(), cm,
+                                                     f->pairs < 0 ? ctx->err_word.as<uint32_t>() : nullptr);
     };
     if (fast)
       go(blend_fwd_warp_kernel<TS, PIX, true>);

@@ -232,7 +232,9 @@ __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS /
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     const float* __restrict__ final_t, const int* __restrict__ last_entry, const float* __restrict__ dimage,
-    float* __restrict__ bgrads, int64_t gstride, const uint32_t* __restrict__ cmask) {
+    float* __restrict__ bgrads, int64_t gstride, const uint32_t* __restrict__ cmask,
+    const uint32_t* __restrict__ err) {
+  if (err && __ldg(err)) return;  // see blend_fwd_warp_kernel
   constexpr int NT = TS * TS / PIX;
   constexpr int NP = PIX / 2 > 0 ? PIX / 2 : 1;  // pixel pairs per lane (PIX = 1: one scalar pixel)
   using WB = WarpBlock<TS, PIX>;
@@ -436,7 +438,8 @@ void bwd_dispatch(sk_ctx* ctx, sk_frame* f) {
   kern<<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
       f->ranges.as<int2>(), f->pair_val, f->mean2d.as<float2>(), f->conic_op.as<float4>(), f->rgb_depth.as<float4>(),
       f->width, f->height, f->tiles_x, f->final_t.as<float>(), f->last_entry.as<int>(), f->dimage.as<float>(),
-      f->bgrads.as<float>(), f->n, (TS == 16 && f->cmask_valid) ? f->cmask.as<uint32_t>() : nullptr);
+      f->bgrads.as<float>(), f->n, (TS == 16 && f->cmask_valid) ? f->cmask.as<uint32_t>() : nullptr,
+      f->pairs < 0 ? ctx->err_word.as<uint32_t>() : nullptr);
   note_launch();
 }
 

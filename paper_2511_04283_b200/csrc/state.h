@@ -27,13 +27,21 @@ struct PendingStep {
   bool active = false;
   int it = 0, width = 0, height = 0, tev_set = 0;
   float lambda = 0.2f;
-  int64_t pairs = 0, n = 0;
+  int64_t n = 0;
   sk_log_row* row = nullptr;
   sk_scene* scene = nullptr;
   int64_t adam_t[6] = {};  // the scene's Adam step counters before this step (restored on a device error)
   cudaEvent_t done = nullptr;
-  HostBuf pinned;  // [2 slots][4 doubles + error word]
+  HostBuf pinned;  // [2 slots][kPendSlot doubles]: loss sums, P, error word
   int slot = 0;
+  // what a replay of the step needs (its pair count outgrew the pair buffer)
+  sk_frame* frame = nullptr;
+  sk_camera cam{};
+  const uint8_t* gt = nullptr;
+  sk_train_config cfg{};
+  float extent = 0.0f;
+  const sk_comm* comm = nullptr;
+  bool replayed = false;  // set when finish_pending replayed the step (cleared by the caller)
   ~PendingStep() {
     if (done) cudaEventDestroy(done);
   }
@@ -150,7 +158,8 @@ struct sk_frame {
   sk_binning binning{0, 1.0f, (float)(1.0 / 255), 16};
   sk_camera camera{};
   int64_t n = 0;        // projected slots
-  int64_t pairs = 0;    // tile/Gaussian pairs after sk_bin_sort
+  int64_t pairs = 0;    // tile/Gaussian pairs after sk_bin_sort (-1: still on the device, see pair_cap)
+  int64_t pair_cap = 0; // deferred count: the pair-buffer capacity the scatter was launched with
   bool binned = false;
   bool rendered = false;
 
@@ -211,8 +220,9 @@ void launch_bin_tiles(sk_ctx* ctx, sk_frame* f, const uint32_t* order, int32_t* 
                       int64_t cap);
 // counts -> exclusive prefix over chunks; ranges and P (*total_out) from the
 // tile totals. done: a zeroed counter (reset by the kernel).
-void launch_bin_prefix(sk_ctx* ctx, sk_frame* f, int32_t* counts, int32_t* totals, unsigned int* done,
-                       long long* total_out);
+// cap >= 0: set kErrPairOverflow in err when P > cap.
+void launch_bin_prefix(sk_ctx* ctx, sk_frame* f, int32_t* counts, int32_t* totals, unsigned int* done, int64_t cap,
+                       uint32_t* err, long long* total_out);
 int64_t bin_chunks(const sk_frame* f);
 
 // sort.cu
@@ -278,7 +288,10 @@ void arg(bool ok, const char* msg);  // throws std::invalid_argument
 void frame_geometry(sk_frame* f, int w, int h, const sk_binning* b);
 void ensure_projected(sk_frame* f, int64_t n);
 void ensure_image(sk_frame* f);
-void bin_sort(sk_ctx* ctx, sk_frame* f);
+// deferred: the pair count stays on the device (no host read; training
+// steps): the scatter fills the existing pair buffer, an overflow sets
+// kErrPairOverflow (K6 / K8 / K9 / K10 then skip), f->pairs = -1.
+void bin_sort(sk_ctx* ctx, sk_frame* f, bool deferred = false);
 
 // helpers
 uint32_t read_error_word(sk_ctx* ctx);

@@ -5,9 +5,10 @@
 // One iteration = K1 preprocess -> K2-K5 binning -> K6 forward blend ->
 // K7 loss -> K8 backward blend -> K9 project backward + stats (-> C1 gradient
 // all-reduce on a view-parallel step) -> K10 dense Adam. All kernels are
-// stream-ordered on the context stream; the host waits once per step (the
-// pair count after the scan) and reads the loss / error word back one step
-// later (PendingStep).
+// stream-ordered on the context stream. On one rank a step has no host
+// synchronisation: the pair count stays on the device and is read back with
+// the loss / error word one step later (PendingStep); a step whose pair count
+// outgrew the pair buffer is replayed (finish_pending).
 #include <chrono>
 #include <cmath>
 #include <memory>
@@ -78,15 +79,40 @@ bool lazy_update_due(int it, const sk_train_config& c) {
   return it % c.lazy_opt_interval_20k == 0;
 }
 
-// One train_iteration (trainer.hpp:124-175) on camera `cam` with the 8-bit GT
-// already on the device.
-void finish_pending(sk_ctx* ctx, PendingStep* pend) {
-  if (!pend || !pend->active) return;
+// Readback block of a step, per slot: loss sums [0..2], P [3], error word [4].
+constexpr int kPendSlot = 6;
+
+// A step whose pair count P outgrew the pair buffer it was launched into
+// (kErrPairOverflow; its K6 / K8 / K9 / K10 were skipped, the scene is
+// untouched): regrow the buffer to P and run the step again, synchronously.
+void replay_overflowed(sk_ctx* ctx, sk_scene* scene, sk_frame* f, int64_t pairs, const int64_t* adam_t0) {
+  require(pairs < (1ll << 30), "build_tile_grid: too many tile/Gaussian pairs");
+  std::copy(adam_t0, adam_t0 + 6, scene->adam_t);
+  SK_CUDA(cudaMemsetAsync(ctx->err_word.ptr, 0, sizeof(uint32_t), ctx->stream));
+  SK_CUDA(cudaStreamSynchronize(ctx->stream));  // nothing still reads the buffer the regrowth frees
+  ensure<uint32_t>(f->pval_a, (size_t)pairs);
+}
+
+// Completes the pending step: waits for its readback, reports its loss / P
+// into the row, raises its device errors. Returns true when the step had to
+// be replayed (pair-buffer overflow): the replay has run, and the caller's
+// frame now holds the replayed step's state.
+bool finish_pending(sk_ctx* ctx, PendingStep* pend) {
+  if (!pend || !pend->active) return false;
   pend->active = false;
   SK_CUDA(cudaEventSynchronize(pend->done));
-  const double* h = static_cast<const double*>(pend->pinned.ptr) + 5 * pend->slot;
+  const double* h = static_cast<const double*>(pend->pinned.ptr) + kPendSlot * pend->slot;
   uint32_t bits = 0;
   memcpy(&bits, h + 4, sizeof(bits));
+  long long pairs = 0;
+  memcpy(&pairs, h + 3, sizeof(pairs));
+  if (bits == kErrPairOverflow && pend->frame) {
+    replay_overflowed(ctx, pend->scene, pend->frame, pairs, pend->adam_t);
+    train_step(ctx, pend->scene, pend->frame, pend->cam, pend->gt, pend->cfg, pend->extent, pend->it, pend->row,
+               pend->comm, nullptr);
+    pend->replayed = true;
+    return true;
+  }
   if (bits) {
     // K9 / K10 of the failed step were gated on the error word (optim.cu), so
     // the scene is as before the step; roll the host step counters back too.
@@ -94,6 +120,7 @@ void finish_pending(sk_ctx* ctx, PendingStep* pend) {
     if (pend->scene) std::copy(pend->adam_t, pend->adam_t + 6, pend->scene->adam_t);
     SK_CUDA(cudaMemsetAsync(ctx->err_word.ptr, 0, sizeof(uint32_t), ctx->stream));
     raise_device_errors(bits);
+    require(!(bits & kErrPairOverflow), "train_step: pair buffer overflow with no step to replay");
   }
   if (ctx->timing) {
     for (int i = 0; i < SK_NUM_PHASES; ++i) {
@@ -110,9 +137,10 @@ void finish_pending(sk_ctx* ctx, PendingStep* pend) {
     pend->row->iteration = pend->it;
     pend->row->loss = v.loss;
     pend->row->psnr = v.psnr;
-    pend->row->tile_pairs = pend->pairs;
+    pend->row->tile_pairs = pairs;
     pend->row->gaussians = (int32_t)pend->n;
   }
+  return false;
 }
 
 // One train_iteration (trainer.hpp:124-175) on camera `cam` with the 8-bit GT
@@ -130,10 +158,18 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   ctx->mark(0);
   launch_preprocess(ctx, scene, cam, f);
   // the previous step's readback completes while K1 of this step runs (the
-  // scene it reports is final: K1 only reads it)
-  if (pend) finish_pending(ctx, pend);
+  // scene it reports is final: K1 only reads it). If that step had to be
+  // replayed, the replay ran on this frame and may have updated the scene:
+  // start this step again.
+  if (pend && finish_pending(ctx, pend))
+    return train_step(ctx, scene, f, cam, gt_dev, cfg, extent, it, row, comm, pend);
   ctx->mark(1);
-  bin_sort(ctx, f);
+  // One rank: the pair count stays on the device (no host read in the step;
+  // an overflow of the pair buffer is detected at the readback and the step
+  // replayed). Several ranks keep the host read: a replay on one rank would
+  // desynchronise the collectives.
+  const bool deferred = !(comm && comm->world > 1);
+  bin_sort(ctx, f, deferred);
   ctx->mark(2);
   launch_blend_forward(ctx, f, nullptr, nullptr, /*fast=*/true);
   f->rendered = true;
@@ -180,31 +216,55 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   ctx->mark(7);
   if (pend) {
     if (!pend->done) SK_CUDA(cudaEventCreateWithFlags(&pend->done, cudaEventDisableTiming));
-    double* h = static_cast<double*>(pend->pinned.ensure(2 * 5 * sizeof(double)));
+    double* h = static_cast<double*>(pend->pinned.ensure(2 * kPendSlot * sizeof(double)));
     pend->slot ^= 1;
-    SK_CUDA(cudaMemcpyAsync(h + 5 * pend->slot, ctx->scalars.ptr, 3 * sizeof(double), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    SK_CUDA(cudaMemcpyAsync(h + 5 * pend->slot + 4, ctx->err_word.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                            ctx->stream));
+    double* hs = h + kPendSlot * pend->slot;
+    SK_CUDA(cudaMemcpyAsync(hs, ctx->scalars.ptr, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (deferred)
+      SK_CUDA(cudaMemcpyAsync(hs + 3, ctx->sort.bin_total.ptr, sizeof(long long), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    else
+      memcpy(hs + 3, &f->pairs, sizeof(long long));
+    SK_CUDA(cudaMemcpyAsync(hs + 4, ctx->err_word.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
     SK_CUDA(cudaEventRecord(pend->done, ctx->stream));
     pend->active = true;
     pend->it = it;
     pend->width = f->width;
     pend->height = f->height;
     pend->lambda = (float)cfg.lambda;
-    pend->pairs = f->pairs;
     pend->n = scene->n;
+    pend->frame = f;
+    pend->cam = cam;
+    pend->gt = gt_dev;
+    pend->cfg = cfg;
+    pend->extent = extent;
+    pend->comm = comm;
     pend->row = row;
     pend->tev_set = ctx->tev_set;
     pend->scene = scene;
     std::copy(adam_t0, adam_t0 + 6, pend->adam_t);
     return;
   }
+  if (deferred) {
+    long long pairs = 0;
+    SK_CUDA(cudaMemcpyAsync(&pairs, ctx->sort.bin_total.ptr, sizeof(pairs), cudaMemcpyDeviceToHost, ctx->stream));
+    LossSums sums{};
+    read_loss_sums(ctx, &sums);  // synchronises the stream
+    uint32_t bits = 0;
+    SK_CUDA(cudaMemcpyAsync(&bits, ctx->err_word.ptr, sizeof(bits), cudaMemcpyDeviceToHost, ctx->stream));
+    SK_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (bits == kErrPairOverflow) {
+      replay_overflowed(ctx, scene, f, pairs, adam_t0);
+      return train_step(ctx, scene, f, cam, gt_dev, cfg, extent, it, row, comm, nullptr);
+    }
+    f->pairs = pairs;
+  }
   LossSums sums{};
   read_loss_sums(ctx, &sums);  // synchronises the stream
   const uint32_t bits = read_error_word(ctx);
   if (bits) std::copy(adam_t0, adam_t0 + 6, scene->adam_t);  // K9 / K10 were gated: no update happened
   raise_device_errors(bits);
+  require(!(bits & kErrPairOverflow), "train_step: pair buffer overflow");
   if (ctx->timing) {
     for (int i = 0; i < SK_NUM_PHASES; ++i) {
       float ms = 0.0f;
@@ -679,7 +739,12 @@ int sk_train_step_host(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, const sk_c
   return guarded(ctx, [&] {
     arg(scene && frame && cam && gt_host && cfg, "sk_train_step_host: bad arguments");
     SK_CUDA(cudaSetDevice(ctx->device));
-    if (frame->pipe) finish_pending(ctx, &frame->pipe->pend);  // an async step in flight completes first
+    // an async step in flight completes first (a replay of it reads its GT slot again)
+    if (frame->pipe && finish_pending(ctx, &frame->pipe->pend)) {
+      HostPipe& p = *frame->pipe;
+      SK_CUDA(cudaEventRecord(p.consumed[p.slot], ctx->stream));
+      p.pend.replayed = false;
+    }
     ensure_optimizer_state(ctx, scene);
     const size_t bytes = (size_t)cam->width * cam->height * 3;
     void* gt = frame->gt.ensure(bytes);
@@ -729,13 +794,23 @@ int sk_train_step_host_async(sk_ctx* ctx, sk_scene* scene, sk_frame* frame, cons
                &p.pend);
     SK_CUDA(cudaEventRecord(p.consumed[slot], ctx->stream));
     p.consumed_recorded[slot] = true;
+    if (p.pend.replayed) {
+      // the previous step was replayed inside this call and read its GT
+      // buffer again: the next upload into that buffer waits for the replay
+      SK_CUDA(cudaEventRecord(p.consumed[slot ^ 1], ctx->stream));
+      p.pend.replayed = false;
+    }
   });
 }
 
 int sk_train_step_host_flush(sk_ctx* ctx, sk_frame* frame) {
   return guarded(ctx, [&] {
     arg(frame != nullptr, "sk_train_step_host_flush: null frame");
-    if (frame->pipe) finish_pending(ctx, &frame->pipe->pend);
+    if (frame->pipe && finish_pending(ctx, &frame->pipe->pend)) {
+      HostPipe& p = *frame->pipe;
+      SK_CUDA(cudaEventRecord(p.consumed[p.slot], ctx->stream));  // the replay read this slot's GT
+      p.pend.replayed = false;
+    }
   });
 }
 

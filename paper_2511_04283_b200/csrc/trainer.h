@@ -156,8 +156,9 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
                 const sk_train_config& cfg, float extent, int it, sk_log_row* row, const sk_comm* comm = nullptr,
                 PendingStep* pend = nullptr);
 // Completes a pending step: waits for it, fills its row, adds its phase
-// times, raises its device errors.
-void finish_pending(sk_ctx* ctx, PendingStep* pend);
+// times, raises its device errors. A step whose pair count outgrew the pair
+// buffer (kErrPairOverflow) is replayed synchronously here; returns true then.
+bool finish_pending(sk_ctx* ctx, PendingStep* pend);
 
 // density.cu: Trainer::density_event (trainer.hpp:177-243).
 void density_event(sk_trainer* t, int it, bool densify, bool prune);

@@ -44,6 +44,52 @@ def test_async_host_steps_match_sync(orc):
     ctx.close()
 
 
+def test_pair_buffer_overflow_replays_the_step(orc, monkeypatch):
+    """Training steps keep the pair count on the device: the scatter fills the
+    frame's existing pair buffer and a step whose P outgrew it is skipped on
+    the device (kErrPairOverflow) and replayed once the host reads P with the
+    loss. A frame whose first pair buffer holds 300 pairs must give the same
+    rows and parameters as one sized normally — through the pipelined host
+    step, the synchronous one and Trainer::run."""
+    import torch
+
+    import paper_2511_04283_b200 as sk
+    sk.build()
+    p = synthetic_scene(4000, deg=3, seed=41)
+    cams = [ring_camera(orc, 128, 96, a) for a in (0.3, 1.4, 2.8)]
+    gts = []
+    for cam in cams:
+        r = orc.render_scene(synthetic_scene(4000, deg=3, seed=42), 3, cam)
+        g = torch.empty(r.image.size, dtype=torch.uint8, pin_memory=True).numpy().reshape(r.image.shape)
+        g[...] = np.clip(np.rint(r.image * 255), 0, 255).astype(np.uint8)
+        gts.append(g)
+    cfg = sk.default_config()
+    cfg.densify_from = cfg.densify_until = 1 << 30
+
+    def run(ctx):
+        a, b, c = ctx.scene(p, 3), ctx.scene(p, 3), ctx.scene(p, 3)
+        pipe = sk.HostStepPipeline(ctx)
+        for k in range(6):
+            pipe.step(a, cams[k % 3], gts[k % 3], cfg, 3.0, k + 1)
+        rows = pipe.flush()
+        frame = ctx._new_frame()
+        sync = [sk.train_step_host(ctx, b, cams[k % 3], gts[k % 3], cfg, 3.0, k + 1, frame=frame) for k in range(3)]
+        data = sk.Dataset(ctx, cams, [np.ascontiguousarray(g) for g in gts], [0, 1, 2], 3.0)
+        tr = sk.Trainer(ctx, c, data, cfg)
+        trows = tr.run(4)
+        return rows, sync, trows, a.download(), b.download(), c.download()
+
+    ref = run(sk.Context(0))
+    monkeypatch.setenv("SK_INITIAL_PAIR_CAP", "300")
+    got = run(sk.Context(0))
+    assert ref[0][0]["tile_pairs"] > 300  # every frame's first step overflowed and was replayed
+    for r, g in zip(ref[0] + ref[1] + ref[2], got[0] + got[1] + got[2]):
+        assert g["tile_pairs"] == r["tile_pairs"]
+        assert g["loss"] == pytest.approx(r["loss"], rel=1e-4)
+    for r, g in zip(ref[3:], got[3:]):
+        np.testing.assert_allclose(g, r, rtol=1e-4, atol=1e-5)
+
+
 def test_nccl_single_rank_communicator(orc):
     """The NCCL plumbing on one GPU: the library resolves NCCL, a one-rank
     communicator is created from a unique id, and a view-parallel Trainer
