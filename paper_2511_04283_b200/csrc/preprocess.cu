@@ -161,6 +161,11 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
     culled();
     return;
   }
+  // L1 prefetch of the SH rows (no registers held): they land while the
+  // projection, covariance and culling arithmetic below runs (K1 -2%)
+#pragma unroll
+  for (int c = SK_COMP_SH; c < SK_COMP_SH + 3 * (DEG + 1) * (DEG + 1); ++c)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p + c * stride + i));
   // projection_jacobian (camera.hpp:80-87)
   const float iz = 1.0f / t2;
   const float iz2 = iz * iz;
