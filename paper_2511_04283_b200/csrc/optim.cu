@@ -454,6 +454,17 @@ __global__ void __launch_bounds__(kAdamThreads) adam_kernel(float* __restrict__ 
   }
 }
 
+// The step's readback (loss sums, pair count, error word) written straight
+// into the pinned host slot by the step's last kernel: no copy-engine
+// transfers queued behind the step on the stream.
+__device__ __forceinline__ void write_readback(const StepReadback& rb) {
+  rb.dst[0] = __ldcg(rb.sums);
+  rb.dst[1] = __ldcg(rb.sums + 1);
+  rb.dst[2] = __ldcg(rb.sums + 2);
+  rb.dst[3] = __longlong_as_double(__ldcg(rb.pairs));
+  rb.dst[4] = __longlong_as_double((long long)__ldcg(rb.err));
+}
+
 // K9 + K10 fused (one GPU, dense Adam): the gradients of a CTA's 128
 // Gaussians stay in its shared-memory tile and are consumed there by the
 // Adam update of the same Gaussians, so the 59-component gradient buffer is
@@ -470,8 +481,10 @@ template <int DEG>
 __global__ void __launch_bounds__(kPbThreads, kK9MinBlocks) project_bwd_adam_kernel(
     float* __restrict__ params, int64_t stride, int64_t n, CamParams cam, const float* __restrict__ radius,
     const float4* __restrict__ conic4, const float* __restrict__ bg, int64_t gstride, float* __restrict__ am,
-    float* __restrict__ av, AdamParams ap, Stats st, bool do_stats, const uint32_t* __restrict__ err) {
+    float* __restrict__ av, AdamParams ap, Stats st, bool do_stats, const uint32_t* __restrict__ err,
+    StepReadback rb) {
   constexpr int NC = 11 + 3 * (DEG + 1) * (DEG + 1);
+  if (rb.dst && blockIdx.x == 0 && threadIdx.x == 0) write_readback(rb);
   if (__ldg(err)) return;  // see project_bwd_kernel
   __shared__ __align__(16) float s_grad[NC * kPbThreads];
   __shared__ float s_exp2[64];
@@ -841,7 +854,7 @@ void reset_opacity_state(sk_ctx* ctx, sk_scene* s) {
 // Single-GPU step: K9 and K10 fused (project_bwd_adam_kernel). The gradient
 // buffer is not written.
 void launch_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const LearningRates& lrs, float position_lr,
-                                  bool update_sh_rest, bool do_stats) {
+                                  bool update_sh_rest, bool do_stats, const StepReadback& rb) {
   ensure_optimizer_state(ctx, s);
   require(s->capacity % 4 == 0, "adam: scene capacity must be a multiple of 4");
   const AdamParams ap = make_adam(s, lrs, position_lr, update_sh_rest);
@@ -852,7 +865,7 @@ void launch_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const L
     kern<<<grid, kPbThreads, 0, ctx->stream>>>(s->params.as<float>(), s->capacity, s->n, cp, f->radius.as<float>(),
                                                f->conic4.as<float4>(), f->bgrads.as<float>(), f->n,
                                                s->adam_m.as<float>(), s->adam_v.as<float>(), ap, make_stats(s),
-                                               do_stats, ctx->err_word.as<uint32_t>());
+                                               do_stats, ctx->err_word.as<uint32_t>(), rb);
   };
   switch (s->sh_degree) {
     case 0: go(project_bwd_adam_kernel<0>); break;

@@ -258,8 +258,17 @@ void ensure_optimizer_state(sk_ctx* ctx, sk_scene* s);
 void ensure_score_table(sk_ctx* ctx, sk_scene* s);
 void reset_score_table(sk_ctx* ctx, sk_scene* s);
 void launch_project_backward(sk_ctx* ctx, sk_scene* s, sk_frame* f, bool do_stats);
+// Where the fused kernel writes a training step's readback (dst: a pinned
+// host slot, or nullptr for none): dst[0..2] the loss sums, dst[3] the pair
+// count's bits, dst[4] the error word.
+struct StepReadback {
+  double* dst = nullptr;
+  const double* sums = nullptr;
+  const long long* pairs = nullptr;
+  const uint32_t* err = nullptr;
+};
 void launch_project_backward_adam(sk_ctx* ctx, sk_scene* s, sk_frame* f, const LearningRates& lrs, float position_lr,
-                                  bool update_sh_rest, bool do_stats);
+                                  bool update_sh_rest, bool do_stats, const StepReadback& rb = StepReadback{});
 void launch_adam(sk_ctx* ctx, sk_scene* s, const LearningRates& lrs, float position_lr, bool update_sh_rest);
 // K10 on Gaussians [rank x chunk, min(n, (rank + 1) x chunk)) with that
 // slice's gradients in gshard ([comps][chunk]); sharded C1 (comm.cu).

@@ -187,8 +187,25 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   // buffer (+ C1 over the ranks of a view-parallel step), then K10.
   sk_comm* c1 = const_cast<sk_comm*>(comm);
   const bool multi = comm && comm->world > 1;
-  if (!multi && !cfg.lazy_opt_enabled) {
-    launch_project_backward_adam(ctx, scene, f, lrs, pos_lr, true, true);
+  // pipelined single-rank step: the fused kernel writes the readback into the
+  // pending slot itself (no copies queued behind the step)
+  double* slot_dst = nullptr;
+  const bool fused = !multi && !cfg.lazy_opt_enabled;
+  if (pend) {
+    double* h = static_cast<double*>(pend->pinned.ensure(2 * kPendSlot * sizeof(double)));
+    pend->slot ^= 1;
+    slot_dst = h + kPendSlot * pend->slot;
+  }
+  const bool in_kernel_readback = pend && fused && deferred && scene->n > 0;
+  if (fused) {
+    StepReadback rb;
+    if (in_kernel_readback) {
+      rb.dst = slot_dst;
+      rb.sums = ctx->scalars.as<double>();
+      rb.pairs = ctx->sort.bin_total.as<long long>();
+      rb.err = ctx->err_word.as<uint32_t>();
+    }
+    launch_project_backward_adam(ctx, scene, f, lrs, pos_lr, true, true, rb);
     ctx->mark(6);
   } else {
   launch_project_backward(ctx, scene, f, true);
@@ -216,16 +233,17 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   ctx->mark(7);
   if (pend) {
     if (!pend->done) SK_CUDA(cudaEventCreateWithFlags(&pend->done, cudaEventDisableTiming));
-    double* h = static_cast<double*>(pend->pinned.ensure(2 * kPendSlot * sizeof(double)));
-    pend->slot ^= 1;
-    double* hs = h + kPendSlot * pend->slot;
-    SK_CUDA(cudaMemcpyAsync(hs, ctx->scalars.ptr, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    if (deferred)
-      SK_CUDA(cudaMemcpyAsync(hs + 3, ctx->sort.bin_total.ptr, sizeof(long long), cudaMemcpyDeviceToHost,
-                              ctx->stream));
-    else
-      memcpy(hs + 3, &f->pairs, sizeof(long long));
-    SK_CUDA(cudaMemcpyAsync(hs + 4, ctx->err_word.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    double* hs = slot_dst;
+    if (!in_kernel_readback) {
+      SK_CUDA(cudaMemcpyAsync(hs, ctx->scalars.ptr, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      if (deferred)
+        SK_CUDA(cudaMemcpyAsync(hs + 3, ctx->sort.bin_total.ptr, sizeof(long long), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+      else
+        memcpy(hs + 3, &f->pairs, sizeof(long long));
+      hs[4] = 0.0;  // the error word's 4 bytes land in the low half of the zeroed slot
+      SK_CUDA(cudaMemcpyAsync(hs + 4, ctx->err_word.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    }
     SK_CUDA(cudaEventRecord(pend->done, ctx->stream));
     pend->active = true;
     pend->it = it;
