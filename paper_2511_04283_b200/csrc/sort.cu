@@ -96,7 +96,7 @@ template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int64_t n, int shift, uint32_t dmask, const uint32_t* __restrict__ digit_base,
-    uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
+    unsigned long long* __restrict__ status, uint32_t epoch, uint32_t* __restrict__ tile_counter) {
   constexpr int kTileT = kSortThreads * ITEMS;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_hist[kSortWarps][kRadix];
@@ -158,8 +158,12 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
     s_hist[w][digit] = total;
     total += c;
   }
-  uint32_t* my_status = status + (size_t)tile * kRadix + digit;
-  st_relaxed(my_status, (tile == 0 ? kFlagInc : kFlagAgg) | total);
+  // look-back words: (pass epoch << 32) | flag | 30-bit count; words of
+  // earlier passes carry an older epoch and read as unpublished, so the
+  // status array is never cleared between passes
+  const unsigned long long tag = (unsigned long long)epoch << 32;
+  unsigned long long* my_status = status + (size_t)tile * kRadix + digit;
+  st_relaxed64(my_status, tag | (tile == 0 ? kFlagInc : kFlagAgg) | total);
 
   // Block-local exclusive scan of the digit totals.
   {
@@ -187,8 +191,14 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
     for (;;) {
       uint32_t st[kLookback];
 #pragma unroll
-      for (int w = 0; w < kLookback; ++w)
-        st[w] = j - w >= 0 ? ld_relaxed(status + (size_t)(j - w) * kRadix + digit) : kFlagInc;
+      for (int w = 0; w < kLookback; ++w) {
+        if (j - w >= 0) {
+          const unsigned long long x = ld_relaxed64(status + (size_t)(j - w) * kRadix + digit);
+          st[w] = (x >> 32) == epoch ? (uint32_t)x : 0u;  // another pass's word: not yet published
+        } else {
+          st[w] = kFlagInc;
+        }
+      }
       int used = 0;
       bool found = false;
 #pragma unroll
@@ -203,7 +213,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
       if (found) break;
       j -= used;
     }
-    st_relaxed(my_status, kFlagInc | (excl + total));
+    st_relaxed64(my_status, tag | kFlagInc | (excl + total));
   }
   s_global[digit] = digit_base[digit] + excl;
   __syncthreads();
@@ -254,21 +264,30 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
   const int tile_keys = kSortThreads * kSortItems;
   const int64_t tiles = (n + tile_keys - 1) / tile_keys;
   require(tiles < (1ll << 31), "radix_sort_pairs: too many keys");
-  uint32_t* hist = ensure<uint32_t>(ctx->sort.hist, (size_t)kMaxPasses * kRadix);
-  uint32_t* status = ensure<uint32_t>(ctx->sort.status, (size_t)tiles * kRadix);
-  uint32_t* counters = ensure<uint32_t>(ctx->sort.counters, kMaxPasses);
+  // digit histograms [passes][256] followed by the passes' tile tickets: one memset
+  uint32_t* hist = ensure<uint32_t>(ctx->sort.hist, (size_t)kMaxPasses * kRadix + kMaxPasses);
+  uint32_t* counters = hist + kMaxPasses * kRadix;
+  void* before = ctx->sort.status.ptr;
+  auto* status = ensure<unsigned long long>(ctx->sort.status, (size_t)tiles * kRadix);
   cudaStream_t s = ctx->stream;
-  SK_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * kMaxPasses, s));
-  SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kRadix, s));
+  if (status != before) {  // fresh memory could hold any tag: clear it once, the epochs restart
+    SK_CUDA(cudaMemsetAsync(status, 0, ctx->sort.status.bytes, s));
+    ctx->sort.epoch = 0;
+  }
+  SK_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * ((size_t)kMaxPasses * kRadix + kMaxPasses), s));
   const int hist_blocks = (int)std::min<int64_t>((n + 4095) / 4096, 148 * 8);
   radix_hist_kernel<<<hist_blocks, 256, 0, s>>>(keys, n, passes, width, hist);
   note_launch();
   radix_bases_kernel<<<passes, kRadix, 0, s>>>(hist);
   note_launch();
   for (int p = 0; p < passes; ++p) {
-    SK_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t) * (size_t)tiles * kRadix, s));
+    if (++ctx->sort.epoch == 0) {  // 2^32 passes: clear once more rather than reuse a tag
+      SK_CUDA(cudaMemsetAsync(status, 0, ctx->sort.status.bytes, s));
+      ctx->sort.epoch = 1;
+    }
     onesweep_kernel<kSortItems><<<(unsigned)tiles, kSortThreads, 0, s>>>(
-        keys, vals, keys_alt, vals_alt, n, p * width, dmask, hist + p * kRadix, status, counters + p);
+        keys, vals, keys_alt, vals_alt, n, p * width, dmask, hist + p * kRadix, status, ctx->sort.epoch,
+        counters + p);
     note_launch();
     std::swap(keys, keys_alt);
     std::swap(vals, vals_alt);

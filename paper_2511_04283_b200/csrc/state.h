@@ -10,9 +10,9 @@ namespace sk {
 
 // Scratch for the radix sort and the decoupled look-back scans.
 struct SortTemp {
-  DevBuf hist;      // [passes][256] digit counts, then exclusive bases
-  DevBuf status;    // [tiles][256] look-back words
-  DevBuf counters;  // tile tickets, one per pass
+  DevBuf hist;      // [passes][256] digit counts, then exclusive bases; then one tile ticket per pass
+  DevBuf status;    // uint64 [tiles][256] epoch-tagged look-back words (never cleared between passes)
+  uint32_t epoch = 0;  // look-back tag of the last pass
   DevBuf bin_counts;  // int32 [chunks][tiles] (K3 counting scatter)
   DevBuf bin_totals;  // int32 [tiles]
   DevBuf bin_total;   // long long [2]: P, then the prefix kernel's done-counter
