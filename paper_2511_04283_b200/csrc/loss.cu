@@ -441,9 +441,12 @@ void launch_loss(sk_ctx* ctx, sk_frame* f, const void* gt, bool gt_u8, float lam
   const int W = f->width, H = f->height;
   const size_t plane = (size_t)W * H;
   float* dimage = want_grad ? ensure<float>(f->dimage, 3 * plane) : nullptr;
+  // sums[0..2] are written whole by the kernel's last CTA, which also resets
+  // the ticket: only a freshly allocated buffer needs clearing
+  const void* before = ctx->scalars.ptr;
   double* sums = ensure<double>(ctx->scalars, 5);
   unsigned int* ticket = reinterpret_cast<unsigned int*>(sums + 4);
-  SK_CUDA(cudaMemsetAsync(sums, 0, 5 * sizeof(double), ctx->stream));
+  if (sums != before) SK_CUDA(cudaMemsetAsync(sums, 0, 5 * sizeof(double), ctx->stream));
   const int dev = ctx->device;
   if (dev >= 64 || g_slots[dev] == 0) {
     const int s = std::min(std::min(march_slots<true, true>(dev), march_slots<true, false>(dev)),

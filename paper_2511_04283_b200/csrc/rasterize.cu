@@ -307,8 +307,8 @@ __global__ void __launch_bounds__(TS* TS / PIX, kFwdMinBlocks * 128 / (TS * TS /
       all_done = ad;
     }
     // contribution mask of this warp block for the batch (read by K8, which
-    // then skips entries no pixel of its block blended); unwalked batches
-    // keep the frame-start zeros
+    // then skips entries no pixel of its block blended); K8 never reads an
+    // unwalked batch (every pixel's last contributor lies in a walked one)
     const uint32_t bits = __reduce_or_sync(0xffffffffu, lane_bits);
     if (cmask && lane == 0) cmask[(size_t)(cmask_word(range.x, tile) + ((b0 - range.x) >> 5)) * kWarps + warp] = bits;
     __syncwarp();
@@ -371,8 +371,9 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
     uint32_t* cm = nullptr;
     if (TS == 16 && PIX == 2) {  // K8 consumes the masks at 16x16 tiles
       const size_t words = cmask_words(f->pairs < 0 ? f->pair_cap : f->pairs, tiles) * (size_t)(TS * TS / PIX / 32);
+      // no clearing: K8 reads the words of batches up to its block's last
+      // contributor only, all of which this K6 warp walked and wrote
       cm = ensure<uint32_t>(f->cmask, words);
-      SK_CUDA(cudaMemsetAsync(cm, 0, words * sizeof(uint32_t), ctx->stream));
     }
     f->cmask_valid = cm != nullptr;
     f->fast_blend = fast;
