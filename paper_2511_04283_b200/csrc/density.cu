@@ -28,34 +28,54 @@
 namespace sk {
 namespace {
 
+// Block-level min / max of non-negative floats (as ordered bits), then one
+// atomic pair per CTA: a per-warp atomic on the same two words from every
+// warp of a 2 MPix frame serialises ~130K atomics at one L2 slice (90 us).
+__device__ __forceinline__ void block_minmax_atomic(uint32_t lo, uint32_t hi, uint32_t* __restrict__ lohi) {
+  __shared__ uint32_t s_lo[32], s_hi[32];
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) s_lo[warp] = lo, s_hi[warp] = hi;
+  __syncthreads();
+  if (warp == 0) {
+    lo = lane < nw ? s_lo[lane] : 0xffffffffu;
+    hi = lane < nw ? s_hi[lane] : 0u;
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (lane == 0) {
+      atomicMin(&lohi[0], lo);
+      atomicMax(&lohi[1], hi);
+    }
+  }
+}
+
 // ---- K11: raw error map + min / max ---------------------------------------
-__global__ void error_raw_kernel(const float* __restrict__ image, const void* __restrict__ gt, bool gt_u8, int W, int H,
-                                 float* __restrict__ raw, uint32_t* __restrict__ lohi) {
+// Grid-stride over the pixels (a few CTAs per SM); the 8-bit GT decoded
+// byte / 255 through a table of the same IEEE quotients.
+__global__ void __launch_bounds__(256) error_raw_kernel(const float* __restrict__ image, const void* __restrict__ gt,
+                                                        bool gt_u8, int W, int H, float* __restrict__ raw,
+                                                        uint32_t* __restrict__ lohi) {
+  __shared__ float s_u8[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_u8[i] = __fdiv_rn((float)i, 255.0f);
+  __syncthreads();
   const int64_t n = (int64_t)W * H;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  float v = 0.0f;
-  const bool ok = p < n;
-  if (ok) {
+  uint32_t lo = 0xffffffffu, hi = 0u;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     float d[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const float g = gt_u8 ? __fdiv_rn((float)static_cast<const uint8_t*>(gt)[p * 3 + c], 255.0f)
-                            : static_cast<const float*>(gt)[p * 3 + c];
+      const float g = gt_u8 ? s_u8[static_cast<const uint8_t*>(gt)[p * 3 + c]] : static_cast<const float*>(gt)[p * 3 + c];
       d[c] = image[c * n + p] - g;
     }
     // (rendered - gt).cwiseAbs().sum() / T(3)
-    v = ((fabsf(d[0]) + fabsf(d[1])) + fabsf(d[2])) / 3.0f;
+    const float v = ((fabsf(d[0]) + fabsf(d[1])) + fabsf(d[2])) / 3.0f;
     raw[p] = v;
+    // raw >= 0: ordering of the float bits is the ordering of the values
+    lo = min(lo, __float_as_uint(v));
+    hi = max(hi, __float_as_uint(v));
   }
-  // raw >= 0: ordering of the float bits is the ordering of the values
-  uint32_t lo = ok ? __float_as_uint(v) : 0xffffffffu;
-  uint32_t hi = ok ? __float_as_uint(v) : 0u;
-  lo = __reduce_min_sync(0xffffffffu, lo);
-  hi = __reduce_max_sync(0xffffffffu, hi);
-  if ((threadIdx.x & 31) == 0) {
-    atomicMin(&lohi[0], lo);
-    atomicMax(&lohi[1], hi);
-  }
+  block_minmax_atomic(lo, hi, lohi);
 }
 
 // normalized = (raw - lo) / (hi - lo) (all zero if degenerate); mask = normalized > tau
@@ -90,14 +110,7 @@ __global__ void scores_kernel(const int32_t* __restrict__ rows, int64_t row_stri
     s_d[i] = sd / (float)k;
     s_p_raw[i] = sp;
   }
-  uint32_t lo = ok ? __float_as_uint(sp) : 0xffffffffu;
-  uint32_t hi = ok ? __float_as_uint(sp) : 0u;
-  lo = __reduce_min_sync(0xffffffffu, lo);
-  hi = __reduce_max_sync(0xffffffffu, hi);
-  if ((threadIdx.x & 31) == 0) {
-    atomicMin(&lohi[0], lo);
-    atomicMax(&lohi[1], hi);
-  }
+  block_minmax_atomic(ok ? __float_as_uint(sp) : 0xffffffffu, ok ? __float_as_uint(sp) : 0u, lohi);
 }
 
 __global__ void minmax_normalize_kernel(const float* __restrict__ v, const uint32_t* __restrict__ lohi, int64_t n,
@@ -579,8 +592,8 @@ void score_view(sk_ctx* c, sk_scene* s, sk_frame* f, const sk_camera& cam, const
   uint32_t* lohi = ensure<uint32_t>(c->ev.lohi, 4);
   const uint32_t init[2] = {0xffffffffu, 0u};
   h2d(c, lohi, init, 2);
-  error_raw_kernel<<<blocks(npx), 256, 0, c->stream>>>(f->image.as<float>(), gt, gt_u8_device, cam.width,
-                                                        cam.height, raw, lohi);
+  error_raw_kernel<<<std::min<unsigned>(blocks(npx), 148 * 8), 256, 0, c->stream>>>(
+      f->image.as<float>(), gt, gt_u8_device, cam.width, cam.height, raw, lohi);
   note_launch();
   error_mask_kernel<<<blocks(npx), 256, 0, c->stream>>>(raw, lohi, npx, tau, mask, nullptr);
   note_launch();
@@ -1007,7 +1020,8 @@ int sk_error_maps(sk_ctx* ctx, const float* rendered, const float* gt, int width
     uint32_t* lohi = ensure<uint32_t>(ctx->ev.lohi, 4);
     const uint32_t init[2] = {0xffffffffu, 0u};
     h2d(ctx, lohi, init, 2);
-    error_raw_kernel<<<blocks(npx), 256, 0, ctx->stream>>>(f.image.as<float>(), g, false, width, height, raw, lohi);
+    error_raw_kernel<<<std::min<unsigned>(blocks(npx), 148 * 8), 256, 0, ctx->stream>>>(f.image.as<float>(), g, false,
+                                                                                         width, height, raw, lohi);
     note_launch();
     error_mask_kernel<<<blocks(npx), 256, 0, ctx->stream>>>(raw, lohi, npx, tau, mask, nrm);
     note_launch();
