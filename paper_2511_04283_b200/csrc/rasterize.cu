@@ -122,6 +122,90 @@ __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) count_bl
   }
 }
 
+// K12 over K6's record (16x16 tiles): the masked pixels' contributors are
+// exactly the entries up to each pixel's last_entry whose alpha reaches
+// 1/255 — K6 of the same frame (exact form) recorded last_entry per pixel and,
+// per (32-entry batch, 8x8 warp block), the mask of entries some pixel of the
+// block blended. So a warp gathers only the marked entries of the batches up
+// to its masked pixels' last entry, needs no transmittance, and decides
+// alpha >= 1/255 with the hardware exp, recomputing the deterministic exp
+// only within 1e-5 of the threshold (as K8 does): the same decisions as K6,
+// bit for bit. Counts use one atomic per (entry, warp).
+template <int PIX>
+__global__ void __launch_bounds__(16 * 16 / PIX, 8) count_walk_kernel(
+    const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
+    const float4* __restrict__ conic_op, int W, int H, int tiles_x, const uint8_t* __restrict__ mask,
+    const int* __restrict__ last_entry, const uint32_t* __restrict__ cmask, int* __restrict__ counts) {
+  constexpr int TS = 16;
+  using WB = WarpBlock<TS, PIX>;
+  constexpr int kWarps = WB::kWarps;
+  __shared__ float4 s_xyq[kWarps][32];
+  __shared__ float4 s_co[kWarps][32];
+  __shared__ float s_exp[kNegExpTable];
+  stage_neg_exp_table(s_exp);
+  __syncthreads();
+  const SmemPinnedTable tab(s_exp);
+  const int tile = blockIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const WB wb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int px = tx * TS + wb.lx;
+  const int2 range = ranges[tile];
+  const float fpx = (float)px;
+  float fpy[PIX];
+  int last[PIX];
+  int my_last = range.x;
+#pragma unroll
+  for (int k = 0; k < PIX; ++k) {
+    const int py = ty * TS + wb.ly0 + 4 * k;
+    fpy[k] = (float)py;
+    last[k] = range.x;  // unmasked / outside: no entry
+    if (px < W && py < H && mask[(size_t)py * W + px] != 0) last[k] = last_entry[(size_t)py * W + px];
+    my_last = max(my_last, last[k]);
+  }
+  const int warp_last = __reduce_max_sync(0xffffffffu, my_last);
+  if (warp_last <= range.x) return;
+  const int64_t wbase = cmask_word(range.x, tile);
+  for (int kb = 0; range.x + 32 * kb < warp_last; ++kb) {
+    const int b0 = range.x + 32 * kb;
+    uint32_t m = __ldg(&cmask[(size_t)(wbase + kb) * kWarps + warp]);
+    const int lim = warp_last - b0;
+    if (lim < 32) m &= (1u << lim) - 1u;
+    if (!m) continue;
+    if ((m >> lane) & 1u) {
+      const uint32_t g = pair_val[b0 + lane];
+      const float4 co = conic_op[g];
+      float4 xyq, bb;
+      stage_entry(mean2d[g], co, xyq, bb);
+      xyq.w = __uint_as_float(g);
+      s_xyq[warp][lane] = xyq;
+      s_co[warp][lane] = co;
+    }
+    __syncwarp();
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const float4 mq = s_xyq[warp][j];
+      const float4 co = s_co[warp][j];
+      const int idx = b0 + j;
+      int hits = 0;
+#pragma unroll
+      for (int k = 0; k < PIX; ++k) {
+        const float dx = fpx - mq.x;
+        const float dy = fpy[k] - mq.y;
+        const float q = co.x * dx * dx + 2.0f * co.y * dx * dy + co.z * dy * dy;  // K6's exact q
+        if (idx >= last[k] || __float_as_uint(__fadd_rn(q, 0.0f)) > __float_as_uint(mq.z)) continue;
+        float raw = co.w * exp2f_approx(q * -0.72134752044448170f);
+        if (fabsf(raw - kAlphaMin) <= 1e-5f) raw = co.w * det_expf_neg(-0.5f * q, tab);
+        hits += (raw < kAlphaCap ? raw : kAlphaCap) < kAlphaMin ? 0 : 1;
+      }
+      hits = __reduce_add_sync(0xffffffffu, hits);
+      if (lane == 0 && hits) atomicAdd(&counts[__float_as_uint(mq.w)], hits);
+    }
+    __syncwarp();
+  }
+}
+
 // K6, warp-staged variant: each warp walks the tile's list for its own
 // 8 x 4·PIX pixel block independently — it stages 32 entries at a time (one
 // per lane: gather, q-cut box, exact ellipse test against its own block),
@@ -364,7 +448,13 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
   const auto* mean2d = f->mean2d.as<float2>();
   const auto* co = f->conic_op.as<float4>();
   const auto* rgb = f->rgb_depth.as<float4>();
-  if (mask)
+  if (mask && TS == 16 && PIX == 2 && f->cmask_valid && !f->fast_blend)
+    // the frame's last K6 (exact, on the current tile lists: binning clears
+    // cmask_valid) recorded last_entry and the contribution masks
+    count_walk_kernel<PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
+        ranges, f->pair_val, mean2d, co, f->width, f->height, f->tiles_x, mask, f->last_entry.as<int>(),
+        f->cmask.as<uint32_t>(), counts);
+  else if (mask)
     count_blend_kernel<TS, PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(ranges, f->pair_val, mean2d, co, f->width,
                                                                           f->height, f->tiles_x, mask, counts);
   else {
