@@ -344,22 +344,26 @@ __global__ void __launch_bounds__(TS* TS / PIX, kFwdMinBlocks * 128 / (TS * TS /
           if (!(ok0 || ok1)) continue;
           lane_bits |= 1u << j;
           const float4 c = s_rgb_w[j];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int k = h == 0 ? a : b;
-            const bool ok = h == 0 ? ok0 : ok1;
-            const float alpha = h == 0 ? al.x : al.y;
-            if (!ok) continue;
-            // (the colour sums may contract: K8 reads only T and last_entry)
-            const float w = T[k] * alpha;
-            C0[k] = fmaf(w, c.x, C0[k]);
-            C1[k] = fmaf(w, c.y, C1[k]);
-            C2[k] = fmaf(w, c.z, C2[k]);
-            ++n[k];
-            last[k] = b0 + j + 1;
-            T[k] = T[k] * (1.0f - alpha);
-            fpy[k] = T[k] < kTransmitMin ? __int_as_float(0x7fc00000) : fpy[k];
-          }
+          // both pixels in packed ops, a non-contributing one with alpha = 0
+          // (T, C unchanged exactly); the colour sums may contract: K8 reads
+          // only T and last_entry
+          const float2 al2 = make_float2(ok0 ? al.x : 0.0f, ok1 ? al.y : 0.0f);
+          float2 t2 = make_float2(T[a], T[b]);
+          const float2 w2 = __fmul2_rn(t2, al2);
+          float2 c0 = __ffma2_rn(w2, make_float2(c.x, c.x), make_float2(C0[a], C0[b]));
+          float2 c1 = __ffma2_rn(w2, make_float2(c.y, c.y), make_float2(C1[a], C1[b]));
+          float2 c2 = __ffma2_rn(w2, make_float2(c.z, c.z), make_float2(C2[a], C2[b]));
+          t2 = __fmul2_rn(t2, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al2.x, -al2.y)));
+          C0[a] = c0.x, C0[b] = c0.y;
+          C1[a] = c1.x, C1[b] = c1.y;
+          C2[a] = c2.x, C2[b] = c2.y;
+          T[a] = t2.x, T[b] = t2.y;
+          n[a] += ok0 ? 1 : 0;
+          n[b] += ok1 ? 1 : 0;
+          last[a] = ok0 ? b0 + j + 1 : last[a];
+          last[b] = ok1 ? b0 + j + 1 : last[b];
+          fpy[a] = t2.x < kTransmitMin ? __int_as_float(0x7fc00000) : fpy[a];
+          fpy[b] = t2.y < kTransmitMin ? __int_as_float(0x7fc00000) : fpy[b];
         }
         continue;
       }
