@@ -95,14 +95,20 @@ def test_blend_kats_gpu(ctx, orc):
     assert r.transmittance[3, 3] == pytest.approx(0.25)
 
 
-def test_footprint_counts_exact(ctx, orc):
-    rng = np.random.default_rng(45)
+@pytest.mark.parametrize("ts,opacity", [(16, 0.9), (16, 0.999), (8, 0.9), (32, 0.9)])
+def test_footprint_counts_exact(ctx, orc, ts, opacity):
+    """K12 counts: at 16-px tiles the walk over K6's record (contribution
+    masks + last_entry, alpha >= 1/255 decided with the hardware exp and a
+    deterministic-exp band), at 8 / 32 the masked recurrence; both exact.
+    Opacities up to 0.999 stack saturating tiles (early termination)."""
+    rng = np.random.default_rng(45 + ts)
+    b = orc.binning(tile_size=ts)
     for _ in range(8):
         n = 2 + int(rng.integers(40))
-        pg = orc.random_projected(rng, n, 48, 40, 0.9, dtype=np.float32)
+        pg = orc.random_projected(rng, n, 48, 40, opacity, dtype=np.float32)
         mask = (rng.uniform(size=(40, 48)) < 0.4).astype(np.uint8)
-        ref = orc.render_pg(pg, 48, 40, mask=mask)
-        ctx.set_projected(pg, 48, 40)
+        ref = orc.render_pg(pg, 48, 40, b, mask=mask)
+        ctx.set_projected(pg, 48, 40, b)
         got = ctx.blend_forward(mask=mask)
         assert np.array_equal(got.counts, ref.counts)
 
