@@ -298,6 +298,7 @@ int sk_frame_set_projected(sk_ctx* ctx, sk_frame* f, const sk_projected* pg, int
     set_device(ctx);
     frame_geometry(f, width, height, b);
     ensure_projected(f, n);
+    f->extras_valid = true;  // the caller's covariances; tiles and a* from the injection kernel
     std::vector<float2> mu(n);
     std::vector<float4> co(n), rgb(n), cov(n), c4(n);
     for (int64_t i = 0; i < n; ++i) {
@@ -416,6 +417,9 @@ int sk_frame_dims(const sk_frame* f, int* w, int* h) {
 int sk_frame_get_projected(sk_ctx* ctx, const sk_frame* f, sk_projected* out) {
   return guarded(ctx, [&] {
     arg(f && out, "sk_frame_get_projected: bad arguments");
+    arg(f->extras_valid || f->n == 0,
+        "sk_frame_get_projected: the frame was last projected by a training step (no covariance / tile counts); "
+        "run sk_preprocess on it first");
     set_device(ctx);
     const int64_t n = f->n;
     std::vector<float2> mu(n);

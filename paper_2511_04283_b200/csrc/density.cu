@@ -575,7 +575,7 @@ void score_view(sk_ctx* c, sk_scene* s, sk_frame* f, const sk_camera& cam, const
   frame_geometry(f, cam.width, cam.height, &bin);
   f->camera = cam;
   ensure_projected(f, n);
-  launch_preprocess(c, s, cam, f);
+  launch_preprocess(c, s, cam, f, /*extras=*/false);
   bin_sort(c, f);
   ensure_image(f);
   launch_blend_forward(c, f, nullptr, nullptr);

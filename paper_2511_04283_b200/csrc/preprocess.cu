@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
   val_out[i] = (uint32_t)i;  // the depth sort's payload (projected index)
   auto culled = [&]() {
     radius_out[i] = 0.0f;
-    tiles_out[i] = 0;
+    if (cov_out) tiles_out[i] = 0;
     rect_out[i] = make_int4(0, 0, -1, -1);  // K3 enumerates rectangles only
     key_out[i] = 0xffffffffu;
   };
@@ -302,12 +302,16 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
   mean2d[i] = make_float2(mx, my);
   conic_op[i] = make_float4(inv00, inv01, inv11, opacity);
   rgbd[i] = make_float4(rgb[0], rgb[1], rgb[2], t2);
-  cov_out[i] = make_float4(c[0][0], c[0][1], c[1][0], c[1][1]);
   conic4[i] = make_float4(inv00, inv01, inv10, inv11);
   radius_out[i] = radius;
-  tiles_out[i] = bo.count;
   rect_out[i] = bo.rect;
-  astar_out[i] = bo.a_star;
+  // the covariance and tile count only leave the device through
+  // sk_frame_get_projected; a* only feeds compact binning
+  if (cov_out) {
+    cov_out[i] = make_float4(c[0][0], c[0][1], c[1][0], c[1][1]);
+    tiles_out[i] = bo.count;
+  }
+  if (cov_out || bp.mode != 0) astar_out[i] = bo.a_star;
   key_out[i] = bo.count > 0 ? depth_key_bits(t2) : 0xffffffffu;
 }
 
@@ -751,17 +755,18 @@ BinParams make_bin_params(const sk_frame* f) {
 
 }  // namespace
 
-void launch_preprocess(sk_ctx* ctx, const sk_scene* scene, const sk_camera& cam, sk_frame* f) {
+void launch_preprocess(sk_ctx* ctx, const sk_scene* scene, const sk_camera& cam, sk_frame* f, bool extras) {
   const int64_t n = scene->n;
   if (n == 0) return;
   const CamParams cp = make_cam_params(cam);
   const BinParams bp = make_bin_params(f);
   const int block = 256;
   const unsigned grid = (unsigned)((n + block - 1) / block);
+  f->extras_valid = extras;
   auto args = [&](auto kern) {
     kern<<<grid, block, 0, ctx->stream>>>(
         scene->params.as<float>(), scene->capacity, n, cp, bp, f->mean2d.as<float2>(), f->conic_op.as<float4>(),
-        f->rgb_depth.as<float4>(), f->cov2d.as<float4>(), f->conic4.as<float4>(), f->radius.as<float>(),
+        f->rgb_depth.as<float4>(), extras ? f->cov2d.as<float4>() : nullptr, f->conic4.as<float4>(), f->radius.as<float>(),
         f->tiles.as<int>(), f->rect.as<int4>(), f->a_star.as<float>(), f->keys_a.as<uint32_t>(),
         f->vals_a.as<uint32_t>(), ctx->err_word.as<uint32_t>());
   };

@@ -188,6 +188,7 @@ struct sk_frame {
   sk::DevBuf cmask;       // uint32 per (batch of 32 entries, K6 warp): entries a pixel of the warp blended
   bool cmask_valid = false;
   bool fast_blend = false;  // K6 ran the MUFU-exp (training) form; K8 must match it
+  bool extras_valid = true; // cov2d / tiles / a* hold the last projection (launch_preprocess extras)
 
   // K7 / K8
   sk::DevBuf dimage;  // planar [3][H][W]
@@ -211,7 +212,10 @@ inline int64_t round_capacity(int64_t n) { return ((n < 1 ? 1 : n) + 31) & ~int6
 
 // ---- launchers (each .cu file owns its kernels) ---------------------------
 // preprocess.cu
-void launch_preprocess(sk_ctx* ctx, const sk_scene* scene, const sk_camera& cam, sk_frame* f);
+// extras = false (training steps, scored views): the 2-D covariance, tile
+// counts and (AABB binning) a* — read back only by sk_frame_get_projected —
+// are not written; f->extras_valid records which.
+void launch_preprocess(sk_ctx* ctx, const sk_scene* scene, const sk_camera& cam, sk_frame* f, bool extras = true);
 void launch_inject_bin(sk_ctx* ctx, sk_frame* f);
 // K3 tile binning (counting scatter): pair_val == nullptr counts pairs per
 // (chunk, tile) into counts; otherwise scatters the Gaussian indices into

@@ -156,20 +156,23 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   ensure<float>(f->bgrads, (size_t)kBGradFields * std::max<int64_t>(f->n, 1));
   if (pend) ctx->tev_set ^= 1;  // the pending step's events stay intact
   ctx->mark(0);
-  launch_preprocess(ctx, scene, cam, f);
-  // the previous step's readback completes while K1 of this step runs (the
-  // scene it reports is final: K1 only reads it). If that step had to be
-  // replayed, the replay ran on this frame and may have updated the scene:
-  // start this step again.
-  if (pend && finish_pending(ctx, pend))
-    return train_step(ctx, scene, f, cam, gt_dev, cfg, extent, it, row, comm, pend);
-  ctx->mark(1);
+  launch_preprocess(ctx, scene, cam, f, /*extras=*/false);
   // One rank: the pair count stays on the device (no host read in the step;
   // an overflow of the pair buffer is detected at the readback and the step
   // replayed). Several ranks keep the host read: a replay on one rank would
   // desynchronise the collectives.
   const bool deferred = !(comm && comm->world > 1);
+  // The previous step's readback completes while this step's first kernels
+  // run (K1 and the whole binning when the pair count stays on the device;
+  // the scene they read is final). If that step had to be replayed, the
+  // replay ran on this frame and may have updated the scene: start this step
+  // again.
+  if (!deferred && pend && finish_pending(ctx, pend))
+    return train_step(ctx, scene, f, cam, gt_dev, cfg, extent, it, row, comm, pend);
+  ctx->mark(1);
   bin_sort(ctx, f, deferred);
+  if (deferred && pend && finish_pending(ctx, pend))
+    return train_step(ctx, scene, f, cam, gt_dev, cfg, extent, it, row, comm, pend);
   ctx->mark(2);
   launch_blend_forward(ctx, f, nullptr, nullptr, /*fast=*/true);
   f->rendered = true;
