@@ -39,7 +39,7 @@ void ensure_projected(sk_frame* f, int64_t n) {
   ensure<int4>(f->rect, m);
   ensure<float>(f->a_star, m);
   ensure<uint32_t>(f->keys_a, m);  // K1 writes the depth keys and the index payload
-  ensure<uint32_t>(f->vals_a, m);  // straight into the sort's first buffers
+  ensure<uint32_t>(f->vals_a, m);
   f->n = n;
 }
 
@@ -71,7 +71,7 @@ void bin_sort(sk_ctx* ctx, sk_frame* f, bool deferred) {
   uint32_t* kb = ensure<uint32_t>(f->keys_b, n);
   uint32_t* va = ensure<uint32_t>(f->vals_a, n);
   uint32_t* vb = ensure<uint32_t>(f->vals_b, n);
-  radix_sort_pairs(ctx, ka, kb, va, vb, n, 32);  // depth_order: (depth, index)
+  radix_sort_pairs(ctx, ka, kb, va, vb, n, 32, /*identity_vals=*/true);  // depth_order: (depth, index)
   int32_t* counts = ensure<int32_t>(ctx->sort.bin_counts, (size_t)bin_chunks(f) * tiles);
   int32_t* totals = ensure<int32_t>(ctx->sort.bin_totals, (size_t)tiles);
   if (!ctx->sort.bin_total.ptr) {

@@ -138,7 +138,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const float* __restrict
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  val_out[i] = (uint32_t)i;  // the depth sort's payload (projected index)
   auto culled = [&]() {
     radius_out[i] = 0.0f;
     if (cov_out) tiles_out[i] = 0;
@@ -324,7 +323,6 @@ __global__ void inject_bin_kernel(int64_t n, BinParams bp, const float2* __restr
                                   uint32_t* __restrict__ val_out, uint32_t* __restrict__ err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  val_out[i] = (uint32_t)i;
   const float2 mu = mean2d[i];
   const float4 co = conic_op[i];
   const float4 cv = cov[i];

@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
     const int64_t idx = wbase + j * 32 + lane;
     const bool valid = idx < n;
     k[j] = valid ? keys_in[idx] : 0u;
-    v[j] = valid ? vals_in[idx] : 0u;
+    // first pass: the payload is the slot index itself (nothing to read)
+    v[j] = valid ? (vals_in ? vals_in[idx] : (uint32_t)idx) : 0u;
   }
   const uint32_t lt = lanemask_lt();
   // All match_any results first (independent, so their latencies overlap),
@@ -254,8 +255,15 @@ int radix_digit_width(int bits) {
 }  // namespace
 
 void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_t*& vals, uint32_t*& vals_alt,
-                      int64_t n, int bits) {
-  if (n <= 1 || bits <= 0) return;
+                      int64_t n, int bits, bool identity_vals) {
+  if (n <= 1 || bits <= 0) {
+    // nothing to sort: the identity payload still has to exist
+    if (identity_vals && n > 0) {
+      if (n == 1) SK_CUDA(cudaMemsetAsync(vals, 0, sizeof(uint32_t), ctx->stream));
+      else require(false, "radix_sort_pairs: identity payload needs key bits");
+    }
+    return;
+  }
   const int passes = radix_passes(bits);
   const int width = radix_digit_width(bits);
   const uint32_t dmask = (1u << width) - 1u;
@@ -286,7 +294,7 @@ void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_
       ctx->sort.epoch = 1;
     }
     onesweep_kernel<kSortItems><<<(unsigned)tiles, kSortThreads, 0, s>>>(
-        keys, vals, keys_alt, vals_alt, n, p * width, dmask, hist + p * kRadix, status, ctx->sort.epoch,
+        keys, p == 0 && identity_vals ? nullptr : vals, keys_alt, vals_alt, n, p * width, dmask, hist + p * kRadix, status, ctx->sort.epoch,
         counters + p);
     note_launch();
     std::swap(keys, keys_alt);

@@ -232,8 +232,9 @@ int64_t bin_chunks(const sk_frame* f);
 // sort.cu
 // Stable LSD radix sort of (key, value) pairs on key bits [0, bits). On
 // return keys/vals point at the sorted data (pointers may be swapped).
+// identity_vals: the payload is the key's position (vals is not read).
 void radix_sort_pairs(sk_ctx* ctx, uint32_t*& keys, uint32_t*& keys_alt, uint32_t*& vals, uint32_t*& vals_alt,
-                      int64_t n, int bits);
+                      int64_t n, int bits, bool identity_vals = false);
 
 // rasterize.cu
 // fast: the MUFU-exp blend of training steps (rasterize.cu); K8 follows the
