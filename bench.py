@@ -137,6 +137,45 @@ def dist_env():
     return world, rank, local
 
 
+# Ranks sharing GPUs (more ranks than visible devices: a one-GPU box checking
+# the multi-rank path) run over gloo with the library's host-callback
+# communicator (sk.HostComm), since NCCL refuses two ranks on one device. Such
+# a run checks the plumbing; it is not a scaling measurement and says so.
+_SHARED = False
+
+
+def init_dist(world, local):
+    """torch.cuda device + process group; returns (dist or None, device)."""
+    global _SHARED
+    import torch
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    if world <= 1:
+        return None, dev
+    import torch.distributed as dist
+    _SHARED = ndev < world
+    if _SHARED:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    return dist, dev
+
+
+def make_comm(sk, ctx, dist, rank, world):
+    return sk.HostComm(ctx, dist, rank, world) if _SHARED else sk.Comm.from_torch(ctx, dist, rank, world)
+
+
+def allmax(dist, x):
+    """max over ranks of a host float (the timing rule: slowest rank)."""
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if _SHARED else "cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def bench_config(args, world):
     """The `config` object of both arms (identical by construction)."""
     return {"workload": "config2: synthetic 1M-Gaussian scene (SH deg 3), 1920x1080 ring view per rank, "
@@ -146,7 +185,9 @@ def bench_config(args, world):
             "start_state": "timed steps are training iterations 1..K from the perturbed initial scene with fresh "
                            "Adam state (warm-up steps run first, then scene and optimizer are restored)",
             "l2": "inputs larger than L2 (944 MB params+moments+grads state per step)",
-            "parallelism": f"view-parallel dp{world} (gradient all-reduce)" if world > 1 else "single device"}
+            "parallelism": (f"view-parallel dp{world} (gradient reduce-scatter / all-gather)"
+                            + (" - ranks sharing one GPU over host collectives: a plumbing check, not a scaling "
+                               "number" if _SHARED else "")) if world > 1 else "single device"}
 
 
 def train_config(default_config, iterations=30000):
@@ -299,12 +340,8 @@ def run_ours(args, world, rank, local):
     import paper_2511_04283_b200 as sk
     import paper_2511_04283_b200.synthetic as syn
 
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    ctx = sk.Context(local)
+    dist, dev = init_dist(world, local)
+    ctx = sk.Context(dev)
     stream = torch.cuda.current_stream()
     ctx.check(ctx._lib.sk_ctx_set_stream(ctx.h, sk.C.c_void_p(stream.cuda_stream)))
 
@@ -320,7 +357,7 @@ def run_ours(args, world, rank, local):
     trainer = sk.Trainer(ctx, scene, data, cfg)
     comm = None
     if world > 1:
-        comm = sk.Comm.from_torch(ctx, dist, rank, world)
+        comm = make_comm(sk, ctx, dist, rank, world)
         trainer.set_comm(comm)
 
     def barrier():
@@ -343,7 +380,7 @@ def run_ours(args, world, rank, local):
     ctx.check(ctx._lib.sk_ctx_reset_timing(ctx.h))
     ctx.check(ctx._lib.sk_ctx_enable_timing(ctx.h, 1))
     launches0 = ctx.launch_count()
-    clock = ClockSampler(local)
+    clock = ClockSampler(dev)
     rows = []
     with (clock if not args.profile else _Null()):
         barrier()
@@ -373,9 +410,7 @@ def run_ours(args, world, rank, local):
         phase_avg[5] += phase_avg[6]
         phase_avg[6] = 0.0
     if dist is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = allmax(dist, ms)
     if args.profile:
         if rank == 0:
             print(json.dumps({"profile": True, "ms_per_step": ms, "phase_ms": phase_avg,
@@ -414,9 +449,7 @@ def run_ours(args, world, rank, local):
     wall_ms = 1000.0 * (time.perf_counter() - t0) / args.steps
     e2e_ms = max(f0.elapsed_time(f1) / args.steps, wall_ms)
     if dist is not None:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = allmax(dist, e2e_ms)
 
     # ---- workload units of the timed steps --------------------
     # visible Gaussians and the reference loop's visited / contributing
@@ -611,7 +644,7 @@ def measure_event(ctx, sk, torch, dist, rank, n, k, width, height, reps, warm):
     scene = ctx.scene(p, 3, capacity=2 * n)
     tr = sk.Trainer(ctx, scene, ds, cfg)
     if dist is not None:
-        tr.set_comm(sk.Comm.from_torch(ctx, dist, rank, dist.get_world_size()))
+        tr.set_comm(make_comm(sk, ctx, dist, rank, dist.get_world_size()))
 
     def restore():
         ctx.check(ctx._lib.sk_scene_upload(ctx.h, scene.h, sk._p(p), sk.C.c_int64(n)))
@@ -637,9 +670,7 @@ def measure_event(ctx, sk, torch, dist, rank, n, k, width, height, reps, warm):
         torch.cuda.synchronize()
         ms = 1000.0 * (time.perf_counter() - a)
         if dist is not None:
-            t = torch.tensor([ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            ms = allmax(dist, ms)
         return ms, scene.size, phases()
 
     ctx.check(ctx._lib.sk_ctx_enable_timing(ctx.h, 1))
@@ -701,12 +732,8 @@ def run_event(args, world, rank, local):
 
     import paper_2511_04283_b200 as sk
 
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    ctx = sk.Context(local)
+    dist, dev = init_dist(world, local)
+    ctx = sk.Context(dev)
     stream = torch.cuda.current_stream()
     ctx.check(ctx._lib.sk_ctx_set_stream(ctx.h, sk.C.c_void_p(stream.cuda_stream)))
     ev = measure_event(ctx, sk, torch, dist, rank, args.n, args.views, args.width, args.height,
