@@ -194,3 +194,26 @@ def test_two_rank_density_event_matches_single_process(two_ranks):
     assert ev["clone"].sum() + ev["split"].sum() > 0 and ev["prune"].sum() > 0
     assert np.array_equal(scene.download(), e0["params"])
     ctx.close()
+
+
+@pytest.mark.slow
+def test_bench_two_ranks_share_the_gpu(tmp_path):
+    """bench.py under torchrun with two ranks on this one-GPU box: the
+    multi-rank legs (training steps, end-to-end pipeline, density event) run
+    over the host-callback communicator and rank 0 prints one JSON line that
+    says it is a plumbing check (the driver's 2/4/8-GPU runs use NCCL)."""
+    import subprocess
+    import sys
+    out = tmp_path / "bench.out"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--gaussians", "20000", "--width", "256", "--height", "192",
+           "--views", "4", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, stdout=open(out, "w"), stderr=subprocess.PIPE, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in open(out).read().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert "plumbing check" in d["config"]["parallelism"]
+    assert d["event"]["value"] > 0 and d["event"]["n_after_early"] > 0
