@@ -80,26 +80,42 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._h = None
+
+    _BITS = [(0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"), (0x20, "sw_thermal_slowdown"),
+             (0x4, "sw_power_cap")]
+
+    def _nvml_open(self):
+        """NVML handle opened before the timed region starts (its first call
+        can take longer than a short timed region), or None."""
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._pynvml = pynvml
+            return h
+        except Exception:
+            return None
+
+    def _sample_nvml(self):
+        pynvml, h = self._pynvml, self._h
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.samples.append([str(sm), str(self._mx), "0"] + ["Active" if r & b else "Not Active" for b, _ in self._BITS])
 
     def _run_nvml(self):
-        import pynvml
-        pynvml.nvmlInit()
-        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-        bits = [(0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"), (0x20, "sw_thermal_slowdown"),
-                (0x4, "sw_power_cap")]
-        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         while not self._stop.is_set():
-            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-            self.samples.append([str(sm), str(mx), "0"] + ["Active" if r & b else "Not Active" for b, _ in bits])
-            self._stop.wait(0.01)
+            self._sample_nvml()
+            self._stop.wait(0.005)
 
     def _run(self):
-        try:
-            self._run_nvml()
-            return
-        except Exception:
-            pass
+        if self._h is not None:
+            try:
+                self._run_nvml()
+                return
+            except Exception:
+                pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -112,11 +128,19 @@ class ClockSampler:
             self._stop.wait(0.1)
 
     def __enter__(self):
+        self._h = self._nvml_open()
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *a):
+        # the region just ended with the GPU still clocked for it: a region
+        # shorter than the sampling period still gets one sample
+        if self._h is not None and not self.samples:
+            try:
+                self._sample_nvml()
+            except Exception:
+                pass
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
@@ -293,7 +317,11 @@ def implementation_bytes(phase, n, visible, pairs, pixels, fused=False):
     over N slots + the counting scatter of the tile lists instead of a 64-bit
     pair sort; K9+K10 fused keep the gradients on chip)."""
     if phase == 0:
-        return 4 * 59 * n + 104 * visible
+        # params: 236 B read per visible Gaussian, 44 B (mean, rotation, scale,
+        # opacity) per culled one; written: mean2d 8 + conic/opacity 16 +
+        # colour/depth 16 + full conic 16 + radius 4 + tile rect 16 + depth key
+        # 4 = 80 B per visible, radius + rect + key = 24 B per culled slot
+        return (4 * 59 + 80) * visible + (44 + 24) * (n - visible)
     if phase == 1:
         # depth sort: hist read 4 B + 4 passes x 16 B per slot; K3: order +
         # rectangle (20 B) twice per slot, the Gaussian index per pair
