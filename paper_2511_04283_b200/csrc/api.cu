@@ -101,6 +101,8 @@ int sk_ctx_destroy(sk_ctx* ctx) {
     cudaStreamDestroy(ctx->count_stream);
   }
   if (ctx->count_ev) cudaEventDestroy(ctx->count_ev);
+  if (ctx->step_graph) cudaGraphExecDestroy(ctx->step_graph);
+  if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return SK_OK;

@@ -1,6 +1,8 @@
 // Shared device/host infrastructure for the splatkit_b200 library.
 #pragma once
 
+#include <atomic>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -39,6 +41,10 @@ inline void require(bool cond, const std::string& msg) {
 }
 
 // Grow-only device buffer.
+// Device / pinned allocations made so far (a captured training step is only
+// attempted when none happened since the previous step: trainer.cu).
+inline std::atomic<uint64_t> g_alloc_count{0};
+
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
@@ -67,6 +73,7 @@ struct DevBuf {
     ptr = nullptr;
     bytes = 0;
     size_t alloc = want < 256 ? 256 : (regrow ? want + want / 4 : want);
+    g_alloc_count.fetch_add(1, std::memory_order_relaxed);
     SK_CUDA(cudaMalloc(&ptr, alloc));
     bytes = alloc;
     return ptr;
@@ -93,6 +100,7 @@ struct HostBuf {
     if (want <= bytes) return ptr;
     if (ptr) SK_CUDA(cudaFreeHost(ptr));
     ptr = nullptr;
+    g_alloc_count.fetch_add(1, std::memory_order_relaxed);
     SK_CUDA(cudaMallocHost(&ptr, want));
     bytes = want;
     return ptr;

@@ -31,7 +31,7 @@ struct PendingStep {
   sk_log_row* row = nullptr;
   sk_scene* scene = nullptr;
   int64_t adam_t[6] = {};  // the scene's Adam step counters before this step (restored on a device error)
-  cudaEvent_t done = nullptr;
+  cudaEvent_t done[2] = {};  // per readback slot: a captured next step records the other one
   HostBuf pinned;  // [2 slots][kPendSlot doubles]: loss sums, P, error word
   int slot = 0;
   // what a replay of the step needs (its pair count outgrew the pair buffer)
@@ -43,7 +43,8 @@ struct PendingStep {
   const sk_comm* comm = nullptr;
   bool replayed = false;  // set when finish_pending replayed the step (cleared by the caller)
   ~PendingStep() {
-    if (done) cudaEventDestroy(done);
+    for (auto e : done)
+      if (e) cudaEventDestroy(e);
   }
 };
 
@@ -106,6 +107,13 @@ struct sk_ctx {
   // speculative K3 queued behind it
   cudaStream_t count_stream = nullptr;
   cudaEvent_t count_ev = nullptr;
+  // captured training step (trainer.cu): the executable graph, updated in
+  // place every step, and the signature / allocation count of the last step
+  cudaGraphExec_t step_graph = nullptr;
+  cudaStream_t capture_stream = nullptr;  // the library's launches are recorded here (the
+                                          // context stream may be the legacy one, which cannot capture)
+  uint64_t step_sig = 0;
+  uint64_t step_allocs = ~0ull;
   sk::HostBuf count_pinned;
   // phase timing (sk_ctx_enable_timing)
   bool timing = false;
@@ -113,8 +121,14 @@ struct sk_ctx {
   int tev_set = 0;
   double phase_ms[SK_NUM_PHASES] = {};
   int64_t timed_steps = 0;
+  // inside a captured step the marks become event-record nodes of the graph
+  bool capturing = false;
   void mark(int i) {
-    if (timing) cudaEventRecord(tev[tev_set][i], stream);
+    if (!timing) return;
+    if (capturing)
+      cudaEventRecordWithFlags(tev[tev_set][i], stream, cudaEventRecordExternal);
+    else
+      cudaEventRecord(tev[tev_set][i], stream);
   }
   // second context of the two-stream density-event score pass (density.cu)
   sk_ctx* helper = nullptr;

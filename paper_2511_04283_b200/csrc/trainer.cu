@@ -100,7 +100,7 @@ void replay_overflowed(sk_ctx* ctx, sk_scene* scene, sk_frame* f, int64_t pairs,
 bool finish_pending(sk_ctx* ctx, PendingStep* pend) {
   if (!pend || !pend->active) return false;
   pend->active = false;
-  SK_CUDA(cudaEventSynchronize(pend->done));
+  SK_CUDA(cudaEventSynchronize(pend->done[pend->slot]));
   const double* h = static_cast<const double*>(pend->pinned.ptr) + kPendSlot * pend->slot;
   uint32_t bits = 0;
   memcpy(&bits, h + 4, sizeof(bits));
@@ -143,11 +143,151 @@ bool finish_pending(sk_ctx* ctx, PendingStep* pend) {
   return false;
 }
 
+// Everything a step's buffer sizes depend on: two steps with the same
+// signature and no allocation in between allocate nothing (the pair buffer
+// is sized by its own capacity while the pair count stays on the device).
+uint64_t step_signature(const sk_scene* s, const sk_frame* f, const sk_camera& cam, const sk_train_config& cfg) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+  mix((uint64_t)(uintptr_t)s);
+  mix((uint64_t)(uintptr_t)f);
+  mix((uint64_t)s->n);
+  mix((uint64_t)s->capacity);
+  mix((uint64_t)s->sh_degree);
+  mix((uint64_t)cam.width);
+  mix((uint64_t)cam.height);
+  mix((uint64_t)cfg.tile_size);
+  mix((uint64_t)cfg.compact);
+  return h;
+}
+
+bool step_graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SK_STEP_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// A pipelined single-rank step as one CUDA graph: its launches (K1, the
+// binning, K6, K7, K8, the fused K9 + K10, the readback into the pinned
+// slot, the phase marks) are captured and the executable graph is updated in
+// place (same topology every step; camera, learning rates, buffer pointers
+// and look-back epochs change), then launched with one call. Taken only in
+// steady state — same signature as the previous step and no allocation since
+// — so nothing inside the capture allocates or synchronises. The previous
+// step's readback completes after the launch; if it has to be replayed
+// (pair-buffer overflow), this step ran with the error word set (K6 .. K10
+// skipped) and is run again uncaptured. Returns false when not taken.
+bool train_step_graph(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam, const uint8_t* gt_dev,
+                      const sk_train_config& cfg, float extent, int it, sk_log_row* row, PendingStep* pend) {
+  if (!step_graphs_enabled() || !pend || cfg.lazy_opt_enabled || scene->n == 0 || !pend->pinned.ptr ||
+      !pend->done[0] || !pend->done[1])
+    return false;
+  const uint64_t sig = step_signature(scene, f, cam, cfg);
+  if (sig != ctx->step_sig || g_alloc_count.load() != ctx->step_allocs) return false;
+  const sk_binning bin = binning_from(cfg);
+  frame_geometry(f, cam.width, cam.height, &bin);
+  f->camera = cam;
+  int64_t adam_t0[6];
+  std::copy(scene->adam_t, scene->adam_t + 6, adam_t0);
+  const int next = pend->slot ^ 1;
+  double* slot_dst = static_cast<double*>(pend->pinned.ptr) + kPendSlot * next;
+  const int tev0 = ctx->tev_set;
+  ctx->tev_set ^= 1;  // the pending step's events stay intact
+  if (!ctx->capture_stream) SK_CUDA(cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking));
+  // record on the capture stream (the launches go to ctx->stream), launch the
+  // graph on the context stream
+  cudaStream_t run = ctx->stream, st = ctx->capture_stream;
+  SK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+  ctx->stream = st;
+  ctx->capturing = true;
+  cudaGraph_t g = nullptr;
+  try {
+    ctx->mark(0);
+    launch_preprocess(ctx, scene, cam, f, /*extras=*/false);
+    ctx->mark(1);
+    bin_sort(ctx, f, /*deferred=*/true);
+    ctx->mark(2);
+    launch_blend_forward(ctx, f, nullptr, nullptr, /*fast=*/true);
+    f->rendered = true;
+    ctx->mark(3);
+    launch_loss(ctx, f, gt_dev, true, (float)cfg.lambda, true, nullptr);
+    ctx->mark(4);
+    launch_blend_backward(ctx, f);
+    ctx->mark(5);
+    const LearningRates lrs = lrs_from(cfg);
+    const float pos_lr = expon_lr(lrs.position * extent, lrs.position_final * extent, it, cfg.iterations);
+    StepReadback rb;
+    rb.dst = slot_dst;
+    rb.sums = ctx->scalars.as<double>();
+    rb.pairs = ctx->sort.bin_total.as<long long>();
+    rb.err = ctx->err_word.as<uint32_t>();
+    launch_project_backward_adam(ctx, scene, f, lrs, pos_lr, true, true, rb);
+    ctx->mark(6);
+    ctx->mark(7);
+    // an event-record node (a plain record inside a capture only orders the capture)
+    SK_CUDA(cudaEventRecordWithFlags(pend->done[next], st, cudaEventRecordExternal));
+    ctx->capturing = false;
+    ctx->stream = run;
+    SK_CUDA(cudaStreamEndCapture(st, &g));
+  } catch (...) {
+    ctx->capturing = false;
+    ctx->stream = run;
+    cudaGraph_t dead = nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+      cudaStreamEndCapture(st, &dead);
+    if (dead) cudaGraphDestroy(dead);
+    cudaGetLastError();
+    std::copy(adam_t0, adam_t0 + 6, scene->adam_t);
+    ctx->tev_set = tev0;
+    ctx->step_sig = 0;  // run uncaptured until a step completes normally
+    return false;
+  }
+  cudaGraphExecUpdateResultInfo info{};
+  if (!ctx->step_graph || cudaGraphExecUpdate(ctx->step_graph, g, &info) != cudaSuccess) {
+    cudaGetLastError();
+    if (ctx->step_graph) SK_CUDA(cudaGraphExecDestroy(ctx->step_graph));
+    ctx->step_graph = nullptr;
+    SK_CUDA(cudaGraphInstantiate(&ctx->step_graph, g, 0));
+  }
+  SK_CUDA(cudaGraphDestroy(g));
+  SK_CUDA(cudaGraphLaunch(ctx->step_graph, run));
+  // the previous step's readback completes while this step runs
+  if (finish_pending(ctx, pend)) {
+    std::copy(adam_t0, adam_t0 + 6, scene->adam_t);
+    ctx->step_sig = 0;
+    train_step(ctx, scene, f, cam, gt_dev, cfg, extent, it, row, nullptr, pend);
+    return true;
+  }
+  pend->slot = next;
+  pend->active = true;
+  pend->it = it;
+  pend->width = f->width;
+  pend->height = f->height;
+  pend->lambda = (float)cfg.lambda;
+  pend->n = scene->n;
+  pend->frame = f;
+  pend->cam = cam;
+  pend->gt = gt_dev;
+  pend->cfg = cfg;
+  pend->extent = extent;
+  pend->comm = nullptr;
+  pend->row = row;
+  pend->tev_set = ctx->tev_set;
+  pend->scene = scene;
+  std::copy(adam_t0, adam_t0 + 6, pend->adam_t);
+  ctx->step_allocs = g_alloc_count.load();
+  return true;
+}
+
 // One train_iteration (trainer.hpp:124-175) on camera `cam` with the 8-bit GT
 // already on the device.
 void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam, const uint8_t* gt_dev,
                 const sk_train_config& cfg, float extent, int it, sk_log_row* row, const sk_comm* comm,
                 PendingStep* pend) {
+  if (!(comm && comm->world > 1) && train_step_graph(ctx, scene, f, cam, gt_dev, cfg, extent, it, row, pend)) return;
   const sk_binning bin = binning_from(cfg);
   frame_geometry(f, cam.width, cam.height, &bin);
   f->camera = cam;
@@ -235,7 +375,8 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
   }
   ctx->mark(7);
   if (pend) {
-    if (!pend->done) SK_CUDA(cudaEventCreateWithFlags(&pend->done, cudaEventDisableTiming));
+    for (auto& e : pend->done)
+      if (!e) SK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     double* hs = slot_dst;
     if (!in_kernel_readback) {
       SK_CUDA(cudaMemcpyAsync(hs, ctx->scalars.ptr, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -247,7 +388,7 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
       hs[4] = 0.0;  // the error word's 4 bytes land in the low half of the zeroed slot
       SK_CUDA(cudaMemcpyAsync(hs + 4, ctx->err_word.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
     }
-    SK_CUDA(cudaEventRecord(pend->done, ctx->stream));
+    SK_CUDA(cudaEventRecord(pend->done[pend->slot], ctx->stream));
     pend->active = true;
     pend->it = it;
     pend->width = f->width;
@@ -264,6 +405,10 @@ void train_step(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera& cam,
     pend->tev_set = ctx->tev_set;
     pend->scene = scene;
     std::copy(adam_t0, adam_t0 + 6, pend->adam_t);
+    // a following step with the same signature can run as a graph
+    const bool graphable = deferred && fused && in_kernel_readback;
+    ctx->step_sig = graphable ? step_signature(scene, f, cam, cfg) : 0;
+    ctx->step_allocs = g_alloc_count.load();
     return;
   }
   if (deferred) {
