@@ -126,6 +126,9 @@ int sk_ctx_get_event_timing(const sk_ctx* ctx, double* ms, int64_t* events);
  * kernel, without the class scans and the host round trip for the split
  * normals (the phase time includes both). */
 int sk_ctx_get_compact_kernel_ms(const sk_ctx* ctx, double* move_ms);
+/* Training steps this context launched as the captured CUDA graph
+ * (single-rank pipelined steps in steady state; SK_STEP_GRAPH=0 disables). */
+int sk_ctx_graph_steps(const sk_ctx* ctx, int64_t* steps);
 const char* sk_version(void);
 
 /* ---- scene (Scene<T>, scene.hpp:30-52) ---------------------------------- */

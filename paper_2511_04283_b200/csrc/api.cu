@@ -166,6 +166,12 @@ int sk_ctx_get_compact_kernel_ms(const sk_ctx* ctx, double* move_ms) {
   return SK_OK;
 }
 
+int sk_ctx_graph_steps(const sk_ctx* ctx, int64_t* steps) {
+  if (!ctx || !steps) return SK_ERR_INVALID_ARGUMENT;
+  *steps = ctx->graph_steps;
+  return SK_OK;
+}
+
 int sk_ctx_reset_timing(sk_ctx* ctx) {
   if (!ctx) return SK_ERR_INVALID_ARGUMENT;
   for (auto& v : ctx->phase_ms) v = 0.0;

@@ -110,6 +110,7 @@ struct sk_ctx {
   // captured training step (trainer.cu): the executable graph, updated in
   // place every step, and the signature / allocation count of the last step
   cudaGraphExec_t step_graph = nullptr;
+  int64_t graph_steps = 0;  // training steps launched as the captured graph
   cudaStream_t capture_stream = nullptr;  // the library's launches are recorded here (the
                                           // context stream may be the legacy one, which cannot capture)
   uint64_t step_sig = 0;

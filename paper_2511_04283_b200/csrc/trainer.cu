@@ -254,6 +254,7 @@ bool train_step_graph(sk_ctx* ctx, sk_scene* scene, sk_frame* f, const sk_camera
   }
   SK_CUDA(cudaGraphDestroy(g));
   SK_CUDA(cudaGraphLaunch(ctx->step_graph, run));
+  ++ctx->graph_steps;
   // the previous step's readback completes while this step runs
   if (finish_pending(ctx, pend)) {
     std::copy(adam_t0, adam_t0 + 6, scene->adam_t);

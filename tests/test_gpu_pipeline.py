@@ -1,6 +1,8 @@
 """The pipelined end-to-end entry point (sk_train_step_host_async): the same
 training steps as the synchronous sk_train_step_host, with the GT uploads on a
 copy stream and each step's loss delivered one call later."""
+import os
+
 import numpy as np
 import pytest
 
@@ -32,6 +34,10 @@ def test_async_host_steps_match_sync(orc):
     for k in range(9):
         pipe.step(b, cams[k % 3], gts[k % 3], cfg, 3.0, k + 1)
     rows = pipe.flush()
+    graph_steps = sk.C.c_int64()
+    ctx.check(ctx._lib.sk_ctx_graph_steps(ctx.h, sk.C.byref(graph_steps)))
+    if os.environ.get("SK_STEP_GRAPH", "1") != "0":
+        assert graph_steps.value >= 6  # steady-state steps ran as the captured graph
     assert [r["iteration"] for r in rows] == list(range(1, 10))
     for s, r in zip(sync_rows, rows):
         assert r["tile_pairs"] == s["tile_pairs"]
