@@ -409,6 +409,9 @@ def run_ours(args, world, rank, local):
     ctx.check(ctx._lib.sk_ctx_reset_timing(ctx.h))
     ctx.check(ctx._lib.sk_ctx_enable_timing(ctx.h, 1))
     launches0 = ctx.launch_count()
+    gs0 = sk.C.c_int64()
+    ctx.check(ctx._lib.sk_ctx_graph_steps(ctx.h, sk.C.byref(gs0)))
+    graph_steps0 = gs0.value
     clock = ClockSampler(dev)
     rows = []
     with (clock if not args.profile else _Null()):
@@ -426,6 +429,9 @@ def run_ours(args, world, rank, local):
             torch.cuda.cudart().cudaProfilerStop()
         barrier()
     launches = ctx.launch_count() - launches0
+    gs = sk.C.c_int64()
+    ctx.check(ctx._lib.sk_ctx_graph_steps(ctx.h, sk.C.byref(gs)))
+    graph_steps = gs.value - graph_steps0
     ctx.check(ctx._lib.sk_ctx_enable_timing(ctx.h, 0))
     ms = e0.elapsed_time(e1) / args.steps
     phase_ms = (sk.C.c_double * len(PHASES))()
@@ -596,6 +602,7 @@ def run_ours(args, world, rank, local):
         "e2e": {"value": world * 1000.0 / e2e_ms, "unit": "iter/s", "h2d_bytes_per_step": int(gt8.size),
                 "d2h_bytes_per_step": 44, "ms_per_step": e2e_ms},
         "gpu_launches": launches,
+        "graph_steps": graph_steps,  # timed steps launched as the captured CUDA graph (the rest: plain launches)
         "clocks": clocks,
         "cpu_baseline": cpu,
         "event": event,
