@@ -105,7 +105,20 @@ template <bool GRAD, bool U8>
 __global__ void __launch_bounds__(kThreads, 2)
     ssim_march_kernel(const float* __restrict__ img, const void* __restrict__ gt, int W, int H,
                       int rows_per_cta, float nrm, float lambda, float inv_n, float* __restrict__ dimage,
-                      double* __restrict__ sums, double* __restrict__ block_sums, unsigned int* __restrict__ ticket) {
+                      double* __restrict__ sums, double* __restrict__ block_sums, unsigned int* __restrict__ ticket,
+                      float* __restrict__ zero, int64_t zero_n) {
+  // K8's blend-gradient accumulator zeroed here, CTA-strided float4 stores
+  // (this kernel is compute-bound; a separate memset would cost its own
+  // launch and pass): K8 runs right after
+  if (GRAD && zero) {
+    const int64_t nb = (int64_t)gridDim.x * gridDim.y * gridDim.z;
+    const int64_t b = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    const int64_t quads = zero_n >> 2;  // cudaMalloc'd: 16-B aligned
+    float4* z4 = reinterpret_cast<float4*>(zero);
+    for (int64_t q = b * kThreads + threadIdx.x; q < quads; q += nb * kThreads)
+      __stcs(z4 + q, make_float4(0.0f, 0.0f, 0.0f, 0.0f));
+    if (b == 0 && threadIdx.x < (zero_n & 3)) zero[4 * quads + threadIdx.x] = 0.0f;
+  }
   extern __shared__ float4 smem_f4[];
   float* sm = reinterpret_cast<float*>(smem_f4);
   float2* s_in = reinterpret_cast<float2*>(sm + kOffIn);
@@ -463,8 +476,16 @@ void launch_loss(sk_ctx* ctx, sk_frame* f, const void* gt, bool gt_u8, float lam
   const float inv_n = 1.0f / (3.0f * (float)plane);
   auto* k = want_grad ? (gt_u8 ? ssim_march_kernel<true, true> : ssim_march_kernel<true, false>)
                       : (gt_u8 ? ssim_march_kernel<false, true> : ssim_march_kernel<false, false>);
+  // with the gradient: zero the frame's blend-gradient buffer for K8
+  float* zero = nullptr;
+  int64_t zero_n = 0;
+  if (want_grad && f->n > 0) {
+    zero_n = (int64_t)kBGradFields * f->n;
+    zero = ensure<float>(f->bgrads, (size_t)zero_n);
+  }
   k<<<grid, kThreads, kSmemBytes, ctx->stream>>>(f->image.as<float>(), gt, W, H, rows, nrm, lambda, inv_n, dimage,
-                                                 sums, block_sums, ticket);
+                                                 sums, block_sums, ticket, zero, zero_n);
+  f->bgrads_zeroed = zero != nullptr;
   note_launch();
   SK_CUDA(cudaGetLastError());
   if (out) read_loss_sums(ctx, out);

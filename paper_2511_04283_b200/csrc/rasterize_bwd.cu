@@ -446,7 +446,9 @@ void bwd_dispatch(sk_ctx* ctx, sk_frame* f) {
 }  // namespace
 
 void launch_blend_backward(sk_ctx* ctx, sk_frame* f) {
-  SK_CUDA(cudaMemsetAsync(f->bgrads.ptr, 0, sizeof(float) * kBGradFields * (size_t)f->n, ctx->stream));
+  if (!f->bgrads_zeroed)
+    SK_CUDA(cudaMemsetAsync(f->bgrads.ptr, 0, sizeof(float) * kBGradFields * (size_t)f->n, ctx->stream));
+  f->bgrads_zeroed = false;
   if (f->tiles_x * f->tiles_y == 0) return;
   switch (f->tile_size) {
     case 8: bwd_dispatch<8, 1>(ctx, f); break;

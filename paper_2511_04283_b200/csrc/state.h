@@ -204,6 +204,7 @@ struct sk_frame {
   bool cmask_valid = false;
   bool fast_blend = false;  // K6 ran the MUFU-exp (training) form; K8 must match it
   bool extras_valid = true; // cov2d / tiles / a* hold the last projection (launch_preprocess extras)
+  bool bgrads_zeroed = false;  // K7 (with the gradient) zeroed bgrads for K8: no memset needed
 
   // K7 / K8
   sk::DevBuf dimage;  // planar [3][H][W]
