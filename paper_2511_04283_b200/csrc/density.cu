@@ -564,19 +564,33 @@ void trace_point(sk_ctx* ctx, const char* what) {
 
 }  // namespace
 
+// photometric = (1 - lambda) mean(raw) + lambda (1 - ssim) (error_maps.hpp:40-41)
+// from the loss sums on the device, with the host's arithmetic (finish_loss:
+// double means, then float): no host round trip per scored view.
+__global__ void photometric_kernel(const double* __restrict__ sums, int width, int height, float lambda,
+                                   float* __restrict__ out) {
+  const double npx = (double)width * height;
+  const double l1 = sums[0] / (3.0 * npx);
+  const double ssim = sums[1] / (3.0 * npx);
+  *out = (1.0f - lambda) * (float)l1 + lambda * (1.0f - (float)ssim);
+}
+
 // Renders the k views and leaves s_d / s_p_raw / s_p in the scene's table.
 // gt: device images (u8 HWC) or host float HWC images (staged per view).
 // One scored view (adc.hpp:101-108): render, error maps, photometric term,
 // and the masked count pass into `row`, on context c (its stream, scratch and
 // error word) with frame f.
 void score_view(sk_ctx* c, sk_scene* s, sk_frame* f, const sk_camera& cam, const void* gt_in, bool gt_u8_device,
-                float tau, float lambda, const sk_binning& bin, int32_t* row, float* photo) {
+                float tau, float lambda, const sk_binning& bin, int32_t* row, float* dphoto) {
+  // No host synchronisation: the pair count stays on the device (an overflow
+  // of the frame's pair buffer raises kErrPairOverflow; score_pass then
+  // regrows and scores again) and the photometric term is formed on the device.
   const int64_t n = s->n;
   frame_geometry(f, cam.width, cam.height, &bin);
   f->camera = cam;
   ensure_projected(f, n);
   launch_preprocess(c, s, cam, f, /*extras=*/false);
-  bin_sort(c, f);
+  bin_sort(c, f, /*deferred=*/true);
   ensure_image(f);
   launch_blend_forward(c, f, nullptr, nullptr);
   f->rendered = true;
@@ -590,19 +604,16 @@ void score_view(sk_ctx* c, sk_scene* s, sk_frame* f, const sk_camera& cam, const
   float* raw = ensure<float>(c->ev.raw, npx);
   uint8_t* mask = ensure<uint8_t>(c->ev.mask, npx);
   uint32_t* lohi = ensure<uint32_t>(c->ev.lohi, 4);
-  const uint32_t init[2] = {0xffffffffu, 0u};
-  h2d(c, lohi, init, 2);
+  SK_CUDA(cudaMemsetAsync(lohi, 0xff, sizeof(uint32_t), c->stream));  // min: all ones
+  SK_CUDA(cudaMemsetAsync(lohi + 1, 0, sizeof(uint32_t), c->stream));  // max: zero
   error_raw_kernel<<<std::min<unsigned>(blocks(npx), 148 * 8), 256, 0, c->stream>>>(
       f->image.as<float>(), gt, gt_u8_device, cam.width, cam.height, raw, lohi);
   note_launch();
   error_mask_kernel<<<blocks(npx), 256, 0, c->stream>>>(raw, lohi, npx, tau, mask, nullptr);
   note_launch();
-  LossSums sums{};
-  launch_loss(c, f, gt, gt_u8_device, lambda, false, &sums);
-  sk_loss_values v{};
-  finish_loss(cam.width, cam.height, lambda, sums, &v);
-  // photometric = (1 - lambda) mean(raw) + lambda (1 - ssim)  (error_maps.hpp:40-41)
-  *photo = (1.0f - lambda) * (float)v.l1 + lambda * (1.0f - (float)v.ssim);
+  launch_loss(c, f, gt, gt_u8_device, lambda, false, nullptr);
+  photometric_kernel<<<1, 1, 0, c->stream>>>(c->scalars.as<double>(), cam.width, cam.height, lambda, dphoto);
+  note_launch();
   launch_blend_forward(c, f, mask, row);
 }
 
@@ -643,7 +654,7 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
   auto slot_of = [&](int j) { return (j % world) * kpr + j / world; };
   int32_t* rows = ensure<int32_t>(ev.rows, (size_t)slots * std::max<int64_t>(n, 1));
   uint32_t* lohi = ensure<uint32_t>(ev.lohi, 4);
-  SK_CUDA(cudaMemsetAsync(rows, 0, sizeof(int32_t) * (size_t)slots * n, ctx->stream));
+  float* dphoto = ensure<float>(ev.photo, slots);
   std::vector<float> photo(slots, 0.0f);
   ctx->event_mark(0);
   std::vector<int> mine;
@@ -651,57 +662,75 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
     if (j % world == rank) mine.push_back(j);
   auto run_view = [&](sk_ctx* c, sk_frame* fr, int j) {
     const int sl = slot_of(j);
-    score_view(c, s, fr, cams[j], gts[j], gt_u8_device, tau, lambda, bin, rows + (size_t)sl * n, &photo[sl]);
+    score_view(c, s, fr, cams[j], gts[j], gt_u8_device, tau, lambda, bin, rows + (size_t)sl * n, dphoto + sl);
   };
+  // Views round-robin over S streams, each driven by its own host thread and
+  // context (scratch, error word) with its own frame: the streams' kernels
+  // overlap on the GPU (a view is a chain of small binning kernels around
+  // the heavy blends). SK_SCORE_STREAMS overrides S (SK_SCORE_ONE_STREAM=1:
+  // one); the result does not depend on S (own count rows and photometric
+  // slots per view).
   const char* one = std::getenv("SK_SCORE_ONE_STREAM");  // runtime override (tests / diagnostics)
-  const bool two = !(one && one[0] == '1');
-  if (!(two && gt_u8_device && mine.size() >= 2)) {
-    for (const int j : mine) run_view(ctx, f, j);
-  } else {
-    sk_ctx* h = score_helper(ctx);
-    prepare_loss(ctx);  // one-time constant upload, before two threads use it
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    SK_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
-    SK_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
-    SK_CUDA(cudaEventRecord(e0, ctx->stream));  // rows zeroed before either stream counts
-    SK_CUDA(cudaStreamWaitEvent(h->stream, e0, 0));
-    std::exception_ptr helper_err;
-    std::thread th([&] {
+  const char* ns = std::getenv("SK_SCORE_STREAMS");
+  int nstreams = ns ? std::max(1, std::atoi(ns)) : 3;  // measured: 2 -> 49.1, 3 -> 48.5, 4 -> 49.1 ms per event
+  if ((one && one[0] == '1') || !gt_u8_device) nstreams = 1;
+  nstreams = std::max(1, std::min<int>(nstreams, (int)mine.size()));
+  std::vector<sk_ctx*> cs{ctx};
+  std::vector<sk_frame*> fs{f};
+  for (int i = 1; i < nstreams; ++i) {
+    cs.push_back(score_helper(cs.back()));
+    fs.push_back(cs[i - 1]->helper_frame);
+  }
+  for (int attempt = 0;; ++attempt) {
+    SK_CUDA(cudaMemsetAsync(rows, 0, sizeof(int32_t) * (size_t)slots * n, ctx->stream));
+    if (nstreams == 1) {
+      for (const int j : mine) run_view(ctx, f, j);
+    } else {
+      prepare_loss(ctx);  // one-time constant upload, before the threads use it
+      cudaEvent_t e0 = nullptr;
+      SK_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+      SK_CUDA(cudaEventRecord(e0, ctx->stream));  // rows zeroed before any stream counts
+      for (int i = 1; i < nstreams; ++i) SK_CUDA(cudaStreamWaitEvent(cs[i]->stream, e0, 0));
+      std::vector<std::exception_ptr> errs(nstreams);
+      std::vector<std::thread> th;
+      for (int i = 1; i < nstreams; ++i)
+        th.emplace_back([&, i] {
+          try {
+            SK_CUDA(cudaSetDevice(cs[i]->device));
+            for (size_t v = i; v < mine.size(); v += nstreams) run_view(cs[i], fs[i], mine[v]);
+          } catch (...) {
+            errs[i] = std::current_exception();
+          }
+        });
       try {
-        SK_CUDA(cudaSetDevice(h->device));
-        for (size_t i = 1; i < mine.size(); i += 2) run_view(h, ctx->helper_frame, mine[i]);
+        for (size_t v = 0; v < mine.size(); v += nstreams) run_view(ctx, f, mine[v]);
       } catch (...) {
-        helper_err = std::current_exception();
+        errs[0] = std::current_exception();
       }
-    });
-    try {
-      for (size_t i = 0; i < mine.size(); i += 2) run_view(ctx, f, mine[i]);
-    } catch (...) {
-      th.join();
-      cudaStreamSynchronize(h->stream);
+      for (auto& t : th) t.join();
+      for (int i = 1; i < nstreams; ++i) {
+        cudaEvent_t e1 = nullptr;
+        SK_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+        SK_CUDA(cudaEventRecord(e1, cs[i]->stream));
+        SK_CUDA(cudaStreamWaitEvent(ctx->stream, e1, 0));
+        SK_CUDA(cudaStreamSynchronize(cs[i]->stream));
+        cudaEventDestroy(e1);
+      }
       cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
-      throw;
+      for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
     }
-    th.join();
-    SK_CUDA(cudaEventRecord(e1, h->stream));
-    SK_CUDA(cudaStreamWaitEvent(ctx->stream, e1, 0));
-    SK_CUDA(cudaStreamSynchronize(h->stream));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (helper_err) std::rethrow_exception(helper_err);
-    raise_device_errors(read_error_word(h));
+    uint32_t bits = 0;
+    for (sk_ctx* c : cs) bits |= read_error_word(c);  // synchronises
+    raise_device_errors(bits);
+    if (!(bits & kErrPairOverflow)) break;
+    require(attempt < 8, "accumulate_scores: pair buffer still overflowing");
+    for (sk_frame* fr : fs) ensure<uint32_t>(fr->pval_a, 2 * std::max<size_t>(fr->pval_a.bytes / sizeof(uint32_t), 1024));
   }
-  float* dphoto = ensure<float>(ev.photo, slots);
-  h2d(ctx, dphoto, photo.data(), slots);
-  if (world > 1) {
-    allgather_scores(const_cast<sk_comm*>(comm), rows, kpr, n, dphoto, ctx->stream);  // C3
-    d2h(ctx, photo.data(), dphoto, slots);
-    sync(ctx);
-  }
+  if (world > 1) allgather_scores(const_cast<sk_comm*>(comm), rows, kpr, n, dphoto, ctx->stream);  // C3
   ctx->event_mark(1);
-  const uint32_t init[2] = {0xffffffffu, 0u};
-  h2d(ctx, lohi, init, 2);
+  SK_CUDA(cudaMemsetAsync(lohi, 0xff, sizeof(uint32_t), ctx->stream));  // min: all ones
+  SK_CUDA(cudaMemsetAsync(lohi + 1, 0, sizeof(uint32_t), ctx->stream));  // max: zero
   if (n > 0) {
     scores_kernel<<<blocks(n), 256, 0, ctx->stream>>>(rows, n, dphoto, k, world, kpr, n, s->s_d.as<float>(),
                                                        s->s_p_raw.as<float>(), lohi);
@@ -712,6 +741,8 @@ void score_pass(sk_ctx* ctx, sk_scene* s, sk_frame* f, const std::vector<sk_came
   SK_CUDA(cudaGetLastError());
   ctx->event_mark(2);
   if (photo_out) {
+    d2h(ctx, photo.data(), dphoto, slots);
+    sync(ctx);
     photo_out->resize(k);
     for (int j = 0; j < k; ++j) (*photo_out)[j] = photo[slot_of(j)];
   }

@@ -36,7 +36,8 @@ template <int TS, int PIX>
 __global__ void __launch_bounds__(TS* TS / PIX, 1024 / (TS * TS / PIX)) count_blend_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, int W, int H, int tiles_x, const uint8_t* __restrict__ mask,
-    int* __restrict__ counts) {
+    int* __restrict__ counts, const uint32_t* __restrict__ err) {
+  if (err && __ldg(err)) return;  // see blend_fwd_warp_kernel
   constexpr int NTH = TS * TS / PIX;                // threads; each owns PIX pixels
   constexpr int B = TS * TS > 256 ? 256 : TS * TS;  // staged entries per batch
   using WB = WarpBlock<TS, PIX>;
@@ -135,7 +136,9 @@ template <int PIX>
 __global__ void __launch_bounds__(16 * 16 / PIX, 8) count_walk_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, int W, int H, int tiles_x, const uint8_t* __restrict__ mask,
-    const int* __restrict__ last_entry, const uint32_t* __restrict__ cmask, int* __restrict__ counts) {
+    const int* __restrict__ last_entry, const uint32_t* __restrict__ cmask, int* __restrict__ counts,
+    const uint32_t* __restrict__ err) {
+  if (err && __ldg(err)) return;  // see blend_fwd_warp_kernel
   constexpr int TS = 16;
   using WB = WarpBlock<TS, PIX>;
   constexpr int kWarps = WB::kWarps;
@@ -457,10 +460,11 @@ void fwd_dispatch(sk_ctx* ctx, sk_frame* f, const uint8_t* mask, int32_t* counts
     // cmask_valid) recorded last_entry and the contribution masks
     count_walk_kernel<PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
         ranges, f->pair_val, mean2d, co, f->width, f->height, f->tiles_x, mask, f->last_entry.as<int>(),
-        f->cmask.as<uint32_t>(), counts);
+        f->cmask.as<uint32_t>(), counts, f->pairs < 0 ? ctx->err_word.as<uint32_t>() : nullptr);
   else if (mask)
-    count_blend_kernel<TS, PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(ranges, f->pair_val, mean2d, co, f->width,
-                                                                          f->height, f->tiles_x, mask, counts);
+    count_blend_kernel<TS, PIX><<<tiles, TS * TS / PIX, 0, ctx->stream>>>(
+        ranges, f->pair_val, mean2d, co, f->width, f->height, f->tiles_x, mask, counts,
+        f->pairs < 0 ? ctx->err_word.as<uint32_t>() : nullptr);
   else {
     uint32_t* cm = nullptr;
     if (TS == 16 && PIX == 2) {  // K8 consumes the masks at 16x16 tiles
