@@ -204,6 +204,16 @@ int sk_loss_u8(sk_ctx* ctx, sk_frame* frame, const uint8_t* gt_host, float lambd
 /* SSIM only (metrics.hpp:83-89), and PSNR (metrics.hpp:126-134). */
 int sk_ssim(sk_ctx* ctx, const float* a_hwc, const float* b_hwc, int width, int height,
             double* ssim_out, double* psnr_out);
+/* float64 value path (the reference's T = double instantiation,
+ * tools/splatkit_main.cpp:31; used by its FD tests, acceptance.cpp:163-254):
+ * project -> tile-binned blend_forward -> training_loss, all in double on the
+ * device. params_host: planar [SK_COMP_COUNT(deg)][n] doubles (n <= 65536).
+ * image_hwc (nullable): [H][W][3] rendered image. gt_hwc + loss3 (both
+ * nullable): loss3 = {loss, l1, ssim}. A checking path for finite
+ * differences, not a training path. */
+int sk_fp64_render_loss(sk_ctx* ctx, const double* params_host, int64_t n, int sh_degree,
+                        const sk_camera* cam, const sk_binning* binning, const double* gt_hwc,
+                        double lambda, double* image_hwc, double* loss3);
 int sk_frame_get_dimage(sk_ctx* ctx, const sk_frame* frame, float* hwc);
 int sk_frame_set_dimage(sk_ctx* ctx, sk_frame* frame, const float* hwc);
 

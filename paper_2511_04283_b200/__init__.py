@@ -347,6 +347,20 @@ class Context:
         self.check(self._lib.sk_ssim(self.h, _p(a), _p(b), C.c_int(w), C.c_int(h), C.byref(s), C.byref(p)))
         return s.value, p.value
 
+    def fp64_render_loss(self, params, sh_degree, cam, gt=None, lam=0.2, bin_=None):
+        """float64 project -> blend_forward -> training_loss on the device (the
+        reference's double instantiation, for finite-difference checks).
+        Returns (image [H][W][3] float64, (loss, l1, ssim) or None)."""
+        p = np.ascontiguousarray(params, np.float64)
+        cam = as_camera(cam)
+        img = np.zeros((cam.height, cam.width, 3), np.float64)
+        out = np.zeros(3, np.float64)
+        g = None if gt is None else np.ascontiguousarray(gt, np.float64)
+        self.check(self._lib.sk_fp64_render_loss(
+            self.h, _p(p), C.c_int64(p.shape[1]), C.c_int(sh_degree), C.byref(cam), C.byref(as_binning(bin_)),
+            _p(g) if g is not None else None, C.c_double(lam), _p(img), _p(out) if g is not None else None))
+        return img, (tuple(float(v) for v in out) if g is not None else None)
+
 
 class Scene:
     """Device-resident Scene<T> (scene.hpp:30-52), planar [C][n] parameters."""

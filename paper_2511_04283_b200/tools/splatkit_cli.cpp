@@ -85,7 +85,7 @@ sk_train_config build_config(const Args& a) {
     if (a.has(flag)) check(sk_config_set(g_ctx, &cfg, key, a.get(flag).c_str()));
   check(sk_validate_config(g_ctx, &cfg));
   if (a.flag("--float64"))
-    throw std::runtime_error("--float64: the B200 path trains in fp32 (the CPU oracle carries the fp64 checks)");
+    throw std::runtime_error("--float64: the B200 path trains in fp32; the float64 value path (sk_fp64_render_loss) serves the finite-difference checks");
   if (a.flag("--plot")) std::fprintf(stderr, "note: --plot charts are not produced by splatkit_b200\n");
   return cfg;
 }
