@@ -15,6 +15,8 @@
 // fast hardware exp, and only alphas within 1e-5 relative of the 1/255 and
 // 0.99 thresholds (the fast exp is within ~1e-6) are recomputed with the
 // shared deterministic exp.
+#include <type_traits>
+
 #include "blend_common.cuh"
 
 namespace sk {
@@ -318,8 +320,12 @@ __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS /
 
   // This lane's 11 partials of staged slot j (list position idx), the
   // -2 d_q scale folded in; returns whether some lane of the warp
-  // contributed (warp-uniform).
-  auto partials = [&](int j, int idx, float (&gv)[kBGradFields]) {
+  // contributed (warp-uniform). VOTE = false (the contribution-mask walk):
+  // K6 marked the entry because a pixel of this very 8x8 block blended it,
+  // with the same decision arithmetic, so the vote is known to be true; and
+  // were it not, the entry's partials would all be zero and its atomics
+  // would add zeros.
+  auto partials = [&](int j, int idx, float (&gv)[kBGradFields], auto vote) {
     const float4 mq = ld_f4(0u, j);
     const float4 co = ld_f4(16u * NT, j);
     const float4 c = ld_f4(32u * NT, j);
@@ -331,7 +337,8 @@ __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS /
     } else {
       contrib = one_partials<FAST>(mq, co, c, fpx, fpy[0], idx, last[0], T1, ns1, d0[0], d1[0], d2[0], tab, gv);
     }
-    return __any_sync(0xffffffffu, contrib);
+    if constexpr (decltype(vote)::value) return __any_sync(0xffffffffu, contrib) != 0;
+    return true;
   };
   // Entries are reduced two at a time (reduce_scatter_2x11): the walk
   // alternates between computing into ga (the pending entry, kept across
@@ -347,17 +354,17 @@ __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS /
     return (int)bit;
   };
   const int base = warp * 32;
-  auto walk = [&](uint32_t m, int b0) {
+  auto walk = [&](uint32_t m, int b0, auto vote) {
     while (m) {
       if (!has_a) {
         const int bit = pop(m);
-        if (partials(base + bit, b0 + bit, ga)) {
+        if (partials(base + bit, b0 + bit, ga, vote)) {
           has_a = true;
           id_a = ld_id(base + bit);
         }
       } else {
         const int bit = pop(m);
-        if (partials(base + bit, b0 + bit, gb)) {
+        if (partials(base + bit, b0 + bit, gb, vote)) {
           reduce_scatter_2x11(ga, gb, id_a, ld_id(base + bit), true, bgrads, gstride);
           has_a = false;
         }
@@ -391,7 +398,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS /
           s_st.id[base + lane] = g;
         }
         __syncwarp();
-        walk(m, b0);
+        walk(m, b0, std::false_type{});
         __syncwarp();
       }
     }
@@ -420,7 +427,7 @@ __global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS /
       }
       const uint32_t m = __ballot_sync(0xffffffffu, hit);
       __syncwarp();
-      walk(m, b0);
+      walk(m, b0, std::true_type{});
       __syncwarp();
     }
   }
