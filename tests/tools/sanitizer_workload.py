@@ -1,9 +1,11 @@
 """Workload run under compute-sanitizer by tests/test_gpu_sanitizer.py:
 a 4K-Gaussian training step (K1-K10), one density event (K11-K15 with a
 two-stream score pass), and a 200K-key depth sort whose onesweep passes span
-dozens of tiles (decoupled look-back). No torch: only the library's kernels.
+dozens of tiles (decoupled look-back), and the float64 value path. No torch:
+only the library's kernels. The training run is long enough for the step to
+be captured into a CUDA graph and replayed.
 
-  python tests/tools/sanitizer_workload.py [train|event|sort|all]
+  python tests/tools/sanitizer_workload.py [train|sort|fp64|all]
 """
 import os
 import sys
@@ -31,7 +33,7 @@ def main(part):
         scene = ctx.scene(p, 3)
         data = sk.Dataset(ctx, cams, gts, [0, 1, 2], 2.64)
         tr = sk.Trainer(ctx, scene, data, cfg)
-        rows = tr.run(2)
+        rows = tr.run(4)
         assert all(np.isfinite(r["loss"]) for r in rows)
         # the event: score pass over both streams, selection, compaction
         cfg.k = 3
@@ -53,6 +55,13 @@ def main(part):
         tl = ctx.tile_lists()
         assert tl.pairs == pairs
         print("sort ok", pairs)
+    if part in ("fp64", "all"):
+        p = synthetic_scene(500, deg=3, seed=6).astype(np.float64)
+        cam = syn.ring_camera(0, 8, 96, 72)
+        for mode in ("aabb", "compact"):
+            _, vals = ctx.fp64_render_loss(p, 3, cam, np.full((72, 96, 3), 0.5), 0.2, sk.binning(mode))
+            assert np.isfinite(vals[0])
+        print("fp64 ok", vals)
     ctx.synchronize()
     ctx.close()
 
