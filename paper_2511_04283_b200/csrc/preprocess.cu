@@ -359,11 +359,15 @@ __global__ void inject_bin_kernel(int64_t n, BinParams bp, const float2* __restr
 //                       Gaussian-major, 32 at a time (lane e takes pair e:
 //                       owner by a shuffle binary search over the lanes'
 //                       offsets, tile from the owner's rectangle). Lower lanes
-//                       therefore hold earlier Gaussians, so __match_any_sync
-//                       on the tile gives each pair its rank among the round's
-//                       same-tile pairs and the round's leader advances the
-//                       tile's counter: slot = ranges[t].x + prefix[chunk][t]
-//                       + the chunk's earlier pairs of t.
+//                       therefore hold earlier Gaussians, so a pair's rank
+//                       among the round's same-tile pairs is its order in the
+//                       warp: a shared-memory tag probe (each lane tags its
+//                       tile, a lane reading back another id has a peer)
+//                       finds the rounds with shared tiles, and only those
+//                       rank with __match_any_sync. The round's first lane of
+//                       each tile advances the tile's counter: slot =
+//                       ranges[t].x + prefix[chunk][t] + the chunk's earlier
+//                       pairs of t.
 // Every tile thus receives its Gaussians in (depth, index) order — the
 // reference's list order — with no key sort over the pairs, and only the
 // 4-byte Gaussian index is written per pair. Compact binning enumerates the
@@ -379,7 +383,7 @@ constexpr int kBinWarps = SK_BIN_WARPS;  // tile-row bands per scatter CTA
 constexpr int kBinThreads = kBinWarps * 32;
 constexpr int kBinStage = 1024;  // slots staged in shared memory per step
 constexpr int kCountThreads = 256;
-constexpr int kBinMaxSmemTiles = 40960;  // 160 KB of int32 counters per row-group
+constexpr int kBinMaxSmemTiles = 24576;  // 96 KB of int32 counters (+ 96 KB of tags) per row-group
 constexpr int kCountSmallArea = 48;      // larger rectangles are counted by the whole warp
 
 struct BinLayout {
@@ -602,6 +606,7 @@ __global__ void __launch_bounds__(kBinThreads, SK_BIN_MINB) bin_scatter_kernel(B
   const int gtiles = rows * bp.tiles_x;
   const int32_t* crow = counts + (int64_t)blockIdx.x * L.tiles + t0;
   for (int i = tid; i < gtiles; i += kBinThreads) s_pos[i] = ranges[t0 + i].x + crow[i];
+  uint32_t* s_tag = reinterpret_cast<uint32_t*>(s_pos + L.rows_per_group * bp.tiles_x);  // per tile: last tagging lane
 
   // warp w owns the group's tile rows row0 + w + q * kBinWarps (interleaved,
   // so the pair load is balanced whatever the scene's vertical profile)
@@ -668,14 +673,26 @@ __global__ void __launch_bounds__(kBinThreads, SK_BIN_MINB) bin_scatter_kernel(B
       bool take = pos < total;
       if (take && bp.mode != 0) take = compact_keeps(bp, ty, tx, mean2d[og], conic_op[og], a_star[og]);
       const int local = (ty - row0) * bp.tiles_x + tx;
-      const uint32_t peers = __match_any_sync(0xffffffffu, take ? (uint32_t)local : 0xffffffffu);
+      // Conflict probe: each taking lane tags its tile with its lane id; a
+      // lane that reads back another id shares its tile with a lower or
+      // higher lane of the round. Depth-adjacent Gaussians are rarely
+      // screen-adjacent, so most rounds have no shared tile and skip the
+      // long-latency MATCH (rank 0, one pair per tile).
+      // (an atomic exchange: concurrent tags of one tile are the point)
+      if (take) atomicExch(&s_tag[local], (uint32_t)lane);
+      __syncwarp();
+      int rank = 0, cnt = 1;
+      if (__any_sync(0xffffffffu, take && s_tag[local] != (uint32_t)lane)) {
+        const uint32_t peers = __match_any_sync(0xffffffffu, take ? (uint32_t)local : 0xffffffffu);
+        rank = __popc(peers & lt);
+        cnt = __popc(peers);
+      }
       // every lane reads the tile's counter, then the round's first lane of
       // each tile advances it (no leader search, no broadcast)
-      const int rank = __popc(peers & lt);
       int base = 0;
       if (take) base = s_pos[local];
       __syncwarp();
-      if (take && rank == 0) s_pos[local] = base + __popc(peers);
+      if (take && rank == 0) s_pos[local] = base + cnt;
       __syncwarp();
       const int64_t slot = (int64_t)base + rank;
       if (take && slot < cap) pair_val[slot] = og;
@@ -822,11 +839,11 @@ void launch_bin_tiles(sk_ctx* ctx, sk_frame* f, const uint32_t* order, int32_t* 
     SK_CUDA(cudaFuncSetAttribute(bin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  sizeof(int32_t) * kBinMaxSmemTiles));
     SK_CUDA(cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 sizeof(int32_t) * kBinMaxSmemTiles));
+                                 2 * sizeof(int32_t) * kBinMaxSmemTiles));
     attr = true;
   }
   if (pair_val)
-    bin_scatter_kernel<<<grid, kBinThreads, smem, ctx->stream>>>(
+    bin_scatter_kernel<<<grid, kBinThreads, 2 * smem, ctx->stream>>>(
         bp, L, order, f->rect.as<int4>(), f->mean2d.as<float2>(), f->conic_op.as<float4>(),
         f->a_star.as<float>(), counts, f->ranges.as<int2>(), pair_val, cap);
   else
