@@ -237,7 +237,7 @@ def test_config1_training_parity(ctx, orc):
     # (GPU runs of one seed differ by 2x in event-300 split counts), so the
     # bar is a sanity bound on a chaotic outcome, not a parity gate (that is
     # the follow-mode 0.05 dB above). Measured on B200: the oracle over seeds
-    # 17-20 ends at 24.82-24.91 dB, N 4923 at seed 17; eight GPU runs of seed
+    # 17-20 ends at 24.82-24.91 dB, N 4923 at seed 17; six GPU runs of seed
     # 17 (atomic summation order varies run to run) at 23.99-24.96 dB, N
     # 4698-5006.
     itr = orc.Trainer(p0, 3, ds, cfg)
