@@ -651,17 +651,19 @@ __global__ void __launch_bounds__(kBinThreads, SK_BIN_MINB) bin_scatter_kernel(B
     const int off = incl - m;  // lanes >= cnt: off == total, never an owner
     for (int e0 = 0; e0 < total; e0 += 32) {
       const int pos = e0 + lane;
-      // owner = the highest lane whose offset is <= pos; its offset comes
-      // out of the search (lane 0's is 0)
-      int o = 0, off_o = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int v = __shfl_sync(0xffffffffu, off, o + step);
-        if (v <= pos) {
-          o += step;
-          off_o = v;
-        }
-      }
+      // owner = the highest lane whose offset is <= pos = (number of queued
+      // lanes with offset <= pos) - 1: queued lanes hold at least one pair,
+      // so their offsets are distinct and increasing. Counted as the lanes
+      // starting before this round (one ballot) plus the segment starts
+      // inside it up to pos (one OR-reduction of start bits), instead of a
+      // 5-step dependent shuffle search.
+      const bool live = lane < cnt;
+      const uint32_t before = __ballot_sync(0xffffffffu, live && off < e0);
+      const uint32_t starts =
+          __reduce_or_sync(0xffffffffu, (live && off >= e0 && off < e0 + 32) ? 1u << (off - e0) : 0u);
+      const uint32_t upto = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;
+      const int o = max(0, __popc(before) + __popc(starts & upto) - 1);
+      const int off_o = __shfl_sync(0xffffffffu, off, o);
       const uint32_t og = __shfl_sync(0xffffffffu, g, o);
       const uint32_t op = __shfl_sync(0xffffffffu, packed, o);
       const uint32_t omag = __shfl_sync(0xffffffffu, magic, o);
