@@ -68,10 +68,12 @@ __device__ __forceinline__ void reduce_scatter_2x11(const float (&a)[kBGradField
 }
 
 // 16x16 tiles: 128 threads (8x8 pixel block per warp, 2 pixels per thread,
-// the same blocks as K6) and 7 resident CTAs (28 warps) per SM, which caps
-// the kernel at 72 registers without spills. Measured against 64 threads x 4
-// pixels (8x16 blocks): -12% K8 time; 7 CTAs/SM instead of 6: -4% more.
-constexpr int kBwdMinBlocks = 7;
+// the same blocks as K6) and 8 resident CTAs (32 warps) per SM, which caps
+// the kernel at 64 registers — without spills since the contribution-mask
+// walk dropped its per-entry vote (measured: 8 CTAs -0.4% against 7, which
+// was the best before; 64 threads x 4 pixels (8x16 blocks): +12% to +18%).
+// (8x8 and 32x32 tiles keep the 7-CTA-equivalent budget: 32x32 would spill.)
+constexpr int kBwdMinBlocks = 8;
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 // 1 / x on MUFU.RCP alone (x = 1 - alpha lies in [0.01, 1]: no range fix-ups)
@@ -230,7 +232,7 @@ __device__ __forceinline__ bool one_partials(const float4 mq, const float4 co, c
 }
 
 template <int TS, int PIX, bool FAST>
-__global__ void __launch_bounds__(TS* TS / PIX, kBwdMinBlocks * 128 / (TS * TS / PIX)) blend_bwd_kernel(
+__global__ void __launch_bounds__(TS* TS / PIX, (TS == 16 ? kBwdMinBlocks : 7) * 128 / (TS * TS / PIX)) blend_bwd_kernel(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ pair_val, const float2* __restrict__ mean2d,
     const float4* __restrict__ conic_op, const float4* __restrict__ rgbd, int W, int H, int tiles_x,
     const float* __restrict__ final_t, const int* __restrict__ last_entry, const float* __restrict__ dimage,
